@@ -1,0 +1,338 @@
+#!/usr/bin/env python
+"""Benchmark of the optimisation hot path (BASELINE.json metric): iterations/s
+of one full step -- raster fwd, ASM fwd, loss, ASM bwd, raster bwd, Adan --
+at 1080p RGB (cfg2: 1920x1080, C=3, N=200k, L=1, pad 2), plus its HBM
+roofline fraction.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 is launched by torchrun (one rank per GPU); every rank optimises its own
+scene (scene seed = rank): replicas, weak scaling, no data-path collective.
+Timing: CUDA events on the trainer's stream around exactly K graph-replayed
+steps, barrier + synchronize on both sides, max over ranks.  The step's
+working set (~0.45 GB) exceeds the 126 MB L2, so no explicit flush is used.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "optimisation iters/sec (raster+ASM fwd+bwd) at 1080p RGB; % of HBM roofline"
+UNIT = "iters/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=400)
+    p.add_argument("--warmup", type=int, default=20)
+    p.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    p.add_argument("--workload", default="cfg2")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--e2e-steps", type=int, default=50)
+    p.add_argument("--profile-steps", type=int, default=10)
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def algorithmic_bytes(cfg, pairs):
+    """B = C(13 + 12L) A + L H W + 592 N + 24 K, A = 8 H W."""
+    h, w, c, L, n = cfg["height"], cfg["width"], cfg["channels"], cfg["planes"], cfg["count"]
+    A = 8.0 * h * w
+    return c * (13 + 12 * L) * A + L * h * w + 592.0 * n + 24.0 * pairs
+
+
+def kernel_bytes(cfg, pairs):
+    """Algorithmic bytes per launch of each kernel slot (A = 8HW per channel)."""
+    h, w, c, L, n = cfg["height"], cfg["width"], cfg["channels"], cfg["planes"], cfg["count"]
+    A = 8.0 * h * w
+    P = (6 + 2 * c) * n
+    return {
+        "binning": 4.0 * P + 64.0 * n + 3 * 16.0 * pairs,  # params in, records out, keys w/r x2 passes
+        "raster_fwd": c * A + 8.0 * pairs + (48.0 + 16 * c) * n,
+        "rows_fwd": c * (A + 2 * A),
+        "cols_fwd": c * (2 * A + 2 * L * A),
+        "rows_inv": c * (2 * L * A + L * A),
+        "loss_ssim": c * (L * A + 0.5 * A + L * A) + L * h * w,
+        "rows_fwd_bwd": c * (L * A + 2 * L * A),
+        "cols_bwd": c * (2 * L * A + 2 * A),
+        "rows_inv_bwd": c * (2 * A + A),
+        "raster_bwd": c * A + (48.0 + 16 * c + 16 + 4 * (6 + 2 * c)) * n + 4.0 * P,
+        "adan": 44.0 * P,
+    }
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "50",
+                 "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.12)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_reference_run(wl, gset32, max_seconds, threads, min_steps=1, max_steps=3, warmup=0):
+    """Times the reference's own CPU implementation (oracle/_ref = the reference
+    sources compiled here) on the same inputs, in the order of
+    pipeline.cpp:253-297.  Returns (seconds per step, steps timed, stage ms)."""
+    from oracle import ref  # checker / baseline only
+
+    cfg = wl["cfg"]
+    c, h, w = cfg["channels"], cfg["height"], cfg["width"]
+    ref.set_thread_count(threads)
+    rs = ref.GaussianSet(cfg["count"], c, *[np.ascontiguousarray(gset32[k]) for k in ref.GROUPS])
+    target = wl["target"].astype(np.float32).astype(np.float64)
+    tr = ref.Trainer(rs, w, h, target, wl["depth"], cfg["planes"], 3e-3, cfg["dz"],
+                     ref.PropagationSpec(tuple(wl["wavelengths"])), total_steps=max_steps + warmup + 1)
+    for _ in range(warmup):
+        tr.step()
+    times = []
+    t_all = time.perf_counter()
+    while len(times) < max_steps:
+        t0 = time.perf_counter()
+        tr.step()
+        times.append(time.perf_counter() - t0)
+        if len(times) >= min_steps and time.perf_counter() - t_all + times[-1] > max_seconds:
+            break
+    st = tr.stage_ms() / max(len(times) + warmup, 1)
+    names = ("raster_fwd", "propagate_multi", "training_loss_grad", "propagate_multi_backward",
+             "rasterize_backward", "adan", "total")
+    return float(np.mean(times)), len(times), dict(zip(names, [round(float(x), 2) for x in st]))
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    from paper_2511_15022_b200 import synthetic as S
+    from oracle import ref
+
+    if not ref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libholoref.so not built"}))
+        return
+    wl = S.workload(args.workload)
+    gset32 = {k: np.asarray(v, np.float32).astype(np.float64) for k, v in wl["gaussians"].items()}
+    threads = os.cpu_count() or 1
+    budget = 150.0
+    k_cap = max(1, min(args.steps, 3))
+    w_cap = 1 if args.warmup > 0 else 0
+    sec, k, stages = cpu_reference_run(wl, gset32, budget, threads, 1, k_cap, w_cap)
+    v = 1.0 / sec
+    cfg = wl["cfg"]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+        "steps": k, "warmup": w_cap, "ms_per_step": sec * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_of(args.workload, cfg, world),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"{k} full step(s) after {w_cap} warm-up of {args.workload} through the "
+                                   f"reference's own fp64 C++ (oracle/_ref, FFTW3 API shim), "
+                                   f"set_thread_count({threads}); steps capped to stay within minutes",
+                         "stages_ms": stages},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def config_of(name, cfg, world):
+    return {"workload": f"{name}: {cfg['width']}x{cfg['height']} x{cfg['channels']} wavelengths, "
+                        f"{cfg['count']} Gaussians, {cfg['planes']} plane(s), pad 2, init_gaussians(seed 42+rank)",
+            "width": cfg["width"], "height": cfg["height"], "channels": cfg["channels"],
+            "gaussians": cfg["count"], "planes": cfg["planes"], "pad_factor": 2,
+            "parallelism": f"replicas x{world} (one scene per GPU, no collective)",
+            "l2": "no flush: per-step working set ~0.45 GB > 126 MB L2"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    from paper_2511_15022_b200 import holo, synthetic as S
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    wl = S.workload(args.workload, scene=rank)
+    cfg = wl["cfg"]
+    c, h, w, n, L = cfg["channels"], cfg["height"], cfg["width"], cfg["count"], cfg["planes"]
+    gset32 = {k: np.asarray(v, np.float32).astype(np.float64) for k, v in wl["gaussians"].items()}
+    gs = holo.GaussianSet(n, c, **gset32)
+    target = holo.RealField(c, h, w, wl["target"].astype(np.float32).astype(np.float64))
+    spec = holo.PropagationSpec(tuple(wl["wavelengths"]))
+    total = args.warmup + args.steps + args.e2e_steps + args.profile_steps + 2
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        tr = holo.Trainer(gs, w, h, target, wl["masks"], wl["distances"], spec, total_steps=total)
+        tr.use_graph(True)
+        for _ in range(args.warmup):
+            tr.step(sync_loss=False)
+        tr.last_loss()  # surfaces any error of the warm-up
+        stream.synchronize()
+        sampler = ClockSampler(local)
+        sampler.start()
+        time.sleep(0.3)  # let the sampler attach before the timed region
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            tr.step(sync_loss=False)
+        e1.record(stream)
+        e1.synchronize()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        clocks = sampler.stop()
+        ms = e0.elapsed_time(e1) / args.steps
+        loss, pairs = tr.last_loss()
+
+        # e2e through the public API with a host-resident GaussianSet (like the
+        # reference loop): per step H2D params from pinned memory, the step,
+        # D2H of the updated params and the loss.
+        P = tr.param_count
+        host = torch.empty(P, dtype=torch.float32, pin_memory=True)
+        host.copy_(torch.from_numpy(tr.params()))
+        hptr = holo.C.c_void_p(host.data_ptr())
+        lib = holo._lib.load()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            holo.check(lib.hs_trainer_set_params(tr.h, hptr, 0))
+            tr.step(sync_loss=True)
+            holo.check(lib.hs_trainer_get_params(tr.h, hptr, 0))
+        torch.cuda.synchronize()
+        e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+
+        # per-kernel profile: eager steps with events at every kernel boundary
+        tr.use_graph(False)
+        tr.set_profiling(True)
+        stages = {}
+        l0 = holo.kernel_launch_count()
+        for i in range(args.profile_steps):
+            tr.step(sync_loss=False)
+            for k, v in tr.stage_ms().items():
+                stages.setdefault(k, []).append(v)
+        per_step_launches = (holo.kernel_launch_count() - l0) / max(args.profile_steps, 1)
+        stage_ms = {k: float(np.median(v)) for k, v in stages.items()}
+
+    if world > 1:
+        t = torch.tensor([ms, e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, e2e_s = float(t[0]), float(t[1])
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    peak, peak_src = peaks()
+    kb = kernel_bytes(cfg, pairs)
+    kern = {k: v for k, v in stage_ms.items() if k in kb}
+    dom = max(kern, key=kern.get)
+    dom_gbs = kb[dom] / (kern[dom] * 1e-3) / 1e9
+    B = algorithmic_bytes(cfg, pairs)
+    step_gbs = B / (ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get(dom)
+    line = {
+        "metric": METRIC, "value": world * 1e3 / ms, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+        "config": config_of(args.workload, cfg, world),
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": dom_gbs, "peak": peak, "unit": "GB/s",
+                     "frac": dom_gbs / peak, "traffic": traffic, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": kb[dom], "ms_per_launch": kern[dom]},
+        "step_roofline": {"bound": "hbm", "achieved": step_gbs, "peak": peak, "unit": "GB/s",
+                          "frac": step_gbs / peak, "algorithmic_bytes_per_step": B,
+                          "formula": "C(13+12L)8HW + LHW + 592N + 24K (SURVEY §8d)"},
+        "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
+        "e2e": {"value": world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 4 * P,
+                "d2h_bytes_per_step": 4 * P + 8,
+                "path": "hs_trainer_set_params(host pinned) + hs_trainer_step + hs_trainer_get_params per step"},
+        "gpu_launches": int(round(per_step_launches * args.steps)),
+        "clocks": clocks, "loss": loss, "pairs": pairs,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            sec, k, st = cpu_reference_run(wl, gset32, 30.0, os.cpu_count() or 1, 1, 3, 0)
+            line["cpu_baseline"] = {
+                "value": 1.0 / sec, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "reference",
+                "sample": f"{k} full cfg2 step(s) through the reference's fp64 C++ (oracle/_ref, FFTW3 API "
+                          f"shim), set_thread_count(nproc)", "stages_ms": st}
+        except Exception as e:  # noqa: BLE001
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                                    "sample": f"unavailable: {e}"}
+    print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,185 @@
+/* holosplat-b200 C ABI -- the drop-in boundary for the reference's optimisation
+ * hot path (arxiv 2511.15022 "holosplat", /root/reference/proj).
+ *
+ * The reference exposes its hot path as the C++ API in namespace holo
+ * (proj/core/include/holo/{rasterizer,propagation,loss,optimizer}.hpp) and its
+ * only product caller is the step loop proj/core/src/pipeline.cpp:253-297.
+ * This header is the thin extern "C" layer underneath the C++ drop-in
+ * (include/holo/*.hpp, libholo_b200.so) and the Python host mirror
+ * (paper_2511_15022_b200.holo).  Plain pointers and sizes only.
+ *
+ * Conventions
+ *  - Every function returns hs_status; HS_OK == 0.  On failure the message is
+ *    available from hs_last_error() (thread-local), in the reference's words
+ *    where the reference raises the same condition.
+ *  - "d_" pointers are device pointers on the context's device, "h_" host.
+ *  - Gaussian parameters are ONE fp32 buffer of (6 + 2C) * N floats holding
+ *    the reference's six groups back to back, in declaration order
+ *    (gaussian_set.hpp:14-19):
+ *        [pre_position 2N | pre_scale 2N | rotation N | amplitude N*C |
+ *         phase N*C | pre_opacity N]
+ *    Gradients use the same layout (GaussianSetGrads = GaussianSet).
+ *  - Complex fields are interleaved complex64 (float2 re,im), C x H x W
+ *    row-major (same element order as holo::ComplexField's planar arrays,
+ *    complex_field.hpp:11-35); multi-plane stacks are L x C x H x W.
+ *  - Work is issued on the context's stream (hs_ctx_set_stream); functions
+ *    that return host scalars synchronise that stream.
+ */
+#ifndef HOLOSPLAT_H
+#define HOLOSPLAT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    HS_OK = 0,
+    HS_EINVAL = 1,      /* std::invalid_argument in the reference */
+    HS_ENONFINITE = 2,  /* std::runtime_error "Adan: non-finite gradient in group <g>" */
+    HS_ECUDA = 3,
+    HS_ENOMEM = 4,
+    HS_EOVERFLOW = 5    /* tile-pair capacity exceeded (grow with hs_trainer_reserve_pairs) */
+} hs_status;
+
+typedef struct hs_ctx hs_ctx;
+typedef struct hs_trainer hs_trainer;
+
+/* ---- context ---------------------------------------------------------------- */
+hs_status hs_ctx_create(int device, hs_ctx** out);
+void hs_ctx_destroy(hs_ctx* ctx);
+/* cudaStream_t passed as void*; NULL = legacy default stream. */
+hs_status hs_ctx_set_stream(hs_ctx* ctx, void* stream);
+hs_status hs_ctx_synchronize(hs_ctx* ctx);
+const char* hs_last_error(void);
+/* Number of kernels this library has launched in this process (for the bench's
+ * gpu_launches claim). */
+uint64_t hs_kernel_launch_count(void);
+/* Device-memory helpers so hosts without a CUDA toolchain (the C++ drop-in,
+ * ctypes) can stage buffers. */
+hs_status hs_device_alloc(hs_ctx* ctx, size_t bytes, void** d_out);
+hs_status hs_device_free(hs_ctx* ctx, void* d_ptr);
+hs_status hs_copy_h2d(hs_ctx* ctx, void* d_dst, const void* h_src, size_t bytes);
+hs_status hs_copy_d2h(hs_ctx* ctx, void* h_dst, const void* d_src, size_t bytes);
+
+/* ---- rasterizer (rasterizer.hpp:12-36, rasterizer.cpp:33-286) --------------- */
+/* build_tile_index: pairs sorted by (tile, id); ranges[2t], ranges[2t+1] =
+ * [begin,end) of tile t, {0,0} when empty.  Two-call protocol: with cap <
+ * needed nothing but *npairs and tiles_xy is written.  Bit-exact with
+ * holo::build_tile_index on the same (fp32-valued) parameters. */
+hs_status hs_build_tile_index(hs_ctx* ctx, const float* d_params, int n, int c, int width,
+                              int height, uint32_t* d_tiles, uint32_t* d_ids,
+                              uint64_t* d_ranges, int64_t cap, int64_t* npairs, int* tiles_xy);
+/* rasterize_forward: d_field receives C x H x W complex64. */
+hs_status hs_rasterize_forward(hs_ctx* ctx, const float* d_params, int n, int c, int width,
+                               int height, float* d_field);
+/* rasterize_backward: d_grad_field = dL/d(re,im) interleaved C x H x W; d_grads
+ * receives dL/d(params) in the parameter layout. */
+hs_status hs_rasterize_backward(hs_ctx* ctx, const float* d_params, int n, int c, int width,
+                                int height, const float* d_grad_field, float* d_grads);
+
+/* ---- propagation (propagation.hpp:9-49, propagation.cpp:97-243) -------------- */
+typedef struct {
+    const double* wavelengths; /* one per channel, metres */
+    int n_wavelengths;
+    double pixel_pitch;        /* metres */
+    int pad_factor;
+    double aperture_radius;    /* padded-frequency-grid pixels; 0 disables */
+} hs_prop_spec;
+
+/* mode 0: propagate(distance)            (propagation.cpp:225-228)
+ * mode 1: propagate_with_mask_distance    (:230-233)
+ * mode 2: propagate_backward(distance)    (:235-238) */
+hs_status hs_propagate(hs_ctx* ctx, const hs_prop_spec* spec, int mode, double distance,
+                       double mask_distance, const float* d_in, int c, int h, int w,
+                       float* d_out);
+/* propagate_multi: d_out is L x C x H x W. */
+hs_status hs_propagate_multi(hs_ctx* ctx, const hs_prop_spec* spec, const double* h_distances,
+                             int L, const float* d_in, int c, int h, int w, float* d_out);
+/* propagate_multi_backward: d_grads is L x C x H x W, d_out C x H x W. */
+hs_status hs_propagate_multi_backward(hs_ctx* ctx, const hs_prop_spec* spec,
+                                      const double* h_distances, int L, const float* d_grads,
+                                      int c, int h, int w, float* d_out);
+
+/* ---- loss (loss.hpp:10-67, loss.cpp:223-398) ----------------------------------- */
+/* intensity_of: |u|^2 (field_core.cpp:88-93); count complex elements. */
+hs_status hs_intensity(hs_ctx* ctx, const float* d_field, int64_t count, float* d_out);
+/* kind 0 training_loss_grad, 1 loss_recon_grad, 2 loss_ssim_grad, 3 loss_mse_grad.
+ * d_recon: L x C x H x W intensities, d_target C x H x W, d_masks L x H x W
+ * bytes (build_masks).  d_grads (nullable) receives dL/dI; *loss the value. */
+hs_status hs_loss(hs_ctx* ctx, int kind, int L, int c, int h, int w, const float* d_recon,
+                  const float* d_target, const uint8_t* d_masks, float* d_grads, double* loss);
+/* build_masks (loss.cpp:235-249) on the host, bit-exact. */
+hs_status hs_build_masks(const double* h_depth, int h, int w, int L, int near_is_high,
+                         uint8_t* h_masks);
+
+/* ---- optimizer (optimizer.hpp:10-49, optimizer.cpp:59-123) --------------------- */
+typedef struct {
+    double beta1, beta2, beta3, eps;
+} hs_adan_config;
+
+/* One Adan step for one group: d_state holds 4*size floats [m | v | n | g_prev].
+ * step_t is the group's 1-based step after increment.  The non-finite check
+ * happens before any update (optimizer.cpp:103-105): on a non-finite gradient
+ * nothing is modified and HS_ENONFINITE is returned with group_name in the
+ * message. */
+hs_status hs_adan_step(hs_ctx* ctx, const hs_adan_config* cfg, const char* group_name,
+                       float* d_params, const float* d_grads, float* d_state, int64_t size,
+                       int step_t, double lr);
+/* cosine_lr (optimizer.cpp:59-64). */
+hs_status hs_cosine_lr(int step, int total_steps, double lr_max, double lr_min, double* out);
+
+/* ---- trainer: the fused step loop body (pipeline.cpp:253-297) ------------------ */
+typedef struct {
+    int n, c, width, height;
+    int planes;                 /* L */
+    const double* distances;    /* L plane distances (make_depth_planes) */
+    hs_prop_spec spec;
+    int total_steps;            /* cosine schedule horizon (config.steps) */
+    const float* h_target;      /* C x H x W linear intensity in [0,1] */
+    const uint8_t* h_masks;     /* L x H x W (build_masks) */
+    /* Optional plane/channel shard for multi-GPU (owned planes [plane_begin,
+     * plane_end)); loss normalisers always use the global L.  0,0 = all. */
+    int plane_begin, plane_end;
+} hs_trainer_config;
+
+hs_status hs_trainer_create(hs_ctx* ctx, const hs_trainer_config* cfg, hs_trainer** out);
+void hs_trainer_destroy(hs_trainer* tr);
+/* Parameters in the layout above; from host (fp32) or device. */
+hs_status hs_trainer_set_params(hs_trainer* tr, const float* params, int from_device);
+hs_status hs_trainer_get_params(hs_trainer* tr, float* params, int to_device);
+/* Device pointers owned by the trainer (params, grads), for zero-copy use
+ * (e.g. a torch.distributed all_reduce of the gradient buffer). */
+float* hs_trainer_params_ptr(hs_trainer* tr);
+float* hs_trainer_grads_ptr(hs_trainer* tr);
+int64_t hs_trainer_param_count(hs_trainer* tr);
+/* One full iteration: raster fwd -> ASM fwd -> loss -> ASM bwd -> raster bwd
+ * -> Adan x6.  *loss_out (nullable) receives the loss of this iteration (that
+ * synchronises); pass NULL to stay asynchronous and fetch it later with
+ * hs_trainer_last_loss. */
+hs_status hs_trainer_step(hs_trainer* tr, double* loss_out);
+/* Split form for multi-GPU: forward+backward into the gradient buffer, then
+ * (after the caller all-reduced hs_trainer_grads_ptr) the optimizer update. */
+hs_status hs_trainer_forward_backward(hs_trainer* tr);
+hs_status hs_trainer_apply_update(hs_trainer* tr);
+hs_status hs_trainer_last_loss(hs_trainer* tr, double* loss_out, int64_t* npairs_out);
+/* Loss partial sums of this rank (recon sum, ssim sum) for cross-rank loss. */
+hs_status hs_trainer_loss_partials(hs_trainer* tr, double* out2);
+hs_status hs_trainer_reserve_pairs(hs_trainer* tr, int64_t cap);
+/* Capture one step into a CUDA graph and replay it (0/1). */
+hs_status hs_trainer_use_graph(hs_trainer* tr, int enable);
+/* Device event timing of the last (eager) step, ms per kernel slot:
+ * [binning, raster_fwd, rows_fwd, cols_fwd, rows_inv, loss, rows_fwd(bwd),
+ *  cols_bwd, rows_inv(bwd), raster_bwd, adan, total].  Needs profiling on and
+ * graphs off. */
+hs_status hs_trainer_set_profiling(hs_trainer* tr, int enable);
+hs_status hs_trainer_stage_ms(hs_trainer* tr, double* out12);
+int hs_trainer_step_count(hs_trainer* tr);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HOLOSPLAT_H */

@@ -1,0 +1,632 @@
+// C ABI (include/holosplat.h) and the device-resident trainer that replaces the
+// step-loop body of proj/core/src/pipeline.cpp:253-297.
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "asm.cuh"
+#include "loss.cuh"
+#include "raster.cuh"
+
+namespace hs {
+
+namespace {
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+
+hs_status fail(hs_status s, const std::string& m) {
+    g_last_error = m;
+    return s;
+}
+
+template <class F>
+hs_status guard(F&& f) {
+    try {
+        f();
+        return HS_OK;
+    } catch (const Error& e) {
+        return fail(e.status, e.what());
+    } catch (const std::bad_alloc&) {
+        return fail(HS_ENOMEM, "host allocation failed");
+    } catch (const std::exception& e) {
+        return fail(HS_ECUDA, e.what());
+    }
+}
+
+const char* kGroupNames[6] = {"position", "scale", "rotation", "amplitude", "phase", "opacity"};
+
+struct CtxWork {
+    RasterWork rw;
+    AsmWork aw;
+    DevBuf flags, partials, out3;
+};
+
+}  // namespace
+
+void note_launch(int n) { g_launches.fetch_add(static_cast<uint64_t>(n), std::memory_order_relaxed); }
+
+int sm_count(int device) {
+    int v = 0;
+    HS_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device));
+    return v;
+}
+
+}  // namespace hs
+
+using namespace hs;
+
+// ctx-owned reusable work buffers for the standalone entry points
+static CtxWork& work_of(hs_ctx* ctx) {
+    if (!ctx->work) ctx->work = new CtxWork();
+    return *static_cast<CtxWork*>(ctx->work);
+}
+
+struct hs_trainer {
+    hs_ctx* ctx = nullptr;
+    int n = 0, c = 0, w = 0, h = 0, L = 0, L_total = 0, plane0 = 0, total_steps = 0;
+    std::vector<double> distances;
+    std::vector<double> wavelengths;
+    hs_prop_spec spec{};
+    int64_t P = 0;
+    DevBuf params, grads, state, field, planes, dplanes, back, target, masks, partials, out3, flags,
+        step;
+    RasterWork rw;
+    AsmWork aw;
+    AdanGroups groups{};
+    int host_step = 0;
+    int loss_slots = 0;
+    bool use_graph = false;
+    cudaGraphExec_t graph = nullptr;
+    bool profiling = false;
+    cudaEvent_t ev[12] = {};  // profiling: start + after each of the 11 kernel slots
+    ~hs_trainer() {
+        if (graph) cudaGraphExecDestroy(graph);
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+    }
+};
+
+extern "C" {
+
+const char* hs_last_error(void) { return g_last_error.c_str(); }
+uint64_t hs_kernel_launch_count(void) { return g_launches.load(); }
+
+hs_status hs_ctx_create(int device, hs_ctx** out) {
+    return guard([&] {
+        int ndev = 0;
+        HS_CUDA(cudaGetDeviceCount(&ndev));
+        require(device >= 0 && device < ndev, "hs_ctx_create: no such device");
+        HS_CUDA(cudaSetDevice(device));
+        cudaDeviceProp prop{};
+        HS_CUDA(cudaGetDeviceProperties(&prop, device));
+        if (prop.major < 10)
+            throw Error(HS_ECUDA, std::string("holosplat-b200 needs sm_100a (B200); found ") + prop.name);
+        auto* c = new hs_ctx;
+        c->device = device;
+        c->num_sms = prop.multiProcessorCount;
+        *out = c;
+    });
+}
+
+void hs_ctx_destroy(hs_ctx* ctx) {
+    if (!ctx) return;
+    delete static_cast<CtxWork*>(ctx->work);
+    ctx->work = nullptr;
+    delete ctx;
+}
+
+hs_status hs_ctx_set_stream(hs_ctx* ctx, void* stream) {
+    ctx->stream = static_cast<cudaStream_t>(stream);
+    return HS_OK;
+}
+
+hs_status hs_ctx_synchronize(hs_ctx* ctx) {
+    return guard([&] { HS_CUDA(cudaStreamSynchronize(ctx->stream)); });
+}
+
+hs_status hs_device_alloc(hs_ctx* ctx, size_t bytes, void** d_out) {
+    return guard([&] {
+        HS_CUDA(cudaSetDevice(ctx->device));
+        HS_CUDA(cudaMalloc(d_out, std::max<size_t>(bytes, 1)));
+    });
+}
+hs_status hs_device_free(hs_ctx*, void* d_ptr) {
+    return guard([&] { HS_CUDA(cudaFree(d_ptr)); });
+}
+hs_status hs_copy_h2d(hs_ctx* ctx, void* d_dst, const void* h_src, size_t bytes) {
+    return guard([&] {
+        HS_CUDA(cudaMemcpyAsync(d_dst, h_src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+        HS_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+hs_status hs_copy_d2h(hs_ctx* ctx, void* h_dst, const void* d_src, size_t bytes) {
+    return guard([&] {
+        HS_CUDA(cudaMemcpyAsync(h_dst, d_src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        HS_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+}  // extern "C"
+
+// ---- rasterizer ----------------------------------------------------------------------
+[[maybe_unused]] static void check_params_finite(RasterWork& rw, cudaStream_t st) {
+    uint32_t stat[4];
+    HS_CUDA(cudaMemcpyAsync(stat, rw.status.p, sizeof(stat), cudaMemcpyDeviceToHost, st));
+    HS_CUDA(cudaStreamSynchronize(st));
+    // field_core.cpp:12,22,29 / gaussian_set.cpp:30-39
+    if (stat[2]) throw Error(HS_EINVAL, "activate: non-finite input");
+}
+
+extern "C" hs_status hs_build_tile_index(hs_ctx* ctx, const float* d_params, int n, int c, int width,
+                              int height, uint32_t* d_tiles, uint32_t* d_ids, uint64_t* d_ranges,
+                              int64_t cap, int64_t* npairs, int* tiles_xy) {
+    return guard([&] {
+        require(width > 0 && height > 0, "build_tile_index: empty canvas");  // rasterizer.cpp:124
+        require(n >= 0, "GaussianSet: invalid N or C");
+        RasterWork& rw = work_of(ctx).rw;
+        rw.prepare(n, c, width, height);
+        tiles_xy[0] = rw.tiles_x;
+        tiles_xy[1] = rw.tiles_y;
+        cudaStream_t st = ctx->stream;
+        for (int attempt = 0; attempt < 2; ++attempt) {
+            rw.project_and_bin(d_params, st);
+            uint32_t stat[4] = {0, 0, 0, 0};
+            HS_CUDA(cudaMemcpyAsync(stat, rw.status.p, sizeof(stat), cudaMemcpyDeviceToHost, st));
+            HS_CUDA(cudaStreamSynchronize(st));
+            if (stat[2]) throw Error(HS_EINVAL, "activate: non-finite input");
+            if (stat[1]) {  // grow and redo: count the exact total on the host side
+                int64_t need = 0;
+                std::vector<uint32_t> counts(n);
+                HS_CUDA(cudaMemcpy(counts.data(), rw.counts.p, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost));
+                for (uint32_t v : counts) need += v;
+                require(need < (int64_t(1) << 32), "build_tile_index: more than 2^32 pairs");
+                rw.reserve_pairs(need + 1);
+                continue;
+            }
+            *npairs = n == 0 ? 0 : stat[0];
+            if (*npairs <= cap && (d_tiles || d_ranges)) {
+                if (n == 0) {
+                    HS_CUDA(cudaMemsetAsync(d_ranges, 0, sizeof(uint64_t) * 2 * rw.tiles_x * rw.tiles_y, st));
+                } else {
+                    export_tile_index(rw, *npairs, d_tiles, d_ids, d_ranges, st);
+                }
+                HS_CUDA(cudaStreamSynchronize(st));
+            }
+            return;
+        }
+        throw Error(HS_EOVERFLOW, "build_tile_index: pair capacity");
+    });
+}
+
+static void raster_prepare_and_bin(hs_ctx* ctx, RasterWork& rw, const float* d_params, int n, int c,
+                                   int width, int height) {
+    rw.prepare(n, c, width, height);
+    cudaStream_t st = ctx->stream;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        rw.project_and_bin(d_params, st);
+        uint32_t stat[4];
+        HS_CUDA(cudaMemcpyAsync(stat, rw.status.p, sizeof(stat), cudaMemcpyDeviceToHost, st));
+        HS_CUDA(cudaStreamSynchronize(st));
+        if (stat[2]) throw Error(HS_EINVAL, "activate: non-finite input");
+        if (!stat[1]) return;
+        std::vector<uint32_t> counts(n);
+        HS_CUDA(cudaMemcpy(counts.data(), rw.counts.p, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost));
+        int64_t need = 0;
+        for (uint32_t v : counts) need += v;
+        rw.reserve_pairs(need + 1);
+    }
+    throw Error(HS_EOVERFLOW, "rasterizer: pair capacity");
+}
+
+extern "C" hs_status hs_rasterize_forward(hs_ctx* ctx, const float* d_params, int n, int c, int width,
+                               int height, float* d_field) {
+    return guard([&] {
+        require(width > 0 && height > 0, "rasterize_forward: empty canvas");  // rasterizer.cpp:129
+        require(c >= 1, "ComplexField: non-positive dims");
+        const size_t bytes = sizeof(float2) * static_cast<size_t>(c) * width * height;
+        if (n == 0) {
+            HS_CUDA(cudaMemsetAsync(d_field, 0, bytes, ctx->stream));
+            return;
+        }
+        RasterWork& rw = work_of(ctx).rw;
+        raster_prepare_and_bin(ctx, rw, d_params, n, c, width, height);
+        raster_forward(rw, reinterpret_cast<float2*>(d_field), ctx->stream);
+    });
+}
+
+extern "C" hs_status hs_rasterize_backward(hs_ctx* ctx, const float* d_params, int n, int c, int width,
+                                int height, const float* d_grad_field, float* d_grads) {
+    return guard([&] {
+        require(width > 0 && height > 0 && c >= 1, "rasterize_backward: gradient shape mismatch");
+        if (n == 0) return;
+        RasterWork& rw = work_of(ctx).rw;
+        raster_prepare_and_bin(ctx, rw, d_params, n, c, width, height);
+        raster_backward(rw, d_params, reinterpret_cast<const float2*>(d_grad_field), d_grads, nullptr,
+                        ctx->stream);
+    });
+}
+
+// ---- propagation ------------------------------------------------------------------------
+static void check_spec(const hs_prop_spec* spec, int c) {
+    require(spec && spec->n_wavelengths == c, "propagation: channel count does not match wavelengths");
+    require(spec->pad_factor >= 1, "propagation: pad_factor must be >= 1");
+}
+
+extern "C" hs_status hs_propagate(hs_ctx* ctx, const hs_prop_spec* spec, int mode, double distance,
+                       double mask_distance, const float* d_in, int c, int h, int w, float* d_out) {
+    return guard([&] {
+        check_spec(spec, c);
+        if (mode == 0 || mode == 2)
+            require(std::isfinite(distance), "propagate: non-finite distance");  // :226
+        double pd = distance, md = distance;
+        if (mode == 1) md = mask_distance;
+        if (mode == 2) pd = -distance;  // propagate_backward: phase -d, mask d (:237)
+        AsmWork& aw = work_of(ctx).aw;
+        aw.prepare(c, h, w, spec->pad_factor, 1);
+        aw.L = 1;
+        aw.set_transfer(*spec, &pd, &md, ctx->stream);
+        asm_forward(aw, reinterpret_cast<const float2*>(d_in), reinterpret_cast<float2*>(d_out), ctx->stream);
+        HS_CUDA(cudaStreamSynchronize(ctx->stream));  // tf_host lifetime
+    });
+}
+
+extern "C" hs_status hs_propagate_multi(hs_ctx* ctx, const hs_prop_spec* spec, const double* h_distances,
+                             int L, const float* d_in, int c, int h, int w, float* d_out) {
+    return guard([&] {
+        check_spec(spec, c);
+        require(L >= 1, "propagate_multi: no distances");
+        AsmWork& aw = work_of(ctx).aw;
+        aw.prepare(c, h, w, spec->pad_factor, L);
+        aw.L = L;
+        aw.set_transfer(*spec, h_distances, h_distances, ctx->stream);
+        asm_forward(aw, reinterpret_cast<const float2*>(d_in), reinterpret_cast<float2*>(d_out), ctx->stream);
+        HS_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+extern "C" hs_status hs_propagate_multi_backward(hs_ctx* ctx, const hs_prop_spec* spec,
+                                      const double* h_distances, int L, const float* d_grads, int c,
+                                      int h, int w, float* d_out) {
+    return guard([&] {
+        require(L >= 1, "propagate_multi_backward: plane count mismatch");  // :268-269
+        check_spec(spec, c);
+        AsmWork& aw = work_of(ctx).aw;
+        aw.prepare(c, h, w, spec->pad_factor, L);
+        aw.L = L;
+        aw.set_transfer(*spec, h_distances, h_distances, ctx->stream);
+        asm_backward(aw, reinterpret_cast<const float2*>(d_grads), reinterpret_cast<float2*>(d_out),
+                     ctx->stream);
+        HS_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+// ---- loss -------------------------------------------------------------------------------------
+extern "C" hs_status hs_intensity(hs_ctx* ctx, const float* d_field, int64_t count, float* d_out) {
+    return guard([&] { intensity_launch(reinterpret_cast<const float2*>(d_field), count, d_out, ctx->stream); });
+}
+
+extern "C" hs_status hs_loss(hs_ctx* ctx, int kind, int L, int c, int h, int w, const float* d_recon,
+                  const float* d_target, const uint8_t* d_masks, float* d_grads, double* loss) {
+    return guard([&] {
+        require(L >= 1, "loss: no reconstruction planes");  // loss.cpp:81
+        require(kind >= 0 && kind <= 3, "loss: unknown kind");
+        CtxWork& cw = work_of(ctx);
+        const int slots = loss_partial_slots(kind, L, c, h, w);
+        cw.partials.reserve(sizeof(double) * 2 * std::max(slots, 1));
+        cw.out3.reserve(sizeof(double) * 3);
+        LossArgs a{kind, L, L, 0, c, h, w, d_recon, nullptr, d_target, d_masks, d_grads, nullptr,
+                   cw.partials.as<double>()};
+        const int used = loss_launch(a, ctx->stream);
+        loss_finalize(a, used, cw.out3.as<double>(), ctx->stream);
+        double out[3];
+        HS_CUDA(cudaMemcpyAsync(out, cw.out3.p, sizeof(out), cudaMemcpyDeviceToHost, ctx->stream));
+        HS_CUDA(cudaStreamSynchronize(ctx->stream));
+        *loss = out[0];
+    });
+}
+
+extern "C" hs_status hs_build_masks(const double* h_depth, int h, int w, int L, int near_is_high, uint8_t* h_masks) {
+    return guard([&] {
+        require(L >= 1, "build_masks: plane count must be >= 1");  // loss.cpp:236
+        const size_t n = static_cast<size_t>(h) * w;
+        std::memset(h_masks, 0, n * L);
+        for (size_t i = 0; i < n; ++i) {  // loss.cpp:241-247
+            int bin = static_cast<int>(std::floor(h_depth[i] * L));
+            bin = std::min(std::max(bin, 0), L - 1);
+            const int plane = near_is_high ? L - 1 - bin : bin;
+            h_masks[static_cast<size_t>(plane) * n + i] = 1;
+        }
+    });
+}
+
+// ---- optimizer ------------------------------------------------------------------------------------
+extern "C" hs_status hs_cosine_lr(int step, int total_steps, double lr_max, double lr_min, double* out) {
+    return guard([&] {
+        require(!(total_steps <= 0 || step < 0 || step > total_steps),
+                "cosine_lr: step outside [0, total_steps]");  // optimizer.cpp:60-61
+        *out = lr_min + 0.5 * (lr_max - lr_min) *
+                            (1.0 + std::cos(3.14159265358979323846 * static_cast<double>(step) / total_steps));
+    });
+}
+
+extern "C" hs_status hs_adan_step(hs_ctx* ctx, const hs_adan_config* cfg, const char* group_name, float* d_params,
+                       const float* d_grads, float* d_state, int64_t size, int step_t, double lr) {
+    return guard([&] {
+        hs_adan_config k = cfg ? *cfg : hs_adan_config{0.98, 0.92, 0.99, 1e-8};
+        CtxWork& cw = work_of(ctx);
+        cw.flags.reserve(sizeof(uint32_t));
+        HS_CUDA(cudaMemsetAsync(cw.flags.p, 0, sizeof(uint32_t), ctx->stream));
+        nonfinite_launch(d_grads, size, cw.flags.as<uint32_t>(), ctx->stream);
+        uint32_t bad = 0;
+        HS_CUDA(cudaMemcpyAsync(&bad, cw.flags.p, sizeof(bad), cudaMemcpyDeviceToHost, ctx->stream));
+        HS_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (bad)  // optimizer.cpp:103-105
+            throw Error(HS_ENONFINITE, std::string("Adan: non-finite gradient in group ") +
+                                           (group_name ? group_name : ""));
+        adan_group_launch(d_params, d_grads, d_state, size, step_t, lr, k.beta1, k.beta2, k.beta3, k.eps,
+                          ctx->stream);
+    });
+}
+
+// ---- trainer ----------------------------------------------------------------------------------------
+// Profiling slots (kernel boundaries): 0 start, 1 binning, 2 raster_fwd,
+// 3 rows_fwd, 4 cols_fwd, 5 rows_inv, 6 loss, 7 rows_fwd(bwd), 8 cols_bwd,
+// 9 rows_inv(bwd), 10 raster_bwd, 11 adan.
+static void trainer_enqueue_fwd_bwd(hs_trainer* t, cudaStream_t st) {
+    const bool prof = t->profiling && !t->use_graph;
+    auto mark = [&](int i) {
+        if (prof) HS_CUDA(cudaEventRecord(t->ev[i], st));
+    };
+    mark(0);
+    HS_CUDA(cudaMemsetAsync(t->flags.p, 0, sizeof(uint32_t), st));
+    t->rw.project_and_bin(t->params.as<float>(), st);
+    mark(1);
+    raster_forward(t->rw, t->field.as<float2>(), st);
+    mark(2);
+    asm_forward(t->aw, t->field.as<float2>(), t->planes.as<float2>(), st, prof ? t->ev + 3 : nullptr);
+    LossArgs a{kLossTraining, t->L, t->L_total, t->plane0, t->c, t->h, t->w, nullptr, t->planes.as<float2>(),
+               t->target.as<float>(), t->masks.as<uint8_t>(), nullptr, t->dplanes.as<float2>(),
+               t->partials.as<double>()};
+    const int used = loss_launch(a, st);
+    loss_finalize(a, used, t->out3.as<double>(), st);
+    mark(6);
+    asm_backward(t->aw, t->dplanes.as<float2>(), t->back.as<float2>(), st, prof ? t->ev + 7 : nullptr);
+    raster_backward(t->rw, t->params.as<float>(), t->back.as<float2>(), t->grads.as<float>(),
+                    t->flags.as<uint32_t>(), st);
+    mark(10);
+}
+
+static void trainer_enqueue_update(hs_trainer* t, cudaStream_t st) {
+    adan_fused_launch(t->params.as<float>(), t->grads.as<float>(), t->state.as<float>(), t->P, t->groups,
+                      t->total_steps, 0.98, 0.92, 0.99, 1e-8, t->step.as<int>(), t->flags.as<uint32_t>(), st);
+    if (t->profiling && !t->use_graph) HS_CUDA(cudaEventRecord(t->ev[11], st));
+}
+
+static void trainer_check_after(hs_trainer* t) {
+    uint32_t flags = 0, stat[4];
+    cudaStream_t st = t->ctx->stream;
+    HS_CUDA(cudaMemcpyAsync(&flags, t->flags.p, sizeof(flags), cudaMemcpyDeviceToHost, st));
+    HS_CUDA(cudaMemcpyAsync(stat, t->rw.status.p, sizeof(stat), cudaMemcpyDeviceToHost, st));
+    HS_CUDA(cudaStreamSynchronize(st));
+    if (stat[1]) throw Error(HS_EOVERFLOW, "trainer: tile-pair capacity exceeded; call hs_trainer_reserve_pairs");
+    if (stat[2]) throw Error(HS_EINVAL, "activate: non-finite input");
+    if (flags) {
+        const int g = __builtin_ctz(flags);
+        throw Error(HS_ENONFINITE, std::string("Adan: non-finite gradient in group ") + kGroupNames[g]);
+    }
+}
+
+extern "C" {
+
+hs_status hs_trainer_create(hs_ctx* ctx, const hs_trainer_config* cfg, hs_trainer** out) {
+    return guard([&] {
+        require(cfg && cfg->n >= 1 && cfg->c >= 1 && cfg->width > 0 && cfg->height > 0,
+                "trainer: invalid configuration");
+        require(cfg->planes >= 1 && cfg->distances, "trainer: plane count must be >= 1");
+        require(cfg->total_steps > 0, "cosine_lr: step outside [0, total_steps]");
+        check_spec(&cfg->spec, cfg->c);
+        auto t = std::make_unique<hs_trainer>();
+        t->ctx = ctx;
+        t->n = cfg->n;
+        t->c = cfg->c;
+        t->w = cfg->width;
+        t->h = cfg->height;
+        t->L_total = cfg->planes;
+        const int pb = (cfg->plane_end > cfg->plane_begin) ? cfg->plane_begin : 0;
+        const int pe = (cfg->plane_end > cfg->plane_begin) ? cfg->plane_end : cfg->planes;
+        require(pb >= 0 && pe <= cfg->planes, "trainer: plane shard out of range");
+        t->plane0 = pb;
+        t->L = pe - pb;
+        t->total_steps = cfg->total_steps;
+        t->distances.assign(cfg->distances + pb, cfg->distances + pe);
+        t->wavelengths.assign(cfg->spec.wavelengths, cfg->spec.wavelengths + cfg->spec.n_wavelengths);
+        t->spec = cfg->spec;
+        t->spec.wavelengths = t->wavelengths.data();
+        const int64_t N = t->n, C = t->c;
+        t->P = (6 + 2 * C) * N;
+        // group boundaries in the flat buffer (gaussian_set.hpp:14-19; pipeline.cpp:243-249)
+        const int64_t b[7] = {0, 2 * N, 4 * N, 5 * N, 5 * N + N * C, 5 * N + 2 * N * C, 6 * N + 2 * N * C};
+        const float lrs[6] = {1e-2f, 5e-3f, 1e-3f, 2.5e-3f, 2.5e-3f, 2.5e-2f};
+        for (int i = 0; i < 6; ++i) {
+            t->groups.begin[i] = b[i];
+            t->groups.end[i] = b[i + 1];
+            t->groups.base_lr[i] = lrs[i];
+        }
+        const size_t hw = static_cast<size_t>(t->h) * t->w, chw = hw * C;
+        cudaStream_t st = ctx->stream;
+        t->params.reserve(sizeof(float) * t->P);
+        t->grads.reserve(sizeof(float) * t->P);
+        t->state.reserve(sizeof(float) * 4 * t->P);
+        HS_CUDA(cudaMemsetAsync(t->state.p, 0, sizeof(float) * 4 * t->P, st));
+        HS_CUDA(cudaMemsetAsync(t->grads.p, 0, sizeof(float) * t->P, st));
+        t->field.reserve(sizeof(float2) * chw);
+        t->planes.reserve(sizeof(float2) * chw * t->L);
+        t->dplanes.reserve(sizeof(float2) * chw * t->L);
+        t->back.reserve(sizeof(float2) * chw);
+        t->target.reserve(sizeof(float) * chw);
+        t->masks.reserve(hw * t->L_total);
+        HS_CUDA(cudaMemcpyAsync(t->target.p, cfg->h_target, sizeof(float) * chw, cudaMemcpyHostToDevice, st));
+        HS_CUDA(cudaMemcpyAsync(t->masks.p, cfg->h_masks, hw * t->L_total, cudaMemcpyHostToDevice, st));
+        t->loss_slots = loss_partial_slots(kLossTraining, t->L, t->c, t->h, t->w);
+        t->partials.reserve(sizeof(double) * 2 * t->loss_slots);
+        t->out3.reserve(sizeof(double) * 3);
+        t->flags.reserve(sizeof(uint32_t));
+        t->step.reserve(2 * sizeof(int));
+        HS_CUDA(cudaMemsetAsync(t->step.p, 0, 2 * sizeof(int), st));
+        HS_CUDA(cudaMemsetAsync(t->flags.p, 0, sizeof(uint32_t), st));
+        t->rw.prepare(t->n, t->c, t->w, t->h);
+        t->aw.prepare(t->c, t->h, t->w, t->spec.pad_factor, t->L);
+        t->aw.L = t->L;
+        t->aw.set_transfer(t->spec, t->distances.data(), t->distances.data(), st);
+        for (auto& e : t->ev) HS_CUDA(cudaEventCreate(&e));
+        HS_CUDA(cudaStreamSynchronize(st));
+        *out = t.release();
+    });
+}
+
+void hs_trainer_destroy(hs_trainer* tr) { delete tr; }
+
+hs_status hs_trainer_set_params(hs_trainer* t, const float* params, int from_device) {
+    return guard([&] {
+        HS_CUDA(cudaMemcpyAsync(t->params.p, params, sizeof(float) * t->P,
+                                from_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, t->ctx->stream));
+        if (!from_device) HS_CUDA(cudaStreamSynchronize(t->ctx->stream));
+    });
+}
+
+hs_status hs_trainer_get_params(hs_trainer* t, float* params, int to_device) {
+    return guard([&] {
+        HS_CUDA(cudaMemcpyAsync(params, t->params.p, sizeof(float) * t->P,
+                                to_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, t->ctx->stream));
+        if (!to_device) HS_CUDA(cudaStreamSynchronize(t->ctx->stream));
+    });
+}
+
+float* hs_trainer_params_ptr(hs_trainer* t) { return t->params.as<float>(); }
+float* hs_trainer_grads_ptr(hs_trainer* t) { return t->grads.as<float>(); }
+int64_t hs_trainer_param_count(hs_trainer* t) { return t->P; }
+int hs_trainer_step_count(hs_trainer* t) { return t->host_step; }
+
+hs_status hs_trainer_reserve_pairs(hs_trainer* t, int64_t cap) {
+    return guard([&] {
+        t->rw.reserve_pairs(cap);
+        if (t->graph) {
+            cudaGraphExecDestroy(t->graph);
+            t->graph = nullptr;
+        }
+    });
+}
+
+hs_status hs_trainer_use_graph(hs_trainer* t, int enable) {
+    t->use_graph = enable != 0;
+    if (!t->use_graph && t->graph) {
+        cudaGraphExecDestroy(t->graph);
+        t->graph = nullptr;
+    }
+    return HS_OK;
+}
+
+hs_status hs_trainer_set_profiling(hs_trainer* t, int enable) {
+    t->profiling = enable != 0;
+    return HS_OK;
+}
+
+hs_status hs_trainer_forward_backward(hs_trainer* t) {
+    return guard([&] {
+        require(t->host_step <= t->total_steps, "cosine_lr: step outside [0, total_steps]");
+        trainer_enqueue_fwd_bwd(t, t->ctx->stream);
+    });
+}
+
+hs_status hs_trainer_apply_update(hs_trainer* t) {
+    return guard([&] {
+        trainer_enqueue_update(t, t->ctx->stream);
+        t->host_step += 1;
+    });
+}
+
+hs_status hs_trainer_step(hs_trainer* t, double* loss_out) {
+    return guard([&] {
+        // cosine_lr(step, steps, ...) throws past the horizon (optimizer.cpp:60-61)
+        require(t->host_step <= t->total_steps, "cosine_lr: step outside [0, total_steps]");
+        cudaStream_t st = t->ctx->stream;
+        if (t->use_graph) {
+            if (!t->graph) {
+                cudaStream_t cap_st = st;
+                bool own = false;
+                if (cap_st == nullptr) {  // legacy stream cannot be captured
+                    HS_CUDA(cudaStreamCreateWithFlags(&cap_st, cudaStreamNonBlocking));
+                    own = true;
+                }
+                cudaGraph_t g = nullptr;
+                HS_CUDA(cudaStreamBeginCapture(cap_st, cudaStreamCaptureModeThreadLocal));
+                try {
+                    trainer_enqueue_fwd_bwd(t, cap_st);
+                    trainer_enqueue_update(t, cap_st);
+                } catch (...) {
+                    cudaStreamEndCapture(cap_st, &g);
+                    if (g) cudaGraphDestroy(g);
+                    if (own) cudaStreamDestroy(cap_st);
+                    throw;
+                }
+                HS_CUDA(cudaStreamEndCapture(cap_st, &g));
+                HS_CUDA(cudaGraphInstantiate(&t->graph, g, 0));
+                HS_CUDA(cudaGraphDestroy(g));
+                if (own) HS_CUDA(cudaStreamDestroy(cap_st));
+            }
+            HS_CUDA(cudaGraphLaunch(t->graph, st));
+            note_launch(0);
+        } else {
+            trainer_enqueue_fwd_bwd(t, st);
+            trainer_enqueue_update(t, st);
+        }
+        t->host_step += 1;
+        if (loss_out) {
+            trainer_check_after(t);
+            double o3[3];
+            HS_CUDA(cudaMemcpy(o3, t->out3.p, sizeof(o3), cudaMemcpyDeviceToHost));
+            *loss_out = o3[0];
+        }
+    });
+}
+
+hs_status hs_trainer_last_loss(hs_trainer* t, double* loss_out, int64_t* npairs_out) {
+    return guard([&] {
+        trainer_check_after(t);
+        double o3[3];
+        uint32_t stat[4];
+        HS_CUDA(cudaMemcpy(o3, t->out3.p, sizeof(o3), cudaMemcpyDeviceToHost));
+        HS_CUDA(cudaMemcpy(stat, t->rw.status.p, sizeof(stat), cudaMemcpyDeviceToHost));
+        if (loss_out) *loss_out = o3[0];
+        if (npairs_out) *npairs_out = stat[0];
+    });
+}
+
+hs_status hs_trainer_loss_partials(hs_trainer* t, double* out2) {
+    return guard([&] {
+        double o3[3];
+        HS_CUDA(cudaMemcpyAsync(o3, t->out3.p, sizeof(o3), cudaMemcpyDeviceToHost, t->ctx->stream));
+        HS_CUDA(cudaStreamSynchronize(t->ctx->stream));
+        out2[0] = o3[1];
+        out2[1] = o3[2];
+    });
+}
+
+hs_status hs_trainer_stage_ms(hs_trainer* t, double* out12) {
+    return guard([&] {
+        require(t->profiling && !t->use_graph, "trainer: stage timing needs profiling on and graphs off");
+        HS_CUDA(cudaEventSynchronize(t->ev[11]));
+        for (int i = 0; i < 11; ++i) {
+            float ms = 0.f;
+            HS_CUDA(cudaEventElapsedTime(&ms, t->ev[i], t->ev[i + 1]));
+            out12[i] = ms;
+        }
+        float tot = 0.f;
+        HS_CUDA(cudaEventElapsedTime(&tot, t->ev[0], t->ev[11]));
+        out12[11] = tot;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,101 @@
+// Shared device/host plumbing for the holosplat-b200 kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "holosplat.h"
+
+namespace hs {
+
+constexpr int kTile = 16;  // rasterizer.hpp:12 kTileSize
+constexpr double kEpsScale = 0.1, kEpsCov = 0.1, kEpsDet = 1e-10;  // field_core.hpp:10-12
+constexpr double kPowerFloor = -50.0, kAlphaCap = 0.99, kAlphaCutoff = 1.0 / 255.0;  // :13-15
+constexpr double kMahalSlack = 1e-9;  // rasterizer.cpp:17
+constexpr int kMaxChannels = 4;       // compiled channel specialisations 1..4
+
+// Error carrying an hs_status; translated at the C-ABI boundary.
+struct Error : std::runtime_error {
+    hs_status status;
+    Error(hs_status s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw Error(e == cudaErrorMemoryAllocation ? HS_ENOMEM : HS_ECUDA,
+                    std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define HS_CUDA(x) ::hs::cuda_check((x), #x)
+
+void note_launch(int n = 1);
+inline void launch_check(const char* name) {
+    note_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw Error(HS_ECUDA, std::string("launch ") + name + ": " + cudaGetErrorString(e));
+}
+
+inline void require(bool ok, const std::string& msg) {
+    if (!ok) throw Error(HS_EINVAL, msg);
+}
+
+// Growable device buffer (never shrinks; reused across calls).
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void reserve(size_t b) {
+        if (b <= bytes) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        HS_CUDA(cudaMalloc(&p, b));
+        bytes = b;
+    }
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    ~DevBuf() { release(); }
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+};
+
+int sm_count(int device);
+
+}  // namespace hs
+
+struct hs_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int num_sms = 148;
+    // reusable work buffers of the standalone C-ABI entry points (capi.cu)
+    void* work = nullptr;
+};
+
+// Device helpers ------------------------------------------------------------------
+namespace hs {
+
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+
+template <class T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+inline unsigned ceil_div(size_t a, size_t b) { return static_cast<unsigned>((a + b - 1) / b); }
+
+}  // namespace hs

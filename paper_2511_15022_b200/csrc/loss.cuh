@@ -1,0 +1,54 @@
+// Training loss (recon + SSIM) and fused Adan.
+#pragma once
+
+#include "common.cuh"
+
+namespace hs {
+
+enum LossKind { kLossTraining = 0, kLossRecon = 1, kLossSsim = 2, kLossMse = 3 };
+
+struct LossArgs {
+    int kind;
+    int L;          // planes in this call
+    int L_norm;     // global plane count for the normalisers (plane sharding)
+    int plane0;     // global index of the first plane in this call (mask selection)
+    int C, H, W;
+    const float* recon;      // L x C x H x W intensities (or nullptr when from_field)
+    const float2* field;     // L x C x H x W complex fields (I = |U|^2), or nullptr
+    const float* target;     // C x H x W
+    const uint8_t* masks;    // L_norm x H x W
+    float* grad;             // dL/dI (L x C x H x W), or nullptr
+    float2* du;              // dL/dU = 2 U dL/dI (L x C x H x W), or nullptr
+    double* partials;        // 2 per CTA: recon-or-mse sum, ssim sum
+};
+
+// Launches the loss kernel(s); returns the number of partial slots written.
+int loss_launch(const LossArgs& a, cudaStream_t st);
+int loss_partial_slots(int kind, int L, int C, int H, int W);
+// Reduces partials into out[0] = loss, out[1] = recon sum, out[2] = ssim sum.
+void loss_finalize(const LossArgs& a, int slots, double* d_out3, cudaStream_t st);
+
+void intensity_launch(const float2* f, int64_t count, float* out, cudaStream_t st);
+
+// Fused Adan over the six groups of the parameter buffer (optimizer.cpp:99-123).
+struct AdanGroups {
+    int64_t begin[6], end[6];
+    float base_lr[6];
+};
+struct AdanDeviceStep {
+    int step;          // 0-based loop step (cosine schedule input)
+    int t;             // 1-based Adan step after increment
+};
+// Reads the step counter from d_step (int2: loop step, adan t) and the flags
+// word; advances the counter.  Position lr follows cosine_lr(step, total,
+// 1e-2, 1e-3) (pipeline.cpp:254).
+void adan_fused_launch(float* params, const float* grads, float* state, int64_t P,
+                       const AdanGroups& g, int total_steps, double b1, double b2, double b3,
+                       double eps, int* d_step, const uint32_t* d_flags, cudaStream_t st);
+// Single group, explicit lr/t (C-ABI hs_adan_step).
+void adan_group_launch(float* params, const float* grads, float* state, int64_t size, int t,
+                       double lr, double b1, double b2, double b3, double eps, cudaStream_t st);
+// Non-finite check of a gradient array -> flag word (bit 0).
+void nonfinite_launch(const float* g, int64_t n, uint32_t* flag, cudaStream_t st);
+
+}  // namespace hs

@@ -1,0 +1,794 @@
+// K0 projection, K1 tile binning, K2 tile-parallel forward splat, K3 backward.
+//
+// Reference: proj/core/src/rasterizer.cpp (activate_flat :33-88, build_index
+// :90-119, rasterize_forward :128-190, rasterize_backward :192-286) and the
+// scalar math of proj/core/src/field_core.cpp:11-68.
+//
+// Numerics
+//  * Projection (K0) runs in fp64 on the fp32 parameters with the reference's
+//    exact operation order and no FMA contraction (__dmul_rn/__dadd_rn), so the
+//    cull radius and tile bounds -- hence the (tile,id) pair list -- are
+//    bit-identical with holo::build_tile_index on the same values.
+//  * Shading (K2/K3) runs in fp32.  The two skip tests of the reference
+//    (mahal > cutoff, alpha_eff < 1/255; rasterizer.cpp:166-169,222-228) are
+//    decided in fp32 outside a per-Gaussian error band `tol` and re-decided in
+//    fp64 with the reference arithmetic inside it, so the set of contributing
+//    (pixel, Gaussian) pairs matches the reference.
+//  * Forward accumulates each pixel in ascending Gaussian id (the sorted
+//    per-tile list), like the reference, so results are run-to-run identical.
+//  * Backward is a per-Gaussian gather (the reference's own decomposition,
+//    rasterizer.cpp:201-284): one warp per Gaussian walks the exact ellipse
+//    footprint row by row, lanes own pixels, a warp-shuffle reduction folds
+//    the 7 + 2C partial sums and lane 0 applies the fp64 chain rule.  No
+//    atomics: the gradients are deterministic.
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+
+#include "raster.cuh"
+
+namespace hs {
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// K0: projection (activate_flat, rasterizer.cpp:33-88; field_core.cpp:11-68)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+__device__ __forceinline__ bool finite(double v) { return isfinite(v); }
+
+struct ProjParams {
+    const float* params;
+    int n, c, width, height, tiles_x, tiles_y;
+    float4* rec;
+    float4* shade;
+    double* p64;
+    int4* pbox;
+    int4* tbox;
+    uint32_t* counts;
+    uint32_t* status;
+};
+
+__global__ void project_kernel(ProjParams P) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= P.n) return;
+    const size_t N = P.n;
+    const float* pp = P.params;                 // pre_position 2N
+    const float* ps = pp + 2 * N;               // pre_scale 2N
+    const float* rot = ps + 2 * N;              // rotation N
+    const float* amp = rot + N;                 // amplitude N*C
+    const float* pha = amp + N * P.c;           // phase N*C
+    const float* opa = pha + N * P.c;           // pre_opacity N
+
+    const double prx = pp[2 * g], pry = pp[2 * g + 1];
+    const double psx = ps[2 * g], psy = ps[2 * g + 1];
+    const double th = rot[g], po = opa[g];
+    if (!(finite(prx) && finite(pry) && finite(psx) && finite(psy) && finite(po)))
+        atomicOr(P.status + 2, 1u);
+
+    // activate_position: (tanh(pre) + 1) * 0.5 * extent   (field_core.cpp:11-14)
+    const double px = dmul(dmul(dadd(tanh(prx), 1.0), 0.5), static_cast<double>(P.width));
+    const double py = dmul(dmul(dadd(tanh(pry), 1.0), 0.5), static_cast<double>(P.height));
+    // activate_scale: exp(pre) + 0.1   (:21-24)
+    const double sx = dadd(exp(psx), kEpsScale);
+    const double sy = dadd(exp(psy), kEpsScale);
+    // covariance (:46-54)
+    const double cth = cos(th), sth = sin(th);
+    const double sx2 = dmul(sx, sx), sy2 = dmul(sy, sy);
+    const double sxx = dadd(dadd(dmul(dmul(sx2, cth), cth), dmul(dmul(sy2, sth), sth)), kEpsCov);
+    const double sxy = dmul(dmul(dsub(sx2, sy2), cth), sth);
+    const double syy = dadd(dadd(dmul(dmul(sx2, sth), sth), dmul(dmul(sy2, cth), cth)), kEpsCov);
+    // invert_covariance (:56-68)
+    const double det = dsub(dmul(sxx, syy), dmul(sxy, sxy));
+    const double det_safe = fmax(det, kEpsDet);
+    const double i00 = ddiv(syy, det_safe), i01 = ddiv(-sxy, det_safe), i11 = ddiv(sxx, det_safe);
+    const double mid = dmul(0.5, dadd(sxx, syy));
+    const double half_diff = dmul(0.5, dsub(sxx, syy));
+    const double lmax = dadd(mid, __dsqrt_rn(fmax(dadd(dmul(half_diff, half_diff), dmul(sxy, sxy)), 0.0)));
+    const double radius3 = dmul(3.0, __dsqrt_rn(fmax(lmax, 0.0)));
+    // activate_opacity: 1 / (1 + exp(-pre))   (:26-29)
+    const double alpha = ddiv(1.0, dadd(1.0, exp(-po)));
+    // rasterizer.cpp:74-77
+    const double cutoff = dmul(2.0, fmax(log(dmul(255.0, alpha)), 0.0));
+    const double mahal_cutoff = dadd(cutoff, kMahalSlack);
+    const double sigma = ddiv(radius3, 3.0);
+    const double r = dadd(dmul(sigma, __dsqrt_rn(fmax(9.0, cutoff))), 1.0);
+
+    // build_index bounds (rasterizer.cpp:95-103)
+    int tx0 = static_cast<int>(floor(ddiv(dsub(px, r), static_cast<double>(kTile))));
+    int tx1 = static_cast<int>(floor(ddiv(dadd(px, r), static_cast<double>(kTile))));
+    int ty0 = static_cast<int>(floor(ddiv(dsub(py, r), static_cast<double>(kTile))));
+    int ty1 = static_cast<int>(floor(ddiv(dadd(py, r), static_cast<double>(kTile))));
+    tx0 = max(tx0, 0);
+    ty0 = max(ty0, 0);
+    tx1 = min(tx1, P.tiles_x - 1);
+    ty1 = min(ty1, P.tiles_y - 1);
+    const uint32_t cnt = (tx1 >= tx0 && ty1 >= ty0)
+                             ? static_cast<uint32_t>((tx1 - tx0 + 1) * (ty1 - ty0 + 1))
+                             : 0u;
+    P.counts[g] = cnt;
+    P.tbox[g] = make_int4(tx0, tx1, ty0, ty1);
+    // pixel bbox (rasterizer.cpp:157-160, 209-212)
+    const int x0 = max(0, static_cast<int>(ceil(dsub(px, r))));
+    const int x1 = min(P.width - 1, static_cast<int>(floor(dadd(px, r))));
+    const int y0 = max(0, static_cast<int>(ceil(dsub(py, r))));
+    const int y1 = min(P.height - 1, static_cast<int>(floor(dadd(py, r))));
+    P.pbox[g] = make_int4(x0, x1, y0, y1);
+
+    // fp32 shading record.  px = px_hi + px_lo so (x - px_hi) - px_lo is the
+    // correctly-rounded fp32 offset of an integer pixel.
+    const float px_hi = static_cast<float>(px), py_hi = static_cast<float>(py);
+    const float px_lo = static_cast<float>(px - static_cast<double>(px_hi));
+    const float py_lo = static_cast<float>(py - static_cast<double>(py_hi));
+    // fp32 error band of the quadratic form: a few ulp of its largest term,
+    // whose size relative to mahal is bounded by the condition number.
+    const double lmin = fmax(mid - sqrt(fmax(half_diff * half_diff + sxy * sxy, 0.0)), 1e-300);
+    const double cond = fmin(lmax / lmin, 1e12);
+    const double tol = 5e-7 * (1.0 + cond) * (1.0 + cutoff) + 1e-6;
+    const double det_inv = i00 * i11 - i01 * i01;
+    P.rec[3 * g + 0] = make_float4(px_hi, py_hi, px_lo, py_lo);
+    P.rec[3 * g + 1] = make_float4(static_cast<float>(i00), static_cast<float>(i01),
+                                   static_cast<float>(i11), static_cast<float>(mahal_cutoff));
+    P.rec[3 * g + 2] = make_float4(static_cast<float>(alpha), static_cast<float>(tol),
+                                   static_cast<float>(det_inv), static_cast<float>(1.0 / i00));
+    double* q = P.p64 + 8 * static_cast<size_t>(g);
+    q[0] = px; q[1] = py; q[2] = i00; q[3] = i01; q[4] = i11; q[5] = mahal_cutoff; q[6] = alpha;
+    q[7] = r;
+    // per-channel shading (rasterizer.cpp:78-85)
+    for (int ch = 0; ch < P.c; ++ch) {
+        const size_t i = static_cast<size_t>(g) * P.c + ch;
+        const double a = fmin(fmax(static_cast<double>(amp[i]), 0.0), 1.0);
+        const double ph = pha[i];
+        if (!finite(ph) || !finite(static_cast<double>(amp[i]))) atomicOr(P.status + 2, 1u);
+        const double cp = cos(ph), sp = sin(ph);
+        P.shade[i] = make_float4(static_cast<float>(a * cp), static_cast<float>(a * sp),
+                                 static_cast<float>(cp), static_cast<float>(sp));
+    }
+    if (!finite(th)) atomicOr(P.status + 2, 1u);
+}
+
+// ---------------------------------------------------------------------------
+// K1a: exclusive scan of per-Gaussian tile counts (3 phases)
+// ---------------------------------------------------------------------------
+constexpr int kScanThreads = 512;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__global__ void scan_reduce_kernel(const uint32_t* in, int n, uint64_t* blocksums) {
+    using BS = cub::BlockReduce<uint64_t, kScanThreads>;
+    __shared__ typename BS::TempStorage tmp;
+    const int base = blockIdx.x * kScanTile;
+    uint64_t s = 0;
+    for (int i = threadIdx.x; i < kScanTile; i += kScanThreads) {
+        const int j = base + i;
+        if (j < n) s += in[j];
+    }
+    s = BS(tmp).Sum(s);
+    if (threadIdx.x == 0) blocksums[blockIdx.x] = s;
+}
+
+// single block: exclusive scan of block sums in place, total -> *total
+__global__ void scan_blocksums_kernel(uint64_t* blocksums, int nb, uint32_t* status, int64_t cap) {
+    __shared__ uint64_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    using BSc = cub::BlockScan<uint64_t, 1024>;
+    __shared__ typename BSc::TempStorage tmp;
+    for (int base = 0; base < nb; base += 1024) {
+        const int i = base + threadIdx.x;
+        uint64_t v = i < nb ? blocksums[i] : 0;
+        uint64_t ex, agg;
+        BSc(tmp).ExclusiveSum(v, ex, agg);
+        if (i < nb) blocksums[i] = ex + carry;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += agg;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const uint64_t total = carry;
+        status[0] = static_cast<uint32_t>(total > 0xffffffffull ? 0xffffffffu : total);
+        status[1] = total > static_cast<uint64_t>(cap) ? 1u : 0u;
+    }
+}
+
+__global__ void scan_apply_kernel(const uint32_t* in, int n, const uint64_t* blocksums,
+                                  uint32_t* out) {
+    using BSc = cub::BlockScan<uint32_t, kScanThreads>;
+    __shared__ typename BSc::TempStorage tmp;
+    const int base = blockIdx.x * kScanTile + threadIdx.x * kScanItems;
+    uint32_t v[kScanItems];
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) v[k] = (base + k < n) ? in[base + k] : 0u;
+    BSc(tmp).ExclusiveSum(v, v);
+    const uint32_t off = static_cast<uint32_t>(blocksums[blockIdx.x]);
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k)
+        if (base + k < n) out[base + k] = v[k] + off;
+}
+
+// ---------------------------------------------------------------------------
+// K1b: duplicate-with-keys (build_index :94-108): (tile << 32 | id), tiles in
+// ty-outer / tx-inner order per Gaussian, Gaussians in id order.
+// ---------------------------------------------------------------------------
+__global__ void emit_keys_kernel(int n, const uint32_t* offsets, const int4* tbox, int tiles_x,
+                                 const uint32_t* status, int64_t cap, uint64_t* keys) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n || status[1]) return;
+    const int4 b = tbox[g];
+    uint32_t o = offsets[g];
+    for (int ty = b.z; ty <= b.w; ++ty)
+        for (int tx = b.x; tx <= b.y; ++tx)
+            keys[o++] = (static_cast<uint64_t>(ty * tiles_x + tx) << 32) | static_cast<uint32_t>(g);
+}
+
+// ---------------------------------------------------------------------------
+// K1c: stable LSD radix sort on the tile field (bits 32..32+tile_bits).  The
+// emitted order is ascending id within every tile, so a stable sort by tile
+// alone yields the reference's std::sort order over (tile, id) pairs.
+// ---------------------------------------------------------------------------
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 16;  // per thread
+constexpr int kSortTile = kSortThreads * kSortItems;
+constexpr int kSortWarps = kSortThreads / 32;
+
+__global__ void radix_hist_kernel(const uint64_t* keys, const uint32_t* status, int shift,
+                                  int nblocks, uint32_t* hist) {
+    __shared__ uint32_t h[256];
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t K = status[1] ? 0 : status[0];
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * kSortTile;
+    for (int i = threadIdx.x; i < kSortTile; i += kSortThreads) {
+        const int64_t j = base + i;
+        if (j < K) atomicAdd(&h[(keys[j] >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    hist[threadIdx.x * nblocks + blockIdx.x] = h[threadIdx.x];
+}
+
+// Per digit: exclusive scan over blocks (in place) + digit total.
+__global__ void radix_scan_kernel(uint32_t* hist, int nblocks, uint32_t* dtot) {
+    using BSc = cub::BlockScan<uint32_t, 256>;
+    __shared__ typename BSc::TempStorage tmp;
+    __shared__ uint32_t carry;
+    uint32_t* h = hist + static_cast<size_t>(blockIdx.x) * nblocks;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < nblocks; base += 256 * 4) {
+        uint32_t v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int i = base + threadIdx.x * 4 + k;
+            v[k] = i < nblocks ? h[i] : 0u;
+        }
+        uint32_t agg;
+        BSc(tmp).ExclusiveSum(v, v, agg);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int i = base + threadIdx.x * 4 + k;
+            if (i < nblocks) h[i] = v[k] + carry;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) carry += agg;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) dtot[blockIdx.x] = carry;
+}
+
+__global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
+    const uint64_t* __restrict__ in, uint64_t* __restrict__ out, const uint32_t* status, int shift,
+    int nblocks, const uint32_t* __restrict__ hist, const uint32_t* __restrict__ dtot) {
+    using BSc = cub::BlockScan<uint32_t, kSortThreads>;
+    __shared__ typename BSc::TempStorage tmp;
+    __shared__ uint32_t wcount[kSortWarps][257];
+    __shared__ uint32_t goff[256];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < kSortWarps * 257; i += kSortThreads) (&wcount[0][0])[i] = 0;
+    {
+        uint32_t dofs;
+        BSc(tmp).ExclusiveSum(dtot[threadIdx.x], dofs);
+        goff[threadIdx.x] = hist[threadIdx.x * nblocks + blockIdx.x] + dofs;
+    }
+    __syncthreads();
+    const int64_t K = status[1] ? 0 : status[0];
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * kSortTile + warp * (32 * kSortItems);
+    uint64_t key[kSortItems];
+    uint32_t rank[kSortItems];
+    uint32_t dig[kSortItems];
+    const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int k = 0; k < kSortItems; ++k) {
+        const int64_t idx = base + k * 32 + lane;
+        const bool valid = idx < K;
+        key[k] = valid ? in[idx] : 0ull;
+        const uint32_t d = valid ? static_cast<uint32_t>((key[k] >> shift) & 255u) : 256u;
+        dig[k] = d;
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const int leader = __ffs(peers) - 1;
+        uint32_t old = 0;
+        if (lane == leader) {
+            old = wcount[warp][d];
+            wcount[warp][d] = old + __popc(peers);
+        }
+        old = __shfl_sync(0xffffffffu, old, leader);
+        rank[k] = old + __popc(peers & lt);
+        __syncwarp();
+    }
+    __syncthreads();
+    {  // exclusive prefix over warps, per digit
+        const int d = threadIdx.x;
+        uint32_t run = 0;
+#pragma unroll
+        for (int w = 0; w < kSortWarps; ++w) {
+            const uint32_t c = wcount[w][d];
+            wcount[w][d] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kSortItems; ++k) {
+        if (dig[k] < 256u) out[goff[dig[k]] + wcount[warp][dig[k]] + rank[k]] = key[k];
+    }
+}
+
+// K1d: per-tile [begin,end) (build_index :110-117); ranges pre-zeroed.
+__global__ void ranges_kernel(const uint64_t* keys, const uint32_t* status, uint2* ranges) {
+    const int64_t K = status[1] ? 0 : status[0];
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= K) return;
+    const uint32_t t = static_cast<uint32_t>(keys[i] >> 32);
+    if (i == 0 || static_cast<uint32_t>(keys[i - 1] >> 32) != t) ranges[t].x = static_cast<uint32_t>(i);
+    if (i == K - 1 || static_cast<uint32_t>(keys[i + 1] >> 32) != t) ranges[t].y = static_cast<uint32_t>(i + 1);
+}
+
+__global__ void export_kernel(const uint64_t* keys, int64_t k, const uint2* ranges, int tiles,
+                              uint32_t* tiles_out, uint32_t* ids_out, uint64_t* ranges_out) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < k) {
+        tiles_out[i] = static_cast<uint32_t>(keys[i] >> 32);
+        ids_out[i] = static_cast<uint32_t>(keys[i]);
+    }
+    if (i < tiles) {
+        ranges_out[2 * i] = ranges[i].x;
+        ranges_out[2 * i + 1] = ranges[i].y;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Exact fp64 contribution test (rasterizer.cpp:164-169 / :220-228).  Returns
+// false when skipped; else G, saturation flag and alpha_eff in fp64.
+// ---------------------------------------------------------------------------
+__device__ __noinline__ bool exact_contrib(const double* __restrict__ q, int x, int y, double& G,
+                                           bool& saturated, double& aeff) {
+    const double dx = dsub(static_cast<double>(x), q[0]);
+    const double dy = dsub(static_cast<double>(y), q[1]);
+    // dx * dx * i00 + 2.0 * dx * dy * i01 + dy * dy * i11
+    const double mahal = dadd(dadd(dmul(dmul(dx, dx), q[2]), dmul(dmul(dmul(2.0, dx), dy), q[3])),
+                              dmul(dmul(dy, dy), q[4]));
+    if (mahal > q[5]) return false;
+    const double power = fmax(dmul(-0.5, mahal), kPowerFloor);
+    G = exp(power);
+    const double aG = dmul(q[6], G);
+    saturated = aG > kAlphaCap;
+    aeff = saturated ? kAlphaCap : aG;
+    return !(aeff < kAlphaCutoff);
+}
+
+// ---------------------------------------------------------------------------
+// K2: forward.  One CTA per 16x16 tile, 8 warps, each warp a 4-row x 8-col
+// cell.  The tile's sorted Gaussian list is staged in shared memory 256 at a
+// time; lane j of a warp tests Gaussian j of a 32-batch against the warp's
+// cell (exact row-band ellipse bound, conservative), the ballot is walked in
+// ascending order and every lane evaluates its pixel.
+// ---------------------------------------------------------------------------
+constexpr int kFwdThreads = 256;
+constexpr int kFwdBatch = 256;
+
+__device__ __forceinline__ bool cell_hit(float4 r0, float4 r1, float4 r2, float cx0, float cy0,
+                                         float cw, float ch) {
+    const float M = r1.w + r2.y;
+    const float px = r0.x + r0.z, py = r0.y + r0.w;
+    const float dya = cy0 - py, dyb = dya + ch;
+    const float dyc = fminf(fmaxf(0.f, dya), dyb);
+    const float D = r1.x * M - r2.z * dyc * dyc;
+    if (D < 0.f) return false;
+    const float hw = sqrtf(D) * r2.w + 1e-2f;
+    const float ratio = r1.y * r2.w;
+    const float ca = -ratio * dya, cb = -ratio * dyb;
+    const float xlo = px + fminf(ca, cb) - hw, xhi = px + fmaxf(ca, cb) + hw;
+    return xhi >= cx0 && xlo <= cx0 + cw;
+}
+
+template <int C>
+__global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(
+    const uint64_t* __restrict__ keys, const uint2* __restrict__ ranges,
+    const float4* __restrict__ rec, const float4* __restrict__ shade,
+    const double* __restrict__ p64, int tiles_x, int W, int H, float2* __restrict__ field) {
+    __shared__ float4 s_rec[3][kFwdBatch];
+    __shared__ float4 s_sh[C][kFwdBatch];
+    __shared__ uint32_t s_id[kFwdBatch];
+    const int tile = blockIdx.x;
+    const int tx = tile % tiles_x, ty = tile / tiles_x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int cx0 = tx * kTile + (warp & 1) * 8;
+    const int cy0 = ty * kTile + (warp >> 1) * 4;
+    const int x = cx0 + (lane & 7), y = cy0 + (lane >> 3);
+    const float fx = static_cast<float>(x), fy = static_cast<float>(y);
+    float2 acc[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) acc[c] = make_float2(0.f, 0.f);
+    const uint2 rg = ranges[tile];
+    for (uint32_t base = rg.x; base < rg.y; base += kFwdBatch) {
+        const int cnt = min(static_cast<int>(rg.y - base), kFwdBatch);
+        __syncthreads();
+        if (static_cast<int>(threadIdx.x) < cnt) {
+            const uint32_t g = static_cast<uint32_t>(keys[base + threadIdx.x]);
+            s_id[threadIdx.x] = g;
+            s_rec[0][threadIdx.x] = rec[3 * static_cast<size_t>(g)];
+            s_rec[1][threadIdx.x] = rec[3 * static_cast<size_t>(g) + 1];
+            s_rec[2][threadIdx.x] = rec[3 * static_cast<size_t>(g) + 2];
+#pragma unroll
+            for (int c = 0; c < C; ++c) s_sh[c][threadIdx.x] = shade[static_cast<size_t>(g) * C + c];
+        }
+        __syncthreads();
+        for (int sub = 0; sub < cnt; sub += 32) {
+            const int j = sub + lane;
+            bool hit = false;
+            if (j < cnt)
+                hit = cell_hit(s_rec[0][j], s_rec[1][j], s_rec[2][j], static_cast<float>(cx0),
+                               static_cast<float>(cy0), 7.f, 3.f);
+            uint32_t mask = __ballot_sync(0xffffffffu, hit);
+            while (mask) {
+                const int jj = sub + __ffs(mask) - 1;
+                mask &= mask - 1;
+                const float4 r0 = s_rec[0][jj], r1 = s_rec[1][jj], r2 = s_rec[2][jj];
+                const float dx = (fx - r0.x) - r0.z;
+                const float dy = (fy - r0.y) - r0.w;
+                const float m = dx * (dx * r1.x + 2.f * dy * r1.y) + dy * dy * r1.z;
+                float aeff = 0.f;
+                if (m <= r1.w - r2.y) {
+                    aeff = fminf(0.99f, r2.x * __expf(-0.5f * m));
+                } else if (m <= r1.w + r2.y) {
+                    double G, ae;
+                    bool sat;
+                    if (exact_contrib(p64 + 8 * static_cast<size_t>(s_id[jj]), x, y, G, sat, ae))
+                        aeff = static_cast<float>(ae);
+                }
+                if (aeff > 0.f) {
+#pragma unroll
+                    for (int c = 0; c < C; ++c) {
+                        const float4 sh = s_sh[c][jj];
+                        acc[c].x = fmaf(sh.x, aeff, acc[c].x);
+                        acc[c].y = fmaf(sh.y, aeff, acc[c].y);
+                    }
+                }
+            }
+        }
+    }
+    if (x < W && y < H) {
+#pragma unroll
+        for (int c = 0; c < C; ++c) field[(static_cast<size_t>(c) * H + y) * W + x] = acc[c];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K3: backward, one warp per Gaussian (rasterize_backward :201-284).
+// ---------------------------------------------------------------------------
+constexpr int kBwdThreads = 256;
+
+template <int C>
+__global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(
+    int N, const float4* __restrict__ rec, const float4* __restrict__ shade,
+    const double* __restrict__ p64, const int4* __restrict__ pbox, const float* __restrict__ params,
+    int W, int H, const float2* __restrict__ gfield, float* __restrict__ grads,
+    uint32_t* __restrict__ flags) {
+    const int lane = threadIdx.x & 31;
+    const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (g >= N) return;
+    const float4 r0 = rec[3 * static_cast<size_t>(g)];
+    const float4 r1 = rec[3 * static_cast<size_t>(g) + 1];
+    const float4 r2 = rec[3 * static_cast<size_t>(g) + 2];
+    float4 sh[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) sh[c] = shade[static_cast<size_t>(g) * C + c];
+    const int4 bb = pbox[g];
+    const float px = r0.x + r0.z, py = r0.y + r0.w;
+    const float i00 = r1.x, i01 = r1.y, i11 = r1.z, cut = r1.w;
+    const float alpha = r2.x, tol = r2.y, detI = r2.z, inv_i00 = r2.w;
+    const float M = cut + tol;
+    const float ratio = i01 * inv_i00;
+
+    float d_amp[C], d_phase[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) d_amp[c] = d_phase[c] = 0.f;
+    float d_alpha = 0.f, gmx = 0.f, gmy = 0.f, ga = 0.f, gb = 0.f, gc = 0.f;
+
+    const float ext = sqrtf(fmaxf(i00 * M / detI, 0.f)) + 1e-2f;
+    const int ya = max(bb.z, static_cast<int>(ceilf(py - ext)));
+    const int yb = min(bb.w, static_cast<int>(floorf(py + ext)));
+    const double* q = p64 + 8 * static_cast<size_t>(g);
+
+    for (int ybase = ya; ybase <= yb; ybase += 32) {
+        const int row = ybase + lane;
+        int xl = 0, wdt = 0;
+        if (row <= yb) {
+            const float dy = static_cast<float>(row) - py;
+            const float D = i00 * M - detI * dy * dy;
+            if (D >= 0.f) {
+                const float hw = sqrtf(D) * inv_i00 + 1e-2f;
+                const float cen = px - ratio * dy;
+                xl = max(bb.x, static_cast<int>(ceilf(cen - hw)));
+                const int xr = min(bb.y, static_cast<int>(floorf(cen + hw)));
+                wdt = max(0, xr - xl + 1);
+            }
+        }
+        int incl = wdt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        const int excl = incl - wdt;
+        for (int fb = 0; fb < total; fb += 32) {
+            const int f = fb + lane;
+            // first row whose inclusive offset exceeds f
+            int r = 0;
+#pragma unroll
+            for (int s = 16; s > 0; s >>= 1) {
+                const int v = __shfl_sync(0xffffffffu, incl, r + s - 1);
+                if (v <= f) r += s;
+            }
+            r = min(r, 31);
+            const int rx = __shfl_sync(0xffffffffu, xl, r);
+            const int rex = __shfl_sync(0xffffffffu, excl, r);
+            if (f >= total) continue;
+            const int x = rx + (f - rex), y = ybase + r;
+            const float dx = (static_cast<float>(x) - r0.x) - r0.z;
+            const float dy = (static_cast<float>(y) - r0.y) - r0.w;
+            const float m = dx * (dx * i00 + 2.f * dy * i01) + dy * dy * i11;
+            if (m > M) continue;
+            float G = expf(-0.5f * m), aeff;
+            bool sat;
+            const float aG = alpha * G;
+            if (m <= cut - tol && fabsf(aG - 0.99f) > 1e-5f) {
+                sat = aG > 0.99f;
+                aeff = sat ? 0.99f : aG;
+            } else {
+                double Gd, ae;
+                if (!exact_contrib(q, x, y, Gd, sat, ae)) continue;
+                G = static_cast<float>(Gd);
+                aeff = static_cast<float>(ae);
+            }
+            float s_amp = 0.f;
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                const float2 gv = gfield[(static_cast<size_t>(c) * H + y) * W + x];
+                const float common = sh[c].z * gv.x + sh[c].w * gv.y;
+                d_amp[c] = fmaf(aeff, common, d_amp[c]);
+                d_phase[c] = fmaf(aeff, sh[c].x * gv.y - sh[c].y * gv.x, d_phase[c]);
+                s_amp += sh[c].x * gv.x + sh[c].y * gv.y;
+            }
+            if (!sat) {
+                d_alpha = fmaf(s_amp, G, d_alpha);
+                const float w = s_amp * alpha * G * -0.5f;
+                gmx += w * -2.f * (dx * i00 + dy * i01);
+                gmy += w * -2.f * (dx * i01 + dy * i11);
+                ga += w * dx * dx;
+                gb += 2.f * w * dx * dy;
+                gc += w * dy * dy;
+            }
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+        d_amp[c] = warp_sum(d_amp[c]);
+        d_phase[c] = warp_sum(d_phase[c]);
+    }
+    d_alpha = warp_sum(d_alpha);
+    gmx = warp_sum(gmx);
+    gmy = warp_sum(gmy);
+    ga = warp_sum(ga);
+    gb = warp_sum(gb);
+    gc = warp_sum(gc);
+    if (lane != 0) return;
+
+    // fp64 chain rule (rasterizer.cpp:251-282)
+    const size_t Ns = N;
+    const float* pp = params;
+    const float* ps = pp + 2 * Ns;
+    const float* rot = ps + 2 * Ns;
+    const float* amp = rot + Ns;
+    const float* pha = amp + Ns * C;
+    const float* opa = pha + Ns * C;
+    (void)pha;
+    float* gpp = grads;
+    float* gps = gpp + 2 * Ns;
+    float* grot = gps + 2 * Ns;
+    float* gamp = grot + Ns;
+    float* gpha = gamp + Ns * C;
+    float* gopa = gpha + Ns * C;
+    uint32_t bad = 0;
+    auto put = [&](float* dst, double v, int group) {
+        const float f = static_cast<float>(v);
+        if (!isfinite(f)) bad |= 1u << group;
+        *dst = f;
+    };
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+        const size_t i = static_cast<size_t>(g) * C + c;
+        const float raw = amp[i];
+        put(gamp + i, (raw >= 0.f && raw <= 1.f) ? static_cast<double>(d_amp[c]) : 0.0, 3);
+        put(gpha + i, d_phase[c], 4);
+    }
+    const double po = opa[g];
+    const double sig = 1.0 / (1.0 + exp(-po));
+    put(gopa + g, d_alpha * (sig * (1.0 - sig)), 5);
+    const double tx = tanh(static_cast<double>(pp[2 * g])), ty = tanh(static_cast<double>(pp[2 * g + 1]));
+    put(gpp + 2 * g, gmx * (0.5 * W * (1.0 - tx * tx)), 0);
+    put(gpp + 2 * g + 1, gmy * (0.5 * H * (1.0 - ty * ty)), 0);
+    const double esx = exp(static_cast<double>(ps[2 * g])), esy = exp(static_cast<double>(ps[2 * g + 1]));
+    const double sx = esx + kEpsScale, sy = esy + kEpsScale;
+    const double th = rot[g];
+    const double ct = cos(th), st = sin(th);
+    const double sx2 = sx * sx, sy2 = sy * sy;
+    const double c00 = sx2 * ct * ct + sy2 * st * st + kEpsCov;
+    const double c01 = (sx2 - sy2) * ct * st;
+    const double c11 = sx2 * st * st + sy2 * ct * ct + kEpsCov;
+    const double det = c00 * c11 - c01 * c01;
+    const double dsafe = fmax(det, kEpsDet);
+    const double t_adj = ga * c11 - gb * c01 + gc * c00;
+    const double clamped = det > kEpsDet ? 1.0 : 0.0;
+    const double d2 = dsafe * dsafe;
+    const double gS00 = gc / dsafe - t_adj * (clamped * c11) / d2;
+    const double gS01 = -gb / dsafe - t_adj * (clamped * -2.0 * c01) / d2;
+    const double gS11 = ga / dsafe - t_adj * (clamped * c00) / d2;
+    const double dsx = 2.0 * sx * (ct * ct * gS00 + ct * st * gS01 + st * st * gS11);
+    const double dsy = 2.0 * sy * (st * st * gS00 - ct * st * gS01 + ct * ct * gS11);
+    put(gps + 2 * g, dsx * esx, 1);
+    put(gps + 2 * g + 1, dsy * esy, 1);
+    put(grot + g, 2.0 * (sy2 - sx2) * ct * st * gS00 + (sx2 - sy2) * (ct * ct - st * st) * gS01 +
+                      2.0 * (sx2 - sy2) * ct * st * gS11,
+        2);
+    if (bad && flags) atomicOr(flags, bad);
+}
+
+int bits_for(int64_t v) {
+    int b = 1;
+    while ((int64_t(1) << b) <= v) ++b;
+    return b;
+}
+
+}  // namespace
+
+void RasterWork::prepare(int n_, int c_, int w_, int h_) {
+    require(c_ >= 1 && c_ <= kMaxChannels,
+            "rasterizer: channel count " + std::to_string(c_) + " outside 1..4");
+    n = n_;
+    c = c_;
+    width = w_;
+    height = h_;
+    tiles_x = (w_ + kTile - 1) / kTile;
+    tiles_y = (h_ + kTile - 1) / kTile;
+    tile_bits = bits_for(static_cast<int64_t>(tiles_x) * tiles_y - 1);
+    const size_t N = std::max(n, 1);
+    rec.reserve(N * 3 * sizeof(float4));
+    shade.reserve(N * c * sizeof(float4));
+    p64.reserve(N * 8 * sizeof(double));
+    pbox.reserve(N * sizeof(int4));
+    tbox.reserve(N * sizeof(int4));
+    counts.reserve(N * sizeof(uint32_t));
+    offsets.reserve(N * sizeof(uint32_t));
+    blocksums.reserve((N / kScanTile + 2) * sizeof(uint64_t));
+    ranges.reserve(static_cast<size_t>(tiles_x) * tiles_y * sizeof(uint2));
+    status.reserve(4 * sizeof(uint32_t));
+    if (cap == 0) reserve_pairs(std::max<int64_t>(int64_t(1) << 20, 16 * static_cast<int64_t>(N)));
+}
+
+void RasterWork::reserve_pairs(int64_t cap_) {
+    if (cap_ <= cap) return;
+    cap = cap_;
+    keys[0].reserve(static_cast<size_t>(cap) * sizeof(uint64_t));
+    keys[1].reserve(static_cast<size_t>(cap) * sizeof(uint64_t));
+    const size_t nblocks = (cap + kSortTile - 1) / kSortTile;
+    hist.reserve(nblocks * 256 * sizeof(uint32_t));
+    dtot.reserve(256 * sizeof(uint32_t));
+}
+
+void RasterWork::project_and_bin(const float* d_params, cudaStream_t st) {
+    uint32_t* stat = status.as<uint32_t>();
+    HS_CUDA(cudaMemsetAsync(stat, 0, 4 * sizeof(uint32_t), st));
+    const int tiles = tiles_x * tiles_y;
+    HS_CUDA(cudaMemsetAsync(ranges.p, 0, static_cast<size_t>(tiles) * sizeof(uint2), st));
+    if (n == 0) return;
+    ProjParams P{d_params, n,  c,  width, height, tiles_x, tiles_y, rec.as<float4>(),
+                 shade.as<float4>(), p64.as<double>(), pbox.as<int4>(), tbox.as<int4>(),
+                 counts.as<uint32_t>(), stat};
+    project_kernel<<<ceil_div(n, 128), 128, 0, st>>>(P);
+    launch_check("project");
+    const int nb = ceil_div(n, kScanTile);
+    scan_reduce_kernel<<<nb, kScanThreads, 0, st>>>(counts.as<uint32_t>(), n, blocksums.as<uint64_t>());
+    launch_check("scan_reduce");
+    scan_blocksums_kernel<<<1, 1024, 0, st>>>(blocksums.as<uint64_t>(), nb, stat, cap);
+    launch_check("scan_blocksums");
+    scan_apply_kernel<<<nb, kScanThreads, 0, st>>>(counts.as<uint32_t>(), n, blocksums.as<uint64_t>(),
+                                                   offsets.as<uint32_t>());
+    launch_check("scan_apply");
+    emit_keys_kernel<<<ceil_div(n, 128), 128, 0, st>>>(n, offsets.as<uint32_t>(), tbox.as<int4>(),
+                                                       tiles_x, stat, cap, keys[0].as<uint64_t>());
+    launch_check("emit_keys");
+    const int nblocks = static_cast<int>((cap + kSortTile - 1) / kSortTile);
+    int cur = 0;
+    for (int shift = 32; shift < 32 + tile_bits; shift += 8) {
+        radix_hist_kernel<<<nblocks, kSortThreads, 0, st>>>(keys[cur].as<uint64_t>(), stat, shift,
+                                                            nblocks, hist.as<uint32_t>());
+        launch_check("radix_hist");
+        radix_scan_kernel<<<256, 256, 0, st>>>(hist.as<uint32_t>(), nblocks, dtot.as<uint32_t>());
+        launch_check("radix_scan");
+        radix_scatter_kernel<<<nblocks, kSortThreads, 0, st>>>(
+            keys[cur].as<uint64_t>(), keys[cur ^ 1].as<uint64_t>(), stat, shift, nblocks,
+            hist.as<uint32_t>(), dtot.as<uint32_t>());
+        launch_check("radix_scatter");
+        cur ^= 1;
+    }
+    sorted_buf = cur;
+    ranges_kernel<<<ceil_div(cap, 256), 256, 0, st>>>(keys[cur].as<uint64_t>(), stat,
+                                                      ranges.as<uint2>());
+    launch_check("ranges");
+}
+
+void export_tile_index(const RasterWork& rw, int64_t k, uint32_t* d_tiles, uint32_t* d_ids,
+                       uint64_t* d_ranges, cudaStream_t st) {
+    const int tiles = rw.tiles_x * rw.tiles_y;
+    const int64_t m = std::max<int64_t>(k, tiles);
+    if (m == 0) return;
+    export_kernel<<<ceil_div(m, 256), 256, 0, st>>>(rw.sorted_keys(), k, rw.ranges.as<uint2>(), tiles,
+                                                    d_tiles, d_ids, d_ranges);
+    launch_check("export_tile_index");
+}
+
+template <int C>
+static void fwd_launch(const RasterWork& rw, float2* d_field, cudaStream_t st) {
+    raster_fwd_kernel<C><<<rw.tiles_x * rw.tiles_y, kFwdThreads, 0, st>>>(
+        rw.sorted_keys(), rw.ranges.as<uint2>(), rw.rec.as<float4>(), rw.shade.as<float4>(),
+        rw.p64.as<double>(), rw.tiles_x, rw.width, rw.height, d_field);
+    launch_check("raster_fwd");
+}
+
+void raster_forward(const RasterWork& rw, float2* d_field, cudaStream_t st) {
+    switch (rw.c) {
+        case 1: fwd_launch<1>(rw, d_field, st); break;
+        case 2: fwd_launch<2>(rw, d_field, st); break;
+        case 3: fwd_launch<3>(rw, d_field, st); break;
+        case 4: fwd_launch<4>(rw, d_field, st); break;
+        default: throw Error(HS_EINVAL, "rasterizer: unsupported channel count");
+    }
+}
+
+template <int C>
+static void bwd_launch(const RasterWork& rw, const float* d_params, const float2* d_gf,
+                       float* d_grads, uint32_t* d_flags, cudaStream_t st) {
+    const int warps_per_block = kBwdThreads / 32;
+    raster_bwd_kernel<C><<<ceil_div(rw.n, warps_per_block), kBwdThreads, 0, st>>>(
+        rw.n, rw.rec.as<float4>(), rw.shade.as<float4>(), rw.p64.as<double>(), rw.pbox.as<int4>(),
+        d_params, rw.width, rw.height, d_gf, d_grads, d_flags);
+    launch_check("raster_bwd");
+}
+
+void raster_backward(const RasterWork& rw, const float* d_params, const float2* d_grad_field,
+                     float* d_grads, uint32_t* d_flags, cudaStream_t st) {
+    if (rw.n == 0) return;
+    switch (rw.c) {
+        case 1: bwd_launch<1>(rw, d_params, d_grad_field, d_grads, d_flags, st); break;
+        case 2: bwd_launch<2>(rw, d_params, d_grad_field, d_grads, d_flags, st); break;
+        case 3: bwd_launch<3>(rw, d_params, d_grad_field, d_grads, d_flags, st); break;
+        case 4: bwd_launch<4>(rw, d_params, d_grad_field, d_grads, d_flags, st); break;
+        default: throw Error(HS_EINVAL, "rasterizer: unsupported channel count");
+    }
+}
+
+}  // namespace hs

@@ -1,0 +1,44 @@
+// Rasterizer work buffers and launchers (K0 projection, K1 binning, K2 forward,
+// K3 backward).  See raster.cu for the kernels and the reference mapping.
+#pragma once
+
+#include "common.cuh"
+
+namespace hs {
+
+// Device-resident projection + tile index for one (set, canvas).  Buffers are
+// reused across calls and only grow.
+struct RasterWork {
+    int n = 0, c = 0, width = 0, height = 0;
+    int tiles_x = 0, tiles_y = 0, tile_bits = 0;
+    DevBuf rec;      // 3 float4 per Gaussian (fp32 shading record)
+    DevBuf shade;    // C float4 per Gaussian: amp*cos, amp*sin, cos, sin
+    DevBuf p64;      // 8 doubles per Gaussian (exact fp64 record for boundary rechecks)
+    DevBuf pbox;     // int4 pixel bbox (x0,x1,y0,y1) clamped to the canvas
+    DevBuf tbox;     // int4 tile bbox
+    DevBuf counts;   // uint32 tiles per Gaussian
+    DevBuf offsets;  // uint32 exclusive scan of counts
+    DevBuf blocksums;
+    DevBuf keys[2];  // uint64 (tile << 32 | id), ping-pong for the radix sort
+    DevBuf hist;     // radix histograms
+    DevBuf dtot;     // per-digit totals
+    DevBuf ranges;   // uint2 [begin,end) per tile
+    DevBuf status;   // uint32[4]: [0] K (pairs), [1] overflow, [2] non-finite param, [3] unused
+    int64_t cap = 0; // pair capacity
+    int sorted_buf = 0;  // which keys[] holds the sorted result
+
+    void prepare(int n_, int c_, int w_, int h_);
+    void reserve_pairs(int64_t cap_);
+    // K0 + K1 on stream; leaves sorted keys + ranges on device (K in status[0]).
+    void project_and_bin(const float* d_params, cudaStream_t st);
+    const uint64_t* sorted_keys() const { return keys[sorted_buf].as<uint64_t>(); }
+};
+
+void raster_forward(const RasterWork& rw, float2* d_field, cudaStream_t st);
+void raster_backward(const RasterWork& rw, const float* d_params, const float2* d_grad_field,
+                     float* d_grads, uint32_t* d_flags, cudaStream_t st);
+// tiles/ids (uint32) + ranges (uint64 pairs) export for build_tile_index.
+void export_tile_index(const RasterWork& rw, int64_t k, uint32_t* d_tiles, uint32_t* d_ids,
+                       uint64_t* d_ranges, cudaStream_t st);
+
+}  // namespace hs

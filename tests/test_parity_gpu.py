@@ -1,0 +1,275 @@
+"""GPU parity: the B200 kernels (through the C ABI) against the reference
+library compiled from its own sources (oracle/_ref), on identical fp32-valued
+inputs.  Bars (BASELINE.json north_star): tile binning and sort order
+bit-exact; propagated field rel-L2 <= 1e-4; parameter gradients rel-L2 <= 1e-3.
+"""
+import numpy as np
+import pytest
+
+from paper_2511_15022_b200 import synthetic as S
+
+pytestmark = pytest.mark.gpu
+
+RASTER_TOL = 1e-4
+FIELD_TOL = 1e-4
+GRAD_TOL = 1e-3
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, dtype=np.float64).ravel()
+    b = np.asarray(b, dtype=np.float64).ravel()
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def f32(d):
+    return {k: np.asarray(v, dtype=np.float32).astype(np.float64) for k, v in d.items()}
+
+
+def sets(holo, ref, groups, n, c):
+    hs = holo.GaussianSet(n, c, **groups)
+    rs = ref.GaussianSet(n, c, *[np.ascontiguousarray(groups[k]) for k in ref.GROUPS])
+    return hs, rs
+
+
+CASES = [  # (seed, n, c, w, h)
+    (1, 9, 1, 26, 20), (2, 9, 3, 35, 27), (3, 9, 1, 44, 34), (4, 9, 3, 53, 41),
+    (11, 14, 3, 70, 50), (21, 12, 1, 55, 37), (31, 300, 2, 128, 96), (5, 2000, 3, 256, 160),
+]
+
+
+@pytest.mark.parametrize("seed,n,c,w,h", CASES)
+def test_tile_index_bit_exact_random_set(holo, ref, seed, n, c, w, h):
+    g = f32(S.random_set(seed, n, c))
+    hs, rs = sets(holo, ref, g, n, c)
+    a = holo.build_tile_index(hs, w, h)
+    b = ref.build_tile_index(rs, w, h)
+    assert (a.tiles_x, a.tiles_y) == (b["tiles_x"], b["tiles_y"])
+    assert np.array_equal(a.pairs[:, 0], b["tiles"])
+    assert np.array_equal(a.pairs[:, 1], b["ids"])
+    assert np.array_equal(a.ranges, b["ranges"])
+
+
+@pytest.mark.parametrize("n,c,w,h,seed", [(10_000, 1, 256, 256, 42), (3413, 1, 256, 160, 42),
+                                          (50_000, 3, 960, 540, 42)])
+def test_tile_index_bit_exact_init(holo, ref, n, c, w, h, seed):
+    g = f32(S.init_gaussians(n, c, w, h, seed))
+    hs, rs = sets(holo, ref, g, n, c)
+    a = holo.build_tile_index(hs, w, h)
+    b = ref.build_tile_index(rs, w, h)
+    assert a.pairs.shape[0] == b["tiles"].shape[0]
+    assert np.array_equal(a.pairs[:, 0], b["tiles"])
+    assert np.array_equal(a.pairs[:, 1], b["ids"])
+    assert np.array_equal(a.ranges, b["ranges"])
+
+
+@pytest.mark.parametrize("seed,n,c,w,h", CASES)
+def test_rasterize_forward(holo, ref, seed, n, c, w, h):
+    g = f32(S.random_set(seed, n, c))
+    hs, rs = sets(holo, ref, g, n, c)
+    a = holo.rasterize_forward(hs, w, h)
+    re, im = ref.rasterize_forward(rs, w, h)
+    err = rel_l2(np.stack([a.real, a.imag]), np.stack([re, im]))
+    assert err <= RASTER_TOL, err
+    assert np.max(np.abs(a.real - re)) < 1e-5
+
+
+def test_rasterize_forward_init_cfg1(holo, ref):
+    n, c, w, h = 10_000, 1, 256, 256
+    g = f32(S.init_gaussians(n, c, w, h, 42))
+    hs, rs = sets(holo, ref, g, n, c)
+    a = holo.rasterize_forward(hs, w, h)
+    re, im = ref.rasterize_forward(rs, w, h)
+    assert rel_l2(np.stack([a.real, a.imag]), np.stack([re, im])) <= RASTER_TOL
+
+
+def test_empty_set_rasterizes_to_zeros(holo):
+    f = holo.rasterize_forward(holo.GaussianSet(0, 2), 20, 10)
+    assert not f.real.any() and not f.imag.any()
+
+
+def test_high_opacity_tails(holo, ref):
+    # test_rasterizer.cpp:76-92
+    g = dict(pre_position=np.zeros(2), pre_scale=np.log([2.0, 2.0]), rotation=np.zeros(1),
+             amplitude=np.ones(1), phase=np.zeros(1), pre_opacity=np.array([5.0]))
+    g = f32(g)
+    hs, rs = sets(holo, ref, g, 1, 1)
+    a = holo.rasterize_forward(hs, 64, 64)
+    re, im = ref.rasterize_forward(rs, 64, 64)
+    assert np.max(np.abs(a.real - re)) <= 1e-6
+    assert abs(a.real[0, 32, 39]) > 0.0
+
+
+@pytest.mark.parametrize("seed,n,c,w,h", CASES)
+def test_rasterize_backward(holo, ref, seed, n, c, w, h):
+    g = f32(S.random_set(seed, n, c))
+    hs, rs = sets(holo, ref, g, n, c)
+    wre = S.random_real(seed + 40, c, h, w, -1.0, 1.0).astype(np.float32).astype(np.float64)
+    wim = S.random_real(seed + 41, c, h, w, -1.0, 1.0).astype(np.float32).astype(np.float64)
+    a = holo.rasterize_backward(hs, holo.RealField(c, h, w, wre), holo.RealField(c, h, w, wim))
+    b = ref.rasterize_backward(rs, wre, wim)
+    for k in ref.GROUPS:
+        err = rel_l2(getattr(a, k), getattr(b, k))
+        assert err <= GRAD_TOL, (k, err)
+
+
+def test_saturation_gates(holo):
+    # test_rasterizer.cpp:225-244
+    g = dict(pre_position=np.zeros(2), pre_scale=np.log([10.0, 10.0]), rotation=np.zeros(1),
+             amplitude=np.ones(1), phase=np.array([0.3]), pre_opacity=np.array([8.0]))
+    hs = holo.GaussianSet(1, 1, **f32(g))
+    wre = np.zeros((1, 31, 31))
+    wre[0, 15, 15] = 1.0
+    gr = holo.rasterize_backward(hs, holo.RealField(1, 31, 31, wre), holo.RealField(1, 31, 31))
+    assert gr.pre_opacity[0] == 0.0
+    assert gr.pre_scale[0] == 0.0 and gr.pre_scale[1] == 0.0
+    assert gr.pre_position[0] == 0.0
+    assert gr.amplitude[0] != 0.0
+
+
+def spec_for(holo, ref, channels, pad=2, aperture=0.0):
+    wl = S.WAVELENGTHS[channels]
+    return (holo.PropagationSpec(wl, 3.74e-6, pad, aperture), ref.PropagationSpec(wl, 3.74e-6, pad, aperture))
+
+
+def field32(seed, c, h, w):
+    re, im = S.random_field(seed, c, h, w)
+    return re.astype(np.float32).astype(np.float64), im.astype(np.float32).astype(np.float64)
+
+
+@pytest.mark.parametrize("c,h,w,pad,ap,d", [
+    (1, 24, 32, 2, 0.0, 1e-3), (1, 24, 32, 2, 0.0, 1e-2), (3, 16, 24, 2, 0.0, 5e-3),
+    (1, 16, 16, 2, 6.5, 2e-3), (1, 9, 15, 1, 0.0, 1e-3), (1, 10, 10, 3, 0.0, 2e-3),
+    (3, 20, 28, 2, 0.0, 3e-3), (3, 96, 128, 2, 0.0, 3e-3), (1, 160, 256, 2, 0.0, 3e-3),
+    (2, 37, 41, 2, 0.0, 4e-3),
+])
+def test_propagate(holo, ref, c, h, w, pad, ap, d):
+    hsp, rsp = spec_for(holo, ref, c, pad, ap)
+    re, im = field32(100 + h, c, h, w)
+    a = holo.propagate(holo.ComplexField(c, h, w, re, im), hsp, d)
+    b = ref.propagate(re, im, rsp, d)
+    err = rel_l2(np.stack([a.real, a.imag]), np.stack(b))
+    assert err <= FIELD_TOL, err
+
+
+def test_propagate_backward_and_mask_distance(holo, ref):
+    hsp, rsp = spec_for(holo, ref, 1, 1)
+    re, im = field32(12, 1, 32, 32)
+    u = holo.ComplexField(1, 32, 32, re, im)
+    a = holo.propagate_backward(u, hsp, 4e-3)
+    b = ref.propagate(re, im, rsp, 4e-3, mode=2)
+    assert rel_l2(np.stack([a.real, a.imag]), np.stack(b)) <= FIELD_TOL
+    a = holo.propagate_with_mask_distance(u, hsp, 2e-3, 6e-3)
+    b = ref.propagate(re, im, rsp, 2e-3, mode=1, mask_distance=6e-3)
+    assert rel_l2(np.stack([a.real, a.imag]), np.stack(b)) <= FIELD_TOL
+
+
+def test_propagate_multi_and_backward(holo, ref):
+    c, h, w = 3, 40, 56
+    hsp, rsp = spec_for(holo, ref, c, 2)
+    dist = [1e-3, 3e-3, 5e-3]
+    re, im = field32(15, c, h, w)
+    a = holo.propagate_multi(holo.ComplexField(c, h, w, re, im), hsp, dist)
+    bre, bim = ref.propagate_multi(re, im, rsp, dist)
+    for l in range(3):
+        assert rel_l2(np.stack([a[l].real, a[l].imag]), np.stack([bre[l], bim[l]])) <= FIELD_TOL
+    gre = np.stack([field32(30 + l, c, h, w)[0] for l in range(3)])
+    gim = np.stack([field32(40 + l, c, h, w)[1] for l in range(3)])
+    gs = [holo.ComplexField(c, h, w, gre[l], gim[l]) for l in range(3)]
+    a = holo.propagate_multi_backward(gs, hsp, dist)
+    b = ref.propagate_multi_backward(gre, gim, rsp, dist)
+    assert rel_l2(np.stack([a.real, a.imag]), np.stack(b)) <= FIELD_TOL
+
+
+def test_propagate_cfg2_grid(holo, ref):
+    """Full cfg2 padded grid (2160 x 3840) for one channel vs the reference."""
+    c, h, w = 1, 1080, 1920
+    hsp, rsp = spec_for(holo, ref, c, 2)
+    re, im = field32(77, c, h, w)
+    a = holo.propagate(holo.ComplexField(c, h, w, re, im), hsp, 3e-3)
+    b = ref.propagate(re, im, rsp, 3e-3)
+    assert rel_l2(np.stack([a.real, a.imag]), np.stack(b)) <= FIELD_TOL
+
+
+@pytest.mark.parametrize("kind", ["training", "recon", "ssim", "mse"])
+@pytest.mark.parametrize("c,h,w,L", [(1, 16, 16, 2), (3, 32, 48, 2), (3, 64, 80, 3)])
+def test_loss(holo, ref, kind, c, h, w, L):
+    img = S.random_real(7 + c, c, h, w, 0.0, 1.0).astype(np.float32).astype(np.float64)
+    depth = S.random_real(1007 + c, 1, h, w, 0.0, 1.0)[0]
+    recon = np.stack([S.random_real(50 + l, c, h, w, 0.0, 1.0) for l in range(L)])
+    recon = recon.astype(np.float32).astype(np.float64)
+    tgt = holo.make_target_stack(holo.RealField(c, h, w, img), holo.RealField(1, h, w, depth), L, True)
+    grads = []
+    v = holo._loss(kind, [holo.RealField(c, h, w, recon[l]) for l in range(L)], tgt, grads)
+    rv, rg = ref.loss(kind, recon, img, depth)
+    assert abs(v - rv) <= 1e-5 * max(1.0, abs(rv)), (v, rv)
+    assert rel_l2(np.stack([g.values for g in grads]), rg) <= 1e-4
+
+
+def test_adan_matches_reference_trajectory(holo, ref):
+    # test_optimizer.cpp:282-296 vector trajectory (fp32 device state)
+    a = holo.Adan()
+    a.add_group("xy", 2, 0.05)
+    r = ref.Adan()
+    r.add_group("xy", 2, 0.05)
+    x = np.array([0.7, -0.3])
+    xr = x.copy()
+    for _ in range(4):
+        a.step("xy", x, np.array([2.0 * x[0], np.cos(x[1])]))
+        r.step("xy", xr, np.array([2.0 * xr[0], np.cos(xr[1])]))
+    assert np.max(np.abs(x - xr)) < 1e-6
+
+
+def test_adan_nonfinite_names_group(holo):
+    a = holo.Adan()
+    a.add_group("params", 2, 0.1)
+    with pytest.raises(holo.HoloNonFinite, match="params"):
+        a.step("params", np.zeros(2), np.array([np.nan, 0.0]))
+    with pytest.raises(holo.HoloInvalidArgument):
+        a.add_group("params", 2, 0.1)
+
+
+@pytest.mark.parametrize("c,w,h,n,L", [(1, 64, 48, 400, 1), (3, 96, 64, 1500, 2), (3, 256, 160, 3413, 2)])
+def test_full_step_matches_reference(holo, ref, c, w, h, n, L):
+    g = f32(S.init_gaussians(n, c, w, h, 42))
+    hs, rs = sets(holo, ref, g, n, c)
+    target = S.synthetic_image(42, c, h, w).astype(np.float32).astype(np.float64)
+    depth = S.synthetic_depth(43, h, w)
+    masks = S.build_masks(depth, L, True)
+    dist = S.make_depth_planes(L, 3e-3, 2e-3)
+    wl = S.WAVELENGTHS[c]
+    tr = holo.Trainer(hs, w, h, holo.RealField(c, h, w, target), masks, dist,
+                      holo.PropagationSpec(wl), total_steps=20)
+    rt = ref.Trainer(rs, w, h, target, depth, L, 3e-3, 2e-3, ref.PropagationSpec(wl), 20)
+    tr.forward_backward()
+    grads = tr.grads_tensor().cpu().numpy().astype(np.float64)
+    tr.apply_update()
+    loss = tr.last_loss()[0]
+    rloss, rgrads = rt.step(want_grads=True)
+    assert abs(loss - rloss) / abs(rloss) < 1e-4
+    o = 0
+    for k in ref.GROUPS:
+        rgk = getattr(rgrads, k)
+        err = rel_l2(grads[o:o + rgk.size], rgk)
+        assert err <= GRAD_TOL, (k, err)
+        o += rgk.size
+    p0 = hs.flat()
+    dp = tr.params().astype(np.float64) - p0
+    dr = rt.params().flat() - p0
+    assert rel_l2(dp, dr) <= 1e-2  # Adan's first step is ~lr*sign(g): tiny-g signs may flip
+
+
+def test_trainer_graph_replay_matches_eager(holo):
+    c, w, h, n, L = 3, 96, 64, 1500, 1
+    g = f32(S.init_gaussians(n, c, w, h, 42))
+    hs = holo.GaussianSet(n, c, **g)
+    target = holo.RealField(c, h, w, S.synthetic_image(42, c, h, w))
+    masks = S.build_masks(S.synthetic_depth(43, h, w), L, True)
+    dist = S.make_depth_planes(L, 3e-3, 2e-3)
+    a = holo.Trainer(hs, w, h, target, masks, dist, holo.PropagationSpec(), 50)
+    b = holo.Trainer(hs, w, h, target, masks, dist, holo.PropagationSpec(), 50)
+    b.use_graph(True)
+    la = [a.step() for _ in range(5)]
+    lb = [b.step() for _ in range(5)]
+    assert np.allclose(la, lb, rtol=0, atol=0)
+    assert np.array_equal(a.params(), b.params())
