@@ -135,11 +135,16 @@ __global__ void __launch_bounds__(kLossThreads) ssim_loss_kernel(LossArgs a, Win
             const float a2 = 2.f * s12 + C2;
             const float b1 = m1 * m1 + m2 * m2 + C1;
             const float b2 = s11 + s22 + C2;
-            const float s = (a1 * a2) / (b1 * b2);
+            // s/a1 and s/a2 are evaluated as a2/(b1 b2) and a1/(b1 b2): identical
+            // to ssim_channel's (s/a1), (s/a2) wherever those are defined, and
+            // finite when a2 rounds to 0 in fp32 (0/0 there would poison the
+            // whole field through the FFT).
+            const float inv = 1.f / (b1 * b2);
+            const float s = a1 * a2 * inv;
             if (vy >= y0 && vy < y0 + kTH && vx >= x0 && vx < x0 + kTW) ssum += s;
-            g1 = (s / a1) * 2.f * m2 - (s / b1) * 2.f * m1 + (s / b2) * 2.f * m1 - (s / a2) * 2.f * m2;
+            g1 = a2 * inv * 2.f * m2 - (s / b1) * 2.f * m1 + (s / b2) * 2.f * m1 - a1 * inv * 2.f * m2;
             g2 = -s / b2;
-            g3 = 2.f * s / a2;
+            g3 = 2.f * a1 * inv;
         }
         S.gm[0][i][j] = g1;
         S.gm[1][i][j] = g2;
@@ -251,7 +256,7 @@ __global__ void __launch_bounds__(kLossThreads) pixel_loss_kernel(LossArgs a, in
     }
 }
 
-__global__ void loss_finalize_kernel(const double* partials, int slots, int kind, double n_el,
+__global__ void __launch_bounds__(1024) loss_finalize_kernel(const double* partials, int slots, int kind, double n_el,
                                      int L_norm, double count, double* out) {
     using BR = cub::BlockReduce<double, 1024>;
     __shared__ typename BR::TempStorage tmp;

@@ -157,7 +157,7 @@ constexpr int kScanThreads = 512;
 constexpr int kScanItems = 8;
 constexpr int kScanTile = kScanThreads * kScanItems;
 
-__global__ void scan_reduce_kernel(const uint32_t* in, int n, uint64_t* blocksums) {
+__global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const uint32_t* in, int n, uint64_t* blocksums) {
     using BS = cub::BlockReduce<uint64_t, kScanThreads>;
     __shared__ typename BS::TempStorage tmp;
     const int base = blockIdx.x * kScanTile;
@@ -171,7 +171,7 @@ __global__ void scan_reduce_kernel(const uint32_t* in, int n, uint64_t* blocksum
 }
 
 // single block: exclusive scan of block sums in place, total -> *total
-__global__ void scan_blocksums_kernel(uint64_t* blocksums, int nb, uint32_t* status, int64_t cap) {
+__global__ void __launch_bounds__(1024) scan_blocksums_kernel(uint64_t* blocksums, int nb, uint32_t* status, int64_t cap) {
     __shared__ uint64_t carry;
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
@@ -194,7 +194,7 @@ __global__ void scan_blocksums_kernel(uint64_t* blocksums, int nb, uint32_t* sta
     }
 }
 
-__global__ void scan_apply_kernel(const uint32_t* in, int n, const uint64_t* blocksums,
+__global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const uint32_t* in, int n, const uint64_t* blocksums,
                                   uint32_t* out) {
     using BSc = cub::BlockScan<uint32_t, kScanThreads>;
     __shared__ typename BSc::TempStorage tmp;
@@ -234,7 +234,7 @@ constexpr int kSortItems = 16;  // per thread
 constexpr int kSortTile = kSortThreads * kSortItems;
 constexpr int kSortWarps = kSortThreads / 32;
 
-__global__ void radix_hist_kernel(const uint64_t* keys, const uint32_t* status, int shift,
+__global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(const uint64_t* keys, const uint32_t* status, int shift,
                                   int nblocks, uint32_t* hist) {
     __shared__ uint32_t h[256];
     h[threadIdx.x] = 0;
@@ -250,7 +250,7 @@ __global__ void radix_hist_kernel(const uint64_t* keys, const uint32_t* status, 
 }
 
 // Per digit: exclusive scan over blocks (in place) + digit total.
-__global__ void radix_scan_kernel(uint32_t* hist, int nblocks, uint32_t* dtot) {
+__global__ void __launch_bounds__(256) radix_scan_kernel(uint32_t* hist, int nblocks, uint32_t* dtot) {
     using BSc = cub::BlockScan<uint32_t, 256>;
     __shared__ typename BSc::TempStorage tmp;
     __shared__ uint32_t carry;
