@@ -25,34 +25,6 @@ namespace hs {
 
 namespace {
 
-__device__ __forceinline__ int wrapped(int k, int n) { return k < n - n / 2 ? k : k - n; }
-
-// H(kx, ky) for one (channel, plane); CONJ applies the adjoint.
-template <bool CONJ>
-__device__ __forceinline__ float2 transfer(const TfConst& t, int mx, int my) {
-    if (abs(mx) > t.mx_max || abs(my) > t.my_max) return make_float2(0.f, 0.f);
-    if (t.a4 > 0.0) {
-        const long long ax = 2LL * mx + 1, ay = 2LL * my + 1;
-        if (static_cast<double>(ax * ax + ay * ay) >= t.a4) return make_float2(0.f, 0.f);
-    }
-    const float fmx = static_cast<float>(mx), fmy = static_cast<float>(my);
-    const float q = t.bx * fmx * fmx + t.by * fmy * fmy;  // (2 pi f / k)^2
-    float ph = 0.f;
-    if (q < 1.f) ph = t.kd_mod - t.kd * q / (1.f + sqrtf(1.f - q));  // kz d = kd - kd q/(1+sqrt(1-q))
-    float s, c;
-    sincosf(ph, &s, &c);
-    return make_float2(c, CONJ ? -s : s);
-}
-
-struct RowArgs {
-    const float2* in;
-    float2* out;
-    int W, H, Px, ox, ntiles;
-    float scale;
-    fft::Plan plan;
-    const float2* tw;
-};
-
 // F1 / B1: one CTA per input row.  Row rho = pc * H + y of a stack of
 // C x H x W (or L x C x H x W) fields -> tiled output block pc.
 template <int CC>
@@ -98,14 +70,6 @@ __global__ void __launch_bounds__(256) rows_inv_kernel(RowArgs a) {
     }
 }
 
-struct ColArgs {
-    const float2* in;   // fwd: T1 [C][tiles][H][CC]; bwd: T3 [L][C][tiles][H][CC]
-    float2* out;        // fwd: T2 [L][C][tiles][H][CC]; bwd: T4 [C][tiles][H][CC]
-    int C, H, Py, Px, oy, ntiles, L;
-    fft::Plan plan;
-    const float2* tw;
-    const TfConst* tf;  // [L][C]
-};
 
 template <int CC>
 __device__ __forceinline__ void load_col_tile(float2* A, const float2* src, int H, int Py, int oy) {
@@ -284,7 +248,10 @@ void AsmWork::prepare(int C_, int H_, int W_, int pad_, int L_) {
     oy = (Py - H) / 2;
     const int nbuf = L_ > 1 ? 3 : 2;
     CC = 4;
-    while (CC > 1 && nbuf * static_cast<size_t>(fft::padded_len(Py * CC)) * sizeof(float2) > kSmemBudget)
+    use_static = static_plan_cc(Px, Py, std::max(L, L_), &CC);
+    if (!use_static) CC = 4;
+    while (!use_static && CC > 1 &&
+           nbuf * static_cast<size_t>(fft::padded_len(Py * CC)) * sizeof(float2) > kSmemBudget)
         CC /= 2;
     require(nbuf * static_cast<size_t>(fft::padded_len(Py * CC)) * sizeof(float2) <= kSmemBudget &&
                 2 * static_cast<size_t>(fft::padded_len(Px)) * sizeof(float2) <= kSmemBudget,
@@ -301,6 +268,7 @@ void AsmWork::prepare(int C_, int H_, int W_, int pad_, int L_) {
         case 2: set_smem_attrs<2>(*this); break;
         default: set_smem_attrs<1>(*this); break;
     }
+    if (use_static) static_prepare(*this);
     const size_t tiled = static_cast<size_t>(ntiles) * H * CC * sizeof(float2);
     T1.reserve(tiled * C);
     T2.reserve(tiled * C * std::max(L, L_));
@@ -396,6 +364,7 @@ static void launch_backward(AsmWork& w, const float2* d_grads, float2* d_out, cu
 }
 
 void asm_forward(AsmWork& w, const float2* d_in, float2* d_out, cudaStream_t st, cudaEvent_t* ev) {
+    if (w.use_static && static_forward(w, d_in, d_out, st, ev)) return;
     switch (w.CC) {
         case 4: launch_forward<4>(w, d_in, d_out, st, ev); break;
         case 2: launch_forward<2>(w, d_in, d_out, st, ev); break;
@@ -404,6 +373,7 @@ void asm_forward(AsmWork& w, const float2* d_in, float2* d_out, cudaStream_t st,
 }
 
 void asm_backward(AsmWork& w, const float2* d_grads, float2* d_out, cudaStream_t st, cudaEvent_t* ev) {
+    if (w.use_static && static_backward(w, d_grads, d_out, st, ev)) return;
     switch (w.CC) {
         case 4: launch_backward<4>(w, d_grads, d_out, st, ev); break;
         case 2: launch_backward<2>(w, d_grads, d_out, st, ev); break;

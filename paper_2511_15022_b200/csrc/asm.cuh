@@ -26,6 +26,10 @@ struct AsmWork {
     DevBuf tf;        // TfConst [L][C]
     std::vector<TfConst> tf_host;
     size_t smem_rows = 0, smem_cols = 0;
+    // compile-time planned path (asm_static.cu), when (Px, Py) has a plan
+    bool use_static = false;
+    const float2* stw_x = nullptr;  // stage twiddle tables of the static plans
+    const float2* stw_y = nullptr;
 
     void prepare(int C, int H, int W, int pad, int L);
     // phase/mask distances per plane (propagate: both = d; backward: phase -d).
@@ -44,5 +48,49 @@ void asm_backward(AsmWork& w, const float2* d_grads, float2* d_out, cudaStream_t
                   cudaEvent_t* ev = nullptr);
 
 fft::Plan make_plan(int n);
+
+// ---- shared device helpers (asm.cu generic kernels, asm_static.cu planned kernels) ----
+__device__ __forceinline__ int wrapped(int k, int n) { return k < n - n / 2 ? k : k - n; }
+
+// H(kx, ky) for one (channel, plane); CONJ applies the adjoint.
+template <bool CONJ>
+__device__ __forceinline__ float2 transfer(const TfConst& t, int mx, int my) {
+    if (abs(mx) > t.mx_max || abs(my) > t.my_max) return make_float2(0.f, 0.f);
+    if (t.a4 > 0.0) {
+        const long long ax = 2LL * mx + 1, ay = 2LL * my + 1;
+        if (static_cast<double>(ax * ax + ay * ay) >= t.a4) return make_float2(0.f, 0.f);
+    }
+    const float fmx = static_cast<float>(mx), fmy = static_cast<float>(my);
+    const float q = t.bx * fmx * fmx + t.by * fmy * fmy;  // (2 pi f / k)^2
+    float ph = 0.f;
+    if (q < 1.f) ph = t.kd_mod - t.kd * q / (1.f + sqrtf(1.f - q));  // kz d = kd - kd q/(1+sqrt(1-q))
+    float s, c;
+    sincosf(ph, &s, &c);
+    return make_float2(c, CONJ ? -s : s);
+}
+
+struct RowArgs {
+    const float2* in;
+    float2* out;
+    int W, H, Px, ox, ntiles;
+    float scale;
+    fft::Plan plan;
+    const float2* tw;
+};
+
+struct ColArgs {
+    const float2* in;   // fwd: T1 [C][tiles][H][CC]; bwd: T3 [L][C][tiles][H][CC]
+    float2* out;        // fwd: T2 [L][C][tiles][H][CC]; bwd: T4 [C][tiles][H][CC]
+    int C, H, Py, Px, oy, ntiles, L;
+    fft::Plan plan;
+    const float2* tw;
+    const TfConst* tf;  // [L][C]
+};
+
+// Static (compile-time planned) propagation path; false when (Px, Py) has no plan.
+bool static_plan_cc(int Px, int Py, int L, int* cc);
+bool static_forward(AsmWork& w, const float2* d_in, float2* d_out, cudaStream_t st, cudaEvent_t* ev);
+bool static_backward(AsmWork& w, const float2* d_grads, float2* d_out, cudaStream_t st, cudaEvent_t* ev);
+void static_prepare(AsmWork& w);
 
 }  // namespace hs

@@ -77,6 +77,8 @@ def kernel_launch_count() -> int:
 
 
 def _dev(device=None):
+    if not torch.cuda.is_available():
+        raise HoloError("holosplat-b200 needs a CUDA device (B200); no CPU fallback")
     return torch.device("cuda", torch.cuda.current_device() if device is None else device)
 
 

@@ -181,6 +181,23 @@ def test_propagate_multi_and_backward(holo, ref):
     assert rel_l2(np.stack([a.real, a.imag]), np.stack(b)) <= FIELD_TOL
 
 
+@pytest.mark.parametrize("c,h,w,L", [(1, 256, 256, 1), (3, 160, 256, 2), (1, 1080, 1920, 2)])
+def test_propagate_multi_static_plans(holo, ref, c, h, w, L):
+    """The compile-time planned kernels (cfg1, desk, cfg2 grids), single- and multi-plane."""
+    hsp, rsp = spec_for(holo, ref, c, 2)
+    dist = S.make_depth_planes(L, 3e-3, 2e-3)
+    re, im = field32(300 + h, c, h, w)
+    a = holo.propagate_multi(holo.ComplexField(c, h, w, re, im), hsp, dist)
+    bre, bim = ref.propagate_multi(re, im, rsp, dist)
+    for l in range(L):
+        assert rel_l2(np.stack([a[l].real, a[l].imag]), np.stack([bre[l], bim[l]])) <= FIELD_TOL
+    gre = np.stack([field32(400 + l, c, h, w)[0] for l in range(L)])
+    gim = np.stack([field32(500 + l, c, h, w)[1] for l in range(L)])
+    b = holo.propagate_multi_backward([holo.ComplexField(c, h, w, gre[l], gim[l]) for l in range(L)], hsp, dist)
+    r = ref.propagate_multi_backward(gre, gim, rsp, dist)
+    assert rel_l2(np.stack([b.real, b.imag]), np.stack(r)) <= FIELD_TOL
+
+
 def test_propagate_cfg2_grid(holo, ref):
     """Full cfg2 padded grid (2160 x 3840) for one channel vs the reference."""
     c, h, w = 1, 1080, 1920
