@@ -5,7 +5,7 @@
  * (proj/core/include/holo/{rasterizer,propagation,loss,optimizer}.hpp) and its
  * only product caller is the step loop proj/core/src/pipeline.cpp:253-297.
  * This header is the thin extern "C" layer underneath the C++ drop-in
- * (include/holo/*.hpp, libholo_b200.so) and the Python host mirror
+ * (include/holo/ headers, libholo_b200.so) and the Python host mirror
  * (paper_2511_15022_b200.holo).  Plain pointers and sizes only.
  *
  * Conventions

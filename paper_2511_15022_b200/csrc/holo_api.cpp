@@ -1,0 +1,574 @@
+// holosplat-b200 C++ drop-in (libholo_b200.so): the reference's holo:: API
+// (proj/core/include/holo/*.hpp) implemented over the C ABI of
+// libholosplat.so.  Host containers stay fp64 like the reference; values are
+// rounded to fp32 for the device, results are widened back.  The hot-path
+// calls (rasterizer, propagation, loss, Adan) always run on the B200 -- there
+// is no CPU fallback; the scalar helpers of field_core and the transfer
+// function sampler are host code, as in the reference.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "holo/complex_field.hpp"
+#include "holo/field_core.hpp"
+#include "holo/gaussian_set.hpp"
+#include "holo/loss.hpp"
+#include "holo/optimizer.hpp"
+#include "holo/parallel.hpp"
+#include "holo/propagation.hpp"
+#include "holo/rasterizer.hpp"
+#include "holosplat.h"
+
+namespace holo {
+
+namespace {
+
+void check(hs_status s) {
+    if (s == HS_OK) return;
+    const std::string msg = hs_last_error();
+    if (s == HS_EINVAL) throw std::invalid_argument(msg);
+    throw std::runtime_error(msg);
+}
+
+hs_ctx* ctx() {
+    static std::once_flag once;
+    static hs_ctx* c = nullptr;
+    std::call_once(once, [] {
+        const char* env = std::getenv("HOLO_B200_DEVICE");
+        check(hs_ctx_create(env ? std::atoi(env) : 0, &c));
+    });
+    return c;
+}
+
+// RAII device buffer over hs_device_alloc.
+struct Dev {
+    void* p = nullptr;
+    size_t bytes = 0;
+    explicit Dev(size_t b) : bytes(b) { check(hs_device_alloc(ctx(), std::max<size_t>(b, 4), &p)); }
+    ~Dev() {
+        if (p) hs_device_free(ctx(), p);
+    }
+    Dev(const Dev&) = delete;
+    Dev& operator=(const Dev&) = delete;
+    Dev(Dev&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; }
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+    void upload(const void* h, size_t b) { check(hs_copy_h2d(ctx(), p, h, b)); }
+    void download(void* h, size_t b) const { check(hs_copy_d2h(ctx(), h, p, b)); }
+};
+
+std::vector<float> flat_params(const GaussianSet& s) {
+    std::vector<float> f;
+    f.reserve(s.pre_position.size() + s.pre_scale.size() + s.rotation.size() + s.amplitude.size() +
+              s.phase.size() + s.pre_opacity.size());
+    for (const auto* v : {&s.pre_position, &s.pre_scale, &s.rotation, &s.amplitude, &s.phase, &s.pre_opacity})
+        for (double x : *v) f.push_back(static_cast<float>(x));
+    return f;
+}
+
+GaussianSet unflatten(const std::vector<float>& f, int n, int c) {
+    GaussianSet g(n, c);
+    size_t o = 0;
+    for (auto* v : {&g.pre_position, &g.pre_scale, &g.rotation, &g.amplitude, &g.phase, &g.pre_opacity})
+        for (double& x : *v) x = f[o++];
+    return g;
+}
+
+Dev upload_params(const GaussianSet& s) {
+    s.validate();
+    const std::vector<float> f = flat_params(s);
+    Dev d(f.size() * sizeof(float));
+    d.upload(f.data(), f.size() * sizeof(float));
+    return d;
+}
+
+// planar fp64 (re, im) -> interleaved complex64 on the device
+Dev upload_field(const std::vector<const ComplexField*>& fs) {
+    size_t n = 0;
+    for (auto* f : fs) n += f->size();
+    std::vector<float> h(2 * n);
+    size_t o = 0;
+    for (auto* f : fs)
+        for (size_t i = 0; i < f->size(); ++i, ++o) {
+            h[2 * o] = static_cast<float>(f->real[i]);
+            h[2 * o + 1] = static_cast<float>(f->imag[i]);
+        }
+    Dev d(h.size() * sizeof(float));
+    d.upload(h.data(), h.size() * sizeof(float));
+    return d;
+}
+
+void download_field(const Dev& d, size_t offset_elems, ComplexField& f) {
+    std::vector<float> h(2 * f.size());
+    check(hs_copy_d2h(ctx(), h.data(), static_cast<float*>(d.p) + 2 * offset_elems, h.size() * sizeof(float)));
+    for (size_t i = 0; i < f.size(); ++i) {
+        f.real[i] = h[2 * i];
+        f.imag[i] = h[2 * i + 1];
+    }
+}
+
+struct SpecHolder {
+    hs_prop_spec s{};
+    std::vector<double> wl;
+    explicit SpecHolder(const PropagationSpec& p) : wl(p.wavelengths) {
+        s.wavelengths = wl.data();
+        s.n_wavelengths = static_cast<int>(wl.size());
+        s.pixel_pitch = p.pixel_pitch;
+        s.pad_factor = p.pad_factor;
+        s.aperture_radius = p.aperture_radius;
+    }
+};
+
+}  // namespace
+
+// ---- gaussian_set (gaussian_set.cpp:9-57) -----------------------------------------------------
+GaussianSet::GaussianSet(int n, int c) : count(n), channels(c) {
+    if (n < 0 || c <= 0) throw std::invalid_argument("GaussianSet: invalid N or C");
+    const size_t N = static_cast<size_t>(n);
+    pre_position.assign(2 * N, 0.0);
+    pre_scale.assign(2 * N, 0.0);
+    rotation.assign(N, 0.0);
+    amplitude.assign(N * c, 0.0);
+    phase.assign(N * c, 0.0);
+    pre_opacity.assign(N, 0.0);
+}
+
+void GaussianSet::validate() const {
+    if (count < 0 || channels <= 0) throw std::invalid_argument("GaussianSet: invalid N or C");
+    const size_t n = static_cast<size_t>(count);
+    const struct {
+        const std::vector<double>* v;
+        size_t want;
+        const char* name;
+    } groups[] = {{&pre_position, 2 * n, "pre_position"}, {&pre_scale, 2 * n, "pre_scale"},
+                  {&rotation, n, "rotation"},           {&amplitude, n * channels, "amplitude"},
+                  {&phase, n * channels, "phase"},      {&pre_opacity, n, "pre_opacity"}};
+    for (const auto& g : groups) {
+        if (g.v->size() != g.want) throw std::invalid_argument(std::string("GaussianSet: bad size for ") + g.name);
+        for (double x : *g.v)
+            if (!std::isfinite(x))
+                throw std::invalid_argument(std::string("GaussianSet: non-finite entry in ") + g.name);
+    }
+}
+
+GaussianSet GaussianSet::concat(const GaussianSet& a, const GaussianSet& b) {
+    if (a.channels != b.channels) throw std::invalid_argument("GaussianSet::concat: channel mismatch");
+    GaussianSet out(a.count + b.count, a.channels);
+    auto join = [](std::vector<double>& d, const std::vector<double>& x, const std::vector<double>& y) {
+        std::copy(x.begin(), x.end(), d.begin());
+        std::copy(y.begin(), y.end(), d.begin() + x.size());
+    };
+    join(out.pre_position, a.pre_position, b.pre_position);
+    join(out.pre_scale, a.pre_scale, b.pre_scale);
+    join(out.rotation, a.rotation, b.rotation);
+    join(out.amplitude, a.amplitude, b.amplitude);
+    join(out.phase, a.phase, b.phase);
+    join(out.pre_opacity, a.pre_opacity, b.pre_opacity);
+    return out;
+}
+
+// ---- field_core (field_core.cpp:11-93), host scalar math ------------------------------------------
+double activate_position(double pre, double extent) {
+    if (!std::isfinite(pre)) throw std::invalid_argument("activate_position: non-finite input");
+    return (std::tanh(pre) + 1.0) * 0.5 * extent;
+}
+double activate_position_deriv(double pre, double extent) {
+    const double t = std::tanh(pre);
+    return 0.5 * extent * (1.0 - t * t);
+}
+double activate_scale(double pre) {
+    if (!std::isfinite(pre)) throw std::invalid_argument("activate_scale: non-finite input");
+    return std::exp(pre) + kEpsScale;
+}
+double activate_scale_deriv(double pre) { return std::exp(pre); }
+double activate_opacity(double pre) {
+    if (!std::isfinite(pre)) throw std::invalid_argument("activate_opacity: non-finite input");
+    return 1.0 / (1.0 + std::exp(-pre));
+}
+double activate_opacity_deriv(double pre) {
+    const double s = activate_opacity(pre);
+    return s * (1.0 - s);
+}
+double activate_amplitude(double raw) { return std::min(std::max(raw, 0.0), 1.0); }
+double activate_amplitude_deriv(double raw) { return (raw >= 0.0 && raw <= 1.0) ? 1.0 : 0.0; }
+double unactivate_position(double value, double extent) { return std::atanh(2.0 * value / extent - 1.0); }
+
+Covariance2 covariance(double sx, double sy, double theta) {
+    const double c = std::cos(theta), s = std::sin(theta), a = sx * sx, b = sy * sy;
+    return Covariance2{a * c * c + b * s * s + kEpsCov, (a - b) * c * s, a * s * s + b * c * c + kEpsCov};
+}
+
+CovarianceInverse invert_covariance(const Covariance2& cv) {
+    const double det = cv.sxx * cv.syy - cv.sxy * cv.sxy;
+    const double d = std::max(det, kEpsDet);
+    CovarianceInverse o;
+    o.inv = InverseCovariance2{cv.syy / d, -cv.sxy / d, cv.sxx / d};
+    const double mid = 0.5 * (cv.sxx + cv.syy), half = 0.5 * (cv.sxx - cv.syy);
+    const double lmax = mid + std::sqrt(std::max(half * half + cv.sxy * cv.sxy, 0.0));
+    o.radius = 3.0 * std::sqrt(std::max(lmax, 0.0));
+    return o;
+}
+
+ActivatedGaussian activate(const GaussianSet& set, int n, int width, int height) {
+    if (n < 0 || n >= set.count) throw std::out_of_range("activate: primitive index");
+    ActivatedGaussian g;
+    g.position[0] = activate_position(set.pre_position[2 * n], width);
+    g.position[1] = activate_position(set.pre_position[2 * n + 1], height);
+    g.scale[0] = activate_scale(set.pre_scale[2 * n]);
+    g.scale[1] = activate_scale(set.pre_scale[2 * n + 1]);
+    g.rotation = set.rotation[n];
+    g.opacity = activate_opacity(set.pre_opacity[n]);
+    for (int c = 0; c < set.channels; ++c) {
+        const size_t i = static_cast<size_t>(n) * set.channels + c;
+        g.amplitude.push_back(activate_amplitude(set.amplitude[i]));
+        g.phase.push_back(set.phase[i]);
+    }
+    return g;
+}
+
+RealField intensity_of(const ComplexField& u) {
+    RealField out(u.channels, u.height, u.width);
+    Dev f = upload_field({&u});
+    Dev o(u.size() * sizeof(float));
+    check(hs_intensity(ctx(), f.as<float>(), static_cast<int64_t>(u.size()), o.as<float>()));
+    std::vector<float> h(u.size());
+    o.download(h.data(), h.size() * sizeof(float));
+    std::copy(h.begin(), h.end(), out.values.begin());
+    return out;
+}
+
+// ---- rasterizer ---------------------------------------------------------------------------------------
+TileIndex build_tile_index(const GaussianSet& set, int width, int height) {
+    if (width <= 0 || height <= 0) throw std::invalid_argument("build_tile_index: empty canvas");
+    Dev p = upload_params(set);
+    int64_t k = 0;
+    int txy[2] = {0, 0};
+    check(hs_build_tile_index(ctx(), p.as<float>(), set.count, set.channels, width, height, nullptr, nullptr,
+                              nullptr, -1, &k, txy));
+    TileIndex idx;
+    idx.tiles_x = txy[0];
+    idx.tiles_y = txy[1];
+    const size_t tiles = static_cast<size_t>(txy[0]) * txy[1];
+    Dev dt(std::max<int64_t>(k, 1) * 4), di(std::max<int64_t>(k, 1) * 4), dr(tiles * 16);
+    check(hs_build_tile_index(ctx(), p.as<float>(), set.count, set.channels, width, height, dt.as<uint32_t>(),
+                              di.as<uint32_t>(), dr.as<uint64_t>(), k, &k, txy));
+    std::vector<uint32_t> t(k), id(k);
+    std::vector<uint64_t> r(2 * tiles);
+    if (k) {
+        dt.download(t.data(), k * 4);
+        di.download(id.data(), k * 4);
+    }
+    dr.download(r.data(), r.size() * 8);
+    idx.pairs.resize(k);
+    for (int64_t i = 0; i < k; ++i) idx.pairs[i] = {t[i], id[i]};
+    idx.ranges.resize(tiles);
+    for (size_t i = 0; i < tiles; ++i) idx.ranges[i] = {static_cast<size_t>(r[2 * i]), static_cast<size_t>(r[2 * i + 1])};
+    return idx;
+}
+
+ComplexField rasterize_forward(const GaussianSet& set, int width, int height) {
+    if (width <= 0 || height <= 0) throw std::invalid_argument("rasterize_forward: empty canvas");
+    ComplexField out(set.channels, height, width);
+    if (set.count == 0) return out;
+    Dev p = upload_params(set);
+    Dev f(out.size() * 2 * sizeof(float));
+    check(hs_rasterize_forward(ctx(), p.as<float>(), set.count, set.channels, width, height, f.as<float>()));
+    download_field(f, 0, out);
+    return out;
+}
+
+GaussianSetGrads rasterize_backward(const GaussianSet& set, const RealField& grad_real,
+                                    const RealField& grad_imag) {
+    if (!grad_real.same_shape(grad_imag) || grad_real.channels != set.channels)
+        throw std::invalid_argument("rasterize_backward: gradient shape mismatch");
+    if (set.count == 0) return GaussianSetGrads(0, set.channels);
+    ComplexField g(grad_real.channels, grad_real.height, grad_real.width);
+    g.real = grad_real.values;
+    g.imag = grad_imag.values;
+    Dev p = upload_params(set);
+    Dev gf = upload_field({&g});
+    const size_t np = p.bytes / sizeof(float);
+    Dev out(np * sizeof(float));
+    check(hs_rasterize_backward(ctx(), p.as<float>(), set.count, set.channels, grad_real.width, grad_real.height,
+                                gf.as<float>(), out.as<float>()));
+    std::vector<float> h(np);
+    out.download(h.data(), np * sizeof(float));
+    return unflatten(h, set.count, set.channels);
+}
+
+// ---- propagation ----------------------------------------------------------------------------------------
+std::vector<TransferFunctionSample> transfer_function(const PropagationSpec& spec, double distance, int channel,
+                                                      int padded_nx, int padded_ny) {
+    // propagation.cpp:105-126 / :208-223 on the host (test-facing sampler)
+    if (padded_nx <= 0 || padded_ny <= 0) throw std::invalid_argument("transfer_function: non-positive dims");
+    if (channel < 0 || channel >= static_cast<int>(spec.wavelengths.size()))
+        throw std::invalid_argument("propagation: channel has no wavelength");
+    const double lambda = spec.wavelengths[channel];
+    if (lambda <= 0.0 || spec.pixel_pitch <= 0.0)
+        throw std::invalid_argument("propagation: non-positive wavelength or pitch");
+    const double two_pi = 6.283185307179586476925286766559;
+    const double k = two_pi / lambda, lx = padded_nx * spec.pixel_pitch, ly = padded_ny * spec.pixel_pitch;
+    const double fx_max = 1.0 / (lambda * std::sqrt((2.0 * distance / lx) * (2.0 * distance / lx) + 1.0));
+    const double fy_max = 1.0 / (lambda * std::sqrt((2.0 * distance / ly) * (2.0 * distance / ly) + 1.0));
+    std::vector<TransferFunctionSample> grid(static_cast<size_t>(padded_nx) * padded_ny);
+    for (int iy = 0; iy < padded_ny; ++iy)
+        for (int ix = 0; ix < padded_nx; ++ix) {
+            auto& s = grid[static_cast<size_t>(iy) * padded_nx + ix];
+            s.fx = (ix - padded_nx / 2) * (1.0 / lx);
+            s.fy = (iy - padded_ny / 2) * (1.0 / ly);
+            const double kz2 = k * k - two_pi * two_pi * (s.fx * s.fx + s.fy * s.fy);
+            s.kz = kz2 > 0.0 ? std::sqrt(kz2) : 0.0;
+            s.inside_bandlimit = std::abs(s.fx) < fx_max && std::abs(s.fy) < fy_max;
+        }
+    return grid;
+}
+
+static ComplexField propagate_mode(const ComplexField& field, const PropagationSpec& spec, int mode, double d,
+                                   double md) {
+    SpecHolder sh(spec);
+    if (field.channels != sh.s.n_wavelengths)
+        throw std::invalid_argument("propagation: channel count does not match wavelengths");
+    Dev in = upload_field({&field});
+    Dev out(in.bytes);
+    check(hs_propagate(ctx(), &sh.s, mode, d, md, in.as<float>(), field.channels, field.height, field.width,
+                       out.as<float>()));
+    ComplexField o(field.channels, field.height, field.width);
+    download_field(out, 0, o);
+    return o;
+}
+
+ComplexField propagate(const ComplexField& field, const PropagationSpec& spec, double distance) {
+    return propagate_mode(field, spec, 0, distance, distance);
+}
+ComplexField propagate_with_mask_distance(const ComplexField& field, const PropagationSpec& spec, double distance,
+                                          double mask_distance) {
+    return propagate_mode(field, spec, 1, distance, mask_distance);
+}
+ComplexField propagate_backward(const ComplexField& grad_out, const PropagationSpec& spec, double distance) {
+    return propagate_mode(grad_out, spec, 2, distance, distance);
+}
+
+std::vector<ComplexField> propagate_multi(const ComplexField& field, const PropagationSpec& spec,
+                                          const std::vector<double>& distances) {
+    SpecHolder sh(spec);
+    const int L = static_cast<int>(distances.size());
+    Dev in = upload_field({&field});
+    Dev out(in.bytes * std::max(L, 1));
+    check(hs_propagate_multi(ctx(), &sh.s, distances.data(), L, in.as<float>(), field.channels, field.height,
+                             field.width, out.as<float>()));
+    std::vector<ComplexField> o(distances.size(), ComplexField(field.channels, field.height, field.width));
+    for (int l = 0; l < L; ++l) download_field(out, static_cast<size_t>(l) * field.size(), o[l]);
+    return o;
+}
+
+ComplexField propagate_multi_backward(const std::vector<ComplexField>& grads, const PropagationSpec& spec,
+                                      const std::vector<double>& distances) {
+    if (grads.empty() || grads.size() != distances.size())
+        throw std::invalid_argument("propagate_multi_backward: plane count mismatch");
+    std::vector<const ComplexField*> ptrs;
+    for (const auto& g : grads) {
+        if (!g.same_shape(grads[0])) throw std::invalid_argument("propagate_multi_backward: gradient shape mismatch");
+        ptrs.push_back(&g);
+    }
+    SpecHolder sh(spec);
+    Dev in = upload_field(ptrs);
+    Dev out(grads[0].size() * 2 * sizeof(float));
+    check(hs_propagate_multi_backward(ctx(), &sh.s, distances.data(), static_cast<int>(distances.size()),
+                                      in.as<float>(), grads[0].channels, grads[0].height, grads[0].width,
+                                      out.as<float>()));
+    ComplexField o(grads[0].channels, grads[0].height, grads[0].width);
+    download_field(out, 0, o);
+    return o;
+}
+
+// ---- loss ---------------------------------------------------------------------------------------------------
+DepthPlaneSet make_depth_planes(int count, double center_distance, double spacing) {
+    if (count < 1) throw std::invalid_argument("make_depth_planes: count must be >= 1");
+    DepthPlaneSet p{count, center_distance, spacing, {}};
+    for (int l = 0; l < count; ++l) p.distances.push_back(center_distance + (l - (count - 1) * 0.5) * spacing);
+    return p;
+}
+
+MaskStack build_masks(const RealField& depth, int plane_count, bool near_is_high) {
+    if (plane_count < 1) throw std::invalid_argument("build_masks: plane count must be >= 1");
+    const size_t n = static_cast<size_t>(depth.height) * depth.width;
+    if (depth.channels != 1 || depth.values.size() != n)
+        throw std::invalid_argument("build_masks: depth must be a single plane");
+    std::vector<uint8_t> flat(n * plane_count);
+    check(hs_build_masks(depth.values.data(), depth.height, depth.width, plane_count, near_is_high ? 1 : 0,
+                         flat.data()));
+    MaskStack m(plane_count);
+    for (int l = 0; l < plane_count; ++l) m[l].assign(flat.begin() + l * n, flat.begin() + (l + 1) * n);
+    return m;
+}
+
+TargetStack make_target_stack(const RealField& intensity, const RealField& depth, int plane_count,
+                              bool near_is_high) {
+    if (depth.height != intensity.height || depth.width != intensity.width)
+        throw std::invalid_argument("make_target_stack: depth/intensity size mismatch");
+    return TargetStack{intensity, depth, build_masks(depth, plane_count, near_is_high)};
+}
+
+static double run_loss(int kind, const std::vector<RealField>& recon, const TargetStack& target,
+                       std::vector<RealField>* grads) {
+    if (recon.empty()) throw std::invalid_argument("loss: no reconstruction planes");
+    if (recon.size() != target.masks.size()) throw std::invalid_argument("loss: plane count does not match masks");
+    for (const auto& r : recon)
+        if (!r.same_shape(target.intensity)) throw std::invalid_argument("loss: reconstruction shape mismatch");
+    const int L = static_cast<int>(recon.size());
+    const RealField& t = target.intensity;
+    const size_t n = t.values.size(), hw = static_cast<size_t>(t.height) * t.width;
+    std::vector<float> hr(n * L), ht(n);
+    for (int l = 0; l < L; ++l)
+        for (size_t i = 0; i < n; ++i) hr[l * n + i] = static_cast<float>(recon[l].values[i]);
+    for (size_t i = 0; i < n; ++i) ht[i] = static_cast<float>(t.values[i]);
+    std::vector<uint8_t> hm(hw * L);
+    for (int l = 0; l < L; ++l) std::copy(target.masks[l].begin(), target.masks[l].end(), hm.begin() + l * hw);
+    Dev dr(hr.size() * 4), dt(ht.size() * 4), dm(hm.size()), dg(hr.size() * 4);
+    dr.upload(hr.data(), hr.size() * 4);
+    dt.upload(ht.data(), ht.size() * 4);
+    dm.upload(hm.data(), hm.size());
+    double v = 0.0;
+    check(hs_loss(ctx(), kind, L, t.channels, t.height, t.width, dr.as<float>(), dt.as<float>(), dm.as<uint8_t>(),
+                  grads ? dg.as<float>() : nullptr, &v));
+    if (grads) {
+        std::vector<float> hg(hr.size());
+        dg.download(hg.data(), hg.size() * 4);
+        grads->assign(L, RealField(t.channels, t.height, t.width));
+        for (int l = 0; l < L; ++l)
+            for (size_t i = 0; i < n; ++i) (*grads)[l].values[i] = hg[l * n + i];
+    }
+    return v;
+}
+
+double loss_mse(const std::vector<RealField>& r, const TargetStack& t) { return run_loss(3, r, t, nullptr); }
+double loss_recon(const std::vector<RealField>& r, const TargetStack& t) { return run_loss(1, r, t, nullptr); }
+double loss_ssim(const std::vector<RealField>& r, const TargetStack& t) { return run_loss(2, r, t, nullptr); }
+double training_loss(const std::vector<RealField>& r, const TargetStack& t) { return run_loss(0, r, t, nullptr); }
+double loss_mse_grad(const std::vector<RealField>& r, const TargetStack& t, std::vector<RealField>& g) {
+    return run_loss(3, r, t, &g);
+}
+double loss_recon_grad(const std::vector<RealField>& r, const TargetStack& t, std::vector<RealField>& g) {
+    return run_loss(1, r, t, &g);
+}
+double loss_ssim_grad(const std::vector<RealField>& r, const TargetStack& t, std::vector<RealField>& g) {
+    return run_loss(2, r, t, &g);
+}
+double training_loss_grad(const std::vector<RealField>& r, const TargetStack& t, std::vector<RealField>& g) {
+    return run_loss(0, r, t, &g);
+}
+
+double plane_recon_loss(const RealField& recon, const TargetStack& target, size_t plane, RealField* grad) {
+    // loss.cpp:400-423: the single-plane recon term (w = 2/n)
+    if (!recon.same_shape(target.intensity)) throw std::invalid_argument("plane_recon_loss: shape mismatch");
+    if (plane >= target.masks.size()) throw std::invalid_argument("plane_recon_loss: plane out of range");
+    TargetStack one{target.intensity, target.depth, MaskStack{target.masks[plane]}};
+    std::vector<RealField> g;
+    const double v = run_loss(1, {recon}, one, grad ? &g : nullptr);
+    if (grad) *grad = g[0];
+    return v;
+}
+
+double ssim_value(const RealField& a, const RealField& b) {
+    // loss.cpp:425-438 = 1 - loss_ssim of one plane
+    if (!a.same_shape(b)) throw std::invalid_argument("ssim_value: shape mismatch");
+    TargetStack t{b, RealField(1, b.height, b.width), MaskStack(1, std::vector<uint8_t>(
+                                                                  static_cast<size_t>(b.height) * b.width, 0))};
+    return 1.0 - run_loss(2, {a}, t, nullptr);
+}
+
+// ---- optimizer -------------------------------------------------------------------------------------------------
+double cosine_lr(int step, int total_steps, double lr_max, double lr_min) {
+    double v = 0.0;
+    check(hs_cosine_lr(step, total_steps, lr_max, lr_min, &v));
+    return v;
+}
+
+struct Adan::Impl {
+    struct Group {
+        std::string name;
+        double lr = 0.0;
+        int t = 0;
+        size_t size = 0;
+        void* state = nullptr;  // 4 * size floats on the device
+    };
+    std::vector<Group> groups;
+    ~Impl() {
+        for (auto& g : groups)
+            if (g.state) hs_device_free(ctx(), g.state);
+    }
+    Group& find(const std::string& n) {
+        for (auto& g : groups)
+            if (g.name == n) return g;
+        throw std::invalid_argument("Adan: unknown group " + n);
+    }
+};
+
+Adan::Adan(AdanConfig cfg) : cfg_(cfg), impl_(std::make_unique<Impl>()) {}
+Adan::~Adan() = default;
+Adan::Adan(Adan&&) noexcept = default;
+Adan& Adan::operator=(Adan&&) noexcept = default;
+
+void Adan::add_group(const std::string& name, size_t size, double lr) {
+    for (const auto& g : impl_->groups)
+        if (g.name == name) throw std::invalid_argument("Adan: duplicate group " + name);
+    Impl::Group g;
+    g.name = name;
+    g.lr = lr;
+    g.size = size;
+    check(hs_device_alloc(ctx(), std::max<size_t>(4 * size, 1) * sizeof(float), &g.state));
+    std::vector<float> zeros(4 * size, 0.f);
+    if (size) check(hs_copy_h2d(ctx(), g.state, zeros.data(), zeros.size() * sizeof(float)));
+    impl_->groups.push_back(std::move(g));
+}
+void Adan::set_lr(const std::string& name, double lr) { impl_->find(name).lr = lr; }
+double Adan::lr(const std::string& name) const { return impl_->find(name).lr; }
+int Adan::step_count(const std::string& name) const { return impl_->find(name).t; }
+
+void Adan::step(const std::string& name, std::span<double> params, std::span<const double> grads) {
+    Impl::Group& g = impl_->find(name);
+    if (params.size() != g.size || grads.size() != g.size)
+        throw std::invalid_argument("Adan: size mismatch for group " + name);
+    std::vector<float> p(params.begin(), params.end()), gr(grads.begin(), grads.end());
+    Dev dp(p.size() * 4), dg(gr.size() * 4);
+    dp.upload(p.data(), p.size() * 4);
+    dg.upload(gr.data(), gr.size() * 4);
+    hs_adan_config c{cfg_.beta1, cfg_.beta2, cfg_.beta3, cfg_.eps};
+    check(hs_adan_step(ctx(), &c, name.c_str(), dp.as<float>(), dg.as<float>(), static_cast<float*>(g.state),
+                       static_cast<int64_t>(g.size), g.t + 1, g.lr));
+    g.t += 1;
+    dp.download(p.data(), p.size() * 4);
+    std::copy(p.begin(), p.end(), params.begin());
+}
+
+// ---- parallel (parallel.cpp:11-44) ---------------------------------------------------------------------------------
+namespace {
+int g_threads = 0;
+}
+void set_thread_count(int n) { g_threads = n < 0 ? 0 : n; }
+int thread_count() {
+    int n = g_threads;
+    if (n == 0) n = std::max(1u, std::thread::hardware_concurrency());
+    return n;
+}
+void parallel_for(int64_t begin, int64_t end, const std::function<void(int64_t, int64_t)>& fn) {
+    const int64_t count = end - begin;
+    if (count <= 0) return;
+    const int workers = static_cast<int>(std::min<int64_t>(thread_count(), count));
+    const int64_t chunk = (count + workers - 1) / workers;
+    std::vector<std::thread> pool;
+    for (int w = 1; w < workers; ++w) {
+        const int64_t lo = begin + w * chunk, hi = std::min(end, lo + chunk);
+        if (lo < hi) pool.emplace_back(fn, lo, hi);
+    }
+    fn(begin, std::min(end, begin + chunk));
+    for (auto& t : pool) t.join();
+}
+
+}  // namespace holo
