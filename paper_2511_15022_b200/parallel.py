@@ -1,0 +1,72 @@
+"""Multi-GPU partitioning of the hot path.
+
+* Plane sharding (cfg3): the forward spectrum is shared per channel, every
+  plane's inverse, loss and adjoint are independent, and the backward is a sum
+  over planes (propagation.cpp:231-237) that the rasterizer backward is linear
+  in.  Rank r owns a contiguous block of planes; the raster forward and the
+  forward row/column FFT are replicated; each rank produces the parameter
+  gradient of its planes with the global normalisers (L_total, SSIM count),
+  one NCCL all-reduce (sum) of the (6+2C)N gradient buffer makes them the full
+  gradient, and every rank applies the identical Adan update.
+* Scene replicas (cfg2 at N>1, cfg5): independent problems, no collective.
+
+The collective is torch.distributed over NCCL (gloo on CPU for the tests).
+"""
+from __future__ import annotations
+
+import math
+from typing import Tuple
+
+import torch
+import torch.distributed as dist
+
+
+def plane_shard(L: int, rank: int, world: int) -> Tuple[int, int]:
+    """Contiguous, balanced block [begin, end) of the L planes for `rank`."""
+    if L < 1 or world < 1 or not 0 <= rank < world:
+        raise ValueError("plane_shard: bad arguments")
+    base, extra = divmod(L, world)
+    begin = rank * base + min(rank, extra)
+    return begin, begin + base + (1 if rank < extra else 0)
+
+
+def combine_loss(recon_sum: float, ssim_sum: float, C: int, H: int, W: int, L: int,
+                 ssim_weight: float = 0.005) -> float:
+    """training_loss from the all-reduced partial sums (loss.cpp:317-398)."""
+    n = C * H * W
+    count = L * C * (H - 10) * (W - 10)
+    return recon_sum / (n * L) + ssim_weight * (1.0 - ssim_sum / count)
+
+
+class ShardedStep:
+    """One optimisation step of a plane-sharded trainer.
+
+    `trainer` needs forward_backward(), grads_tensor(), apply_update(),
+    loss_partials() -- holo.Trainer built with plane_range=plane_shard(...).
+    """
+
+    def __init__(self, trainer, C, H, W, L_total, group=None):
+        self.tr = trainer
+        self.C, self.H, self.W, self.L = C, H, W, L_total
+        self.group = group
+
+    def step(self) -> float:
+        self.tr.forward_backward()
+        g = self.tr.grads_tensor()
+        if dist.is_initialized() and dist.get_world_size(self.group) > 1:
+            if g.is_cuda:
+                torch.cuda.current_stream().synchronize()
+            dist.all_reduce(g, op=dist.ReduceOp.SUM, group=self.group)
+        self.tr.apply_update()
+        parts = torch.tensor(self.tr.loss_partials(), dtype=torch.float64,
+                             device=g.device if g.is_cuda else "cpu")
+        if dist.is_initialized() and dist.get_world_size(self.group) > 1:
+            dist.all_reduce(parts, op=dist.ReduceOp.SUM, group=self.group)
+        return combine_loss(float(parts[0]), float(parts[1]), self.C, self.H, self.W, self.L)
+
+
+def amdahl_plane_speedup(L: int, world: int) -> float:
+    """Ideal speed-up of plane sharding in the byte model B = C(13+12L)A:
+    13A per channel is replicated, 12A per plane is split."""
+    per_rank_planes = math.ceil(L / world)
+    return (13 + 12 * L) / (13 + 12 * per_rank_planes)

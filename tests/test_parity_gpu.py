@@ -290,3 +290,28 @@ def test_trainer_graph_replay_matches_eager(holo):
     lb = [b.step() for _ in range(5)]
     assert np.allclose(la, lb, rtol=0, atol=0)
     assert np.array_equal(a.params(), b.params())
+
+
+def test_plane_sharded_trainers_sum_to_full_step(holo):
+    """Two trainers owning planes [0,2) and [2,4) (hs_trainer_config.plane_begin/end)
+    produce gradients and loss partials that sum to the unsharded step's."""
+    from paper_2511_15022_b200 import parallel as P
+    c, w, h, n, L = 3, 96, 64, 1500, 4
+    g = f32(S.init_gaussians(n, c, w, h, 42))
+    hs = holo.GaussianSet(n, c, **g)
+    target = holo.RealField(c, h, w, S.synthetic_image(42, c, h, w))
+    masks = S.build_masks(S.synthetic_depth(43, h, w), L, True)
+    dist = S.make_depth_planes(L, 3e-3, 4e-3 / 7)
+    spec = holo.PropagationSpec()
+    full = holo.Trainer(hs, w, h, target, masks, dist, spec, 10)
+    full.forward_backward()
+    gfull = full.grads_tensor().cpu().numpy().astype(np.float64)
+    pf = full.loss_partials()
+    gs, parts = 0.0, np.zeros(2)
+    for r in range(2):
+        t = holo.Trainer(hs, w, h, target, masks, dist, spec, 10, plane_range=P.plane_shard(L, r, 2))
+        t.forward_backward()
+        gs = gs + t.grads_tensor().cpu().numpy().astype(np.float64)
+        parts += np.array(t.loss_partials())
+    assert rel_l2(gs, gfull) < 1e-5
+    assert parts[0] == pytest.approx(pf[0], rel=1e-6) and parts[1] == pytest.approx(pf[1], rel=1e-6)

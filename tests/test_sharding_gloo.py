@@ -1,0 +1,120 @@
+"""CPU, world_size 2 over gloo: plane sharding of the optimisation step.
+
+1. The math: per-shard gradients (oracle restatement, global normalisers)
+   summed with a gloo all-reduce equal the unsharded step's gradients, and the
+   combined loss equals the full loss.
+2. The orchestration (paper_2511_15022_b200.parallel.ShardedStep) all-reduces
+   the gradient buffer between forward_backward and apply_update.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import holo_oracle as O
+from paper_2511_15022_b200 import parallel as P
+from paper_2511_15022_b200 import synthetic as S
+
+N, C, W, H, L = 40, 3, 32, 24, 4
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def scene():
+    g = S.init_gaussians(N, C, W, H, 42)
+    g = {k: np.asarray(v, np.float32).astype(np.float64) for k, v in g.items()}
+    target = S.synthetic_image(42, C, H, W)
+    masks = S.build_masks(S.synthetic_depth(43, H, W), L, True)
+    dist_ = S.make_depth_planes(L, 3e-3, 4e-3 / 7)
+    return g, target, masks, dist_
+
+
+def _worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g, target, masks, d = scene()
+    b, e = P.plane_shard(L, rank, world)
+    r = O.step_grads(g, N, C, W, H, target, masks, d, S.WAVELENGTHS[C], planes=range(b, e), L_norm=L)
+    flat = torch.from_numpy(np.concatenate([r["grads"][k] for k in O.GROUPS]))
+    dist.all_reduce(flat)
+    parts = torch.tensor([r["recon_sum"], r["ssim_sum"]], dtype=torch.float64)
+    dist.all_reduce(parts)
+    if rank == 0:
+        np.save(out + "_grads.npy", flat.numpy())
+        np.save(out + "_parts.npy", parts.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_plane_shard_partitions():
+    for L_ in range(1, 17):
+        for world in range(1, 9):
+            seen = []
+            for r in range(world):
+                b, e = P.plane_shard(L_, r, world)
+                assert 0 <= b <= e <= L_
+                seen += list(range(b, e))
+            assert seen == list(range(L_))
+    assert P.amdahl_plane_speedup(8, 8) == pytest.approx(109 / 25)
+
+
+def test_sharded_step_equals_full_step_gloo(tmp_path):
+    out = str(tmp_path / "r")
+    mp.spawn(_worker, args=(2, free_port(), out), nprocs=2, join=True)
+    grads = np.load(out + "_grads.npy")
+    parts = np.load(out + "_parts.npy")
+    g, target, masks, d = scene()
+    full = O.step_grads(g, N, C, W, H, target, masks, d, S.WAVELENGTHS[C])
+    ref = np.concatenate([full["grads"][k] for k in O.GROUPS])
+    assert np.linalg.norm(grads - ref) / np.linalg.norm(ref) < 1e-12
+    loss = P.combine_loss(parts[0], parts[1], C, H, W, L)
+    full_loss = P.combine_loss(full["recon_sum"], full["ssim_sum"], C, H, W, L)
+    assert loss == pytest.approx(full_loss, rel=1e-12)
+
+
+class FakeTrainer:
+    """Stands in for holo.Trainer on CPU: gradient = (rank+1) * ones."""
+
+    def __init__(self, rank, n):
+        self.rank, self.g, self.applied = rank, torch.zeros(n), None
+
+    def forward_backward(self):
+        self.g.fill_(self.rank + 1.0)
+
+    def grads_tensor(self):
+        return self.g
+
+    def apply_update(self):
+        self.applied = self.g.clone()
+
+    def loss_partials(self):
+        return (10.0 * (self.rank + 1), 1.0)
+
+
+def _orchestration_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    tr = FakeTrainer(rank, 16)
+    loss = P.ShardedStep(tr, 1, 16, 16, 2).step()
+    np.save(f"{out}_{rank}.npy", np.concatenate([tr.applied.numpy(), [loss]]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_step_orchestration_gloo(tmp_path):
+    out = str(tmp_path / "o")
+    mp.spawn(_orchestration_worker, args=(2, free_port(), out), nprocs=2, join=True)
+    a, b = np.load(out + "_0.npy"), np.load(out + "_1.npy")
+    assert np.array_equal(a, b)                 # identical update on every rank
+    assert np.all(a[:16] == 3.0)                # 1 + 2: the summed gradient reached Adan
+    assert a[16] == pytest.approx(P.combine_loss(30.0, 2.0, 1, 16, 16, 2))
