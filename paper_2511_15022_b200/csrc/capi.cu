@@ -40,7 +40,7 @@ const char* kGroupNames[6] = {"position", "scale", "rotation", "amplitude", "pha
 struct CtxWork {
     RasterWork rw;
     AsmWork aw;
-    DevBuf flags, partials, out3;
+    DevBuf flags, partials, out3, tstats;
 };
 
 }  // namespace
@@ -70,8 +70,8 @@ struct hs_trainer {
     std::vector<double> wavelengths;
     hs_prop_spec spec{};
     int64_t P = 0;
-    DevBuf params, grads, state, field, planes, dplanes, back, target, masks, partials, out3, flags,
-        step;
+    DevBuf params, grads, state, field, planes, dplanes, back, target, tstats, masks, partials, out3,
+        flags, step;
     RasterWork rw;
     AsmWork aw;
     AdanGroups groups{};
@@ -316,8 +316,13 @@ extern "C" hs_status hs_loss(hs_ctx* ctx, int kind, int L, int c, int h, int w, 
         const int slots = loss_partial_slots(kind, L, c, h, w);
         cw.partials.reserve(sizeof(double) * 2 * std::max(slots, 1));
         cw.out3.reserve(sizeof(double) * 3);
-        LossArgs a{kind, L, L, 0, c, h, w, d_recon, nullptr, d_target, d_masks, d_grads, nullptr,
-                   cw.partials.as<double>()};
+        cw.tstats.reserve(sizeof(float2) * ssim_target_stats_elems(c, h, w));
+        if (kind == kLossTraining || kind == kLossSsim) {
+            require(h >= 11 && w >= 11, "ssim: image smaller than the 11x11 window");
+            ssim_target_stats(d_target, c, h, w, cw.tstats.as<float2>(), ctx->stream);
+        }
+        LossArgs a{kind, L, L, 0, c, h, w, d_recon, nullptr, d_target, cw.tstats.as<float2>(), d_masks, d_grads,
+                   nullptr, cw.partials.as<double>()};
         const int used = loss_launch(a, ctx->stream);
         loss_finalize(a, used, cw.out3.as<double>(), ctx->stream);
         double out[3];
@@ -387,8 +392,8 @@ static void trainer_enqueue_fwd_bwd(hs_trainer* t, cudaStream_t st) {
     mark(2);
     asm_forward(t->aw, t->field.as<float2>(), t->planes.as<float2>(), st, prof ? t->ev + 3 : nullptr);
     LossArgs a{kLossTraining, t->L, t->L_total, t->plane0, t->c, t->h, t->w, nullptr, t->planes.as<float2>(),
-               t->target.as<float>(), t->masks.as<uint8_t>(), nullptr, t->dplanes.as<float2>(),
-               t->partials.as<double>()};
+               t->target.as<float>(), t->tstats.as<float2>(), t->masks.as<uint8_t>(), nullptr,
+               t->dplanes.as<float2>(), t->partials.as<double>()};
     const int used = loss_launch(a, st);
     loss_finalize(a, used, t->out3.as<double>(), st);
     mark(6);
@@ -469,6 +474,9 @@ hs_status hs_trainer_create(hs_ctx* ctx, const hs_trainer_config* cfg, hs_traine
         t->masks.reserve(hw * t->L_total);
         HS_CUDA(cudaMemcpyAsync(t->target.p, cfg->h_target, sizeof(float) * chw, cudaMemcpyHostToDevice, st));
         HS_CUDA(cudaMemcpyAsync(t->masks.p, cfg->h_masks, hw * t->L_total, cudaMemcpyHostToDevice, st));
+        require(t->h >= 11 && t->w >= 11, "ssim: image smaller than the 11x11 window");
+        t->tstats.reserve(sizeof(float2) * ssim_target_stats_elems(t->c, t->h, t->w));
+        ssim_target_stats(t->target.as<float>(), t->c, t->h, t->w, t->tstats.as<float2>(), st);
         t->loss_slots = loss_partial_slots(kLossTraining, t->L, t->c, t->h, t->w);
         t->partials.reserve(sizeof(double) * 2 * t->loss_slots);
         t->out3.reserve(sizeof(double) * 3);

@@ -47,13 +47,6 @@ Win ssim_window_f32() {  // loss.cpp:89-100
     return w;
 }
 
-struct SsimSmem {
-    float I[kRH][kRW];
-    float T[kRH][kRW];
-    float h[5][kRH][kVW];   // horizontal means of I, T, I^2, T^2, I*T; reused for spreads
-    float gm[3][kVH][kVW];  // g1, g2, g3 on the valid grid
-};
-
 template <bool FROM_FIELD>
 __device__ __forceinline__ float load_I(const LossArgs& a, size_t idx) {
     if (FROM_FIELD) {
@@ -63,16 +56,58 @@ __device__ __forceinline__ float load_I(const LossArgs& a, size_t idx) {
     return a.recon[idx];
 }
 
+// Target window statistics on the valid grid, per channel: (mu2, sigma2^2) =
+// (E_w[t], E_w[t^2] - E_w[t]^2) -- constant over an optimisation run, so the
+// trainer computes them once (ssim_channel :173-176, :190).
+__global__ void ssim_target_stats_kernel(const float* __restrict__ target, int C, int H, int W, Win win,
+                                         float2* __restrict__ out) {
+    const int vh = H - kWin + 1, vw = W - kWin + 1;
+    const int64_t total = static_cast<int64_t>(C) * vh * vw;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int c = static_cast<int>(i / (static_cast<int64_t>(vh) * vw));
+        const int rem = static_cast<int>(i - static_cast<int64_t>(c) * vh * vw);
+        const int vy = rem / vw, vx = rem - vy * vw;
+        const float* t = target + static_cast<size_t>(c) * H * W;
+        float m = 0.f, e = 0.f;
+        for (int yy = 0; yy < kWin; ++yy) {
+            float rm = 0.f, re = 0.f;
+            for (int xx = 0; xx < kWin; ++xx) {
+                const float v = t[static_cast<size_t>(vy + yy) * W + vx + xx];
+                rm = fmaf(win.g[xx], v, rm);
+                re = fmaf(win.g[xx], v * v, re);
+            }
+            m = fmaf(win.g[yy], rm, m);
+            e = fmaf(win.g[yy], re, e);
+        }
+        out[i] = make_float2(m, e - m * m);
+    }
+}
+
+struct SsimSmem {
+    float I[kRH][kRW];        // I over tile + halo
+    float T[kRH][kRW];        // target over tile + halo
+    float h[3][kRH][kVW];     // corr_x of I, I^2, I*t; reused for the vertical spreads
+    float gm[3][kVH][kVW];    // g1, g2, g3 on the valid grid
+};
+
+// Work split of the 256 threads (register-blocked separable correlations):
+constexpr int kHB = 11;  // corr_x: 36 rows x 7 runs of 11 outputs      = 252 items
+constexpr int kVB = 9;   // corr_y: 74 cols x 3 runs of 9 valid rows    = 222 items
+constexpr int kSX = 4;   // spread_x: 16 rows x 16 runs of 4 outputs    = 256 items
+
 template <bool FROM_FIELD>
-__global__ void __launch_bounds__(kLossThreads) ssim_loss_kernel(LossArgs a, Win win) {
+__global__ void __launch_bounds__(kLossThreads, 2) ssim_loss_kernel(LossArgs a, Win win) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SsimSmem& S = *reinterpret_cast<SsimSmem*>(smem_raw);
     const int plane = blockIdx.z;  // l * C + c
     const int l = plane / a.C, c = plane - l * a.C;
     const int x0 = blockIdx.x * kTW, y0 = blockIdx.y * kTH;
     const int H = a.H, W = a.W;
+    const int vh = H - kWin + 1, vw = W - kWin + 1;
     const size_t plane_off = static_cast<size_t>(plane) * H * W;
     const float* tgt = a.target + static_cast<size_t>(c) * H * W;
+    const float2* tst = a.tstats + static_cast<size_t>(c) * vh * vw;
     const uint8_t* mask = a.masks + static_cast<size_t>(a.plane0 + l) * H * W;
     const int tid = threadIdx.x;
 
@@ -89,118 +124,146 @@ __global__ void __launch_bounds__(kLossThreads) ssim_loss_kernel(LossArgs a, Win
         S.T[ry][rx] = tv;
     }
     __syncthreads();
-    // corr_x over the five maps
-    for (int e = tid; e < kRH * kVW; e += kLossThreads) {
-        const int ry = e / kVW, j = e - ry * kVW;
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f, s4 = 0.f;
+    // corr_x (loss.cpp:103-111) of I, I^2, I*t: each item a run of kHB outputs
+    if (tid < kRH * 7) {
+        const int ry = tid / 7, j0 = (tid - ry * 7) * kHB;
+        float in_i[kHB + kWin - 1], in_t[kHB + kWin - 1];
 #pragma unroll
-        for (int k = 0; k < kWin; ++k) {
-            const float g = win.g[k];
-            const float iv = S.I[ry][j + k], tv = S.T[ry][j + k];
-            s0 = fmaf(g, iv, s0);
-            s1 = fmaf(g, tv, s1);
-            s2 = fmaf(g, iv * iv, s2);
-            s3 = fmaf(g, tv * tv, s3);
-            s4 = fmaf(g, iv * tv, s4);
+        for (int q = 0; q < kHB + kWin - 1; ++q) {
+            const int j = min(j0 + q, kRW - 1);
+            in_i[q] = S.I[ry][j];
+            in_t[q] = S.T[ry][j];
         }
-        S.h[0][ry][j] = s0;
-        S.h[1][ry][j] = s1;
-        S.h[2][ry][j] = s2;
-        S.h[3][ry][j] = s3;
-        S.h[4][ry][j] = s4;
+#pragma unroll
+        for (int o = 0; o < kHB; ++o) {
+            float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+#pragma unroll
+            for (int k = 0; k < kWin; ++k) {
+                const float g = win.g[k], iv = in_i[o + k], tv = in_t[o + k];
+                s0 = fmaf(g, iv, s0);
+                s1 = fmaf(g, iv * iv, s1);
+                s2 = fmaf(g, iv * tv, s2);
+            }
+            if (j0 + o < kVW) {
+                S.h[0][ry][j0 + o] = s0;
+                S.h[1][ry][j0 + o] = s1;
+                S.h[2][ry][j0 + o] = s2;
+            }
+        }
     }
     __syncthreads();
     // corr_y + SSIM map + derivative maps (ssim_channel :187-205)
     double ssum = 0.0;
     const float C1 = static_cast<float>(kSsimC1), C2 = static_cast<float>(kSsimC2);
-    for (int e = tid; e < kVH * kVW; e += kLossThreads) {
-        const int i = e / kVW, j = e - i * kVW;
-        const int vy = y0 - kHalo + i, vx = x0 - kHalo + j;
-        float g1 = 0.f, g2 = 0.f, g3 = 0.f;
-        if (vy >= 0 && vy <= H - kWin && vx >= 0 && vx <= W - kWin) {
-            float m1 = 0.f, m2 = 0.f, exx = 0.f, eyy = 0.f, exy = 0.f;
+    if (tid < kVW * 3) {
+        const int j = tid % kVW, i0 = (tid / kVW) * kVB;
+        const int vx = x0 - kHalo + j;
+        float col0[kVB + kWin - 1], col1[kVB + kWin - 1], col2[kVB + kWin - 1];
 #pragma unroll
-            for (int k = 0; k < kWin; ++k) {
-                const float g = win.g[k];
-                m1 = fmaf(g, S.h[0][i + k][j], m1);
-                m2 = fmaf(g, S.h[1][i + k][j], m2);
-                exx = fmaf(g, S.h[2][i + k][j], exx);
-                eyy = fmaf(g, S.h[3][i + k][j], eyy);
-                exy = fmaf(g, S.h[4][i + k][j], exy);
-            }
-            const float s12 = exy - m1 * m2;
-            const float s11 = exx - m1 * m1;
-            const float s22 = eyy - m2 * m2;
-            const float a1 = 2.f * m1 * m2 + C1;
-            const float a2 = 2.f * s12 + C2;
-            const float b1 = m1 * m1 + m2 * m2 + C1;
-            const float b2 = s11 + s22 + C2;
-            // s/a1 and s/a2 are evaluated as a2/(b1 b2) and a1/(b1 b2): identical
-            // to ssim_channel's (s/a1), (s/a2) wherever those are defined, and
-            // finite when a2 rounds to 0 in fp32 (0/0 there would poison the
-            // whole field through the FFT).
-            const float inv = 1.f / (b1 * b2);
-            const float s = a1 * a2 * inv;
-            if (vy >= y0 && vy < y0 + kTH && vx >= x0 && vx < x0 + kTW) ssum += s;
-            g1 = a2 * inv * 2.f * m2 - (s / b1) * 2.f * m1 + (s / b2) * 2.f * m1 - a1 * inv * 2.f * m2;
-            g2 = -s / b2;
-            g3 = 2.f * a1 * inv;
+        for (int q = 0; q < kVB + kWin - 1; ++q) {
+            const int i = min(i0 + q, kRH - 1);
+            col0[q] = S.h[0][i][j];
+            col1[q] = S.h[1][i][j];
+            col2[q] = S.h[2][i][j];
         }
-        S.gm[0][i][j] = g1;
-        S.gm[1][i][j] = g2;
-        S.gm[2][i][j] = g3;
+#pragma unroll
+        for (int o = 0; o < kVB; ++o) {
+            const int i = i0 + o;
+            if (i >= kVH) break;
+            const int vy = y0 - kHalo + i;
+            float g1 = 0.f, g2 = 0.f, g3 = 0.f;
+            if (vy >= 0 && vy < vh && vx >= 0 && vx < vw) {
+                float m1 = 0.f, exx = 0.f, exy = 0.f;
+#pragma unroll
+                for (int k = 0; k < kWin; ++k) {
+                    const float g = win.g[k];
+                    m1 = fmaf(g, col0[o + k], m1);
+                    exx = fmaf(g, col1[o + k], exx);
+                    exy = fmaf(g, col2[o + k], exy);
+                }
+                const float2 ts = tst[static_cast<size_t>(vy) * vw + vx];
+                const float m2 = ts.x;
+                const float s12 = exy - m1 * m2;
+                const float s11 = exx - m1 * m1;
+                const float a1 = 2.f * m1 * m2 + C1;
+                const float a2 = 2.f * s12 + C2;
+                const float b1 = m1 * m1 + m2 * m2 + C1;
+                const float b2 = s11 + ts.y + C2;
+                // s/a1, s/a2 evaluated as a2/(b1 b2), a1/(b1 b2): equal where
+                // ssim_channel's form is defined and finite when a2 rounds to
+                // 0 in fp32 (a 0/0 there would poison the field via the FFT).
+                const float inv = 1.f / (b1 * b2);
+                const float s = a1 * a2 * inv;
+                if (vy >= y0 && vy < y0 + kTH && vx >= x0 && vx < x0 + kTW) ssum += s;
+                g1 = a2 * inv * 2.f * m2 - (s / b1) * 2.f * m1 + (s / b2) * 2.f * m1 - a1 * inv * 2.f * m2;
+                g2 = -s / b2;
+                g3 = 2.f * a1 * inv;
+            }
+            S.gm[0][i][j] = g1;
+            S.gm[1][i][j] = g2;
+            S.gm[2][i][j] = g3;
+        }
     }
     __syncthreads();
-    // spread_t vertical (:138-145): sv[y][vx] = sum_i g[i] gm[y - i][vx]
+    // spread_t vertical (:138-145): sv[y][vx] = sum_k g[k] gm[y - k][vx]; item = (col, map)
     float(*sv)[kVW] = reinterpret_cast<float(*)[kVW]>(&S.h[0][0][0]);  // 3 x kTH x kVW
-    for (int e = tid; e < kTH * kVW; e += kLossThreads) {
-        const int oy = e / kVW, j = e - oy * kVW;
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+    if (tid < kVW * 3) {
+        const int j = tid % kVW, m = tid / kVW;
+        float col[kVH];
 #pragma unroll
-        for (int k = 0; k < kWin; ++k) {
-            const float g = win.g[k];
-            s0 = fmaf(g, S.gm[0][oy + kHalo - k][j], s0);
-            s1 = fmaf(g, S.gm[1][oy + kHalo - k][j], s1);
-            s2 = fmaf(g, S.gm[2][oy + kHalo - k][j], s2);
+        for (int q = 0; q < kVH; ++q) col[q] = S.gm[m][q][j];
+#pragma unroll
+        for (int oy = 0; oy < kTH; ++oy) {
+            float acc = 0.f;
+#pragma unroll
+            for (int k = 0; k < kWin; ++k) acc = fmaf(win.g[k], col[oy + kHalo - k], acc);
+            sv[m * kTH + oy][j] = acc;
         }
-        sv[oy][j] = s0;
-        sv[kTH + oy][j] = s1;
-        sv[2 * kTH + oy][j] = s2;
     }
     __syncthreads();
     // spread_t horizontal (:146-151) + combine (:211) + recon term + output
     const int kind = a.kind;
     const double n_el = static_cast<double>(a.C) * H * W;
     const float wr = static_cast<float>(2.0 / (n_el * a.L_norm));
-    const double count = static_cast<double>(a.L_norm) * a.C * (H - kWin + 1) * (W - kWin + 1);
+    const double count = static_cast<double>(a.L_norm) * a.C * vh * vw;
     const float ws = static_cast<float>((kind == kLossTraining ? kSsimWeight : 1.0) * (-1.0 / count));
     double rsum = 0.0;
-    for (int e = tid; e < kTH * kTW; e += kLossThreads) {
-        const int oy = e / kTW, ox = e - oy * kTW;
-        const int y = y0 + oy, x = x0 + ox;
-        if (y >= H || x >= W) continue;
-        float o0 = 0.f, o1 = 0.f, o2 = 0.f;
+    {
+        const int oy = tid / (kTW / kSX), ox0 = (tid - oy * (kTW / kSX)) * kSX;
+        float o[3][kSX];
 #pragma unroll
-        for (int k = 0; k < kWin; ++k) {
-            const float g = win.g[k];
-            o0 = fmaf(g, sv[oy][ox + kHalo - k], o0);
-            o1 = fmaf(g, sv[kTH + oy][ox + kHalo - k], o1);
-            o2 = fmaf(g, sv[2 * kTH + oy][ox + kHalo - k], o2);
+        for (int m = 0; m < 3; ++m) {
+            float row[kSX + kWin - 1];
+#pragma unroll
+            for (int q = 0; q < kSX + kWin - 1; ++q) row[q] = sv[m * kTH + oy][ox0 + q];
+#pragma unroll
+            for (int u = 0; u < kSX; ++u) {
+                float acc = 0.f;
+#pragma unroll
+                for (int k = 0; k < kWin; ++k) acc = fmaf(win.g[k], row[u + kHalo - k], acc);
+                o[m][u] = acc;
+            }
         }
-        const float iv = S.I[oy + kHalo][ox + kHalo], tv = S.T[oy + kHalo][ox + kHalo];
-        const float gs = o0 + 2.f * iv * o1 + tv * o2;
-        const size_t p = static_cast<size_t>(y) * W + x;
-        float g = ws * gs;
-        if (kind == kLossTraining) {
-            const float d = iv - tv;
-            const float k = 1.f + (mask[p] ? 1.f : 0.f) + tv * tv;
-            rsum += static_cast<double>(d * d * k);
-            g = fmaf(wr * d, k, g);
-        }
-        if (a.grad) a.grad[plane_off + p] = g;
-        if (a.du) {
-            const float2 u = a.field[plane_off + p];
-            a.du[plane_off + p] = make_float2(2.f * u.x * g, 2.f * u.y * g);
+        const int y = y0 + oy;
+#pragma unroll
+        for (int u = 0; u < kSX; ++u) {
+            const int x = x0 + ox0 + u;
+            if (y >= H || x >= W) continue;
+            const float iv = S.I[oy + kHalo][ox0 + u + kHalo], tv = S.T[oy + kHalo][ox0 + u + kHalo];
+            const float gs = o[0][u] + 2.f * iv * o[1][u] + tv * o[2][u];
+            const size_t p = static_cast<size_t>(y) * W + x;
+            float g = ws * gs;
+            if (kind == kLossTraining) {
+                const float d = iv - tv;
+                const float k = 1.f + (mask[p] ? 1.f : 0.f) + tv * tv;
+                rsum += static_cast<double>(d * d * k);
+                g = fmaf(wr * d, k, g);
+            }
+            if (a.grad) a.grad[plane_off + p] = g;
+            if (a.du) {
+                const float2 uu = a.field[plane_off + p];
+                a.du[plane_off + p] = make_float2(2.f * uu.x * g, 2.f * uu.y * g);
+            }
         }
     }
     using BR = cub::BlockReduce<double, kLossThreads>;
@@ -402,6 +465,7 @@ int loss_launch(const LossArgs& a, cudaStream_t st) {
         const dim3 grid(ceil_div(a.W, kTW), ceil_div(a.H, kTH), a.L * a.C);
         const size_t smem = sizeof(SsimSmem);
         static const Win win = ssim_window_f32();
+        require(a.tstats != nullptr, "ssim: target statistics missing");
         if (a.field) {
             HS_CUDA(cudaFuncSetAttribute(ssim_loss_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem)));
@@ -428,6 +492,14 @@ void loss_finalize(const LossArgs& a, int slots, double* d_out3, cudaStream_t st
                          std::max(a.W - kWin + 1, 0);
     loss_finalize_kernel<<<1, 1024, 0, st>>>(a.partials, slots, a.kind, n_el, a.L_norm, count, d_out3);
     launch_check("loss_finalize");
+}
+
+void ssim_target_stats(const float* target, int C, int H, int W, float2* out, cudaStream_t st) {
+    if (H < kWin || W < kWin) return;
+    static const Win win = ssim_window_f32();
+    const int64_t total = static_cast<int64_t>(C) * (H - kWin + 1) * (W - kWin + 1);
+    ssim_target_stats_kernel<<<grid_for(total, 256), 256, 0, st>>>(target, C, H, W, win, out);
+    launch_check("ssim_target_stats");
 }
 
 void intensity_launch(const float2* f, int64_t count, float* out, cudaStream_t st) {

@@ -16,6 +16,7 @@ struct LossArgs {
     const float* recon;      // L x C x H x W intensities (or nullptr when from_field)
     const float2* field;     // L x C x H x W complex fields (I = |U|^2), or nullptr
     const float* target;     // C x H x W
+    const float2* tstats;    // C x (H-10) x (W-10) target window stats (ssim_target_stats)
     const uint8_t* masks;    // L_norm x H x W
     float* grad;             // dL/dI (L x C x H x W), or nullptr
     float2* du;              // dL/dU = 2 U dL/dI (L x C x H x W), or nullptr
@@ -29,6 +30,11 @@ int loss_partial_slots(int kind, int L, int C, int H, int W);
 void loss_finalize(const LossArgs& a, int slots, double* d_out3, cudaStream_t st);
 
 void intensity_launch(const float2* f, int64_t count, float* out, cudaStream_t st);
+// (mu2, sigma2^2) of the target on the valid 11x11 grid, per channel.
+void ssim_target_stats(const float* target, int C, int H, int W, float2* out, cudaStream_t st);
+inline size_t ssim_target_stats_elems(int C, int H, int W) {
+    return (H < 11 || W < 11) ? 1 : static_cast<size_t>(C) * (H - 10) * (W - 10);
+}
 
 // Fused Adan over the six groups of the parameter buffer (optimizer.cpp:99-123).
 struct AdanGroups {

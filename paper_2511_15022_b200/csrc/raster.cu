@@ -483,9 +483,8 @@ constexpr int kBwdThreads = 256;
 template <int C>
 __global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(
     int N, const float4* __restrict__ rec, const float4* __restrict__ shade,
-    const double* __restrict__ p64, const int4* __restrict__ pbox, const float* __restrict__ params,
-    int W, int H, const float2* __restrict__ gfield, float* __restrict__ grads,
-    uint32_t* __restrict__ flags) {
+    const double* __restrict__ p64, const int4* __restrict__ pbox, int W, int H,
+    const float2* __restrict__ gfield, float* __restrict__ raw) {
     const int lane = threadIdx.x & 31;
     const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (g >= N) return;
@@ -584,21 +583,50 @@ __global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(
             }
         }
     }
+    // Transpose reduction: 16 shuffles fold the 7 + 2C partial sums (padded
+    // to 16); afterwards lanes 2k, 2k+1 hold the warp total of value k.
+    float v[16];
 #pragma unroll
     for (int c = 0; c < C; ++c) {
-        d_amp[c] = warp_sum(d_amp[c]);
-        d_phase[c] = warp_sum(d_phase[c]);
+        v[c] = d_amp[c];
+        v[C + c] = d_phase[c];
     }
-    d_alpha = warp_sum(d_alpha);
-    gmx = warp_sum(gmx);
-    gmy = warp_sum(gmy);
-    ga = warp_sum(ga);
-    gb = warp_sum(gb);
-    gc = warp_sum(gc);
-    if (lane != 0) return;
+    v[2 * C + 0] = d_alpha;
+    v[2 * C + 1] = gmx;
+    v[2 * C + 2] = gmy;
+    v[2 * C + 3] = ga;
+    v[2 * C + 4] = gb;
+    v[2 * C + 5] = gc;
+#pragma unroll
+    for (int i = 2 * C + 6; i < 16; ++i) v[i] = 0.f;
+#pragma unroll
+    for (int half = 8; half >= 1; half >>= 1) {
+        const bool hi = (lane & (2 * half)) != 0;
+#pragma unroll
+        for (int i = 0; i < half; ++i) {
+            const float send = hi ? v[i] : v[i + half];
+            const float keep = hi ? v[i + half] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2 * half);
+        }
+    }
+    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+    const int k = lane >> 1;
+    if ((lane & 1) == 0 && k < 2 * C + 6) raw[static_cast<size_t>(k) * N + g] = v[0];
+}
 
-    // fp64 chain rule (rasterizer.cpp:251-282)
+// Chain rule of rasterize_backward (rasterizer.cpp:251-282) in fp64, one
+// thread per Gaussian, from the warp-reduced raw sums [d_amp[C], d_phase[C],
+// d_alpha, gmx, gmy, ga, gb, gc] (SoA, N each).
+template <int C>
+__global__ void __launch_bounds__(256) raster_finalize_kernel(int N, const float* __restrict__ raw,
+                                                               const float* __restrict__ params, int W, int H,
+                                                               float* __restrict__ grads, uint32_t* flags) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= N) return;
     const size_t Ns = N;
+    auto R = [&](int k) { return static_cast<double>(raw[static_cast<size_t>(k) * Ns + g]); };
+    const double d_alpha = R(2 * C), gmx = R(2 * C + 1), gmy = R(2 * C + 2);
+    const double ga = R(2 * C + 3), gb = R(2 * C + 4), gc = R(2 * C + 5);
     const float* pp = params;
     const float* ps = pp + 2 * Ns;
     const float* rot = ps + 2 * Ns;
@@ -621,9 +649,9 @@ __global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(
 #pragma unroll
     for (int c = 0; c < C; ++c) {
         const size_t i = static_cast<size_t>(g) * C + c;
-        const float raw = amp[i];
-        put(gamp + i, (raw >= 0.f && raw <= 1.f) ? static_cast<double>(d_amp[c]) : 0.0, 3);
-        put(gpha + i, d_phase[c], 4);
+        const float rawp = amp[i];
+        put(gamp + i, (rawp >= 0.f && rawp <= 1.f) ? R(c) : 0.0, 3);
+        put(gpha + i, R(C + c), 4);
     }
     const double po = opa[g];
     const double sig = 1.0 / (1.0 + exp(-po));
@@ -682,6 +710,7 @@ void RasterWork::prepare(int n_, int c_, int w_, int h_) {
     pbox.reserve(N * sizeof(int4));
     tbox.reserve(N * sizeof(int4));
     counts.reserve(N * sizeof(uint32_t));
+    raw.reserve(N * (2 * c + 6) * sizeof(float));
     offsets.reserve(N * sizeof(uint32_t));
     blocksums.reserve((N / kScanTile + 2) * sizeof(uint64_t));
     ranges.reserve(static_cast<size_t>(tiles_x) * tiles_y * sizeof(uint2));
@@ -775,8 +804,11 @@ static void bwd_launch(const RasterWork& rw, const float* d_params, const float2
     const int warps_per_block = kBwdThreads / 32;
     raster_bwd_kernel<C><<<ceil_div(rw.n, warps_per_block), kBwdThreads, 0, st>>>(
         rw.n, rw.rec.as<float4>(), rw.shade.as<float4>(), rw.p64.as<double>(), rw.pbox.as<int4>(),
-        d_params, rw.width, rw.height, d_gf, d_grads, d_flags);
+        rw.width, rw.height, d_gf, rw.raw.as<float>());
     launch_check("raster_bwd");
+    raster_finalize_kernel<C><<<ceil_div(rw.n, 256), 256, 0, st>>>(rw.n, rw.raw.as<float>(), d_params, rw.width,
+                                                                   rw.height, d_grads, d_flags);
+    launch_check("raster_finalize");
 }
 
 void raster_backward(const RasterWork& rw, const float* d_params, const float2* d_grad_field,

@@ -17,6 +17,7 @@ struct RasterWork {
     DevBuf pbox;     // int4 pixel bbox (x0,x1,y0,y1) clamped to the canvas
     DevBuf tbox;     // int4 tile bbox
     DevBuf counts;   // uint32 tiles per Gaussian
+    DevBuf raw;      // backward partial sums, (7+2C) x N floats (SoA)
     DevBuf offsets;  // uint32 exclusive scan of counts
     DevBuf blocksums;
     DevBuf keys[2];  // uint64 (tile << 32 | id), ping-pong for the radix sort
