@@ -34,8 +34,16 @@ __device__ __forceinline__ float2 transfer_fast(const TfConst& t, int mx, int my
     }
     const float fmx = static_cast<float>(mx), fmy = static_cast<float>(my);
     const float q = t.bx * fmx * fmx + t.by * fmy * fmy;
+    // kz d = kd - kd * q / (1 + sqrt(1 - q)); for q < 1/32 the series
+    // q/2 + q^2/8 + q^3/16 + 5q^4/128 + 7q^5/256 (truncation < 1e-9 rad here)
+    // replaces the sqrt and the division.
     float ph = 0.f;
-    if (q < 1.f) ph = t.kd_mod - t.kd * q / (1.f + sqrtf(1.f - q));
+    if (q < 0.03125f) {
+        const float ser = q * fmaf(q, fmaf(q, fmaf(q, fmaf(q, 0.02734375f, 0.0390625f), 0.0625f), 0.125f), 0.5f);
+        ph = fmaf(-t.kd, ser, t.kd_mod);
+    } else if (q < 1.f) {
+        ph = t.kd_mod - t.kd * q / (1.f + sqrtf(1.f - q));
+    }
     const float n = rintf(ph * 0.15915494309189535f);
     ph = fmaf(-n, 6.28318548202514648f, ph);      // 2pi rounded to fp32
     ph = fmaf(n, 1.7484555314695172e-7f, ph);     // + (fp32(2pi) - 2pi)

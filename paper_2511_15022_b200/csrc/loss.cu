@@ -89,6 +89,7 @@ struct SsimSmem {
     float T[kRH][kRW];        // target over tile + halo
     float h[3][kRH][kVW];     // corr_x of I, I^2, I*t; reused for the vertical spreads
     float gm[3][kVH][kVW];    // g1, g2, g3 on the valid grid
+    float2 ts[kVH][kVW];      // target window stats (mu2, sigma2^2) on the valid grid
 };
 
 // Work split of the 256 threads (register-blocked separable correlations):
@@ -111,17 +112,46 @@ __global__ void __launch_bounds__(kLossThreads, 2) ssim_loss_kernel(LossArgs a, 
     const uint8_t* mask = a.masks + static_cast<size_t>(a.plane0 + l) * H * W;
     const int tid = threadIdx.x;
 
-    for (int e = tid; e < kRH * kRW; e += kLossThreads) {
-        const int ry = e / kRW, rx = e - ry * kRW;
-        const int y = y0 - kHalo + ry, x = x0 - kHalo + rx;
-        float iv = 0.f, tv = 0.f;
-        if (y >= 0 && y < H && x >= 0 && x < W) {
-            const size_t p = static_cast<size_t>(y) * W + x;
-            iv = load_I<FROM_FIELD>(a, plane_off + p);
-            tv = tgt[p];
+    {  // all global loads of this thread in flight at once, then the smem stores
+        constexpr int kLoads = (kRH * kRW + kLossThreads - 1) / kLossThreads;
+        float iv[kLoads], tv[kLoads];
+#pragma unroll
+        for (int q = 0; q < kLoads; ++q) {
+            const int e = tid + q * kLossThreads;
+            const int ry = e / kRW, rx = e - ry * kRW;
+            const int y = y0 - kHalo + ry, x = x0 - kHalo + rx;
+            iv[q] = 0.f;
+            tv[q] = 0.f;
+            if (e < kRH * kRW && y >= 0 && y < H && x >= 0 && x < W) {
+                const size_t p = static_cast<size_t>(y) * W + x;
+                iv[q] = load_I<FROM_FIELD>(a, plane_off + p);
+                tv[q] = tgt[p];
+            }
         }
-        S.I[ry][rx] = iv;
-        S.T[ry][rx] = tv;
+        constexpr int kTs = (kVH * kVW + kLossThreads - 1) / kLossThreads;
+        float2 tsv[kTs];
+#pragma unroll
+        for (int q = 0; q < kTs; ++q) {
+            const int e = tid + q * kLossThreads;
+            const int i = e / kVW, j = e - i * kVW;
+            const int vy = y0 - kHalo + i, vx = x0 - kHalo + j;
+            tsv[q] = (e < kVH * kVW && vy >= 0 && vy < vh && vx >= 0 && vx < vw)
+                         ? tst[static_cast<size_t>(vy) * vw + vx] : make_float2(0.f, 0.f);
+        }
+#pragma unroll
+        for (int q = 0; q < kLoads; ++q) {
+            const int e = tid + q * kLossThreads;
+            if (e < kRH * kRW) {
+                const int ry = e / kRW, rx = e - ry * kRW;
+                S.I[ry][rx] = iv[q];
+                S.T[ry][rx] = tv[q];
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < kTs; ++q) {
+            const int e = tid + q * kLossThreads;
+            if (e < kVH * kVW) S.ts[e / kVW][e % kVW] = tsv[q];
+        }
     }
     __syncthreads();
     // corr_x (loss.cpp:103-111) of I, I^2, I*t: each item a run of kHB outputs
@@ -181,7 +211,7 @@ __global__ void __launch_bounds__(kLossThreads, 2) ssim_loss_kernel(LossArgs a, 
                     exx = fmaf(g, col1[o + k], exx);
                     exy = fmaf(g, col2[o + k], exy);
                 }
-                const float2 ts = tst[static_cast<size_t>(vy) * vw + vx];
+                const float2 ts = S.ts[i][j];
                 const float m2 = ts.x;
                 const float s12 = exy - m1 * m2;
                 const float s11 = exx - m1 * m1;
