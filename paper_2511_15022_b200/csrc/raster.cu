@@ -481,7 +481,7 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(
 constexpr int kBwdThreads = 256;
 
 template <int C>
-__global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(
+__global__ void __launch_bounds__(kBwdThreads, 3) raster_bwd_kernel(
     int N, const float4* __restrict__ rec, const float4* __restrict__ shade,
     const double* __restrict__ p64, const int4* __restrict__ pbox, int W, int H,
     const float2* __restrict__ gfield, float* __restrict__ raw) {
@@ -533,53 +533,72 @@ __global__ void __launch_bounds__(kBwdThreads) raster_bwd_kernel(
         }
         const int total = __shfl_sync(0xffffffffu, incl, 31);
         const int excl = incl - wdt;
-        for (int fb = 0; fb < total; fb += 32) {
-            const int f = fb + lane;
-            // first row whose inclusive offset exceeds f
-            int r = 0;
+        // Two flattened pixels per lane per iteration: both pixels' grad-field
+        // gathers are issued before either is consumed.
+        for (int fb = 0; fb < total; fb += 64) {
+            int px_[2], py_[2];
+            bool act[2];
 #pragma unroll
-            for (int s = 16; s > 0; s >>= 1) {
-                const int v = __shfl_sync(0xffffffffu, incl, r + s - 1);
-                if (v <= f) r += s;
-            }
-            r = min(r, 31);
-            const int rx = __shfl_sync(0xffffffffu, xl, r);
-            const int rex = __shfl_sync(0xffffffffu, excl, r);
-            if (f >= total) continue;
-            const int x = rx + (f - rex), y = ybase + r;
-            const float dx = (static_cast<float>(x) - r0.x) - r0.z;
-            const float dy = (static_cast<float>(y) - r0.y) - r0.w;
-            const float m = dx * (dx * i00 + 2.f * dy * i01) + dy * dy * i11;
-            if (m > M) continue;
-            float G = expf(-0.5f * m), aeff;
-            bool sat;
-            const float aG = alpha * G;
-            if (m <= cut - tol && fabsf(aG - 0.99f) > 1e-5f) {
-                sat = aG > 0.99f;
-                aeff = sat ? 0.99f : aG;
-            } else {
-                double Gd, ae;
-                if (!exact_contrib(q, x, y, Gd, sat, ae)) continue;
-                G = static_cast<float>(Gd);
-                aeff = static_cast<float>(ae);
-            }
-            float s_amp = 0.f;
+            for (int u = 0; u < 2; ++u) {
+                const int f = fb + u * 32 + lane;
+                int r = 0;  // first row whose inclusive offset exceeds f
 #pragma unroll
-            for (int c = 0; c < C; ++c) {
-                const float2 gv = gfield[(static_cast<size_t>(c) * H + y) * W + x];
-                const float common = sh[c].z * gv.x + sh[c].w * gv.y;
-                d_amp[c] = fmaf(aeff, common, d_amp[c]);
-                d_phase[c] = fmaf(aeff, sh[c].x * gv.y - sh[c].y * gv.x, d_phase[c]);
-                s_amp += sh[c].x * gv.x + sh[c].y * gv.y;
+                for (int s = 16; s > 0; s >>= 1) {
+                    const int v = __shfl_sync(0xffffffffu, incl, r + s - 1);
+                    if (v <= f) r += s;
+                }
+                r = min(r, 31);
+                const int rx = __shfl_sync(0xffffffffu, xl, r);
+                const int rex = __shfl_sync(0xffffffffu, excl, r);
+                act[u] = f < total;
+                px_[u] = rx + (f - rex);
+                py_[u] = ybase + r;
             }
-            if (!sat) {
-                d_alpha = fmaf(s_amp, G, d_alpha);
-                const float w = s_amp * alpha * G * -0.5f;
-                gmx += w * -2.f * (dx * i00 + dy * i01);
-                gmy += w * -2.f * (dx * i01 + dy * i11);
-                ga += w * dx * dx;
-                gb += 2.f * w * dx * dy;
-                gc += w * dy * dy;
+            float2 gv[2][C];
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+                for (int c = 0; c < C; ++c)
+                    gv[u][c] = act[u] ? gfield[(static_cast<size_t>(c) * H + py_[u]) * W + px_[u]]
+                                      : make_float2(0.f, 0.f);
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                if (!act[u]) continue;
+                const int x = px_[u], y = py_[u];
+                const float dx = (static_cast<float>(x) - r0.x) - r0.z;
+                const float dy = (static_cast<float>(y) - r0.y) - r0.w;
+                const float m = dx * (dx * i00 + 2.f * dy * i01) + dy * dy * i11;
+                if (m > M) continue;
+                float G = expf(-0.5f * m), aeff;
+                bool sat;
+                const float aG = alpha * G;
+                if (m <= cut - tol && fabsf(aG - 0.99f) > 1e-5f) {
+                    sat = aG > 0.99f;
+                    aeff = sat ? 0.99f : aG;
+                } else {
+                    double Gd, ae;
+                    if (!exact_contrib(q, x, y, Gd, sat, ae)) continue;
+                    G = static_cast<float>(Gd);
+                    aeff = static_cast<float>(ae);
+                }
+                float s_amp = 0.f;
+#pragma unroll
+                for (int c = 0; c < C; ++c) {
+                    const float2 g2 = gv[u][c];
+                    const float common = sh[c].z * g2.x + sh[c].w * g2.y;
+                    d_amp[c] = fmaf(aeff, common, d_amp[c]);
+                    d_phase[c] = fmaf(aeff, sh[c].x * g2.y - sh[c].y * g2.x, d_phase[c]);
+                    s_amp += sh[c].x * g2.x + sh[c].y * g2.y;
+                }
+                if (!sat) {
+                    d_alpha = fmaf(s_amp, G, d_alpha);
+                    const float w = s_amp * alpha * G * -0.5f;
+                    gmx += w * -2.f * (dx * i00 + dy * i01);
+                    gmy += w * -2.f * (dx * i01 + dy * i11);
+                    ga += w * dx * dx;
+                    gb += 2.f * w * dx * dy;
+                    gc += w * dy * dy;
+                }
             }
         }
     }
