@@ -176,12 +176,9 @@ extern "C" hs_status hs_build_tile_index(hs_ctx* ctx, const float* d_params, int
             HS_CUDA(cudaMemcpyAsync(stat, rw.status.p, sizeof(stat), cudaMemcpyDeviceToHost, st));
             HS_CUDA(cudaStreamSynchronize(st));
             if (stat[2]) throw Error(HS_EINVAL, "activate: non-finite input");
-            if (stat[1]) {  // grow and redo: count the exact total on the host side
-                int64_t need = 0;
-                std::vector<uint32_t> counts(n);
-                HS_CUDA(cudaMemcpy(counts.data(), rw.counts.p, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost));
-                for (uint32_t v : counts) need += v;
-                require(need < (int64_t(1) << 32), "build_tile_index: more than 2^32 pairs");
+            if (stat[1]) {  // grow to the exact total (status[0], saturated) and redo
+                const int64_t need = stat[0];
+                require(need < 0xffffffffll, "build_tile_index: more than 2^32 pairs");
                 rw.reserve_pairs(need + 1);
                 continue;
             }
@@ -211,10 +208,8 @@ static void raster_prepare_and_bin(hs_ctx* ctx, RasterWork& rw, const float* d_p
         HS_CUDA(cudaStreamSynchronize(st));
         if (stat[2]) throw Error(HS_EINVAL, "activate: non-finite input");
         if (!stat[1]) return;
-        std::vector<uint32_t> counts(n);
-        HS_CUDA(cudaMemcpy(counts.data(), rw.counts.p, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost));
-        int64_t need = 0;
-        for (uint32_t v : counts) need += v;
+        const int64_t need = stat[0];
+        require(need < 0xffffffffll, "rasterizer: more than 2^32 tile pairs");
         rw.reserve_pairs(need + 1);
     }
     throw Error(HS_EOVERFLOW, "rasterizer: pair capacity");

@@ -48,7 +48,7 @@ struct ProjParams {
     double* p64;
     int4* pbox;
     int4* tbox;
-    uint32_t* counts;
+    uint32_t* tcount;  // Gaussians per tile (atomics)
     uint32_t* status;
 };
 
@@ -106,10 +106,8 @@ __global__ void project_kernel(ProjParams P) {
     ty0 = max(ty0, 0);
     tx1 = min(tx1, P.tiles_x - 1);
     ty1 = min(ty1, P.tiles_y - 1);
-    const uint32_t cnt = (tx1 >= tx0 && ty1 >= ty0)
-                             ? static_cast<uint32_t>((tx1 - tx0 + 1) * (ty1 - ty0 + 1))
-                             : 0u;
-    P.counts[g] = cnt;
+    for (int ty = ty0; ty <= ty1; ++ty)
+        for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(P.tcount + ty * P.tiles_x + tx, 1u);
     P.tbox[g] = make_int4(tx0, tx1, ty0, ty1);
     // pixel bbox (rasterizer.cpp:157-160, 209-212)
     const int x0 = max(0, static_cast<int>(ceil(dsub(px, r))));
@@ -151,210 +149,173 @@ __global__ void project_kernel(ProjParams P) {
 }
 
 // ---------------------------------------------------------------------------
-// K1a: exclusive scan of per-Gaussian tile counts (3 phases)
+// K1: tile binning (build_index, rasterizer.cpp:90-119).  The projection
+// kernel counts the Gaussians of every tile (atomics); one CTA scans the
+// counts into per-tile offsets and writes ranges ({0,0} for empty tiles, as
+// the reference); a scatter drops each Gaussian id into its tiles' segments;
+// each tile's segment is then sorted ascending in shared memory.  (tile, id)
+// pairs are unique, so the result equals the reference's std::sort order
+// exactly, independent of the scatter order.
 // ---------------------------------------------------------------------------
-constexpr int kScanThreads = 512;
-constexpr int kScanItems = 8;
-constexpr int kScanTile = kScanThreads * kScanItems;
-
-__global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const uint32_t* in, int n, uint64_t* blocksums) {
-    using BS = cub::BlockReduce<uint64_t, kScanThreads>;
-    __shared__ typename BS::TempStorage tmp;
-    const int base = blockIdx.x * kScanTile;
-    uint64_t s = 0;
-    for (int i = threadIdx.x; i < kScanTile; i += kScanThreads) {
-        const int j = base + i;
-        if (j < n) s += in[j];
-    }
-    s = BS(tmp).Sum(s);
-    if (threadIdx.x == 0) blocksums[blockIdx.x] = s;
-}
-
-// single block: exclusive scan of block sums in place, total -> *total
-__global__ void __launch_bounds__(1024) scan_blocksums_kernel(uint64_t* blocksums, int nb, uint32_t* status, int64_t cap) {
+__global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restrict__ tcount, int tiles,
+                                                         uint32_t* __restrict__ toffset, uint2* __restrict__ ranges,
+                                                         uint32_t* __restrict__ status, int64_t cap) {
+    using BSc = cub::BlockScan<uint64_t, 1024>;
+    __shared__ typename BSc::TempStorage tmp;
     __shared__ uint64_t carry;
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
-    using BSc = cub::BlockScan<uint64_t, 1024>;
-    __shared__ typename BSc::TempStorage tmp;
-    for (int base = 0; base < nb; base += 1024) {
+    for (int base = 0; base < tiles; base += 1024) {
         const int i = base + threadIdx.x;
-        uint64_t v = i < nb ? blocksums[i] : 0;
+        const uint64_t v = i < tiles ? tcount[i] : 0u;
         uint64_t ex, agg;
         BSc(tmp).ExclusiveSum(v, ex, agg);
-        if (i < nb) blocksums[i] = ex + carry;
+        ex += carry;
+        if (i < tiles) {
+            toffset[i] = static_cast<uint32_t>(ex);
+            ranges[i] = v ? make_uint2(static_cast<uint32_t>(ex), static_cast<uint32_t>(ex + v)) : make_uint2(0u, 0u);
+        }
         __syncthreads();
         if (threadIdx.x == 0) carry += agg;
         __syncthreads();
     }
     if (threadIdx.x == 0) {
-        const uint64_t total = carry;
-        status[0] = static_cast<uint32_t>(total > 0xffffffffull ? 0xffffffffu : total);
-        status[1] = total > static_cast<uint64_t>(cap) ? 1u : 0u;
+        status[0] = static_cast<uint32_t>(carry > 0xffffffffull ? 0xffffffffull : carry);
+        status[1] = carry > static_cast<uint64_t>(cap) ? 1u : 0u;
     }
 }
 
-__global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const uint32_t* in, int n, const uint64_t* blocksums,
-                                  uint32_t* out) {
-    using BSc = cub::BlockScan<uint32_t, kScanThreads>;
-    __shared__ typename BSc::TempStorage tmp;
-    const int base = blockIdx.x * kScanTile + threadIdx.x * kScanItems;
-    uint32_t v[kScanItems];
-#pragma unroll
-    for (int k = 0; k < kScanItems; ++k) v[k] = (base + k < n) ? in[base + k] : 0u;
-    BSc(tmp).ExclusiveSum(v, v);
-    const uint32_t off = static_cast<uint32_t>(blocksums[blockIdx.x]);
-#pragma unroll
-    for (int k = 0; k < kScanItems; ++k)
-        if (base + k < n) out[base + k] = v[k] + off;
-}
-
-// ---------------------------------------------------------------------------
-// K1b: duplicate-with-keys (build_index :94-108): (tile << 32 | id), tiles in
-// ty-outer / tx-inner order per Gaussian, Gaussians in id order.
-// ---------------------------------------------------------------------------
-__global__ void emit_keys_kernel(int n, const uint32_t* offsets, const int4* tbox, int tiles_x,
-                                 const uint32_t* status, int64_t cap, uint64_t* keys) {
+// Scatter (duplicate-with-keys, :94-108): tcount is consumed as a countdown.
+__global__ void scatter_ids_kernel(int n, const int4* __restrict__ tbox, int tiles_x,
+                                   const uint32_t* __restrict__ toffset, uint32_t* __restrict__ tcount,
+                                   const uint32_t* __restrict__ status, uint32_t* __restrict__ ids) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n || status[1]) return;
     const int4 b = tbox[g];
-    uint32_t o = offsets[g];
     for (int ty = b.z; ty <= b.w; ++ty)
-        for (int tx = b.x; tx <= b.y; ++tx)
-            keys[o++] = (static_cast<uint64_t>(ty * tiles_x + tx) << 32) | static_cast<uint32_t>(g);
+        for (int tx = b.x; tx <= b.y; ++tx) {
+            const int t = ty * tiles_x + tx;
+            const uint32_t slot = atomicSub(tcount + t, 1u) - 1u;
+            ids[toffset[t] + slot] = static_cast<uint32_t>(g);
+        }
 }
 
-// ---------------------------------------------------------------------------
-// K1c: stable LSD radix sort on the tile field (bits 32..32+tile_bits).  The
-// emitted order is ascending id within every tile, so a stable sort by tile
-// alone yields the reference's std::sort order over (tile, id) pairs.
-// ---------------------------------------------------------------------------
-constexpr int kSortThreads = 256;
-constexpr int kSortItems = 16;  // per thread
-constexpr int kSortTile = kSortThreads * kSortItems;
-constexpr int kSortWarps = kSortThreads / 32;
+constexpr int kSegSmem = 4096;  // ids sorted in shared memory per tile
 
-__global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(const uint64_t* keys, const uint32_t* status, int shift,
-                                  int nblocks, uint32_t* hist) {
-    __shared__ uint32_t h[256];
-    h[threadIdx.x] = 0;
-    __syncthreads();
-    const int64_t K = status[1] ? 0 : status[0];
-    const int64_t base = static_cast<int64_t>(blockIdx.x) * kSortTile;
-    for (int i = threadIdx.x; i < kSortTile; i += kSortThreads) {
-        const int64_t j = base + i;
-        if (j < K) atomicAdd(&h[(keys[j] >> shift) & 255u], 1u);
+__device__ __forceinline__ void bitonic_smem(uint32_t* s, int P) {
+    for (int k = 2; k <= P; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < P; i += blockDim.x) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const uint32_t a = s[i], b = s[ixj];
+                    if ((a > b) == ((i & k) == 0)) {
+                        s[i] = b;
+                        s[ixj] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+}
+
+// Warp per tile for segments of <= 256 ids: an in-register bitonic network,
+// 8 ids per lane (element e = lane * 8 + i); distances < 8 are register
+// swaps, larger ones use shuffles.
+constexpr int kWarpSeg = 256;
+
+__global__ void __launch_bounds__(256) segment_sort_warp_kernel(const uint2* __restrict__ ranges, int tiles,
+                                                                uint32_t* __restrict__ ids,
+                                                                const uint32_t* __restrict__ status) {
+    const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (t >= tiles || status[1]) return;
+    const uint2 r = ranges[t];
+    const int n = static_cast<int>(r.y - r.x);
+    if (n <= 1 || n > kWarpSeg) return;
+    uint32_t v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int e = lane * 8 + i;
+        v[i] = e < n ? ids[r.x + e] : 0xffffffffu;
     }
-    __syncthreads();
-    hist[threadIdx.x * nblocks + blockIdx.x] = h[threadIdx.x];
+#pragma unroll
+    for (int k = 2; k <= kWarpSeg; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= 8) {
+                const int lj = j >> 3;  // partner lane distance
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int e = lane * 8 + i;
+                    const uint32_t o = __shfl_xor_sync(0xffffffffu, v[i], lj);
+                    const bool lower = (e & j) == 0;
+                    const bool up = (e & k) == 0;
+                    // keep min if (lower == up) else max
+                    v[i] = (lower == up) ? min(v[i], o) : max(v[i], o);
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int ixj = i ^ j;
+                    if (ixj > i) {
+                        const int e = lane * 8 + i;
+                        const bool up = (e & k) == 0;
+                        const uint32_t a = v[i], b = v[ixj];
+                        const bool sw = (a > b) == up;
+                        v[i] = sw ? b : a;
+                        v[ixj] = sw ? a : b;
+                    }
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int e = lane * 8 + i;
+        if (e < n) ids[r.x + e] = v[i];
+    }
 }
 
-// Per digit: exclusive scan over blocks (in place) + digit total.
-__global__ void __launch_bounds__(256) radix_scan_kernel(uint32_t* hist, int nblocks, uint32_t* dtot) {
-    using BSc = cub::BlockScan<uint32_t, 256>;
-    __shared__ typename BSc::TempStorage tmp;
-    __shared__ uint32_t carry;
-    uint32_t* h = hist + static_cast<size_t>(blockIdx.x) * nblocks;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    for (int base = 0; base < nblocks; base += 256 * 4) {
-        uint32_t v[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int i = base + threadIdx.x * 4 + k;
-            v[k] = i < nblocks ? h[i] : 0u;
-        }
-        uint32_t agg;
-        BSc(tmp).ExclusiveSum(v, v, agg);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int i = base + threadIdx.x * 4 + k;
-            if (i < nblocks) h[i] = v[k] + carry;
-        }
+__global__ void __launch_bounds__(256) segment_sort_kernel(const uint2* __restrict__ ranges, uint32_t* __restrict__ ids,
+                                                           uint32_t* __restrict__ scratch,
+                                                           const uint32_t* __restrict__ status) {
+    __shared__ uint32_t s[kSegSmem];
+    if (status[1]) return;
+    const uint2 r = ranges[blockIdx.x];
+    const int n = static_cast<int>(r.y - r.x);
+    if (n <= kWarpSeg) return;  // done by segment_sort_warp_kernel
+    int P = 1;
+    while (P < n) P <<= 1;
+    if (P <= kSegSmem) {
+        for (int i = threadIdx.x; i < P; i += blockDim.x) s[i] = i < n ? ids[r.x + i] : 0xffffffffu;
         __syncthreads();
-        if (threadIdx.x == 0) carry += agg;
-        __syncthreads();
+        bitonic_smem(s, P);
+        for (int i = threadIdx.x; i < n; i += blockDim.x) ids[r.x + i] = s[i];
+        return;
     }
-    if (threadIdx.x == 0) dtot[blockIdx.x] = carry;
+    // pathological tile (> kSegSmem Gaussians): same network in global memory,
+    // on a private padded copy at scratch[2*begin, 2*begin + P)
+    uint32_t* g = scratch + 2 * static_cast<size_t>(r.x);
+    for (int i = threadIdx.x; i < P; i += blockDim.x) g[i] = i < n ? ids[r.x + i] : 0xffffffffu;
+    __syncthreads();
+    bitonic_smem(g, P);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) ids[r.x + i] = g[i];
 }
 
-__global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
-    const uint64_t* __restrict__ in, uint64_t* __restrict__ out, const uint32_t* status, int shift,
-    int nblocks, const uint32_t* __restrict__ hist, const uint32_t* __restrict__ dtot) {
-    using BSc = cub::BlockScan<uint32_t, kSortThreads>;
-    __shared__ typename BSc::TempStorage tmp;
-    __shared__ uint32_t wcount[kSortWarps][257];
-    __shared__ uint32_t goff[256];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int i = threadIdx.x; i < kSortWarps * 257; i += kSortThreads) (&wcount[0][0])[i] = 0;
-    {
-        uint32_t dofs;
-        BSc(tmp).ExclusiveSum(dtot[threadIdx.x], dofs);
-        goff[threadIdx.x] = hist[threadIdx.x * nblocks + blockIdx.x] + dofs;
+// build_tile_index export: CTA per tile writes its (tile, id) pairs + range.
+__global__ void export_kernel(const uint32_t* __restrict__ ids, const uint2* __restrict__ ranges,
+                              uint32_t* __restrict__ tiles_out, uint32_t* __restrict__ ids_out,
+                              uint64_t* __restrict__ ranges_out) {
+    const int t = blockIdx.x;
+    const uint2 r = ranges[t];
+    if (threadIdx.x == 0) {
+        ranges_out[2 * static_cast<size_t>(t)] = r.x;
+        ranges_out[2 * static_cast<size_t>(t) + 1] = r.y;
     }
-    __syncthreads();
-    const int64_t K = status[1] ? 0 : status[0];
-    const int64_t base = static_cast<int64_t>(blockIdx.x) * kSortTile + warp * (32 * kSortItems);
-    uint64_t key[kSortItems];
-    uint32_t rank[kSortItems];
-    uint32_t dig[kSortItems];
-    const uint32_t lt = (1u << lane) - 1u;
-#pragma unroll
-    for (int k = 0; k < kSortItems; ++k) {
-        const int64_t idx = base + k * 32 + lane;
-        const bool valid = idx < K;
-        key[k] = valid ? in[idx] : 0ull;
-        const uint32_t d = valid ? static_cast<uint32_t>((key[k] >> shift) & 255u) : 256u;
-        dig[k] = d;
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
-        const int leader = __ffs(peers) - 1;
-        uint32_t old = 0;
-        if (lane == leader) {
-            old = wcount[warp][d];
-            wcount[warp][d] = old + __popc(peers);
-        }
-        old = __shfl_sync(0xffffffffu, old, leader);
-        rank[k] = old + __popc(peers & lt);
-        __syncwarp();
-    }
-    __syncthreads();
-    {  // exclusive prefix over warps, per digit
-        const int d = threadIdx.x;
-        uint32_t run = 0;
-#pragma unroll
-        for (int w = 0; w < kSortWarps; ++w) {
-            const uint32_t c = wcount[w][d];
-            wcount[w][d] = run;
-            run += c;
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < kSortItems; ++k) {
-        if (dig[k] < 256u) out[goff[dig[k]] + wcount[warp][dig[k]] + rank[k]] = key[k];
-    }
-}
-
-// K1d: per-tile [begin,end) (build_index :110-117); ranges pre-zeroed.
-__global__ void ranges_kernel(const uint64_t* keys, const uint32_t* status, uint2* ranges) {
-    const int64_t K = status[1] ? 0 : status[0];
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= K) return;
-    const uint32_t t = static_cast<uint32_t>(keys[i] >> 32);
-    if (i == 0 || static_cast<uint32_t>(keys[i - 1] >> 32) != t) ranges[t].x = static_cast<uint32_t>(i);
-    if (i == K - 1 || static_cast<uint32_t>(keys[i + 1] >> 32) != t) ranges[t].y = static_cast<uint32_t>(i + 1);
-}
-
-__global__ void export_kernel(const uint64_t* keys, int64_t k, const uint2* ranges, int tiles,
-                              uint32_t* tiles_out, uint32_t* ids_out, uint64_t* ranges_out) {
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i < k) {
-        tiles_out[i] = static_cast<uint32_t>(keys[i] >> 32);
-        ids_out[i] = static_cast<uint32_t>(keys[i]);
-    }
-    if (i < tiles) {
-        ranges_out[2 * i] = ranges[i].x;
-        ranges_out[2 * i + 1] = ranges[i].y;
+    for (uint32_t i = r.x + threadIdx.x; i < r.y; i += blockDim.x) {
+        tiles_out[i] = static_cast<uint32_t>(t);
+        ids_out[i] = ids[i];
     }
 }
 
@@ -385,8 +346,8 @@ __device__ __noinline__ bool exact_contrib(const double* __restrict__ q, int x, 
 // cell (exact row-band ellipse bound, conservative), the ballot is walked in
 // ascending order and every lane evaluates its pixel.
 // ---------------------------------------------------------------------------
-constexpr int kFwdThreads = 256;
-constexpr int kFwdBatch = 256;
+constexpr int kFwdThreads = 128;  // 4 warps per 16x16 tile, each an 8x8 cell
+constexpr int kFwdBatch = 128;
 
 __device__ __forceinline__ bool cell_hit(float4 r0, float4 r1, float4 r2, float cx0, float cy0,
                                          float cw, float ch) {
@@ -403,9 +364,20 @@ __device__ __forceinline__ bool cell_hit(float4 r0, float4 r1, float4 r2, float 
     return xhi >= cx0 && xlo <= cx0 + cw;
 }
 
+// fast fp32 contribution with the exact fp64 recheck inside the error band
+__device__ __forceinline__ float fwd_aeff(float m, float4 r1, float4 r2, const double* q, int x, int y) {
+    if (m <= r1.w - r2.y) return fminf(0.99f, r2.x * __expf(-0.5f * m));
+    if (m <= r1.w + r2.y) {
+        double G, ae;
+        bool sat;
+        if (exact_contrib(q, x, y, G, sat, ae)) return static_cast<float>(ae);
+    }
+    return 0.f;
+}
+
 template <int C>
 __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(
-    const uint64_t* __restrict__ keys, const uint2* __restrict__ ranges,
+    const uint32_t* __restrict__ ids, const uint2* __restrict__ ranges,
     const float4* __restrict__ rec, const float4* __restrict__ shade,
     const double* __restrict__ p64, int tiles_x, int W, int H, float2* __restrict__ field) {
     __shared__ float4 s_rec[3][kFwdBatch];
@@ -415,18 +387,19 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int cx0 = tx * kTile + (warp & 1) * 8;
-    const int cy0 = ty * kTile + (warp >> 1) * 4;
+    const int cy0 = ty * kTile + (warp >> 1) * 8;
+    // each lane owns two pixels of its column: rows ly and ly + 4 of the cell
     const int x = cx0 + (lane & 7), y = cy0 + (lane >> 3);
     const float fx = static_cast<float>(x), fy = static_cast<float>(y);
-    float2 acc[C];
+    float2 accA[C], accB[C];
 #pragma unroll
-    for (int c = 0; c < C; ++c) acc[c] = make_float2(0.f, 0.f);
+    for (int c = 0; c < C; ++c) accA[c] = accB[c] = make_float2(0.f, 0.f);
     const uint2 rg = ranges[tile];
     for (uint32_t base = rg.x; base < rg.y; base += kFwdBatch) {
         const int cnt = min(static_cast<int>(rg.y - base), kFwdBatch);
         __syncthreads();
         if (static_cast<int>(threadIdx.x) < cnt) {
-            const uint32_t g = static_cast<uint32_t>(keys[base + threadIdx.x]);
+            const uint32_t g = ids[base + threadIdx.x];
             s_id[threadIdx.x] = g;
             s_rec[0][threadIdx.x] = rec[3 * static_cast<size_t>(g)];
             s_rec[1][threadIdx.x] = rec[3 * static_cast<size_t>(g) + 1];
@@ -440,38 +413,40 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(
             bool hit = false;
             if (j < cnt)
                 hit = cell_hit(s_rec[0][j], s_rec[1][j], s_rec[2][j], static_cast<float>(cx0),
-                               static_cast<float>(cy0), 7.f, 3.f);
+                               static_cast<float>(cy0), 7.f, 7.f);
             uint32_t mask = __ballot_sync(0xffffffffu, hit);
             while (mask) {
                 const int jj = sub + __ffs(mask) - 1;
                 mask &= mask - 1;
                 const float4 r0 = s_rec[0][jj], r1 = s_rec[1][jj], r2 = s_rec[2][jj];
                 const float dx = (fx - r0.x) - r0.z;
-                const float dy = (fy - r0.y) - r0.w;
-                const float m = dx * (dx * r1.x + 2.f * dy * r1.y) + dy * dy * r1.z;
-                float aeff = 0.f;
-                if (m <= r1.w - r2.y) {
-                    aeff = fminf(0.99f, r2.x * __expf(-0.5f * m));
-                } else if (m <= r1.w + r2.y) {
-                    double G, ae;
-                    bool sat;
-                    if (exact_contrib(p64 + 8 * static_cast<size_t>(s_id[jj]), x, y, G, sat, ae))
-                        aeff = static_cast<float>(ae);
-                }
-                if (aeff > 0.f) {
+                const float dyA = (fy - r0.y) - r0.w;
+                const float dyB = dyA + 4.f;
+                const float ex = dx * r1.x;
+                const float mA = dx * (ex + 2.f * dyA * r1.y) + dyA * dyA * r1.z;
+                const float mB = dx * (ex + 2.f * dyB * r1.y) + dyB * dyB * r1.z;
+                const double* q = p64 + 8 * static_cast<size_t>(s_id[jj]);
+                const float aA = fwd_aeff(mA, r1, r2, q, x, y);
+                const float aB = fwd_aeff(mB, r1, r2, q, x, y + 4);
+                if (aA > 0.f || aB > 0.f) {
 #pragma unroll
                     for (int c = 0; c < C; ++c) {
                         const float4 sh = s_sh[c][jj];
-                        acc[c].x = fmaf(sh.x, aeff, acc[c].x);
-                        acc[c].y = fmaf(sh.y, aeff, acc[c].y);
+                        accA[c].x = fmaf(sh.x, aA, accA[c].x);
+                        accA[c].y = fmaf(sh.y, aA, accA[c].y);
+                        accB[c].x = fmaf(sh.x, aB, accB[c].x);
+                        accB[c].y = fmaf(sh.y, aB, accB[c].y);
                     }
                 }
             }
         }
     }
-    if (x < W && y < H) {
+    if (x < W) {
 #pragma unroll
-        for (int c = 0; c < C; ++c) field[(static_cast<size_t>(c) * H + y) * W + x] = acc[c];
+        for (int c = 0; c < C; ++c) {
+            if (y < H) field[(static_cast<size_t>(c) * H + y) * W + x] = accA[c];
+            if (y + 4 < H) field[(static_cast<size_t>(c) * H + y + 4) * W + x] = accB[c];
+        }
     }
 }
 
@@ -728,10 +703,9 @@ void RasterWork::prepare(int n_, int c_, int w_, int h_) {
     p64.reserve(N * 8 * sizeof(double));
     pbox.reserve(N * sizeof(int4));
     tbox.reserve(N * sizeof(int4));
-    counts.reserve(N * sizeof(uint32_t));
     raw.reserve(N * (2 * c + 6) * sizeof(float));
-    offsets.reserve(N * sizeof(uint32_t));
-    blocksums.reserve((N / kScanTile + 2) * sizeof(uint64_t));
+    tcount.reserve(static_cast<size_t>(tiles_x) * tiles_y * sizeof(uint32_t));
+    toffset.reserve(static_cast<size_t>(tiles_x) * tiles_y * sizeof(uint32_t));
     ranges.reserve(static_cast<size_t>(tiles_x) * tiles_y * sizeof(uint2));
     status.reserve(4 * sizeof(uint32_t));
     if (cap == 0) reserve_pairs(std::max<int64_t>(int64_t(1) << 20, 16 * static_cast<int64_t>(N)));
@@ -740,69 +714,51 @@ void RasterWork::prepare(int n_, int c_, int w_, int h_) {
 void RasterWork::reserve_pairs(int64_t cap_) {
     if (cap_ <= cap) return;
     cap = cap_;
-    keys[0].reserve(static_cast<size_t>(cap) * sizeof(uint64_t));
-    keys[1].reserve(static_cast<size_t>(cap) * sizeof(uint64_t));
-    const size_t nblocks = (cap + kSortTile - 1) / kSortTile;
-    hist.reserve(nblocks * 256 * sizeof(uint32_t));
-    dtot.reserve(256 * sizeof(uint32_t));
+    ids.reserve(static_cast<size_t>(cap) * sizeof(uint32_t));
+    scratch.reserve(2 * static_cast<size_t>(cap) * sizeof(uint32_t));
 }
 
 void RasterWork::project_and_bin(const float* d_params, cudaStream_t st) {
     uint32_t* stat = status.as<uint32_t>();
     HS_CUDA(cudaMemsetAsync(stat, 0, 4 * sizeof(uint32_t), st));
     const int tiles = tiles_x * tiles_y;
-    HS_CUDA(cudaMemsetAsync(ranges.p, 0, static_cast<size_t>(tiles) * sizeof(uint2), st));
-    if (n == 0) return;
+    if (n == 0) {
+        HS_CUDA(cudaMemsetAsync(ranges.p, 0, static_cast<size_t>(tiles) * sizeof(uint2), st));
+        return;
+    }
+    HS_CUDA(cudaMemsetAsync(tcount.p, 0, static_cast<size_t>(tiles) * sizeof(uint32_t), st));
     ProjParams P{d_params, n,  c,  width, height, tiles_x, tiles_y, rec.as<float4>(),
                  shade.as<float4>(), p64.as<double>(), pbox.as<int4>(), tbox.as<int4>(),
-                 counts.as<uint32_t>(), stat};
+                 tcount.as<uint32_t>(), stat};
     project_kernel<<<ceil_div(n, 128), 128, 0, st>>>(P);
     launch_check("project");
-    const int nb = ceil_div(n, kScanTile);
-    scan_reduce_kernel<<<nb, kScanThreads, 0, st>>>(counts.as<uint32_t>(), n, blocksums.as<uint64_t>());
-    launch_check("scan_reduce");
-    scan_blocksums_kernel<<<1, 1024, 0, st>>>(blocksums.as<uint64_t>(), nb, stat, cap);
-    launch_check("scan_blocksums");
-    scan_apply_kernel<<<nb, kScanThreads, 0, st>>>(counts.as<uint32_t>(), n, blocksums.as<uint64_t>(),
-                                                   offsets.as<uint32_t>());
-    launch_check("scan_apply");
-    emit_keys_kernel<<<ceil_div(n, 128), 128, 0, st>>>(n, offsets.as<uint32_t>(), tbox.as<int4>(),
-                                                       tiles_x, stat, cap, keys[0].as<uint64_t>());
-    launch_check("emit_keys");
-    const int nblocks = static_cast<int>((cap + kSortTile - 1) / kSortTile);
-    int cur = 0;
-    for (int shift = 32; shift < 32 + tile_bits; shift += 8) {
-        radix_hist_kernel<<<nblocks, kSortThreads, 0, st>>>(keys[cur].as<uint64_t>(), stat, shift,
-                                                            nblocks, hist.as<uint32_t>());
-        launch_check("radix_hist");
-        radix_scan_kernel<<<256, 256, 0, st>>>(hist.as<uint32_t>(), nblocks, dtot.as<uint32_t>());
-        launch_check("radix_scan");
-        radix_scatter_kernel<<<nblocks, kSortThreads, 0, st>>>(
-            keys[cur].as<uint64_t>(), keys[cur ^ 1].as<uint64_t>(), stat, shift, nblocks,
-            hist.as<uint32_t>(), dtot.as<uint32_t>());
-        launch_check("radix_scatter");
-        cur ^= 1;
-    }
-    sorted_buf = cur;
-    ranges_kernel<<<ceil_div(cap, 256), 256, 0, st>>>(keys[cur].as<uint64_t>(), stat,
-                                                      ranges.as<uint2>());
-    launch_check("ranges");
+    tile_scan_kernel<<<1, 1024, 0, st>>>(tcount.as<uint32_t>(), tiles, toffset.as<uint32_t>(), ranges.as<uint2>(),
+                                         stat, cap);
+    launch_check("tile_scan");
+    scatter_ids_kernel<<<ceil_div(n, 128), 128, 0, st>>>(n, tbox.as<int4>(), tiles_x, toffset.as<uint32_t>(),
+                                                         tcount.as<uint32_t>(), stat, ids.as<uint32_t>());
+    launch_check("scatter_ids");
+    segment_sort_warp_kernel<<<ceil_div(tiles, 8), 256, 0, st>>>(ranges.as<uint2>(), tiles, ids.as<uint32_t>(),
+                                                                  stat);
+    launch_check("segment_sort_warp");
+    segment_sort_kernel<<<tiles, 256, 0, st>>>(ranges.as<uint2>(), ids.as<uint32_t>(), scratch.as<uint32_t>(),
+                                               stat);
+    launch_check("segment_sort");
 }
 
 void export_tile_index(const RasterWork& rw, int64_t k, uint32_t* d_tiles, uint32_t* d_ids,
                        uint64_t* d_ranges, cudaStream_t st) {
+    (void)k;
     const int tiles = rw.tiles_x * rw.tiles_y;
-    const int64_t m = std::max<int64_t>(k, tiles);
-    if (m == 0) return;
-    export_kernel<<<ceil_div(m, 256), 256, 0, st>>>(rw.sorted_keys(), k, rw.ranges.as<uint2>(), tiles,
-                                                    d_tiles, d_ids, d_ranges);
+    if (tiles == 0) return;
+    export_kernel<<<tiles, 128, 0, st>>>(rw.ids.as<uint32_t>(), rw.ranges.as<uint2>(), d_tiles, d_ids, d_ranges);
     launch_check("export_tile_index");
 }
 
 template <int C>
 static void fwd_launch(const RasterWork& rw, float2* d_field, cudaStream_t st) {
     raster_fwd_kernel<C><<<rw.tiles_x * rw.tiles_y, kFwdThreads, 0, st>>>(
-        rw.sorted_keys(), rw.ranges.as<uint2>(), rw.rec.as<float4>(), rw.shade.as<float4>(),
+        rw.ids.as<uint32_t>(), rw.ranges.as<uint2>(), rw.rec.as<float4>(), rw.shade.as<float4>(),
         rw.p64.as<double>(), rw.tiles_x, rw.width, rw.height, d_field);
     launch_check("raster_fwd");
 }

@@ -16,23 +16,19 @@ struct RasterWork {
     DevBuf p64;      // 8 doubles per Gaussian (exact fp64 record for boundary rechecks)
     DevBuf pbox;     // int4 pixel bbox (x0,x1,y0,y1) clamped to the canvas
     DevBuf tbox;     // int4 tile bbox
-    DevBuf counts;   // uint32 tiles per Gaussian
+    DevBuf tcount;   // uint32 Gaussians per tile
+    DevBuf toffset;  // uint32 exclusive scan of tcount
     DevBuf raw;      // backward partial sums, (7+2C) x N floats (SoA)
-    DevBuf offsets;  // uint32 exclusive scan of counts
-    DevBuf blocksums;
-    DevBuf keys[2];  // uint64 (tile << 32 | id), ping-pong for the radix sort
-    DevBuf hist;     // radix histograms
-    DevBuf dtot;     // per-digit totals
+    DevBuf ids;      // uint32 Gaussian ids grouped by tile, ascending within a tile
+    DevBuf scratch;  // 2 x cap uint32: global bitonic fallback for huge tiles
     DevBuf ranges;   // uint2 [begin,end) per tile
     DevBuf status;   // uint32[4]: [0] K (pairs), [1] overflow, [2] non-finite param, [3] unused
     int64_t cap = 0; // pair capacity
-    int sorted_buf = 0;  // which keys[] holds the sorted result
 
     void prepare(int n_, int c_, int w_, int h_);
     void reserve_pairs(int64_t cap_);
-    // K0 + K1 on stream; leaves sorted keys + ranges on device (K in status[0]).
+    // K0 + K1 on stream; leaves per-tile sorted ids + ranges on device (K in status[0]).
     void project_and_bin(const float* d_params, cudaStream_t st);
-    const uint64_t* sorted_keys() const { return keys[sorted_buf].as<uint64_t>(); }
 };
 
 void raster_forward(const RasterWork& rw, float2* d_field, cudaStream_t st);
