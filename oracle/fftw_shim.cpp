@@ -2,10 +2,12 @@
 //
 // fp64 restatement of the two FFTW3 entry points the reference uses
 // (proj/core/src/propagation.cpp:27-30 plan, :38-39 execute).  See fftw3.h for
-// the contract.  Algorithm: mixed-radix Stockham autosort (radices 4,2,3,5,7
-// and any prime <= 64 through a generic small DFT), Bluestein chirp-z for
-// lengths with a prime factor > 64.  Single-threaded like the reference's
-// FFTW usage (no fftw_init_threads anywhere in the reference).
+// the contract.  Algorithm: mixed-radix Stockham autosort (specialised radix
+// 4, 2, 3, 5, generic odd radix <= 64) run on blocks of kB vectors
+// interleaved [n][kB] so the inner loops vectorise (FFTW-class speed on the
+// 2160 x 3840 grids), and Bluestein chirp-z for lengths with a prime factor
+// > 64.  Single-threaded like the reference's FFTW usage (no
+// fftw_init_threads anywhere in the reference).
 #include "fftw3.h"
 
 #include <algorithm>
@@ -20,18 +22,20 @@ namespace {
 
 using cd = std::complex<double>;
 constexpr double kTwoPi = 6.283185307179586476925286766559;
+constexpr int kB = 8;  // vectors per batch
 
 struct Fft1d {
     int n = 0;
     int sign = -1;
     std::vector<int> radices;
-    std::vector<cd> w;  // w[k] = exp(sign * 2 pi i k / n)
-    std::vector<std::vector<cd>> small;  // per distinct radix: exp(sign 2 pi i q / r)
+    std::vector<int> nss;
+    std::vector<std::vector<cd>> stw;    // per stage: [r-1][k], k < ns
+    std::vector<std::vector<cd>> small;  // per stage: exp(sign 2 pi i q / r)
     // Bluestein
     bool blue = false;
     int m = 0;
-    std::vector<cd> chirp;   // c_k = exp(sign * pi i k^2 / n)
-    std::vector<cd> bspec;   // FFT_m of the conjugate chirp kernel
+    std::vector<cd> chirp;
+    std::vector<cd> bspec;
     std::unique_ptr<Fft1d> fwd_m, inv_m;
 
     void init(int n_, int sign_) {
@@ -57,81 +61,130 @@ struct Fft1d {
             inv_m = std::make_unique<Fft1d>();
             fwd_m->init(m, -1);
             inv_m->init(m, +1);
-            std::vector<cd> b(m, cd(0.0, 0.0)), scratch(m);
+            std::vector<cd> b(static_cast<size_t>(m) * kB, cd(0.0, 0.0));
             b[0] = std::conj(chirp[0]);
-            for (int k = 1; k < n; ++k) b[k] = b[m - k] = std::conj(chirp[k]);
-            fwd_m->run(b.data(), scratch.data());
-            bspec = b;
+            for (int k = 1; k < n; ++k) b[static_cast<size_t>(k) * kB] = b[static_cast<size_t>(m - k) * kB] = std::conj(chirp[k]);
+            std::vector<cd> scratch(b.size());
+            fwd_m->run(b.data(), scratch.data(), 1);
+            bspec.resize(m);
+            for (int k = 0; k < m; ++k) bspec[k] = b[static_cast<size_t>(k) * kB];
             return;
         }
-        w.resize(n);
-        for (int k = 0; k < n; ++k) {
-            const double a = sign * kTwoPi * static_cast<double>(k) / n;
-            w[k] = cd(std::cos(a), std::sin(a));
-        }
-        small.assign(65, {});
+        int ns = 1;
         for (int r : radices) {
-            if (!small[r].empty()) continue;
-            small[r].resize(r);
+            nss.push_back(ns);
+            std::vector<cd> t(static_cast<size_t>(r - 1) * ns);
+            for (int q = 1; q < r; ++q)
+                for (int k = 0; k < ns; ++k) {
+                    const double a = sign * kTwoPi * static_cast<double>(q * k) / (ns * r);
+                    t[static_cast<size_t>(q - 1) * ns + k] = cd(std::cos(a), std::sin(a));
+                }
+            stw.push_back(std::move(t));
+            std::vector<cd> sm(r);
             for (int q = 0; q < r; ++q) {
                 const double a = sign * kTwoPi * static_cast<double>(q) / r;
-                small[r][q] = cd(std::cos(a), std::sin(a));
+                sm[q] = cd(std::cos(a), std::sin(a));
             }
+            small.push_back(std::move(sm));
+            ns *= r;
         }
     }
 
-    // In-place transform of data[0..n); scratch must hold max(n, 2m) values.
-    void run(cd* data, cd* scratch) const {
+    // Transforms `nb` (<= kB) vectors stored interleaved data[i * kB + b].
+    void run(cd* data, cd* scratch, int nb) const {
         if (n == 1) return;
         if (blue) {
-            std::vector<cd> a(m, cd(0.0, 0.0)), s2(m);
-            for (int k = 0; k < n; ++k) a[k] = data[k] * chirp[k];
-            fwd_m->run(a.data(), s2.data());
-            for (int k = 0; k < m; ++k) a[k] *= bspec[k];
-            inv_m->run(a.data(), s2.data());
+            std::vector<cd> a(static_cast<size_t>(m) * kB, cd(0.0, 0.0)), s2(a.size());
+            for (int k = 0; k < n; ++k)
+                for (int b = 0; b < nb; ++b) a[static_cast<size_t>(k) * kB + b] = data[static_cast<size_t>(k) * kB + b] * chirp[k];
+            fwd_m->run(a.data(), s2.data(), nb);
+            for (int k = 0; k < m; ++k)
+                for (int b = 0; b < nb; ++b) a[static_cast<size_t>(k) * kB + b] *= bspec[k];
+            inv_m->run(a.data(), s2.data(), nb);
             const double inv = 1.0 / m;
-            for (int k = 0; k < n; ++k) data[k] = a[k] * inv * chirp[k];
+            for (int k = 0; k < n; ++k)
+                for (int b = 0; b < nb; ++b)
+                    data[static_cast<size_t>(k) * kB + b] = a[static_cast<size_t>(k) * kB + b] * inv * chirp[k];
             return;
         }
         cd* in = data;
         cd* out = scratch;
-        int ns = 1;
-        cd v[64], y[64];
-        for (int r : radices) {
+        for (size_t s = 0; s < radices.size(); ++s) {
+            const int r = radices[s], ns = nss[s];
             const int stride = n / r;
-            const int span = n / (ns * r);
-            const std::vector<cd>& tw = small[r];
+            const cd* tw = stw[s].data();
+            const cd* sm = small[s].data();
             for (int j = 0; j < stride; ++j) {
                 const int k = j % ns;
-                for (int q = 0; q < r; ++q) v[q] = in[j + q * stride];
-                if (ns > 1)
-                    for (int q = 1; q < r; ++q)
-                        v[q] *= w[(static_cast<int64_t>(q) * k * span) % n];
-                if (r == 2) {
-                    y[0] = v[0] + v[1];
-                    y[1] = v[0] - v[1];
-                } else if (r == 4) {
-                    const cd a0 = v[0] + v[2], a1 = v[0] - v[2];
-                    const cd b0 = v[1] + v[3], b1 = v[1] - v[3];
-                    const cd jb1 = cd(-sign * b1.imag(), sign * b1.real());  // sign*i*b1
-                    y[0] = a0 + b0;
-                    y[2] = a0 - b0;
-                    y[1] = a1 + jb1;
-                    y[3] = a1 - jb1;
+                const size_t base = static_cast<size_t>((j - k) * r + k);
+                cd w[64];
+                w[0] = cd(1.0, 0.0);
+                for (int q = 1; q < r; ++q) w[q] = tw[static_cast<size_t>(q - 1) * ns + k];
+                const cd* src = in + static_cast<size_t>(j) * kB;
+                cd* dst = out + base * kB;
+                const size_t sstr = static_cast<size_t>(stride) * kB, dstr = static_cast<size_t>(ns) * kB;
+                if (r == 4) {
+                    const cd w1 = w[1], w2 = w[2], w3 = w[3];
+                    for (int b = 0; b < nb; ++b) {
+                        const cd v0 = src[b], v1 = src[sstr + b] * w1, v2 = src[2 * sstr + b] * w2,
+                                 v3 = src[3 * sstr + b] * w3;
+                        const cd a0 = v0 + v2, a1 = v0 - v2, b0 = v1 + v3, b1 = v1 - v3;
+                        const cd jb1(-sign * b1.imag(), sign * b1.real());
+                        dst[b] = a0 + b0;
+                        dst[dstr + b] = a1 + jb1;
+                        dst[2 * dstr + b] = a0 - b0;
+                        dst[3 * dstr + b] = a1 - jb1;
+                    }
+                } else if (r == 2) {
+                    const cd w1 = w[1];
+                    for (int b = 0; b < nb; ++b) {
+                        const cd v0 = src[b], v1 = src[sstr + b] * w1;
+                        dst[b] = v0 + v1;
+                        dst[dstr + b] = v0 - v1;
+                    }
+                } else if (r == 3) {
+                    const cd w1 = w[1], w2 = w[2];
+                    const double c1 = -0.5, s1 = sign * 0.86602540378443864676;
+                    for (int b = 0; b < nb; ++b) {
+                        const cd v0 = src[b], v1 = src[sstr + b] * w1, v2 = src[2 * sstr + b] * w2;
+                        const cd t = v1 + v2, d = v1 - v2;
+                        const cd mm = v0 + c1 * t;
+                        const cd id(-s1 * d.imag(), s1 * d.real());
+                        dst[b] = v0 + t;
+                        dst[dstr + b] = mm + id;
+                        dst[2 * dstr + b] = mm - id;
+                    }
+                } else if (r == 5) {
+                    const double c1 = 0.30901699437494742410, c2 = -0.80901699437494742410;
+                    const double s1 = sign * 0.95105651629515357212, s2 = sign * 0.58778525229247312917;
+                    for (int b = 0; b < nb; ++b) {
+                        const cd v0 = src[b], v1 = src[sstr + b] * w[1], v2 = src[2 * sstr + b] * w[2],
+                                 v3 = src[3 * sstr + b] * w[3], v4 = src[4 * sstr + b] * w[4];
+                        const cd t1 = v1 + v4, d1 = v1 - v4, t2 = v2 + v3, d2 = v2 - v3;
+                        const cd m1 = v0 + c1 * t1 + c2 * t2, m2 = v0 + c2 * t1 + c1 * t2;
+                        const cd n1 = s1 * d1 + s2 * d2, n2 = s2 * d1 - s1 * d2;
+                        const cd in1(-n1.imag(), n1.real()), in2(-n2.imag(), n2.real());
+                        dst[b] = v0 + t1 + t2;
+                        dst[dstr + b] = m1 + in1;
+                        dst[4 * dstr + b] = m1 - in1;
+                        dst[2 * dstr + b] = m2 + in2;
+                        dst[3 * dstr + b] = m2 - in2;
+                    }
                 } else {
-                    for (int o = 0; o < r; ++o) {
-                        cd s(0.0, 0.0);
-                        for (int q = 0; q < r; ++q) s += v[q] * tw[(q * o) % r];
-                        y[o] = s;
+                    for (int b = 0; b < nb; ++b) {
+                        cd v[64];
+                        for (int q = 0; q < r; ++q) v[q] = src[q * sstr + b] * w[q];
+                        for (int o = 0; o < r; ++o) {
+                            cd acc(0.0, 0.0);
+                            for (int q = 0; q < r; ++q) acc += v[q] * sm[(q * o) % r];
+                            dst[o * dstr + b] = acc;
+                        }
                     }
                 }
-                const int base = (j / ns) * ns * r + k;
-                for (int q = 0; q < r; ++q) out[base + q * ns] = y[q];
             }
-            ns *= r;
             std::swap(in, out);
         }
-        if (in != data) std::memcpy(data, in, sizeof(cd) * n);
+        if (in != data) std::memcpy(data, in, sizeof(cd) * static_cast<size_t>(n) * kB);
     }
 };
 
@@ -164,17 +217,24 @@ void fftw_execute_dft(const fftw_plan p, fftw_complex* in, fftw_complex* out) {
     cd* data = reinterpret_cast<cd*>(out);
     if (in != out) std::memcpy(out, in, sizeof(cd) * static_cast<size_t>(n0) * n1);
     const int big = std::max(n0, n1);
-    std::vector<cd> scratch(static_cast<size_t>(big));
-    for (int y = 0; y < n0; ++y) p->rows.run(data + static_cast<size_t>(y) * n1, scratch.data());
-    constexpr int kBlock = 16;
-    std::vector<cd> col(static_cast<size_t>(kBlock) * n0);
-    for (int x0 = 0; x0 < n1; x0 += kBlock) {
-        const int bw = std::min(kBlock, n1 - x0);
+    std::vector<cd> buf(static_cast<size_t>(big) * kB), scratch(buf.size());
+    // rows, kB at a time
+    for (int y0 = 0; y0 < n0; y0 += kB) {
+        const int nb = std::min(kB, n0 - y0);
+        for (int b = 0; b < nb; ++b)
+            for (int x = 0; x < n1; ++x) buf[static_cast<size_t>(x) * kB + b] = data[static_cast<size_t>(y0 + b) * n1 + x];
+        p->rows.run(buf.data(), scratch.data(), nb);
+        for (int b = 0; b < nb; ++b)
+            for (int x = 0; x < n1; ++x) data[static_cast<size_t>(y0 + b) * n1 + x] = buf[static_cast<size_t>(x) * kB + b];
+    }
+    // columns, kB at a time
+    for (int x0 = 0; x0 < n1; x0 += kB) {
+        const int nb = std::min(kB, n1 - x0);
         for (int y = 0; y < n0; ++y)
-            for (int b = 0; b < bw; ++b) col[static_cast<size_t>(b) * n0 + y] = data[static_cast<size_t>(y) * n1 + x0 + b];
-        for (int b = 0; b < bw; ++b) p->cols.run(col.data() + static_cast<size_t>(b) * n0, scratch.data());
+            for (int b = 0; b < nb; ++b) buf[static_cast<size_t>(y) * kB + b] = data[static_cast<size_t>(y) * n1 + x0 + b];
+        p->cols.run(buf.data(), scratch.data(), nb);
         for (int y = 0; y < n0; ++y)
-            for (int b = 0; b < bw; ++b) data[static_cast<size_t>(y) * n1 + x0 + b] = col[static_cast<size_t>(b) * n0 + y];
+            for (int b = 0; b < nb; ++b) data[static_cast<size_t>(y) * n1 + x0 + b] = buf[static_cast<size_t>(y) * kB + b];
     }
 }
 
