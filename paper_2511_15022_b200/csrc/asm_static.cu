@@ -54,27 +54,40 @@ __device__ __forceinline__ float2 transfer_fast(const TfConst& t, int mx, int my
 
 // One work item per CTA throughout: a loop around the unrolled FFT makes
 // ptxas spill heavily (measured), so persistence is traded for more CTAs.
+// Per-row bases are hoisted out of the element loops (a runtime division by
+// H per element was ~15% of the row kernels' instructions).
 template <int N, int RB, int NT, int CCO, class RAD>
 __global__ void __launch_bounds__(NT) srows_fwd_kernel(RowArgs a, int nrows, const float2* __restrict__ tw) {
     extern __shared__ float2 smem[];
     const int tid = threadIdx.x;
     const int rho0 = blockIdx.x * RB;
-    for (int e = tid; e < N * RB; e += NT) {
-        const int i = e / RB, rr = e - i * RB;
-        const int x = i - a.ox, rho = rho0 + rr;
-        smem[fft::pidx(e)] = (x >= 0 && x < a.W && rho < nrows) ? a.in[static_cast<size_t>(rho) * a.W + x]
-                                                               : make_float2(0.f, 0.f);
+    const float2* src[RB];
+    float2* dst[RB];
+    bool ok[RB];
+#pragma unroll
+    for (int rr = 0; rr < RB; ++rr) {
+        const int rho = rho0 + rr;
+        ok[rr] = rho < nrows;
+        const int pc = rho / a.H, y = rho - pc * a.H;
+        src[rr] = a.in + static_cast<size_t>(rho) * a.W - a.ox;
+        dst[rr] = a.out + (static_cast<size_t>(pc) * a.ntiles * a.H + y) * CCO;
+    }
+    const size_t tile_stride = static_cast<size_t>(a.H) * CCO;
+#pragma unroll 4
+    for (int i = tid; i < N; i += NT) {
+        const bool in = i >= a.ox && i < a.ox + a.W;
+#pragma unroll
+        for (int rr = 0; rr < RB; ++rr)
+            smem[fft::pidx(i * RB + rr)] = (in && ok[rr]) ? src[rr][i] : make_float2(0.f, 0.f);
     }
     __syncthreads();
     sfft::run<N, RB, NT, -1>(smem, tw, tid, RAD{});
-    constexpr int NTILE = (N + CCO - 1) / CCO;
-    for (int e = tid; e < NTILE * RB * CCO; e += NT) {
-        const int cc = e % CCO, rr = (e / CCO) % RB, t = e / (CCO * RB);
-        const int i = t * CCO + cc, rho = rho0 + rr;
-        if (i < N && rho < nrows) {
-            const int pc = rho / a.H, y = rho - pc * a.H;
-            a.out[((static_cast<size_t>(pc) * a.ntiles + t) * a.H + y) * CCO + cc] = smem[fft::pidx(i * RB + rr)];
-        }
+#pragma unroll 4
+    for (int i = tid; i < N; i += NT) {
+        const size_t off = static_cast<size_t>(i / CCO) * tile_stride + (i % CCO);
+#pragma unroll
+        for (int rr = 0; rr < RB; ++rr)
+            if (ok[rr]) dst[rr][off] = smem[fft::pidx(i * RB + rr)];
     }
 }
 
@@ -82,27 +95,35 @@ template <int N, int RB, int NT, int CCO, class RAD>
 __global__ void __launch_bounds__(NT) srows_inv_kernel(RowArgs a, int nrows, const float2* __restrict__ tw) {
     extern __shared__ float2 smem[];
     const int tid = threadIdx.x;
-    constexpr int NTILE = (N + CCO - 1) / CCO;
     const int rho0 = blockIdx.x * RB;
-    for (int e = tid; e < NTILE * RB * CCO; e += NT) {
-        const int cc = e % CCO, rr = (e / CCO) % RB, t = e / (CCO * RB);
-        const int i = t * CCO + cc, rho = rho0 + rr;
-        if (i < N) {
-            float2 v = make_float2(0.f, 0.f);
-            if (rho < nrows) {
-                const int pc = rho / a.H, y = rho - pc * a.H;
-                v = a.in[((static_cast<size_t>(pc) * a.ntiles + t) * a.H + y) * CCO + cc];
-            }
-            smem[fft::pidx(i * RB + rr)] = v;
-        }
+    const float2* src[RB];
+    float2* dst[RB];
+    bool ok[RB];
+#pragma unroll
+    for (int rr = 0; rr < RB; ++rr) {
+        const int rho = rho0 + rr;
+        ok[rr] = rho < nrows;
+        const int pc = rho / a.H, y = rho - pc * a.H;
+        src[rr] = a.in + (static_cast<size_t>(pc) * a.ntiles * a.H + y) * CCO;
+        dst[rr] = a.out + static_cast<size_t>(rho) * a.W - a.ox;
+    }
+    const size_t tile_stride = static_cast<size_t>(a.H) * CCO;
+#pragma unroll 4
+    for (int i = tid; i < N; i += NT) {
+        const size_t off = static_cast<size_t>(i / CCO) * tile_stride + (i % CCO);
+#pragma unroll
+        for (int rr = 0; rr < RB; ++rr) smem[fft::pidx(i * RB + rr)] = ok[rr] ? src[rr][off] : make_float2(0.f, 0.f);
     }
     __syncthreads();
     sfft::run<N, RB, NT, +1>(smem, tw, tid, RAD{});
-    for (int e = tid; e < a.W * RB; e += NT) {
-        const int rr = e / a.W, x = e - rr * a.W, rho = rho0 + rr;
-        if (rho < nrows) {
-            const float2 v = smem[fft::pidx((x + a.ox) * RB + rr)];
-            a.out[static_cast<size_t>(rho) * a.W + x] = make_float2(v.x * a.scale, v.y * a.scale);
+    const float sc = a.scale;
+#pragma unroll 4
+    for (int i = a.ox + tid; i < a.ox + a.W; i += NT) {
+#pragma unroll
+        for (int rr = 0; rr < RB; ++rr) {
+            if (!ok[rr]) continue;
+            const float2 v = smem[fft::pidx(i * RB + rr)];
+            dst[rr][i] = make_float2(v.x * sc, v.y * sc);
         }
     }
 }
@@ -132,7 +153,7 @@ __device__ __forceinline__ void apply_transfer(float2* dst, const float2* src, c
 
 // Single plane (the benchmark case): no loops around the FFTs.
 template <int N, int CC, int NT, class RAD>
-__global__ void __launch_bounds__(NT) scols_fwd1_kernel(ColArgs a, const float2* __restrict__ tw) {
+__global__ void __launch_bounds__(NT, 2) scols_fwd1_kernel(ColArgs a, const float2* __restrict__ tw) {
     extern __shared__ float2 smem[];
     const int tile = blockIdx.x, c = blockIdx.y;
     const size_t tile_elems = static_cast<size_t>(a.H) * CC;
@@ -146,7 +167,7 @@ __global__ void __launch_bounds__(NT) scols_fwd1_kernel(ColArgs a, const float2*
 }
 
 template <int N, int CC, int NT, class RAD>
-__global__ void __launch_bounds__(NT) scols_bwd1_kernel(ColArgs a, const float2* __restrict__ tw) {
+__global__ void __launch_bounds__(NT, 2) scols_bwd1_kernel(ColArgs a, const float2* __restrict__ tw) {
     extern __shared__ float2 smem[];
     const int tile = blockIdx.x, c = blockIdx.y;
     const size_t tile_elems = static_cast<size_t>(a.H) * CC;
@@ -163,7 +184,7 @@ __global__ void __launch_bounds__(NT) scols_bwd1_kernel(ColArgs a, const float2*
 // a second shared buffer); the adjoint sums the planes' spectra before one
 // inverse FFT (propagation.cpp:240-294).
 template <int N, int CC, int NT, class RAD>
-__global__ void __launch_bounds__(NT) scols_fwdL_kernel(ColArgs a, const float2* __restrict__ tw) {
+__global__ void __launch_bounds__(NT, 2) scols_fwdL_kernel(ColArgs a, const float2* __restrict__ tw) {
     extern __shared__ float2 smem[];
     float2* A = smem;
     float2* Sp = smem + fft::padded_len(N * CC);
@@ -184,7 +205,7 @@ __global__ void __launch_bounds__(NT) scols_fwdL_kernel(ColArgs a, const float2*
 }
 
 template <int N, int CC, int NT, class RAD>
-__global__ void __launch_bounds__(NT) scols_bwdL_kernel(ColArgs a, const float2* __restrict__ tw) {
+__global__ void __launch_bounds__(NT, 2) scols_bwdL_kernel(ColArgs a, const float2* __restrict__ tw) {
     extern __shared__ float2 smem[];
     float2* A = smem;
     float2* Z = smem + fft::padded_len(N * CC);

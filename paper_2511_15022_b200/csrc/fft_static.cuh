@@ -34,8 +34,15 @@ __device__ __forceinline__ void stage(float2* __restrict__ buf, const float2* __
         const int bi = tid + b * NT;
         if (NB % NT == 0 || bi < NB) {
             const int cc = bi % CC, j = bi / CC;
+            const int q0 = j * CC + cc;
+            if constexpr ((M * CC) % 16 == 0) {  // padded stride is linear: one index, immediate offsets
+                const int p0 = fft::pidx(q0);
 #pragma unroll
-            for (int r = 0; r < R; ++r) v[b][r] = buf[fft::pidx((j + r * M) * CC + cc)];
+                for (int r = 0; r < R; ++r) v[b][r] = buf[p0 + r * (M * CC / 16 * 17)];
+            } else {
+#pragma unroll
+                for (int r = 0; r < R; ++r) v[b][r] = buf[fft::pidx(q0 + r * M * CC)];
+            }
         }
     }
     __syncthreads();
@@ -55,9 +62,15 @@ __device__ __forceinline__ void stage(float2* __restrict__ buf, const float2* __
                 }
             }
             fft::dft<R, S>(v[b]);
-            const int base = (j - k) * R + k;
+            const int qs = ((j - k) * R + k) * CC + cc;
+            if constexpr ((NS * CC) % 16 == 0) {
+                const int ps = fft::pidx(qs);
 #pragma unroll
-            for (int r = 0; r < R; ++r) buf[fft::pidx((base + r * NS) * CC + cc)] = v[b][r];
+                for (int r = 0; r < R; ++r) buf[ps + r * (NS * CC / 16 * 17)] = v[b][r];
+            } else {
+#pragma unroll
+                for (int r = 0; r < R; ++r) buf[fft::pidx(qs + r * NS * CC)] = v[b][r];
+            }
         }
     }
     __syncthreads();
