@@ -248,7 +248,7 @@ void AsmWork::prepare(int C_, int H_, int W_, int pad_, int L_) {
     oy = (Py - H) / 2;
     const int nbuf = L_ > 1 ? 3 : 2;
     CC = 4;
-    use_static = static_plan_cc(Px, Py, std::max(L, L_), &CC);
+    use_static = static_plan_cc(Px, Py, pad, std::max(L, L_), &CC);
     if (!use_static) CC = 4;
     while (!use_static && CC > 1 &&
            nbuf * static_cast<size_t>(fft::padded_len(Py * CC)) * sizeof(float2) > kSmemBudget)

@@ -88,7 +88,7 @@ struct ColArgs {
 };
 
 // Static (compile-time planned) propagation path; false when (Px, Py) has no plan.
-bool static_plan_cc(int Px, int Py, int L, int* cc);
+bool static_plan_cc(int Px, int Py, int pad, int L, int* cc);
 bool static_forward(AsmWork& w, const float2* d_in, float2* d_out, cudaStream_t st, cudaEvent_t* ev);
 bool static_backward(AsmWork& w, const float2* d_grads, float2* d_out, cudaStream_t st, cudaEvent_t* ev);
 void static_prepare(AsmWork& w);

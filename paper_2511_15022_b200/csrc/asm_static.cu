@@ -2,10 +2,13 @@
 //
 // Same data path and numerics contract as asm.cu (propagation.cpp:186-294),
 // with the FFT engine of fft_static.cuh: in-place stages, constant strides,
-// persistent CTAs looping over rows / column tiles, and the transfer function
-// H = exp(i kz d) evaluated with a Cody-Waite reduced fast sincos.
+// first stages read straight from global memory (zero pad skipped), last
+// stages write straight to global memory (crop skipped) or apply the transfer
+// function H = exp(i kz d) in registers (Cody-Waite reduced fast sincos).
+// The pruning assumes the centred pad of factor 2 (offset = padded length / 4),
+// so these plans are only used when pad == 2.
 //
-// Plans (Px x Py, column tile width CC):
+// Plans (Px x Py, column tile width CC; radices with first and last % 4 == 0):
 //   3840 x 2160, CC 4   cfg2/cfg3 (1920x1080, pad 2)
 //    512 x  512, CC 4   cfg1 (256x256, pad 2)
 //    512 x  320, CC 4   desk regression (256x160, pad 2)
@@ -52,176 +55,142 @@ __device__ __forceinline__ float2 transfer_fast(const TfConst& t, int mx, int my
     return make_float2(c, CONJ ? -s : s);
 }
 
-// One work item per CTA throughout: a loop around the unrolled FFT makes
-// ptxas spill heavily (measured), so persistence is traded for more CTAs.
-// Per-row bases are hoisted out of the element loops (a runtime division by
-// H per element was ~15% of the row kernels' instructions).
+// Row kernels: RB rows per CTA, interleaved in the engine (its CC = RB); a
+// thread always serves row rr = tid % RB (NT % RB == 0), so its row pointers
+// are computed once.  The forward reads only the W live inputs of each row
+// (first stage pruned to the centred block) and writes the column-tiled T
+// layout from the last stage; the inverse writes only the W cropped outputs.
 template <int N, int RB, int NT, int CCO, class RAD>
 __global__ void __launch_bounds__(NT) srows_fwd_kernel(RowArgs a, int nrows, const float2* __restrict__ tw) {
+    static_assert(NT % RB == 0, "row of a thread must be fixed");
     extern __shared__ float2 smem[];
     const int tid = threadIdx.x;
-    const int rho0 = blockIdx.x * RB;
-    const float2* src[RB];
-    float2* dst[RB];
-    bool ok[RB];
-#pragma unroll
-    for (int rr = 0; rr < RB; ++rr) {
-        const int rho = rho0 + rr;
-        ok[rr] = rho < nrows;
-        const int pc = rho / a.H, y = rho - pc * a.H;
-        src[rr] = a.in + static_cast<size_t>(rho) * a.W - a.ox;
-        dst[rr] = a.out + (static_cast<size_t>(pc) * a.ntiles * a.H + y) * CCO;
-    }
-    const size_t tile_stride = static_cast<size_t>(a.H) * CCO;
-#pragma unroll 4
-    for (int i = tid; i < N; i += NT) {
-        const bool in = i >= a.ox && i < a.ox + a.W;
-#pragma unroll
-        for (int rr = 0; rr < RB; ++rr)
-            smem[fft::pidx(i * RB + rr)] = (in && ok[rr]) ? src[rr][i] : make_float2(0.f, 0.f);
-    }
-    __syncthreads();
-    sfft::run<N, RB, NT, -1>(smem, tw, tid, RAD{});
-#pragma unroll 4
-    for (int i = tid; i < N; i += NT) {
-        const size_t off = static_cast<size_t>(i / CCO) * tile_stride + (i % CCO);
-#pragma unroll
-        for (int rr = 0; rr < RB; ++rr)
-            if (ok[rr]) dst[rr][off] = smem[fft::pidx(i * RB + rr)];
-    }
+    const int rho = blockIdx.x * RB + tid % RB;
+    const bool ok = rho < nrows;
+    const int pc = rho / a.H, y = rho - pc * a.H;
+    const float2* src = a.in + static_cast<size_t>(rho) * a.W - a.ox;  // src[i], i in [ox, ox + W)
+    float2* dst = a.out + (static_cast<size_t>(pc) * a.ntiles * a.H + y) * CCO;
+    const size_t ts = static_cast<size_t>(a.H) * CCO;
+    sfft::run<N, RB, NT, -1, sfft::Half, sfft::Full>(
+        smem, tw, tid, RAD{},
+        sfft::in_fn([&](int i, int) { return ok ? src[i] : make_float2(0.f, 0.f); }),
+        sfft::out_fn([&](int i, int, float2 v) {
+            if (ok) dst[static_cast<size_t>(i / CCO) * ts + (i % CCO)] = v;
+        }));
 }
 
 template <int N, int RB, int NT, int CCO, class RAD>
 __global__ void __launch_bounds__(NT) srows_inv_kernel(RowArgs a, int nrows, const float2* __restrict__ tw) {
+    static_assert(NT % RB == 0, "row of a thread must be fixed");
     extern __shared__ float2 smem[];
     const int tid = threadIdx.x;
-    const int rho0 = blockIdx.x * RB;
-    const float2* src[RB];
-    float2* dst[RB];
-    bool ok[RB];
-#pragma unroll
-    for (int rr = 0; rr < RB; ++rr) {
-        const int rho = rho0 + rr;
-        ok[rr] = rho < nrows;
-        const int pc = rho / a.H, y = rho - pc * a.H;
-        src[rr] = a.in + (static_cast<size_t>(pc) * a.ntiles * a.H + y) * CCO;
-        dst[rr] = a.out + static_cast<size_t>(rho) * a.W - a.ox;
-    }
-    const size_t tile_stride = static_cast<size_t>(a.H) * CCO;
-#pragma unroll 4
-    for (int i = tid; i < N; i += NT) {
-        const size_t off = static_cast<size_t>(i / CCO) * tile_stride + (i % CCO);
-#pragma unroll
-        for (int rr = 0; rr < RB; ++rr) smem[fft::pidx(i * RB + rr)] = ok[rr] ? src[rr][off] : make_float2(0.f, 0.f);
-    }
-    __syncthreads();
-    sfft::run<N, RB, NT, +1>(smem, tw, tid, RAD{});
+    const int rho = blockIdx.x * RB + tid % RB;
+    const bool ok = rho < nrows;
+    const int pc = rho / a.H, y = rho - pc * a.H;
+    const float2* src = a.in + (static_cast<size_t>(pc) * a.ntiles * a.H + y) * CCO;
+    float2* dst = a.out + static_cast<size_t>(rho) * a.W - a.ox;  // dst[i], i in [ox, ox + W)
+    const size_t ts = static_cast<size_t>(a.H) * CCO;
     const float sc = a.scale;
-#pragma unroll 4
-    for (int i = a.ox + tid; i < a.ox + a.W; i += NT) {
-#pragma unroll
-        for (int rr = 0; rr < RB; ++rr) {
-            if (!ok[rr]) continue;
-            const float2 v = smem[fft::pidx(i * RB + rr)];
-            dst[rr][i] = make_float2(v.x * sc, v.y * sc);
-        }
-    }
+    sfft::run<N, RB, NT, +1, sfft::Full, sfft::Half>(
+        smem, tw, tid, RAD{},
+        sfft::in_fn([&](int i, int) {
+            return ok ? src[static_cast<size_t>(i / CCO) * ts + (i % CCO)] : make_float2(0.f, 0.f);
+        }),
+        sfft::out_fn([&](int i, int, float2 v) {
+            if (ok) dst[i] = make_float2(v.x * sc, v.y * sc);
+        }));
 }
 
-template <int N, int CC, int NT>
-__device__ __forceinline__ void load_tile(float2* A, const float2* __restrict__ src, int H, int oy) {
-    for (int e = threadIdx.x; e < N * CC; e += NT) {
-        const int i = e / CC, y = i - oy;
-        A[fft::pidx(e)] = (y >= 0 && y < H) ? src[static_cast<size_t>(y) * CC + (e - i * CC)] : make_float2(0.f, 0.f);
-    }
+// Column kernels: one CTA per CC-column tile of one channel.  The forward FFT
+// reads the H live rows of the tile straight from T1, its last stage applies
+// H(kx, ky) in registers, and the inverse's last stage writes only the H
+// cropped rows to T2.  A thread always serves column cc = tid % CC.
+template <int N, int CC, int NT, bool CONJ, class RAD>
+__device__ __forceinline__ void col_single(const ColArgs& a, const float2* __restrict__ tw, int plane_in,
+                                           int plane_out) {
+    static_assert(NT % CC == 0, "column of a thread must be fixed");
+    extern __shared__ float2 smem[];
+    const int tile = blockIdx.x, c = blockIdx.y, tid = threadIdx.x;
+    const size_t tile_elems = static_cast<size_t>(a.H) * CC;
+    const size_t shift = static_cast<size_t>(a.oy) * CC;
+    const float2* src = a.in + (static_cast<size_t>(plane_in) * a.ntiles + tile) * tile_elems - shift;
+    float2* dst = a.out + (static_cast<size_t>(plane_out) * a.ntiles + tile) * tile_elems - shift;
+    const TfConst t = a.tf[c];
+    const int mx = wrapped(tile * CC + tid % CC, a.Px);
+    sfft::run<N, CC, NT, -1, sfft::Half, sfft::Full>(
+        smem, tw, tid, RAD{}, sfft::in_fn([&](int i, int cc) { return src[i * CC + cc]; }),
+        sfft::out_smem(smem, [&](int i, int, float2 v, float2& slot) {
+            slot = cmul(v, transfer_fast<CONJ>(t, mx, wrapped(i, N)));
+        }));
+    sfft::run<N, CC, NT, +1, sfft::Full, sfft::Half>(
+        smem, tw, tid, RAD{}, sfft::in_smem(smem),
+        sfft::out_fn([&](int i, int cc, float2 v) { dst[i * CC + cc] = v; }));
 }
 
-template <int N, int CC, int NT>
-__device__ __forceinline__ void store_tile(float2* __restrict__ dst, const float2* A, int H, int oy) {
-    for (int e = threadIdx.x; e < H * CC; e += NT) dst[e] = A[fft::pidx(e + oy * CC)];
-}
-
-template <bool CONJ, int N, int CC, int NT>
-__device__ __forceinline__ void apply_transfer(float2* dst, const float2* src, const TfConst& t, int tile, int Px,
-                                               bool accumulate) {
-    for (int e = threadIdx.x; e < N * CC; e += NT) {
-        const int ky = e / CC, kx = tile * CC + (e - ky * CC);
-        const float2 v = cmul(src[fft::pidx(e)], transfer_fast<CONJ>(t, wrapped(kx, Px), wrapped(ky, N)));
-        dst[fft::pidx(e)] = accumulate ? cadd(dst[fft::pidx(e)], v) : v;
-    }
-}
-
-// Single plane (the benchmark case): no loops around the FFTs.
+// Single plane (the benchmark case).
 template <int N, int CC, int NT, class RAD>
 __global__ void __launch_bounds__(NT, 2) scols_fwd1_kernel(ColArgs a, const float2* __restrict__ tw) {
-    extern __shared__ float2 smem[];
-    const int tile = blockIdx.x, c = blockIdx.y;
-    const size_t tile_elems = static_cast<size_t>(a.H) * CC;
-    load_tile<N, CC, NT>(smem, a.in + (static_cast<size_t>(c) * a.ntiles + tile) * tile_elems, a.H, a.oy);
-    __syncthreads();
-    sfft::run<N, CC, NT, -1>(smem, tw, threadIdx.x, RAD{});
-    apply_transfer<false, N, CC, NT>(smem, smem, a.tf[c], tile, a.Px, false);
-    __syncthreads();
-    sfft::run<N, CC, NT, +1>(smem, tw, threadIdx.x, RAD{});
-    store_tile<N, CC, NT>(a.out + (static_cast<size_t>(c) * a.ntiles + tile) * tile_elems, smem, a.H, a.oy);
+    col_single<N, CC, NT, false, RAD>(a, tw, blockIdx.y, blockIdx.y);
 }
 
 template <int N, int CC, int NT, class RAD>
 __global__ void __launch_bounds__(NT, 2) scols_bwd1_kernel(ColArgs a, const float2* __restrict__ tw) {
-    extern __shared__ float2 smem[];
-    const int tile = blockIdx.x, c = blockIdx.y;
-    const size_t tile_elems = static_cast<size_t>(a.H) * CC;
-    load_tile<N, CC, NT>(smem, a.in + (static_cast<size_t>(c) * a.ntiles + tile) * tile_elems, a.H, a.oy);
-    __syncthreads();
-    sfft::run<N, CC, NT, -1>(smem, tw, threadIdx.x, RAD{});
-    apply_transfer<true, N, CC, NT>(smem, smem, a.tf[c], tile, a.Px, false);
-    __syncthreads();
-    sfft::run<N, CC, NT, +1>(smem, tw, threadIdx.x, RAD{});
-    store_tile<N, CC, NT>(a.out + (static_cast<size_t>(c) * a.ntiles + tile) * tile_elems, smem, a.H, a.oy);
+    col_single<N, CC, NT, true, RAD>(a, tw, blockIdx.y, blockIdx.y);
 }
 
 // Multi-plane: one forward FFT per tile shared by all planes (spectrum kept in
-// a second shared buffer); the adjoint sums the planes' spectra before one
-// inverse FFT (propagation.cpp:240-294).
+// a second shared buffer; each plane's inverse reads it through H_l); the
+// adjoint accumulates every plane's conj(H_l)-weighted spectrum straight from
+// its FFT's last stage before one inverse FFT (propagation.cpp:240-294).
 template <int N, int CC, int NT, class RAD>
 __global__ void __launch_bounds__(NT, 2) scols_fwdL_kernel(ColArgs a, const float2* __restrict__ tw) {
+    static_assert(NT % CC == 0, "column of a thread must be fixed");
     extern __shared__ float2 smem[];
     float2* A = smem;
     float2* Sp = smem + fft::padded_len(N * CC);
-    const int tile = blockIdx.x, c = blockIdx.y;
+    const int tile = blockIdx.x, c = blockIdx.y, tid = threadIdx.x;
     const size_t tile_elems = static_cast<size_t>(a.H) * CC;
-    load_tile<N, CC, NT>(Sp, a.in + (static_cast<size_t>(c) * a.ntiles + tile) * tile_elems, a.H, a.oy);
-    __syncthreads();
-    sfft::run<N, CC, NT, -1>(Sp, tw, threadIdx.x, RAD{});
+    const size_t shift = static_cast<size_t>(a.oy) * CC;
+    const float2* src = a.in + (static_cast<size_t>(c) * a.ntiles + tile) * tile_elems - shift;
+    const int mx = wrapped(tile * CC + tid % CC, a.Px);
+    sfft::run<N, CC, NT, -1, sfft::Half, sfft::Full>(
+        Sp, tw, tid, RAD{}, sfft::in_fn([&](int i, int cc) { return src[i * CC + cc]; }), sfft::out_smem(Sp));
 #pragma unroll 1
     for (int l = 0; l < a.L; ++l) {
-        apply_transfer<false, N, CC, NT>(A, Sp, a.tf[l * a.C + c], tile, a.Px, false);
-        __syncthreads();
-        sfft::run<N, CC, NT, +1>(A, tw, threadIdx.x, RAD{});
-        store_tile<N, CC, NT>(a.out + ((static_cast<size_t>(l) * a.C + c) * a.ntiles + tile) * tile_elems, A,
-                              a.H, a.oy);
-        __syncthreads();
+        const TfConst t = a.tf[l * a.C + c];
+        float2* dst = a.out + ((static_cast<size_t>(l) * a.C + c) * a.ntiles + tile) * tile_elems - shift;
+        sfft::run<N, CC, NT, +1, sfft::Full, sfft::Half>(
+            A, tw, tid, RAD{},
+            sfft::in_smem(Sp, [&](int i, int, float2 v) { return cmul(v, transfer_fast<false>(t, mx, wrapped(i, N))); }),
+            sfft::out_fn([&](int i, int cc, float2 v) { dst[i * CC + cc] = v; }));
     }
 }
 
 template <int N, int CC, int NT, class RAD>
 __global__ void __launch_bounds__(NT, 2) scols_bwdL_kernel(ColArgs a, const float2* __restrict__ tw) {
+    static_assert(NT % CC == 0, "column of a thread must be fixed");
     extern __shared__ float2 smem[];
     float2* A = smem;
     float2* Z = smem + fft::padded_len(N * CC);
-    const int tile = blockIdx.x, c = blockIdx.y;
+    const int tile = blockIdx.x, c = blockIdx.y, tid = threadIdx.x;
     const size_t tile_elems = static_cast<size_t>(a.H) * CC;
+    const size_t shift = static_cast<size_t>(a.oy) * CC;
+    const int mx = wrapped(tile * CC + tid % CC, a.Px);
 #pragma unroll 1
     for (int l = 0; l < a.L; ++l) {
-        load_tile<N, CC, NT>(A, a.in + ((static_cast<size_t>(l) * a.C + c) * a.ntiles + tile) * tile_elems, a.H,
-                             a.oy);
-        __syncthreads();
-        sfft::run<N, CC, NT, -1>(A, tw, threadIdx.x, RAD{});
-        apply_transfer<true, N, CC, NT>(Z, A, a.tf[l * a.C + c], tile, a.Px, l > 0);
-        __syncthreads();
+        const TfConst t = a.tf[l * a.C + c];
+        const float2* src = a.in + ((static_cast<size_t>(l) * a.C + c) * a.ntiles + tile) * tile_elems - shift;
+        const bool first = l == 0;
+        sfft::run<N, CC, NT, -1, sfft::Half, sfft::Full>(
+            A, tw, tid, RAD{}, sfft::in_fn([&](int i, int cc) { return src[i * CC + cc]; }),
+            sfft::out_smem(Z, [&](int i, int, float2 v, float2& slot) {
+                const float2 w = cmul(v, transfer_fast<true>(t, mx, wrapped(i, N)));
+                slot = first ? w : cadd(slot, w);
+            }));
     }
-    sfft::run<N, CC, NT, +1>(Z, tw, threadIdx.x, RAD{});
-    store_tile<N, CC, NT>(a.out + (static_cast<size_t>(c) * a.ntiles + tile) * tile_elems, Z, a.H, a.oy);
+    float2* dst = a.out + (static_cast<size_t>(c) * a.ntiles + tile) * tile_elems - shift;
+    sfft::run<N, CC, NT, +1, sfft::Full, sfft::Half>(
+        Z, tw, tid, RAD{}, sfft::in_smem(Z), sfft::out_fn([&](int i, int cc, float2 v) { dst[i * CC + cc] = v; }));
 }
 
 // ---- plan table -------------------------------------------------------------------------------
@@ -260,12 +229,12 @@ struct Plans {
 
 const std::vector<Plans>& plans() {
     static const std::vector<Plans> p = {
-        {3840, 2160, 4, row_plan<3840, 1, 256, 4, Radices<16, 16, 15>>(),
-         col_plan<2160, 4, 736, Radices<12, 12, 15>>()},
+        {3840, 2160, 4, row_plan<3840, 1, 256, 4, Radices<16, 15, 16>>(),
+         col_plan<2160, 4, 720, Radices<12, 15, 12>>()},
         {512, 512, 4, row_plan<512, 1, 64, 4, Radices<8, 8, 8>>(), col_plan<512, 4, 128, Radices<8, 8, 8>>()},
         {512, 320, 4, row_plan<512, 1, 64, 4, Radices<8, 8, 8>>(), col_plan<320, 4, 128, Radices<16, 20>>()},
-        {7680, 4320, 2, row_plan<7680, 2, 512, 2, Radices<16, 16, 30>>(),
-         col_plan<4320, 2, 576, Radices<16, 18, 15>>()},
+        {7680, 4320, 2, row_plan<7680, 2, 512, 2, Radices<16, 30, 16>>(),
+         col_plan<4320, 2, 360, Radices<12, 30, 12>>()},
     };
     return p;
 }
@@ -304,7 +273,8 @@ size_t cols_smem(const Plans& p, int L) {
 
 }  // namespace
 
-bool static_plan_cc(int Px, int Py, int L, int* cc) {
+bool static_plan_cc(int Px, int Py, int pad, int L, int* cc) {
+    if (pad != 2 || Px % 4 != 0 || Py % 4 != 0) return false;  // pruned stages need offset = P / 4
     const Plans* p = find(Px, Py);
     if (!p) return false;
     if (cols_smem(*p, L) > 220 * 1024) return false;

@@ -198,6 +198,30 @@ def test_propagate_multi_static_plans(holo, ref, c, h, w, L):
     assert rel_l2(np.stack([b.real, b.imag]), np.stack(r)) <= FIELD_TOL
 
 
+@pytest.mark.parametrize("h,w,pad", [(512, 512, 1), (256, 256, 3)])
+def test_static_grid_sizes_with_other_pads(holo, ref, h, w, pad):
+    """A padded grid that has a compile-time plan but a pad factor other than 2
+    must take the generic kernels (the planned ones prune for offset = P/4)."""
+    hsp, rsp = spec_for(holo, ref, 1, pad)
+    re, im = field32(91 + pad, 1, h, w)
+    a = holo.propagate(holo.ComplexField(1, h, w, re, im), hsp, 3e-3)
+    b = ref.propagate(re, im, rsp, 3e-3)
+    assert rel_l2(np.stack([a.real, a.imag]), np.stack(b)) <= FIELD_TOL
+
+
+def test_propagate_4k_grid(holo, ref):
+    """cfg4 padded grid (4320 x 7680, the CC=2 plan) for one channel, fwd and adjoint."""
+    c, h, w = 1, 2160, 3840
+    hsp, rsp = spec_for(holo, ref, c, 2)
+    re, im = field32(78, c, h, w)
+    a = holo.propagate(holo.ComplexField(c, h, w, re, im), hsp, 3e-3)
+    b = ref.propagate(re, im, rsp, 3e-3)
+    assert rel_l2(np.stack([a.real, a.imag]), np.stack(b)) <= FIELD_TOL
+    a = holo.propagate_backward(holo.ComplexField(c, h, w, re, im), hsp, 3e-3)
+    b = ref.propagate(re, im, rsp, 3e-3, mode=2)
+    assert rel_l2(np.stack([a.real, a.imag]), np.stack(b)) <= FIELD_TOL
+
+
 def test_propagate_cfg2_grid(holo, ref):
     """Full cfg2 padded grid (2160 x 3840) for one channel vs the reference."""
     c, h, w = 1, 1080, 1920
