@@ -13,6 +13,7 @@
 //    512 x  512, CC 4   cfg1 (256x256, pad 2)
 //    512 x  320, CC 4   desk regression (256x160, pad 2)
 //   7680 x 4320, CC 2   cfg4 (3840x2160, pad 2)
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -128,13 +129,13 @@ __device__ __forceinline__ void col_single(const ColArgs& a, const float2* __res
 }
 
 // Single plane (the benchmark case).
-template <int N, int CC, int NT, class RAD>
-__global__ void __launch_bounds__(NT, 2) scols_fwd1_kernel(ColArgs a, const float2* __restrict__ tw) {
+template <int N, int CC, int NT, int MINB, class RAD>
+__global__ void __launch_bounds__(NT, MINB) scols_fwd1_kernel(ColArgs a, const float2* __restrict__ tw) {
     col_single<N, CC, NT, false, RAD>(a, tw, blockIdx.y, blockIdx.y);
 }
 
-template <int N, int CC, int NT, class RAD>
-__global__ void __launch_bounds__(NT, 2) scols_bwd1_kernel(ColArgs a, const float2* __restrict__ tw) {
+template <int N, int CC, int NT, int MINB, class RAD>
+__global__ void __launch_bounds__(NT, MINB) scols_bwd1_kernel(ColArgs a, const float2* __restrict__ tw) {
     col_single<N, CC, NT, true, RAD>(a, tw, blockIdx.y, blockIdx.y);
 }
 
@@ -142,8 +143,8 @@ __global__ void __launch_bounds__(NT, 2) scols_bwd1_kernel(ColArgs a, const floa
 // a second shared buffer; each plane's inverse reads it through H_l); the
 // adjoint accumulates every plane's conj(H_l)-weighted spectrum straight from
 // its FFT's last stage before one inverse FFT (propagation.cpp:240-294).
-template <int N, int CC, int NT, class RAD>
-__global__ void __launch_bounds__(NT, 2) scols_fwdL_kernel(ColArgs a, const float2* __restrict__ tw) {
+template <int N, int CC, int NT, int MINB, class RAD>
+__global__ void __launch_bounds__(NT, MINB) scols_fwdL_kernel(ColArgs a, const float2* __restrict__ tw) {
     static_assert(NT % CC == 0, "column of a thread must be fixed");
     extern __shared__ float2 smem[];
     float2* A = smem;
@@ -166,8 +167,8 @@ __global__ void __launch_bounds__(NT, 2) scols_fwdL_kernel(ColArgs a, const floa
     }
 }
 
-template <int N, int CC, int NT, class RAD>
-__global__ void __launch_bounds__(NT, 2) scols_bwdL_kernel(ColArgs a, const float2* __restrict__ tw) {
+template <int N, int CC, int NT, int MINB, class RAD>
+__global__ void __launch_bounds__(NT, MINB) scols_bwdL_kernel(ColArgs a, const float2* __restrict__ tw) {
     static_assert(NT % CC == 0, "column of a thread must be fixed");
     extern __shared__ float2 smem[];
     float2* A = smem;
@@ -214,10 +215,10 @@ RowPlan row_plan() {
     return RowPlan{srows_fwd_kernel<N, RB, NT, CCO, RAD>, srows_inv_kernel<N, RB, NT, CCO, RAD>, NT, RB,
                    [](int n) { return sfft::twiddle_table(n, RAD{}); }};
 }
-template <int N, int CC, int NT, class RAD>
+template <int N, int CC, int NT, int MINB, class RAD>
 ColPlan col_plan() {
-    return ColPlan{scols_fwd1_kernel<N, CC, NT, RAD>, scols_bwd1_kernel<N, CC, NT, RAD>,
-                   scols_fwdL_kernel<N, CC, NT, RAD>, scols_bwdL_kernel<N, CC, NT, RAD>, NT, CC,
+    return ColPlan{scols_fwd1_kernel<N, CC, NT, MINB, RAD>, scols_bwd1_kernel<N, CC, NT, MINB, RAD>,
+                   scols_fwdL_kernel<N, CC, NT, MINB, RAD>, scols_bwdL_kernel<N, CC, NT, MINB, RAD>, NT, CC,
                    [](int n) { return sfft::twiddle_table(n, RAD{}); }};
 }
 
@@ -230,19 +231,39 @@ struct Plans {
 const std::vector<Plans>& plans() {
     static const std::vector<Plans> p = {
         {3840, 2160, 4, row_plan<3840, 1, 256, 4, Radices<16, 15, 16>>(),
-         col_plan<2160, 4, 720, Radices<12, 15, 12>>()},
-        {512, 512, 4, row_plan<512, 1, 64, 4, Radices<8, 8, 8>>(), col_plan<512, 4, 128, Radices<8, 8, 8>>()},
-        {512, 320, 4, row_plan<512, 1, 64, 4, Radices<8, 8, 8>>(), col_plan<320, 4, 128, Radices<16, 20>>()},
+         col_plan<2160, 4, 720, 2, Radices<12, 15, 12>>()},
+        {512, 512, 4, row_plan<512, 1, 64, 4, Radices<8, 8, 8>>(), col_plan<512, 4, 128, 2, Radices<8, 8, 8>>()},
+        {512, 320, 4, row_plan<512, 1, 64, 4, Radices<8, 8, 8>>(), col_plan<320, 4, 128, 2, Radices<16, 20>>()},
         {7680, 4320, 2, row_plan<7680, 2, 512, 2, Radices<16, 30, 16>>(),
-         col_plan<4320, 2, 360, Radices<12, 30, 12>>()},
+         col_plan<4320, 2, 360, 2, Radices<12, 30, 12>>()},
+        // tuning variants of the cfg2 grid (HS_FFT_VARIANT=k picks the k-th plan of a grid)
+        {3840, 2160, 2, row_plan<3840, 1, 256, 2, Radices<16, 15, 16>>(),
+         col_plan<2160, 2, 360, 4, Radices<12, 15, 12>>()},
+        {3840, 2160, 4, row_plan<3840, 1, 128, 4, Radices<16, 15, 16>>(),
+         col_plan<2160, 4, 360, 3, Radices<12, 15, 12>>()},
+        {3840, 2160, 4, row_plan<3840, 2, 256, 4, Radices<16, 15, 16>>(),
+         col_plan<2160, 4, 720, 2, Radices<12, 15, 12>>()},
     };
     return p;
 }
 
+int variant() {
+    static const int v = [] {
+        const char* e = std::getenv("HS_FFT_VARIANT");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+
 const Plans* find(int Px, int Py) {
-    for (const auto& p : plans())
-        if (p.Px == Px && p.Py == Py) return &p;
-    return nullptr;
+    const Plans* first = nullptr;
+    int k = 0;
+    for (const auto& p : plans()) {
+        if (p.Px != Px || p.Py != Py) continue;
+        if (!first) first = &p;
+        if (k++ == variant()) return &p;
+    }
+    return first;
 }
 
 struct STwCache {

@@ -5,16 +5,22 @@
 // :135-152), loss_ssim_grad :361-383, training_loss_grad :389-398,
 // loss_mse_grad :277-294; proj/core/src/optimizer.cpp:59-123 (cosine_lr, Adan).
 //
-// SSIM kernel: one CTA per 64x16 output tile of one (plane, channel).  It
-// loads I (= |U|^2 when fed the propagated field directly) and the target over
-// the tile plus a 10-pixel halo, computes the five 11-tap separable window
-// means on the valid grid, the SSIM map and its three partial-derivative maps
-// (g1, g2, g3 of ssim_channel), spreads them back with the transposed
-// correlation and combines grad = sp1 + 2 I sp2 + t sp3, all in shared memory.
-// The recon term (I - t)^2 (1 + M + t^2) and its gradient are fused in the
-// same epilogue; in trainer mode the epilogue writes dL/dU = 2 U dL/dI
-// (pipeline.cpp:265-274) directly.  Loss sums are per-CTA fp64 partials
-// reduced by one deterministic final block.
+// SSIM kernel (sliding window): one CTA of 128 threads owns a strip of 118
+// output columns and kSR output rows of one (plane, channel) and walks down
+// it row by row.  Thread t owns column c = x0 - 10 + t of both the valid
+// (H-10)x(W-10) grid and the output grid.  Per step it
+//   1. correlates its input row horizontally (I, I^2, I t from a shared row),
+//   2. keeps the last 11 such rows in a register ring and correlates them
+//      vertically -> window means of valid row v, SSIM map and the three
+//      derivative maps g1, g2, g3 (ssim_channel :187-205),
+//   3. spreads g back horizontally from a shared row of its 10 left
+//      neighbours, keeps the last 11 spread rows in a second register ring and
+//      spreads vertically -> dSSIM/dI of output row v (spread_t :135-152),
+//   4. fuses the recon term (I - t)^2 (1 + M + t^2) and, in trainer mode,
+//      dL/dU = 2 U dL/dI (pipeline.cpp:265-274).
+// Every input row is read once per strip (no vertical halo re-reads beyond
+// the 20-row pipeline fill per CTA); one barrier per row.  Loss sums are
+// per-CTA fp64 partials reduced by one deterministic final block.
 #include <cmath>
 
 #include <cub/block/block_reduce.cuh>
@@ -25,10 +31,13 @@ namespace hs {
 
 namespace {
 
-constexpr int kTW = 64, kTH = 16, kHalo = 10, kWin = 11;
-constexpr int kRW = kTW + 2 * kHalo, kRH = kTH + 2 * kHalo;  // loaded region
-constexpr int kVW = kTW + kHalo, kVH = kTH + kHalo;          // valid-grid region
-constexpr int kLossThreads = 256;
+constexpr int kWin = 11, kHalo = 10;
+constexpr int kSW = 128;            // threads per CTA = valid/output columns touched per strip
+constexpr int kSO = kSW - kHalo;    // output columns per strip
+constexpr int kSR = 101;            // output rows per CTA (kSR + 20 steps = 11 x 11-step ring cycles);
+                                    // 1080p x 3 channels -> 561 CTAs = one wave at 4 CTAs/SM
+constexpr int kSIn = kSW + kHalo;   // input columns per strip
+constexpr int kLossThreads = 256;   // elementwise kernels
 constexpr double kSsimC1 = 0.01 * 0.01, kSsimC2 = 0.03 * 0.03, kSsimWeight = 0.005;  // loss.hpp:12-14
 
 struct Win {
@@ -84,224 +93,269 @@ __global__ void ssim_target_stats_kernel(const float* __restrict__ target, int C
     }
 }
 
-struct SsimSmem {
-    float I[kRH][kRW];        // I over tile + halo
-    float T[kRH][kRW];        // target over tile + halo
-    float h[3][kRH][kVW];     // corr_x of I, I^2, I*t; reused for the vertical spreads
-    float gm[3][kVH][kVW];    // g1, g2, g3 on the valid grid
-    float2 ts[kVH][kVW];      // target window stats (mu2, sigma2^2) on the valid grid
+// 11-tap correlation with the symmetric window: sum_j g[j] f(j).
+// (two interleaved FMA chains: short dependency chains for the latency-bound SSIM kernel)
+template <class F>
+__device__ __forceinline__ float corr11(const Win& w, F f) {
+    float a = w.g[5] * f(5);
+    float b = w.g[1] * (f(1) + f(9));
+    a = fmaf(w.g[0], f(0) + f(10), a);
+    b = fmaf(w.g[3], f(3) + f(7), b);
+    a = fmaf(w.g[2], f(2) + f(8), a);
+    a = fmaf(w.g[4], f(4) + f(6), a);
+    return a + b;
+}
+
+// Three 11-tap correlations at once from a loader f(j) -> float4 (x, y, z used),
+// loading the symmetric pairs progressively (few live registers).
+template <class F>
+__device__ __forceinline__ void corr11x3(const Win& w, F f, float& a0, float& a1, float& a2) {
+    const float4 m = f(5);
+    a0 = w.g[5] * m.x;
+    a1 = w.g[5] * m.y;
+    a2 = w.g[5] * m.z;
+    float b0 = 0.f, b1 = 0.f, b2 = 0.f;
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+        const float4 p = f(j), q = f(10 - j);
+        if (j & 1) {
+            b0 = fmaf(w.g[j], p.x + q.x, b0);
+            b1 = fmaf(w.g[j], p.y + q.y, b1);
+            b2 = fmaf(w.g[j], p.z + q.z, b2);
+        } else {
+            a0 = fmaf(w.g[j], p.x + q.x, a0);
+            a1 = fmaf(w.g[j], p.y + q.y, a1);
+            a2 = fmaf(w.g[j], p.z + q.z, a2);
+        }
+    }
+    a0 += b0;
+    a1 += b1;
+    a2 += b2;
+}
+
+struct SsimState {
+    float h0[kWin], h1[kWin], h2[kWin];  // horizontal correlations of I, I^2, I t (ring by row)
+    float s0[kWin], s1[kWin], s2[kWin];  // horizontal spreads of g1, g2, g3 (ring by valid row)
+    double ssum, rsum;
 };
 
-// Work split of the 256 threads (register-blocked separable correlations):
-constexpr int kHB = 11;  // corr_x: 36 rows x 7 runs of 11 outputs      = 252 items
-constexpr int kVB = 9;   // corr_y: 74 cols x 3 runs of 9 valid rows    = 222 items
-constexpr int kSX = 4;   // spread_x: 16 rows x 16 runs of 4 outputs    = 256 items
+// Asynchronous global->shared copies (cp.async); src_bytes = 0 zero-fills.
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, bool ok) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(ok ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src, bool ok) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(ok ? 4 : 0));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+constexpr int kRaw = 16;  // ring of raw input rows (U or I, and t): covers rows r-12 .. r+3
+constexpr int kPD = 3;    // prefetch distance (rows) of the cp.async pipeline
+constexpr int kTsRing = 4;
+
+struct SsimSmem {
+    float2 rawU[kRaw][kSIn];    // U (or I in .x when the loss gets intensities)
+    float rawT[kRaw][kSIn];     // target
+    float2 ts[kTsRing][kSW];    // target window stats of the valid row
+    float4 in[2][kSIn];         // (I, I^2, I t, -) of the row being correlated
+    float4 gm[2][kSW];          // (g1, g2, g3, -) of the valid row being spread
+};
 
 template <bool FROM_FIELD>
-__global__ void __launch_bounds__(kLossThreads, 2) ssim_loss_kernel(LossArgs a, Win win) {
+struct SsimCta {
+    const LossArgs& a;
+    const Win& win;
+    SsimSmem& S;
+    int t, x0, y0, c, H, W, vh, vw, kind;
+    size_t plane_off;
+    const float* tgt;
+    const float2* tst;
+    const uint8_t* mask;
+    float wr, ws;
+
+    // cp.async of input row r (own column, plus the right halo for t < 10)
+    // and of the target statistics of valid row v; one commit group.
+    __device__ __forceinline__ void issue(int r, int v) const {
+        const bool rok = r >= 0 && r < H;
+        const int rs = min(max(r, 0), H - 1);
+        const int slot = (r + 4 * kRaw) % kRaw;
+        const size_t rowp = static_cast<size_t>(rs) * W;
+        const int xa = x0 - kHalo + t, xb = x0 + kSO + t;
+        const bool oka = rok && xa >= 0 && xa < W;
+        const size_t pa = rowp + min(max(xa, 0), W - 1);
+        if (FROM_FIELD) cp_async8(&S.rawU[slot][t], a.field + plane_off + pa, oka);
+        else cp_async4(&S.rawU[slot][t], a.recon + plane_off + pa, oka);
+        cp_async4(&S.rawT[slot][t], tgt + pa, oka);
+        if (t < kHalo) {
+            const bool okb = rok && xb < W;
+            const size_t pb = rowp + min(xb, W - 1);
+            if (FROM_FIELD) cp_async8(&S.rawU[slot][kSW + t], a.field + plane_off + pb, okb);
+            else cp_async4(&S.rawU[slot][kSW + t], a.recon + plane_off + pb, okb);
+            cp_async4(&S.rawT[slot][kSW + t], tgt + pb, okb);
+        }
+        const bool vok = v >= 0 && v < vh && c >= 0 && c < vw;
+        const size_t pv = static_cast<size_t>(min(max(v, 0), vh - 1)) * vw + min(max(c, 0), vw - 1);
+        cp_async8(&S.ts[(v + 4 * kTsRing) % kTsRing][t], tst + pv, vok);
+        cp_commit();
+    }
+    __device__ __forceinline__ float intensity(float2 u) const { return FROM_FIELD ? u.x * u.x + u.y * u.y : u.x; }
+    // (I, I^2, I t) of raw row r -> the correlation row buffer (own columns only)
+    __device__ __forceinline__ void convert(int r, int buf) const {
+        const int slot = (r + 4 * kRaw) % kRaw;
+        {
+            const float i = intensity(S.rawU[slot][t]), tv = S.rawT[slot][t];
+            S.in[buf][t] = make_float4(i, i * i, i * tv, 0.f);
+        }
+        if (t < kHalo) {
+            const float i = intensity(S.rawU[slot][kSW + t]), tv = S.rawT[slot][kSW + t];
+            S.in[buf][kSW + t] = make_float4(i, i * i, i * tv, 0.f);
+        }
+    }
+
+    // One row step s (valid row v = y0 - 20 + s), ring slot U = s mod 11.
+    template <int U>
+    __device__ __forceinline__ void step(SsimState& st, int s, float& mk_next) const {
+        const int v = y0 - 2 * kHalo + s;
+        const int r = v + kHalo;  // input row correlated horizontally this step
+        const int buf = s & 1;
+        issue(r + kPD, v + kPD);
+        const int y = v, x = c;
+        const bool out_ok = t >= kHalo && y >= y0 && y < y0 + kSR && y < H && x < W;
+        const float mk = mk_next;
+        if (kind == kLossTraining) {  // mask of the next step's output row, one step ahead
+            const int yn = y + 1;
+            mk_next = (t >= kHalo && yn >= y0 && yn < y0 + kSR && yn < H && x < W)
+                          ? (mask[static_cast<size_t>(yn) * W + x] ? 1.f : 0.f) : 0.f;
+        }
+        // 1. horizontal correlation of input row r (ssim_channel corr_x, loss.cpp:103-111)
+        {
+            const float4* row = &S.in[buf][t];
+            corr11x3(win, [&](int j) { return row[j]; }, st.h0[U], st.h1[U], st.h2[U]);
+        }
+        // 2. vertical correlation of rows v..v+10 + SSIM map and derivative maps
+        cp_wait<kPD - 1>();  // groups of rows <= r + 1 (and stats of v) have landed
+        float4 gv = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (v >= 0 && v < vh && c >= 0 && c < vw) {
+            const float m1 = corr11(win, [&](int i) { return st.h0[(U + 1 + i) % kWin]; });
+            const float exx = corr11(win, [&](int i) { return st.h1[(U + 1 + i) % kWin]; });
+            const float exy = corr11(win, [&](int i) { return st.h2[(U + 1 + i) % kWin]; });
+            const float2 ts = S.ts[(v + 4 * kTsRing) % kTsRing][t];
+            const float C1 = static_cast<float>(kSsimC1), C2 = static_cast<float>(kSsimC2);
+            const float m2 = ts.x;
+            const float s12 = exy - m1 * m2;
+            const float s11 = exx - m1 * m1;
+            const float a1 = 2.f * m1 * m2 + C1;
+            const float a2 = 2.f * s12 + C2;
+            const float b1 = m1 * m1 + m2 * m2 + C1;
+            const float b2 = s11 + ts.y + C2;
+            // s/a1, s/a2 evaluated as a2/(b1 b2), a1/(b1 b2): equal where
+            // ssim_channel's form is defined and finite when a2 rounds to 0
+            // in fp32 (a 0/0 there would poison the field via the FFT).
+            const float inv = 1.f / (b1 * b2);
+            const float sv = a1 * a2 * inv;
+            if (t >= kHalo && v >= y0 && v < y0 + kSR) st.ssum += static_cast<double>(sv);
+            gv.x = a2 * inv * 2.f * m2 - (sv / b1) * 2.f * m1 + (sv / b2) * 2.f * m1 - a1 * inv * 2.f * m2;
+            gv.y = -sv / b2;
+            gv.z = 2.f * a1 * inv;
+        }
+        S.gm[buf][t] = gv;
+        convert(r + 1, buf ^ 1);
+        __syncthreads();
+        // 3. horizontal spread of g over valid columns c-10..c, then vertical
+        //    spread over valid rows v-10..v (spread_t, loss.cpp:135-152)
+        {
+            // threads t < 10 own no output column: their spread row stays 0
+            const float4* gr = &S.gm[buf][max(t, kHalo)];
+            corr11x3(win, [&](int j) { return gr[-j]; }, st.s0[U], st.s1[U], st.s2[U]);
+            if (t < kHalo) st.s0[U] = st.s1[U] = st.s2[U] = 0.f;
+        }
+        if (out_ok) {
+            const float G1 = corr11(win, [&](int i) { return st.s0[(U + kWin - i) % kWin]; });
+            const float G2 = corr11(win, [&](int i) { return st.s1[(U + kWin - i) % kWin]; });
+            const float G3 = corr11(win, [&](int i) { return st.s2[(U + kWin - i) % kWin]; });
+            const int slot = (y + 4 * kRaw) % kRaw;
+            const float2 uu = S.rawU[slot][t];
+            const float tv = S.rawT[slot][t];
+            const float iv = intensity(uu);
+            const float gs = G1 + 2.f * iv * G2 + tv * G3;  // loss.cpp:211
+            float g = ws * gs;
+            if (kind == kLossTraining) {  // loss_recon_grad, loss.cpp:317-341
+                const float d = iv - tv;
+                const float k = 1.f + mk + tv * tv;
+                st.rsum += static_cast<double>(d * d * k);
+                g = fmaf(wr * d, k, g);
+            }
+            const size_t p = plane_off + static_cast<size_t>(y) * W + x;
+            if (a.grad) a.grad[p] = g;
+            if (a.du) a.du[p] = make_float2(2.f * uu.x * g, 2.f * uu.y * g);
+        }
+    }
+};
+
+template <bool FROM_FIELD>
+__global__ void __launch_bounds__(kSW, 4) ssim_loss_kernel(LossArgs a, Win win) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SsimSmem& S = *reinterpret_cast<SsimSmem*>(smem_raw);
     const int plane = blockIdx.z;  // l * C + c
-    const int l = plane / a.C, c = plane - l * a.C;
-    const int x0 = blockIdx.x * kTW, y0 = blockIdx.y * kTH;
-    const int H = a.H, W = a.W;
-    const int vh = H - kWin + 1, vw = W - kWin + 1;
-    const size_t plane_off = static_cast<size_t>(plane) * H * W;
-    const float* tgt = a.target + static_cast<size_t>(c) * H * W;
-    const float2* tst = a.tstats + static_cast<size_t>(c) * vh * vw;
-    const uint8_t* mask = a.masks + static_cast<size_t>(a.plane0 + l) * H * W;
-    const int tid = threadIdx.x;
+    const int l = plane / a.C, ch = plane - l * a.C;
+    SsimCta<FROM_FIELD> K{a, win, S};
+    K.t = threadIdx.x;
+    K.x0 = blockIdx.x * kSO;
+    K.y0 = blockIdx.y * kSR;
+    K.c = K.x0 - kHalo + K.t;
+    K.H = a.H;
+    K.W = a.W;
+    K.vh = a.H - kWin + 1;
+    K.vw = a.W - kWin + 1;
+    K.kind = a.kind;
+    K.plane_off = static_cast<size_t>(plane) * a.H * a.W;
+    K.tgt = a.target + static_cast<size_t>(ch) * a.H * a.W;
+    K.tst = a.tstats + static_cast<size_t>(ch) * K.vh * K.vw;
+    K.mask = a.masks + static_cast<size_t>(a.plane0 + l) * a.H * a.W;
+    const double n_el = static_cast<double>(a.C) * a.H * a.W;
+    K.wr = static_cast<float>(2.0 / (n_el * a.L_norm));
+    const double count = static_cast<double>(a.L_norm) * a.C * K.vh * K.vw;
+    K.ws = static_cast<float>((a.kind == kLossTraining ? kSsimWeight : 1.0) * (-1.0 / count));
 
-    {  // all global loads of this thread in flight at once, then the smem stores
-        constexpr int kLoads = (kRH * kRW + kLossThreads - 1) / kLossThreads;
-        float iv[kLoads], tv[kLoads];
+    SsimState st;
 #pragma unroll
-        for (int q = 0; q < kLoads; ++q) {
-            const int e = tid + q * kLossThreads;
-            const int ry = e / kRW, rx = e - ry * kRW;
-            const int y = y0 - kHalo + ry, x = x0 - kHalo + rx;
-            iv[q] = 0.f;
-            tv[q] = 0.f;
-            if (e < kRH * kRW && y >= 0 && y < H && x >= 0 && x < W) {
-                const size_t p = static_cast<size_t>(y) * W + x;
-                iv[q] = load_I<FROM_FIELD>(a, plane_off + p);
-                tv[q] = tgt[p];
-            }
-        }
-        constexpr int kTs = (kVH * kVW + kLossThreads - 1) / kLossThreads;
-        float2 tsv[kTs];
+    for (int i = 0; i < kWin; ++i) st.h0[i] = st.h1[i] = st.h2[i] = st.s0[i] = st.s1[i] = st.s2[i] = 0.f;
+    st.ssum = st.rsum = 0.0;
+    // steps s = 0 .. kSteps-1 cover valid rows v = y0-20 .. y0+kSR-1 (output rows y0..y0+kSR-1);
+    // rows past the image are guarded inside the step
+    constexpr int kSteps = kSR + 2 * kHalo;
+    static_assert(kSteps % kWin == 0, "whole ring cycles");
+    const int r0 = K.y0 - kHalo, v0 = K.y0 - 2 * kHalo;
 #pragma unroll
-        for (int q = 0; q < kTs; ++q) {
-            const int e = tid + q * kLossThreads;
-            const int i = e / kVW, j = e - i * kVW;
-            const int vy = y0 - kHalo + i, vx = x0 - kHalo + j;
-            tsv[q] = (e < kVH * kVW && vy >= 0 && vy < vh && vx >= 0 && vx < vw)
-                         ? tst[static_cast<size_t>(vy) * vw + vx] : make_float2(0.f, 0.f);
-        }
-#pragma unroll
-        for (int q = 0; q < kLoads; ++q) {
-            const int e = tid + q * kLossThreads;
-            if (e < kRH * kRW) {
-                const int ry = e / kRW, rx = e - ry * kRW;
-                S.I[ry][rx] = iv[q];
-                S.T[ry][rx] = tv[q];
-            }
-        }
-#pragma unroll
-        for (int q = 0; q < kTs; ++q) {
-            const int e = tid + q * kLossThreads;
-            if (e < kVH * kVW) S.ts[e / kVW][e % kVW] = tsv[q];
-        }
-    }
+    for (int q = 0; q < kPD; ++q) K.issue(r0 + q, v0 + q);
+    cp_wait<kPD - 1>();
+    K.convert(r0, 0);
+    float mk_next = 0.f;  // first output row comes 20 steps in
     __syncthreads();
-    // corr_x (loss.cpp:103-111) of I, I^2, I*t: each item a run of kHB outputs
-    if (tid < kRH * 7) {
-        const int ry = tid / 7, j0 = (tid - ry * 7) * kHB;
-        float in_i[kHB + kWin - 1], in_t[kHB + kWin - 1];
-#pragma unroll
-        for (int q = 0; q < kHB + kWin - 1; ++q) {
-            const int j = min(j0 + q, kRW - 1);
-            in_i[q] = S.I[ry][j];
-            in_t[q] = S.T[ry][j];
-        }
-#pragma unroll
-        for (int o = 0; o < kHB; ++o) {
-            float s0 = 0.f, s1 = 0.f, s2 = 0.f;
-#pragma unroll
-            for (int k = 0; k < kWin; ++k) {
-                const float g = win.g[k], iv = in_i[o + k], tv = in_t[o + k];
-                s0 = fmaf(g, iv, s0);
-                s1 = fmaf(g, iv * iv, s1);
-                s2 = fmaf(g, iv * tv, s2);
-            }
-            if (j0 + o < kVW) {
-                S.h[0][ry][j0 + o] = s0;
-                S.h[1][ry][j0 + o] = s1;
-                S.h[2][ry][j0 + o] = s2;
-            }
-        }
+#pragma unroll 1
+    for (int sb = 0; sb < kSteps; sb += kWin) {
+        K.template step<0>(st, sb + 0, mk_next);
+        K.template step<1>(st, sb + 1, mk_next);
+        K.template step<2>(st, sb + 2, mk_next);
+        K.template step<3>(st, sb + 3, mk_next);
+        K.template step<4>(st, sb + 4, mk_next);
+        K.template step<5>(st, sb + 5, mk_next);
+        K.template step<6>(st, sb + 6, mk_next);
+        K.template step<7>(st, sb + 7, mk_next);
+        K.template step<8>(st, sb + 8, mk_next);
+        K.template step<9>(st, sb + 9, mk_next);
+        K.template step<10>(st, sb + 10, mk_next);
     }
-    __syncthreads();
-    // corr_y + SSIM map + derivative maps (ssim_channel :187-205)
-    double ssum = 0.0;
-    const float C1 = static_cast<float>(kSsimC1), C2 = static_cast<float>(kSsimC2);
-    if (tid < kVW * 3) {
-        const int j = tid % kVW, i0 = (tid / kVW) * kVB;
-        const int vx = x0 - kHalo + j;
-        float col0[kVB + kWin - 1], col1[kVB + kWin - 1], col2[kVB + kWin - 1];
-#pragma unroll
-        for (int q = 0; q < kVB + kWin - 1; ++q) {
-            const int i = min(i0 + q, kRH - 1);
-            col0[q] = S.h[0][i][j];
-            col1[q] = S.h[1][i][j];
-            col2[q] = S.h[2][i][j];
-        }
-#pragma unroll
-        for (int o = 0; o < kVB; ++o) {
-            const int i = i0 + o;
-            if (i >= kVH) break;
-            const int vy = y0 - kHalo + i;
-            float g1 = 0.f, g2 = 0.f, g3 = 0.f;
-            if (vy >= 0 && vy < vh && vx >= 0 && vx < vw) {
-                float m1 = 0.f, exx = 0.f, exy = 0.f;
-#pragma unroll
-                for (int k = 0; k < kWin; ++k) {
-                    const float g = win.g[k];
-                    m1 = fmaf(g, col0[o + k], m1);
-                    exx = fmaf(g, col1[o + k], exx);
-                    exy = fmaf(g, col2[o + k], exy);
-                }
-                const float2 ts = S.ts[i][j];
-                const float m2 = ts.x;
-                const float s12 = exy - m1 * m2;
-                const float s11 = exx - m1 * m1;
-                const float a1 = 2.f * m1 * m2 + C1;
-                const float a2 = 2.f * s12 + C2;
-                const float b1 = m1 * m1 + m2 * m2 + C1;
-                const float b2 = s11 + ts.y + C2;
-                // s/a1, s/a2 evaluated as a2/(b1 b2), a1/(b1 b2): equal where
-                // ssim_channel's form is defined and finite when a2 rounds to
-                // 0 in fp32 (a 0/0 there would poison the field via the FFT).
-                const float inv = 1.f / (b1 * b2);
-                const float s = a1 * a2 * inv;
-                if (vy >= y0 && vy < y0 + kTH && vx >= x0 && vx < x0 + kTW) ssum += s;
-                g1 = a2 * inv * 2.f * m2 - (s / b1) * 2.f * m1 + (s / b2) * 2.f * m1 - a1 * inv * 2.f * m2;
-                g2 = -s / b2;
-                g3 = 2.f * a1 * inv;
-            }
-            S.gm[0][i][j] = g1;
-            S.gm[1][i][j] = g2;
-            S.gm[2][i][j] = g3;
-        }
-    }
-    __syncthreads();
-    // spread_t vertical (:138-145): sv[y][vx] = sum_k g[k] gm[y - k][vx]; item = (col, map)
-    float(*sv)[kVW] = reinterpret_cast<float(*)[kVW]>(&S.h[0][0][0]);  // 3 x kTH x kVW
-    if (tid < kVW * 3) {
-        const int j = tid % kVW, m = tid / kVW;
-        float col[kVH];
-#pragma unroll
-        for (int q = 0; q < kVH; ++q) col[q] = S.gm[m][q][j];
-#pragma unroll
-        for (int oy = 0; oy < kTH; ++oy) {
-            float acc = 0.f;
-#pragma unroll
-            for (int k = 0; k < kWin; ++k) acc = fmaf(win.g[k], col[oy + kHalo - k], acc);
-            sv[m * kTH + oy][j] = acc;
-        }
-    }
-    __syncthreads();
-    // spread_t horizontal (:146-151) + combine (:211) + recon term + output
-    const int kind = a.kind;
-    const double n_el = static_cast<double>(a.C) * H * W;
-    const float wr = static_cast<float>(2.0 / (n_el * a.L_norm));
-    const double count = static_cast<double>(a.L_norm) * a.C * vh * vw;
-    const float ws = static_cast<float>((kind == kLossTraining ? kSsimWeight : 1.0) * (-1.0 / count));
-    double rsum = 0.0;
-    {
-        const int oy = tid / (kTW / kSX), ox0 = (tid - oy * (kTW / kSX)) * kSX;
-        float o[3][kSX];
-#pragma unroll
-        for (int m = 0; m < 3; ++m) {
-            float row[kSX + kWin - 1];
-#pragma unroll
-            for (int q = 0; q < kSX + kWin - 1; ++q) row[q] = sv[m * kTH + oy][ox0 + q];
-#pragma unroll
-            for (int u = 0; u < kSX; ++u) {
-                float acc = 0.f;
-#pragma unroll
-                for (int k = 0; k < kWin; ++k) acc = fmaf(win.g[k], row[u + kHalo - k], acc);
-                o[m][u] = acc;
-            }
-        }
-        const int y = y0 + oy;
-#pragma unroll
-        for (int u = 0; u < kSX; ++u) {
-            const int x = x0 + ox0 + u;
-            if (y >= H || x >= W) continue;
-            const float iv = S.I[oy + kHalo][ox0 + u + kHalo], tv = S.T[oy + kHalo][ox0 + u + kHalo];
-            const float gs = o[0][u] + 2.f * iv * o[1][u] + tv * o[2][u];
-            const size_t p = static_cast<size_t>(y) * W + x;
-            float g = ws * gs;
-            if (kind == kLossTraining) {
-                const float d = iv - tv;
-                const float k = 1.f + (mask[p] ? 1.f : 0.f) + tv * tv;
-                rsum += static_cast<double>(d * d * k);
-                g = fmaf(wr * d, k, g);
-            }
-            if (a.grad) a.grad[plane_off + p] = g;
-            if (a.du) {
-                const float2 uu = a.field[plane_off + p];
-                a.du[plane_off + p] = make_float2(2.f * uu.x * g, 2.f * uu.y * g);
-            }
-        }
-    }
-    using BR = cub::BlockReduce<double, kLossThreads>;
+    cp_wait<0>();
+    using BR = cub::BlockReduce<double, kSW>;
     __shared__ typename BR::TempStorage tmp;
-    const double r_tot = BR(tmp).Sum(rsum);
+    const double r_tot = BR(tmp).Sum(st.rsum);
     __syncthreads();
-    const double s_tot = BR(tmp).Sum(ssum);
-    if (tid == 0) {
+    const double s_tot = BR(tmp).Sum(st.ssum);
+    if (threadIdx.x == 0) {
         const int slot = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
         a.partials[2 * slot] = r_tot;
         a.partials[2 * slot + 1] = s_tot;
@@ -484,7 +538,7 @@ unsigned grid_for(int64_t n, int threads) {
 
 int loss_partial_slots(int kind, int L, int C, int H, int W) {
     if (kind == kLossTraining || kind == kLossSsim)
-        return ceil_div(W, kTW) * ceil_div(H, kTH) * L * C;
+        return ceil_div(W, kSO) * ceil_div(H, kSR) * L * C;
     const int64_t total = static_cast<int64_t>(L) * C * H * W;
     return static_cast<int>(grid_for(total, kLossThreads));
 }
@@ -492,18 +546,18 @@ int loss_partial_slots(int kind, int L, int C, int H, int W) {
 int loss_launch(const LossArgs& a, cudaStream_t st) {
     if (a.kind == kLossTraining || a.kind == kLossSsim) {
         require(a.H >= kWin && a.W >= kWin, "ssim: image smaller than the 11x11 window");
-        const dim3 grid(ceil_div(a.W, kTW), ceil_div(a.H, kTH), a.L * a.C);
-        const size_t smem = sizeof(SsimSmem);
+        const dim3 grid(ceil_div(a.W, kSO), ceil_div(a.H, kSR), a.L * a.C);
         static const Win win = ssim_window_f32();
         require(a.tstats != nullptr, "ssim: target statistics missing");
+        const size_t smem = sizeof(SsimSmem);
         if (a.field) {
             HS_CUDA(cudaFuncSetAttribute(ssim_loss_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem)));
-            ssim_loss_kernel<true><<<grid, kLossThreads, smem, st>>>(a, win);
+            ssim_loss_kernel<true><<<grid, kSW, smem, st>>>(a, win);
         } else {
             HS_CUDA(cudaFuncSetAttribute(ssim_loss_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem)));
-            ssim_loss_kernel<false><<<grid, kLossThreads, smem, st>>>(a, win);
+            ssim_loss_kernel<false><<<grid, kSW, smem, st>>>(a, win);
         }
         launch_check("ssim_loss");
         return static_cast<int>(grid.x * grid.y * grid.z);
