@@ -22,6 +22,8 @@
 // the 20-row pipeline fill per CTA); one barrier per row.  Loss sums are
 // per-CTA fp64 partials reduced by one deterministic final block.
 #include <cmath>
+#include <cstdlib>
+#include <type_traits>
 
 #include <cub/block/block_reduce.cuh>
 
@@ -107,46 +109,64 @@ __device__ __forceinline__ float corr11(const Win& w, F f) {
 }
 
 // Three 11-tap correlations at once from a loader f(j) -> float4 (x, y, z used),
-// loading the symmetric pairs progressively (few live registers).
+// loading the symmetric pairs progressively (few live registers); x and y run
+// as packed fp32x2 pairs.
 template <class F>
-__device__ __forceinline__ void corr11x3(const Win& w, F f, float& a0, float& a1, float& a2) {
+__device__ __forceinline__ void corr11x3(const Win& w, F f, float2& a01, float& a2) {
     const float4 m = f(5);
-    a0 = w.g[5] * m.x;
-    a1 = w.g[5] * m.y;
-    a2 = w.g[5] * m.z;
-    float b0 = 0.f, b1 = 0.f, b2 = 0.f;
+    float2 axy = f2mul(f2splat(w.g[5]), make_float2(m.x, m.y));
+    float az = w.g[5] * m.z;
+    float2 bxy = make_float2(0.f, 0.f);
+    float bz = 0.f;
 #pragma unroll
     for (int j = 0; j < 5; ++j) {
         const float4 p = f(j), q = f(10 - j);
+        const float2 sxy = f2add(make_float2(p.x, p.y), make_float2(q.x, q.y));
         if (j & 1) {
-            b0 = fmaf(w.g[j], p.x + q.x, b0);
-            b1 = fmaf(w.g[j], p.y + q.y, b1);
-            b2 = fmaf(w.g[j], p.z + q.z, b2);
+            bxy = f2fma(f2splat(w.g[j]), sxy, bxy);
+            bz = fmaf(w.g[j], p.z + q.z, bz);
         } else {
-            a0 = fmaf(w.g[j], p.x + q.x, a0);
-            a1 = fmaf(w.g[j], p.y + q.y, a1);
-            a2 = fmaf(w.g[j], p.z + q.z, a2);
+            axy = f2fma(f2splat(w.g[j]), sxy, axy);
+            az = fmaf(w.g[j], p.z + q.z, az);
         }
     }
-    a0 += b0;
-    a1 += b1;
-    a2 += b2;
+    a01 = f2add(axy, bxy);
+    a2 = az + bz;
+}
+
+// Same for a packed ring pair and a scalar ring: f(i) -> row i of (pair, scalar).
+template <class F2, class F1>
+__device__ __forceinline__ void corr11x3r(const Win& w, F2 f2, F1 f1, float2& a01, float& a2) {
+    float2 axy = f2mul(f2splat(w.g[5]), f2(5)), bxy = make_float2(0.f, 0.f);
+    float az = w.g[5] * f1(5), bz = 0.f;
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+        const float2 sxy = f2add(f2(j), f2(10 - j));
+        if (j & 1) {
+            bxy = f2fma(f2splat(w.g[j]), sxy, bxy);
+            bz = fmaf(w.g[j], f1(j) + f1(10 - j), bz);
+        } else {
+            axy = f2fma(f2splat(w.g[j]), sxy, axy);
+            az = fmaf(w.g[j], f1(j) + f1(10 - j), az);
+        }
+    }
+    a01 = f2add(axy, bxy);
+    a2 = az + bz;
 }
 
 struct SsimState {
-    float h0[kWin], h1[kWin], h2[kWin];  // horizontal correlations of I, I^2, I t (ring by row)
-    float s0[kWin], s1[kWin], s2[kWin];  // horizontal spreads of g1, g2, g3 (ring by valid row)
-    double ssum, rsum;
+    float2 h01[kWin];  // horizontal correlations of (I, I^2) (ring by row; packed pair)
+    float h2[kWin];    // ... of I t
+    float2 s01[kWin];  // horizontal spreads of (g1, g2) (ring by valid row)
+    float s2[kWin];    // ... of g3
+    float ssum, rsum;                    // per-thread sums (<= kSR terms each; fp64 across threads)
 };
 
 // Asynchronous global->shared copies (cp.async); src_bytes = 0 zero-fills.
-__device__ __forceinline__ void cp_async8(void* dst, const void* src, bool ok) {
+template <int B>
+__device__ __forceinline__ void cp_async(void* dst, const void* src, bool ok) {
     const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(ok ? 8 : 0));
-}
-__device__ __forceinline__ void cp_async4(void* dst, const void* src, bool ok) {
-    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(ok ? 4 : 0));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(d), "l"(src), "n"(B), "r"(ok ? B : 0));
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;"); }
 template <int N>
@@ -156,8 +176,9 @@ constexpr int kRaw = 16;  // ring of raw input rows (U or I, and t): covers rows
 constexpr int kPD = 3;    // prefetch distance (rows) of the cp.async pipeline
 constexpr int kTsRing = 4;
 
+template <class Raw>
 struct SsimSmem {
-    float2 rawU[kRaw][kSIn];    // U (or I in .x when the loss gets intensities)
+    Raw rawU[kRaw][kSIn];       // U (or I when the loss gets intensities)
     float rawT[kRaw][kSIn];     // target
     float2 ts[kTsRing][kSW];    // target window stats of the valid row
     float4 in[2][kSIn];         // (I, I^2, I t, -) of the row being correlated
@@ -166,45 +187,62 @@ struct SsimSmem {
 
 template <bool FROM_FIELD>
 struct SsimCta {
+    using Raw = typename std::conditional<FROM_FIELD, float2, float>::type;
     const LossArgs& a;
     const Win& win;
-    SsimSmem& S;
+    SsimSmem<Raw>& S;
     int t, x0, y0, c, H, W, vh, vw, kind;
     size_t plane_off;
     const float* tgt;
     const float2* tst;
     const uint8_t* mask;
     float wr, ws;
+    // per-thread copy sources (column clamped into the image) and validity
+    const Raw* srcA;     // own input column (plane base + column)
+    const Raw* srcB;     // right-halo column (t < 10)
+    const float* tgtA;
+    const float* tgtB;
+    const float2* tsA;   // target stats, own valid column
+    bool okA, okB, okV;
+
+    __device__ __forceinline__ void init_sources() {
+        const int xa = x0 - kHalo + t, xb = x0 + kSO + t;
+        okA = xa >= 0 && xa < W;
+        okB = t < kHalo && xb < W;
+        okV = c >= 0 && c < vw;
+        const Raw* base = FROM_FIELD ? reinterpret_cast<const Raw*>(a.field + plane_off)
+                                     : reinterpret_cast<const Raw*>(a.recon + plane_off);
+        srcA = base + min(max(xa, 0), W - 1);
+        srcB = base + min(max(xb, 0), W - 1);
+        tgtA = tgt + min(max(xa, 0), W - 1);
+        tgtB = tgt + min(max(xb, 0), W - 1);
+        tsA = tst + min(max(c, 0), vw - 1);
+    }
 
     // cp.async of input row r (own column, plus the right halo for t < 10)
     // and of the target statistics of valid row v; one commit group.
     __device__ __forceinline__ void issue(int r, int v) const {
         const bool rok = r >= 0 && r < H;
-        const int rs = min(max(r, 0), H - 1);
-        const int slot = (r + 4 * kRaw) % kRaw;
-        const size_t rowp = static_cast<size_t>(rs) * W;
-        const int xa = x0 - kHalo + t, xb = x0 + kSO + t;
-        const bool oka = rok && xa >= 0 && xa < W;
-        const size_t pa = rowp + min(max(xa, 0), W - 1);
-        if (FROM_FIELD) cp_async8(&S.rawU[slot][t], a.field + plane_off + pa, oka);
-        else cp_async4(&S.rawU[slot][t], a.recon + plane_off + pa, oka);
-        cp_async4(&S.rawT[slot][t], tgt + pa, oka);
+        const size_t rowp = static_cast<size_t>(min(max(r, 0), H - 1)) * W;
+        const int slot = r & (kRaw - 1);
+        cp_async<sizeof(Raw)>(&S.rawU[slot][t], srcA + rowp, rok && okA);
+        cp_async<4>(&S.rawT[slot][t], tgtA + rowp, rok && okA);
         if (t < kHalo) {
-            const bool okb = rok && xb < W;
-            const size_t pb = rowp + min(xb, W - 1);
-            if (FROM_FIELD) cp_async8(&S.rawU[slot][kSW + t], a.field + plane_off + pb, okb);
-            else cp_async4(&S.rawU[slot][kSW + t], a.recon + plane_off + pb, okb);
-            cp_async4(&S.rawT[slot][kSW + t], tgt + pb, okb);
+            cp_async<sizeof(Raw)>(&S.rawU[slot][kSW + t], srcB + rowp, rok && okB);
+            cp_async<4>(&S.rawT[slot][kSW + t], tgtB + rowp, rok && okB);
         }
-        const bool vok = v >= 0 && v < vh && c >= 0 && c < vw;
-        const size_t pv = static_cast<size_t>(min(max(v, 0), vh - 1)) * vw + min(max(c, 0), vw - 1);
-        cp_async8(&S.ts[(v + 4 * kTsRing) % kTsRing][t], tst + pv, vok);
+        const bool vok = v >= 0 && v < vh;
+        cp_async<8>(&S.ts[v & (kTsRing - 1)][t], tsA + static_cast<size_t>(min(max(v, 0), vh - 1)) * vw,
+                    vok && okV);
         cp_commit();
     }
-    __device__ __forceinline__ float intensity(float2 u) const { return FROM_FIELD ? u.x * u.x + u.y * u.y : u.x; }
+    __device__ __forceinline__ float intensity(Raw u) const {
+        if constexpr (FROM_FIELD) return u.x * u.x + u.y * u.y;
+        else return u;
+    }
     // (I, I^2, I t) of raw row r -> the correlation row buffer (own columns only)
     __device__ __forceinline__ void convert(int r, int buf) const {
-        const int slot = (r + 4 * kRaw) % kRaw;
+        const int slot = r & (kRaw - 1);
         {
             const float i = intensity(S.rawU[slot][t]), tv = S.rawT[slot][t];
             S.in[buf][t] = make_float4(i, i * i, i * tv, 0.f);
@@ -233,16 +271,18 @@ struct SsimCta {
         // 1. horizontal correlation of input row r (ssim_channel corr_x, loss.cpp:103-111)
         {
             const float4* row = &S.in[buf][t];
-            corr11x3(win, [&](int j) { return row[j]; }, st.h0[U], st.h1[U], st.h2[U]);
+            corr11x3(win, [&](int j) { return row[j]; }, st.h01[U], st.h2[U]);
         }
         // 2. vertical correlation of rows v..v+10 + SSIM map and derivative maps
         cp_wait<kPD - 1>();  // groups of rows <= r + 1 (and stats of v) have landed
         float4 gv = make_float4(0.f, 0.f, 0.f, 0.f);
         if (v >= 0 && v < vh && c >= 0 && c < vw) {
-            const float m1 = corr11(win, [&](int i) { return st.h0[(U + 1 + i) % kWin]; });
-            const float exx = corr11(win, [&](int i) { return st.h1[(U + 1 + i) % kWin]; });
-            const float exy = corr11(win, [&](int i) { return st.h2[(U + 1 + i) % kWin]; });
-            const float2 ts = S.ts[(v + 4 * kTsRing) % kTsRing][t];
+            float2 mm;
+            float exy;
+            corr11x3r(win, [&](int i) { return st.h01[(U + 1 + i) % kWin]; },
+                      [&](int i) { return st.h2[(U + 1 + i) % kWin]; }, mm, exy);
+            const float m1 = mm.x, exx = mm.y;
+            const float2 ts = S.ts[v & (kTsRing - 1)][t];
             const float C1 = static_cast<float>(kSsimC1), C2 = static_cast<float>(kSsimC2);
             const float m2 = ts.x;
             const float s12 = exy - m1 * m2;
@@ -254,11 +294,12 @@ struct SsimCta {
             // s/a1, s/a2 evaluated as a2/(b1 b2), a1/(b1 b2): equal where
             // ssim_channel's form is defined and finite when a2 rounds to 0
             // in fp32 (a 0/0 there would poison the field via the FFT).
-            const float inv = 1.f / (b1 * b2);
+            const float rb1 = __fdividef(1.f, b1), rb2 = __fdividef(1.f, b2);
+            const float inv = rb1 * rb2;
             const float sv = a1 * a2 * inv;
-            if (t >= kHalo && v >= y0 && v < y0 + kSR) st.ssum += static_cast<double>(sv);
-            gv.x = a2 * inv * 2.f * m2 - (sv / b1) * 2.f * m1 + (sv / b2) * 2.f * m1 - a1 * inv * 2.f * m2;
-            gv.y = -sv / b2;
+            if (t >= kHalo && v >= y0 && v < y0 + kSR) st.ssum += sv;
+            gv.x = 2.f * (a2 * inv * m2 - sv * rb1 * m1 + sv * rb2 * m1 - a1 * inv * m2);
+            gv.y = -sv * rb2;
             gv.z = 2.f * a1 * inv;
         }
         S.gm[buf][t] = gv;
@@ -269,15 +310,20 @@ struct SsimCta {
         {
             // threads t < 10 own no output column: their spread row stays 0
             const float4* gr = &S.gm[buf][max(t, kHalo)];
-            corr11x3(win, [&](int j) { return gr[-j]; }, st.s0[U], st.s1[U], st.s2[U]);
-            if (t < kHalo) st.s0[U] = st.s1[U] = st.s2[U] = 0.f;
+            corr11x3(win, [&](int j) { return gr[-j]; }, st.s01[U], st.s2[U]);
+            if (t < kHalo) {
+                st.s01[U] = make_float2(0.f, 0.f);
+                st.s2[U] = 0.f;
+            }
         }
         if (out_ok) {
-            const float G1 = corr11(win, [&](int i) { return st.s0[(U + kWin - i) % kWin]; });
-            const float G2 = corr11(win, [&](int i) { return st.s1[(U + kWin - i) % kWin]; });
-            const float G3 = corr11(win, [&](int i) { return st.s2[(U + kWin - i) % kWin]; });
-            const int slot = (y + 4 * kRaw) % kRaw;
-            const float2 uu = S.rawU[slot][t];
+            float2 G12;
+            float G3;
+            corr11x3r(win, [&](int i) { return st.s01[(U + kWin - i) % kWin]; },
+                      [&](int i) { return st.s2[(U + kWin - i) % kWin]; }, G12, G3);
+            const float G1 = G12.x, G2 = G12.y;
+            const int slot = y & (kRaw - 1);
+            const Raw uu = S.rawU[slot][t];
             const float tv = S.rawT[slot][t];
             const float iv = intensity(uu);
             const float gs = G1 + 2.f * iv * G2 + tv * G3;  // loss.cpp:211
@@ -285,20 +331,23 @@ struct SsimCta {
             if (kind == kLossTraining) {  // loss_recon_grad, loss.cpp:317-341
                 const float d = iv - tv;
                 const float k = 1.f + mk + tv * tv;
-                st.rsum += static_cast<double>(d * d * k);
+                st.rsum += d * d * k;
                 g = fmaf(wr * d, k, g);
             }
             const size_t p = plane_off + static_cast<size_t>(y) * W + x;
             if (a.grad) a.grad[p] = g;
-            if (a.du) a.du[p] = make_float2(2.f * uu.x * g, 2.f * uu.y * g);
+            if constexpr (FROM_FIELD) {
+                if (a.du) a.du[p] = make_float2(2.f * uu.x * g, 2.f * uu.y * g);
+            }
         }
     }
 };
 
-template <bool FROM_FIELD>
-__global__ void __launch_bounds__(kSW, 4) ssim_loss_kernel(LossArgs a, Win win) {
+template <bool FROM_FIELD, int MINB>
+__global__ void __launch_bounds__(kSW, MINB) ssim_loss_kernel(LossArgs a, Win win) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    SsimSmem& S = *reinterpret_cast<SsimSmem*>(smem_raw);
+    using Raw = typename SsimCta<FROM_FIELD>::Raw;
+    SsimSmem<Raw>& S = *reinterpret_cast<SsimSmem<Raw>*>(smem_raw);
     const int plane = blockIdx.z;  // l * C + c
     const int l = plane / a.C, ch = plane - l * a.C;
     SsimCta<FROM_FIELD> K{a, win, S};
@@ -319,11 +368,15 @@ __global__ void __launch_bounds__(kSW, 4) ssim_loss_kernel(LossArgs a, Win win) 
     K.wr = static_cast<float>(2.0 / (n_el * a.L_norm));
     const double count = static_cast<double>(a.L_norm) * a.C * K.vh * K.vw;
     K.ws = static_cast<float>((a.kind == kLossTraining ? kSsimWeight : 1.0) * (-1.0 / count));
+    K.init_sources();
 
     SsimState st;
 #pragma unroll
-    for (int i = 0; i < kWin; ++i) st.h0[i] = st.h1[i] = st.h2[i] = st.s0[i] = st.s1[i] = st.s2[i] = 0.f;
-    st.ssum = st.rsum = 0.0;
+    for (int i = 0; i < kWin; ++i) {
+        st.h01[i] = st.s01[i] = make_float2(0.f, 0.f);
+        st.h2[i] = st.s2[i] = 0.f;
+    }
+    st.ssum = st.rsum = 0.f;
     // steps s = 0 .. kSteps-1 cover valid rows v = y0-20 .. y0+kSR-1 (output rows y0..y0+kSR-1);
     // rows past the image are guarded inside the step
     constexpr int kSteps = kSR + 2 * kHalo;
@@ -352,9 +405,9 @@ __global__ void __launch_bounds__(kSW, 4) ssim_loss_kernel(LossArgs a, Win win) 
     cp_wait<0>();
     using BR = cub::BlockReduce<double, kSW>;
     __shared__ typename BR::TempStorage tmp;
-    const double r_tot = BR(tmp).Sum(st.rsum);
+    const double r_tot = BR(tmp).Sum(static_cast<double>(st.rsum));
     __syncthreads();
-    const double s_tot = BR(tmp).Sum(st.ssum);
+    const double s_tot = BR(tmp).Sum(static_cast<double>(st.ssum));
     if (threadIdx.x == 0) {
         const int slot = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
         a.partials[2 * slot] = r_tot;
@@ -549,15 +602,20 @@ int loss_launch(const LossArgs& a, cudaStream_t st) {
         const dim3 grid(ceil_div(a.W, kSO), ceil_div(a.H, kSR), a.L * a.C);
         static const Win win = ssim_window_f32();
         require(a.tstats != nullptr, "ssim: target statistics missing");
-        const size_t smem = sizeof(SsimSmem);
+        static const int minb = [] {
+            const char* e = std::getenv("HS_SSIM_MINB");
+            return e ? std::atoi(e) : 4;
+        }();
+        auto go = [&](auto kern, size_t smem) {
+            HS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+            kern<<<grid, kSW, smem, st>>>(a, win);
+        };
         if (a.field) {
-            HS_CUDA(cudaFuncSetAttribute(ssim_loss_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem)));
-            ssim_loss_kernel<true><<<grid, kSW, smem, st>>>(a, win);
+            if (minb == 3) go(ssim_loss_kernel<true, 3>, sizeof(SsimSmem<float2>));
+            else go(ssim_loss_kernel<true, 4>, sizeof(SsimSmem<float2>));
         } else {
-            HS_CUDA(cudaFuncSetAttribute(ssim_loss_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem)));
-            ssim_loss_kernel<false><<<grid, kSW, smem, st>>>(a, win);
+            if (minb == 3) go(ssim_loss_kernel<false, 3>, sizeof(SsimSmem<float>));
+            else go(ssim_loss_kernel<false, 4>, sizeof(SsimSmem<float>));
         }
         launch_check("ssim_loss");
         return static_cast<int>(grid.x * grid.y * grid.z);
