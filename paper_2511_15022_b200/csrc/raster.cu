@@ -452,39 +452,60 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(
 
 // ---------------------------------------------------------------------------
 // K3: backward, one warp per Gaussian (rasterize_backward :201-284).
+//
+// The warp walks the Gaussian's exact ellipse footprint in bands of 32 rows:
+// lane r computes row r's x-interval, the nonempty rows are compacted into a
+// per-warp shared table (y, x - flat index), and the band's pixels are
+// flattened so that every lane always has a pixel.  A lane finds the row of
+// its flat pixel with two warp reductions per 32-pixel chunk (row starts
+// inside the chunk as a bitmask, rows before it as a count) and one popc.
+// The per-pixel math runs on packed fp32x2 pairs: (dx, dy), the rows of
+// Sigma^-1 (dx, dy), per channel (d_amp, d_phase), (gmx, gmy) and (ga, gc).
 // ---------------------------------------------------------------------------
 constexpr int kBwdThreads = 256;
+constexpr int kBwdWarps = kBwdThreads / 32;
 
 template <int C>
 __global__ void __launch_bounds__(kBwdThreads, 3) raster_bwd_kernel(
     int N, const float4* __restrict__ rec, const float4* __restrict__ shade,
     const double* __restrict__ p64, const int4* __restrict__ pbox, int W, int H,
     const float2* __restrict__ gfield, float* __restrict__ raw) {
-    const int lane = threadIdx.x & 31;
-    const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    __shared__ int2 s_rows[kBwdWarps][32];  // compact nonempty rows: (y, x - flat index)
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int g = blockIdx.x * kBwdWarps + wid;
     if (g >= N) return;
     const float4 r0 = rec[3 * static_cast<size_t>(g)];
     const float4 r1 = rec[3 * static_cast<size_t>(g) + 1];
     const float4 r2 = rec[3 * static_cast<size_t>(g) + 2];
-    float4 sh[C];
+    float2 A[C], B[C], S[C];  // (sh.z, -sh.y), (sh.w, sh.x), (sh.x, sh.y)
 #pragma unroll
-    for (int c = 0; c < C; ++c) sh[c] = shade[static_cast<size_t>(g) * C + c];
+    for (int c = 0; c < C; ++c) {
+        const float4 sh = shade[static_cast<size_t>(g) * C + c];
+        A[c] = make_float2(sh.z, -sh.y);
+        B[c] = make_float2(sh.w, sh.x);
+        S[c] = make_float2(sh.x, sh.y);
+    }
     const int4 bb = pbox[g];
     const float px = r0.x + r0.z, py = r0.y + r0.w;
+    const float2 p_hi = make_float2(r0.x, r0.y), p_lo = make_float2(r0.z, r0.w);
     const float i00 = r1.x, i01 = r1.y, i11 = r1.z, cut = r1.w;
+    const float2 row0 = make_float2(i00, i01), row1 = make_float2(i01, i11);
     const float alpha = r2.x, tol = r2.y, detI = r2.z, inv_i00 = r2.w;
     const float M = cut + tol;
     const float ratio = i01 * inv_i00;
+    const size_t HW = static_cast<size_t>(H) * W;
 
-    float d_amp[C], d_phase[C];
+    float2 dap[C];  // (d_amp, d_phase) per channel
 #pragma unroll
-    for (int c = 0; c < C; ++c) d_amp[c] = d_phase[c] = 0.f;
-    float d_alpha = 0.f, gmx = 0.f, gmy = 0.f, ga = 0.f, gb = 0.f, gc = 0.f;
+    for (int c = 0; c < C; ++c) dap[c] = make_float2(0.f, 0.f);
+    float2 gm = make_float2(0.f, 0.f), gac = make_float2(0.f, 0.f);
+    float d_alpha = 0.f, gb = 0.f;
 
     const float ext = sqrtf(fmaxf(i00 * M / detI, 0.f)) + 1e-2f;
     const int ya = max(bb.z, static_cast<int>(ceilf(py - ext)));
     const int yb = min(bb.w, static_cast<int>(floorf(py + ext)));
     const double* q = p64 + 8 * static_cast<size_t>(g);
+    const unsigned lanemask_le = 0xffffffffu >> (31 - lane);
 
     for (int ybase = ya; ybase <= yb; ybase += 32) {
         const int row = ybase + lane;
@@ -507,46 +528,47 @@ __global__ void __launch_bounds__(kBwdThreads, 3) raster_bwd_kernel(
             if (lane >= o) incl += v;
         }
         const int total = __shfl_sync(0xffffffffu, incl, 31);
+        if (total == 0) continue;
         const int excl = incl - wdt;
-        // Two flattened pixels per lane per iteration: both pixels' grad-field
-        // gathers are issued before either is consumed.
+        const unsigned nonempty = __ballot_sync(0xffffffffu, wdt > 0);
+        __syncwarp();
+        if (wdt > 0) s_rows[wid][__popc(nonempty & (lanemask_le >> 1))] = make_int2(row, xl - excl);
+        __syncwarp();
+        // Two 32-pixel chunks per iteration: both chunks' gathers are in flight together.
         for (int fb = 0; fb < total; fb += 64) {
-            int px_[2], py_[2];
+            int ox[2], oy[2];
             bool act[2];
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
-                const int f = fb + u * 32 + lane;
-                int r = 0;  // first row whose inclusive offset exceeds f
-#pragma unroll
-                for (int s = 16; s > 0; s >>= 1) {
-                    const int v = __shfl_sync(0xffffffffu, incl, r + s - 1);
-                    if (v <= f) r += s;
-                }
-                r = min(r, 31);
-                const int rx = __shfl_sync(0xffffffffu, xl, r);
-                const int rex = __shfl_sync(0xffffffffu, excl, r);
+                const int cb = fb + 32 * u;
+                const unsigned bit = (wdt > 0 && excl > cb && excl < cb + 32) ? 1u << (excl - cb) : 0u;
+                const unsigned starts = __reduce_or_sync(0xffffffffu, bit);
+                const int k0 = static_cast<int>(__reduce_add_sync(0xffffffffu, (wdt > 0 && excl <= cb) ? 1u : 0u)) - 1;
+                const int f = cb + lane;
                 act[u] = f < total;
-                px_[u] = rx + (f - rex);
-                py_[u] = ybase + r;
+                const int kk = min(k0 + __popc(starts & lanemask_le), 31);
+                const int2 info = s_rows[wid][kk];
+                oy[u] = info.x;
+                ox[u] = f + info.y;
             }
             float2 gv[2][C];
 #pragma unroll
-            for (int u = 0; u < 2; ++u)
+            for (int u = 0; u < 2; ++u) {
+                const float2* base = gfield + (static_cast<size_t>(oy[u]) * W + ox[u]);
 #pragma unroll
-                for (int c = 0; c < C; ++c)
-                    gv[u][c] = act[u] ? gfield[(static_cast<size_t>(c) * H + py_[u]) * W + px_[u]]
-                                      : make_float2(0.f, 0.f);
+                for (int c = 0; c < C; ++c) gv[u][c] = act[u] ? base[c * HW] : make_float2(0.f, 0.f);
+            }
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
                 if (!act[u]) continue;
-                const int x = px_[u], y = py_[u];
-                const float dx = (static_cast<float>(x) - r0.x) - r0.z;
-                const float dy = (static_cast<float>(y) - r0.y) - r0.w;
-                const float m = dx * (dx * i00 + 2.f * dy * i01) + dy * dy * i11;
+                const int x = ox[u], y = oy[u];
+                const float2 dxy = f2sub(f2sub(make_float2(static_cast<float>(x), static_cast<float>(y)), p_hi), p_lo);
+                const float2 e = f2fma(f2splat(dxy.x), row0, f2mul(f2splat(dxy.y), row1));  // Sigma^-1 (dx, dy)
+                const float m = fmaf(dxy.x, e.x, dxy.y * e.y);
                 if (m > M) continue;
-                float G = expf(-0.5f * m), aeff;
+                float G = __expf(-0.5f * m), aeff;
                 bool sat;
-                const float aG = alpha * G;
+                float aG = alpha * G;
                 if (m <= cut - tol && fabsf(aG - 0.99f) > 1e-5f) {
                     sat = aG > 0.99f;
                     aeff = sat ? 0.99f : aG;
@@ -554,25 +576,24 @@ __global__ void __launch_bounds__(kBwdThreads, 3) raster_bwd_kernel(
                     double Gd, ae;
                     if (!exact_contrib(q, x, y, Gd, sat, ae)) continue;
                     G = static_cast<float>(Gd);
+                    aG = alpha * G;
                     aeff = static_cast<float>(ae);
                 }
                 float s_amp = 0.f;
 #pragma unroll
                 for (int c = 0; c < C; ++c) {
                     const float2 g2 = gv[u][c];
-                    const float common = sh[c].z * g2.x + sh[c].w * g2.y;
-                    d_amp[c] = fmaf(aeff, common, d_amp[c]);
-                    d_phase[c] = fmaf(aeff, sh[c].x * g2.y - sh[c].y * g2.x, d_phase[c]);
-                    s_amp += sh[c].x * g2.x + sh[c].y * g2.y;
+                    // (common, cross) = (cos g.re + sin g.im, amp cos g.im - amp sin g.re)
+                    const float2 P = f2fma(f2splat(g2.y), B[c], f2mul(f2splat(g2.x), A[c]));
+                    dap[c] = f2fma(f2splat(aeff), P, dap[c]);
+                    s_amp = fmaf(S[c].x, g2.x, fmaf(S[c].y, g2.y, s_amp));
                 }
                 if (!sat) {
                     d_alpha = fmaf(s_amp, G, d_alpha);
-                    const float w = s_amp * alpha * G * -0.5f;
-                    gmx += w * -2.f * (dx * i00 + dy * i01);
-                    gmy += w * -2.f * (dx * i01 + dy * i11);
-                    ga += w * dx * dx;
-                    gb += 2.f * w * dx * dy;
-                    gc += w * dy * dy;
+                    const float qv = s_amp * aG;  // = -2 w of the reference (w = s_amp alpha G / -2)
+                    gm = f2fma(f2splat(qv), e, gm);
+                    gac = f2fma(f2splat(-0.5f * qv), f2mul(dxy, dxy), gac);
+                    gb = fmaf(-qv * dxy.x, dxy.y, gb);
                 }
             }
         }
@@ -582,15 +603,15 @@ __global__ void __launch_bounds__(kBwdThreads, 3) raster_bwd_kernel(
     float v[16];
 #pragma unroll
     for (int c = 0; c < C; ++c) {
-        v[c] = d_amp[c];
-        v[C + c] = d_phase[c];
+        v[c] = dap[c].x;
+        v[C + c] = dap[c].y;
     }
     v[2 * C + 0] = d_alpha;
-    v[2 * C + 1] = gmx;
-    v[2 * C + 2] = gmy;
-    v[2 * C + 3] = ga;
+    v[2 * C + 1] = gm.x;
+    v[2 * C + 2] = gm.y;
+    v[2 * C + 3] = gac.x;
     v[2 * C + 4] = gb;
-    v[2 * C + 5] = gc;
+    v[2 * C + 5] = gac.y;
 #pragma unroll
     for (int i = 2 * C + 6; i < 16; ++i) v[i] = 0.f;
 #pragma unroll
