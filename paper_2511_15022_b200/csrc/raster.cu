@@ -493,7 +493,9 @@ __global__ void __launch_bounds__(kBwdThreads, 3) raster_bwd_kernel(
     const float alpha = r2.x, tol = r2.y, detI = r2.z, inv_i00 = r2.w;
     const float M = cut + tol;
     const float ratio = i01 * inv_i00;
-    const size_t HW = static_cast<size_t>(H) * W;
+    const float2* gch[C];  // channel planes of the gradient field
+#pragma unroll
+    for (int c = 0; c < C; ++c) gch[c] = gfield + static_cast<size_t>(c) * H * W;
 
     float2 dap[C];  // (d_amp, d_phase) per channel
 #pragma unroll
@@ -541,7 +543,8 @@ __global__ void __launch_bounds__(kBwdThreads, 3) raster_bwd_kernel(
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
                 const int cb = fb + 32 * u;
-                const unsigned bit = (wdt > 0 && excl > cb && excl < cb + 32) ? 1u << (excl - cb) : 0u;
+                const unsigned d = static_cast<unsigned>(excl - cb - 1);  // start strictly inside the chunk
+                const unsigned bit = (wdt > 0 && d < 31u) ? 2u << d : 0u;
                 const unsigned starts = __reduce_or_sync(0xffffffffu, bit);
                 const int k0 = static_cast<int>(__reduce_add_sync(0xffffffffu, (wdt > 0 && excl <= cb) ? 1u : 0u)) - 1;
                 const int f = cb + lane;
@@ -551,12 +554,13 @@ __global__ void __launch_bounds__(kBwdThreads, 3) raster_bwd_kernel(
                 oy[u] = info.x;
                 ox[u] = f + info.y;
             }
+            // inactive lanes load pixel 0 (always valid) and skip the math
             float2 gv[2][C];
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
-                const float2* base = gfield + (static_cast<size_t>(oy[u]) * W + ox[u]);
+                const int o = act[u] ? oy[u] * W + ox[u] : 0;
 #pragma unroll
-                for (int c = 0; c < C; ++c) gv[u][c] = act[u] ? base[c * HW] : make_float2(0.f, 0.f);
+                for (int c = 0; c < C; ++c) gv[u][c] = gch[c][o];
             }
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
