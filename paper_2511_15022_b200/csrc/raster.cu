@@ -21,6 +21,8 @@
 //    footprint row by row, lanes own pixels, a warp-shuffle reduction folds
 //    the 7 + 2C partial sums and lane 0 applies the fp64 chain rule.  No
 //    atomics: the gradients are deterministic.
+#include <cstdlib>
+
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
 
@@ -127,14 +129,15 @@ __global__ void project_kernel(ProjParams P) {
     const double cond = fmin(lmax / lmin, 1e12);
     const double tol = 5e-7 * (1.0 + cond) * (1.0 + cutoff) + 1e-6;
     const double det_inv = i00 * i11 - i01 * i01;
-    P.rec[3 * g + 0] = make_float4(px_hi, py_hi, px_lo, py_lo);
-    P.rec[3 * g + 1] = make_float4(static_cast<float>(i00), static_cast<float>(i01),
-                                   static_cast<float>(i11), static_cast<float>(mahal_cutoff));
-    P.rec[3 * g + 2] = make_float4(static_cast<float>(alpha), static_cast<float>(tol),
+    // SoA records (coalesced stores; the kernels gather them by Gaussian id)
+    P.rec[g] = make_float4(px_hi, py_hi, px_lo, py_lo);
+    P.rec[N + g] = make_float4(static_cast<float>(i00), static_cast<float>(i01),
+                               static_cast<float>(i11), static_cast<float>(mahal_cutoff));
+    P.rec[2 * N + g] = make_float4(static_cast<float>(alpha), static_cast<float>(tol),
                                    static_cast<float>(det_inv), static_cast<float>(1.0 / i00));
-    double* q = P.p64 + 8 * static_cast<size_t>(g);
-    q[0] = px; q[1] = py; q[2] = i00; q[3] = i01; q[4] = i11; q[5] = mahal_cutoff; q[6] = alpha;
-    q[7] = r;
+    double* q = P.p64 + g;
+    q[0] = px; q[N] = py; q[2 * N] = i00; q[3 * N] = i01; q[4 * N] = i11; q[5 * N] = mahal_cutoff;
+    q[6 * N] = alpha; q[7 * N] = r;
     // per-channel shading (rasterizer.cpp:78-85)
     for (int ch = 0; ch < P.c; ++ch) {
         const size_t i = static_cast<size_t>(g) * P.c + ch;
@@ -142,8 +145,8 @@ __global__ void project_kernel(ProjParams P) {
         const double ph = pha[i];
         if (!finite(ph) || !finite(static_cast<double>(amp[i]))) atomicOr(P.status + 2, 1u);
         const double cp = cos(ph), sp = sin(ph);
-        P.shade[i] = make_float4(static_cast<float>(a * cp), static_cast<float>(a * sp),
-                                 static_cast<float>(cp), static_cast<float>(sp));
+        P.shade[static_cast<size_t>(ch) * N + g] = make_float4(static_cast<float>(a * cp), static_cast<float>(a * sp),
+                                                               static_cast<float>(cp), static_cast<float>(sp));
     }
     if (!finite(th)) atomicOr(P.status + 2, 1u);
 }
@@ -157,47 +160,68 @@ __global__ void project_kernel(ProjParams P) {
 // pairs are unique, so the result equals the reference's std::sort order
 // exactly, independent of the scatter order.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restrict__ tcount, int tiles,
-                                                         uint32_t* __restrict__ toffset, uint2* __restrict__ ranges,
-                                                         uint32_t* __restrict__ status, int64_t cap) {
-    using BSc = cub::BlockScan<uint64_t, 1024>;
+constexpr int kScanThreads = 512;
+__global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(const uint32_t* __restrict__ tcount, int tiles,
+                                                                 uint32_t* __restrict__ toffset,
+                                                                 uint2* __restrict__ ranges,
+                                                                 uint32_t* __restrict__ status, int64_t cap) {
+    // each thread scans a contiguous run of tiles serially; one block scan joins the runs
+    using BSc = cub::BlockScan<unsigned long long, kScanThreads>;
     __shared__ typename BSc::TempStorage tmp;
-    __shared__ uint64_t carry;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    for (int base = 0; base < tiles; base += 1024) {
-        const int i = base + threadIdx.x;
-        const uint64_t v = i < tiles ? tcount[i] : 0u;
-        uint64_t ex, agg;
-        BSc(tmp).ExclusiveSum(v, ex, agg);
-        ex += carry;
-        if (i < tiles) {
-            toffset[i] = static_cast<uint32_t>(ex);
-            ranges[i] = v ? make_uint2(static_cast<uint32_t>(ex), static_cast<uint32_t>(ex + v)) : make_uint2(0u, 0u);
+    // up to kReg tiles per thread live in registers (all loads in flight at once)
+    constexpr int kReg = 16;
+    const int per = (tiles + kScanThreads - 1) / kScanThreads;
+    const int t0 = threadIdx.x * per, t1 = min(t0 + per, tiles);
+    unsigned long long run = 0;
+    uint32_t c[kReg];
+#pragma unroll
+    for (int i = 0; i < kReg; ++i) c[i] = (t0 + i < t1) ? tcount[t0 + i] : 0u;
+#pragma unroll
+    for (int i = 0; i < kReg; ++i) run += c[i];
+    for (int t = t0 + kReg; t < t1; ++t) run += tcount[t];
+    unsigned long long ex, agg;
+    BSc(tmp).ExclusiveSum(run, ex, agg);
+#pragma unroll
+    for (int i = 0; i < kReg; ++i) {
+        if (t0 + i < t1) {
+            toffset[t0 + i] = static_cast<uint32_t>(ex);
+            ranges[t0 + i] = c[i] ? make_uint2(static_cast<uint32_t>(ex), static_cast<uint32_t>(ex + c[i]))
+                                  : make_uint2(0u, 0u);
+            ex += c[i];
         }
-        __syncthreads();
-        if (threadIdx.x == 0) carry += agg;
-        __syncthreads();
+    }
+    for (int t = t0 + kReg; t < t1; ++t) {
+        const uint32_t v = tcount[t];
+        toffset[t] = static_cast<uint32_t>(ex);
+        ranges[t] = v ? make_uint2(static_cast<uint32_t>(ex), static_cast<uint32_t>(ex + v)) : make_uint2(0u, 0u);
+        ex += v;
     }
     if (threadIdx.x == 0) {
-        status[0] = static_cast<uint32_t>(carry > 0xffffffffull ? 0xffffffffull : carry);
-        status[1] = carry > static_cast<uint64_t>(cap) ? 1u : 0u;
+        status[0] = static_cast<uint32_t>(agg > 0xffffffffull ? 0xffffffffull : agg);
+        status[1] = agg > static_cast<unsigned long long>(cap) ? 1u : 0u;
     }
 }
 
 // Scatter (duplicate-with-keys, :94-108): tcount is consumed as a countdown.
-__global__ void scatter_ids_kernel(int n, const int4* __restrict__ tbox, int tiles_x,
-                                   const uint32_t* __restrict__ toffset, uint32_t* __restrict__ tcount,
-                                   const uint32_t* __restrict__ status, uint32_t* __restrict__ ids) {
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+// 16 threads per Gaussian, thread k handling tiles k, k + 16, ... of its tile
+// box: one slot atomic per thread in the common case, so the atomics' round
+// trips overlap across many resident threads instead of chaining per Gaussian.
+constexpr int kScatterSub = 16;
+__global__ void __launch_bounds__(256) scatter_ids_kernel(int n, const int4* __restrict__ tbox, int tiles_x,
+                                                          const uint32_t* __restrict__ toffset,
+                                                          uint32_t* __restrict__ tcount,
+                                                          const uint32_t* __restrict__ status,
+                                                          uint32_t* __restrict__ ids) {
+    const int g = blockIdx.x * (256 / kScatterSub) + threadIdx.x / kScatterSub;
+    const int sub = threadIdx.x % kScatterSub;
     if (g >= n || status[1]) return;
     const int4 b = tbox[g];
-    for (int ty = b.z; ty <= b.w; ++ty)
-        for (int tx = b.x; tx <= b.y; ++tx) {
-            const int t = ty * tiles_x + tx;
-            const uint32_t slot = atomicSub(tcount + t, 1u) - 1u;
-            ids[toffset[t] + slot] = static_cast<uint32_t>(g);
-        }
+    const int nx = b.y - b.x + 1, cnt = nx * (b.w - b.z + 1);
+    for (int k = sub; k < cnt; k += kScatterSub) {
+        const int t = (b.z + k / nx) * tiles_x + b.x + k % nx;
+        const uint32_t slot = atomicSub(tcount + t, 1u) - 1u;
+        ids[toffset[t] + slot] = static_cast<uint32_t>(g);
+    }
 }
 
 constexpr int kSegSmem = 4096;  // ids sorted in shared memory per tile
@@ -219,35 +243,29 @@ __device__ __forceinline__ void bitonic_smem(uint32_t* s, int P) {
         }
 }
 
-// Warp per tile for segments of <= 256 ids: an in-register bitonic network,
-// 8 ids per lane (element e = lane * 8 + i); distances < 8 are register
+// Warp per tile for segments of <= 512 ids: an in-register bitonic network,
+// PER ids per lane (element e = lane * PER + i); distances < PER are register
 // swaps, larger ones use shuffles.
-constexpr int kWarpSeg = 256;
+constexpr int kWarpSeg = 512;
 
-__global__ void __launch_bounds__(256) segment_sort_warp_kernel(const uint2* __restrict__ ranges, int tiles,
-                                                                uint32_t* __restrict__ ids,
-                                                                const uint32_t* __restrict__ status) {
-    const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (t >= tiles || status[1]) return;
-    const uint2 r = ranges[t];
-    const int n = static_cast<int>(r.y - r.x);
-    if (n <= 1 || n > kWarpSeg) return;
-    uint32_t v[8];
+template <int PER>
+__device__ __forceinline__ void warp_bitonic(uint32_t* __restrict__ seg, int n, int lane) {
+    constexpr int P = 32 * PER;
+    uint32_t v[PER];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int e = lane * 8 + i;
-        v[i] = e < n ? ids[r.x + e] : 0xffffffffu;
+    for (int i = 0; i < PER; ++i) {
+        const int e = lane * PER + i;
+        v[i] = e < n ? seg[e] : 0xffffffffu;
     }
 #pragma unroll
-    for (int k = 2; k <= kWarpSeg; k <<= 1) {
+    for (int k = 2; k <= P; k <<= 1) {
 #pragma unroll
         for (int j = k >> 1; j > 0; j >>= 1) {
-            if (j >= 8) {
-                const int lj = j >> 3;  // partner lane distance
+            if (j >= PER) {
+                const int lj = j / PER;  // partner lane distance
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const int e = lane * 8 + i;
+                for (int i = 0; i < PER; ++i) {
+                    const int e = lane * PER + i;
                     const uint32_t o = __shfl_xor_sync(0xffffffffu, v[i], lj);
                     const bool lower = (e & j) == 0;
                     const bool up = (e & k) == 0;
@@ -256,10 +274,10 @@ __global__ void __launch_bounds__(256) segment_sort_warp_kernel(const uint2* __r
                 }
             } else {
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
+                for (int i = 0; i < PER; ++i) {
                     const int ixj = i ^ j;
                     if (ixj > i) {
-                        const int e = lane * 8 + i;
+                        const int e = lane * PER + i;
                         const bool up = (e & k) == 0;
                         const uint32_t a = v[i], b = v[ixj];
                         const bool sw = (a > b) == up;
@@ -271,20 +289,28 @@ __global__ void __launch_bounds__(256) segment_sort_warp_kernel(const uint2* __r
         }
     }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int e = lane * 8 + i;
-        if (e < n) ids[r.x + e] = v[i];
+    for (int i = 0; i < PER; ++i) {
+        const int e = lane * PER + i;
+        if (e < n) seg[e] = v[i];
     }
 }
 
-__global__ void __launch_bounds__(256) segment_sort_kernel(const uint2* __restrict__ ranges, uint32_t* __restrict__ ids,
-                                                           uint32_t* __restrict__ scratch,
-                                                           const uint32_t* __restrict__ status) {
-    __shared__ uint32_t s[kSegSmem];
-    if (status[1]) return;
-    const uint2 r = ranges[blockIdx.x];
+__global__ void __launch_bounds__(256) segment_sort_warp_kernel(const uint2* __restrict__ ranges, int tiles,
+                                                                uint32_t* __restrict__ ids,
+                                                                const uint32_t* __restrict__ status) {
+    const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (t >= tiles || status[1]) return;
+    const uint2 r = ranges[t];
     const int n = static_cast<int>(r.y - r.x);
-    if (n <= kWarpSeg) return;  // done by segment_sort_warp_kernel
+    if (n <= 1 || n > kWarpSeg) return;
+    if (n <= 256) warp_bitonic<8>(ids + r.x, n, lane);
+    else warp_bitonic<16>(ids + r.x, n, lane);
+}
+
+__device__ void sort_big_tile(const uint2 r, uint32_t* __restrict__ ids, uint32_t* __restrict__ scratch) {
+    __shared__ uint32_t s[kSegSmem];
+    const int n = static_cast<int>(r.y - r.x);
     int P = 1;
     while (P < n) P <<= 1;
     if (P <= kSegSmem) {
@@ -301,6 +327,29 @@ __global__ void __launch_bounds__(256) segment_sort_kernel(const uint2* __restri
     __syncthreads();
     bitonic_smem(g, P);
     for (int i = threadIdx.x; i < n; i += blockDim.x) ids[r.x + i] = g[i];
+}
+
+// Tiles with more than kWarpSeg ids (rare): each CTA checks 256 tiles at once
+// and sorts the big ones it found, one after another.
+__global__ void __launch_bounds__(256) segment_sort_kernel(const uint2* __restrict__ ranges, int tiles,
+                                                           uint32_t* __restrict__ ids, uint32_t* __restrict__ scratch,
+                                                           const uint32_t* __restrict__ status) {
+    __shared__ int s_big[256];
+    __shared__ int s_nbig;
+    if (status[1]) return;
+    if (threadIdx.x == 0) s_nbig = 0;
+    __syncthreads();
+    const int t = blockIdx.x * 256 + threadIdx.x;
+    if (t < tiles) {
+        const uint2 r = ranges[t];
+        if (static_cast<int>(r.y - r.x) > kWarpSeg) s_big[atomicAdd(&s_nbig, 1)] = t;
+    }
+    __syncthreads();
+    const int nb = s_nbig;
+    for (int i = 0; i < nb; ++i) {
+        sort_big_tile(ranges[s_big[i]], ids, scratch);
+        __syncthreads();
+    }
 }
 
 // build_tile_index export: CTA per tile writes its (tile, id) pairs + range.
@@ -323,17 +372,18 @@ __global__ void export_kernel(const uint32_t* __restrict__ ids, const uint2* __r
 // Exact fp64 contribution test (rasterizer.cpp:164-169 / :220-228).  Returns
 // false when skipped; else G, saturation flag and alpha_eff in fp64.
 // ---------------------------------------------------------------------------
-__device__ __noinline__ bool exact_contrib(const double* __restrict__ q, int x, int y, double& G,
+// q = p64 + g, fields at stride n (SoA: px, py, i00, i01, i11, mahal_cutoff, alpha, r).
+__device__ __noinline__ bool exact_contrib(const double* __restrict__ q, size_t n, int x, int y, double& G,
                                            bool& saturated, double& aeff) {
     const double dx = dsub(static_cast<double>(x), q[0]);
-    const double dy = dsub(static_cast<double>(y), q[1]);
+    const double dy = dsub(static_cast<double>(y), q[n]);
     // dx * dx * i00 + 2.0 * dx * dy * i01 + dy * dy * i11
-    const double mahal = dadd(dadd(dmul(dmul(dx, dx), q[2]), dmul(dmul(dmul(2.0, dx), dy), q[3])),
-                              dmul(dmul(dy, dy), q[4]));
-    if (mahal > q[5]) return false;
+    const double mahal = dadd(dadd(dmul(dmul(dx, dx), q[2 * n]), dmul(dmul(dmul(2.0, dx), dy), q[3 * n])),
+                              dmul(dmul(dy, dy), q[4 * n]));
+    if (mahal > q[5 * n]) return false;
     const double power = fmax(dmul(-0.5, mahal), kPowerFloor);
     G = exp(power);
-    const double aG = dmul(q[6], G);
+    const double aG = dmul(q[6 * n], G);
     saturated = aG > kAlphaCap;
     aeff = saturated ? kAlphaCap : aG;
     return !(aeff < kAlphaCutoff);
@@ -365,12 +415,12 @@ __device__ __forceinline__ bool cell_hit(float4 r0, float4 r1, float4 r2, float 
 }
 
 // fast fp32 contribution with the exact fp64 recheck inside the error band
-__device__ __forceinline__ float fwd_aeff(float m, float4 r1, float4 r2, const double* q, int x, int y) {
+__device__ __forceinline__ float fwd_aeff(float m, float4 r1, float4 r2, const double* q, size_t n, int x, int y) {
     if (m <= r1.w - r2.y) return fminf(0.99f, r2.x * __expf(-0.5f * m));
     if (m <= r1.w + r2.y) {
         double G, ae;
         bool sat;
-        if (exact_contrib(q, x, y, G, sat, ae)) return static_cast<float>(ae);
+        if (exact_contrib(q, n, x, y, G, sat, ae)) return static_cast<float>(ae);
     }
     return 0.f;
 }
@@ -379,7 +429,7 @@ template <int C>
 __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(
     const uint32_t* __restrict__ ids, const uint2* __restrict__ ranges,
     const float4* __restrict__ rec, const float4* __restrict__ shade,
-    const double* __restrict__ p64, int tiles_x, int W, int H, float2* __restrict__ field) {
+    const double* __restrict__ p64, int N, int tiles_x, int W, int H, float2* __restrict__ field) {
     __shared__ float4 s_rec[3][kFwdBatch];
     __shared__ float4 s_sh[C][kFwdBatch];
     __shared__ uint32_t s_id[kFwdBatch];
@@ -401,11 +451,11 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(
         if (static_cast<int>(threadIdx.x) < cnt) {
             const uint32_t g = ids[base + threadIdx.x];
             s_id[threadIdx.x] = g;
-            s_rec[0][threadIdx.x] = rec[3 * static_cast<size_t>(g)];
-            s_rec[1][threadIdx.x] = rec[3 * static_cast<size_t>(g) + 1];
-            s_rec[2][threadIdx.x] = rec[3 * static_cast<size_t>(g) + 2];
+            s_rec[0][threadIdx.x] = rec[g];
+            s_rec[1][threadIdx.x] = rec[static_cast<size_t>(N) + g];
+            s_rec[2][threadIdx.x] = rec[2 * static_cast<size_t>(N) + g];
 #pragma unroll
-            for (int c = 0; c < C; ++c) s_sh[c][threadIdx.x] = shade[static_cast<size_t>(g) * C + c];
+            for (int c = 0; c < C; ++c) s_sh[c][threadIdx.x] = shade[static_cast<size_t>(c) * N + g];
         }
         __syncthreads();
         for (int sub = 0; sub < cnt; sub += 32) {
@@ -425,9 +475,9 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(
                 const float ex = dx * r1.x;
                 const float mA = dx * (ex + 2.f * dyA * r1.y) + dyA * dyA * r1.z;
                 const float mB = dx * (ex + 2.f * dyB * r1.y) + dyB * dyB * r1.z;
-                const double* q = p64 + 8 * static_cast<size_t>(s_id[jj]);
-                const float aA = fwd_aeff(mA, r1, r2, q, x, y);
-                const float aB = fwd_aeff(mB, r1, r2, q, x, y + 4);
+                const double* q = p64 + s_id[jj];
+                const float aA = fwd_aeff(mA, r1, r2, q, N, x, y);
+                const float aB = fwd_aeff(mB, r1, r2, q, N, x, y + 4);
                 if (aA > 0.f || aB > 0.f) {
 #pragma unroll
                     for (int c = 0; c < C; ++c) {
@@ -465,8 +515,8 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(
 constexpr int kBwdThreads = 256;
 constexpr int kBwdWarps = kBwdThreads / 32;
 
-template <int C>
-__global__ void __launch_bounds__(kBwdThreads, 3) raster_bwd_kernel(
+template <int C, int MINB, int NCH>
+__global__ void __launch_bounds__(kBwdThreads, MINB) raster_bwd_kernel(
     int N, const float4* __restrict__ rec, const float4* __restrict__ shade,
     const double* __restrict__ p64, const int4* __restrict__ pbox, int W, int H,
     const float2* __restrict__ gfield, float* __restrict__ raw) {
@@ -474,13 +524,13 @@ __global__ void __launch_bounds__(kBwdThreads, 3) raster_bwd_kernel(
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int g = blockIdx.x * kBwdWarps + wid;
     if (g >= N) return;
-    const float4 r0 = rec[3 * static_cast<size_t>(g)];
-    const float4 r1 = rec[3 * static_cast<size_t>(g) + 1];
-    const float4 r2 = rec[3 * static_cast<size_t>(g) + 2];
+    const float4 r0 = rec[g];
+    const float4 r1 = rec[static_cast<size_t>(N) + g];
+    const float4 r2 = rec[2 * static_cast<size_t>(N) + g];
     float2 A[C], B[C], S[C];  // (sh.z, -sh.y), (sh.w, sh.x), (sh.x, sh.y)
 #pragma unroll
     for (int c = 0; c < C; ++c) {
-        const float4 sh = shade[static_cast<size_t>(g) * C + c];
+        const float4 sh = shade[static_cast<size_t>(c) * N + g];
         A[c] = make_float2(sh.z, -sh.y);
         B[c] = make_float2(sh.w, sh.x);
         S[c] = make_float2(sh.x, sh.y);
@@ -506,7 +556,7 @@ __global__ void __launch_bounds__(kBwdThreads, 3) raster_bwd_kernel(
     const float ext = sqrtf(fmaxf(i00 * M / detI, 0.f)) + 1e-2f;
     const int ya = max(bb.z, static_cast<int>(ceilf(py - ext)));
     const int yb = min(bb.w, static_cast<int>(floorf(py + ext)));
-    const double* q = p64 + 8 * static_cast<size_t>(g);
+    const double* q = p64 + g;
     const unsigned lanemask_le = 0xffffffffu >> (31 - lane);
 
     for (int ybase = ya; ybase <= yb; ybase += 32) {
@@ -536,12 +586,12 @@ __global__ void __launch_bounds__(kBwdThreads, 3) raster_bwd_kernel(
         __syncwarp();
         if (wdt > 0) s_rows[wid][__popc(nonempty & (lanemask_le >> 1))] = make_int2(row, xl - excl);
         __syncwarp();
-        // Two 32-pixel chunks per iteration: both chunks' gathers are in flight together.
-        for (int fb = 0; fb < total; fb += 64) {
-            int ox[2], oy[2];
-            bool act[2];
+        // NCH 32-pixel chunks per iteration: their gathers are in flight together.
+        for (int fb = 0; fb < total; fb += 32 * NCH) {
+            int ox[NCH], oy[NCH];
+            bool act[NCH];
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
+            for (int u = 0; u < NCH; ++u) {
                 const int cb = fb + 32 * u;
                 const unsigned d = static_cast<unsigned>(excl - cb - 1);  // start strictly inside the chunk
                 const unsigned bit = (wdt > 0 && d < 31u) ? 2u << d : 0u;
@@ -555,15 +605,15 @@ __global__ void __launch_bounds__(kBwdThreads, 3) raster_bwd_kernel(
                 ox[u] = f + info.y;
             }
             // inactive lanes load pixel 0 (always valid) and skip the math
-            float2 gv[2][C];
+            float2 gv[NCH][C];
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
+            for (int u = 0; u < NCH; ++u) {
                 const int o = act[u] ? oy[u] * W + ox[u] : 0;
 #pragma unroll
                 for (int c = 0; c < C; ++c) gv[u][c] = gch[c][o];
             }
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
+            for (int u = 0; u < NCH; ++u) {
                 if (!act[u]) continue;
                 const int x = ox[u], y = oy[u];
                 const float2 dxy = f2sub(f2sub(make_float2(static_cast<float>(x), static_cast<float>(y)), p_hi), p_lo);
@@ -578,7 +628,7 @@ __global__ void __launch_bounds__(kBwdThreads, 3) raster_bwd_kernel(
                     aeff = sat ? 0.99f : aG;
                 } else {
                     double Gd, ae;
-                    if (!exact_contrib(q, x, y, Gd, sat, ae)) continue;
+                    if (!exact_contrib(q, N, x, y, Gd, sat, ae)) continue;
                     G = static_cast<float>(Gd);
                     aG = alpha * G;
                     aeff = static_cast<float>(ae);
@@ -757,17 +807,17 @@ void RasterWork::project_and_bin(const float* d_params, cudaStream_t st) {
                  tcount.as<uint32_t>(), stat};
     project_kernel<<<ceil_div(n, 128), 128, 0, st>>>(P);
     launch_check("project");
-    tile_scan_kernel<<<1, 1024, 0, st>>>(tcount.as<uint32_t>(), tiles, toffset.as<uint32_t>(), ranges.as<uint2>(),
+    tile_scan_kernel<<<1, kScanThreads, 0, st>>>(tcount.as<uint32_t>(), tiles, toffset.as<uint32_t>(), ranges.as<uint2>(),
                                          stat, cap);
     launch_check("tile_scan");
-    scatter_ids_kernel<<<ceil_div(n, 128), 128, 0, st>>>(n, tbox.as<int4>(), tiles_x, toffset.as<uint32_t>(),
+    scatter_ids_kernel<<<ceil_div(n, 256 / kScatterSub), 256, 0, st>>>(n, tbox.as<int4>(), tiles_x, toffset.as<uint32_t>(),
                                                          tcount.as<uint32_t>(), stat, ids.as<uint32_t>());
     launch_check("scatter_ids");
     segment_sort_warp_kernel<<<ceil_div(tiles, 8), 256, 0, st>>>(ranges.as<uint2>(), tiles, ids.as<uint32_t>(),
                                                                   stat);
     launch_check("segment_sort_warp");
-    segment_sort_kernel<<<tiles, 256, 0, st>>>(ranges.as<uint2>(), ids.as<uint32_t>(), scratch.as<uint32_t>(),
-                                               stat);
+    segment_sort_kernel<<<ceil_div(tiles, 256), 256, 0, st>>>(ranges.as<uint2>(), tiles, ids.as<uint32_t>(),
+                                                               scratch.as<uint32_t>(), stat);
     launch_check("segment_sort");
 }
 
@@ -784,7 +834,7 @@ template <int C>
 static void fwd_launch(const RasterWork& rw, float2* d_field, cudaStream_t st) {
     raster_fwd_kernel<C><<<rw.tiles_x * rw.tiles_y, kFwdThreads, 0, st>>>(
         rw.ids.as<uint32_t>(), rw.ranges.as<uint2>(), rw.rec.as<float4>(), rw.shade.as<float4>(),
-        rw.p64.as<double>(), rw.tiles_x, rw.width, rw.height, d_field);
+        rw.p64.as<double>(), rw.n, rw.tiles_x, rw.width, rw.height, d_field);
     launch_check("raster_fwd");
 }
 
@@ -798,13 +848,27 @@ void raster_forward(const RasterWork& rw, float2* d_field, cudaStream_t st) {
     }
 }
 
+static int bwd_variant() {
+    static const int v = [] {
+        const char* e = std::getenv("HS_BWD_VARIANT");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+
 template <int C>
 static void bwd_launch(const RasterWork& rw, const float* d_params, const float2* d_gf,
                        float* d_grads, uint32_t* d_flags, cudaStream_t st) {
     const int warps_per_block = kBwdThreads / 32;
-    raster_bwd_kernel<C><<<ceil_div(rw.n, warps_per_block), kBwdThreads, 0, st>>>(
-        rw.n, rw.rec.as<float4>(), rw.shade.as<float4>(), rw.p64.as<double>(), rw.pbox.as<int4>(),
-        rw.width, rw.height, d_gf, rw.raw.as<float>());
+    auto go = [&](auto kern) {
+        kern<<<ceil_div(rw.n, warps_per_block), kBwdThreads, 0, st>>>(
+            rw.n, rw.rec.as<float4>(), rw.shade.as<float4>(), rw.p64.as<double>(), rw.pbox.as<int4>(),
+            rw.width, rw.height, d_gf, rw.raw.as<float>());
+    };
+    switch (bwd_variant()) {
+        case 1: go(raster_bwd_kernel<C, 3, 2>); break;
+        default: go(raster_bwd_kernel<C, 4, 1>); break;  // measured best at cfg2
+    }
     launch_check("raster_bwd");
     raster_finalize_kernel<C><<<ceil_div(rw.n, 256), 256, 0, st>>>(rw.n, rw.raw.as<float>(), d_params, rw.width,
                                                                    rw.height, d_grads, d_flags);

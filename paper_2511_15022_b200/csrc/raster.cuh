@@ -11,9 +11,9 @@ namespace hs {
 struct RasterWork {
     int n = 0, c = 0, width = 0, height = 0;
     int tiles_x = 0, tiles_y = 0, tile_bits = 0;
-    DevBuf rec;      // 3 float4 per Gaussian (fp32 shading record)
-    DevBuf shade;    // C float4 per Gaussian: amp*cos, amp*sin, cos, sin
-    DevBuf p64;      // 8 doubles per Gaussian (exact fp64 record for boundary rechecks)
+    DevBuf rec;      // 3 x N float4, SoA (fp32 shading record)
+    DevBuf shade;    // C x N float4, SoA: amp*cos, amp*sin, cos, sin
+    DevBuf p64;      // 8 x N doubles, SoA (exact fp64 record for boundary rechecks)
     DevBuf pbox;     // int4 pixel bbox (x0,x1,y0,y1) clamped to the canvas
     DevBuf tbox;     // int4 tile bbox
     DevBuf tcount;   // uint32 Gaussians per tile
