@@ -108,9 +108,7 @@ __global__ void project_kernel(ProjParams P) {
     ty0 = max(ty0, 0);
     tx1 = min(tx1, P.tiles_x - 1);
     ty1 = min(ty1, P.tiles_y - 1);
-    for (int ty = ty0; ty <= ty1; ++ty)
-        for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(P.tcount + ty * P.tiles_x + tx, 1u);
-    P.tbox[g] = make_int4(tx0, tx1, ty0, ty1);
+    P.tbox[g] = make_int4(tx0, tx1, ty0, ty1);  // per-tile counts: count_tiles_kernel
     // pixel bbox (rasterizer.cpp:157-160, 209-212)
     const int x0 = max(0, static_cast<int>(ceil(dsub(px, r))));
     const int x1 = min(P.width - 1, static_cast<int>(floor(dadd(px, r))));
@@ -141,12 +139,14 @@ __global__ void project_kernel(ProjParams P) {
     // per-channel shading (rasterizer.cpp:78-85)
     for (int ch = 0; ch < P.c; ++ch) {
         const size_t i = static_cast<size_t>(g) * P.c + ch;
-        const double a = fmin(fmax(static_cast<double>(amp[i]), 0.0), 1.0);
-        const double ph = pha[i];
-        if (!finite(ph) || !finite(static_cast<double>(amp[i]))) atomicOr(P.status + 2, 1u);
-        const double cp = cos(ph), sp = sin(ph);
-        P.shade[static_cast<size_t>(ch) * N + g] = make_float4(static_cast<float>(a * cp), static_cast<float>(a * sp),
-                                                               static_cast<float>(cp), static_cast<float>(sp));
+        // fp32 shading: only consumed in fp32 (the record is float), so the
+        // phase's sin/cos run in fp32 (accurate range reduction, ~1 ulp)
+        const float a = fminf(fmaxf(amp[i], 0.f), 1.f);
+        const float ph = pha[i];
+        if (!isfinite(ph) || !isfinite(amp[i])) atomicOr(P.status + 2, 1u);
+        float sp, cp;
+        sincosf(ph, &sp, &cp);
+        P.shade[static_cast<size_t>(ch) * N + g] = make_float4(a * cp, a * sp, cp, sp);
     }
     if (!finite(th)) atomicOr(P.status + 2, 1u);
 }
@@ -203,10 +203,22 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(const uint32_t*
 }
 
 // Scatter (duplicate-with-keys, :94-108): tcount is consumed as a countdown.
+// Per-tile Gaussian counts: 16 threads per Gaussian, one fire-and-forget
+// atomic per (Gaussian, tile) pair.
+constexpr int kScatterSub = 16;
+__global__ void __launch_bounds__(256) count_tiles_kernel(int n, const int4* __restrict__ tbox, int tiles_x,
+                                                          uint32_t* __restrict__ tcount) {
+    const int g = blockIdx.x * (256 / kScatterSub) + threadIdx.x / kScatterSub;
+    const int sub = threadIdx.x % kScatterSub;
+    if (g >= n) return;
+    const int4 b = tbox[g];
+    const int nx = b.y - b.x + 1, cnt = nx * (b.w - b.z + 1);
+    for (int k = sub; k < cnt; k += kScatterSub) atomicAdd(tcount + (b.z + k / nx) * tiles_x + b.x + k % nx, 1u);
+}
+
 // 16 threads per Gaussian, thread k handling tiles k, k + 16, ... of its tile
 // box: one slot atomic per thread in the common case, so the atomics' round
 // trips overlap across many resident threads instead of chaining per Gaussian.
-constexpr int kScatterSub = 16;
 __global__ void __launch_bounds__(256) scatter_ids_kernel(int n, const int4* __restrict__ tbox, int tiles_x,
                                                           const uint32_t* __restrict__ toffset,
                                                           uint32_t* __restrict__ tcount,
@@ -807,6 +819,9 @@ void RasterWork::project_and_bin(const float* d_params, cudaStream_t st) {
                  tcount.as<uint32_t>(), stat};
     project_kernel<<<ceil_div(n, 128), 128, 0, st>>>(P);
     launch_check("project");
+    count_tiles_kernel<<<ceil_div(n, 256 / kScatterSub), 256, 0, st>>>(n, tbox.as<int4>(), tiles_x,
+                                                                       tcount.as<uint32_t>());
+    launch_check("count_tiles");
     tile_scan_kernel<<<1, kScanThreads, 0, st>>>(tcount.as<uint32_t>(), tiles, toffset.as<uint32_t>(), ranges.as<uint2>(),
                                          stat, cap);
     launch_check("tile_scan");
