@@ -426,24 +426,13 @@ __device__ __forceinline__ bool cell_hit(float4 r0, float4 r1, float4 r2, float 
     return xhi >= cx0 && xlo <= cx0 + cw;
 }
 
-// fast fp32 contribution with the exact fp64 recheck inside the error band
-__device__ __forceinline__ float fwd_aeff(float m, float4 r1, float4 r2, const double* q, size_t n, int x, int y) {
-    if (m <= r1.w - r2.y) return fminf(0.99f, r2.x * __expf(-0.5f * m));
-    if (m <= r1.w + r2.y) {
-        double G, ae;
-        bool sat;
-        if (exact_contrib(q, n, x, y, G, sat, ae)) return static_cast<float>(ae);
-    }
-    return 0.f;
-}
-
 template <int C>
 __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(
     const uint32_t* __restrict__ ids, const uint2* __restrict__ ranges,
     const float4* __restrict__ rec, const float4* __restrict__ shade,
     const double* __restrict__ p64, int N, int tiles_x, int W, int H, float2* __restrict__ field) {
     __shared__ float4 s_rec[3][kFwdBatch];
-    __shared__ float4 s_sh[C][kFwdBatch];
+    __shared__ float2 s_sh[C][kFwdBatch];  // (amp cos, amp sin) per channel
     __shared__ uint32_t s_id[kFwdBatch];
     const int tile = blockIdx.x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
@@ -467,7 +456,10 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(
             s_rec[1][threadIdx.x] = rec[static_cast<size_t>(N) + g];
             s_rec[2][threadIdx.x] = rec[2 * static_cast<size_t>(N) + g];
 #pragma unroll
-            for (int c = 0; c < C; ++c) s_sh[c][threadIdx.x] = shade[static_cast<size_t>(c) * N + g];
+            for (int c = 0; c < C; ++c) {
+                const float4 sh = shade[static_cast<size_t>(c) * N + g];
+                s_sh[c][threadIdx.x] = make_float2(sh.x, sh.y);
+            }
         }
         __syncthreads();
         for (int sub = 0; sub < cnt; sub += 32) {
@@ -477,7 +469,7 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(
                 hit = cell_hit(s_rec[0][j], s_rec[1][j], s_rec[2][j], static_cast<float>(cx0),
                                static_cast<float>(cy0), 7.f, 7.f);
             uint32_t mask = __ballot_sync(0xffffffffu, hit);
-            while (mask) {
+            while (mask) {  // warp-uniform: hits in ascending id order
                 const int jj = sub + __ffs(mask) - 1;
                 mask &= mask - 1;
                 const float4 r0 = s_rec[0][jj], r1 = s_rec[1][jj], r2 = s_rec[2][jj];
@@ -487,18 +479,23 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(
                 const float ex = dx * r1.x;
                 const float mA = dx * (ex + 2.f * dyA * r1.y) + dyA * dyA * r1.z;
                 const float mB = dx * (ex + 2.f * dyB * r1.y) + dyB * dyB * r1.z;
-                const double* q = p64 + s_id[jj];
-                const float aA = fwd_aeff(mA, r1, r2, q, N, x, y);
-                const float aB = fwd_aeff(mB, r1, r2, q, N, x, y + 4);
-                if (aA > 0.f || aB > 0.f) {
+                // fast fp32 decision outside the error band [cut - tol, cut + tol]
+                const float lo = r1.w - r2.y, hi = r1.w + r2.y;
+                float aA = mA <= lo ? fminf(0.99f, r2.x * __expf(-0.5f * mA)) : 0.f;
+                float aB = mB <= lo ? fminf(0.99f, r2.x * __expf(-0.5f * mB)) : 0.f;
+                const bool bandA = mA > lo && mA <= hi, bandB = mB > lo && mB <= hi;
+                if (__any_sync(0xffffffffu, bandA || bandB)) {  // rare: exact fp64 decision
+                    const double* q = p64 + s_id[jj];
+                    double G, ae;
+                    bool sat;
+                    if (bandA) aA = exact_contrib(q, N, x, y, G, sat, ae) ? static_cast<float>(ae) : 0.f;
+                    if (bandB) aB = exact_contrib(q, N, x, y + 4, G, sat, ae) ? static_cast<float>(ae) : 0.f;
+                }
 #pragma unroll
-                    for (int c = 0; c < C; ++c) {
-                        const float4 sh = s_sh[c][jj];
-                        accA[c].x = fmaf(sh.x, aA, accA[c].x);
-                        accA[c].y = fmaf(sh.y, aA, accA[c].y);
-                        accB[c].x = fmaf(sh.x, aB, accB[c].x);
-                        accB[c].y = fmaf(sh.y, aB, accB[c].y);
-                    }
+                for (int c = 0; c < C; ++c) {
+                    const float2 sh = s_sh[c][jj];
+                    accA[c] = f2fma(f2splat(aA), sh, accA[c]);
+                    accB[c] = f2fma(f2splat(aB), sh, accB[c]);
                 }
             }
         }
