@@ -131,7 +131,7 @@ __global__ void project_kernel(ProjParams P) {
     P.rec[g] = make_float4(px_hi, py_hi, px_lo, py_lo);
     P.rec[N + g] = make_float4(static_cast<float>(i00), static_cast<float>(i01),
                                static_cast<float>(i11), static_cast<float>(mahal_cutoff));
-    P.rec[2 * N + g] = make_float4(static_cast<float>(alpha), static_cast<float>(tol),
+    P.rec[2 * N + g] = make_float4(static_cast<float>(log2(alpha)), static_cast<float>(tol),
                                    static_cast<float>(det_inv), static_cast<float>(1.0 / i00));
     double* q = P.p64 + g;
     q[0] = px; q[N] = py; q[2 * N] = i00; q[3 * N] = i01; q[4 * N] = i11; q[5 * N] = mahal_cutoff;
@@ -476,13 +476,17 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(
                 const float dx = (fx - r0.x) - r0.z;
                 const float dyA = (fy - r0.y) - r0.w;
                 const float dyB = dyA + 4.f;
-                const float ex = dx * r1.x;
-                const float mA = dx * (ex + 2.f * dyA * r1.y) + dyA * dyA * r1.z;
-                const float mB = dx * (ex + 2.f * dyB * r1.y) + dyB * dyB * r1.z;
-                // fast fp32 decision outside the error band [cut - tol, cut + tol]
+                // Sigma^-1 (dx, dy) for both pixels (rows y, y + 4), then the quadratic forms
+                const float2 i0 = make_float2(r1.x, r1.y), i1 = make_float2(r1.y, r1.z);
+                const float2 eA = f2fma(f2splat(dyA), i1, f2mul(f2splat(dx), i0));
+                const float2 eB = f2fma(f2splat(4.f), i1, eA);
+                const float mA = fmaf(dx, eA.x, dyA * eA.y);
+                const float mB = fmaf(dx, eB.x, dyB * eB.y);
+                // fast fp32 decision outside the error band [cut - tol, cut + tol];
+                // alpha e^{-m/2} = 2^(log2 alpha - m / (2 ln 2))
                 const float lo = r1.w - r2.y, hi = r1.w + r2.y;
-                float aA = mA <= lo ? fminf(0.99f, r2.x * __expf(-0.5f * mA)) : 0.f;
-                float aB = mB <= lo ? fminf(0.99f, r2.x * __expf(-0.5f * mB)) : 0.f;
+                float aA = mA <= lo ? fminf(0.99f, ex2f(fmaf(mA, kNegHalfLog2e, r2.x))) : 0.f;
+                float aB = mB <= lo ? fminf(0.99f, ex2f(fmaf(mB, kNegHalfLog2e, r2.x))) : 0.f;
                 const bool bandA = mA > lo && mA <= hi, bandB = mB > lo && mB <= hi;
                 if (__any_sync(0xffffffffu, bandA || bandB)) {  // rare: exact fp64 decision
                     const double* q = p64 + s_id[jj];
@@ -549,7 +553,7 @@ __global__ void __launch_bounds__(kBwdThreads, MINB) raster_bwd_kernel(
     const float2 p_hi = make_float2(r0.x, r0.y), p_lo = make_float2(r0.z, r0.w);
     const float i00 = r1.x, i01 = r1.y, i11 = r1.z, cut = r1.w;
     const float2 row0 = make_float2(i00, i01), row1 = make_float2(i01, i11);
-    const float alpha = r2.x, tol = r2.y, detI = r2.z, inv_i00 = r2.w;
+    const float alpha = exp2f(r2.x), tol = r2.y, detI = r2.z, inv_i00 = r2.w;  // r2.x = log2 alpha
     const float M = cut + tol;
     const float ratio = i01 * inv_i00;
     const float2* gch[C];  // channel planes of the gradient field
@@ -629,7 +633,7 @@ __global__ void __launch_bounds__(kBwdThreads, MINB) raster_bwd_kernel(
                 const float2 e = f2fma(f2splat(dxy.x), row0, f2mul(f2splat(dxy.y), row1));  // Sigma^-1 (dx, dy)
                 const float m = fmaf(dxy.x, e.x, dxy.y * e.y);
                 if (m > M) continue;
-                float G = __expf(-0.5f * m), aeff;
+                float G = ex2f(m * kNegHalfLog2e), aeff;
                 bool sat;
                 float aG = alpha * G;
                 if (m <= cut - tol && fabsf(aG - 0.99f) > 1e-5f) {
