@@ -159,7 +159,7 @@ struct SsimState {
     float h2[kWin];    // ... of I t
     float2 s01[kWin];  // horizontal spreads of (g1, g2) (ring by valid row)
     float s2[kWin];    // ... of g3
-    float ssum, rsum;                    // per-thread sums (<= kSR terms each; fp64 across threads)
+    double ssum, rsum;  // per-thread fp64 sums (same arithmetic as the recon-only kernel, loss.cpp:320-329)
 };
 
 // Asynchronous global->shared copies (cp.async); src_bytes = 0 zero-fills.
@@ -297,7 +297,7 @@ struct SsimCta {
             const float rb1 = __fdividef(1.f, b1), rb2 = __fdividef(1.f, b2);
             const float inv = rb1 * rb2;
             const float sv = a1 * a2 * inv;
-            if (t >= kHalo && v >= y0 && v < y0 + kSR) st.ssum += sv;
+            if (t >= kHalo && v >= y0 && v < y0 + kSR) st.ssum += static_cast<double>(sv);
             gv.x = 2.f * (a2 * inv * m2 - sv * rb1 * m1 + sv * rb2 * m1 - a1 * inv * m2);
             gv.y = -sv * rb2;
             gv.z = 2.f * a1 * inv;
@@ -331,7 +331,7 @@ struct SsimCta {
             if (kind == kLossTraining) {  // loss_recon_grad, loss.cpp:317-341
                 const float d = iv - tv;
                 const float k = 1.f + mk + tv * tv;
-                st.rsum += d * d * k;
+                st.rsum += static_cast<double>(d * d * k);
                 g = fmaf(wr * d, k, g);
             }
             const size_t p = plane_off + static_cast<size_t>(y) * W + x;
@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(kSW, MINB) ssim_loss_kernel(LossArgs a, Win wi
         st.h01[i] = st.s01[i] = make_float2(0.f, 0.f);
         st.h2[i] = st.s2[i] = 0.f;
     }
-    st.ssum = st.rsum = 0.f;
+    st.ssum = st.rsum = 0.0;
     // steps s = 0 .. kSteps-1 cover valid rows v = y0-20 .. y0+kSR-1 (output rows y0..y0+kSR-1);
     // rows past the image are guarded inside the step
     constexpr int kSteps = kSR + 2 * kHalo;
@@ -405,9 +405,9 @@ __global__ void __launch_bounds__(kSW, MINB) ssim_loss_kernel(LossArgs a, Win wi
     cp_wait<0>();
     using BR = cub::BlockReduce<double, kSW>;
     __shared__ typename BR::TempStorage tmp;
-    const double r_tot = BR(tmp).Sum(static_cast<double>(st.rsum));
+    const double r_tot = BR(tmp).Sum(st.rsum);
     __syncthreads();
-    const double s_tot = BR(tmp).Sum(static_cast<double>(st.ssum));
+    const double s_tot = BR(tmp).Sum(st.ssum);
     if (threadIdx.x == 0) {
         const int slot = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
         a.partials[2 * slot] = r_tot;
