@@ -6,7 +6,7 @@
 // loss_mse_grad :277-294; proj/core/src/optimizer.cpp:59-123 (cosine_lr, Adan).
 //
 // SSIM kernel (sliding window): one CTA of 128 threads owns a strip of 118
-// output columns and kSR output rows of one (plane, channel) and walks down
+// output columns and SR output rows of one (plane, channel) and walks down
 // it row by row.  Thread t owns column c = x0 - 10 + t of both the valid
 // (H-10)x(W-10) grid and the output grid.  Per step it
 //   1. correlates its input row horizontally (I, I^2, I t from a shared row),
@@ -36,8 +36,9 @@ namespace {
 constexpr int kWin = 11, kHalo = 10;
 constexpr int kSW = 128;            // threads per CTA = valid/output columns touched per strip
 constexpr int kSO = kSW - kHalo;    // output columns per strip
-constexpr int kSR = 101;            // output rows per CTA (kSR + 20 steps = 11 x 11-step ring cycles);
-                                    // 1080p x 3 channels -> 561 CTAs = one wave at 4 CTAs/SM
+// output rows per CTA: SR + 20 steps must be whole 11-step ring cycles; the
+// variants trade pipeline fill (20 / SR) against a single wave at MINB CTAs/SM
+// (1080p x 3 channels: SR 101 -> 561 CTAs, SR 145 -> 408 CTAs)
 constexpr int kSIn = kSW + kHalo;   // input columns per strip
 constexpr int kLossThreads = 256;   // elementwise kernels
 constexpr double kSsimC1 = 0.01 * 0.01, kSsimC2 = 0.03 * 0.03, kSsimWeight = 0.005;  // loss.hpp:12-14
@@ -154,12 +155,13 @@ __device__ __forceinline__ void corr11x3r(const Win& w, F2 f2, F1 f1, float2& a0
     a2 = az + bz;
 }
 
+// One 11-row register ring per thread.  Producer threads keep the horizontal
+// correlations of (I, I^2 | I t) in it, consumer threads the horizontal spreads
+// of (g1, g2 | g3): the same registers, role-dependent meaning.
 struct SsimState {
-    float2 h01[kWin];  // horizontal correlations of (I, I^2) (ring by row; packed pair)
-    float h2[kWin];    // ... of I t
-    float2 s01[kWin];  // horizontal spreads of (g1, g2) (ring by valid row)
-    float s2[kWin];    // ... of g3
-    double ssum, rsum;  // per-thread fp64 sums (same arithmetic as the recon-only kernel, loss.cpp:320-329)
+    float2 r01[kWin];  // packed pair
+    float r2[kWin];
+    double sum;        // producer: SSIM map sum; consumer: recon sum (fp64, as loss.cpp:320-329)
 };
 
 // Asynchronous global->shared copies (cp.async); src_bytes = 0 zero-fills.
@@ -185,7 +187,7 @@ struct SsimSmem {
     float4 gm[2][kSW];          // (g1, g2, g3, -) of the valid row being spread
 };
 
-template <bool FROM_FIELD>
+template <bool FROM_FIELD, int SR>
 struct SsimCta {
     using Raw = typename std::conditional<FROM_FIELD, float2, float>::type;
     const LossArgs& a;
@@ -253,34 +255,27 @@ struct SsimCta {
         }
     }
 
-    // One row step s (valid row v = y0 - 20 + s), ring slot U = s mod 11.
+    // Producer half (threads 0..127) of row step s: valid row v = y0 - 20 + s,
+    // ring slot U = s mod 11.  Horizontal correlation of input row r = v + 10,
+    // vertical correlation of rows v..v+10, SSIM map and derivative maps of row v
+    // -> gm[s & 1]; next input row -> in[(s + 1) & 1].
     template <int U>
-    __device__ __forceinline__ void step(SsimState& st, int s, float& mk_next) const {
+    __device__ __forceinline__ void produce(SsimState& st, int s) const {
         const int v = y0 - 2 * kHalo + s;
-        const int r = v + kHalo;  // input row correlated horizontally this step
+        const int r = v + kHalo;
         const int buf = s & 1;
         issue(r + kPD, v + kPD);
-        const int y = v, x = c;
-        const bool out_ok = t >= kHalo && y >= y0 && y < y0 + kSR && y < H && x < W;
-        const float mk = mk_next;
-        if (kind == kLossTraining) {  // mask of the next step's output row, one step ahead
-            const int yn = y + 1;
-            mk_next = (t >= kHalo && yn >= y0 && yn < y0 + kSR && yn < H && x < W)
-                          ? (mask[static_cast<size_t>(yn) * W + x] ? 1.f : 0.f) : 0.f;
-        }
-        // 1. horizontal correlation of input row r (ssim_channel corr_x, loss.cpp:103-111)
-        {
+        {  // ssim_channel corr_x (loss.cpp:103-111)
             const float4* row = &S.in[buf][t];
-            corr11x3(win, [&](int j) { return row[j]; }, st.h01[U], st.h2[U]);
+            corr11x3(win, [&](int j) { return row[j]; }, st.r01[U], st.r2[U]);
         }
-        // 2. vertical correlation of rows v..v+10 + SSIM map and derivative maps
         cp_wait<kPD - 1>();  // groups of rows <= r + 1 (and stats of v) have landed
         float4 gv = make_float4(0.f, 0.f, 0.f, 0.f);
         if (v >= 0 && v < vh && c >= 0 && c < vw) {
             float2 mm;
             float exy;
-            corr11x3r(win, [&](int i) { return st.h01[(U + 1 + i) % kWin]; },
-                      [&](int i) { return st.h2[(U + 1 + i) % kWin]; }, mm, exy);
+            corr11x3r(win, [&](int i) { return st.r01[(U + 1 + i) % kWin]; },
+                      [&](int i) { return st.r2[(U + 1 + i) % kWin]; }, mm, exy);
             const float m1 = mm.x, exx = mm.y;
             const float2 ts = S.ts[v & (kTsRing - 1)][t];
             const float C1 = static_cast<float>(kSsimC1), C2 = static_cast<float>(kSsimC2);
@@ -297,30 +292,44 @@ struct SsimCta {
             const float rb1 = __fdividef(1.f, b1), rb2 = __fdividef(1.f, b2);
             const float inv = rb1 * rb2;
             const float sv = a1 * a2 * inv;
-            if (t >= kHalo && v >= y0 && v < y0 + kSR) st.ssum += static_cast<double>(sv);
+            if (t >= kHalo && v >= y0 && v < y0 + SR) st.sum += static_cast<double>(sv);
             gv.x = 2.f * (a2 * inv * m2 - sv * rb1 * m1 + sv * rb2 * m1 - a1 * inv * m2);
             gv.y = -sv * rb2;
             gv.z = 2.f * a1 * inv;
         }
         S.gm[buf][t] = gv;
         convert(r + 1, buf ^ 1);
-        __syncthreads();
-        // 3. horizontal spread of g over valid columns c-10..c, then vertical
-        //    spread over valid rows v-10..v (spread_t, loss.cpp:135-152)
+    }
+
+    // Consumer half (threads 128..255, column t = tid - 128) of row step s:
+    // horizontal spread of gm[s & 1] over valid columns c-10..c, vertical spread
+    // over valid rows v-10..v (spread_t, loss.cpp:135-152), output row y = v.
+    template <int U>
+    __device__ __forceinline__ void consume(SsimState& st, int s, float& mk_next) const {
+        const int v = y0 - 2 * kHalo + s;
+        const int buf = s & 1;
+        const int y = v, x = c;
+        const bool out_ok = t >= kHalo && y >= y0 && y < y0 + SR && y < H && x < W;
+        const float mk = mk_next;
+        if (kind == kLossTraining) {  // mask of the next step's output row, one step ahead
+            const int yn = y + 1;
+            mk_next = (t >= kHalo && yn >= y0 && yn < y0 + SR && yn < H && x < W)
+                          ? (mask[static_cast<size_t>(yn) * W + x] ? 1.f : 0.f) : 0.f;
+        }
         {
             // threads t < 10 own no output column: their spread row stays 0
             const float4* gr = &S.gm[buf][max(t, kHalo)];
-            corr11x3(win, [&](int j) { return gr[-j]; }, st.s01[U], st.s2[U]);
+            corr11x3(win, [&](int j) { return gr[-j]; }, st.r01[U], st.r2[U]);
             if (t < kHalo) {
-                st.s01[U] = make_float2(0.f, 0.f);
-                st.s2[U] = 0.f;
+                st.r01[U] = make_float2(0.f, 0.f);
+                st.r2[U] = 0.f;
             }
         }
         if (out_ok) {
             float2 G12;
             float G3;
-            corr11x3r(win, [&](int i) { return st.s01[(U + kWin - i) % kWin]; },
-                      [&](int i) { return st.s2[(U + kWin - i) % kWin]; }, G12, G3);
+            corr11x3r(win, [&](int i) { return st.r01[(U + kWin - i) % kWin]; },
+                      [&](int i) { return st.r2[(U + kWin - i) % kWin]; }, G12, G3);
             const float G1 = G12.x, G2 = G12.y;
             const int slot = y & (kRaw - 1);
             const Raw uu = S.rawU[slot][t];
@@ -331,7 +340,7 @@ struct SsimCta {
             if (kind == kLossTraining) {  // loss_recon_grad, loss.cpp:317-341
                 const float d = iv - tv;
                 const float k = 1.f + mk + tv * tv;
-                st.rsum += static_cast<double>(d * d * k);
+                st.sum += static_cast<double>(d * d * k);
                 g = fmaf(wr * d, k, g);
             }
             const size_t p = plane_off + static_cast<size_t>(y) * W + x;
@@ -343,17 +352,21 @@ struct SsimCta {
     }
 };
 
-template <bool FROM_FIELD, int MINB>
-__global__ void __launch_bounds__(kSW, MINB) ssim_loss_kernel(LossArgs a, Win win) {
+// Producer/consumer warp groups: threads [0, 128) produce SSIM rows, threads
+// [128, 256) consume them one step behind, so the two halves of a row step run
+// concurrently and each thread carries a single 11-row register ring.
+template <bool FROM_FIELD, int MINB, int SR>
+__global__ void __launch_bounds__(2 * kSW, MINB) ssim_loss_kernel(LossArgs a, Win win) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    using Raw = typename SsimCta<FROM_FIELD>::Raw;
+    using Raw = typename SsimCta<FROM_FIELD, SR>::Raw;
     SsimSmem<Raw>& S = *reinterpret_cast<SsimSmem<Raw>*>(smem_raw);
     const int plane = blockIdx.z;  // l * C + c
     const int l = plane / a.C, ch = plane - l * a.C;
-    SsimCta<FROM_FIELD> K{a, win, S};
-    K.t = threadIdx.x;
+    const bool producer = threadIdx.x < kSW;
+    SsimCta<FROM_FIELD, SR> K{a, win, S};
+    K.t = producer ? threadIdx.x : threadIdx.x - kSW;
     K.x0 = blockIdx.x * kSO;
-    K.y0 = blockIdx.y * kSR;
+    K.y0 = blockIdx.y * SR;
     K.c = K.x0 - kHalo + K.t;
     K.H = a.H;
     K.W = a.W;
@@ -373,41 +386,40 @@ __global__ void __launch_bounds__(kSW, MINB) ssim_loss_kernel(LossArgs a, Win wi
     SsimState st;
 #pragma unroll
     for (int i = 0; i < kWin; ++i) {
-        st.h01[i] = st.s01[i] = make_float2(0.f, 0.f);
-        st.h2[i] = st.s2[i] = 0.f;
+        st.r01[i] = make_float2(0.f, 0.f);
+        st.r2[i] = 0.f;
     }
-    st.ssum = st.rsum = 0.0;
-    // steps s = 0 .. kSteps-1 cover valid rows v = y0-20 .. y0+kSR-1 (output rows y0..y0+kSR-1);
-    // rows past the image are guarded inside the step
-    constexpr int kSteps = kSR + 2 * kHalo;
+    st.sum = 0.0;
+    // steps s = 0 .. kSteps-1 cover valid rows v = y0-20 .. y0+SR-1 (output rows y0..y0+SR-1);
+    // rows past the image are guarded inside the steps
+    constexpr int kSteps = SR + 2 * kHalo;
     static_assert(kSteps % kWin == 0, "whole ring cycles");
     const int r0 = K.y0 - kHalo, v0 = K.y0 - 2 * kHalo;
+    if (producer) {
 #pragma unroll
-    for (int q = 0; q < kPD; ++q) K.issue(r0 + q, v0 + q);
-    cp_wait<kPD - 1>();
-    K.convert(r0, 0);
+        for (int q = 0; q < kPD; ++q) K.issue(r0 + q, v0 + q);
+        cp_wait<kPD - 1>();
+        K.convert(r0, 0);
+    }
     float mk_next = 0.f;  // first output row comes 20 steps in
     __syncthreads();
+#define HS_SSIM_STEP(U)                                      \
+    if (producer) K.template produce<U>(st, sb + U);         \
+    __syncthreads();                                         \
+    if (!producer) K.template consume<U>(st, sb + U, mk_next);
 #pragma unroll 1
     for (int sb = 0; sb < kSteps; sb += kWin) {
-        K.template step<0>(st, sb + 0, mk_next);
-        K.template step<1>(st, sb + 1, mk_next);
-        K.template step<2>(st, sb + 2, mk_next);
-        K.template step<3>(st, sb + 3, mk_next);
-        K.template step<4>(st, sb + 4, mk_next);
-        K.template step<5>(st, sb + 5, mk_next);
-        K.template step<6>(st, sb + 6, mk_next);
-        K.template step<7>(st, sb + 7, mk_next);
-        K.template step<8>(st, sb + 8, mk_next);
-        K.template step<9>(st, sb + 9, mk_next);
-        K.template step<10>(st, sb + 10, mk_next);
+        HS_SSIM_STEP(0) HS_SSIM_STEP(1) HS_SSIM_STEP(2) HS_SSIM_STEP(3) HS_SSIM_STEP(4) HS_SSIM_STEP(5)
+        HS_SSIM_STEP(6) HS_SSIM_STEP(7) HS_SSIM_STEP(8) HS_SSIM_STEP(9) HS_SSIM_STEP(10)
     }
-    cp_wait<0>();
-    using BR = cub::BlockReduce<double, kSW>;
+#undef HS_SSIM_STEP
+    if (producer) cp_wait<0>();
+    // producers hold the SSIM sums, consumers the recon sums
+    using BR = cub::BlockReduce<double, 2 * kSW>;
     __shared__ typename BR::TempStorage tmp;
-    const double r_tot = BR(tmp).Sum(st.rsum);
+    const double r_tot = BR(tmp).Sum(producer ? 0.0 : st.sum);
     __syncthreads();
-    const double s_tot = BR(tmp).Sum(st.ssum);
+    const double s_tot = BR(tmp).Sum(producer ? st.sum : 0.0);
     if (threadIdx.x == 0) {
         const int slot = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
         a.partials[2 * slot] = r_tot;
@@ -582,6 +594,16 @@ __global__ void nonfinite_kernel(const float* g, int64_t n, uint32_t* flag) {
         }
 }
 
+constexpr int kSRv0 = 145, kSRv1 = 101;
+int ssim_variant() {
+    static const int v = [] {
+        const char* e = std::getenv("HS_SSIM_VARIANT");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+int ssim_rows() { return ssim_variant() == 1 ? kSRv1 : kSRv0; }
+
 unsigned grid_for(int64_t n, int threads) {
     const int64_t b = (n + threads - 1) / threads;
     return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(b, 148 * 16)));
@@ -591,7 +613,7 @@ unsigned grid_for(int64_t n, int threads) {
 
 int loss_partial_slots(int kind, int L, int C, int H, int W) {
     if (kind == kLossTraining || kind == kLossSsim)
-        return ceil_div(W, kSO) * ceil_div(H, kSR) * L * C;
+        return ceil_div(W, kSO) * ceil_div(H, ssim_rows()) * L * C;
     const int64_t total = static_cast<int64_t>(L) * C * H * W;
     return static_cast<int>(grid_for(total, kLossThreads));
 }
@@ -599,23 +621,20 @@ int loss_partial_slots(int kind, int L, int C, int H, int W) {
 int loss_launch(const LossArgs& a, cudaStream_t st) {
     if (a.kind == kLossTraining || a.kind == kLossSsim) {
         require(a.H >= kWin && a.W >= kWin, "ssim: image smaller than the 11x11 window");
-        const dim3 grid(ceil_div(a.W, kSO), ceil_div(a.H, kSR), a.L * a.C);
+        const dim3 grid(ceil_div(a.W, kSO), ceil_div(a.H, ssim_rows()), a.L * a.C);
         static const Win win = ssim_window_f32();
         require(a.tstats != nullptr, "ssim: target statistics missing");
-        static const int minb = [] {
-            const char* e = std::getenv("HS_SSIM_MINB");
-            return e ? std::atoi(e) : 4;
-        }();
         auto go = [&](auto kern, size_t smem) {
             HS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-            kern<<<grid, kSW, smem, st>>>(a, win);
+            kern<<<grid, 2 * kSW, smem, st>>>(a, win);
         };
+        const bool v1 = ssim_variant() == 1;
         if (a.field) {
-            if (minb == 3) go(ssim_loss_kernel<true, 3>, sizeof(SsimSmem<float2>));
-            else go(ssim_loss_kernel<true, 4>, sizeof(SsimSmem<float2>));
+            if (v1) go(ssim_loss_kernel<true, 4, kSRv1>, sizeof(SsimSmem<float2>));
+            else go(ssim_loss_kernel<true, 3, kSRv0>, sizeof(SsimSmem<float2>));
         } else {
-            if (minb == 3) go(ssim_loss_kernel<false, 3>, sizeof(SsimSmem<float>));
-            else go(ssim_loss_kernel<false, 4>, sizeof(SsimSmem<float>));
+            if (v1) go(ssim_loss_kernel<false, 4, kSRv1>, sizeof(SsimSmem<float>));
+            else go(ssim_loss_kernel<false, 3, kSRv0>, sizeof(SsimSmem<float>));
         }
         launch_check("ssim_loss");
         return static_cast<int>(grid.x * grid.y * grid.z);
