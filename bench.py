@@ -41,6 +41,11 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=50)
     p.add_argument("--profile-steps", type=int, default=10)
+    p.add_argument("--shard", choices=("replicas", "channels", "planes"), default="replicas",
+                   help="N>1: replicas = one scene per GPU (weak scaling, no collective); "
+                        "channels = the wavelengths of one scene split over ranks (<= C ranks), "
+                        "planes = the depth planes of one scene (cfg3) split over ranks; both "
+                        "all-reduce gradients over NCCL (strong scaling)")
     return p.parse_args()
 
 
@@ -191,19 +196,109 @@ def run_reference(args):
     print(json.dumps(line))
 
 
-def config_of(name, cfg, world):
+def config_of(name, cfg, world, shard="replicas"):
+    par = {"replicas": f"replicas x{world} (one scene per GPU, no collective)",
+           "channels": f"wavelength shards x{world} (one scene; NCCL all-reduce of the 6N geometry gradients)",
+           "planes": f"plane shards x{world} (one scene; NCCL all-reduce of the gradient buffer)"}[shard]
+    seed = "init_gaussians(seed 42+rank)" if shard == "replicas" else "init_gaussians(seed 42)"
     return {"workload": f"{name}: {cfg['width']}x{cfg['height']} x{cfg['channels']} wavelengths, "
-                        f"{cfg['count']} Gaussians, {cfg['planes']} plane(s), pad 2, init_gaussians(seed 42+rank)",
+                        f"{cfg['count']} Gaussians, {cfg['planes']} plane(s), pad 2, {seed}",
             "width": cfg["width"], "height": cfg["height"], "channels": cfg["channels"],
-            "gaussians": cfg["count"], "planes": cfg["planes"], "pad_factor": 2,
-            "parallelism": f"replicas x{world} (one scene per GPU, no collective)",
+            "gaussians": cfg["count"], "planes": cfg["planes"], "pad_factor": 2, "parallelism": par,
             "l2": "no flush: per-step working set ~0.45 GB > 126 MB L2"}
+
+
+def run_sharded(args):
+    """--shard channels|planes: one scene split over the ranks with a real
+    gradient exchange (parallel.ChannelShardedStep / ShardedStep); eager steps
+    (the NCCL all-reduce sits between the trainer's two halves), timed with CUDA
+    events on the trainer stream, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2511_15022_b200 import holo, parallel as P, synthetic as S
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    wl = S.workload(args.workload, scene=0)
+    cfg = wl["cfg"]
+    C_, h, w, n, L = cfg["channels"], cfg["height"], cfg["width"], cfg["count"], cfg["planes"]
+    g32 = {k: np.asarray(v, np.float32).astype(np.float64) for k, v in wl["gaussians"].items()}
+    total = args.warmup + args.steps + 2
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        if args.shard == "channels":
+            if world > C_:
+                raise SystemExit(f"--shard channels needs <= {C_} ranks")
+            b, e = P.channel_shard(C_, rank, world)
+            gs = P.slice_channels(g32, n, C_, b, e)
+            tr = holo.Trainer(holo.GaussianSet(n, e - b, **gs), w, h,
+                              holo.RealField(e - b, h, w, wl["target"][b:e].astype(np.float32).astype(np.float64)),
+                              wl["masks"], wl["distances"], holo.PropagationSpec(tuple(wl["wavelengths"][b:e])),
+                              total_steps=total, channels_total=C_)
+            step = P.ChannelShardedStep(tr, n, e - b, C_, h, w, L)
+        else:
+            tr = holo.Trainer(holo.GaussianSet(n, C_, **g32), w, h,
+                              holo.RealField(C_, h, w, wl["target"].astype(np.float32).astype(np.float64)),
+                              wl["masks"], wl["distances"], holo.PropagationSpec(tuple(wl["wavelengths"])),
+                              total_steps=total, plane_range=P.plane_shard(L, rank, world))
+            step = P.ShardedStep(tr, C_, h, w, L)
+        for _ in range(args.warmup):
+            loss = step.step()
+        stream.synchronize()
+        sampler = ClockSampler(local)
+        sampler.start()
+        time.sleep(0.3)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        l0 = holo.kernel_launch_count()
+        for _ in range(args.steps):
+            loss = step.step()
+        e1.record(stream)
+        e1.synchronize()
+        torch.cuda.synchronize()
+        launches = holo.kernel_launch_count() - l0
+        if world > 1:
+            dist.barrier()
+        clocks = sampler.stop()
+        ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+    if rank == 0:
+        peak, peak_src = peaks()
+        B = algorithmic_bytes(cfg, tr.last_loss()[1])
+        line = {
+            "metric": METRIC, "value": 1e3 / ms, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+            "config": config_of(args.workload, cfg, world, args.shard),
+            "step_roofline": {"bound": "hbm", "achieved": B / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                              "frac": B / (ms * 1e-3) / 1e9 / peak / world, "peak_source": peak_src,
+                              "note": "whole-job algorithmic bytes over world x peak"},
+            "gpu_launches": int(launches), "clocks": clocks, "loss": loss,
+            "timing": "eager steps (NCCL all-reduce between forward_backward and apply_update), "
+                      "CUDA events on the trainer stream, max over ranks",
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.shard != "replicas":
+        run_sharded(args)
         return
     import torch
     import torch.distributed as dist

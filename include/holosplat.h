@@ -140,9 +140,14 @@ typedef struct {
     int total_steps;            /* cosine schedule horizon (config.steps) */
     const float* h_target;      /* C x H x W linear intensity in [0,1] */
     const uint8_t* h_masks;     /* L x H x W (build_masks) */
-    /* Optional plane/channel shard for multi-GPU (owned planes [plane_begin,
+    /* Optional plane shard for multi-GPU (owned planes [plane_begin,
      * plane_end)); loss normalisers always use the global L.  0,0 = all. */
     int plane_begin, plane_end;
+    /* Optional wavelength (channel) shard: this trainer holds c of the
+     * channels_total channels of the scene (its spec, target and amplitude /
+     * phase columns are that slice); the loss normalisers use channels_total.
+     * 0 = c (no channel sharding). */
+    int channels_total;
 } hs_trainer_config;
 
 hs_status hs_trainer_create(hs_ctx* ctx, const hs_trainer_config* cfg, hs_trainer** out);

@@ -433,10 +433,10 @@ def _check_pair(recon, target, masks):       # :80-87
             raise ValueError("loss: reconstruction shape mismatch")
 
 
-def loss_recon_grad(recon, target, masks, L_norm=None):  # :317-341
+def loss_recon_grad(recon, target, masks, L_norm=None, C_norm=None):  # :317-341
     _check_pair(recon, target, masks)
     L = len(recon) if L_norm is None else L_norm
-    n = target.size
+    n = target.size if C_norm is None else target.size // target.shape[0] * C_norm  # channel shard: global C
     w = 2.0 / (n * L)
     k = 1.0 + masks[:, None, :, :].astype(np.float64) + target[None] ** 2
     d = recon - target[None]
@@ -450,7 +450,7 @@ def loss_mse_grad(recon, target, masks):     # :277-294
     return float(np.sum(d * d) / (n * L)), (2.0 / (n * L)) * d
 
 
-def loss_ssim_grad(recon, target, masks, L_norm=None):  # :361-383
+def loss_ssim_grad(recon, target, masks, L_norm=None, C_norm=None):  # :361-383
     _check_pair(recon, target, masks)
     total, count = 0.0, 0
     grads = np.zeros_like(recon)
@@ -462,6 +462,8 @@ def loss_ssim_grad(recon, target, masks, L_norm=None):  # :361-383
             grads[l, ch] = gr
     if L_norm is not None:  # plane shard: global normaliser
         count = count // recon.shape[0] * L_norm
+    if C_norm is not None:  # channel shard: global normaliser
+        count = count // recon.shape[1] * C_norm
     return 1.0 - total / count, grads * (-1.0 / count), total
 
 
@@ -520,10 +522,11 @@ GROUP_LRS = (("position", 1e-2), ("scale", 5e-3), ("rotation", 1e-3), ("amplitud
 
 
 def step_grads(g, n, c, width, height, target, masks, distances, wavelengths, pitch=3.74e-6, pad=2,
-               aperture=0.0, planes=None, L_norm=None):
+               aperture=0.0, planes=None, L_norm=None, C_norm=None):
     """Forward + backward of pipeline.cpp:256-279 for the planes in `planes`
-    (all by default).  With a plane subset and L_norm the loss normalisers are
-    the global ones, so summing the per-shard results gives the full step."""
+    (all by default).  With a plane subset and L_norm (or a channel slice of
+    the scene and C_norm) the loss normalisers are the global ones, so summing
+    the per-shard results gives the full step."""
     L = len(distances)
     sel = list(range(L)) if planes is None else list(planes)
     re, im = rasterize_forward(g, n, c, width, height)
@@ -532,11 +535,12 @@ def step_grads(g, n, c, width, height, target, masks, distances, wavelengths, pi
     I = np.abs(U) ** 2
     m_sel = masks[sel]
     Lg = L if L_norm is None else L_norm
-    lr, gr = loss_recon_grad(I, target, m_sel, Lg)
-    _, gs, ssum = loss_ssim_grad(I, target, m_sel, Lg)
+    lr, gr = loss_recon_grad(I, target, m_sel, Lg, C_norm)
+    _, gs, ssum = loss_ssim_grad(I, target, m_sel, Lg, C_norm)
     gi = gr + kSsimWeight * gs
     du = 2.0 * U * gi
     back = propagate_multi_backward(du, wavelengths, pitch, pad, aperture, d_sel)
     grads = rasterize_backward(g, n, c, back.real, back.imag)
-    count = Lg * c * (height - 10) * (width - 10)
-    return dict(recon_sum=lr * target.size * Lg, ssim_sum=ssum, count=count, grads=grads)
+    Cg = c if C_norm is None else C_norm
+    count = Lg * Cg * (height - 10) * (width - 10)
+    return dict(recon_sum=lr * (target.size // c * Cg) * Lg, ssim_sum=ssum, count=count, grads=grads)

@@ -55,7 +55,7 @@ class hs_trainer_config(C.Structure):
                 ("planes", C.c_int), ("distances", C.POINTER(C.c_double)),
                 ("spec", hs_prop_spec), ("total_steps", C.c_int),
                 ("h_target", C.POINTER(C.c_float)), ("h_masks", C.POINTER(C.c_uint8)),
-                ("plane_begin", C.c_int), ("plane_end", C.c_int)]
+                ("plane_begin", C.c_int), ("plane_end", C.c_int), ("channels_total", C.c_int)]
 
 
 _SIGS = {

@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(NT, MINB) scols_fwdL_kernel(ColArgs a, const f
         const TfConst t = a.tf[l * a.C + c];
         float2* dst = a.out + ((static_cast<size_t>(l) * a.C + c) * a.ntiles + tile) * tile_elems - shift;
         sfft::run<N, CC, NT, +1, sfft::Full, sfft::Half>(
-            A, tw, tid, RAD{},
+            A, sfft::launder(tw), sfft::launder(tid), RAD{},
             sfft::in_smem(Sp, [&](int i, int, float2 v) { return cmul(v, transfer_fast<false>(t, mx, wrapped(i, N))); }),
             sfft::out_fn([&](int i, int cc, float2 v) { dst[i * CC + cc] = v; }));
     }
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(NT, MINB) scols_bwdL_kernel(ColArgs a, const f
         const float2* src = a.in + ((static_cast<size_t>(l) * a.C + c) * a.ntiles + tile) * tile_elems - shift;
         const bool first = l == 0;
         sfft::run<N, CC, NT, -1, sfft::Half, sfft::Full>(
-            A, tw, tid, RAD{}, sfft::in_fn([&](int i, int cc) { return src[i * CC + cc]; }),
+            A, sfft::launder(tw), sfft::launder(tid), RAD{}, sfft::in_fn([&](int i, int cc) { return src[i * CC + cc]; }),
             sfft::out_smem(Z, [&](int i, int, float2 v, float2& slot) {
                 const float2 w = cmul(v, transfer_fast<true>(t, mx, wrapped(i, N)));
                 slot = first ? w : cadd(slot, w);
@@ -215,10 +215,12 @@ RowPlan row_plan() {
     return RowPlan{srows_fwd_kernel<N, RB, NT, CCO, RAD>, srows_inv_kernel<N, RB, NT, CCO, RAD>, NT, RB,
                    [](int n) { return sfft::twiddle_table(n, RAD{}); }};
 }
+// The multi-plane kernels hold two tiles in shared memory (spectrum + work),
+// so they run one CTA per SM regardless of MINB: they get the full register file.
 template <int N, int CC, int NT, int MINB, class RAD>
 ColPlan col_plan() {
     return ColPlan{scols_fwd1_kernel<N, CC, NT, MINB, RAD>, scols_bwd1_kernel<N, CC, NT, MINB, RAD>,
-                   scols_fwdL_kernel<N, CC, NT, MINB, RAD>, scols_bwdL_kernel<N, CC, NT, MINB, RAD>, NT, CC,
+                   scols_fwdL_kernel<N, CC, NT, 1, RAD>, scols_bwdL_kernel<N, CC, NT, 1, RAD>, NT, CC,
                    [](int n) { return sfft::twiddle_table(n, RAD{}); }};
 }
 

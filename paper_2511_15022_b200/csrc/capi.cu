@@ -65,7 +65,7 @@ static CtxWork& work_of(hs_ctx* ctx) {
 
 struct hs_trainer {
     hs_ctx* ctx = nullptr;
-    int n = 0, c = 0, w = 0, h = 0, L = 0, L_total = 0, plane0 = 0, total_steps = 0;
+    int n = 0, c = 0, w = 0, h = 0, L = 0, L_total = 0, plane0 = 0, total_steps = 0, C_total = 0;
     std::vector<double> distances;
     std::vector<double> wavelengths;
     hs_prop_spec spec{};
@@ -388,7 +388,7 @@ static void trainer_enqueue_fwd_bwd(hs_trainer* t, cudaStream_t st) {
     asm_forward(t->aw, t->field.as<float2>(), t->planes.as<float2>(), st, prof ? t->ev + 3 : nullptr);
     LossArgs a{kLossTraining, t->L, t->L_total, t->plane0, t->c, t->h, t->w, nullptr, t->planes.as<float2>(),
                t->target.as<float>(), t->tstats.as<float2>(), t->masks.as<uint8_t>(), nullptr,
-               t->dplanes.as<float2>(), t->partials.as<double>()};
+               t->dplanes.as<float2>(), t->partials.as<double>(), t->C_total};
     const int used = loss_launch(a, st);
     loss_finalize(a, used, t->out3.as<double>(), st);
     mark(6);
@@ -434,6 +434,9 @@ hs_status hs_trainer_create(hs_ctx* ctx, const hs_trainer_config* cfg, hs_traine
         t->w = cfg->width;
         t->h = cfg->height;
         t->L_total = cfg->planes;
+        require(cfg->channels_total == 0 || cfg->channels_total >= cfg->c,
+                "trainer: channels_total must be 0 or >= the shard's channel count");
+        t->C_total = cfg->channels_total > 0 ? cfg->channels_total : cfg->c;
         const int pb = (cfg->plane_end > cfg->plane_begin) ? cfg->plane_begin : 0;
         const int pe = (cfg->plane_end > cfg->plane_begin) ? cfg->plane_end : cfg->planes;
         require(pb >= 0 && pe <= cfg->planes, "trainer: plane shard out of range");

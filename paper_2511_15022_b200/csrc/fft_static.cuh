@@ -202,6 +202,21 @@ __device__ __forceinline__ void run(float2* buf, const float2* tw, int tid, Radi
     chain<N, CC, NT, S, 1, LIN, LOUT, IN, OUT, R...>(buf, tw, tid, in, out);
 }
 
+// Opaque copies of a value / pointer: inside loops over planes they stop the
+// compiler from hoisting every stage's (loop-invariant) twiddle loads and smem
+// offsets out of the loop, which pins ~100 registers and spills.
+template <class T>
+__device__ __forceinline__ T* launder(T* p) {
+    T* q;
+    asm volatile("mov.b64 %0, %1;" : "=l"(q) : "l"(p));
+    return q;
+}
+__device__ __forceinline__ int launder(int v) {
+    int q;
+    asm volatile("mov.b32 %0, %1;" : "=r"(q) : "r"(v));
+    return q;
+}
+
 // Host: stage twiddle table for a plan (N - 1 entries, forward sign).
 template <int... R>
 std::vector<float2> twiddle_table(int N, Radices<R...>) {

@@ -377,9 +377,9 @@ __global__ void __launch_bounds__(2 * kSW, MINB) ssim_loss_kernel(LossArgs a, Wi
     K.tgt = a.target + static_cast<size_t>(ch) * a.H * a.W;
     K.tst = a.tstats + static_cast<size_t>(ch) * K.vh * K.vw;
     K.mask = a.masks + static_cast<size_t>(a.plane0 + l) * a.H * a.W;
-    const double n_el = static_cast<double>(a.C) * a.H * a.W;
+    const double n_el = static_cast<double>(a.channels_norm()) * a.H * a.W;
     K.wr = static_cast<float>(2.0 / (n_el * a.L_norm));
-    const double count = static_cast<double>(a.L_norm) * a.C * K.vh * K.vw;
+    const double count = static_cast<double>(a.L_norm) * a.channels_norm() * K.vh * K.vw;
     K.ws = static_cast<float>((a.kind == kLossTraining ? kSsimWeight : 1.0) * (-1.0 / count));
     K.init_sources();
 
@@ -430,7 +430,7 @@ __global__ void __launch_bounds__(2 * kSW, MINB) ssim_loss_kernel(LossArgs a, Wi
 // recon / mse only: elementwise
 template <bool FROM_FIELD>
 __global__ void __launch_bounds__(kLossThreads) pixel_loss_kernel(LossArgs a, int64_t total) {
-    const double n_el = static_cast<double>(a.C) * a.H * a.W;
+    const double n_el = static_cast<double>(a.channels_norm()) * a.H * a.W;
     const float wr = static_cast<float>(2.0 / (n_el * a.L_norm));
     const int64_t hw = static_cast<int64_t>(a.H) * a.W;
     const int64_t chw = hw * a.C;
@@ -648,8 +648,8 @@ int loss_launch(const LossArgs& a, cudaStream_t st) {
 }
 
 void loss_finalize(const LossArgs& a, int slots, double* d_out3, cudaStream_t st) {
-    const double n_el = static_cast<double>(a.C) * a.H * a.W;
-    const double count = static_cast<double>(a.L_norm) * a.C * std::max(a.H - kWin + 1, 0) *
+    const double n_el = static_cast<double>(a.channels_norm()) * a.H * a.W;
+    const double count = static_cast<double>(a.L_norm) * a.channels_norm() * std::max(a.H - kWin + 1, 0) *
                          std::max(a.W - kWin + 1, 0);
     loss_finalize_kernel<<<1, 1024, 0, st>>>(a.partials, slots, a.kind, n_el, a.L_norm, count, d_out3);
     launch_check("loss_finalize");

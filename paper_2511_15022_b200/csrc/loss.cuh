@@ -21,6 +21,8 @@ struct LossArgs {
     float* grad;             // dL/dI (L x C x H x W), or nullptr
     float2* du;              // dL/dU = 2 U dL/dI (L x C x H x W), or nullptr
     double* partials;        // 2 per CTA: recon-or-mse sum, ssim sum
+    int C_norm = 0;          // global channel count for the normalisers (channel sharding); 0 = C
+    __host__ __device__ int channels_norm() const { return C_norm > 0 ? C_norm : C; }
 };
 
 // Launches the loss kernel(s); returns the number of partial slots written.

@@ -546,7 +546,7 @@ class Trainer:
 
     def __init__(self, gaussians: GaussianSet, width: int, height: int, target: RealField,
                  masks: np.ndarray, distances: Sequence[float], spec: PropagationSpec, total_steps: int,
-                 plane_range=None, device=None):
+                 plane_range=None, device=None, channels_total=None):
         self.n, self.c = gaussians.count, gaussians.channels
         self.width, self.height = width, height
         self.L = len(distances)
@@ -559,7 +559,8 @@ class Trainer:
         cfg = hs_trainer_config(self.n, self.c, width, height, self.L,
                                 C.cast(self._dist, C.POINTER(C.c_double)), self._spec, int(total_steps),
                                 tgt.ctypes.data_as(C.POINTER(C.c_float)),
-                                msk.ctypes.data_as(C.POINTER(C.c_uint8)), pb, pe)
+                                msk.ctypes.data_as(C.POINTER(C.c_uint8)), pb, pe,
+                                int(channels_total or 0))
         h = C.c_void_p()
         self._ctx = ctx_handle(device)
         check(_lib.load().hs_trainer_create(self._ctx, C.byref(cfg), C.byref(h)))

@@ -8,6 +8,14 @@
   gradient of its planes with the global normalisers (L_total, SSIM count),
   one NCCL all-reduce (sum) of the (6+2C)N gradient buffer makes them the full
   gradient, and every rank applies the identical Adan update.
+* Wavelength sharding (cfg2, up to C ranks): the channels of a scene are
+  independent through propagation and loss; amplitude/phase of channel c only
+  see channel c, the geometry (position, scale, rotation, opacity) gets a sum
+  over channels.  Rank r owns a contiguous block of channels: its trainer is
+  built on that slice (wavelengths, target, amplitude/phase columns) with the
+  global channel count for the loss normalisers, one NCCL all-reduce of the
+  geometry gradients (6N floats) completes them, and every rank applies the
+  identical geometry update plus the update of its own amplitude/phase.
 * Scene replicas (cfg2 at N>1, cfg5): independent problems, no collective.
 
 The collective is torch.distributed over NCCL (gloo on CPU for the tests).
@@ -28,6 +36,26 @@ def plane_shard(L: int, rank: int, world: int) -> Tuple[int, int]:
     base, extra = divmod(L, world)
     begin = rank * base + min(rank, extra)
     return begin, begin + base + (1 if rank < extra else 0)
+
+
+def channel_shard(C: int, rank: int, world: int) -> Tuple[int, int]:
+    """Contiguous block [begin, end) of the C channels (wavelengths) for `rank`."""
+    return plane_shard(C, rank, world)
+
+
+def slice_channels(groups: dict, n: int, C: int, begin: int, end: int) -> dict:
+    """The six parameter groups of a scene restricted to channels [begin, end):
+    amplitude and phase are N x C row-major (gaussian_set.hpp:14-19)."""
+    out = dict(groups)
+    for k in ("amplitude", "phase"):
+        out[k] = groups[k].reshape(n, C)[:, begin:end].reshape(-1).copy()
+    return out
+
+
+def geometry_ranges(n: int, c: int):
+    """[begin, end) ranges of the channel-independent groups in the flat layout
+    [pre_position 2N | pre_scale 2N | rotation N | amplitude NC | phase NC | pre_opacity N]."""
+    return [(0, 5 * n), (5 * n + 2 * n * c, 6 * n + 2 * n * c)]
 
 
 def combine_loss(recon_sum: float, ssim_sum: float, C: int, H: int, W: int, L: int,
@@ -61,6 +89,34 @@ class ShardedStep:
         parts = torch.tensor(self.tr.loss_partials(), dtype=torch.float64,
                              device=g.device if g.is_cuda else "cpu")
         if dist.is_initialized() and dist.get_world_size(self.group) > 1:
+            dist.all_reduce(parts, op=dist.ReduceOp.SUM, group=self.group)
+        return combine_loss(float(parts[0]), float(parts[1]), self.C, self.H, self.W, self.L)
+
+
+class ChannelShardedStep:
+    """One optimisation step of a wavelength-sharded trainer: `trainer` holds
+    c_local of C_total channels (holo.Trainer(..., channels_total=C_total) on
+    slice_channels(...)); the geometry gradients are all-reduced, amplitude and
+    phase stay local."""
+
+    def __init__(self, trainer, n, c_local, C_total, H, W, L, group=None):
+        self.tr, self.n, self.c = trainer, n, c_local
+        self.C, self.H, self.W, self.L = C_total, H, W, L
+        self.group = group
+
+    def step(self) -> float:
+        self.tr.forward_backward()
+        g = self.tr.grads_tensor()
+        multi = dist.is_initialized() and dist.get_world_size(self.group) > 1
+        if multi:
+            if g.is_cuda:
+                torch.cuda.current_stream().synchronize()
+            for b, e in geometry_ranges(self.n, self.c):
+                dist.all_reduce(g[b:e], op=dist.ReduceOp.SUM, group=self.group)
+        self.tr.apply_update()
+        parts = torch.tensor(self.tr.loss_partials(), dtype=torch.float64,
+                             device=g.device if g.is_cuda else "cpu")
+        if multi:
             dist.all_reduce(parts, op=dist.ReduceOp.SUM, group=self.group)
         return combine_loss(float(parts[0]), float(parts[1]), self.C, self.H, self.W, self.L)
 

@@ -339,3 +339,41 @@ def test_plane_sharded_trainers_sum_to_full_step(holo):
         parts += np.array(t.loss_partials())
     assert rel_l2(gs, gfull) < 1e-5
     assert parts[0] == pytest.approx(pf[0], rel=1e-6) and parts[1] == pytest.approx(pf[1], rel=1e-6)
+
+
+def test_channel_sharded_trainers_match_full_step(holo):
+    """Wavelength sharding: trainers owning channels [0,2) and [2,3) of a C=3
+    scene (hs_trainer_config.channels_total = 3) give geometry gradients that
+    sum to the full step's, amplitude/phase gradients equal to its columns, and
+    loss partials that sum to its partials."""
+    from paper_2511_15022_b200 import parallel as P
+    c, w, h, n, L = 3, 96, 64, 1500, 2
+    g = f32(S.init_gaussians(n, c, w, h, 42))
+    img = S.synthetic_image(42, c, h, w)
+    masks = S.build_masks(S.synthetic_depth(43, h, w), L, True)
+    dist = S.make_depth_planes(L, 3e-3, 2e-3)
+    wl = S.WAVELENGTHS[c]
+    full = holo.Trainer(holo.GaussianSet(n, c, **g), w, h, holo.RealField(c, h, w, img), masks, dist,
+                        holo.PropagationSpec(wl), 10)
+    full.forward_backward()
+    gf = full.grads_tensor().cpu().numpy().astype(np.float64)
+    pf = np.array(full.loss_partials())
+    geo_sum, parts = 0.0, np.zeros(2)
+    for r in range(2):
+        b, e = P.channel_shard(c, r, 2)
+        cl = e - b
+        gs = P.slice_channels(g, n, c, b, e)
+        t = holo.Trainer(holo.GaussianSet(n, cl, **gs), w, h, holo.RealField(cl, h, w, img[b:e]), masks, dist,
+                         holo.PropagationSpec(wl[b:e]), 10, channels_total=c)
+        t.forward_backward()
+        gr = t.grads_tensor().cpu().numpy().astype(np.float64)
+        geo = np.concatenate([gr[lo:hi] for lo, hi in P.geometry_ranges(n, cl)])
+        geo_sum = geo_sum + geo
+        for k, off in (("amplitude", 5 * n), ("phase", 5 * n + n * c)):
+            mine = gr[5 * n + (0 if k == "amplitude" else n * cl):][:n * cl].reshape(n, cl)
+            ref = gf[off:off + n * c].reshape(n, c)[:, b:e]
+            assert rel_l2(mine, ref) < 1e-5, k
+        parts += np.array(t.loss_partials())
+    geo_full = np.concatenate([gf[lo:hi] for lo, hi in P.geometry_ranges(n, c)])
+    assert rel_l2(geo_sum, geo_full) < 1e-5
+    assert parts[0] == pytest.approx(pf[0], rel=1e-6) and parts[1] == pytest.approx(pf[1], rel=1e-6)

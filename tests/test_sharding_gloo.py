@@ -118,3 +118,65 @@ def test_sharded_step_orchestration_gloo(tmp_path):
     assert np.array_equal(a, b)                 # identical update on every rank
     assert np.all(a[:16] == 3.0)                # 1 + 2: the summed gradient reached Adan
     assert a[16] == pytest.approx(P.combine_loss(30.0, 2.0, 1, 16, 16, 2))
+
+
+# ---- wavelength (channel) sharding ---------------------------------------------------------
+
+def _channel_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g, target, masks, d = scene()
+    b, e = P.channel_shard(C, rank, world)
+    gs = P.slice_channels(g, N, C, b, e)
+    r = O.step_grads(gs, N, e - b, W, H, target[b:e], masks, d, S.WAVELENGTHS[C][b:e], C_norm=C)
+    flat = torch.from_numpy(np.concatenate([r["grads"][k] for k in O.GROUPS]))
+    for lo, hi in P.geometry_ranges(N, e - b):  # the collective of ChannelShardedStep
+        dist.all_reduce(flat[lo:hi])
+    parts = torch.tensor([r["recon_sum"], r["ssim_sum"]], dtype=torch.float64)
+    dist.all_reduce(parts)
+    np.save(f"{out}_{rank}_grads.npy", flat.numpy())
+    if rank == 0:
+        np.save(out + "_parts.npy", parts.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_channel_shard_partitions_and_ranges():
+    for world in (1, 2, 3):
+        seen = []
+        for r in range(world):
+            b, e = P.channel_shard(3, r, world)
+            seen += list(range(b, e))
+        assert seen == [0, 1, 2]
+    n, c = 5, 2
+    geo = sum(e - b for b, e in P.geometry_ranges(n, c))
+    assert geo == 6 * n  # position 2N + scale 2N + rotation N + opacity N
+
+
+def test_channel_sharded_step_equals_full_step_gloo(tmp_path):
+    """Two ranks owning channels [0,2) and [2,3): all-reduced geometry gradients
+    equal the full step's, each rank's amplitude/phase gradients equal the full
+    step's columns, and the combined loss equals the full loss."""
+    out = str(tmp_path / "c")
+    mp.spawn(_channel_worker, args=(2, free_port(), out), nprocs=2, join=True)
+    g, target, masks, d = scene()
+    full = O.step_grads(g, N, C, W, H, target, masks, d, S.WAVELENGTHS[C])
+    fg = full["grads"]
+    for rank in range(2):
+        b, e = P.channel_shard(C, rank, 2)
+        cl = e - b
+        got = np.load(f"{out}_{rank}_grads.npy")
+        o = 0
+        parts = {}
+        for k in O.GROUPS:
+            size = {"amplitude": N * cl, "phase": N * cl}.get(k, fg[k].size)
+            parts[k] = got[o:o + size]
+            o += size
+        for k in ("pre_position", "pre_scale", "rotation", "pre_opacity"):
+            assert np.linalg.norm(parts[k] - fg[k]) <= 1e-12 * np.linalg.norm(fg[k]), k
+        for k in ("amplitude", "phase"):
+            ref = fg[k].reshape(N, C)[:, b:e].reshape(-1)
+            assert np.linalg.norm(parts[k] - ref) <= 1e-12 * max(np.linalg.norm(ref), 1e-30), k
+    p = np.load(out + "_parts.npy")
+    loss = P.combine_loss(p[0], p[1], C, H, W, L)
+    assert loss == pytest.approx(P.combine_loss(full["recon_sum"], full["ssim_sum"], C, H, W, L), rel=1e-12)
