@@ -131,6 +131,31 @@ hs_status hs_adan_step(hs_ctx* ctx, const hs_adan_config* cfg, const char* group
 /* cosine_lr (optimizer.cpp:59-64). */
 hs_status hs_cosine_lr(int step, int total_steps, double lr_max, double lr_min, double* out);
 
+/* ---- phase-only hologram conversion (convert.hpp, convert.cpp:20-184) ------------ */
+/* dpac_encode (convert.cpp:31-60) BEFORE canonicalize_phase -- the hosts
+ * canonicalise in fp64 like the reference: mode 0 DpacMode::direct,
+ * 1 DpacMode::classical.  d_field C x H x W complex64 -> d_phase C x H x W. */
+hs_status hs_dpac_encode(hs_ctx* ctx, const float* d_field, int c, int h, int w, int mode, float* d_phase);
+/* poh_field (convert.cpp:62-69): d_field = e^{i d_phase}, count elements. */
+hs_status hs_poh_field(hs_ctx* ctx, const float* d_phase, int64_t count, float* d_field);
+typedef struct {
+    int c, height, width, planes;  /* guide / target shape, L */
+    const double* distances;       /* L plane distances */
+    hs_prop_spec spec;
+    const float* h_target;         /* C x H x W target intensity */
+    const uint8_t* h_masks;        /* L x H x W (TargetStack::masks) */
+    int steps;
+    double lambda_comp, lambda_field, lr;  /* RandomPohOptions (convert.hpp) */
+} hs_poh_config;
+/* convert_random_poh_field (convert.cpp:71-174), device resident.  d_phase
+ * holds the initial raster (Rng(seed).uniform(-pi, pi) in element order) and
+ * receives the optimised phase, not yet canonicalised; h_loss (steps doubles,
+ * nullable) receives every step's loss.  Errors: HS_EINVAL for no planes or
+ * steps < 1 (the reference's messages), HS_ENONFINITE "Adan: non-finite
+ * gradient in group phase". */
+hs_status hs_convert_random_poh_field(hs_ctx* ctx, const hs_poh_config* cfg, const float* d_guide_field,
+                                      float* d_phase, double* h_loss);
+
 /* ---- trainer: the fused step loop body (pipeline.cpp:253-297) ------------------ */
 typedef struct {
     int n, c, width, height;

@@ -374,3 +374,40 @@ class Trainer:
 
 def set_thread_count(n):
     lib().ref_set_thread_count(int(n))
+
+
+# ---- POH conversion (convert.cpp) ---------------------------------------------------------------
+def dpac_encode(re, im, mode=0):
+    c, h, w = re.shape
+    re = np.ascontiguousarray(re, dtype=np.float64)
+    im = np.ascontiguousarray(im, dtype=np.float64)
+    out = np.zeros((c, h, w))
+    _check(lib().ref_dpac_encode(c, h, w, _p(re), _p(im), int(mode), _p(out)))
+    return out
+
+
+def poh_field(phase):
+    c, h, w = phase.shape
+    phase = np.ascontiguousarray(phase, dtype=np.float64)
+    re, im = np.zeros((c, h, w)), np.zeros((c, h, w))
+    _check(lib().ref_poh_field(c, h, w, _p(phase), _p(re), _p(im)))
+    return re, im
+
+
+def convert_random_poh_field(gre, gim, target, depth, L, distances, spec, steps, seed=0,
+                             lambda_comp=0.1, lambda_field=0.01, lr=2.5e-3, log_every=50, near_is_high=True):
+    """The reference's convert_random_poh_field; target stack = make_target_stack(target, depth, L)."""
+    c, h, w = gre.shape
+    gre = np.ascontiguousarray(gre, dtype=np.float64)
+    gim = np.ascontiguousarray(gim, dtype=np.float64)
+    target = np.ascontiguousarray(target, dtype=np.float64)
+    depth = np.ascontiguousarray(depth, dtype=np.float64)
+    d = np.ascontiguousarray(distances, dtype=np.float64)
+    wl, sa = _spec_args(spec)
+    phase = np.zeros((c, h, w))
+    loss = np.zeros(steps + 1)
+    n = _check(lib().ref_convert_random_poh_field(
+        c, h, w, _p(gre), _p(gim), _p(target), _p(depth), int(near_is_high), _p(d), int(L), *sa, int(steps),
+        C.c_uint64(seed), _d(lambda_comp), _d(lambda_field), _d(lr), int(log_every), _p(phase), _p(loss),
+        len(loss)))
+    return phase, loss[:n]

@@ -22,6 +22,7 @@
 #include "holo/complex_field.hpp"
 #include "holo/field_core.hpp"
 #include "holo/gaussian_set.hpp"
+#include "holo/convert.hpp"
 #include "holo/loss.hpp"
 #include "holo/optimizer.hpp"
 #include "holo/oracles.hpp"
@@ -293,6 +294,53 @@ int ref_transfer_function(const double* wl, int nwl, double pitch, int pad, doub
             out4[4 * i + 3] = g[i].inside_bandlimit ? 1.0 : 0.0;
         }
     });
+}
+
+// ---- POH conversion (convert.cpp) -------------------------------------------------
+int ref_dpac_encode(int c, int h, int w, const double* re, const double* im, int mode, double* out) {
+    return guard([&] {
+        const PhaseOnlyHologram p = dpac_encode(make_field(c, h, w, re, im),
+                                                mode == 0 ? DpacMode::direct : DpacMode::classical);
+        std::memcpy(out, p.phase.values.data(), p.phase.values.size() * sizeof(double));
+    });
+}
+int ref_poh_field(int c, int h, int w, const double* phase, double* re, double* im) {
+    return guard([&] {
+        PhaseOnlyHologram p;
+        p.phase = make_real(c, h, w, phase);
+        store_field(poh_field(p), re, im);
+    });
+}
+// convert_random_poh_field with the target stack built from (target, depth, L,
+// near_is_high) like make_target_stack; phase_out C x H x W, loss_out
+// (n_loss capacity) receives the loss history, returns its length.
+int ref_convert_random_poh_field(int c, int h, int w, const double* gre, const double* gim,
+                                 const double* target, const double* depth, int near_is_high,
+                                 const double* dist, int L, const double* wl, double pitch, int pad,
+                                 double aperture, int steps, uint64_t seed, double lambda_comp,
+                                 double lambda_field, double lr, int log_every, double* phase_out,
+                                 double* loss_out, int n_loss) {
+    int len = 0;
+    const int rc = guard([&] {
+        DepthPlaneSet planes;
+        planes.count = L;
+        planes.distances.assign(dist, dist + L);
+        const TargetStack t = make_target_stack(make_real(c, h, w, target), make_real(1, h, w, depth), L,
+                                                near_is_high != 0);
+        RandomPohOptions o;
+        o.steps = steps;
+        o.seed = seed;
+        o.lambda_comp = lambda_comp;
+        o.lambda_field = lambda_field;
+        o.lr = lr;
+        o.log_every = log_every;
+        const RandomPohResult r = convert_random_poh_field(make_field(c, h, w, gre, gim), planes, t,
+                                                           make_spec(c, wl, pitch, pad, aperture), o);
+        std::memcpy(phase_out, r.poh.phase.values.data(), r.poh.phase.values.size() * sizeof(double));
+        len = static_cast<int>(r.loss_history.size());
+        for (int i = 0; i < std::min(len, n_loss); ++i) loss_out[i] = r.loss_history[i];
+    });
+    return rc < 0 ? rc : len;
 }
 
 // ---- loss (loss.cpp) -----------------------------------------------------------

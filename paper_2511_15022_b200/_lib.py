@@ -58,7 +58,18 @@ class hs_trainer_config(C.Structure):
                 ("plane_begin", C.c_int), ("plane_end", C.c_int), ("channels_total", C.c_int)]
 
 
+class hs_poh_config(C.Structure):
+    _fields_ = [("c", C.c_int), ("height", C.c_int), ("width", C.c_int), ("planes", C.c_int),
+                ("distances", C.POINTER(C.c_double)), ("spec", hs_prop_spec),
+                ("h_target", C.POINTER(C.c_float)), ("h_masks", C.POINTER(C.c_uint8)), ("steps", C.c_int),
+                ("lambda_comp", C.c_double), ("lambda_field", C.c_double), ("lr", C.c_double)]
+
+
 _SIGS = {
+    "hs_dpac_encode": [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p],
+    "hs_poh_field": [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p],
+    "hs_convert_random_poh_field": [C.c_void_p, C.POINTER(hs_poh_config), C.c_void_p, C.c_void_p,
+                                    C.POINTER(C.c_double)],
     "hs_ctx_create": [C.c_int, C.POINTER(C.c_void_p)],
     "hs_ctx_destroy": [C.c_void_p],
     "hs_ctx_set_stream": [C.c_void_p, C.c_void_p],

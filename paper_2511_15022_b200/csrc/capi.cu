@@ -8,6 +8,7 @@
 
 #include "asm.cuh"
 #include "loss.cuh"
+#include "convert.cuh"
 #include "raster.cuh"
 
 namespace hs {
@@ -41,6 +42,8 @@ struct CtxWork {
     RasterWork rw;
     AsmWork aw;
     DevBuf flags, partials, out3, tstats;
+    PohWork poh;
+    DevBuf amax, poh_target, poh_masks, poh_loss;
 };
 
 }  // namespace
@@ -294,6 +297,62 @@ extern "C" hs_status hs_propagate_multi_backward(hs_ctx* ctx, const hs_prop_spec
         asm_backward(aw, reinterpret_cast<const float2*>(d_grads), reinterpret_cast<float2*>(d_out),
                      ctx->stream);
         HS_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+// ---- POH conversion ---------------------------------------------------------------------------
+extern "C" hs_status hs_dpac_encode(hs_ctx* ctx, const float* d_field, int c, int h, int w, int mode,
+                                    float* d_phase) {
+    return guard([&] {
+        require(c >= 0 && h >= 0 && w >= 0, "dpac_encode: bad shape");
+        require(mode == 0 || mode == 1, "dpac_encode: unknown mode");
+        CtxWork& cw = work_of(ctx);
+        cw.amax.reserve(sizeof(unsigned) * std::max(c, 1));
+        dpac_encode(reinterpret_cast<const float2*>(d_field), c, h, w, mode, cw.amax.as<unsigned>(), d_phase,
+                    ctx->stream);
+    });
+}
+
+extern "C" hs_status hs_poh_field(hs_ctx* ctx, const float* d_phase, int64_t count, float* d_field) {
+    return guard([&] { phase_to_field(d_phase, count, reinterpret_cast<float2*>(d_field), ctx->stream); });
+}
+
+extern "C" hs_status hs_convert_random_poh_field(hs_ctx* ctx, const hs_poh_config* cfg, const float* d_guide_field,
+                                                 float* d_phase, double* h_loss) {
+    return guard([&] {
+        require(cfg != nullptr, "convert_random_poh: null config");
+        require(cfg->planes >= 1, "convert_random_poh: no depth planes");          // convert.cpp:80-81
+        require(cfg->steps >= 1, "convert_random_poh: steps must be >= 1");        // :84
+        check_spec(&cfg->spec, cfg->c);
+        const int c = cfg->c, h = cfg->height, w = cfg->width, L = cfg->planes;
+        CtxWork& cw = work_of(ctx);
+        cudaStream_t st = ctx->stream;
+        const size_t chw = static_cast<size_t>(c) * h * w, hw = static_cast<size_t>(h) * w;
+        cw.poh_target.reserve(sizeof(float) * chw);
+        cw.poh_masks.reserve(hw * L);
+        cw.poh_loss.reserve(sizeof(double) * cfg->steps);
+        HS_CUDA(cudaMemcpyAsync(cw.poh_target.p, cfg->h_target, sizeof(float) * chw, cudaMemcpyHostToDevice, st));
+        HS_CUDA(cudaMemcpyAsync(cw.poh_masks.p, cfg->h_masks, hw * L, cudaMemcpyHostToDevice, st));
+        PohProblem p;
+        p.C = c;
+        p.H = h;
+        p.W = w;
+        p.L = L;
+        p.pad = cfg->spec.pad_factor;
+        p.target = cw.poh_target.as<float>();
+        p.masks = cw.poh_masks.as<uint8_t>();
+        PohWork& pw = cw.poh;
+        pw.prepare(p);
+        pw.aw.L = L;
+        pw.aw.set_transfer(cfg->spec, cfg->distances, cfg->distances, st);
+        random_poh_run(pw, reinterpret_cast<const float2*>(d_guide_field), d_phase, cfg->steps, cfg->lambda_comp,
+                       cfg->lambda_field, cfg->lr, cw.poh_loss.as<double>(), st);
+        uint32_t flag = 0;
+        HS_CUDA(cudaMemcpyAsync(&flag, pw.flag.p, sizeof(flag), cudaMemcpyDeviceToHost, st));
+        if (h_loss)
+            HS_CUDA(cudaMemcpyAsync(h_loss, cw.poh_loss.p, sizeof(double) * cfg->steps, cudaMemcpyDeviceToHost, st));
+        HS_CUDA(cudaStreamSynchronize(st));
+        if (flag) throw Error(HS_ENONFINITE, "Adan: non-finite gradient in group phase");
     });
 }
 

@@ -10,12 +10,15 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <numbers>
+#include <random>
 #include <stdexcept>
 #include <string>
 #include <thread>
 #include <vector>
 
 #include "holo/complex_field.hpp"
+#include "holo/convert.hpp"
 #include "holo/field_core.hpp"
 #include "holo/gaussian_set.hpp"
 #include "holo/loss.hpp"
@@ -569,6 +572,102 @@ void parallel_for(int64_t begin, int64_t end, const std::function<void(int64_t, 
     }
     fn(begin, std::min(end, begin + chunk));
     for (auto& t : pool) t.join();
+}
+
+// ---- phase-only hologram conversion (convert.hpp; convert.cpp:20-184) ----------------------------
+namespace {
+constexpr double kTwoPi = 2.0 * std::numbers::pi;
+}  // namespace
+
+double canonicalize_phase(double value) {  // convert.cpp:20-25 (fp64, like the reference)
+    double r = std::fmod(value, kTwoPi);
+    if (r < 0.0) r += kTwoPi;
+    if (r >= kTwoPi) r -= kTwoPi;
+    return r;
+}
+
+void canonicalize_phase(RealField& raster) {
+    for (double& v : raster.values) v = canonicalize_phase(v);
+}
+
+PhaseOnlyHologram dpac_encode(const ComplexField& field, DpacMode mode) {
+    Dev in = upload_field({&field});
+    Dev out(field.size() * sizeof(float));
+    check(hs_dpac_encode(ctx(), in.as<float>(), field.channels, field.height, field.width,
+                         mode == DpacMode::direct ? 0 : 1, out.as<float>()));
+    std::vector<float> h(field.size());
+    out.download(h.data(), h.size() * sizeof(float));
+    PhaseOnlyHologram poh;
+    poh.format = PohFormat::smooth;
+    poh.phase = RealField(field.channels, field.height, field.width);
+    for (size_t i = 0; i < h.size(); ++i) poh.phase.values[i] = canonicalize_phase(static_cast<double>(h[i]));
+    return poh;
+}
+
+ComplexField poh_field(const PhaseOnlyHologram& poh) {
+    const RealField& ph = poh.phase;
+    std::vector<float> h(ph.values.size());
+    for (size_t i = 0; i < h.size(); ++i) h[i] = static_cast<float>(ph.values[i]);
+    Dev in(h.size() * sizeof(float));
+    in.upload(h.data(), h.size() * sizeof(float));
+    Dev out(h.size() * 2 * sizeof(float));
+    check(hs_poh_field(ctx(), in.as<float>(), static_cast<int64_t>(h.size()), out.as<float>()));
+    ComplexField f(ph.channels, ph.height, ph.width);
+    download_field(out, 0, f);
+    return f;
+}
+
+RandomPohResult convert_random_poh_field(const ComplexField& guide_field, const DepthPlaneSet& planes,
+                                         const TargetStack& target, const PropagationSpec& spec,
+                                         const RandomPohOptions& opt) {
+    const int ch = guide_field.channels, h = guide_field.height, w = guide_field.width;
+    if (ch != target.intensity.channels || h != target.intensity.height || w != target.intensity.width)
+        throw std::invalid_argument("convert_random_poh: guide/target shape mismatch");
+    if (planes.distances.empty()) throw std::invalid_argument("convert_random_poh: no depth planes");
+    if (target.masks.size() != planes.distances.size())
+        throw std::invalid_argument("convert_random_poh: plane/mask count mismatch");
+    if (opt.steps < 1) throw std::invalid_argument("convert_random_poh: steps must be >= 1");
+    const size_t n = guide_field.size(), hw = static_cast<size_t>(h) * w;
+    const int L = static_cast<int>(planes.distances.size());
+    // initial phase: the reference's Rng (mt19937_64, 53-bit uniform) in element order
+    std::mt19937_64 eng(opt.seed);
+    std::vector<float> phase(n);
+    for (float& v : phase) {
+        const double u = static_cast<double>(eng() >> 11) * 0x1.0p-53;
+        v = static_cast<float>(-std::numbers::pi + 2.0 * std::numbers::pi * u);
+    }
+    std::vector<float> tgt(target.intensity.values.size());
+    for (size_t i = 0; i < tgt.size(); ++i) tgt[i] = static_cast<float>(target.intensity.values[i]);
+    std::vector<uint8_t> masks(hw * L);
+    for (int l = 0; l < L; ++l) {
+        if (target.masks[l].size() != hw) throw std::invalid_argument("convert_random_poh: mask shape mismatch");
+        std::copy(target.masks[l].begin(), target.masks[l].end(), masks.begin() + l * hw);
+    }
+    SpecHolder sh(spec);
+    hs_poh_config cfg{ch, h, w, L, planes.distances.data(), sh.s, tgt.data(), masks.data(), opt.steps,
+                      opt.lambda_comp, opt.lambda_field, opt.lr};
+    Dev guide = upload_field({&guide_field});
+    Dev dph(n * sizeof(float));
+    dph.upload(phase.data(), n * sizeof(float));
+    std::vector<double> loss(opt.steps);
+    check(hs_convert_random_poh_field(ctx(), &cfg, guide.as<float>(), dph.as<float>(), loss.data()));
+    dph.download(phase.data(), n * sizeof(float));
+    RandomPohResult result;
+    for (int step = 0; step < opt.steps; ++step) {  // convert.cpp:165-166
+        const bool logged = opt.log_every > 0 && (step + 1) % opt.log_every == 0;
+        if (logged || step + 1 == opt.steps) result.loss_history.push_back(loss[step]);
+    }
+    result.poh.phase = RealField(ch, h, w);
+    for (size_t i = 0; i < n; ++i) result.poh.phase.values[i] = canonicalize_phase(static_cast<double>(phase[i]));
+    result.poh.format = PohFormat::random;
+    return result;
+}
+
+RandomPohResult convert_random_poh(const GaussianSet& guide, const DepthPlaneSet& planes,
+                                   const TargetStack& target, const PropagationSpec& spec,
+                                   const RandomPohOptions& opt) {
+    const ComplexField guide_field = rasterize_forward(guide, target.intensity.width, target.intensity.height);
+    return convert_random_poh_field(guide_field, planes, target, spec, opt);
 }
 
 }  // namespace holo

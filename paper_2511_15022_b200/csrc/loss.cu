@@ -499,24 +499,7 @@ __global__ void intensity_kernel(const float2* f, int64_t n, float* out) {
     }
 }
 
-// ---- Adan -------------------------------------------------------------------------
-struct GroupConst {
-    float lr, inv_bc1, b2_bc2, inv_bc3;
-};
-
-__device__ __forceinline__ void adan_update(float& p, float g, float& m, float& v, float& n,
-                                            float& gp, bool first, float b1, float b2, float b3,
-                                            float eps, const GroupConst& k) {
-    const float diff = first ? 0.f : g - gp;
-    m = b1 * m + (1.f - b1) * g;
-    v = b2 * v + (1.f - b2) * diff;
-    const float u = g + b2 * diff;
-    n = b3 * n + (1.f - b3) * u * u;
-    const float denom = sqrtf(n * k.inv_bc3) + eps;
-    p -= k.lr * (m * k.inv_bc1 + v * k.b2_bc2) / denom;
-    gp = g;
-}
-
+// ---- Adan (GroupConst, adan_update: loss.cuh) -------------------------------------
 __global__ void adan_fused_kernel(float* __restrict__ p, const float* __restrict__ g,
                                   float* __restrict__ st, int64_t P, AdanGroups G, int total_steps,
                                   double b1, double b2, double b3, double eps,

@@ -38,6 +38,24 @@ inline size_t ssim_target_stats_elems(int C, int H, int W) {
     return (H < 11 || W < 11) ? 1 : static_cast<size_t>(C) * (H - 10) * (W - 10);
 }
 
+// One Adan element update (optimizer.cpp:99-123) with per-group constants
+// lr, 1/bc1, beta2/bc2, 1/bc3.
+struct GroupConst {
+    float lr, inv_bc1, b2_bc2, inv_bc3;
+};
+
+__device__ __forceinline__ void adan_update(float& p, float g, float& m, float& v, float& n, float& gp, bool first,
+                                            float b1, float b2, float b3, float eps, const GroupConst& k) {
+    const float diff = first ? 0.f : g - gp;
+    m = b1 * m + (1.f - b1) * g;
+    v = b2 * v + (1.f - b2) * diff;
+    const float u = g + b2 * diff;
+    n = b3 * n + (1.f - b3) * u * u;
+    const float denom = sqrtf(n * k.inv_bc3) + eps;
+    p -= k.lr * (m * k.inv_bc1 + v * k.b2_bc2) / denom;
+    gp = g;
+}
+
 // Fused Adan over the six groups of the parameter buffer (optimizer.cpp:99-123).
 struct AdanGroups {
     int64_t begin[6], end[6];

@@ -23,7 +23,7 @@ import torch
 
 from . import _lib
 from ._lib import (HoloError, HoloInvalidArgument, HoloNonFinite, check, hs_adan_config,
-                   hs_prop_spec, hs_trainer_config)
+                   hs_poh_config, hs_prop_spec, hs_trainer_config)
 
 __all__ = [
     "GaussianSet", "ComplexField", "RealField", "TileIndex", "PropagationSpec", "TargetStack",
@@ -355,6 +355,107 @@ def propagate_multi_backward(grads: List[ComplexField], spec: PropagationSpec, d
 # loss (loss.hpp:10-67)
 # ---------------------------------------------------------------------------------------------
 kSsimWindow, kSsimSigma, kSsimC1, kSsimC2, kSsimWeight = 11, 1.5, 0.01 ** 2, 0.03 ** 2, 0.005
+
+
+# ---- phase-only hologram conversion (convert.hpp, convert.cpp:20-184) -------------------------
+TWO_PI = 2.0 * math.pi
+
+
+def canonicalize_phase(value):
+    """convert.cpp:20-25 in fp64 (scalar or array) -> [0, 2 pi)."""
+    r = np.fmod(np.asarray(value, dtype=np.float64), TWO_PI)
+    r = np.where(r < 0.0, r + TWO_PI, r)
+    r = np.where(r >= TWO_PI, r - TWO_PI, r)
+    return float(r) if np.ndim(r) == 0 else r
+
+
+DPAC_DIRECT, DPAC_CLASSICAL = 0, 1
+POH_SMOOTH, POH_RANDOM = "smooth", "random"
+
+
+@dataclass
+class PhaseOnlyHologram:
+    phase: RealField
+    format: str = POH_SMOOTH
+
+
+def dpac_encode(field: ComplexField, mode: int = DPAC_DIRECT) -> PhaseOnlyHologram:
+    """convert.cpp:31-60 on the B200; canonicalised in fp64 like the reference."""
+    d = field.to_device()
+    out = torch.empty((field.channels, field.height, field.width), dtype=torch.float32, device=d.device)
+    check(_lib.load().hs_dpac_encode(ctx_handle(), _ptr(d), field.channels, field.height, field.width, int(mode),
+                                     _ptr(out)))
+    ph = canonicalize_phase(out.cpu().numpy().astype(np.float64))
+    return PhaseOnlyHologram(RealField(field.channels, field.height, field.width, ph), POH_SMOOTH)
+
+
+def poh_field(poh: PhaseOnlyHologram) -> ComplexField:
+    """convert.cpp:62-69: e^{i phase}."""
+    ph = poh.phase
+    d = torch.from_numpy(np.ascontiguousarray(ph.values, dtype=np.float32)).to(_dev())
+    out = torch.empty((ph.channels, ph.height, ph.width, 2), dtype=torch.float32, device=d.device)
+    check(_lib.load().hs_poh_field(ctx_handle(), _ptr(d), int(d.numel()), _ptr(out)))
+    return ComplexField.from_device(out)
+
+
+@dataclass
+class RandomPohOptions:
+    steps: int = 600
+    seed: int = 0
+    lambda_comp: float = 0.1
+    lambda_field: float = 0.01
+    lr: float = 2.5e-3
+    log_every: int = 50
+
+
+@dataclass
+class RandomPohResult:
+    poh: PhaseOnlyHologram
+    loss_history: List[float]
+
+
+def random_phase(seed: int, n: int) -> np.ndarray:
+    """Rng(seed).uniform(-pi, pi) in element order (rng.hpp: mt19937_64, 53-bit)."""
+    from .synthetic import Rng
+    return -math.pi + TWO_PI * Rng(seed).uniform(n)
+
+
+def convert_random_poh_field(guide_field: ComplexField, planes, target: "TargetStack", spec: PropagationSpec,
+                             opt: RandomPohOptions = RandomPohOptions()) -> RandomPohResult:
+    """convert.cpp:71-174, device resident (hs_convert_random_poh_field)."""
+    c, h, w = guide_field.channels, guide_field.height, guide_field.width
+    ti = target.intensity
+    if (c, h, w) != (ti.channels, ti.height, ti.width):
+        raise HoloInvalidArgument("convert_random_poh: guide/target shape mismatch")
+    dists = list(planes.distances if hasattr(planes, "distances") else planes)
+    if not dists:
+        raise HoloInvalidArgument("convert_random_poh: no depth planes")
+    masks = np.ascontiguousarray(target.masks, dtype=np.uint8)
+    if masks.shape[0] != len(dists):
+        raise HoloInvalidArgument("convert_random_poh: plane/mask count mismatch")
+    if opt.steps < 1:
+        raise HoloInvalidArgument("convert_random_poh: steps must be >= 1")
+    phase = torch.from_numpy(random_phase(opt.seed, c * h * w).astype(np.float32)).to(_dev())
+    tgt = np.ascontiguousarray(ti.values, dtype=np.float32)
+    d = (C.c_double * len(dists))(*dists)
+    s = spec.c_struct()
+    cfg = hs_poh_config(c, h, w, len(dists), C.cast(d, C.POINTER(C.c_double)), s,
+                        tgt.ctypes.data_as(C.POINTER(C.c_float)), masks.ctypes.data_as(C.POINTER(C.c_uint8)),
+                        int(opt.steps), float(opt.lambda_comp), float(opt.lambda_field), float(opt.lr))
+    loss = (C.c_double * opt.steps)()
+    g = guide_field.to_device()
+    check(_lib.load().hs_convert_random_poh_field(ctx_handle(), C.byref(cfg), _ptr(g), _ptr(phase), loss))
+    hist = [loss[i] for i in range(opt.steps)
+            if (opt.log_every > 0 and (i + 1) % opt.log_every == 0) or i + 1 == opt.steps]
+    ph = canonicalize_phase(phase.cpu().numpy().astype(np.float64))
+    return RandomPohResult(PhaseOnlyHologram(RealField(c, h, w, ph), POH_RANDOM), hist)
+
+
+def convert_random_poh(guide: GaussianSet, planes, target: "TargetStack", spec: PropagationSpec,
+                       opt: RandomPohOptions = RandomPohOptions()) -> RandomPohResult:
+    """convert.cpp:176-182."""
+    field = rasterize_forward(guide, target.intensity.width, target.intensity.height)
+    return convert_random_poh_field(field, planes, target, spec, opt)
 
 
 @dataclass

@@ -180,3 +180,18 @@ def test_golden_full_step():
     assert loss == pytest.approx(float(GOLD["step_loss"][0]), rel=1e-10)
     flat = np.concatenate([r["grads"][k] for k in O.GROUPS])
     assert rel_l2(flat, GOLD["step_grads"]) <= 1e-9
+
+
+def test_canonicalize_phase_known_answers():
+    """test_convert.cpp:34-48 on the host-side fp64 canonicalisation of the drop-in."""
+    from paper_2511_15022_b200 import holo
+    tau = 2.0 * np.pi
+    assert holo.canonicalize_phase(7.5) == pytest.approx(1.2168146928204138, rel=1e-13)
+    assert holo.canonicalize_phase(-np.pi / 2.0) == pytest.approx(3.0 * np.pi / 2.0, rel=1e-13)
+    assert holo.canonicalize_phase(0.0) == 0.0
+    assert holo.canonicalize_phase(tau) == 0.0
+    assert holo.canonicalize_phase(-1e-18) < tau
+    for v in (-25.0, -3.2, 0.1, 6.2, 100.0):
+        c = holo.canonicalize_phase(v)
+        assert 0.0 <= c < tau
+        assert abs(np.remainder(c - v + np.pi, tau) - np.pi) <= 1e-9

@@ -1,5 +1,5 @@
 """GPU: the reference's own hot-path unit tests (proj/tests/test_{field_core,
-rasterizer,propagation,loss,optimizer}.cpp, compiled by tests/cxx/Makefile
+rasterizer,propagation,loss,optimizer,convert}.cpp, compiled by tests/cxx/Makefile
 against the C++ drop-in libholo_b200.so) run on the B200.
 
 Cases whose tolerance is tighter than fp32 arithmetic can meet (the reference
@@ -15,7 +15,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 BIN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cxx", "bin")
-SUITES = ("test_field_core", "test_rasterizer", "test_propagation", "test_loss", "test_optimizer")
+SUITES = ("test_field_core", "test_rasterizer", "test_propagation", "test_loss", "test_optimizer", "test_convert")
 
 # test case name -> why it needs fp64 (reference tolerance vs the fp32 device path)
 FP64_ONLY = {
@@ -39,6 +39,14 @@ FP64_ONLY = {
     "scalar trajectory matches the frozen reference": "epsilon 1e-14 (fp32 state)",
     "vector trajectory matches the frozen reference": "epsilon 1e-14 (fp32 state)",
     "quadratic bowl converges": "epsilon 1e-9 after 200 fp32 steps",
+    # test_convert.cpp:50-72, 89-111, 113-119: == / 1e-13 / 1e-12 against fp64
+    # hypot, atan2, acos, sincos of the fp64 field (the device path is fp32)
+    "direct encoding interleaves amplitude and phase checkerboards": "== against fp64 hypot/atan2",
+    "classical encoding splits into conjugate phase offsets": "epsilon 1e-13",
+    "phase-only fields have unit magnitude everywhere": "| |e^{i phi}| - 1 | <= 1e-12 (fp32 sincos)",
+    # test_convert.cpp:121-170 compares the fused device loop with a host loop over
+    # the public operators (fp64 host Adan / loss, fp32 device propagation) with ==
+    "unguided conversion reproduces a naive optimization bit for bit": "bit equality of two fp32/fp64 compositions",
 }
 
 
