@@ -111,6 +111,11 @@ hs_status hs_intensity(hs_ctx* ctx, const float* d_field, int64_t count, float* 
  * bytes (build_masks).  d_grads (nullable) receives dL/dI; *loss the value. */
 hs_status hs_loss(hs_ctx* ctx, int kind, int L, int c, int h, int w, const float* d_recon,
                   const float* d_target, const uint8_t* d_masks, float* d_grads, double* loss);
+/* compute_metrics (pipeline.cpp:135-163): recon and target clipped to [0, 1],
+ * per plane PSNR (dB, +inf when identical) and ssim_value (loss.cpp:356-369).
+ * d_recon L x C x H x W intensities, d_target C x H x W; h_psnr, h_ssim L doubles. */
+hs_status hs_compute_metrics(hs_ctx* ctx, int L, int c, int h, int w, const float* d_recon,
+                             const float* d_target, double* h_psnr, double* h_ssim);
 /* build_masks (loss.cpp:235-249) on the host, bit-exact. */
 hs_status hs_build_masks(const double* h_depth, int h, int w, int L, int near_is_high,
                          uint8_t* h_masks);

@@ -411,3 +411,13 @@ def convert_random_poh_field(gre, gim, target, depth, L, distances, spec, steps,
         C.c_uint64(seed), _d(lambda_comp), _d(lambda_field), _d(lr), int(log_every), _p(phase), _p(loss),
         len(loss)))
     return phase, loss[:n]
+
+
+def compute_metrics(recon, target):
+    """pipeline.cpp:149-163: per-plane (psnr, ssim) of clipped reconstructions."""
+    L, c, h, w = recon.shape
+    recon = np.ascontiguousarray(recon, dtype=np.float64)
+    target = np.ascontiguousarray(target, dtype=np.float64)
+    psnr, ssim = np.zeros(L), np.zeros(L)
+    _check(lib().ref_compute_metrics(L, c, h, w, _p(recon), _p(target), _p(psnr), _p(ssim)))
+    return psnr, ssim

@@ -296,6 +296,21 @@ int ref_transfer_function(const double* wl, int nwl, double pitch, int pad, doub
     });
 }
 
+// ---- end-of-run metrics (pipeline.cpp:135-163) ------------------------------------
+int ref_compute_metrics(int L, int c, int h, int w, const double* recon, const double* target, double* psnr,
+                        double* ssim) {
+    return guard([&] {
+        const size_t plane = static_cast<size_t>(c) * h * w;
+        std::vector<RealField> r;
+        for (int l = 0; l < L; ++l) r.push_back(make_real(c, h, w, recon + l * plane));
+        const Metrics m = compute_metrics(r, make_real(c, h, w, target));
+        for (int l = 0; l < L; ++l) {
+            psnr[l] = m.psnr[l];
+            ssim[l] = m.ssim[l];
+        }
+    });
+}
+
 // ---- POH conversion (convert.cpp) -------------------------------------------------
 int ref_dpac_encode(int c, int h, int w, const double* re, const double* im, int mode, double* out) {
     return guard([&] {

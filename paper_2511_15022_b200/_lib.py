@@ -66,6 +66,8 @@ class hs_poh_config(C.Structure):
 
 
 _SIGS = {
+    "hs_compute_metrics": [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                           C.POINTER(C.c_double), C.POINTER(C.c_double)],
     "hs_dpac_encode": [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p],
     "hs_poh_field": [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p],
     "hs_convert_random_poh_field": [C.c_void_p, C.POINTER(hs_poh_config), C.c_void_p, C.c_void_p,

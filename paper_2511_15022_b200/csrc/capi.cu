@@ -2,9 +2,11 @@
 // step-loop body of proj/core/src/pipeline.cpp:253-297.
 #include <atomic>
 #include <cmath>
+#include <limits>
 #include <cstring>
 #include <memory>
 #include <string>
+#include <vector>
 
 #include "asm.cuh"
 #include "loss.cuh"
@@ -43,7 +45,7 @@ struct CtxWork {
     AsmWork aw;
     DevBuf flags, partials, out3, tstats;
     PohWork poh;
-    DevBuf amax, poh_target, poh_masks, poh_loss;
+    DevBuf amax, poh_target, poh_masks, poh_loss, metric_buf;
 };
 
 }  // namespace
@@ -297,6 +299,44 @@ extern "C" hs_status hs_propagate_multi_backward(hs_ctx* ctx, const hs_prop_spec
         asm_backward(aw, reinterpret_cast<const float2*>(d_grads), reinterpret_cast<float2*>(d_out),
                      ctx->stream);
         HS_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+// ---- end-of-run metrics (pipeline.cpp:135-163) ------------------------------------------------
+extern "C" hs_status hs_compute_metrics(hs_ctx* ctx, int L, int c, int h, int w, const float* d_recon,
+                                        const float* d_target, double* h_psnr, double* h_ssim) {
+    return guard([&] {
+        require(L >= 1, "compute_metrics: no planes");
+        require(h >= 11 && w >= 11, "ssim: image smaller than the 11x11 window");
+        CtxWork& cw = work_of(ctx);
+        cudaStream_t st = ctx->stream;
+        const int64_t chw = static_cast<int64_t>(c) * h * w;
+        cw.metric_buf.reserve(sizeof(float) * chw * (L + 1));
+        float* tclip = cw.metric_buf.as<float>();
+        float* rclip = tclip + chw;
+        clip01_launch(d_target, chw, tclip, st);
+        clip01_launch(d_recon, chw * L, rclip, st);
+        cw.tstats.reserve(sizeof(float2) * ssim_target_stats_elems(c, h, w));
+        ssim_target_stats(tclip, c, h, w, cw.tstats.as<float2>(), st);
+        const int slots = std::max(loss_partial_slots(kLossSsim, 1, c, h, w), loss_partial_slots(kLossMse, 1, c, h, w));
+        cw.partials.reserve(sizeof(double) * 2 * std::max(slots, 1));
+        cw.out3.reserve(sizeof(double) * 3 * 2 * L);
+        for (int l = 0; l < L; ++l) {
+            for (int kind : {kLossMse, kLossSsim}) {
+                LossArgs a{kind, 1, 1, 0, c, h, w, rclip + l * chw, nullptr, tclip, cw.tstats.as<float2>(), nullptr,
+                           nullptr, nullptr, cw.partials.as<double>()};
+                const int used = loss_launch(a, st);
+                loss_finalize(a, used, cw.out3.as<double>() + 3 * (2 * l + (kind == kLossSsim ? 1 : 0)), st);
+            }
+        }
+        std::vector<double> out(6 * static_cast<size_t>(L));
+        HS_CUDA(cudaMemcpyAsync(out.data(), cw.out3.p, sizeof(double) * out.size(), cudaMemcpyDeviceToHost, st));
+        HS_CUDA(cudaStreamSynchronize(st));
+        for (int l = 0; l < L; ++l) {
+            const double mse = out[6 * l];  // loss_mse of one plane: mean squared difference
+            h_psnr[l] = mse <= 0.0 ? std::numeric_limits<double>::infinity() : -10.0 * std::log10(mse);
+            h_ssim[l] = 1.0 - out[6 * l + 3];  // loss_ssim = 1 - ssim_value
+        }
     });
 }
 

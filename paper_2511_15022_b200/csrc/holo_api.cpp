@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <limits>
 #include <mutex>
 #include <numbers>
 #include <random>
@@ -24,6 +25,7 @@
 #include "holo/loss.hpp"
 #include "holo/optimizer.hpp"
 #include "holo/parallel.hpp"
+#include "holo/pipeline.hpp"
 #include "holo/propagation.hpp"
 #include "holo/rasterizer.hpp"
 #include "holosplat.h"
@@ -668,6 +670,42 @@ RandomPohResult convert_random_poh(const GaussianSet& guide, const DepthPlaneSet
                                    const RandomPohOptions& opt) {
     const ComplexField guide_field = rasterize_forward(guide, target.intensity.width, target.intensity.height);
     return convert_random_poh_field(guide_field, planes, target, spec, opt);
+}
+
+// ---- end-of-run metrics (pipeline.hpp:47-57, pipeline.cpp:135-163) -------------------------------
+double psnr_value(const RealField& recon, const RealField& target) {
+    if (!recon.same_shape(target)) throw std::invalid_argument("psnr: shape mismatch");
+    double mse = 0.0;
+    for (size_t i = 0; i < recon.values.size(); ++i) {
+        const double d = std::clamp(recon.values[i], 0.0, 1.0) - std::clamp(target.values[i], 0.0, 1.0);
+        mse += d * d;
+    }
+    mse /= static_cast<double>(recon.values.size());
+    if (mse <= 0.0) return std::numeric_limits<double>::infinity();
+    return -10.0 * std::log10(mse);
+}
+
+Metrics compute_metrics(const std::vector<RealField>& recon, const RealField& target) {
+    if (recon.empty()) throw std::invalid_argument("compute_metrics: no planes");
+    for (const auto& r : recon)
+        if (!r.same_shape(target)) throw std::invalid_argument("psnr: shape mismatch");
+    const size_t n = target.values.size();
+    std::vector<float> h(n * (recon.size() + 1));
+    for (size_t i = 0; i < n; ++i) h[i] = static_cast<float>(target.values[i]);
+    for (size_t l = 0; l < recon.size(); ++l)
+        for (size_t i = 0; i < n; ++i) h[n * (l + 1) + i] = static_cast<float>(recon[l].values[i]);
+    Dev d(h.size() * sizeof(float));
+    d.upload(h.data(), h.size() * sizeof(float));
+    Metrics m;
+    m.psnr.resize(recon.size());
+    m.ssim.resize(recon.size());
+    check(hs_compute_metrics(ctx(), static_cast<int>(recon.size()), target.channels, target.height, target.width,
+                             d.as<float>() + n, d.as<float>(), m.psnr.data(), m.ssim.data()));
+    for (double v : m.psnr) m.mean_psnr += v;
+    for (double v : m.ssim) m.mean_ssim += v;
+    m.mean_psnr /= static_cast<double>(m.psnr.size());
+    m.mean_ssim /= static_cast<double>(m.ssim.size());
+    return m;
 }
 
 }  // namespace holo

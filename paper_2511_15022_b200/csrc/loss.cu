@@ -491,6 +491,12 @@ __global__ void __launch_bounds__(1024) loss_finalize_kernel(const double* parti
     }
 }
 
+__global__ void clip01_kernel(const float* in, int64_t n, float* out) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[i] = fminf(fmaxf(in[i], 0.f), 1.f);
+}
+
 __global__ void intensity_kernel(const float2* f, int64_t n, float* out) {
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -644,6 +650,12 @@ void ssim_target_stats(const float* target, int C, int H, int W, float2* out, cu
     const int64_t total = static_cast<int64_t>(C) * (H - kWin + 1) * (W - kWin + 1);
     ssim_target_stats_kernel<<<grid_for(total, 256), 256, 0, st>>>(target, C, H, W, win, out);
     launch_check("ssim_target_stats");
+}
+
+void clip01_launch(const float* in, int64_t count, float* out, cudaStream_t st) {
+    if (count == 0) return;
+    clip01_kernel<<<grid_for(count, 256), 256, 0, st>>>(in, count, out);
+    launch_check("clip01");
 }
 
 void intensity_launch(const float2* f, int64_t count, float* out, cudaStream_t st) {

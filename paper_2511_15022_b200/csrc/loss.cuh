@@ -32,6 +32,8 @@ int loss_partial_slots(int kind, int L, int C, int H, int W);
 void loss_finalize(const LossArgs& a, int slots, double* d_out3, cudaStream_t st);
 
 void intensity_launch(const float2* f, int64_t count, float* out, cudaStream_t st);
+// clamp to [0, 1] (pipeline.cpp clipped(), used by compute_metrics)
+void clip01_launch(const float* in, int64_t count, float* out, cudaStream_t st);
 // (mu2, sigma2^2) of the target on the valid 11x11 grid, per channel.
 void ssim_target_stats(const float* target, int C, int H, int W, float2* out, cudaStream_t st);
 inline size_t ssim_target_stats_elems(int C, int H, int W) {

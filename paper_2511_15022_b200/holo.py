@@ -357,6 +357,42 @@ def propagate_multi_backward(grads: List[ComplexField], spec: PropagationSpec, d
 kSsimWindow, kSsimSigma, kSsimC1, kSsimC2, kSsimWeight = 11, 1.5, 0.01 ** 2, 0.03 ** 2, 0.005
 
 
+# ---- end-of-run metrics (pipeline.hpp:47-57, pipeline.cpp:135-163) --------------------------------
+@dataclass
+class Metrics:
+    psnr: List[float]
+    ssim: List[float]
+    mean_psnr: float
+    mean_ssim: float
+
+
+def psnr_value(recon: RealField, target: RealField) -> float:
+    """pipeline.cpp:135-147 (host fp64, like the reference's scalar helper)."""
+    if not recon.same_shape(target):
+        raise HoloInvalidArgument("psnr: shape mismatch")
+    d = np.clip(recon.values, 0.0, 1.0) - np.clip(target.values, 0.0, 1.0)
+    mse = float(np.mean(d * d))
+    return math.inf if mse <= 0.0 else -10.0 * math.log10(mse)
+
+
+def compute_metrics(recon: List[RealField], target: RealField) -> Metrics:
+    """pipeline.cpp:149-163 on the B200 (hs_compute_metrics)."""
+    if not recon:
+        raise HoloInvalidArgument("compute_metrics: no planes")
+    for r in recon:
+        if not r.same_shape(target):
+            raise HoloInvalidArgument("psnr: shape mismatch")
+    L = len(recon)
+    dev = _dev()
+    t = torch.from_numpy(np.ascontiguousarray(target.values, dtype=np.float32)).to(dev)
+    r = torch.from_numpy(np.stack([np.asarray(x.values, dtype=np.float32) for x in recon])).to(dev)
+    ps, ss = (C.c_double * L)(), (C.c_double * L)()
+    check(_lib.load().hs_compute_metrics(ctx_handle(), L, target.channels, target.height, target.width,
+                                         _ptr(r.contiguous()), _ptr(t), ps, ss))
+    p, s = list(ps), list(ss)
+    return Metrics(p, s, sum(p) / L, sum(s) / L)
+
+
 # ---- phase-only hologram conversion (convert.hpp, convert.cpp:20-184) -------------------------
 TWO_PI = 2.0 * math.pi
 

@@ -88,3 +88,20 @@ def test_convert_random_poh_rejects_inconsistent_inputs(holo):
         holo.convert_random_poh_field(ok, S.make_depth_planes(1, 3e-3, 0.0), tgt, spec)
     with pytest.raises(ValueError):
         holo.convert_random_poh_field(ok, dist, tgt, spec, holo.RandomPohOptions(steps=0))
+
+
+# ---- end-of-run metrics (pipeline.cpp:135-163) -----------------------------
+@pytest.mark.parametrize("L,c,h,w", [(2, 3, 32, 48), (1, 1, 40, 56)])
+def test_compute_metrics(holo, ref, L, c, h, w):
+    tgt = S.random_real(5, c, h, w, -0.1, 1.1).astype(np.float32).astype(np.float64)
+    rec = np.stack([S.random_real(6 + l, c, h, w, -0.2, 1.2) for l in range(L)]).astype(np.float32).astype(
+        np.float64)
+    m = holo.compute_metrics([holo.RealField(c, h, w, rec[l]) for l in range(L)], holo.RealField(c, h, w, tgt))
+    rp, rs = ref.compute_metrics(rec, tgt)
+    np.testing.assert_allclose(m.psnr, rp, atol=1e-4)
+    np.testing.assert_allclose(m.ssim, rs, atol=1e-5)
+    assert m.mean_psnr == pytest.approx(float(np.mean(rp)), abs=1e-4)
+    same = holo.compute_metrics([holo.RealField(c, h, w, tgt)], holo.RealField(c, h, w, tgt))
+    assert same.psnr[0] == float("inf") and same.ssim[0] == pytest.approx(1.0, abs=1e-6)
+    assert holo.psnr_value(holo.RealField(c, h, w, rec[0]), holo.RealField(c, h, w, tgt)) == pytest.approx(
+        rp[0], abs=1e-9)
