@@ -7,6 +7,9 @@
 // function sampler are host code, as in the reference.
 #include <algorithm>
 #include <cmath>
+#include <iterator>
+#include <fstream>
+#include <cstdint>
 #include <cstdlib>
 #include <cstring>
 #include <limits>
@@ -22,6 +25,7 @@
 #include "holo/convert.hpp"
 #include "holo/field_core.hpp"
 #include "holo/gaussian_set.hpp"
+#include "holo/io.hpp"
 #include "holo/loss.hpp"
 #include "holo/optimizer.hpp"
 #include "holo/parallel.hpp"
@@ -706,6 +710,114 @@ Metrics compute_metrics(const std::vector<RealField>& recon, const RealField& ta
     m.mean_psnr /= static_cast<double>(m.psnr.size());
     m.mean_ssim /= static_cast<double>(m.ssim.size());
     return m;
+}
+
+// ---- artifact formats (io.hpp; io.cpp:237-335) ----------------------------------------------------
+namespace {
+template <class T>
+void put_le(std::string& out, T v) {  // little-endian, like the reference's append_* helpers
+    unsigned char b[sizeof(T)];
+    std::memcpy(b, &v, sizeof(T));
+    out.append(reinterpret_cast<const char*>(b), sizeof(T));  // x86-64 / aarch64 hosts are little-endian
+}
+
+struct ByteReader {
+    const std::string& path;
+    const unsigned char* p;
+    size_t left;
+    void need(size_t n) const {
+        if (left < n) throw std::runtime_error(path + ": truncated file");
+    }
+    template <class T>
+    T get() {
+        need(sizeof(T));
+        T v;
+        std::memcpy(&v, p, sizeof(T));
+        p += sizeof(T);
+        left -= sizeof(T);
+        return v;
+    }
+    void magic(const char* m, const char* what) {
+        need(4);
+        if (std::memcmp(p, m, 4) != 0) throw std::runtime_error(path + ": not a " + what + " file");
+        p += 4;
+        left -= 4;
+    }
+};
+
+std::string slurp_file(const std::string& path) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw std::runtime_error("cannot open " + path);
+    return std::string(std::istreambuf_iterator<char>(in), std::istreambuf_iterator<char>());
+}
+}  // namespace
+
+void atomic_write(const std::string& path, const std::string& bytes) {
+    const std::string tmp = path + ".tmp";
+    {
+        std::ofstream out(tmp, std::ios::binary | std::ios::trunc);
+        if (!out) throw std::runtime_error("cannot write " + tmp);
+        out.write(bytes.data(), static_cast<std::streamsize>(bytes.size()));
+        if (!out) throw std::runtime_error("short write to " + tmp);
+    }
+    if (std::rename(tmp.c_str(), path.c_str()) != 0) throw std::runtime_error("cannot rename into " + path);
+}
+
+void write_field(const std::string& path, const ComplexField& field, bool as_f64) {
+    std::string out;
+    out.reserve(19 + field.size() * 2 * (as_f64 ? 8 : 4));
+    out += "CGHF";
+    put_le<uint16_t>(out, 1);
+    put_le<uint32_t>(out, static_cast<uint32_t>(field.channels));
+    put_le<uint32_t>(out, static_cast<uint32_t>(field.height));
+    put_le<uint32_t>(out, static_cast<uint32_t>(field.width));
+    out.push_back(as_f64 ? 1 : 0);
+    for (const auto* plane : {&field.real, &field.imag})
+        for (double v : *plane) {
+            if (as_f64) put_le<double>(out, v);
+            else put_le<float>(out, static_cast<float>(v));
+        }
+    atomic_write(path, out);
+}
+
+ComplexField read_field(const std::string& path) {
+    const std::string bytes = slurp_file(path);
+    ByteReader r{path, reinterpret_cast<const unsigned char*>(bytes.data()), bytes.size()};
+    r.magic("CGHF", "CGHF");
+    if (r.get<uint16_t>() != 1) throw std::runtime_error(path + ": unsupported CGHF version");
+    const uint32_t c = r.get<uint32_t>(), h = r.get<uint32_t>(), w = r.get<uint32_t>();
+    const uint8_t dtype = r.get<uint8_t>();
+    if (dtype > 1) throw std::runtime_error(path + ": unknown CGHF dtype");
+    ComplexField f(static_cast<int>(c), static_cast<int>(h), static_cast<int>(w));
+    r.need(f.size() * 2 * (dtype ? 8 : 4));
+    for (auto* plane : {&f.real, &f.imag})
+        for (double& v : *plane) v = dtype ? r.get<double>() : static_cast<double>(r.get<float>());
+    if (r.left != 0) throw std::runtime_error(path + ": trailing bytes");
+    return f;
+}
+
+void write_gaussians(const std::string& path, const GaussianSet& set) {
+    std::string out = "CGGS";
+    put_le<uint16_t>(out, 1);
+    put_le<uint32_t>(out, static_cast<uint32_t>(set.count));
+    put_le<uint32_t>(out, static_cast<uint32_t>(set.channels));
+    for (const auto* v : {&set.pre_position, &set.pre_scale, &set.rotation, &set.amplitude, &set.phase,
+                          &set.pre_opacity})
+        for (double x : *v) put_le<float>(out, static_cast<float>(x));
+    atomic_write(path, out);
+}
+
+GaussianSet read_gaussians(const std::string& path) {
+    const std::string bytes = slurp_file(path);
+    ByteReader r{path, reinterpret_cast<const unsigned char*>(bytes.data()), bytes.size()};
+    r.magic("CGGS", "CGGS");
+    if (r.get<uint16_t>() != 1) throw std::runtime_error(path + ": unsupported CGGS version");
+    const uint32_t n = r.get<uint32_t>(), c = r.get<uint32_t>();
+    GaussianSet set(static_cast<int>(n), static_cast<int>(c));
+    for (auto* v : {&set.pre_position, &set.pre_scale, &set.rotation, &set.amplitude, &set.phase, &set.pre_opacity})
+        for (double& x : *v) x = static_cast<double>(r.get<float>());
+    if (r.left != 0) throw std::runtime_error(path + ": trailing bytes");
+    return set;
 }
 
 }  // namespace holo

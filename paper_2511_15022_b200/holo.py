@@ -357,6 +357,73 @@ def propagate_multi_backward(grads: List[ComplexField], spec: PropagationSpec, d
 kSsimWindow, kSsimSigma, kSsimC1, kSsimC2, kSsimWeight = 11, 1.5, 0.01 ** 2, 0.03 ** 2, 0.005
 
 
+# ---- artifact formats (io.hpp; io.cpp:237-335) -----------------------------------------------------
+def atomic_write(path: str, data: bytes) -> None:
+    """Temp file in the same directory, then rename (io.cpp:237-247)."""
+    import os
+    tmp = path + ".tmp"
+    with open(tmp, "wb") as f:
+        f.write(data)
+    os.replace(tmp, path)
+
+
+def write_field(path: str, field: ComplexField, as_f64: bool = True) -> None:
+    """CGHF: magic, u16 1, u32 C/H/W, u8 dtype, planar real then imag, little-endian."""
+    import struct
+    dt = "<f8" if as_f64 else "<f4"
+    head = b"CGHF" + struct.pack("<HIIIB", 1, field.channels, field.height, field.width, 1 if as_f64 else 0)
+    body = np.ascontiguousarray(field.real, dtype=dt).tobytes() + np.ascontiguousarray(field.imag, dtype=dt).tobytes()
+    atomic_write(path, head + body)
+
+
+def read_field(path: str) -> ComplexField:
+    import struct
+    data = open(path, "rb").read()
+    if len(data) < 4 or data[:4] != b"CGHF":
+        raise HoloError(f"{path}: not a CGHF file")
+    if len(data) < 19:
+        raise HoloError(f"{path}: truncated file")
+    ver, c, h, w, dtype = struct.unpack_from("<HIIIB", data, 4)
+    if ver != 1:
+        raise HoloError(f"{path}: unsupported CGHF version")
+    if dtype > 1:
+        raise HoloError(f"{path}: unknown CGHF dtype")
+    n = c * h * w
+    item = 8 if dtype else 4
+    if len(data) < 19 + 2 * n * item:
+        raise HoloError(f"{path}: truncated file")
+    if len(data) != 19 + 2 * n * item:
+        raise HoloError(f"{path}: trailing bytes")
+    v = np.frombuffer(data, dtype="<f8" if dtype else "<f4", offset=19, count=2 * n).astype(np.float64)
+    return ComplexField(c, h, w, v[:n].reshape(c, h, w), v[n:].reshape(c, h, w))
+
+
+def write_gaussians(path: str, gs: GaussianSet) -> None:
+    """CGGS: magic, u16 1, u32 N, u32 C, the six groups in declaration order as f32."""
+    import struct
+    head = b"CGGS" + struct.pack("<HII", 1, gs.count, gs.channels)
+    atomic_write(path, head + np.asarray(gs.flat(), dtype="<f4").tobytes())
+
+
+def read_gaussians(path: str) -> GaussianSet:
+    import struct
+    data = open(path, "rb").read()
+    if len(data) < 4 or data[:4] != b"CGGS":
+        raise HoloError(f"{path}: not a CGGS file")
+    if len(data) < 14:
+        raise HoloError(f"{path}: truncated file")
+    ver, n, c = struct.unpack_from("<HII", data, 4)
+    if ver != 1:
+        raise HoloError(f"{path}: unsupported CGGS version")
+    count = (6 + 2 * c) * n
+    if len(data) < 14 + 4 * count:
+        raise HoloError(f"{path}: truncated file")
+    if len(data) != 14 + 4 * count:
+        raise HoloError(f"{path}: trailing bytes")
+    flat = np.frombuffer(data, dtype="<f4", offset=14, count=count).astype(np.float64)
+    return GaussianSet.from_flat(flat, n, c)
+
+
 # ---- end-of-run metrics (pipeline.hpp:47-57, pipeline.cpp:135-163) --------------------------------
 @dataclass
 class Metrics:
