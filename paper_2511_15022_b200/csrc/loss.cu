@@ -536,20 +536,40 @@ __global__ void adan_fused_kernel(float* __restrict__ p, const float* __restrict
     float* v = st + P;
     float* n = st + 2 * P;
     float* gp = st + 3 * P;
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < P;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        int gi = 0;
+    // four grid-strided elements per thread per iteration: all their loads are
+    // issued before any update (memory-level parallelism for the HBM stream)
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    constexpr int U = 4;
+    for (int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i0 < P; i0 += U * stride) {
+        float pv[U], gv[U], mv[U], vv[U], nv[U], gpv[U];
+        int gi[U];
 #pragma unroll
-        for (int q = 1; q < 6; ++q) gi += (i >= G.begin[q]) ? 1 : 0;
-        if (gi >= first_bad) continue;
-        float pv = p[i], mv = m[i], vv = v[i], nv = n[i], gpv = gp[i];
-        adan_update(pv, g[i], mv, vv, nv, gpv, first, static_cast<float>(b1), static_cast<float>(b2),
-                    static_cast<float>(b3), static_cast<float>(eps), K[gi]);
-        p[i] = pv;
-        m[i] = mv;
-        v[i] = vv;
-        n[i] = nv;
-        gp[i] = gpv;
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = i0 + u * stride;
+            gi[u] = 0;
+#pragma unroll
+            for (int q = 1; q < 6; ++q) gi[u] += (i >= G.begin[q]) ? 1 : 0;
+            if (i < P) {
+                pv[u] = p[i];
+                gv[u] = g[i];
+                mv[u] = m[i];
+                vv[u] = v[i];
+                nv[u] = n[i];
+                gpv[u] = gp[i];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = i0 + u * stride;
+            if (i >= P || gi[u] >= first_bad) continue;
+            adan_update(pv[u], gv[u], mv[u], vv[u], nv[u], gpv[u], first, static_cast<float>(b1),
+                        static_cast<float>(b2), static_cast<float>(b3), static_cast<float>(eps), K[gi[u]]);
+            p[i] = pv[u];
+            m[i] = mv[u];
+            v[i] = vv[u];
+            n[i] = nv[u];
+            gp[i] = gpv[u];
+        }
     }
 }
 
