@@ -20,6 +20,7 @@
 
 #include "asm.cuh"
 #include "fft_static.cuh"
+#include "fft_pair.cuh"
 
 namespace hs {
 
@@ -128,6 +129,53 @@ __device__ __forceinline__ void col_single(const ColArgs& a, const float2* __res
         sfft::out_fn([&](int i, int cc, float2 v) { dst[i * CC + cc] = v; }));
 }
 
+// Column-pair SIMD variant of col_single (fft_pair.cuh): CC = 4 columns as two
+// pairs, every thread transforms one butterfly of one pair.  The tile layout in
+// global memory is the same [row][4] complex; a 16-byte load/store moves one
+// pair's (re0, im0, re1, im1).
+template <int N, int NT, bool CONJ, class RAD>
+__device__ __forceinline__ void pcol_single(const ColArgs& a, const float2* __restrict__ tw, int plane) {
+    constexpr int CC = 4, NP = 2;
+    static_assert(NT % NP == 0, "pair of a thread must be fixed");
+    extern __shared__ float4 smem4[];
+    const int tile = blockIdx.x, c = blockIdx.y, tid = threadIdx.x;
+    const size_t tile_elems = static_cast<size_t>(a.H) * CC;
+    const size_t shift = static_cast<size_t>(a.oy) * CC;
+    const float2* src = a.in + (static_cast<size_t>(plane) * a.ntiles + tile) * tile_elems - shift;
+    float2* dst = a.out + (static_cast<size_t>(plane) * a.ntiles + tile) * tile_elems - shift;
+    const TfConst t = a.tf[c];
+    const int pp = tid % NP;
+    const int mx0 = wrapped(tile * CC + 2 * pp, a.Px), mx1 = wrapped(tile * CC + 2 * pp + 1, a.Px);
+    pfft::run<N, NP, NT, -1, pfft::Half, pfft::Full>(
+        smem4, tw, tid, RAD{},
+        pfft::in_fn([&](int i, int p) {
+            const float4 q = *reinterpret_cast<const float4*>(src + static_cast<size_t>(i) * CC + 2 * p);
+            return pfft::C2{make_float2(q.x, q.z), make_float2(q.y, q.w)};
+        }),
+        pfft::out_map([&](int i, int, pfft::C2 v) {
+            const int my = wrapped(i, N);
+            const float2 h0 = transfer_fast<CONJ>(t, mx0, my), h1 = transfer_fast<CONJ>(t, mx1, my);
+            const float2 hc = make_float2(h0.x, h1.x), hs = make_float2(h0.y, h1.y);
+            return pfft::C2{f2fma(v.im, make_float2(-hs.x, -hs.y), f2mul(v.re, hc)), f2fma(v.im, hc, f2mul(v.re, hs))};
+        }));
+    pfft::run<N, NP, NT, +1, pfft::Full, pfft::Half>(
+        smem4, tw, tid, RAD{}, pfft::InSmem{},
+        pfft::out_fn([&](int i, int p, pfft::C2 v) {
+            *reinterpret_cast<float4*>(dst + static_cast<size_t>(i) * CC + 2 * p) =
+                make_float4(v.re.x, v.im.x, v.re.y, v.im.y);
+        }));
+}
+
+template <int N, int NT, int MINB, class RAD>
+__global__ void __launch_bounds__(NT, MINB) pcols_fwd1_kernel(ColArgs a, const float2* __restrict__ tw) {
+    pcol_single<N, NT, false, RAD>(a, tw, blockIdx.y);
+}
+
+template <int N, int NT, int MINB, class RAD>
+__global__ void __launch_bounds__(NT, MINB) pcols_bwd1_kernel(ColArgs a, const float2* __restrict__ tw) {
+    pcol_single<N, NT, true, RAD>(a, tw, blockIdx.y);
+}
+
 // Single plane (the benchmark case).
 template <int N, int CC, int NT, int MINB, class RAD>
 __global__ void __launch_bounds__(NT, MINB) scols_fwd1_kernel(ColArgs a, const float2* __restrict__ tw) {
@@ -208,6 +256,8 @@ struct ColPlan {
     void (*bwdL)(ColArgs, const float2*);
     int nt, cc;
     std::vector<float2> (*table)(int);
+    int nt1 = 0;        // threads of the single-plane kernels (0: nt)
+    bool pair = false;  // single-plane kernels use the column-pair SIMD engine (float4 smem)
 };
 
 template <int N, int RB, int NT, int CCO, class RAD>
@@ -215,6 +265,17 @@ RowPlan row_plan() {
     return RowPlan{srows_fwd_kernel<N, RB, NT, CCO, RAD>, srows_inv_kernel<N, RB, NT, CCO, RAD>, NT, RB,
                    [](int n) { return sfft::twiddle_table(n, RAD{}); }};
 }
+// Column-pair SIMD single-plane kernels (CC = 4), standard multi-plane kernels.
+template <int N, int NT1, int MINB1, int NTL, class RAD>
+ColPlan pcol_plan() {
+    ColPlan p{pcols_fwd1_kernel<N, NT1, MINB1, RAD>, pcols_bwd1_kernel<N, NT1, MINB1, RAD>,
+              scols_fwdL_kernel<N, 4, NTL, 1, RAD>, scols_bwdL_kernel<N, 4, NTL, 1, RAD>, NTL, 4,
+              [](int n) { return sfft::twiddle_table(n, RAD{}); }};
+    p.nt1 = NT1;
+    p.pair = true;
+    return p;
+}
+
 // The multi-plane kernels hold two tiles in shared memory (spectrum + work),
 // so they run one CTA per SM regardless of MINB: they get the full register file.
 template <int N, int CC, int NT, int MINB, class RAD>
@@ -239,8 +300,8 @@ const std::vector<Plans>& plans() {
         {7680, 4320, 2, row_plan<7680, 2, 512, 2, Radices<16, 30, 16>>(),
          col_plan<4320, 2, 360, 2, Radices<12, 30, 12>>()},
         // tuning variants of the cfg2 grid (HS_FFT_VARIANT=k picks the k-th plan of a grid)
-        {3840, 2160, 2, row_plan<3840, 1, 256, 2, Radices<16, 15, 16>>(),
-         col_plan<2160, 2, 360, 4, Radices<12, 15, 12>>()},
+        {3840, 2160, 4, row_plan<3840, 1, 256, 4, Radices<16, 15, 16>>(),
+         pcol_plan<2160, 360, 2, 720, Radices<12, 15, 12>>()},
         {3840, 2160, 4, row_plan<3840, 1, 128, 4, Radices<16, 15, 16>>(),
          col_plan<2160, 4, 360, 3, Radices<12, 15, 12>>()},
         {3840, 2160, 4, row_plan<3840, 2, 256, 4, Radices<16, 15, 16>>(),
@@ -290,8 +351,10 @@ const float2* stable(int plan_idx, int axis, const std::vector<float2>& h) {
 
 size_t rows_smem(const Plans& p) { return sizeof(float2) * fft::padded_len(p.Px * p.row.rb); }
 size_t cols_smem(const Plans& p, int L) {
+    if (L == 1 && p.col.pair) return sizeof(float4) * pfft::padded_len4(p.Py * p.col.cc / 2);
     return sizeof(float2) * fft::padded_len(p.Py * p.col.cc) * (L > 1 ? 2 : 1);
 }
+int cols_threads(const Plans& p, int L) { return (L == 1 && p.col.nt1) ? p.col.nt1 : p.col.nt; }
 
 
 }  // namespace
@@ -329,7 +392,7 @@ bool static_forward(AsmWork& w, const float2* d_in, float2* d_out, cudaStream_t 
     if (ev) HS_CUDA(cudaEventRecord(ev[0], st));
     ColArgs c{w.T1.as<float2>(), w.T2.as<float2>(), w.C, w.H, w.Py, w.Px, w.oy, w.ntiles, w.L, w.plan_y, nullptr,
               w.tf.as<TfConst>()};
-    (w.L > 1 ? p->col.fwdL : p->col.fwd)<<<dim3(w.ntiles, w.C), p->col.nt, cs, st>>>(c, w.stw_y);
+    (w.L > 1 ? p->col.fwdL : p->col.fwd)<<<dim3(w.ntiles, w.C), cols_threads(*p, w.L), cs, st>>>(c, w.stw_y);
     launch_check("scols_fwd");
     if (ev) HS_CUDA(cudaEventRecord(ev[1], st));
     const int rows2 = w.L * w.C * w.H;
@@ -352,7 +415,7 @@ bool static_backward(AsmWork& w, const float2* d_grads, float2* d_out, cudaStrea
     if (ev) HS_CUDA(cudaEventRecord(ev[0], st));
     ColArgs c{w.T2.as<float2>(), w.T1.as<float2>(), w.C, w.H, w.Py, w.Px, w.oy, w.ntiles, w.L, w.plan_y, nullptr,
               w.tf.as<TfConst>()};
-    (w.L > 1 ? p->col.bwdL : p->col.bwd)<<<dim3(w.ntiles, w.C), p->col.nt, cs, st>>>(c, w.stw_y);
+    (w.L > 1 ? p->col.bwdL : p->col.bwd)<<<dim3(w.ntiles, w.C), cols_threads(*p, w.L), cs, st>>>(c, w.stw_y);
     launch_check("scols_bwd");
     if (ev) HS_CUDA(cudaEventRecord(ev[1], st));
     const int rows2 = w.C * w.H;
