@@ -129,6 +129,47 @@ __device__ __forceinline__ void col_single(const ColArgs& a, const float2* __res
         sfft::out_fn([&](int i, int cc, float2 v) { dst[i * CC + cc] = v; }));
 }
 
+// H(kx, ky) for the two columns of a pair at once (packed fp32x2), with the
+// same arithmetic as transfer_fast: q = bx mx^2 + by my^2, the series form of
+// kz d for q < 1/32, 2-constant Cody-Waite, MUFU sincos.  Falls back to the
+// scalar form when the aperture is on or a q of the pair is >= 1/32.
+struct PairTf {
+    float2 qx;       // (bx mx0^2, bx mx1^2)
+    float2 inband;   // 1 / 0 per column of the |mx| band limit
+    int mx0, mx1;
+};
+template <bool CONJ>
+__device__ __forceinline__ void transfer_pair(const TfConst& t, const PairTf& p, int my, float2& hc, float2& hs) {
+    if (abs(my) > t.my_max) {
+        hc = hs = make_float2(0.f, 0.f);
+        return;
+    }
+    const float fmy = static_cast<float>(my);
+    const float2 q = f2add(p.qx, f2splat(t.by * fmy * fmy));
+    if (t.a4 > 0.0 || q.x >= 0.03125f || q.y >= 0.03125f) {
+        const float2 h0 = transfer_fast<CONJ>(t, p.mx0, my), h1 = transfer_fast<CONJ>(t, p.mx1, my);
+        hc = make_float2(h0.x, h1.x);
+        hs = make_float2(h0.y, h1.y);
+        return;
+    }
+    // ser = q/2 + q^2/8 + q^3/16 + 5q^4/128 + 7q^5/256
+    float2 ser = f2fma(q, f2splat(0.02734375f), f2splat(0.0390625f));
+    ser = f2fma(q, ser, f2splat(0.0625f));
+    ser = f2fma(q, ser, f2splat(0.125f));
+    ser = f2fma(q, ser, f2splat(0.5f));
+    ser = f2mul(q, ser);
+    float2 ph = f2fma(f2splat(-t.kd), ser, f2splat(t.kd_mod));
+    const float2 nn = f2mul(ph, f2splat(0.15915494309189535f));
+    const float2 n = make_float2(rintf(nn.x), rintf(nn.y));
+    ph = f2fma(n, f2splat(-6.28318548202514648f), ph);  // 2pi rounded to fp32
+    ph = f2fma(n, f2splat(1.7484555314695172e-7f), ph);  // + (fp32(2pi) - 2pi)
+    float s0, c0, s1, c1;
+    __sincosf(ph.x, &s0, &c0);
+    __sincosf(ph.y, &s1, &c1);
+    hc = f2mul(make_float2(c0, c1), p.inband);
+    hs = f2mul(make_float2(CONJ ? -s0 : s0, CONJ ? -s1 : s1), p.inband);
+}
+
 // Column-pair SIMD variant of col_single (fft_pair.cuh): CC = 4 columns as two
 // pairs, every thread transforms one butterfly of one pair.  The tile layout in
 // global memory is the same [row][4] complex; a 16-byte load/store moves one
@@ -145,7 +186,14 @@ __device__ __forceinline__ void pcol_single(const ColArgs& a, const float2* __re
     float2* dst = a.out + (static_cast<size_t>(plane) * a.ntiles + tile) * tile_elems - shift;
     const TfConst t = a.tf[c];
     const int pp = tid % NP;
-    const int mx0 = wrapped(tile * CC + 2 * pp, a.Px), mx1 = wrapped(tile * CC + 2 * pp + 1, a.Px);
+    PairTf ptf;
+    ptf.mx0 = wrapped(tile * CC + 2 * pp, a.Px);
+    ptf.mx1 = wrapped(tile * CC + 2 * pp + 1, a.Px);
+    {
+        const float f0 = static_cast<float>(ptf.mx0), f1 = static_cast<float>(ptf.mx1);
+        ptf.qx = make_float2(t.bx * f0 * f0, t.bx * f1 * f1);
+        ptf.inband = make_float2(abs(ptf.mx0) <= t.mx_max ? 1.f : 0.f, abs(ptf.mx1) <= t.mx_max ? 1.f : 0.f);
+    }
     pfft::run<N, NP, NT, -1, pfft::Half, pfft::Full>(
         smem4, tw, tid, RAD{},
         pfft::in_fn([&](int i, int p) {
@@ -153,10 +201,10 @@ __device__ __forceinline__ void pcol_single(const ColArgs& a, const float2* __re
             return pfft::C2{make_float2(q.x, q.z), make_float2(q.y, q.w)};
         }),
         pfft::out_map([&](int i, int, pfft::C2 v) {
-            const int my = wrapped(i, N);
-            const float2 h0 = transfer_fast<CONJ>(t, mx0, my), h1 = transfer_fast<CONJ>(t, mx1, my);
-            const float2 hc = make_float2(h0.x, h1.x), hs = make_float2(h0.y, h1.y);
-            return pfft::C2{f2fma(v.im, make_float2(-hs.x, -hs.y), f2mul(v.re, hc)), f2fma(v.im, hc, f2mul(v.re, hs))};
+            float2 hc, hs;
+            transfer_pair<CONJ>(t, ptf, wrapped(i, N), hc, hs);
+            // (re + i im)(hc + i hs) per column
+            return pfft::C2{f2sub(f2mul(v.re, hc), f2mul(v.im, hs)), f2fma(v.im, hc, f2mul(v.re, hs))};
         }));
     pfft::run<N, NP, NT, +1, pfft::Full, pfft::Half>(
         smem4, tw, tid, RAD{}, pfft::InSmem{},
@@ -294,18 +342,19 @@ struct Plans {
 const std::vector<Plans>& plans() {
     static const std::vector<Plans> p = {
         {3840, 2160, 4, row_plan<3840, 1, 256, 4, Radices<16, 15, 16>>(),
-         col_plan<2160, 4, 720, 2, Radices<12, 15, 12>>()},
+         pcol_plan<2160, 360, 2, 720, Radices<12, 15, 12>>()},
         {512, 512, 4, row_plan<512, 1, 64, 4, Radices<8, 8, 8>>(), col_plan<512, 4, 128, 2, Radices<8, 8, 8>>()},
         {512, 320, 4, row_plan<512, 1, 64, 4, Radices<8, 8, 8>>(), col_plan<320, 4, 128, 2, Radices<16, 20>>()},
         {7680, 4320, 2, row_plan<7680, 2, 512, 2, Radices<16, 30, 16>>(),
          col_plan<4320, 2, 360, 2, Radices<12, 30, 12>>()},
         // tuning variants of the cfg2 grid (HS_FFT_VARIANT=k picks the k-th plan of a grid)
         {3840, 2160, 4, row_plan<3840, 1, 256, 4, Radices<16, 15, 16>>(),
-         pcol_plan<2160, 360, 2, 720, Radices<12, 15, 12>>()},
+         col_plan<2160, 4, 720, 2, Radices<12, 15, 12>>()},
         {3840, 2160, 4, row_plan<3840, 1, 128, 4, Radices<16, 15, 16>>(),
          col_plan<2160, 4, 360, 3, Radices<12, 15, 12>>()},
         {3840, 2160, 4, row_plan<3840, 2, 256, 4, Radices<16, 15, 16>>(),
          col_plan<2160, 4, 720, 2, Radices<12, 15, 12>>()},
+
     };
     return p;
 }

@@ -24,6 +24,13 @@ struct C2 {
 
 __device__ __forceinline__ C2 c2(float4 v) { return C2{make_float2(v.x, v.y), make_float2(v.z, v.w)}; }
 __device__ __forceinline__ float4 f4(C2 a) { return make_float4(a.re.x, a.re.y, a.im.x, a.im.y); }
+// store as two 8-byte halves: the re and im pairs need not sit in four
+// consecutive registers (which would cost MOVs per STS.128)
+__device__ __forceinline__ void st2(float4* dst, C2 a) {
+    float2* d = reinterpret_cast<float2*>(dst);
+    d[0] = a.re;
+    d[1] = a.im;
+}
 __device__ __forceinline__ C2 zero2() { return C2{make_float2(0.f, 0.f), make_float2(0.f, 0.f)}; }
 __device__ __forceinline__ C2 add(C2 a, C2 b) { return C2{f2add(a.re, b.re), f2add(a.im, b.im)}; }
 __device__ __forceinline__ C2 sub(C2 a, C2 b) { return C2{f2sub(a.re, b.re), f2sub(a.im, b.im)}; }
@@ -160,9 +167,11 @@ __device__ __forceinline__ void dft(C2 (&v)[R]) {
     }
 }
 
-// Padded float4 index: one pad per 8 entries.
-__device__ __forceinline__ int pidx4(int q) { return q + (q >> 3); }
-__host__ __device__ constexpr int padded_len4(int q) { return q + (q >> 3) + 8; }
+// Padded float4 index: one pad per 8 entries (1/16 was measured slower: bank
+// conflicts of the strided first-stage stores).
+constexpr int kPadShift = 3;
+__device__ __forceinline__ int pidx4(int q) { return q + (q >> kPadShift); }
+__host__ __device__ constexpr int padded_len4(int q) { return q + (q >> kPadShift) + 16; }
 
 struct Full {
     template <int R>
@@ -232,8 +241,8 @@ __device__ __forceinline__ void stage(float4* buf, const float2* __restrict__ tw
                 if (r < I0 || r >= I1) {
                     v[b][r] = zero2();
                 } else if constexpr (smem_in) {
-                    if constexpr ((M * NP) % 8 == 0)  // linear padded stride
-                        v[b][r] = c2(buf[pidx4(j * NP + pp) + r * (M * NP / 8 * 9)]);
+                    if constexpr ((M * NP) % (1 << kPadShift) == 0)  // linear padded stride
+                        v[b][r] = c2(buf[pidx4(j * NP + pp) + r * ((M * NP) >> kPadShift) * ((1 << kPadShift) + 1)]);
                     else
                         v[b][r] = c2(buf[pidx4((j + r * M) * NP + pp)]);
                 } else {
@@ -264,9 +273,11 @@ __device__ __forceinline__ void stage(float4* buf, const float2* __restrict__ tw
             for (int r = O0; r < O1; ++r) {
                 const int i = i0 + r * NS;
                 if constexpr (is_out_smem<OUT>::value) {
-                    const int q = (NS * NP) % 8 == 0 ? pidx4(i0 * NP + pp) + r * (NS * NP / 8 * 9) : pidx4(i * NP + pp);
-                    if constexpr (std::is_same<OUT, OutSmem>::value) buf[q] = f4(v[b][r]);
-                    else buf[q] = f4(out.g(i, pp, v[b][r]));
+                    const int q = (NS * NP) % (1 << kPadShift) == 0
+                                      ? pidx4(i0 * NP + pp) + r * ((NS * NP) >> kPadShift) * ((1 << kPadShift) + 1)
+                                      : pidx4(i * NP + pp);
+                    if constexpr (std::is_same<OUT, OutSmem>::value) st2(buf + q, v[b][r]);
+                    else st2(buf + q, out.g(i, pp, v[b][r]));
                 } else {
                     out.g(i, pp, v[b][r]);
                 }
