@@ -316,7 +316,7 @@ def main():
     gs = holo.GaussianSet(n, c, **gset32)
     target = holo.RealField(c, h, w, wl["target"].astype(np.float32).astype(np.float64))
     spec = holo.PropagationSpec(tuple(wl["wavelengths"]))
-    total = args.warmup + args.steps + args.e2e_steps + args.profile_steps + 2
+    total = args.warmup + args.steps + args.e2e_steps + args.profile_steps + 5
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
         tr = holo.Trainer(gs, w, h, target, wl["masks"], wl["distances"], spec, total_steps=total)
@@ -346,18 +346,16 @@ def main():
 
         # e2e through the public API with a host-resident GaussianSet (like the
         # reference loop): per step H2D params from pinned memory, the step,
-        # D2H of the updated params and the loss.
+        # D2H of the updated params and the loss (hs_trainer_step_host).
         P = tr.param_count
         host = torch.empty(P, dtype=torch.float32, pin_memory=True)
         host.copy_(torch.from_numpy(tr.params()))
-        hptr = holo.C.c_void_p(host.data_ptr())
-        lib = holo._lib.load()
+        for _ in range(3):  # warm-up (captures the host-step graph)
+            tr.step_host(host, host)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            holo.check(lib.hs_trainer_set_params(tr.h, hptr, 0))
-            tr.step(sync_loss=True)
-            holo.check(lib.hs_trainer_get_params(tr.h, hptr, 0))
+            tr.step_host(host, host)
         torch.cuda.synchronize()
         e2e_s = (time.perf_counter() - t0) / args.e2e_steps
 
@@ -409,7 +407,8 @@ def main():
         "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
         "e2e": {"value": world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 4 * P,
                 "d2h_bytes_per_step": 4 * P + 8,
-                "path": "hs_trainer_set_params(host pinned) + hs_trainer_step + hs_trainer_get_params per step"},
+                "path": "hs_trainer_step_host per step: H2D of all params from pinned host memory, graph step, "
+                        "D2H of the updated params + loss, one sync"},
         "gpu_launches": int(round(per_step_launches * args.steps)),
         "clocks": clocks, "loss": loss, "pairs": pairs,
     }

@@ -195,6 +195,12 @@ int64_t hs_trainer_param_count(hs_trainer* tr);
  * synchronises); pass NULL to stay asynchronous and fetch it later with
  * hs_trainer_last_loss. */
 hs_status hs_trainer_step(hs_trainer* tr, double* loss_out);
+/* One iteration with HOST-resident parameters, like the reference loop where the
+ * GaussianSet lives on the host: H2D of h_params_in (nullable), the step, D2H
+ * of the updated parameters into h_params_out (nullable) and of the loss --
+ * queued on the trainer stream with a single synchronisation.  Use pinned host
+ * memory for full copy bandwidth. */
+hs_status hs_trainer_step_host(hs_trainer* tr, const float* h_params_in, float* h_params_out, double* loss_out);
 /* Split form for multi-GPU: forward+backward into the gradient buffer, then
  * (after the caller all-reduced hs_trainer_grads_ptr) the optimizer update. */
 hs_status hs_trainer_forward_backward(hs_trainer* tr);

@@ -86,10 +86,25 @@ struct hs_trainer {
     cudaGraphExec_t graph = nullptr;
     bool profiling = false;
     cudaEvent_t ev[12] = {};  // profiling: start + after each of the 11 kernel slots
+    // host-resident step (hs_trainer_step_host): copy stream, fork/join events,
+    // pinned result words, and its own graph keyed by the host buffers
+    cudaStream_t copy_st = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_ap = nullptr;
+    uint32_t* h_words = nullptr;  // pinned: flags, status[4]
+    double* h_o3 = nullptr;       // pinned: loss, recon sum, ssim sum
+    cudaGraphExec_t host_graph = nullptr;
+    const float* host_in = nullptr;
+    float* host_out = nullptr;
     ~hs_trainer() {
         if (graph) cudaGraphExecDestroy(graph);
+        if (host_graph) cudaGraphExecDestroy(host_graph);
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
+        if (ev_fork) cudaEventDestroy(ev_fork);
+        if (ev_ap) cudaEventDestroy(ev_ap);
+        if (copy_st) cudaStreamDestroy(copy_st);
+        if (h_words) cudaFreeHost(h_words);
+        if (h_o3) cudaFreeHost(h_o3);
     }
 };
 
@@ -473,14 +488,14 @@ extern "C" hs_status hs_adan_step(hs_ctx* ctx, const hs_adan_config* cfg, const 
 // Profiling slots (kernel boundaries): 0 start, 1 binning, 2 raster_fwd,
 // 3 rows_fwd, 4 cols_fwd, 5 rows_inv, 6 loss, 7 rows_fwd(bwd), 8 cols_bwd,
 // 9 rows_inv(bwd), 10 raster_bwd, 11 adan.
-static void trainer_enqueue_fwd_bwd(hs_trainer* t, cudaStream_t st) {
+static void trainer_enqueue_fwd_bwd(hs_trainer* t, cudaStream_t st, cudaEvent_t shading_ready = nullptr) {
     const bool prof = t->profiling && !t->use_graph;
     auto mark = [&](int i) {
         if (prof) HS_CUDA(cudaEventRecord(t->ev[i], st));
     };
     mark(0);
     HS_CUDA(cudaMemsetAsync(t->flags.p, 0, sizeof(uint32_t), st));
-    t->rw.project_and_bin(t->params.as<float>(), st);
+    t->rw.project_and_bin(t->params.as<float>(), st, shading_ready);
     mark(1);
     raster_forward(t->rw, t->field.as<float2>(), st);
     mark(2);
@@ -503,12 +518,19 @@ static void trainer_enqueue_update(hs_trainer* t, cudaStream_t st) {
     if (t->profiling && !t->use_graph) HS_CUDA(cudaEventRecord(t->ev[11], st));
 }
 
+static void trainer_raise(hs_trainer* t, uint32_t flags, const uint32_t* stat);
+
 static void trainer_check_after(hs_trainer* t) {
     uint32_t flags = 0, stat[4];
     cudaStream_t st = t->ctx->stream;
     HS_CUDA(cudaMemcpyAsync(&flags, t->flags.p, sizeof(flags), cudaMemcpyDeviceToHost, st));
     HS_CUDA(cudaMemcpyAsync(stat, t->rw.status.p, sizeof(stat), cudaMemcpyDeviceToHost, st));
     HS_CUDA(cudaStreamSynchronize(st));
+    trainer_raise(t, flags, stat);
+}
+
+static void trainer_raise(hs_trainer* t, uint32_t flags, const uint32_t* stat) {
+    (void)t;
     if (stat[1]) throw Error(HS_EOVERFLOW, "trainer: tile-pair capacity exceeded; call hs_trainer_reserve_pairs");
     if (stat[2]) throw Error(HS_EINVAL, "activate: non-finite input");
     if (flags) {
@@ -652,8 +674,8 @@ hs_status hs_trainer_apply_update(hs_trainer* t) {
     });
 }
 
-hs_status hs_trainer_step(hs_trainer* t, double* loss_out) {
-    return guard([&] {
+static void trainer_launch_step(hs_trainer* t) {
+    {
         // cosine_lr(step, steps, ...) throws past the horizon (optimizer.cpp:60-61)
         require(t->host_step <= t->total_steps, "cosine_lr: step outside [0, total_steps]");
         cudaStream_t st = t->ctx->stream;
@@ -688,12 +710,91 @@ hs_status hs_trainer_step(hs_trainer* t, double* loss_out) {
             trainer_enqueue_update(t, st);
         }
         t->host_step += 1;
+    }
+}
+
+hs_status hs_trainer_step(hs_trainer* t, double* loss_out) {
+    return guard([&] {
+        trainer_launch_step(t);
         if (loss_out) {
             trainer_check_after(t);
             double o3[3];
             HS_CUDA(cudaMemcpy(o3, t->out3.p, sizeof(o3), cudaMemcpyDeviceToHost));
             *loss_out = o3[0];
         }
+    });
+}
+
+// One step with host-resident parameters (the reference's GaussianSet lives on
+// the host, pipeline.cpp:253-297).  The geometry groups are uploaded first on
+// the trainer stream; the amplitude/phase groups then go up on a copy stream
+// while the geometry is projected and binned, and only the shading kernel
+// waits for them.  Then the step, the D2H of the updated parameters and of the loss /
+// error words, and ONE synchronisation.  With graphs on, the whole sequence
+// (copies included) is one CUDA graph, re-captured when the host buffers change.
+static void enqueue_host_step(hs_trainer* t, cudaStream_t st, const float* in, float* out) {
+    const size_t N = t->n, geo0 = 5 * N, ap = 2 * N * t->c;  // [pos 2N | scale 2N | rot N | amp | phase | opa N]
+    float* d = t->params.as<float>();
+    // geometry first (the copy engines would otherwise split the link between
+    // the two uploads and delay the binning), then amplitude/phase alongside it
+    if (in) {
+        HS_CUDA(cudaMemcpyAsync(d, in, sizeof(float) * geo0, cudaMemcpyHostToDevice, st));
+        HS_CUDA(cudaMemcpyAsync(d + geo0 + ap, in + geo0 + ap, sizeof(float) * N, cudaMemcpyHostToDevice, st));
+    }
+    HS_CUDA(cudaEventRecord(t->ev_fork, st));
+    HS_CUDA(cudaStreamWaitEvent(t->copy_st, t->ev_fork, 0));
+    if (in) HS_CUDA(cudaMemcpyAsync(d + geo0, in + geo0, sizeof(float) * ap, cudaMemcpyHostToDevice, t->copy_st));
+    HS_CUDA(cudaEventRecord(t->ev_ap, t->copy_st));
+    trainer_enqueue_fwd_bwd(t, st, t->ev_ap);
+    trainer_enqueue_update(t, st);
+    if (out) HS_CUDA(cudaMemcpyAsync(out, d, sizeof(float) * t->P, cudaMemcpyDeviceToHost, st));
+    HS_CUDA(cudaMemcpyAsync(t->h_words, t->flags.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    HS_CUDA(cudaMemcpyAsync(t->h_words + 1, t->rw.status.p, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    HS_CUDA(cudaMemcpyAsync(t->h_o3, t->out3.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+}
+
+hs_status hs_trainer_step_host(hs_trainer* t, const float* h_params_in, float* h_params_out, double* loss_out) {
+    return guard([&] {
+        require(t->host_step <= t->total_steps, "cosine_lr: step outside [0, total_steps]");
+        cudaStream_t st = t->ctx->stream;
+        if (!t->copy_st) {
+            HS_CUDA(cudaStreamCreateWithFlags(&t->copy_st, cudaStreamNonBlocking));
+            HS_CUDA(cudaEventCreateWithFlags(&t->ev_fork, cudaEventDisableTiming));
+            HS_CUDA(cudaEventCreateWithFlags(&t->ev_ap, cudaEventDisableTiming));
+            HS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&t->h_words), 5 * sizeof(uint32_t), cudaHostAllocDefault));
+            HS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&t->h_o3), 3 * sizeof(double), cudaHostAllocDefault));
+        }
+        bool done = false;
+        if (t->use_graph && st != nullptr) {
+            if (t->host_graph && (t->host_in != h_params_in || t->host_out != h_params_out)) {
+                HS_CUDA(cudaGraphExecDestroy(t->host_graph));
+                t->host_graph = nullptr;
+            }
+            if (!t->host_graph) {
+                cudaGraph_t g = nullptr;
+                HS_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+                try {
+                    enqueue_host_step(t, st, h_params_in, h_params_out);
+                } catch (...) {
+                    cudaStreamEndCapture(st, &g);
+                    if (g) cudaGraphDestroy(g);
+                    throw;
+                }
+                HS_CUDA(cudaStreamEndCapture(st, &g));
+                HS_CUDA(cudaGraphInstantiate(&t->host_graph, g, 0));
+                HS_CUDA(cudaGraphDestroy(g));
+                t->host_in = h_params_in;
+                t->host_out = h_params_out;
+            }
+            HS_CUDA(cudaGraphLaunch(t->host_graph, st));
+            note_launch(0);
+            done = true;
+        }
+        if (!done) enqueue_host_step(t, st, h_params_in, h_params_out);
+        t->host_step += 1;
+        HS_CUDA(cudaStreamSynchronize(st));
+        trainer_raise(t, t->h_words[0], t->h_words + 1);
+        if (loss_out) *loss_out = t->h_o3[0];
     });
 }
 

@@ -61,9 +61,7 @@ __global__ void project_kernel(ProjParams P) {
     const float* pp = P.params;                 // pre_position 2N
     const float* ps = pp + 2 * N;               // pre_scale 2N
     const float* rot = ps + 2 * N;              // rotation N
-    const float* amp = rot + N;                 // amplitude N*C
-    const float* pha = amp + N * P.c;           // phase N*C
-    const float* opa = pha + N * P.c;           // pre_opacity N
+    const float* opa = rot + N + 2 * N * P.c;   // pre_opacity N (after amplitude, phase N*C each)
 
     const double prx = pp[2 * g], pry = pp[2 * g + 1];
     const double psx = ps[2 * g], psy = ps[2 * g + 1];
@@ -136,19 +134,30 @@ __global__ void project_kernel(ProjParams P) {
     double* q = P.p64 + g;
     q[0] = px; q[N] = py; q[2 * N] = i00; q[3 * N] = i01; q[4 * N] = i11; q[5 * N] = mahal_cutoff;
     q[6 * N] = alpha; q[7 * N] = r;
-    // per-channel shading (rasterizer.cpp:78-85)
-    for (int ch = 0; ch < P.c; ++ch) {
-        const size_t i = static_cast<size_t>(g) * P.c + ch;
-        // fp32 shading: only consumed in fp32 (the record is float), so the
-        // phase's sin/cos run in fp32 (accurate range reduction, ~1 ulp)
+    // per-channel shading (rasterizer.cpp:78-85): shade_kernel
+    if (!finite(th)) atomicOr(P.status + 2, 1u);
+}
+
+// Per-channel shading (rasterizer.cpp:78-85), its own kernel so that the
+// amplitude/phase groups can still be in flight (host-resident parameter
+// upload) while the geometry is binned.  fp32: the record is only consumed in
+// fp32, and sincosf has accurate range reduction (~1 ulp).
+__global__ void shade_kernel(const float* __restrict__ params, int n, int c, float4* __restrict__ shade,
+                             uint32_t* __restrict__ status) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    const size_t N = n;
+    const float* amp = params + 5 * N;       // after pre_position 2N | pre_scale 2N | rotation N
+    const float* pha = amp + N * c;
+    for (int ch = 0; ch < c; ++ch) {
+        const size_t i = static_cast<size_t>(g) * c + ch;
         const float a = fminf(fmaxf(amp[i], 0.f), 1.f);
         const float ph = pha[i];
-        if (!isfinite(ph) || !isfinite(amp[i])) atomicOr(P.status + 2, 1u);
+        if (!isfinite(ph) || !isfinite(amp[i])) atomicOr(status + 2, 1u);
         float sp, cp;
         sincosf(ph, &sp, &cp);
-        P.shade[static_cast<size_t>(ch) * N + g] = make_float4(a * cp, a * sp, cp, sp);
+        shade[static_cast<size_t>(ch) * N + g] = make_float4(a * cp, a * sp, cp, sp);
     }
-    if (!finite(th)) atomicOr(P.status + 2, 1u);
 }
 
 // ---------------------------------------------------------------------------
@@ -806,7 +815,7 @@ void RasterWork::reserve_pairs(int64_t cap_) {
     scratch.reserve(2 * static_cast<size_t>(cap) * sizeof(uint32_t));
 }
 
-void RasterWork::project_and_bin(const float* d_params, cudaStream_t st) {
+void RasterWork::project_and_bin(const float* d_params, cudaStream_t st, cudaEvent_t shading_ready) {
     uint32_t* stat = status.as<uint32_t>();
     HS_CUDA(cudaMemsetAsync(stat, 0, 4 * sizeof(uint32_t), st));
     const int tiles = tiles_x * tiles_y;
@@ -835,6 +844,9 @@ void RasterWork::project_and_bin(const float* d_params, cudaStream_t st) {
     segment_sort_kernel<<<ceil_div(tiles, 256), 256, 0, st>>>(ranges.as<uint2>(), tiles, ids.as<uint32_t>(),
                                                                scratch.as<uint32_t>(), stat);
     launch_check("segment_sort");
+    if (shading_ready) HS_CUDA(cudaStreamWaitEvent(st, shading_ready, 0));  // amplitude/phase uploaded
+    shade_kernel<<<ceil_div(n, 256), 256, 0, st>>>(d_params, n, c, shade.as<float4>(), stat);
+    launch_check("shade");
 }
 
 void export_tile_index(const RasterWork& rw, int64_t k, uint32_t* d_tiles, uint32_t* d_ids,

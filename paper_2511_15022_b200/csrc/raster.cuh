@@ -27,8 +27,11 @@ struct RasterWork {
 
     void prepare(int n_, int c_, int w_, int h_);
     void reserve_pairs(int64_t cap_);
-    // K0 + K1 on stream; leaves per-tile sorted ids + ranges on device (K in status[0]).
-    void project_and_bin(const float* d_params, cudaStream_t st);
+    // K0 + K1 + shading on stream; leaves per-tile sorted ids + ranges on device
+    // (K in status[0]).  shading_ready (nullable): event the shading kernel waits
+    // for -- the amplitude/phase groups may still be uploading while the
+    // geometry is projected and binned.
+    void project_and_bin(const float* d_params, cudaStream_t st, cudaEvent_t shading_ready = nullptr);
 };
 
 void raster_forward(const RasterWork& rw, float2* d_field, cudaStream_t st);

@@ -819,6 +819,28 @@ class Trainer:
         check(_lib.load().hs_trainer_stage_ms(self.h, out))
         return dict(zip(self.STAGES, list(out)))
 
+    def step_host(self, params_in, params_out=None) -> float:
+        """One step with host-resident parameters (hs_trainer_step_host): H2D of
+        params_in, the step, D2H of the updated parameters into params_out and of
+        the loss, one synchronisation.  Pass pinned torch tensors (fp32, CPU) for
+        full copy bandwidth; numpy arrays work too."""
+        self._ctx = ctx_handle()
+
+        def addr(x):
+            if x is None:
+                return None
+            if isinstance(x, torch.Tensor):
+                if x.is_cuda or x.dtype != torch.float32 or not x.is_contiguous() or x.numel() != self.param_count:
+                    raise HoloInvalidArgument("step_host: need a contiguous fp32 host tensor of param_count floats")
+                return C.c_void_p(x.data_ptr())
+            if x.dtype != np.float32 or not x.flags.c_contiguous or x.size != self.param_count:
+                raise HoloInvalidArgument("step_host: need a contiguous fp32 array of param_count floats")
+            return x.ctypes.data_as(C.c_void_p)
+
+        v = C.c_double(0.0)
+        check(_lib.load().hs_trainer_step_host(self.h, addr(params_in), addr(params_out), C.byref(v)))
+        return v.value
+
     def step(self, sync_loss=True):
         self._ctx = ctx_handle()
         if sync_loss:

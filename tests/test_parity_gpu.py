@@ -377,3 +377,24 @@ def test_channel_sharded_trainers_match_full_step(holo):
     geo_full = np.concatenate([gf[lo:hi] for lo, hi in P.geometry_ranges(n, c)])
     assert rel_l2(geo_sum, geo_full) < 1e-5
     assert parts[0] == pytest.approx(pf[0], rel=1e-6) and parts[1] == pytest.approx(pf[1], rel=1e-6)
+
+
+def test_trainer_step_host_matches_device_step(holo):
+    """hs_trainer_step_host (host-resident parameters, one sync) runs the same
+    step as set_params + step + get_params."""
+    import torch
+    c, w, h, n, L = 3, 64, 48, 400, 1
+    g = f32(S.init_gaussians(n, c, w, h, 5))
+    img = S.synthetic_image(42, c, h, w)
+    masks = S.build_masks(S.synthetic_depth(43, h, w), L, True)
+    dist = S.make_depth_planes(L, 3e-3, 2e-3)
+    mk = lambda: holo.Trainer(holo.GaussianSet(n, c, **g), w, h, holo.RealField(c, h, w, img), masks, dist,
+                              holo.PropagationSpec(), 10)
+    a, b = mk(), mk()
+    p0 = a.params()
+    host = torch.from_numpy(p0.copy()).pin_memory()
+    la = a.step(sync_loss=True)
+    pa = a.params()
+    lb = b.step_host(host, host)
+    assert lb == la
+    assert np.array_equal(host.numpy(), pa)
