@@ -209,6 +209,23 @@ def test_static_grid_sizes_with_other_pads(holo, ref, h, w, pad):
     assert rel_l2(np.stack([a.real, a.imag]), np.stack(b)) <= FIELD_TOL
 
 
+@pytest.mark.parametrize("pitch,ap,d", [(1.0e-6, 0.0, 1e-3), (3.74e-6, 900.0, 3e-3)])
+def test_cfg2_grid_band_limit_and_aperture(holo, ref, pitch, ap, d):
+    """The pair-SIMD column kernel of the cfg2 grid on its fallback paths: a fine
+    pitch makes q = (2 pi f / k)^2 exceed the series range (and activates the band
+    limit), an aperture switches the transfer to the scalar form."""
+    c, h, w = 1, 1080, 1920
+    hsp = holo.PropagationSpec((532e-9,), pixel_pitch=pitch, pad_factor=2, aperture_radius=ap)
+    rsp = ref.PropagationSpec((532e-9,), pixel_pitch=pitch, pad_factor=2, aperture_radius=ap)
+    re, im = field32(79, c, h, w)
+    a = holo.propagate(holo.ComplexField(c, h, w, re, im), hsp, d)
+    b = ref.propagate(re, im, rsp, d)
+    assert rel_l2(np.stack([a.real, a.imag]), np.stack(b)) <= FIELD_TOL
+    a = holo.propagate_backward(holo.ComplexField(c, h, w, re, im), hsp, d)
+    b = ref.propagate(re, im, rsp, d, mode=2)
+    assert rel_l2(np.stack([a.real, a.imag]), np.stack(b)) <= FIELD_TOL
+
+
 def test_propagate_4k_grid(holo, ref):
     """cfg4 padded grid (4320 x 7680, the CC=2 plan) for one channel, fwd and adjoint."""
     c, h, w = 1, 2160, 3840
