@@ -435,14 +435,22 @@ __device__ __forceinline__ bool cell_hit(float4 r0, float4 r1, float4 r2, float 
     return xhi >= cx0 && xlo <= cx0 + cw;
 }
 
+// staged Gaussian of the forward kernel (shared memory)
+template <int C>
+struct alignas(16) FwdRec {
+    float4 r0, r1, r2;  // projection record (raster.cu K0)
+    float2 sh[C];       // (amp cos, amp sin) per channel
+    uint32_t id;
+};
+
 template <int C>
 __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(
     const uint32_t* __restrict__ ids, const uint2* __restrict__ ranges,
     const float4* __restrict__ rec, const float4* __restrict__ shade,
     const double* __restrict__ p64, int N, int tiles_x, int W, int H, float2* __restrict__ field) {
-    __shared__ float4 s_rec[3][kFwdBatch];
-    __shared__ float2 s_sh[C][kFwdBatch];  // (amp cos, amp sin) per channel
-    __shared__ uint32_t s_id[kFwdBatch];
+    // one contiguous record per staged Gaussian: a hit reads it through one
+    // base address with immediate offsets (lanes broadcast the same record)
+    __shared__ FwdRec<C> s_g[kFwdBatch];
     const int tile = blockIdx.x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -460,14 +468,15 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(
         __syncthreads();
         if (static_cast<int>(threadIdx.x) < cnt) {
             const uint32_t g = ids[base + threadIdx.x];
-            s_id[threadIdx.x] = g;
-            s_rec[0][threadIdx.x] = rec[g];
-            s_rec[1][threadIdx.x] = rec[static_cast<size_t>(N) + g];
-            s_rec[2][threadIdx.x] = rec[2 * static_cast<size_t>(N) + g];
+            FwdRec<C>& d = s_g[threadIdx.x];
+            d.id = g;
+            d.r0 = rec[g];
+            d.r1 = rec[static_cast<size_t>(N) + g];
+            d.r2 = rec[2 * static_cast<size_t>(N) + g];
 #pragma unroll
             for (int c = 0; c < C; ++c) {
                 const float4 sh = shade[static_cast<size_t>(c) * N + g];
-                s_sh[c][threadIdx.x] = make_float2(sh.x, sh.y);
+                d.sh[c] = make_float2(sh.x, sh.y);
             }
         }
         __syncthreads();
@@ -475,13 +484,14 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(
             const int j = sub + lane;
             bool hit = false;
             if (j < cnt)
-                hit = cell_hit(s_rec[0][j], s_rec[1][j], s_rec[2][j], static_cast<float>(cx0),
-                               static_cast<float>(cy0), 7.f, 7.f);
+                hit = cell_hit(s_g[j].r0, s_g[j].r1, s_g[j].r2, static_cast<float>(cx0), static_cast<float>(cy0),
+                               7.f, 7.f);
             uint32_t mask = __ballot_sync(0xffffffffu, hit);
             while (mask) {  // warp-uniform: hits in ascending id order
                 const int jj = sub + __ffs(mask) - 1;
                 mask &= mask - 1;
-                const float4 r0 = s_rec[0][jj], r1 = s_rec[1][jj], r2 = s_rec[2][jj];
+                const FwdRec<C>& G = s_g[jj];
+                const float4 r0 = G.r0, r1 = G.r1, r2 = G.r2;
                 const float dx = (fx - r0.x) - r0.z;
                 const float dyA = (fy - r0.y) - r0.w;
                 const float dyB = dyA + 4.f;
@@ -498,7 +508,7 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(
                 float aB = mB <= lo ? fminf(0.99f, ex2f(fmaf(mB, kNegHalfLog2e, r2.x))) : 0.f;
                 const bool bandA = mA > lo && mA <= hi, bandB = mB > lo && mB <= hi;
                 if (__any_sync(0xffffffffu, bandA || bandB)) {  // rare: exact fp64 decision
-                    const double* q = p64 + s_id[jj];
+                    const double* q = p64 + G.id;
                     double G, ae;
                     bool sat;
                     if (bandA) aA = exact_contrib(q, N, x, y, G, sat, ae) ? static_cast<float>(ae) : 0.f;
@@ -506,7 +516,7 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(
                 }
 #pragma unroll
                 for (int c = 0; c < C; ++c) {
-                    const float2 sh = s_sh[c][jj];
+                    const float2 sh = G.sh[c];
                     accA[c] = f2fma(f2splat(aA), sh, accA[c]);
                     accB[c] = f2fma(f2splat(aB), sh, accB[c]);
                 }

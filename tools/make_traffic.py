@@ -9,7 +9,7 @@ SLOTS = {  # kernel-name fragment -> bench.py stage slots it serves
 }
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
-def main(rep, out):
+def main(rep, out, workload="cfg2"):
     txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     h, u = rows[0], rows[1]
@@ -22,9 +22,11 @@ def main(rep, out):
                 for s in slots:
                     res.setdefault(s, []).append(b)
     res = {k: sum(v) / len(v) for k, v in res.items()}
-    json.dump({"source": rep, "unit": "bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum)", **res},
+    json.dump({"source": rep, "workload": workload,
+               "unit": "bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum)", **res},
               open(out, "w"), indent=1)
     print(json.dumps(res, indent=1))
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "profiles/traffic.json")
+    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "profiles/traffic.json",
+         sys.argv[3] if len(sys.argv) > 3 else "cfg2")
