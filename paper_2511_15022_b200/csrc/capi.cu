@@ -600,8 +600,9 @@ hs_status hs_trainer_create(hs_ctx* ctx, const hs_trainer_config* cfg, hs_traine
         t->partials.reserve(sizeof(double) * 2 * t->loss_slots);
         t->out3.reserve(sizeof(double) * 3);
         t->flags.reserve(sizeof(uint32_t));
-        t->step.reserve(2 * sizeof(int));
-        HS_CUDA(cudaMemsetAsync(t->step.p, 0, 2 * sizeof(int), st));
+        t->step.reserve(kAdanStepBytes);  // step counters + the fused Adan's precomputed group constants
+        HS_CUDA(cudaMemsetAsync(t->step.p, 0, kAdanStepBytes, st));
+        adan_init_consts(t->groups, t->total_steps, 0.98, 0.92, 0.99, t->step.as<int>(), st);
         HS_CUDA(cudaMemsetAsync(t->flags.p, 0, sizeof(uint32_t), st));
         t->rw.prepare(t->n, t->c, t->w, t->h);
         t->aw.prepare(t->c, t->h, t->w, t->spec.pad_factor, t->L);

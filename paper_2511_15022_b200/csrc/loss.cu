@@ -506,69 +506,103 @@ __global__ void intensity_kernel(const float2* f, int64_t n, float* out) {
 }
 
 // ---- Adan (GroupConst, adan_update: loss.cuh) -------------------------------------
-__global__ void adan_fused_kernel(float* __restrict__ p, const float* __restrict__ g,
-                                  float* __restrict__ st, int64_t P, AdanGroups G, int total_steps,
-                                  double b1, double b2, double b3, double eps,
-                                  const int* __restrict__ step, const uint32_t* __restrict__ flags) {
-    __shared__ GroupConst K[6];
-    __shared__ int first_bad;
-    const int t = step[1] + 1;
-    if (threadIdx.x < 6) {
-        const int gi = threadIdx.x;
+// Per-group Adan constants for loop step s and Adan step t: lr (cosine for
+// the position group, pipeline.cpp:254) and the bias corrections.
+__device__ void adan_consts(const AdanGroups& G, int total_steps, double b1, double b2, double b3, int s, int t,
+                            GroupConst* K) {
+    for (int gi = 0; gi < 6; ++gi) {
         double lr = G.base_lr[gi];
-        if (gi == 0) {  // cosine_lr(step, total, 1e-2, 1e-3), pipeline.cpp:254
-            const double s = static_cast<double>(step[0]);
-            lr = 1e-3 + 0.5 * (1e-2 - 1e-3) * (1.0 + cos(3.14159265358979323846 * s / total_steps));
-        }
+        if (gi == 0)  // cosine_lr(step, total, 1e-2, 1e-3)
+            lr = 1e-3 + 0.5 * (1e-2 - 1e-3) * (1.0 + cos(3.14159265358979323846 * static_cast<double>(s) / total_steps));
         const double bc1 = 1.0 - pow(b1, static_cast<double>(t));
         const double bc2 = 1.0 - pow(b2, static_cast<double>(t));
         const double bc3 = 1.0 - pow(b3, static_cast<double>(t));
-        K[gi] = GroupConst{static_cast<float>(lr), static_cast<float>(1.0 / bc1),
-                           static_cast<float>(b2 / bc2), static_cast<float>(1.0 / bc3)};
+        K[gi] = GroupConst{static_cast<float>(lr), static_cast<float>(1.0 / bc1), static_cast<float>(b2 / bc2),
+                           static_cast<float>(1.0 / bc3)};
     }
+}
+
+__global__ void adan_consts_kernel(AdanGroups G, int total_steps, double b1, double b2, double b3,
+                                   const int* __restrict__ step, GroupConst* __restrict__ K) {
+    adan_consts(G, total_steps, b1, b2, b3, step[0], step[1] + 1, K);
+}
+
+// Fused Adan over the six groups (optimizer.cpp:99-123) with the group
+// constants of this step precomputed in Kc.  VEC: every group boundary and P
+// are multiples of 4, so a thread updates a float4 of one group with 16-byte
+// loads/stores.  The last CTA to finish advances the device step counter (not
+// after a non-finite gradient: the reference aborts) and precomputes the next
+// step's constants.
+template <bool VEC>
+__global__ void adan_fused_kernel(float* __restrict__ p, const float* __restrict__ g,
+                                  float* __restrict__ st, int64_t P, AdanGroups G, int total_steps,
+                                  double b1, double b2, double b3, double eps,
+                                  int* __restrict__ step, const uint32_t* __restrict__ flags,
+                                  unsigned* __restrict__ done, GroupConst* __restrict__ Kc) {
+    __shared__ GroupConst K[6];
+    __shared__ int first_bad;
+    if (threadIdx.x < 6) K[threadIdx.x] = Kc[threadIdx.x];
     if (threadIdx.x == 0) {
         const uint32_t f = flags ? *flags : 0u;
         first_bad = f ? __ffs(f) - 1 : 6;
     }
+    const bool first = step[1] == 0;  // Adan t == 1
     __syncthreads();
-    const bool first = t == 1;
+    const float fb1 = static_cast<float>(b1), fb2 = static_cast<float>(b2), fb3 = static_cast<float>(b3);
+    const float feps = static_cast<float>(eps);
     float* m = st;
     float* v = st + P;
     float* n = st + 2 * P;
     float* gp = st + 3 * P;
-    // four grid-strided elements per thread per iteration: all their loads are
-    // issued before any update (memory-level parallelism for the HBM stream)
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    constexpr int U = 4;
-    for (int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i0 < P; i0 += U * stride) {
-        float pv[U], gv[U], mv[U], vv[U], nv[U], gpv[U];
-        int gi[U];
+    if constexpr (VEC) {
+        const int64_t P4 = P / 4;
+        for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < P4; q += stride) {
+            const int64_t i = 4 * q;
+            int gi = 0;
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t i = i0 + u * stride;
-            gi[u] = 0;
-#pragma unroll
-            for (int q = 1; q < 6; ++q) gi[u] += (i >= G.begin[q]) ? 1 : 0;
-            if (i < P) {
-                pv[u] = p[i];
-                gv[u] = g[i];
-                mv[u] = m[i];
-                vv[u] = v[i];
-                nv[u] = n[i];
-                gpv[u] = gp[i];
-            }
+            for (int k = 1; k < 6; ++k) gi += (i >= G.begin[k]) ? 1 : 0;
+            if (gi >= first_bad) continue;
+            float4 pv = reinterpret_cast<float4*>(p)[q], gv = reinterpret_cast<const float4*>(g)[q];
+            float4 mv = reinterpret_cast<float4*>(m)[q], vv = reinterpret_cast<float4*>(v)[q];
+            float4 nv = reinterpret_cast<float4*>(n)[q], gpv = reinterpret_cast<float4*>(gp)[q];
+            adan_update(pv.x, gv.x, mv.x, vv.x, nv.x, gpv.x, first, fb1, fb2, fb3, feps, K[gi]);
+            adan_update(pv.y, gv.y, mv.y, vv.y, nv.y, gpv.y, first, fb1, fb2, fb3, feps, K[gi]);
+            adan_update(pv.z, gv.z, mv.z, vv.z, nv.z, gpv.z, first, fb1, fb2, fb3, feps, K[gi]);
+            adan_update(pv.w, gv.w, mv.w, vv.w, nv.w, gpv.w, first, fb1, fb2, fb3, feps, K[gi]);
+            reinterpret_cast<float4*>(p)[q] = pv;
+            reinterpret_cast<float4*>(m)[q] = mv;
+            reinterpret_cast<float4*>(v)[q] = vv;
+            reinterpret_cast<float4*>(n)[q] = nv;
+            reinterpret_cast<float4*>(gp)[q] = gpv;
         }
+    } else {
+        for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < P; i += stride) {
+            int gi = 0;
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t i = i0 + u * stride;
-            if (i >= P || gi[u] >= first_bad) continue;
-            adan_update(pv[u], gv[u], mv[u], vv[u], nv[u], gpv[u], first, static_cast<float>(b1),
-                        static_cast<float>(b2), static_cast<float>(b3), static_cast<float>(eps), K[gi[u]]);
-            p[i] = pv[u];
-            m[i] = mv[u];
-            v[i] = vv[u];
-            n[i] = nv[u];
-            gp[i] = gpv[u];
+            for (int k = 1; k < 6; ++k) gi += (i >= G.begin[k]) ? 1 : 0;
+            if (gi >= first_bad) continue;
+            float pv = p[i], mv = m[i], vv = v[i], nv = n[i], gpv = gp[i];
+            adan_update(pv, g[i], mv, vv, nv, gpv, first, fb1, fb2, fb3, feps, K[gi]);
+            p[i] = pv;
+            m[i] = mv;
+            v[i] = vv;
+            n[i] = nv;
+            gp[i] = gpv;
+        }
+    }
+    // last CTA out (every CTA has read step and Kc) advances the counter and
+    // prepares the next step's constants
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(done, 1u) == gridDim.x - 1) {
+            *done = 0u;
+            if (!(flags && *flags)) {
+                step[0] += 1;
+                step[1] += 1;
+            }
+            adan_consts(G, total_steps, b1, b2, b3, step[0], step[1] + 1, Kc);
         }
     }
 }
@@ -687,11 +721,24 @@ void intensity_launch(const float2* f, int64_t count, float* out, cudaStream_t s
 void adan_fused_launch(float* params, const float* grads, float* state, int64_t P,
                        const AdanGroups& g, int total_steps, double b1, double b2, double b3,
                        double eps, int* d_step, const uint32_t* d_flags, cudaStream_t st) {
-    adan_fused_kernel<<<grid_for(P, 256), 256, 0, st>>>(params, grads, state, P, g, total_steps, b1, b2,
-                                                        b3, eps, d_step, d_flags);
+    bool vec = P % 4 == 0;
+    for (int k = 0; k < 6; ++k) vec = vec && g.begin[k] % 4 == 0;
+    // d_step holds {loop step, adan t, CTA done counter, pad, GroupConst[6]}
+    unsigned* done = reinterpret_cast<unsigned*>(d_step + 2);
+    GroupConst* kc = reinterpret_cast<GroupConst*>(d_step + 4);
+    if (vec)
+        adan_fused_kernel<true><<<grid_for(P / 4, 256), 256, 0, st>>>(params, grads, state, P, g, total_steps, b1, b2,
+                                                                      b3, eps, d_step, d_flags, done, kc);
+    else
+        adan_fused_kernel<false><<<grid_for(P, 256), 256, 0, st>>>(params, grads, state, P, g, total_steps, b1, b2,
+                                                                   b3, eps, d_step, d_flags, done, kc);
     launch_check("adan_fused");
-    adan_advance_kernel<<<1, 1, 0, st>>>(d_step, d_flags);
-    launch_check("adan_advance");
+}
+
+void adan_init_consts(const AdanGroups& g, int total_steps, double b1, double b2, double b3, int* d_step,
+                      cudaStream_t st) {
+    adan_consts_kernel<<<1, 1, 0, st>>>(g, total_steps, b1, b2, b3, d_step, reinterpret_cast<GroupConst*>(d_step + 4));
+    launch_check("adan_consts");
 }
 
 void adan_group_launch(float* params, const float* grads, float* state, int64_t size, int t,

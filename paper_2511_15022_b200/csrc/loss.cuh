@@ -67,7 +67,12 @@ struct AdanDeviceStep {
     int step;          // 0-based loop step (cosine schedule input)
     int t;             // 1-based Adan step after increment
 };
-// Reads the step counter from d_step (int2: loop step, adan t) and the flags
+// d_step layout: int[4] {loop step, adan t, CTA done counter, pad} then the 6
+// GroupConst of the coming step (adan_init_consts once, then kept by the kernel).
+inline constexpr size_t kAdanStepBytes = 4 * sizeof(int) + 6 * sizeof(GroupConst);
+void adan_init_consts(const AdanGroups& g, int total_steps, double b1, double b2, double b3, int* d_step,
+                      cudaStream_t st);
+// Reads the step counter from d_step and the flags
 // word; advances the counter.  Position lr follows cosine_lr(step, total,
 // 1e-2, 1e-3) (pipeline.cpp:254).
 void adan_fused_launch(float* params, const float* grads, float* state, int64_t P,
