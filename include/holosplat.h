@@ -219,6 +219,32 @@ hs_status hs_trainer_set_profiling(hs_trainer* tr, int enable);
 hs_status hs_trainer_stage_ms(hs_trainer* tr, double* out12);
 int hs_trainer_step_count(hs_trainer* tr);
 
+/* ---- row-slab sharding: the 4K step over R GPUs -------------
+ * No reference interface: the reference is single-process (propagation.cpp:
+ * 186-294 runs one 2D FFT per channel on the host).  Rank `rank` of `ranks`
+ * owns canvas rows [rank H/R, (rank+1) H/R) and padded-spectrum column tiles
+ * [rank nt/R, (rank+1) nt/R).  A step is five stages with an all-to-all between
+ * consecutive stages (the 2D-FFT transposes):
+ *   stage 0  binning, raster forward of the own rows, row FFTs        -> exchange 0
+ *   stage 1  column FFT x H_l, column IFFT of the own tiles            -> exchange 1
+ *   stage 2  row IFFTs of the loss band (own rows + 10-row halos),
+ *            loss + dL/dU, backward row FFTs                           -> exchange 2
+ *   stage 3  adjoint column pass of the own tiles                      -> exchange 3
+ *   stage 4  row IFFTs of the own rows, raster backward over them
+ * then an all-reduce (sum) of hs_trainer_grads_ptr, hs_trainer_apply_update,
+ * and an all-reduce of hs_trainer_loss_partials.  Exchange e sends
+ * counts[p] floats from the send buffer (peer-major, in peer order) to peer p
+ * and receives recv[p] floats from peer p into the receive buffer (peer-major):
+ * all_to_all_single(recv, send, recv_counts, send_counts).
+ * Requires H % ranks == 0, (padded width / tile width) % ranks == 0, ranks <= 16,
+ * no plane or channel sharding. */
+hs_status hs_trainer_set_row_slab(hs_trainer* tr, int rank, int ranks);
+/* out[2*ranks]: send counts per peer, then receive counts per peer (floats). */
+hs_status hs_trainer_slab_counts(hs_trainer* tr, int exchange, int64_t* out);
+float* hs_trainer_slab_send_ptr(hs_trainer* tr);
+float* hs_trainer_slab_recv_ptr(hs_trainer* tr);
+hs_status hs_trainer_slab_stage(hs_trainer* tr, int stage);
+
 #ifdef __cplusplus
 }
 #endif

@@ -117,6 +117,11 @@ _SIGS = {
     "hs_trainer_set_profiling": [C.c_void_p, C.c_int],
     "hs_trainer_stage_ms": [C.c_void_p, C.POINTER(C.c_double)],
     "hs_trainer_step_count": [C.c_void_p],
+    "hs_trainer_set_row_slab": [C.c_void_p, C.c_int, C.c_int],
+    "hs_trainer_slab_counts": [C.c_void_p, C.c_int, C.POINTER(C.c_int64)],
+    "hs_trainer_slab_send_ptr": [C.c_void_p],
+    "hs_trainer_slab_recv_ptr": [C.c_void_p],
+    "hs_trainer_slab_stage": [C.c_void_p, C.c_int],
     "hs_last_error": [],
     "hs_kernel_launch_count": [],
 }
@@ -126,6 +131,8 @@ _RESTYPES = {
     "hs_kernel_launch_count": C.c_uint64,
     "hs_trainer_params_ptr": C.c_void_p,
     "hs_trainer_grads_ptr": C.c_void_p,
+    "hs_trainer_slab_send_ptr": C.c_void_p,
+    "hs_trainer_slab_recv_ptr": C.c_void_p,
     "hs_trainer_param_count": C.c_int64,
     "hs_trainer_step_count": C.c_int,
     "hs_ctx_destroy": None,

@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(256) cols_fwd_kernel(ColArgs a) {
         __syncthreads();
         for (int e = threadIdx.x; e < n * CC; e += blockDim.x) {
             const int ky = e / CC;
-            const int kx = tile * CC + (e - ky * CC);
+            const int kx = (a.tile0 + tile) * CC + (e - ky * CC);
             const float2 h = transfer<false>(t, wrapped(kx, a.Px), wrapped(ky, n));
             work[fft::pidx(e)] = cmul(from[fft::pidx(e)], h);
         }
@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(256) cols_bwd_kernel(ColArgs a) {
         float2* dst = (a.L > 1) ? Z : spec;
         for (int e = threadIdx.x; e < n * CC; e += blockDim.x) {
             const int ky = e / CC;
-            const int kx = tile * CC + (e - ky * CC);
+            const int kx = (a.tile0 + tile) * CC + (e - ky * CC);
             const float2 h = transfer<true>(t, wrapped(kx, a.Px), wrapped(ky, n));
             const float2 v = cmul(spec[fft::pidx(e)], h);
             if (a.L > 1 && l > 0) dst[fft::pidx(e)] = cadd(dst[fft::pidx(e)], v);
@@ -379,6 +379,82 @@ void asm_backward(AsmWork& w, const float2* d_grads, float2* d_out, cudaStream_t
         case 2: launch_backward<2>(w, d_grads, d_out, st, ev); break;
         default: launch_backward<1>(w, d_grads, d_out, st, ev); break;
     }
+}
+
+// ---- row-slab passes and the exchange block copy ----------------------------------------
+template <int CC>
+static void rows_pass_generic(AsmWork& w, bool inverse, const float2* in, float2* out, int planes, int h,
+                              cudaStream_t st) {
+    const float scale = inverse ? static_cast<float>(1.0 / (static_cast<double>(w.Px) * w.Py)) : 1.f;
+    RowArgs r{in, out, w.W, h, w.Px, w.ox, w.ntiles, scale, w.plan_x, w.twx_ptr};
+    if (inverse) rows_inv_kernel<CC><<<planes * h, 256, w.smem_rows, st>>>(r);
+    else rows_fwd_kernel<CC><<<planes * h, 256, w.smem_rows, st>>>(r);
+    launch_check(inverse ? "rows_inv" : "rows_fwd");
+}
+
+template <int CC>
+static void cols_pass_generic(AsmWork& w, bool backward, const float2* in, float2* out, int tile0, int nt,
+                              cudaStream_t st) {
+    ColArgs c{in, out, w.C, w.H, w.Py, w.Px, w.oy, nt, w.L, w.plan_y, w.twy_ptr, w.tf.as<TfConst>()};
+    c.tile0 = tile0;
+    if (backward) cols_bwd_kernel<CC><<<dim3(nt, w.C), 256, w.smem_cols, st>>>(c);
+    else cols_fwd_kernel<CC><<<dim3(nt, w.C), 256, w.smem_cols, st>>>(c);
+    launch_check(backward ? "cols_bwd" : "cols_fwd");
+}
+
+void asm_rows_pass(AsmWork& w, bool inverse, const float2* in, float2* out, int planes, int h, cudaStream_t st) {
+    if (planes * h == 0) return;
+    if (w.use_static && static_rows_pass(w, inverse, in, out, planes, h, st)) return;
+    switch (w.CC) {
+        case 4: rows_pass_generic<4>(w, inverse, in, out, planes, h, st); break;
+        case 2: rows_pass_generic<2>(w, inverse, in, out, planes, h, st); break;
+        default: rows_pass_generic<1>(w, inverse, in, out, planes, h, st); break;
+    }
+}
+
+void asm_cols_pass(AsmWork& w, bool backward, const float2* in, float2* out, int tile0, int ntiles_local,
+                   cudaStream_t st) {
+    require(tile0 >= 0 && ntiles_local >= 1 && tile0 + ntiles_local <= w.ntiles, "propagation: column slab out of range");
+    if (w.use_static && static_cols_pass(w, backward, in, out, tile0, ntiles_local, st)) return;
+    switch (w.CC) {
+        case 4: cols_pass_generic<4>(w, backward, in, out, tile0, ntiles_local, st); break;
+        case 2: cols_pass_generic<2>(w, backward, in, out, tile0, ntiles_local, st); break;
+        default: cols_pass_generic<1>(w, backward, in, out, tile0, ntiles_local, st); break;
+    }
+}
+
+namespace {
+// One warp per chunk; 16-byte moves when the chunk's offsets and length are even.
+__global__ void __launch_bounds__(256) chunk_copy_kernel(const float2* __restrict__ src, float2* __restrict__ dst,
+                                                         ChunkMap m) {
+    const int64_t nchunks = static_cast<int64_t>(m.A) * m.B * m.T;
+    const int lane = threadIdx.x & 31;
+    for (int64_t k = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; k < nchunks;
+         k += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+        const int t = static_cast<int>(k % m.T);
+        const int64_t ab = k / m.T;
+        const int b = static_cast<int>(ab % m.B), a = static_cast<int>(ab / m.B);
+        const int64_t so = m.sA[a] + b * m.sB[a] + t * m.sT[a];
+        const int64_t dof = m.dA[a] + b * m.dB[a] + t * m.dT[a];
+        const int64_t len = m.len[a];
+        if (((so | dof | len) & 1) == 0) {
+            const float4* s4 = reinterpret_cast<const float4*>(src + so);
+            float4* d4 = reinterpret_cast<float4*>(dst + dof);
+            for (int64_t i = lane; i < len / 2; i += 32) d4[i] = s4[i];
+        } else {
+            for (int64_t i = lane; i < len; i += 32) dst[dof + i] = src[so + i];
+        }
+    }
+}
+}  // namespace
+
+void chunk_copy(const float2* src, float2* dst, const ChunkMap& m, cudaStream_t st) {
+    require(m.A >= 1 && m.A <= kMaxPeers, "slab exchange: peer count outside 1..16");
+    const int64_t nchunks = static_cast<int64_t>(m.A) * m.B * m.T;
+    if (nchunks == 0) return;
+    const int64_t blocks = std::min<int64_t>((nchunks + 7) / 8, 148 * 8);
+    chunk_copy_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(src, dst, m);
+    launch_check("chunk_copy");
 }
 
 }  // namespace hs

@@ -85,12 +85,39 @@ struct ColArgs {
     fft::Plan plan;
     const float2* tw;
     const TfConst* tf;  // [L][C]
+    int tile0 = 0;      // global index of tile 0 of this call (column-slab shard)
 };
+
+// ---- row-slab sharding (cfg4 distributed FFT) ------------------------
+// The three passes of asm_forward / asm_backward on explicit buffers.
+// Row pass over `planes` stacked fields of h rows each: forward
+// in [planes][h][W] -> T [planes][ntiles][h][CC]; inverse T -> [planes][h][W]
+// (cropped, x 1/(Px Py)).
+void asm_rows_pass(AsmWork& w, bool inverse, const float2* in, float2* out, int planes, int h, cudaStream_t st);
+// Column pass over the column tiles [tile0, tile0 + ntiles_local) of all H
+// rows: forward T [C][nt][H][CC] -> [L][C][nt][H][CC] (x H_l), backward
+// [L][C][nt][H][CC] -> [C][nt][H][CC] (sum_l x conj H_l).
+void asm_cols_pass(AsmWork& w, bool backward, const float2* in, float2* out, int tile0, int ntiles_local,
+                   cudaStream_t st);
+
+// Block copy for the all-to-all layouts: chunk (a, b, t), a < A (peer),
+// b < B (plane), t < T (tile), copies len[a] float2 from
+// src[sA[a] + b sB[a] + t sT[a]] to dst[dA[a] + b dB[a] + t dT[a]].
+constexpr int kMaxPeers = 16;
+struct ChunkMap {
+    int A = 0, B = 0, T = 0;
+    int64_t len[kMaxPeers], sA[kMaxPeers], sB[kMaxPeers], sT[kMaxPeers], dA[kMaxPeers], dB[kMaxPeers],
+        dT[kMaxPeers];
+};
+void chunk_copy(const float2* src, float2* dst, const ChunkMap& m, cudaStream_t st);
 
 // Static (compile-time planned) propagation path; false when (Px, Py) has no plan.
 bool static_plan_cc(int Px, int Py, int pad, int L, int* cc);
 bool static_forward(AsmWork& w, const float2* d_in, float2* d_out, cudaStream_t st, cudaEvent_t* ev);
 bool static_backward(AsmWork& w, const float2* d_grads, float2* d_out, cudaStream_t st, cudaEvent_t* ev);
 void static_prepare(AsmWork& w);
+bool static_rows_pass(AsmWork& w, bool inverse, const float2* in, float2* out, int planes, int h, cudaStream_t st);
+bool static_cols_pass(AsmWork& w, bool backward, const float2* in, float2* out, int tile0, int ntiles_local,
+                      cudaStream_t st);
 
 }  // namespace hs

@@ -118,7 +118,7 @@ __device__ __forceinline__ void col_single(const ColArgs& a, const float2* __res
     const float2* src = a.in + (static_cast<size_t>(plane_in) * a.ntiles + tile) * tile_elems - shift;
     float2* dst = a.out + (static_cast<size_t>(plane_out) * a.ntiles + tile) * tile_elems - shift;
     const TfConst t = a.tf[c];
-    const int mx = wrapped(tile * CC + tid % CC, a.Px);
+    const int mx = wrapped((a.tile0 + tile) * CC + tid % CC, a.Px);
     sfft::run<N, CC, NT, -1, sfft::Half, sfft::Full>(
         smem, tw, tid, RAD{}, sfft::in_fn([&](int i, int cc) { return src[i * CC + cc]; }),
         sfft::out_smem(smem, [&](int i, int, float2 v, float2& slot) {
@@ -187,8 +187,8 @@ __device__ __forceinline__ void pcol_single(const ColArgs& a, const float2* __re
     const TfConst t = a.tf[c];
     const int pp = tid % NP;
     PairTf ptf;
-    ptf.mx0 = wrapped(tile * CC + 2 * pp, a.Px);
-    ptf.mx1 = wrapped(tile * CC + 2 * pp + 1, a.Px);
+    ptf.mx0 = wrapped((a.tile0 + tile) * CC + 2 * pp, a.Px);
+    ptf.mx1 = wrapped((a.tile0 + tile) * CC + 2 * pp + 1, a.Px);
     {
         const float f0 = static_cast<float>(ptf.mx0), f1 = static_cast<float>(ptf.mx1);
         ptf.qx = make_float2(t.bx * f0 * f0, t.bx * f1 * f1);
@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(NT, MINB) scols_fwdL_kernel(ColArgs a, const f
     const size_t tile_elems = static_cast<size_t>(a.H) * CC;
     const size_t shift = static_cast<size_t>(a.oy) * CC;
     const float2* src = a.in + (static_cast<size_t>(c) * a.ntiles + tile) * tile_elems - shift;
-    const int mx = wrapped(tile * CC + tid % CC, a.Px);
+    const int mx = wrapped((a.tile0 + tile) * CC + tid % CC, a.Px);
     sfft::run<N, CC, NT, -1, sfft::Half, sfft::Full>(
         Sp, tw, tid, RAD{}, sfft::in_fn([&](int i, int cc) { return src[i * CC + cc]; }), sfft::out_smem(Sp));
 #pragma unroll 1
@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(NT, MINB) scols_bwdL_kernel(ColArgs a, const f
     const int tile = blockIdx.x, c = blockIdx.y, tid = threadIdx.x;
     const size_t tile_elems = static_cast<size_t>(a.H) * CC;
     const size_t shift = static_cast<size_t>(a.oy) * CC;
-    const int mx = wrapped(tile * CC + tid % CC, a.Px);
+    const int mx = wrapped((a.tile0 + tile) * CC + tid % CC, a.Px);
 #pragma unroll 1
     for (int l = 0; l < a.L; ++l) {
         const TfConst t = a.tf[l * a.C + c];
@@ -473,6 +473,31 @@ bool static_backward(AsmWork& w, const float2* d_grads, float2* d_out, cudaStrea
     p->row.inv<<<(rows2 + p->row.rb - 1) / p->row.rb, p->row.nt, rs, st>>>(ri, rows2, w.stw_x);
     launch_check("srows_inv");
     if (ev) HS_CUDA(cudaEventRecord(ev[2], st));
+    return true;
+}
+
+bool static_rows_pass(AsmWork& w, bool inverse, const float2* in, float2* out, int planes, int h, cudaStream_t st) {
+    const Plans* p = find(w.Px, w.Py);
+    if (!p || p->cc != w.CC) return false;
+    const size_t rs = rows_smem(*p);
+    const int rows = planes * h;
+    const float scale = inverse ? static_cast<float>(1.0 / (static_cast<double>(w.Px) * w.Py)) : 1.f;
+    RowArgs r{in, out, w.W, h, w.Px, w.ox, w.ntiles, scale, w.plan_x, nullptr};
+    (inverse ? p->row.inv : p->row.fwd)<<<(rows + p->row.rb - 1) / p->row.rb, p->row.nt, rs, st>>>(r, rows, w.stw_x);
+    launch_check(inverse ? "srows_inv" : "srows_fwd");
+    return true;
+}
+
+bool static_cols_pass(AsmWork& w, bool backward, const float2* in, float2* out, int tile0, int ntiles_local,
+                      cudaStream_t st) {
+    const Plans* p = find(w.Px, w.Py);
+    if (!p || p->cc != w.CC) return false;
+    const size_t cs = cols_smem(*p, w.L);
+    ColArgs c{in, out, w.C, w.H, w.Py, w.Px, w.oy, ntiles_local, w.L, w.plan_y, nullptr, w.tf.as<TfConst>()};
+    c.tile0 = tile0;
+    auto k = backward ? (w.L > 1 ? p->col.bwdL : p->col.bwd) : (w.L > 1 ? p->col.fwdL : p->col.fwd);
+    k<<<dim3(ntiles_local, w.C), cols_threads(*p, w.L), cs, st>>>(c, w.stw_y);
+    launch_check(backward ? "scols_bwd" : "scols_fwd");
     return true;
 }
 

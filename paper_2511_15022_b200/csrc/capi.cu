@@ -95,6 +95,15 @@ struct hs_trainer {
     cudaGraphExec_t host_graph = nullptr;
     const float* host_in = nullptr;
     float* host_out = nullptr;
+    // row-slab sharding (hs_trainer_set_row_slab): rank `rank` of R owns canvas
+    // rows [h0, h0 + hr) and column tiles [rank ts, rank ts + ts); its loss band
+    // is rows [g0, g0 + He) (own rows + up to 10 halo rows each side)
+    int R = 0, rank = 0, hr = 0, ts = 0, h0 = 0, g0 = 0, He = 0, top = 0;
+    std::vector<int> He_of, g0_of;
+    DevBuf s_planes, s_dplanes, s_target, s_tstats, s_masks, s_T, s_send, s_recv;
+    ChunkMap m_pack[4], m_unpack[4];
+    int64_t s_counts[4][2 * kMaxPeers] = {};
+    int s_loss_slots = 0;
     ~hs_trainer() {
         if (graph) cudaGraphExecDestroy(graph);
         if (host_graph) cudaGraphExecDestroy(host_graph);
@@ -837,3 +846,192 @@ hs_status hs_trainer_stage_ms(hs_trainer* t, double* out12) {
 }
 
 }  // extern "C"
+
+// ---- row-slab sharding (cfg4: distributed 2D FFT with all-to-all transposes) ----------------
+// Layouts (float2 units, CC = column tile width, nt = tiles, ts = nt / R):
+//   T1r [C][nt][hr][CC]   row side: this rank's rows of every tile
+//   T1c [C][ts][H][CC]    column side: all rows of this rank's tiles
+//   exchange buffers are peer-major: [peer][planes][ts][rows][CC]
+// Exchange 0: T1r -> T1c (forward rows -> columns), 1: T2c -> T2r with the
+// loss-band rows (columns -> rows), 2: T3r own rows -> T3c (backward rows ->
+// columns), 3: T4c -> T4r (columns -> rows).
+static void slab_build_maps(hs_trainer* t) {
+    const int R = t->R, C = t->c, LC = t->L * t->c, H = t->h, hr = t->hr, ts = t->ts, He = t->He;
+    const int64_t CC = t->aw.CC, nt = t->aw.ntiles;
+    auto fill = [&](ChunkMap& m, int B, auto f) {
+        m.A = R;
+        m.B = B;
+        m.T = ts;
+        for (int a = 0; a < R; ++a) f(a, m);
+    };
+    // 0 pack T1r -> send [s][C][ts][hr][CC]
+    fill(t->m_pack[0], C, [&](int a, ChunkMap& m) {
+        m.len[a] = hr * CC; m.sA[a] = a * ts * hr * CC; m.sB[a] = nt * hr * CC; m.sT[a] = hr * CC;
+        m.dA[a] = int64_t(a) * C * ts * hr * CC; m.dB[a] = ts * hr * CC; m.dT[a] = hr * CC;
+    });
+    // 0 unpack recv [r][C][ts][hr][CC] -> T1c
+    auto unpack_cols = [&](int B) {
+        return [=](int a, ChunkMap& m) {
+            m.len[a] = hr * CC; m.sA[a] = int64_t(a) * B * ts * hr * CC; m.sB[a] = ts * hr * CC; m.sT[a] = hr * CC;
+            m.dA[a] = a * hr * CC; m.dB[a] = int64_t(ts) * H * CC; m.dT[a] = H * CC;
+        };
+    };
+    fill(t->m_unpack[0], C, unpack_cols(C));
+    // 1 pack T2c [LC][ts][H][CC] -> send [d][LC][ts][He_d][CC] (loss-band rows of d)
+    int64_t off = 0;
+    fill(t->m_pack[1], LC, [&](int a, ChunkMap& m) {
+        const int64_t he = t->He_of[a];
+        m.len[a] = he * CC; m.sA[a] = t->g0_of[a] * CC; m.sB[a] = int64_t(ts) * H * CC; m.sT[a] = H * CC;
+        m.dA[a] = off; m.dB[a] = ts * he * CC; m.dT[a] = he * CC;
+        off += LC * ts * he * CC;
+    });
+    // 1 unpack recv [s][LC][ts][He][CC] -> T2r [LC][nt][He][CC]
+    fill(t->m_unpack[1], LC, [&](int a, ChunkMap& m) {
+        m.len[a] = He * CC; m.sA[a] = int64_t(a) * LC * ts * He * CC; m.sB[a] = int64_t(ts) * He * CC;
+        m.sT[a] = He * CC; m.dA[a] = int64_t(a) * ts * He * CC; m.dB[a] = nt * He * CC; m.dT[a] = He * CC;
+    });
+    // 2 pack T3r own rows -> send [s][LC][ts][hr][CC]
+    fill(t->m_pack[2], LC, [&](int a, ChunkMap& m) {
+        m.len[a] = hr * CC; m.sA[a] = int64_t(a) * ts * He * CC + t->top * CC; m.sB[a] = nt * He * CC;
+        m.sT[a] = He * CC; m.dA[a] = int64_t(a) * LC * ts * hr * CC; m.dB[a] = ts * hr * CC; m.dT[a] = hr * CC;
+    });
+    fill(t->m_unpack[2], LC, unpack_cols(LC));
+    // 3 pack T4c [C][ts][H][CC] -> send [d][C][ts][hr][CC]
+    fill(t->m_pack[3], C, [&](int a, ChunkMap& m) {
+        m.len[a] = hr * CC; m.sA[a] = a * hr * CC; m.sB[a] = int64_t(ts) * H * CC; m.sT[a] = H * CC;
+        m.dA[a] = int64_t(a) * C * ts * hr * CC; m.dB[a] = ts * hr * CC; m.dT[a] = hr * CC;
+    });
+    // 3 unpack recv [s][C][ts][hr][CC] -> T4r [C][nt][hr][CC]
+    fill(t->m_unpack[3], C, [&](int a, ChunkMap& m) {
+        m.len[a] = hr * CC; m.sA[a] = int64_t(a) * C * ts * hr * CC; m.sB[a] = ts * hr * CC; m.sT[a] = hr * CC;
+        m.dA[a] = int64_t(a) * ts * hr * CC; m.dB[a] = nt * hr * CC; m.dT[a] = hr * CC;
+    });
+    // element counts (floats) per peer: send, recv
+    for (int a = 0; a < R; ++a) {
+        const int64_t f = 2 * CC * ts;
+        t->s_counts[0][a] = t->s_counts[0][R + a] = f * C * hr;
+        t->s_counts[1][a] = f * LC * t->He_of[a];
+        t->s_counts[1][R + a] = f * LC * He;
+        t->s_counts[2][a] = t->s_counts[2][R + a] = f * LC * hr;
+        t->s_counts[3][a] = t->s_counts[3][R + a] = f * C * hr;
+    }
+}
+
+extern "C" hs_status hs_trainer_set_row_slab(hs_trainer* t, int rank, int ranks) {
+    return guard([&] {
+        require(ranks >= 1 && ranks <= kMaxPeers && rank >= 0 && rank < ranks, "row slab: bad rank / rank count");
+        require(t->L == t->L_total && t->C_total == t->c, "row slab: not combinable with plane or channel shards");
+        require(t->h % ranks == 0, "row slab: canvas height must divide into equal slabs");
+        AsmWork& aw = t->aw;
+        require(static_cast<int64_t>(aw.ntiles) * aw.CC == aw.Px && aw.ntiles % ranks == 0,
+                "row slab: padded width must divide into equal column-tile slabs");
+        t->R = ranks;
+        t->rank = rank;
+        t->hr = t->h / ranks;
+        t->ts = aw.ntiles / ranks;
+        t->He_of.assign(ranks, 0);
+        t->g0_of.assign(ranks, 0);
+        for (int r = 0; r < ranks; ++r) {
+            const int a = std::max(0, r * t->hr - 10), b = std::min(t->h, (r + 1) * t->hr + 10);
+            t->g0_of[r] = a;
+            t->He_of[r] = b - a;
+        }
+        t->h0 = rank * t->hr;
+        t->g0 = t->g0_of[rank];
+        t->He = t->He_of[rank];
+        t->top = t->h0 - t->g0;
+        require(t->He >= 11, "ssim: image smaller than the 11x11 window");
+        const int C = t->c, LC = t->L * t->c, W = t->w, Hm = t->hr + 20;
+        const size_t band = static_cast<size_t>(t->He) * W;
+        cudaStream_t st = t->ctx->stream;
+        t->s_planes.reserve(sizeof(float2) * LC * band);
+        t->s_dplanes.reserve(sizeof(float2) * LC * band);
+        t->s_target.reserve(sizeof(float) * C * band);
+        t->s_masks.reserve(static_cast<size_t>(t->L) * band);
+        t->s_tstats.reserve(sizeof(float2) * ssim_target_stats_elems(C, t->He, W));
+        const size_t tiled = static_cast<size_t>(aw.ntiles) * Hm * aw.CC;
+        t->s_T.reserve(sizeof(float2) * LC * tiled);
+        t->s_send.reserve(sizeof(float2) * LC * tiled);
+        t->s_recv.reserve(sizeof(float2) * LC * tiled);
+        // loss-band slices of the target and the masks, and the band's target window stats
+        HS_CUDA(cudaMemcpy2DAsync(t->s_target.p, band * sizeof(float), t->target.as<float>() + static_cast<size_t>(t->g0) * W,
+                                  static_cast<size_t>(t->h) * W * sizeof(float), band * sizeof(float), C,
+                                  cudaMemcpyDeviceToDevice, st));
+        HS_CUDA(cudaMemcpy2DAsync(t->s_masks.p, band, t->masks.as<uint8_t>() + static_cast<size_t>(t->g0) * W,
+                                  static_cast<size_t>(t->h) * W, band, t->L, cudaMemcpyDeviceToDevice, st));
+        ssim_target_stats(t->s_target.as<float>(), C, t->He, W, t->s_tstats.as<float2>(), st);
+        t->s_loss_slots = loss_partial_slots(kLossTraining, t->L, C, t->He, W);
+        if (t->s_loss_slots > t->loss_slots) t->partials.reserve(sizeof(double) * 2 * t->s_loss_slots);
+        slab_build_maps(t);
+        HS_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+extern "C" hs_status hs_trainer_slab_counts(hs_trainer* t, int exchange, int64_t* out) {
+    return guard([&] {
+        require(t->R >= 1, "row slab: trainer is not row-slab sharded");
+        require(exchange >= 0 && exchange < 4, "row slab: exchange index outside 0..3");
+        for (int i = 0; i < 2 * t->R; ++i) out[i] = t->s_counts[exchange][i];
+    });
+}
+
+extern "C" float* hs_trainer_slab_send_ptr(hs_trainer* t) { return t->s_send.as<float>(); }
+extern "C" float* hs_trainer_slab_recv_ptr(hs_trainer* t) { return t->s_recv.as<float>(); }
+
+// Stage k (0..4) of a row-slab step; between stage k and k+1 the caller runs
+// all-to-all exchange k (send buffer -> peers' receive buffers, counts from
+// hs_trainer_slab_counts).  After stage 4 the gradient buffer holds this
+// rank's partial gradient (sum over its rows): all-reduce it, then
+// hs_trainer_apply_update.  Loss partial sums: hs_trainer_loss_partials.
+extern "C" hs_status hs_trainer_slab_stage(hs_trainer* t, int stage) {
+    return guard([&] {
+        require(t->R >= 1, "row slab: trainer is not row-slab sharded");
+        require(t->host_step <= t->total_steps, "cosine_lr: step outside [0, total_steps]");
+        cudaStream_t st = t->ctx->stream;
+        AsmWork& aw = t->aw;
+        const int C = t->c, LC = t->L * t->c;
+        float2* send = t->s_send.as<float2>();
+        const float2* recv = t->s_recv.as<float2>();
+        switch (stage) {
+            case 0:  // binning (replicated), raster forward of the own rows, row FFTs, pack
+                HS_CUDA(cudaMemsetAsync(t->flags.p, 0, sizeof(uint32_t), st));
+                t->rw.project_and_bin(t->params.as<float>(), st);
+                raster_forward(t->rw, t->field.as<float2>(), st, t->h0, t->hr);
+                asm_rows_pass(aw, false, t->field.as<float2>(), aw.T1.as<float2>(), C, t->hr, st);
+                chunk_copy(aw.T1.as<float2>(), send, t->m_pack[0], st);
+                break;
+            case 1:  // column FFT x H_l + column IFFT on the own tiles, pack loss bands
+                chunk_copy(recv, aw.T1.as<float2>(), t->m_unpack[0], st);
+                asm_cols_pass(aw, false, aw.T1.as<float2>(), aw.T2.as<float2>(), t->rank * t->ts, t->ts, st);
+                chunk_copy(aw.T2.as<float2>(), send, t->m_pack[1], st);
+                break;
+            case 2: {  // row IFFTs of the loss band, loss + dU, backward row FFTs, pack own rows
+                chunk_copy(recv, t->s_T.as<float2>(), t->m_unpack[1], st);
+                asm_rows_pass(aw, true, t->s_T.as<float2>(), t->s_planes.as<float2>(), LC, t->He, st);
+                LossArgs a{kLossTraining, t->L, t->L_total, 0, C, t->He, t->w, nullptr, t->s_planes.as<float2>(),
+                           t->s_target.as<float>(), t->s_tstats.as<float2>(), t->s_masks.as<uint8_t>(), nullptr,
+                           t->s_dplanes.as<float2>(), t->partials.as<double>(), t->C_total};
+                a.H_norm = t->h;
+                a.own0 = t->top;
+                a.own1 = t->top + t->hr;
+                const int used = loss_launch(a, st);
+                loss_finalize(a, used, t->out3.as<double>(), st);
+                asm_rows_pass(aw, false, t->s_dplanes.as<float2>(), t->s_T.as<float2>(), LC, t->He, st);
+                chunk_copy(t->s_T.as<float2>(), send, t->m_pack[2], st);
+                break;
+            }
+            case 3:  // adjoint column pass on the own tiles, pack
+                chunk_copy(recv, aw.T2.as<float2>(), t->m_unpack[2], st);
+                asm_cols_pass(aw, true, aw.T2.as<float2>(), aw.T1.as<float2>(), t->rank * t->ts, t->ts, st);
+                chunk_copy(aw.T1.as<float2>(), send, t->m_pack[3], st);
+                break;
+            case 4:  // row IFFTs of the own rows, raster backward over the own rows
+                chunk_copy(recv, aw.T2.as<float2>(), t->m_unpack[3], st);
+                asm_rows_pass(aw, true, aw.T2.as<float2>(), t->back.as<float2>(), C, t->hr, st);
+                raster_backward(t->rw, t->params.as<float>(), t->back.as<float2>(), t->grads.as<float>(),
+                                t->flags.as<uint32_t>(), st, t->h0, t->hr);
+                break;
+            default: throw Error(HS_EINVAL, "row slab: stage outside 0..4");
+        }
+    });
+}

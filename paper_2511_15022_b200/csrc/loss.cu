@@ -187,7 +187,7 @@ struct SsimSmem {
     float4 gm[2][kSW];          // (g1, g2, g3, -) of the valid row being spread
 };
 
-template <bool FROM_FIELD, int SR>
+template <bool FROM_FIELD, int SR, bool BAND = false>
 struct SsimCta {
     using Raw = typename std::conditional<FROM_FIELD, float2, float>::type;
     const LossArgs& a;
@@ -292,7 +292,9 @@ struct SsimCta {
             const float rb1 = __fdividef(1.f, b1), rb2 = __fdividef(1.f, b2);
             const float inv = rb1 * rb2;
             const float sv = a1 * a2 * inv;
-            if (t >= kHalo && v >= y0 && v < y0 + SR) st.sum += static_cast<double>(sv);
+            if (t >= kHalo && v >= y0 && v < y0 + SR &&
+                (!BAND || static_cast<unsigned>(v - a.own0) < static_cast<unsigned>(a.own1 - a.own0)))
+                st.sum += static_cast<double>(sv);
             gv.x = 2.f * (a2 * inv * m2 - sv * rb1 * m1 + sv * rb2 * m1 - a1 * inv * m2);
             gv.y = -sv * rb2;
             gv.z = 2.f * a1 * inv;
@@ -340,7 +342,7 @@ struct SsimCta {
             if (kind == kLossTraining) {  // loss_recon_grad, loss.cpp:317-341
                 const float d = iv - tv;
                 const float k = 1.f + mk + tv * tv;
-                st.sum += static_cast<double>(d * d * k);
+                if (!BAND || static_cast<unsigned>(y - a.own0) < static_cast<unsigned>(a.own1 - a.own0)) st.sum += static_cast<double>(d * d * k);
                 g = fmaf(wr * d, k, g);
             }
             const size_t p = plane_off + static_cast<size_t>(y) * W + x;
@@ -355,15 +357,16 @@ struct SsimCta {
 // Producer/consumer warp groups: threads [0, 128) produce SSIM rows, threads
 // [128, 256) consume them one step behind, so the two halves of a row step run
 // concurrently and each thread carries a single 11-row register ring.
-template <bool FROM_FIELD, int MINB, int SR>
+// BAND: row-slab shard, loss sums restricted to rows [own0, own1) (LossArgs)
+template <bool FROM_FIELD, int MINB, int SR, bool BAND = false>
 __global__ void __launch_bounds__(2 * kSW, MINB) ssim_loss_kernel(LossArgs a, Win win) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    using Raw = typename SsimCta<FROM_FIELD, SR>::Raw;
+    using Raw = typename SsimCta<FROM_FIELD, SR, BAND>::Raw;
     SsimSmem<Raw>& S = *reinterpret_cast<SsimSmem<Raw>*>(smem_raw);
     const int plane = blockIdx.z;  // l * C + c
     const int l = plane / a.C, ch = plane - l * a.C;
     const bool producer = threadIdx.x < kSW;
-    SsimCta<FROM_FIELD, SR> K{a, win, S};
+    SsimCta<FROM_FIELD, SR, BAND> K{a, win, S};
     K.t = producer ? threadIdx.x : threadIdx.x - kSW;
     K.x0 = blockIdx.x * kSO;
     K.y0 = blockIdx.y * SR;
@@ -377,9 +380,9 @@ __global__ void __launch_bounds__(2 * kSW, MINB) ssim_loss_kernel(LossArgs a, Wi
     K.tgt = a.target + static_cast<size_t>(ch) * a.H * a.W;
     K.tst = a.tstats + static_cast<size_t>(ch) * K.vh * K.vw;
     K.mask = a.masks + static_cast<size_t>(a.plane0 + l) * a.H * a.W;
-    const double n_el = static_cast<double>(a.channels_norm()) * a.H * a.W;
+    const double n_el = static_cast<double>(a.channels_norm()) * a.rows_norm() * a.W;
     K.wr = static_cast<float>(2.0 / (n_el * a.L_norm));
-    const double count = static_cast<double>(a.L_norm) * a.channels_norm() * K.vh * K.vw;
+    const double count = static_cast<double>(a.L_norm) * a.channels_norm() * (a.rows_norm() - kWin + 1) * K.vw;
     K.ws = static_cast<float>((a.kind == kLossTraining ? kSsimWeight : 1.0) * (-1.0 / count));
     K.init_sources();
 
@@ -672,7 +675,11 @@ int loss_launch(const LossArgs& a, cudaStream_t st) {
             kern<<<grid, 2 * kSW, smem, st>>>(a, win);
         };
         const bool v1 = ssim_variant() == 1;
-        if (a.field) {
+        const bool band = a.own0 > 0 || a.own1 < a.H;
+        if (band) {
+            require(a.field != nullptr, "ssim: row-band loss needs the complex field");
+            go(ssim_loss_kernel<true, 3, kSRv0, true>, sizeof(SsimSmem<float2>));
+        } else if (a.field) {
             if (v1) go(ssim_loss_kernel<true, 4, kSRv1>, sizeof(SsimSmem<float2>));
             else go(ssim_loss_kernel<true, 3, kSRv0>, sizeof(SsimSmem<float2>));
         } else {
@@ -691,8 +698,8 @@ int loss_launch(const LossArgs& a, cudaStream_t st) {
 }
 
 void loss_finalize(const LossArgs& a, int slots, double* d_out3, cudaStream_t st) {
-    const double n_el = static_cast<double>(a.channels_norm()) * a.H * a.W;
-    const double count = static_cast<double>(a.L_norm) * a.channels_norm() * std::max(a.H - kWin + 1, 0) *
+    const double n_el = static_cast<double>(a.channels_norm()) * a.rows_norm() * a.W;
+    const double count = static_cast<double>(a.L_norm) * a.channels_norm() * std::max(a.rows_norm() - kWin + 1, 0) *
                          std::max(a.W - kWin + 1, 0);
     loss_finalize_kernel<<<1, 1024, 0, st>>>(a.partials, slots, a.kind, n_el, a.L_norm, count, d_out3);
     launch_check("loss_finalize");

@@ -22,7 +22,14 @@ struct LossArgs {
     float2* du;              // dL/dU = 2 U dL/dI (L x C x H x W), or nullptr
     double* partials;        // 2 per CTA: recon-or-mse sum, ssim sum
     int C_norm = 0;          // global channel count for the normalisers (channel sharding); 0 = C
+    // Row-slab sharding: this call sees a band of H rows of an image of H_norm
+    // rows (the normalisers use H_norm); the loss sums count only rows
+    // [own0, own1) of the band (SSIM: windows whose top row is there), the
+    // gradient is produced for every row of the band.  0 / full = unsharded.
+    int H_norm = 0;
+    int own0 = 0, own1 = 1 << 30;
     __host__ __device__ int channels_norm() const { return C_norm > 0 ? C_norm : C; }
+    __host__ __device__ int rows_norm() const { return H_norm > 0 ? H_norm : H; }
 };
 
 // Launches the loss kernel(s); returns the number of partial slots written.

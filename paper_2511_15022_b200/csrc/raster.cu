@@ -447,11 +447,14 @@ template <int C>
 __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(
     const uint32_t* __restrict__ ids, const uint2* __restrict__ ranges,
     const float4* __restrict__ rec, const float4* __restrict__ shade,
-    const double* __restrict__ p64, int N, int tiles_x, int W, int H, float2* __restrict__ field) {
+    const double* __restrict__ p64, int N, int tiles_x, int W, int H, float2* __restrict__ field, int y0,
+    int hs, int ty0) {
     // one contiguous record per staged Gaussian: a hit reads it through one
     // base address with immediate offsets (lanes broadcast the same record)
     __shared__ FwdRec<C> s_g[kFwdBatch];
-    const int tile = blockIdx.x;
+    // row band [y0, y0 + hs) of the canvas (the whole canvas unless row-slab
+    // sharded); the grid covers its tile rows from ty0, the field holds its rows
+    const int tile = blockIdx.x + ty0 * tiles_x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int cx0 = tx * kTile + (warp & 1) * 8;
@@ -523,11 +526,13 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(
             }
         }
     }
+    (void)H;
     if (x < W) {
+        const int ya = y - y0, yb = y + 4 - y0;
 #pragma unroll
         for (int c = 0; c < C; ++c) {
-            if (y < H) field[(static_cast<size_t>(c) * H + y) * W + x] = accA[c];
-            if (y + 4 < H) field[(static_cast<size_t>(c) * H + y + 4) * W + x] = accB[c];
+            if (ya >= 0 && ya < hs) field[(static_cast<size_t>(c) * hs + ya) * W + x] = accA[c];
+            if (yb >= 0 && yb < hs) field[(static_cast<size_t>(c) * hs + yb) * W + x] = accB[c];
         }
     }
 }
@@ -551,7 +556,7 @@ template <int C, int MINB, int NCH>
 __global__ void __launch_bounds__(kBwdThreads, MINB) raster_bwd_kernel(
     int N, const float4* __restrict__ rec, const float4* __restrict__ shade,
     const double* __restrict__ p64, const int4* __restrict__ pbox, int W, int H,
-    const float2* __restrict__ gfield, float* __restrict__ raw) {
+    const float2* __restrict__ gfield, float* __restrict__ raw, int y0, int hs) {
     __shared__ int2 s_rows[kBwdWarps][32];  // compact nonempty rows: (y, x - flat index)
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int g = blockIdx.x * kBwdWarps + wid;
@@ -575,9 +580,13 @@ __global__ void __launch_bounds__(kBwdThreads, MINB) raster_bwd_kernel(
     const float alpha = exp2f(r2.x), tol = r2.y, detI = r2.z, inv_i00 = r2.w;  // r2.x = log2 alpha
     const float M = cut + tol;
     const float ratio = i01 * inv_i00;
-    const float2* gch[C];  // channel planes of the gradient field
+    // channel planes of the gradient field: rows [y0, y0 + hs) of the canvas
+    // (the whole canvas unless row-slab sharded), indexed by canvas row
+    (void)H;
+    const float2* gch[C];
 #pragma unroll
-    for (int c = 0; c < C; ++c) gch[c] = gfield + static_cast<size_t>(c) * H * W;
+    for (int c = 0; c < C; ++c) gch[c] = gfield + static_cast<size_t>(c) * hs * W - static_cast<ptrdiff_t>(y0) * W;
+    const int o_idle = y0 * W;  // a valid pixel for idle lanes
 
     float2 dap[C];  // (d_amp, d_phase) per channel
 #pragma unroll
@@ -586,8 +595,8 @@ __global__ void __launch_bounds__(kBwdThreads, MINB) raster_bwd_kernel(
     float d_alpha = 0.f, gb = 0.f;
 
     const float ext = sqrtf(fmaxf(i00 * M / detI, 0.f)) + 1e-2f;
-    const int ya = max(bb.z, static_cast<int>(ceilf(py - ext)));
-    const int yb = min(bb.w, static_cast<int>(floorf(py + ext)));
+    const int ya = max(max(bb.z, y0), static_cast<int>(ceilf(py - ext)));
+    const int yb = min(min(bb.w, y0 + hs - 1), static_cast<int>(floorf(py + ext)));
     const double* q = p64 + g;
     const unsigned lanemask_le = 0xffffffffu >> (31 - lane);
 
@@ -636,11 +645,11 @@ __global__ void __launch_bounds__(kBwdThreads, MINB) raster_bwd_kernel(
                 oy[u] = info.x;
                 ox[u] = f + info.y;
             }
-            // inactive lanes load pixel 0 (always valid) and skip the math
+            // inactive lanes load the band's first pixel (always valid) and skip the math
             float2 gv[NCH][C];
 #pragma unroll
             for (int u = 0; u < NCH; ++u) {
-                const int o = act[u] ? oy[u] * W + ox[u] : 0;
+                const int o = act[u] ? oy[u] * W + ox[u] : o_idle;
 #pragma unroll
                 for (int c = 0; c < C; ++c) gv[u][c] = gch[c][o];
             }
@@ -869,19 +878,22 @@ void export_tile_index(const RasterWork& rw, int64_t k, uint32_t* d_tiles, uint3
 }
 
 template <int C>
-static void fwd_launch(const RasterWork& rw, float2* d_field, cudaStream_t st) {
-    raster_fwd_kernel<C><<<rw.tiles_x * rw.tiles_y, kFwdThreads, 0, st>>>(
+static void fwd_launch(const RasterWork& rw, float2* d_field, int y0, int hs, cudaStream_t st) {
+    const int ty0 = y0 / kTile, ty1 = (y0 + hs - 1) / kTile;
+    raster_fwd_kernel<C><<<rw.tiles_x * (ty1 - ty0 + 1), kFwdThreads, 0, st>>>(
         rw.ids.as<uint32_t>(), rw.ranges.as<uint2>(), rw.rec.as<float4>(), rw.shade.as<float4>(),
-        rw.p64.as<double>(), rw.n, rw.tiles_x, rw.width, rw.height, d_field);
+        rw.p64.as<double>(), rw.n, rw.tiles_x, rw.width, rw.height, d_field, y0, hs, ty0);
     launch_check("raster_fwd");
 }
 
-void raster_forward(const RasterWork& rw, float2* d_field, cudaStream_t st) {
+void raster_forward(const RasterWork& rw, float2* d_field, cudaStream_t st, int y0, int hs) {
+    if (hs < 0) hs = rw.height - y0;
+    require(y0 >= 0 && hs >= 1 && y0 + hs <= rw.height, "rasterizer: row band outside the canvas");
     switch (rw.c) {
-        case 1: fwd_launch<1>(rw, d_field, st); break;
-        case 2: fwd_launch<2>(rw, d_field, st); break;
-        case 3: fwd_launch<3>(rw, d_field, st); break;
-        case 4: fwd_launch<4>(rw, d_field, st); break;
+        case 1: fwd_launch<1>(rw, d_field, y0, hs, st); break;
+        case 2: fwd_launch<2>(rw, d_field, y0, hs, st); break;
+        case 3: fwd_launch<3>(rw, d_field, y0, hs, st); break;
+        case 4: fwd_launch<4>(rw, d_field, y0, hs, st); break;
         default: throw Error(HS_EINVAL, "rasterizer: unsupported channel count");
     }
 }
@@ -896,12 +908,12 @@ static int bwd_variant() {
 
 template <int C>
 static void bwd_launch(const RasterWork& rw, const float* d_params, const float2* d_gf,
-                       float* d_grads, uint32_t* d_flags, cudaStream_t st) {
+                       float* d_grads, uint32_t* d_flags, int y0, int hs, cudaStream_t st) {
     const int warps_per_block = kBwdThreads / 32;
     auto go = [&](auto kern) {
         kern<<<ceil_div(rw.n, warps_per_block), kBwdThreads, 0, st>>>(
             rw.n, rw.rec.as<float4>(), rw.shade.as<float4>(), rw.p64.as<double>(), rw.pbox.as<int4>(),
-            rw.width, rw.height, d_gf, rw.raw.as<float>());
+            rw.width, rw.height, d_gf, rw.raw.as<float>(), y0, hs);
     };
     switch (bwd_variant()) {
         case 1: go(raster_bwd_kernel<C, 3, 2>); break;
@@ -914,13 +926,15 @@ static void bwd_launch(const RasterWork& rw, const float* d_params, const float2
 }
 
 void raster_backward(const RasterWork& rw, const float* d_params, const float2* d_grad_field,
-                     float* d_grads, uint32_t* d_flags, cudaStream_t st) {
+                     float* d_grads, uint32_t* d_flags, cudaStream_t st, int y0, int hs) {
     if (rw.n == 0) return;
+    if (hs < 0) hs = rw.height - y0;
+    require(y0 >= 0 && hs >= 1 && y0 + hs <= rw.height, "rasterizer: row band outside the canvas");
     switch (rw.c) {
-        case 1: bwd_launch<1>(rw, d_params, d_grad_field, d_grads, d_flags, st); break;
-        case 2: bwd_launch<2>(rw, d_params, d_grad_field, d_grads, d_flags, st); break;
-        case 3: bwd_launch<3>(rw, d_params, d_grad_field, d_grads, d_flags, st); break;
-        case 4: bwd_launch<4>(rw, d_params, d_grad_field, d_grads, d_flags, st); break;
+        case 1: bwd_launch<1>(rw, d_params, d_grad_field, d_grads, d_flags, y0, hs, st); break;
+        case 2: bwd_launch<2>(rw, d_params, d_grad_field, d_grads, d_flags, y0, hs, st); break;
+        case 3: bwd_launch<3>(rw, d_params, d_grad_field, d_grads, d_flags, y0, hs, st); break;
+        case 4: bwd_launch<4>(rw, d_params, d_grad_field, d_grads, d_flags, y0, hs, st); break;
         default: throw Error(HS_EINVAL, "rasterizer: unsupported channel count");
     }
 }

@@ -34,9 +34,13 @@ struct RasterWork {
     void project_and_bin(const float* d_params, cudaStream_t st, cudaEvent_t shading_ready = nullptr);
 };
 
-void raster_forward(const RasterWork& rw, float2* d_field, cudaStream_t st);
+// Row band [y0, y0 + hs) (hs < 0: to the bottom): the forward writes only
+// those rows (field = C x hs x W), the backward reads only those rows of the
+// gradient field (C x hs x W) and sums each Gaussian over its footprint inside
+// the band -- the partial gradient of a row-slab shard.
+void raster_forward(const RasterWork& rw, float2* d_field, cudaStream_t st, int y0 = 0, int hs = -1);
 void raster_backward(const RasterWork& rw, const float* d_params, const float2* d_grad_field,
-                     float* d_grads, uint32_t* d_flags, cudaStream_t st);
+                     float* d_grads, uint32_t* d_flags, cudaStream_t st, int y0 = 0, int hs = -1);
 // tiles/ids (uint32) + ranges (uint64 pairs) export for build_tile_index.
 void export_tile_index(const RasterWork& rw, int64_t k, uint32_t* d_tiles, uint32_t* d_ids,
                        uint64_t* d_ranges, cudaStream_t st);

@@ -872,6 +872,32 @@ class Trainer:
     def reserve_pairs(self, cap):
         check(_lib.load().hs_trainer_reserve_pairs(self.h, C.c_int64(int(cap))))
 
+    # ---- row-slab sharding (cfg4: distributed 2D FFT, parallel.SlabShardedStep) ----
+    def set_row_slab(self, rank: int, ranks: int):
+        """Make this trainer rank `rank` of `ranks` row slabs (hs_trainer_set_row_slab)."""
+        check(_lib.load().hs_trainer_set_row_slab(self.h, int(rank), int(ranks)))
+        self.slab = (int(rank), int(ranks))
+        counts = [self.slab_counts(e) for e in range(4)]
+        size = max(max(sum(s), sum(r)) for s, r in counts)
+        lib = _lib.load()
+        self._slab_send = _wrap(self, lib.hs_trainer_slab_send_ptr(self.h), size)
+        self._slab_recv = _wrap(self, lib.hs_trainer_slab_recv_ptr(self.h), size)
+
+    def slab_counts(self, exchange: int):
+        """(send counts, recv counts) in floats per peer of all-to-all `exchange` (0..3)."""
+        R = self.slab[1]
+        out = (C.c_int64 * (2 * R))()
+        check(_lib.load().hs_trainer_slab_counts(self.h, int(exchange), out))
+        return list(out[:R]), list(out[R:])
+
+    def slab_buffers(self):
+        """(send, recv) fp32 device views of the exchange buffers."""
+        return self._slab_send, self._slab_recv
+
+    def slab_stage(self, stage: int):
+        ctx_handle()
+        check(_lib.load().hs_trainer_slab_stage(self.h, int(stage)))
+
 
 def _wrap(owner, ptr, count) -> torch.Tensor:
     """torch view over trainer-owned device memory (kept alive by owner)."""

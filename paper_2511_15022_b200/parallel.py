@@ -16,6 +16,15 @@
   global channel count for the loss normalisers, one NCCL all-reduce of the
   geometry gradients (6N floats) completes them, and every rank applies the
   identical geometry update plus the update of its own amplitude/phase.
+* Row-slab sharding (cfg4, 4K): rank r owns H/R canvas rows and 1/R of the
+  padded spectrum's column tiles.  The 2D FFTs become row FFTs on the own rows,
+  an all-to-all transpose (NCCL over NVLink), column FFTs on the own tiles and
+  an all-to-all back -- four transposes per step (forward and adjoint
+  propagation).  The loss runs on the own rows plus 10-row SSIM halos that the
+  second transpose delivers with the rows (computed redundantly, counted once),
+  the rasterizer backward sums each Gaussian over the own rows only, and one
+  all-reduce of the gradient buffer completes the gradient (the backward is
+  linear in the gradient field).  Binning is replicated.
 * Scene replicas (cfg2 at N>1, cfg5): independent problems, no collective.
 
 The collective is torch.distributed over NCCL (gloo on CPU for the tests).
@@ -119,6 +128,101 @@ class ChannelShardedStep:
         if multi:
             dist.all_reduce(parts, op=dist.ReduceOp.SUM, group=self.group)
         return combine_loss(float(parts[0]), float(parts[1]), self.C, self.H, self.W, self.L)
+
+
+def row_slab(H: int, rank: int, world: int) -> Tuple[int, int]:
+    """Rows [begin, end) of the canvas owned by `rank` (equal slabs)."""
+    if world < 1 or not 0 <= rank < world or H % world:
+        raise ValueError("row_slab: the canvas height must divide into equal slabs")
+    hr = H // world
+    return rank * hr, (rank + 1) * hr
+
+
+def loss_band(H: int, rank: int, world: int, halo: int = 10) -> Tuple[int, int]:
+    """Rows [begin, end) of the loss band of `rank`: its slab plus up to `halo`
+    rows each side (the 11x11 SSIM windows that touch the own rows)."""
+    b, e = row_slab(H, rank, world)
+    return max(0, b - halo), min(H, e + halo)
+
+
+class SlabShardedStep:
+    """One optimisation step of a row-slab sharded trainer (cfg4): five
+    stages with an NCCL all-to-all between them (hs_trainer_slab_stage), then
+    the gradient all-reduce and the replicated Adan update.
+
+    `trainer` is a holo.Trainer on which set_row_slab(rank, world) was called.
+    """
+
+    def __init__(self, trainer, C, H, W, L, group=None):
+        self.tr = trainer
+        self.C, self.H, self.W, self.L = C, H, W, L
+        self.group = group
+        self.counts = [trainer.slab_counts(e) for e in range(4)]
+
+    def _exchange(self, e):
+        send, recv = self.tr.slab_buffers()
+        sc, rc = self.counts[e]
+        if dist.is_initialized() and dist.get_world_size(self.group) > 1:
+            dist.all_to_all_single(recv[:sum(rc)], send[:sum(sc)], rc, sc, group=self.group)
+        else:
+            recv[:sum(rc)].copy_(send[:sum(sc)])
+
+    def step(self) -> float:
+        for e in range(4):
+            self.tr.slab_stage(e)
+            self._exchange(e)
+        self.tr.slab_stage(4)
+        g = self.tr.grads_tensor()
+        multi = dist.is_initialized() and dist.get_world_size(self.group) > 1
+        if multi:
+            dist.all_reduce(g, op=dist.ReduceOp.SUM, group=self.group)
+        self.tr.apply_update()
+        parts = torch.tensor(self.tr.loss_partials(), dtype=torch.float64, device=g.device)
+        if multi:
+            dist.all_reduce(parts, op=dist.ReduceOp.SUM, group=self.group)
+        return combine_loss(float(parts[0]), float(parts[1]), self.C, self.H, self.W, self.L)
+
+
+class LocalSlabGroup:
+    """R row-slab trainers on ONE device, stepped in lock-step with the
+    all-to-all and the all-reduce done as device copies: the single-GPU
+    check that the R-rank decomposition reproduces the unsharded step
+    (tests and bench; a real run uses SlabShardedStep, one rank per GPU)."""
+
+    def __init__(self, trainers, C, H, W, L):
+        self.trs = list(trainers)
+        self.C, self.H, self.W, self.L = C, H, W, L
+        self.counts = [[t.slab_counts(e) for e in range(4)] for t in self.trs]
+
+    def _exchange(self, e):
+        R = len(self.trs)
+        for r, tr in enumerate(self.trs):
+            recv = tr.slab_buffers()[1]
+            off = 0
+            for s, ts in enumerate(self.trs):
+                sc = self.counts[s][e][0]
+                so = sum(sc[:r])
+                recv[off:off + sc[r]].copy_(ts.slab_buffers()[0][so:so + sc[r]])
+                off += sc[r]
+            assert off == sum(self.counts[r][e][1]) and len(sc) == R
+
+    def step(self) -> float:
+        for e in range(4):
+            for t in self.trs:
+                t.slab_stage(e)
+            self._exchange(e)
+        for t in self.trs:
+            t.slab_stage(4)
+        grads = [t.grads_tensor() for t in self.trs]
+        total = grads[0].clone()
+        for g in grads[1:]:
+            total += g
+        for g in grads:
+            g.copy_(total)
+        for t in self.trs:
+            t.apply_update()
+        parts = [t.loss_partials() for t in self.trs]
+        return combine_loss(sum(p[0] for p in parts), sum(p[1] for p in parts), self.C, self.H, self.W, self.L)
 
 
 def amdahl_plane_speedup(L: int, world: int) -> float:

@@ -1,0 +1,111 @@
+"""Row-slab sharding (distributed 2D FFT with all-to-all
+transposes) on the B200: R slab trainers on one device, exchanged by device
+copies in the all-to-all layout (parallel.LocalSlabGroup), against the
+unsharded trainer on the same scene.  The decomposition changes only the fp32
+summation order of the per-Gaussian sums (rows split over ranks) and of the
+loss partials, so gradients, losses and updated parameters agree far inside
+the parity bars (field 1e-4, gradients 1e-3); the 2D FFTs of every rank are
+the unsharded FFTs' own row and column passes.
+"""
+import numpy as np
+import pytest
+
+from paper_2511_15022_b200 import synthetic as S
+
+pytestmark = pytest.mark.gpu
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, dtype=np.float64).ravel()
+    b = np.asarray(b, dtype=np.float64).ravel()
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def scene(holo, n, c, w, h, L, seed=42):
+    g = {k: np.asarray(v, dtype=np.float32).astype(np.float64) for k, v in S.init_gaussians(n, c, w, h, seed).items()}
+    gs = holo.GaussianSet(n, c, **g)
+    target = holo.RealField(c, h, w, S.synthetic_image(seed, c, h, w).astype(np.float32).astype(np.float64))
+    masks = S.build_masks(S.synthetic_depth(seed + 1, h, w), L, True)
+    dist = S.make_depth_planes(L, 3e-3, 4e-3 / 7 if L > 2 else 2e-3)
+    spec = holo.PropagationSpec(S.WAVELENGTHS[c])
+    return gs, target, masks, dist, spec
+
+
+def run(holo, R, n, c, w, h, L, steps):
+    from paper_2511_15022_b200 import parallel as P
+    gs, target, masks, dist, spec = scene(holo, n, c, w, h, L)
+    full = holo.Trainer(gs, w, h, target, masks, dist, spec, 20)
+    trs = []
+    for r in range(R):
+        t = holo.Trainer(gs, w, h, target, masks, dist, spec, 20)
+        t.set_row_slab(r, R)
+        trs.append(t)
+    grp = P.LocalSlabGroup(trs, c, h, w, L)
+    out = []
+    for s in range(steps):
+        full.forward_backward()
+        gfull = full.grads_tensor().cpu().numpy().astype(np.float64)
+        full.apply_update()
+        lf = full.last_loss()[0]
+        ls = grp.step()
+        gslab = trs[0].grads_tensor().cpu().numpy().astype(np.float64)
+        out.append((lf, ls, rel_l2(gslab, gfull)))
+    pf = full.params()
+    ps = [t.params() for t in trs]
+    return out, pf, ps
+
+
+@pytest.mark.parametrize("R,n,c,w,h,L", [
+    (1, 400, 3, 64, 48, 1),
+    (2, 400, 3, 64, 48, 1),
+    (4, 400, 3, 64, 48, 2),
+    (2, 3000, 1, 256, 256, 1),    # cfg1 grid, compile-time planned FFT
+    (4, 800, 2, 96, 64, 3),
+])
+def test_slab_step_matches_unsharded(holo, R, n, c, w, h, L):
+    out, pf, ps = run(holo, R, n, c, w, h, L, steps=3)
+    for lf, ls, gerr in out:
+        assert ls == pytest.approx(lf, rel=2e-6), (lf, ls)
+        assert gerr < 1e-5, gerr
+    for p in ps:  # every rank applied the same update
+        assert np.array_equal(p, ps[0])
+    assert rel_l2(ps[0], pf) < 1e-6
+
+
+@pytest.mark.parametrize("R", [2, 4])
+def test_slab_step_cfg2_grid(holo, R):
+    """1080p RGB on the compile-time planned 3840x2160 FFT (CC 4 column tiles)."""
+    out, pf, ps = run(holo, R, 200_000, 3, 1920, 1080, 1, steps=2)
+    for lf, ls, gerr in out:
+        assert ls == pytest.approx(lf, rel=2e-6), (lf, ls)
+        assert gerr < 1e-5, gerr
+    assert rel_l2(ps[-1], pf) < 1e-6
+
+
+def test_slab_step_cfg4_eight_ranks(holo):
+    """cfg4 (4K RGB, 1M Gaussians) split into 8 row slabs of 270 rows and 8
+    column slabs of 480 two-column tiles of the 7680x4320 spectrum."""
+    out, pf, ps = run(holo, 8, 1_000_000, 3, 3840, 2160, 1, steps=1)
+    lf, ls, gerr = out[0]
+    assert ls == pytest.approx(lf, rel=2e-6), (lf, ls)
+    assert gerr < 1e-5, gerr
+    assert rel_l2(ps[3], pf) < 1e-6
+
+
+def test_slab_layout_errors(holo):
+    gs, target, masks, dist, spec = scene(holo, 100, 1, 64, 48, 1)
+    t = holo.Trainer(gs, 64, 48, target, masks, dist, spec, 5)
+    with pytest.raises(holo.HoloInvalidArgument):
+        t.set_row_slab(0, 5)      # 48 rows do not split into 5 slabs
+    with pytest.raises(holo.HoloInvalidArgument):
+        t.set_row_slab(2, 2)      # rank outside the group
+    with pytest.raises(holo.HoloInvalidArgument):
+        t.slab_stage(0)           # not sharded yet
+    t.set_row_slab(1, 2)
+    with pytest.raises(holo.HoloInvalidArgument):
+        t.slab_stage(7)
+    # exchange 0: 24 own rows x 16 four-column tiles per peer (floats);
+    # exchange 1 carries each peer's loss band: rank 0 rows [0, 34), rank 1 rows [14, 48)
+    assert t.slab_counts(0) == ([2 * 4 * 16 * 24] * 2, [2 * 4 * 16 * 24] * 2)
+    assert t.slab_counts(1) == ([2 * 4 * 16 * 34] * 2, [2 * 4 * 16 * 34] * 2)
