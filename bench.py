@@ -41,11 +41,17 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=50)
     p.add_argument("--profile-steps", type=int, default=10)
-    p.add_argument("--shard", choices=("replicas", "channels", "planes"), default="replicas",
+    p.add_argument("--virtual-ranks", type=int, default=0,
+                   help="--shard slabs on ONE GPU: R slab trainers stepped in lock-step with the "
+                        "all-to-alls done as device copies (parallel.LocalSlabGroup); reports the "
+                        "decomposition's compute per rank, no interconnect")
+    p.add_argument("--shard", choices=("replicas", "channels", "planes", "slabs"), default="replicas",
                    help="N>1: replicas = one scene per GPU (weak scaling, no collective); "
                         "channels = the wavelengths of one scene split over ranks (<= C ranks), "
                         "planes = the depth planes of one scene (cfg3) split over ranks; both "
-                        "all-reduce gradients over NCCL (strong scaling)")
+                        "all-reduce gradients over NCCL (strong scaling); slabs = the canvas rows "
+                        "and spectrum columns of one scene (cfg4) split over ranks: four NCCL "
+                        "all-to-all transposes + the gradient all-reduce per step")
     return p.parse_args()
 
 
@@ -199,7 +205,9 @@ def run_reference(args):
 def config_of(name, cfg, world, shard="replicas"):
     par = {"replicas": f"replicas x{world} (one scene per GPU, no collective)",
            "channels": f"wavelength shards x{world} (one scene; NCCL all-reduce of the 6N geometry gradients)",
-           "planes": f"plane shards x{world} (one scene; NCCL all-reduce of the gradient buffer)"}[shard]
+           "planes": f"plane shards x{world} (one scene; NCCL all-reduce of the gradient buffer)",
+           "slabs": f"row slabs x{world} (one scene; 4 NCCL all-to-all FFT transposes + gradient all-reduce)",
+           }[shard]
     seed = "init_gaussians(seed 42+rank)" if shard == "replicas" else "init_gaussians(seed 42)"
     return {"workload": f"{name}: {cfg['width']}x{cfg['height']} x{cfg['channels']} wavelengths, "
                         f"{cfg['count']} Gaussians, {cfg['planes']} plane(s), pad 2, {seed}",
@@ -239,6 +247,21 @@ def run_sharded(args):
                               wl["masks"], wl["distances"], holo.PropagationSpec(tuple(wl["wavelengths"][b:e])),
                               total_steps=total, channels_total=C_)
             step = P.ChannelShardedStep(tr, n, e - b, C_, h, w, L)
+        elif args.shard == "slabs":
+            def mk(r, R):
+                t = holo.Trainer(holo.GaussianSet(n, C_, **g32), w, h,
+                                 holo.RealField(C_, h, w, wl["target"].astype(np.float32).astype(np.float64)),
+                                 wl["masks"], wl["distances"], holo.PropagationSpec(tuple(wl["wavelengths"])),
+                                 total_steps=total)
+                t.set_row_slab(r, R)
+                return t
+            if args.virtual_ranks > 1 and world == 1:
+                trs = [mk(r, args.virtual_ranks) for r in range(args.virtual_ranks)]
+                tr = trs[0]
+                step = P.LocalSlabGroup(trs, C_, h, w, L)
+            else:
+                tr = mk(rank, world)
+                step = P.SlabShardedStep(tr, C_, h, w, L)
         else:
             tr = holo.Trainer(holo.GaussianSet(n, C_, **g32), w, h,
                               holo.RealField(C_, h, w, wl["target"].astype(np.float32).astype(np.float64)),
@@ -286,6 +309,14 @@ def run_sharded(args):
             "timing": "eager steps (NCCL all-reduce between forward_backward and apply_update), "
                       "CUDA events on the trainer stream, max over ranks",
         }
+        if args.shard == "slabs" and args.virtual_ranks > 1 and world == 1:
+            R = args.virtual_ranks
+            line["virtual_ranks"] = {
+                "ranks": R, "ms_all_ranks_one_gpu": ms, "ms_per_rank_compute": ms / R,
+                "note": "R slab trainers on one GPU, exchanges as device copies: ms/R is the "
+                        "per-rank compute of an R-GPU run without the interconnect time"}
+            line["value"] = None
+            line["metric"] = METRIC + " (virtual ranks: decomposition check, not a throughput)"
         print(json.dumps(line))
     if world > 1:
         dist.barrier()
