@@ -513,15 +513,17 @@ __global__ void intensity_kernel(const float2* f, int64_t n, float* out) {
 // the position group, pipeline.cpp:254) and the bias corrections.
 __device__ void adan_consts(const AdanGroups& G, int total_steps, double b1, double b2, double b3, int s, int t,
                             GroupConst* K) {
+    // the bias corrections are shared by the six groups: three pow() per step
+    const double bc1 = 1.0 - pow(b1, static_cast<double>(t));
+    const double bc2 = 1.0 - pow(b2, static_cast<double>(t));
+    const double bc3 = 1.0 - pow(b3, static_cast<double>(t));
+    const float ib1 = static_cast<float>(1.0 / bc1), bb2 = static_cast<float>(b2 / bc2),
+                ib3 = static_cast<float>(1.0 / bc3);
     for (int gi = 0; gi < 6; ++gi) {
         double lr = G.base_lr[gi];
         if (gi == 0)  // cosine_lr(step, total, 1e-2, 1e-3)
             lr = 1e-3 + 0.5 * (1e-2 - 1e-3) * (1.0 + cos(3.14159265358979323846 * static_cast<double>(s) / total_steps));
-        const double bc1 = 1.0 - pow(b1, static_cast<double>(t));
-        const double bc2 = 1.0 - pow(b2, static_cast<double>(t));
-        const double bc3 = 1.0 - pow(b3, static_cast<double>(t));
-        K[gi] = GroupConst{static_cast<float>(lr), static_cast<float>(1.0 / bc1), static_cast<float>(b2 / bc2),
-                           static_cast<float>(1.0 / bc3)};
+        K[gi] = GroupConst{static_cast<float>(lr), ib1, bb2, ib3};
     }
 }
 

@@ -169,41 +169,71 @@ __global__ void shade_kernel(const float* __restrict__ params, int n, int c, flo
 // pairs are unique, so the result equals the reference's std::sort order
 // exactly, independent of the scatter order.
 // ---------------------------------------------------------------------------
-constexpr int kScanThreads = 512;
+constexpr int kScanThreads = 1024;
 __global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(const uint32_t* __restrict__ tcount, int tiles,
                                                                  uint32_t* __restrict__ toffset,
                                                                  uint2* __restrict__ ranges,
                                                                  uint32_t* __restrict__ status, int64_t cap) {
-    // each thread scans a contiguous run of tiles serially; one block scan joins the runs
+    // each thread scans a contiguous run of tiles serially (16-byte loads and
+    // stores when the runs are multiples of 4 tiles); one block scan joins the runs
     using BSc = cub::BlockScan<unsigned long long, kScanThreads>;
     __shared__ typename BSc::TempStorage tmp;
-    // up to kReg tiles per thread live in registers (all loads in flight at once)
-    constexpr int kReg = 16;
+    constexpr int kReg = 8;  // tiles per thread held in registers (cfg2: 8160 tiles -> 8 per thread)
     const int per = (tiles + kScanThreads - 1) / kScanThreads;
     const int t0 = threadIdx.x * per, t1 = min(t0 + per, tiles);
+    const bool vec = (per % 4) == 0 && t1 - t0 == per;
     unsigned long long run = 0;
     uint32_t c[kReg];
+    if (vec && per <= kReg) {
 #pragma unroll
-    for (int i = 0; i < kReg; ++i) c[i] = (t0 + i < t1) ? tcount[t0 + i] : 0u;
+        for (int i = 0; i < kReg; i += 4) {
+            uint4 q = make_uint4(0u, 0u, 0u, 0u);
+            if (i < per) q = *reinterpret_cast<const uint4*>(tcount + t0 + i);
+            c[i] = q.x; c[i + 1] = q.y; c[i + 2] = q.z; c[i + 3] = q.w;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < kReg; ++i) c[i] = (t0 + i < t1) ? tcount[t0 + i] : 0u;
+    }
 #pragma unroll
     for (int i = 0; i < kReg; ++i) run += c[i];
     for (int t = t0 + kReg; t < t1; ++t) run += tcount[t];
     unsigned long long ex, agg;
     BSc(tmp).ExclusiveSum(run, ex, agg);
+    if (vec && per <= kReg) {
 #pragma unroll
-    for (int i = 0; i < kReg; ++i) {
-        if (t0 + i < t1) {
-            toffset[t0 + i] = static_cast<uint32_t>(ex);
-            ranges[t0 + i] = c[i] ? make_uint2(static_cast<uint32_t>(ex), static_cast<uint32_t>(ex + c[i]))
-                                  : make_uint2(0u, 0u);
-            ex += c[i];
+        for (int i = 0; i < kReg; i += 4) {
+            if (i < per) {
+                uint32_t o[4];
+                uint2 r[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    o[k] = static_cast<uint32_t>(ex);
+                    r[k] = c[i + k] ? make_uint2(static_cast<uint32_t>(ex), static_cast<uint32_t>(ex + c[i + k]))
+                                    : make_uint2(0u, 0u);
+                    ex += c[i + k];
+                }
+                *reinterpret_cast<uint4*>(toffset + t0 + i) = make_uint4(o[0], o[1], o[2], o[3]);
+                reinterpret_cast<uint4*>(ranges + t0 + i)[0] = make_uint4(r[0].x, r[0].y, r[1].x, r[1].y);
+                reinterpret_cast<uint4*>(ranges + t0 + i)[1] = make_uint4(r[2].x, r[2].y, r[3].x, r[3].y);
+            }
         }
-    }
-    for (int t = t0 + kReg; t < t1; ++t) {
-        const uint32_t v = tcount[t];
-        toffset[t] = static_cast<uint32_t>(ex);
-        ranges[t] = v ? make_uint2(static_cast<uint32_t>(ex), static_cast<uint32_t>(ex + v)) : make_uint2(0u, 0u);
-        ex += v;
+    } else {
+#pragma unroll
+        for (int i = 0; i < kReg; ++i) {
+            if (t0 + i < t1) {
+                toffset[t0 + i] = static_cast<uint32_t>(ex);
+                ranges[t0 + i] = c[i] ? make_uint2(static_cast<uint32_t>(ex), static_cast<uint32_t>(ex + c[i]))
+                                      : make_uint2(0u, 0u);
+                ex += c[i];
+            }
+        }
+        for (int t = t0 + kReg; t < t1; ++t) {
+            const uint32_t v = tcount[t];
+            toffset[t] = static_cast<uint32_t>(ex);
+            ranges[t] = v ? make_uint2(static_cast<uint32_t>(ex), static_cast<uint32_t>(ex + v)) : make_uint2(0u, 0u);
+            ex += v;
+        }
     }
     if (threadIdx.x == 0) {
         status[0] = static_cast<uint32_t>(agg > 0xffffffffull ? 0xffffffffull : agg);
@@ -394,20 +424,22 @@ __global__ void export_kernel(const uint32_t* __restrict__ ids, const uint2* __r
 // false when skipped; else G, saturation flag and alpha_eff in fp64.
 // ---------------------------------------------------------------------------
 // q = p64 + g, fields at stride n (SoA: px, py, i00, i01, i11, mahal_cutoff, alpha, r).
-__device__ __noinline__ bool exact_contrib(const double* __restrict__ q, size_t n, int x, int y, double& G,
-                                           bool& saturated, double& aeff) {
+// Returns (G, alpha_eff, saturated, contributes) by value: the out-values stay
+// in registers on the callers' fast paths (no local-memory round trip).
+__device__ __noinline__ float4 exact_contrib4(const double* __restrict__ q, size_t n, int x, int y) {
     const double dx = dsub(static_cast<double>(x), q[0]);
     const double dy = dsub(static_cast<double>(y), q[n]);
     // dx * dx * i00 + 2.0 * dx * dy * i01 + dy * dy * i11
     const double mahal = dadd(dadd(dmul(dmul(dx, dx), q[2 * n]), dmul(dmul(dmul(2.0, dx), dy), q[3 * n])),
                               dmul(dmul(dy, dy), q[4 * n]));
-    if (mahal > q[5 * n]) return false;
+    if (mahal > q[5 * n]) return make_float4(0.f, 0.f, 0.f, 0.f);
     const double power = fmax(dmul(-0.5, mahal), kPowerFloor);
-    G = exp(power);
+    const double G = exp(power);
     const double aG = dmul(q[6 * n], G);
-    saturated = aG > kAlphaCap;
-    aeff = saturated ? kAlphaCap : aG;
-    return !(aeff < kAlphaCutoff);
+    const bool saturated = aG > kAlphaCap;
+    const double aeff = saturated ? kAlphaCap : aG;
+    return make_float4(static_cast<float>(G), static_cast<float>(aeff), saturated ? 1.f : 0.f,
+                       aeff < kAlphaCutoff ? 0.f : 1.f);
 }
 
 // ---------------------------------------------------------------------------
@@ -512,10 +544,14 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(
                 const bool bandA = mA > lo && mA <= hi, bandB = mB > lo && mB <= hi;
                 if (__any_sync(0xffffffffu, bandA || bandB)) {  // rare: exact fp64 decision
                     const double* q = p64 + G.id;
-                    double G, ae;
-                    bool sat;
-                    if (bandA) aA = exact_contrib(q, N, x, y, G, sat, ae) ? static_cast<float>(ae) : 0.f;
-                    if (bandB) aB = exact_contrib(q, N, x, y + 4, G, sat, ae) ? static_cast<float>(ae) : 0.f;
+                    if (bandA) {
+                        const float4 e4 = exact_contrib4(q, N, x, y);
+                        aA = e4.w != 0.f ? e4.y : 0.f;
+                    }
+                    if (bandB) {
+                        const float4 e4 = exact_contrib4(q, N, x, y + 4);
+                        aB = e4.w != 0.f ? e4.y : 0.f;
+                    }
                 }
 #pragma unroll
                 for (int c = 0; c < C; ++c) {
@@ -581,12 +617,12 @@ __global__ void __launch_bounds__(kBwdThreads, MINB) raster_bwd_kernel(
     const float M = cut + tol;
     const float ratio = i01 * inv_i00;
     // channel planes of the gradient field: rows [y0, y0 + hs) of the canvas
-    // (the whole canvas unless row-slab sharded), indexed by canvas row
+    // (the whole canvas unless row-slab sharded), indexed by canvas offset
+    // y W + x (32-bit) from one base; channel c is c * cs further on
     (void)H;
-    const float2* gch[C];
-#pragma unroll
-    for (int c = 0; c < C; ++c) gch[c] = gfield + static_cast<size_t>(c) * hs * W - static_cast<ptrdiff_t>(y0) * W;
-    const int o_idle = y0 * W;  // a valid pixel for idle lanes
+    const float2* gbase = gfield - static_cast<ptrdiff_t>(y0) * W;
+    const unsigned cs = static_cast<unsigned>(hs) * static_cast<unsigned>(W);
+    const unsigned o_idle = static_cast<unsigned>(y0) * static_cast<unsigned>(W);  // a valid pixel for idle lanes
 
     float2 dap[C];  // (d_amp, d_phase) per channel
 #pragma unroll
@@ -649,9 +685,13 @@ __global__ void __launch_bounds__(kBwdThreads, MINB) raster_bwd_kernel(
             float2 gv[NCH][C];
 #pragma unroll
             for (int u = 0; u < NCH; ++u) {
-                const int o = act[u] ? oy[u] * W + ox[u] : o_idle;
+                const unsigned o = act[u] ? static_cast<unsigned>(oy[u] * W + ox[u]) : o_idle;
+                const float2* p = gbase + o;
 #pragma unroll
-                for (int c = 0; c < C; ++c) gv[u][c] = gch[c][o];
+                for (int c = 0; c < C; ++c) {
+                    gv[u][c] = __ldg(p);
+                    p += cs;
+                }
             }
 #pragma unroll
             for (int u = 0; u < NCH; ++u) {
@@ -668,11 +708,12 @@ __global__ void __launch_bounds__(kBwdThreads, MINB) raster_bwd_kernel(
                     sat = aG > 0.99f;
                     aeff = sat ? 0.99f : aG;
                 } else {
-                    double Gd, ae;
-                    if (!exact_contrib(q, N, x, y, Gd, sat, ae)) continue;
-                    G = static_cast<float>(Gd);
+                    const float4 e4 = exact_contrib4(q, N, x, y);
+                    if (e4.w == 0.f) continue;
+                    G = e4.x;
                     aG = alpha * G;
-                    aeff = static_cast<float>(ae);
+                    aeff = e4.y;
+                    sat = e4.z != 0.f;
                 }
                 float s_amp = 0.f;
 #pragma unroll
