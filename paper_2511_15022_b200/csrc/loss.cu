@@ -225,7 +225,9 @@ struct SsimCta {
     // and of the target statistics of valid row v; one commit group.
     __device__ __forceinline__ void issue(int r, int v) const {
         const bool rok = r >= 0 && r < H;
-        const size_t rowp = static_cast<size_t>(min(max(r, 0), H - 1)) * W;
+        // 32-bit row offset (a plane is < 2^32 elements); out-of-image rows
+        // zero-fill from the (valid) row-0 address
+        const unsigned rowp = rok ? static_cast<unsigned>(r) * static_cast<unsigned>(W) : 0u;
         const int slot = r & (kRaw - 1);
         cp_async<sizeof(Raw)>(&S.rawU[slot][t], srcA + rowp, rok && okA);
         cp_async<4>(&S.rawT[slot][t], tgtA + rowp, rok && okA);
@@ -234,7 +236,7 @@ struct SsimCta {
             cp_async<4>(&S.rawT[slot][kSW + t], tgtB + rowp, rok && okB);
         }
         const bool vok = v >= 0 && v < vh;
-        cp_async<8>(&S.ts[v & (kTsRing - 1)][t], tsA + static_cast<size_t>(min(max(v, 0), vh - 1)) * vw,
+        cp_async<8>(&S.ts[v & (kTsRing - 1)][t], tsA + (vok ? static_cast<unsigned>(v) * static_cast<unsigned>(vw) : 0u),
                     vok && okV);
         cp_commit();
     }
@@ -316,7 +318,8 @@ struct SsimCta {
         if (kind == kLossTraining) {  // mask of the next step's output row, one step ahead
             const int yn = y + 1;
             mk_next = (t >= kHalo && yn >= y0 && yn < y0 + SR && yn < H && x < W)
-                          ? (mask[static_cast<size_t>(yn) * W + x] ? 1.f : 0.f) : 0.f;
+                          ? (mask[static_cast<unsigned>(yn) * static_cast<unsigned>(W) + static_cast<unsigned>(x)] ? 1.f : 0.f)
+                          : 0.f;
         }
         {
             // threads t < 10 own no output column: their spread row stays 0
@@ -345,10 +348,10 @@ struct SsimCta {
                 if (!BAND || static_cast<unsigned>(y - a.own0) < static_cast<unsigned>(a.own1 - a.own0)) st.sum += static_cast<double>(d * d * k);
                 g = fmaf(wr * d, k, g);
             }
-            const size_t p = plane_off + static_cast<size_t>(y) * W + x;
-            if (a.grad) a.grad[p] = g;
+            const unsigned p = static_cast<unsigned>(y) * static_cast<unsigned>(W) + static_cast<unsigned>(x);
+            if (a.grad) a.grad[plane_off + p] = g;
             if constexpr (FROM_FIELD) {
-                if (a.du) a.du[p] = make_float2(2.f * uu.x * g, 2.f * uu.y * g);
+                if (a.du) (a.du + plane_off)[p] = make_float2(2.f * uu.x * g, 2.f * uu.y * g);
             }
         }
     }
