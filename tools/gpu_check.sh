@@ -2,8 +2,8 @@
 # One gpurun call: GPU parity tests, smoke, bench line (+ reference arm), launch list,
 # ncu --set full on the top kernels.   usage: tools/gpu_check.sh TAG [ncu-kernel-regex] [skip] [count]
 TAG=${1:-check}
-KRE=${2:-'raster_bwd_kernel|ssim_loss_kernel|scols_fwd1|raster_fwd_kernel|srows_inv|srows_fwd'}
-SKIP=${3:-18}; CNT=${4:-7}
+KRE=${2:-'raster_bwd_kernel|ssim_loss_kernel|pcols_fwd1|pcols_bwd1|raster_fwd_kernel|srows_inv|srows_fwd|adan_fused|scatter_ids'}
+SKIP=${3:-22}; CNT=${4:-11}
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/${TAG}_smi.txt 2>&1
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/${TAG}_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/${TAG}_pytest.log
