@@ -214,6 +214,129 @@ __device__ __forceinline__ void pcol_single(const ColArgs& a, const float2* __re
         }));
 }
 
+// ---- column-pair kernel with the tile staged by a TMA bulk copy ----
+// The H live rows of a tile are one contiguous run of H * CC complex in the T
+// layout, so ONE cp.async.bulk (mbarrier completion) stages it in shared
+// memory and the forward FFT's first stage reads shared memory (no per-thread
+// global loads).  With KT > 1 tiles per CTA the next tile is prefetched while
+// the current tile's inverse FFT runs.
+// tiles per CTA of the staged column kernels; measured at cfg2 (us per pass):
+// 1 -> 152 (the plain kernel: 154), 2 (prefetch of the second tile overlapping
+// the first tile's inverse FFT) -> 160: the global loads were not the limiter.
+constexpr int kPersistTiles = 1;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra.uni WAIT_%=;\n}\n"
+        ::"r"(smem_u32(bar)), "r"(parity));
+}
+
+// One tile of the prefetching column kernel: wait for its staged rows, forward
+// FFT from shared memory x H, prefetch tile tn into the staging buffer, inverse
+// FFT to global (cropped rows).
+template <int N, int NT, bool CONJ, class RAD>
+__device__ __forceinline__ void pcol_tile(float4* work, float4* stage_buf, uint64_t* bar, unsigned parity,
+                                          const float2* __restrict__ tw, TfConst tf, int t, int tn, int total,
+                                          int ntiles, int tile0, int Px, int oy, const float2* gin, float2* gout,
+                                          size_t tile_elems, unsigned bytes) {
+    constexpr int CC = 4, NP = 2;
+    const int tid = threadIdx.x, pp = tid % NP;
+    const int tile = t % ntiles;
+    PairTf ptf;
+    ptf.mx0 = wrapped((tile0 + tile) * CC + 2 * pp, Px);
+    ptf.mx1 = wrapped((tile0 + tile) * CC + 2 * pp + 1, Px);
+    {
+        const float f0 = static_cast<float>(ptf.mx0), f1 = static_cast<float>(ptf.mx1);
+        ptf.qx = make_float2(tf.bx * f0 * f0, tf.bx * f1 * f1);
+        ptf.inband = make_float2(abs(ptf.mx0) <= tf.mx_max ? 1.f : 0.f, abs(ptf.mx1) <= tf.mx_max ? 1.f : 0.f);
+    }
+    mbar_wait(bar, parity);
+    const float4* stg = stage_buf - oy * NP;  // row i of the padded column
+    pfft::run<N, NP, NT, -1, pfft::Half, pfft::Full>(
+        work, tw, tid, RAD{},
+        pfft::in_fn([stg](int i, int p) {
+            const float4 q = stg[i * NP + p];
+            return pfft::C2{make_float2(q.x, q.z), make_float2(q.y, q.w)};
+        }),
+        pfft::out_map([tf, ptf](int i, int, pfft::C2 v) {
+            float2 hc, hs;
+            transfer_pair<CONJ>(tf, ptf, wrapped(i, N), hc, hs);
+            return pfft::C2{f2sub(f2mul(v.re, hc), f2mul(v.im, hs)), f2fma(v.im, hc, f2mul(v.re, hs))};
+        }));
+    // the staging buffer is free (the forward FFT ended with a barrier): prefetch tile tn
+    if (tid == 0 && tn < total) bulk_load(stage_buf, gin + static_cast<size_t>(tn) * tile_elems, bytes, bar);
+    float2* dst = gout + static_cast<size_t>(t) * tile_elems - static_cast<size_t>(oy) * CC;
+    pfft::run<N, NP, NT, +1, pfft::Full, pfft::Half>(
+        work, tw, tid, RAD{}, pfft::InSmem{},
+        pfft::out_fn([dst](int i, int p, pfft::C2 v) {
+            *reinterpret_cast<float4*>(dst + static_cast<size_t>(i) * CC + 2 * p) =
+                make_float4(v.re.x, v.im.x, v.re.y, v.im.y);
+        }));
+}
+
+template <int N, int NT, bool CONJ, class RAD, int KT>
+__device__ __forceinline__ void pcol_persist(const ColArgs& a, const float2* __restrict__ tw) {
+    constexpr int CC = 4, NP = 2;
+    static_assert(NT % NP == 0, "pair of a thread must be fixed");
+    static_assert(KT >= 1 && KT <= 3, "tiles per CTA");
+    extern __shared__ float4 smem4[];
+    float4* work = smem4;
+    const int H = a.H, oy = a.oy, ntiles = a.ntiles, Px = a.Px, tile0 = a.tile0;
+    const int total = ntiles * a.C;
+    float4* stage_buf = smem4 + pfft::padded_len4(N * NP);  // H rows x 2 pairs
+    uint64_t* bar = reinterpret_cast<uint64_t*>(stage_buf + H * NP);
+    const size_t tile_elems = static_cast<size_t>(H) * CC;
+    const unsigned bytes = static_cast<unsigned>(tile_elems * sizeof(float2));
+    const int G = gridDim.x;
+    const int t0 = blockIdx.x;
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        if (t0 < total) bulk_load(stage_buf, a.in + static_cast<size_t>(t0) * tile_elems, bytes, bar);
+    }
+    __syncthreads();
+    // KT tiles per CTA (t0, t0 + G, ...) in straight-line code
+    if (t0 < total)
+        pcol_tile<N, NT, CONJ, RAD>(work, stage_buf, bar, 0u, tw, a.tf[t0 / ntiles], t0, KT >= 2 ? t0 + G : total,
+                                    total, ntiles, tile0, Px, oy, a.in, a.out, tile_elems, bytes);
+    if constexpr (KT >= 2) {
+        const int t1 = t0 + G;
+        __syncthreads();  // work buffer reuse
+        if (t1 < total)
+            pcol_tile<N, NT, CONJ, RAD>(work, stage_buf, bar, 1u, tw, a.tf[t1 / ntiles], t1, KT >= 3 ? t1 + G : total,
+                                        total, ntiles, tile0, Px, oy, a.in, a.out, tile_elems, bytes);
+    }
+    if constexpr (KT >= 3) {
+        const int t2 = t0 + 2 * G;
+        __syncthreads();
+        if (t2 < total)
+            pcol_tile<N, NT, CONJ, RAD>(work, stage_buf, bar, 0u, tw, a.tf[t2 / ntiles], t2, total, total, ntiles,
+                                        tile0, Px, oy, a.in, a.out, tile_elems, bytes);
+    }
+}
+
+template <int N, int NT, int MINB, class RAD>
+__global__ void __launch_bounds__(NT, MINB) pcols_fwdP_kernel(ColArgs a, const float2* __restrict__ tw) {
+    pcol_persist<N, NT, false, RAD, kPersistTiles>(a, tw);
+}
+template <int N, int NT, int MINB, class RAD>
+__global__ void __launch_bounds__(NT, MINB) pcols_bwdP_kernel(ColArgs a, const float2* __restrict__ tw) {
+    pcol_persist<N, NT, true, RAD, kPersistTiles>(a, tw);
+}
+
 template <int N, int NT, int MINB, class RAD>
 __global__ void __launch_bounds__(NT, MINB) pcols_fwd1_kernel(ColArgs a, const float2* __restrict__ tw) {
     pcol_single<N, NT, false, RAD>(a, tw, blockIdx.y);
@@ -306,6 +429,8 @@ struct ColPlan {
     std::vector<float2> (*table)(int);
     int nt1 = 0;        // threads of the single-plane kernels (0: nt)
     bool pair = false;  // single-plane kernels use the column-pair SIMD engine (float4 smem)
+    void (*fwdP)(ColArgs, const float2*) = nullptr;  // bulk-copy staged single-plane kernels
+    void (*bwdP)(ColArgs, const float2*) = nullptr;
 };
 
 template <int N, int RB, int NT, int CCO, class RAD>
@@ -321,6 +446,8 @@ ColPlan pcol_plan() {
               [](int n) { return sfft::twiddle_table(n, RAD{}); }};
     p.nt1 = NT1;
     p.pair = true;
+    p.fwdP = pcols_fwdP_kernel<N, NT1, MINB1, RAD>;
+    p.bwdP = pcols_bwdP_kernel<N, NT1, MINB1, RAD>;
     return p;
 }
 
@@ -405,6 +532,35 @@ size_t cols_smem(const Plans& p, int L) {
 }
 int cols_threads(const Plans& p, int L) { return (L == 1 && p.col.nt1) ? p.col.nt1 : p.col.nt; }
 
+// bulk-copy staged column kernels (HS_COL_PERSIST=0 turns them off)
+bool persist_on() {
+    static const bool v = [] {
+        const char* e = std::getenv("HS_COL_PERSIST");
+        return e ? std::atoi(e) != 0 : true;
+    }();
+    return v;
+}
+size_t cols_smem_persist(const Plans& p, int H) {
+    return cols_smem(p, 1) + sizeof(float2) * static_cast<size_t>(H) * p.col.cc + 16;
+}
+
+// Column pass launch: the staged kernels for a single plane when the plan has
+// them (KT tiles per CTA), else one CTA per (tile, channel).
+void launch_cols(const Plans* p, const AsmWork& w, bool backward, const ColArgs& c, cudaStream_t st) {
+    if (w.L == 1 && p->col.fwdP && persist_on()) {
+        int dev = 0;
+        const int total = c.ntiles * c.C;
+        const int grid = (total + kPersistTiles - 1) / kPersistTiles;
+        (void)dev;
+        (backward ? p->col.bwdP : p->col.fwdP)<<<grid, p->col.nt1, cols_smem_persist(*p, w.H), st>>>(c, w.stw_y);
+    } else {
+        const size_t cs = cols_smem(*p, w.L);
+        auto k = backward ? (w.L > 1 ? p->col.bwdL : p->col.bwd) : (w.L > 1 ? p->col.fwdL : p->col.fwd);
+        k<<<dim3(c.ntiles, c.C), cols_threads(*p, w.L), cs, st>>>(c, w.stw_y);
+    }
+    launch_check(backward ? "scols_bwd" : "scols_fwd");
+}
+
 
 }  // namespace
 
@@ -427,13 +583,20 @@ void static_prepare(AsmWork& w) {
     HS_CUDA(cudaFuncSetAttribute(p->row.inv, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rs)));
     for (auto k : {p->col.fwd, p->col.bwd, p->col.fwdL, p->col.bwdL})
         HS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cs)));
+    if (p->col.fwdP) {
+        const int csp = static_cast<int>(cols_smem_persist(*p, w.H));
+        for (auto k : {p->col.fwdP, p->col.bwdP}) {
+            HS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, csp));
+            HS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        }
+    }
 }
 
 
 bool static_forward(AsmWork& w, const float2* d_in, float2* d_out, cudaStream_t st, cudaEvent_t* ev) {
     const Plans* p = find(w.Px, w.Py);
     if (!p || p->cc != w.CC) return false;
-    const size_t rs = rows_smem(*p), cs = cols_smem(*p, w.L);
+    const size_t rs = rows_smem(*p);
     const int rows1 = w.C * w.H;
     RowArgs r{d_in, w.T1.as<float2>(), w.W, w.H, w.Px, w.ox, w.ntiles, 1.f, w.plan_x, nullptr};
     p->row.fwd<<<(rows1 + p->row.rb - 1) / p->row.rb, p->row.nt, rs, st>>>(r, rows1, w.stw_x);
@@ -441,8 +604,7 @@ bool static_forward(AsmWork& w, const float2* d_in, float2* d_out, cudaStream_t 
     if (ev) HS_CUDA(cudaEventRecord(ev[0], st));
     ColArgs c{w.T1.as<float2>(), w.T2.as<float2>(), w.C, w.H, w.Py, w.Px, w.oy, w.ntiles, w.L, w.plan_y, nullptr,
               w.tf.as<TfConst>()};
-    (w.L > 1 ? p->col.fwdL : p->col.fwd)<<<dim3(w.ntiles, w.C), cols_threads(*p, w.L), cs, st>>>(c, w.stw_y);
-    launch_check("scols_fwd");
+    launch_cols(p, w, false, c, st);
     if (ev) HS_CUDA(cudaEventRecord(ev[1], st));
     const int rows2 = w.L * w.C * w.H;
     RowArgs ri{w.T2.as<float2>(), d_out, w.W, w.H, w.Px, w.ox, w.ntiles,
@@ -456,7 +618,7 @@ bool static_forward(AsmWork& w, const float2* d_in, float2* d_out, cudaStream_t 
 bool static_backward(AsmWork& w, const float2* d_grads, float2* d_out, cudaStream_t st, cudaEvent_t* ev) {
     const Plans* p = find(w.Px, w.Py);
     if (!p || p->cc != w.CC) return false;
-    const size_t rs = rows_smem(*p), cs = cols_smem(*p, w.L);
+    const size_t rs = rows_smem(*p);
     const int rows1 = w.L * w.C * w.H;
     RowArgs r{d_grads, w.T2.as<float2>(), w.W, w.H, w.Px, w.ox, w.ntiles, 1.f, w.plan_x, nullptr};
     p->row.fwd<<<(rows1 + p->row.rb - 1) / p->row.rb, p->row.nt, rs, st>>>(r, rows1, w.stw_x);
@@ -464,8 +626,7 @@ bool static_backward(AsmWork& w, const float2* d_grads, float2* d_out, cudaStrea
     if (ev) HS_CUDA(cudaEventRecord(ev[0], st));
     ColArgs c{w.T2.as<float2>(), w.T1.as<float2>(), w.C, w.H, w.Py, w.Px, w.oy, w.ntiles, w.L, w.plan_y, nullptr,
               w.tf.as<TfConst>()};
-    (w.L > 1 ? p->col.bwdL : p->col.bwd)<<<dim3(w.ntiles, w.C), cols_threads(*p, w.L), cs, st>>>(c, w.stw_y);
-    launch_check("scols_bwd");
+    launch_cols(p, w, true, c, st);
     if (ev) HS_CUDA(cudaEventRecord(ev[1], st));
     const int rows2 = w.C * w.H;
     RowArgs ri{w.T1.as<float2>(), d_out, w.W, w.H, w.Px, w.ox, w.ntiles,
@@ -492,12 +653,9 @@ bool static_cols_pass(AsmWork& w, bool backward, const float2* in, float2* out, 
                       cudaStream_t st) {
     const Plans* p = find(w.Px, w.Py);
     if (!p || p->cc != w.CC) return false;
-    const size_t cs = cols_smem(*p, w.L);
     ColArgs c{in, out, w.C, w.H, w.Py, w.Px, w.oy, ntiles_local, w.L, w.plan_y, nullptr, w.tf.as<TfConst>()};
     c.tile0 = tile0;
-    auto k = backward ? (w.L > 1 ? p->col.bwdL : p->col.bwd) : (w.L > 1 ? p->col.fwdL : p->col.fwd);
-    k<<<dim3(ntiles_local, w.C), cols_threads(*p, w.L), cs, st>>>(c, w.stw_y);
-    launch_check(backward ? "scols_bwd" : "scols_fwd");
+    launch_cols(p, w, backward, c, st);
     return true;
 }
 
