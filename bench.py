@@ -41,6 +41,11 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=50)
     p.add_argument("--profile-steps", type=int, default=10)
+    p.add_argument("--scenes", type=int, default=64, help="cfg5: scenes in the batch (split over ranks)")
+    p.add_argument("--scene-sample", type=int, default=2,
+                   help="cfg5: scenes this rank actually runs (a bounded sample of its share; 0 = all)")
+    p.add_argument("--train-steps", type=int, default=2000, help="cfg5: optimisation steps per scene")
+    p.add_argument("--poh-steps", type=int, default=600, help="cfg5: random-POH conversion steps per scene")
     p.add_argument("--virtual-ranks", type=int, default=0,
                    help="--shard slabs on ONE GPU: R slab trainers stepped in lock-step with the "
                         "all-to-alls done as device copies (parallel.LocalSlabGroup); reports the "
@@ -323,10 +328,100 @@ def run_sharded(args):
         dist.destroy_process_group()
 
 
+def run_cfg5(args):
+    """cfg5: a batch of 1080p RGB scenes (L = 2), each optimised
+    for --train-steps iterations, rasterised, DPAC-encoded (smooth POH) and
+    converted to a random POH (--poh-steps); scenes are split over the ranks
+    (replicas, no collective).  Reports scenes/s for the whole batch from the
+    measured per-scene device time of a bounded sample (--scene-sample)."""
+    import ctypes as C
+    import torch
+    import torch.distributed as dist
+
+    from paper_2511_15022_b200 import _lib, holo, synthetic as S
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    mine = list(range(rank, args.scenes, world))
+    run = mine if args.scene_sample <= 0 else mine[:args.scene_sample]
+    lib = _lib.load()
+    phase_ms = {"train": 0.0, "raster": 0.0, "dpac": 0.0, "random_poh": 0.0}
+    stream = torch.cuda.Stream()
+    launches0 = holo.kernel_launch_count()
+    with torch.cuda.stream(stream):
+        for i in run:
+            wl = S.workload("cfg5", scene=i)
+            cfg = wl["cfg"]
+            c, h, w, n, L = cfg["channels"], cfg["height"], cfg["width"], cfg["count"], cfg["planes"]
+            g32 = {k: np.asarray(v, np.float32).astype(np.float64) for k, v in wl["gaussians"].items()}
+            spec = holo.PropagationSpec(tuple(wl["wavelengths"]))
+            tr = holo.Trainer(holo.GaussianSet(n, c, **g32), w, h,
+                              holo.RealField(c, h, w, wl["target"].astype(np.float32).astype(np.float64)),
+                              wl["masks"], wl["distances"], spec, total_steps=args.train_steps)
+            tr.use_graph(True)
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+            stream.synchronize()
+            ev[0].record(stream)
+            for _ in range(args.train_steps):
+                tr.step(sync_loss=False)
+            ev[1].record(stream)
+            field = holo.rasterize_forward_device(tr.params_tensor(), n, c, w, h)
+            ev[2].record(stream)
+            smooth = torch.empty((c, h, w), dtype=torch.float32, device=field.device)
+            holo.check(lib.hs_dpac_encode(holo.ctx_handle(), holo._ptr(field), c, h, w, 0, holo._ptr(smooth)))
+            ev[3].record(stream)
+            phase = torch.from_numpy(holo.random_phase(i, c * h * w).astype(np.float32)).to(field.device)
+            d = (C.c_double * L)(*wl["distances"])
+            tgt = np.ascontiguousarray(wl["target"], dtype=np.float32)
+            msk = np.ascontiguousarray(wl["masks"], dtype=np.uint8)
+            pc = holo.hs_poh_config(c, h, w, L, C.cast(d, C.POINTER(C.c_double)), spec.c_struct(),
+                                    tgt.ctypes.data_as(C.POINTER(C.c_float)), msk.ctypes.data_as(C.POINTER(C.c_uint8)),
+                                    int(args.poh_steps), 0.1, 0.01, 2.5e-3)
+            holo.check(lib.hs_convert_random_poh_field(holo.ctx_handle(), C.byref(pc), holo._ptr(field),
+                                                       holo._ptr(phase), None))
+            ev[4].record(stream)
+            ev[4].synchronize()
+            for k, (a, b) in zip(phase_ms, zip(ev[:-1], ev[1:])):
+                phase_ms[k] += a.elapsed_time(b)
+            del tr
+    launches = holo.kernel_launch_count() - launches0
+    per_scene = sum(phase_ms.values()) / max(1, len(run))
+    total_ms = per_scene * len(mine)  # this rank's share of the batch
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t[0])
+    if rank == 0:
+        line = {
+            "metric": "cfg5 conversion batch: scenes/s (train + raster + DPAC + random POH per scene)",
+            "value": args.scenes / (total_ms * 1e-3), "unit": "scenes/s", "n_gpus": world,
+            "higher_is_better": True, "scaling": "weak" if world == 1 else "strong", "dtype": "fp32",
+            "data": "synthetic", "vs_baseline": None,
+            "config": {"workload": f"cfg5: {args.scenes} scenes of 1920x1080 x3, {S.CONFIGS['cfg5']['count']} "
+                                   f"Gaussians, 2 planes, {args.train_steps} train steps + {args.poh_steps} "
+                                   "random-POH steps per scene",
+                       "parallelism": f"replicas x{world} (scenes split over ranks, no collective)",
+                       "sample": f"{len(run)} of this rank's {len(mine)} scenes timed; the batch time is "
+                                 "the per-scene device time x the rank's share (max over ranks)"},
+            "ms_per_scene": per_scene,
+            "phase_ms_per_scene": {k: v / max(1, len(run)) for k, v in phase_ms.items()},
+            "gpu_launches": int(launches),
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.workload == "cfg5" and args.shard == "replicas":
+        run_cfg5(args)
         return
     if args.shard != "replicas":
         run_sharded(args)

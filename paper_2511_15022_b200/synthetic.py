@@ -223,6 +223,8 @@ CONFIGS = {
     "cfg3": dict(width=1920, height=1080, channels=3, count=200_000, planes=8, dz=4e-3 / 7),
     "cfg4": dict(width=3840, height=2160, channels=3, count=1_000_000, planes=1, dz=2e-3),
     "desk": dict(width=256, height=160, channels=1, count=3413, planes=2, dz=2e-3),
+    # cfg5: one scene of the 64-scene conversion batch (N from ratio 5: round(2 C H W / 60))
+    "cfg5": dict(width=1920, height=1080, channels=3, count=207_360, planes=2, dz=2e-3),
 }
 WAVELENGTHS = {1: (532e-9,), 2: (639e-9, 473e-9), 3: (639e-9, 532e-9, 473e-9)}
 
