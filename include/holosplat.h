@@ -244,6 +244,24 @@ hs_status hs_trainer_slab_counts(hs_trainer* tr, int exchange, int64_t* out);
 float* hs_trainer_slab_send_ptr(hs_trainer* tr);
 float* hs_trainer_slab_recv_ptr(hs_trainer* tr);
 hs_status hs_trainer_slab_stage(hs_trainer* tr, int stage);
+/* Peer-put exchange (instead of an all-to-all between the stages): the pack
+ * at the end of stage k stores straight into every peer's receive buffer of
+ * parity k & 1 (at this rank's slot) and signals the peers' flag arrays; stage
+ * k + 1 begins by waiting on this rank's flags (bounded: ~2 s, then
+ * hs_trainer_slab_status reports 1).  recv0 / recv1 / flags hold, per rank,
+ * device addresses valid in this context -- the peers' hs_trainer_slab_recv_ptr,
+ * hs_trainer_slab_recv2_ptr and hs_trainer_slab_flags_ptr mapped with CUDA IPC
+ * (hs_ipc_*) or P2P; the own entries are the own buffers. */
+float* hs_trainer_slab_recv2_ptr(hs_trainer* tr);
+uint32_t* hs_trainer_slab_flags_ptr(hs_trainer* tr);
+hs_status hs_trainer_slab_set_peers(hs_trainer* tr, float* const* recv0, float* const* recv1,
+                                    uint32_t* const* flags);
+hs_status hs_trainer_slab_status(hs_trainer* tr, uint32_t* error);
+/* CUDA IPC of a device allocation: 64-byte handle out; open maps a peer
+ * process's allocation into this context (lazy peer access); close unmaps. */
+hs_status hs_ipc_get_handle(const void* d_ptr, void* handle64);
+hs_status hs_ipc_open_handle(const void* handle64, void** d_ptr);
+hs_status hs_ipc_close(void* d_ptr);
 
 #ifdef __cplusplus
 }

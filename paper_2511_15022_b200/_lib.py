@@ -122,6 +122,13 @@ _SIGS = {
     "hs_trainer_slab_send_ptr": [C.c_void_p],
     "hs_trainer_slab_recv_ptr": [C.c_void_p],
     "hs_trainer_slab_stage": [C.c_void_p, C.c_int],
+    "hs_trainer_slab_recv2_ptr": [C.c_void_p],
+    "hs_trainer_slab_flags_ptr": [C.c_void_p],
+    "hs_trainer_slab_set_peers": [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)],
+    "hs_trainer_slab_status": [C.c_void_p, C.POINTER(C.c_uint32)],
+    "hs_ipc_get_handle": [C.c_void_p, C.c_void_p],
+    "hs_ipc_open_handle": [C.c_void_p, C.POINTER(C.c_void_p)],
+    "hs_ipc_close": [C.c_void_p],
     "hs_last_error": [],
     "hs_kernel_launch_count": [],
 }
@@ -133,6 +140,8 @@ _RESTYPES = {
     "hs_trainer_grads_ptr": C.c_void_p,
     "hs_trainer_slab_send_ptr": C.c_void_p,
     "hs_trainer_slab_recv_ptr": C.c_void_p,
+    "hs_trainer_slab_recv2_ptr": C.c_void_p,
+    "hs_trainer_slab_flags_ptr": C.c_void_p,
     "hs_trainer_param_count": C.c_int64,
     "hs_trainer_step_count": C.c_int,
     "hs_ctx_destroy": None,

@@ -437,16 +437,59 @@ __global__ void __launch_bounds__(256) chunk_copy_kernel(const float2* __restric
         const int64_t so = m.sA[a] + b * m.sB[a] + t * m.sT[a];
         const int64_t dof = m.dA[a] + b * m.dB[a] + t * m.dT[a];
         const int64_t len = m.len[a];
+        float2* out = m.dptr[a] ? m.dptr[a] : dst;  // a peer's buffer: the stores travel over NVLink
         if (((so | dof | len) & 1) == 0) {
             const float4* s4 = reinterpret_cast<const float4*>(src + so);
-            float4* d4 = reinterpret_cast<float4*>(dst + dof);
+            float4* d4 = reinterpret_cast<float4*>(out + dof);
             for (int64_t i = lane; i < len / 2; i += 32) d4[i] = s4[i];
         } else {
-            for (int64_t i = lane; i < len; i += 32) dst[dof + i] = src[so + i];
+            for (int64_t i = lane; i < len; i += 32) out[dof + i] = src[so + i];
         }
     }
 }
+struct PeerFlags {
+    uint32_t* f[kMaxPeers];
+};
+
+__global__ void slab_signal_kernel(PeerFlags pf, int ranks, int me, uint32_t epoch) {
+    const int a = threadIdx.x;
+    if (a >= ranks) return;
+    // every store of the preceding pack kernel (stream order) is made visible
+    // system-wide before the flag
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(pf.f[a] + me), "r"(epoch) : "memory");
+}
+
+__global__ void slab_wait_kernel(const uint32_t* flags, int ranks, uint32_t epoch, uint32_t* error) {
+    const int a = threadIdx.x;
+    if (a < ranks) {
+        const long long t0 = clock64();
+        uint32_t v = 0;
+        for (;;) {
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + a) : "memory");
+            if (static_cast<int32_t>(v - epoch) >= 0) break;
+            if (clock64() - t0 > 4000000000LL) {  // ~2 s at 1.97 GHz: a peer never signalled
+                atomicExch(error, 1u);
+                break;
+            }
+            __nanosleep(64);
+        }
+    }
+    __syncthreads();
+}
 }  // namespace
+
+void slab_signal(uint32_t* const* peer_flags, int ranks, int me, uint32_t epoch, cudaStream_t st) {
+    PeerFlags pf{};
+    for (int a = 0; a < ranks; ++a) pf.f[a] = peer_flags[a];
+    slab_signal_kernel<<<1, 32, 0, st>>>(pf, ranks, me, epoch);
+    launch_check("slab_signal");
+}
+
+void slab_wait(const uint32_t* flags, int ranks, uint32_t epoch, uint32_t* error, cudaStream_t st) {
+    slab_wait_kernel<<<1, 32, 0, st>>>(flags, ranks, epoch, error);
+    launch_check("slab_wait");
+}
 
 void chunk_copy(const float2* src, float2* dst, const ChunkMap& m, cudaStream_t st) {
     require(m.A >= 1 && m.A <= kMaxPeers, "slab exchange: peer count outside 1..16");

@@ -104,12 +104,21 @@ void asm_cols_pass(AsmWork& w, bool backward, const float2* in, float2* out, int
 // b < B (plane), t < T (tile), copies len[a] float2 from
 // src[sA[a] + b sB[a] + t sT[a]] to dst[dA[a] + b dB[a] + t dT[a]].
 constexpr int kMaxPeers = 16;
+// dptr[a] (optional): destination base for peer a (a peer's receive buffer
+// mapped into this context: same device, P2P or CUDA IPC), else dst.
 struct ChunkMap {
     int A = 0, B = 0, T = 0;
     int64_t len[kMaxPeers], sA[kMaxPeers], sB[kMaxPeers], sT[kMaxPeers], dA[kMaxPeers], dB[kMaxPeers],
         dT[kMaxPeers];
+    float2* dptr[kMaxPeers] = {};
 };
 void chunk_copy(const float2* src, float2* dst, const ChunkMap& m, cudaStream_t st);
+// Exchange flags of the peer-put transposes: signal writes `epoch` into slot
+// `me` of every peer's flag array (system-scope release after a fence); wait
+// spins (acquire) until every slot of this rank's flags reaches `epoch`, and
+// gives up after ~2 s with error[0] = 1 (no hang when a peer died).
+void slab_signal(uint32_t* const* peer_flags, int ranks, int me, uint32_t epoch, cudaStream_t st);
+void slab_wait(const uint32_t* flags, int ranks, uint32_t epoch, uint32_t* error, cudaStream_t st);
 
 // Static (compile-time planned) propagation path; false when (Px, Py) has no plan.
 bool static_plan_cc(int Px, int Py, int pad, int L, int* cc);

@@ -548,10 +548,8 @@ size_t cols_smem_persist(const Plans& p, int H) {
 // them (KT tiles per CTA), else one CTA per (tile, channel).
 void launch_cols(const Plans* p, const AsmWork& w, bool backward, const ColArgs& c, cudaStream_t st) {
     if (w.L == 1 && p->col.fwdP && persist_on()) {
-        int dev = 0;
         const int total = c.ntiles * c.C;
         const int grid = (total + kPersistTiles - 1) / kPersistTiles;
-        (void)dev;
         (backward ? p->col.bwdP : p->col.fwdP)<<<grid, p->col.nt1, cols_smem_persist(*p, w.H), st>>>(c, w.stw_y);
     } else {
         const size_t cs = cols_smem(*p, w.L);

@@ -103,6 +103,15 @@ struct hs_trainer {
     DevBuf s_planes, s_dplanes, s_target, s_tstats, s_masks, s_T, s_send, s_recv;
     ChunkMap m_pack[4], m_unpack[4];
     int64_t s_counts[4][2 * kMaxPeers] = {};
+    // peer-put exchange (hs_trainer_slab_set_peers): the pack kernels store
+    // straight into the peers' receive buffers (double-buffered by exchange
+    // parity), then signal the peers' flag arrays; the next stage waits on
+    // this rank's flags.  No NCCL call on the data path.
+    bool s_put = false;
+    float2* s_peer_recv[2][kMaxPeers] = {};
+    uint32_t* s_peer_flags[kMaxPeers] = {};
+    DevBuf s_recv2, s_flags;  // flags: [0, R) per-source epochs, [kMaxPeers] error word
+    uint32_t s_epoch = 0;
     int s_loss_slots = 0;
     ~hs_trainer() {
         if (graph) cudaGraphExecDestroy(graph);
@@ -953,6 +962,11 @@ extern "C" hs_status hs_trainer_set_row_slab(hs_trainer* t, int rank, int ranks)
         t->s_T.reserve(sizeof(float2) * LC * tiled);
         t->s_send.reserve(sizeof(float2) * LC * tiled);
         t->s_recv.reserve(sizeof(float2) * LC * tiled);
+        t->s_recv2.reserve(sizeof(float2) * LC * tiled);
+        t->s_flags.reserve(sizeof(uint32_t) * (kMaxPeers + 1));
+        HS_CUDA(cudaMemsetAsync(t->s_flags.p, 0, sizeof(uint32_t) * (kMaxPeers + 1), st));
+        t->s_epoch = 0;
+        t->s_put = false;
         // loss-band slices of the target and the masks, and the band's target window stats
         HS_CUDA(cudaMemcpy2DAsync(t->s_target.p, band * sizeof(float), t->target.as<float>() + static_cast<size_t>(t->g0) * W,
                                   static_cast<size_t>(t->h) * W * sizeof(float), band * sizeof(float), C,
@@ -977,6 +991,53 @@ extern "C" hs_status hs_trainer_slab_counts(hs_trainer* t, int exchange, int64_t
 
 extern "C" float* hs_trainer_slab_send_ptr(hs_trainer* t) { return t->s_send.as<float>(); }
 extern "C" float* hs_trainer_slab_recv_ptr(hs_trainer* t) { return t->s_recv.as<float>(); }
+extern "C" float* hs_trainer_slab_recv2_ptr(hs_trainer* t) { return t->s_recv2.as<float>(); }
+extern "C" uint32_t* hs_trainer_slab_flags_ptr(hs_trainer* t) { return t->s_flags.as<uint32_t>(); }
+
+extern "C" hs_status hs_trainer_slab_set_peers(hs_trainer* t, float* const* recv0, float* const* recv1,
+                                               uint32_t* const* flags) {
+    return guard([&] {
+        require(t->R >= 1, "row slab: trainer is not row-slab sharded");
+        require(recv0 && recv1 && flags, "row slab: peer pointer arrays missing");
+        for (int a = 0; a < t->R; ++a) {
+            require(recv0[a] && recv1[a] && flags[a], "row slab: null peer pointer");
+            t->s_peer_recv[0][a] = reinterpret_cast<float2*>(recv0[a]);
+            t->s_peer_recv[1][a] = reinterpret_cast<float2*>(recv1[a]);
+            t->s_peer_flags[a] = flags[a];
+        }
+        t->s_put = true;
+    });
+}
+
+extern "C" hs_status hs_trainer_slab_status(hs_trainer* t, uint32_t* error) {
+    return guard([&] {
+        require(t->R >= 1, "row slab: trainer is not row-slab sharded");
+        HS_CUDA(cudaMemcpyAsync(error, t->s_flags.as<uint32_t>() + kMaxPeers, sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                                t->ctx->stream));
+        HS_CUDA(cudaStreamSynchronize(t->ctx->stream));
+    });
+}
+
+extern "C" hs_status hs_ipc_get_handle(const void* d_ptr, void* handle64) {
+    return guard([&] {
+        static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+        cudaIpcMemHandle_t h;
+        HS_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr)));
+        std::memcpy(handle64, &h, sizeof(h));
+    });
+}
+
+extern "C" hs_status hs_ipc_open_handle(const void* handle64, void** d_ptr) {
+    return guard([&] {
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle64, sizeof(h));
+        HS_CUDA(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    });
+}
+
+extern "C" hs_status hs_ipc_close(void* d_ptr) {
+    return guard([&] { HS_CUDA(cudaIpcCloseMemHandle(d_ptr)); });
+}
 
 // Stage k (0..4) of a row-slab step; between stage k and k+1 the caller runs
 // all-to-all exchange k (send buffer -> peers' receive buffers, counts from
@@ -991,19 +1052,39 @@ extern "C" hs_status hs_trainer_slab_stage(hs_trainer* t, int stage) {
         AsmWork& aw = t->aw;
         const int C = t->c, LC = t->L * t->c;
         float2* send = t->s_send.as<float2>();
-        const float2* recv = t->s_recv.as<float2>();
+        // exchange k = stage - 1 arrives in the receive buffer of its parity (put
+        // mode; the NCCL path always receives into the first buffer)
+        const float2* recv = (t->s_put && ((stage - 1) & 1)) ? t->s_recv2.as<float2>() : t->s_recv.as<float2>();
+        if (t->s_put && stage >= 1 && stage <= 4)
+            slab_wait(t->s_flags.as<uint32_t>(), t->R, t->s_epoch, t->s_flags.as<uint32_t>() + kMaxPeers, st);
+        // pack of exchange k: into the send buffer (NCCL), or straight into the
+        // peers' receive buffers at this rank's slot followed by the flag signal
+        auto pack = [&](int k, const float2* src) {
+            if (!t->s_put) {
+                chunk_copy(src, send, t->m_pack[k], st);
+                return;
+            }
+            ChunkMap m = t->m_pack[k];
+            for (int a = 0; a < t->R; ++a) {
+                m.dptr[a] = t->s_peer_recv[k & 1][a];
+                m.dA[a] = static_cast<int64_t>(t->rank) * (t->s_counts[k][a] / 2);
+            }
+            chunk_copy(src, nullptr, m, st);
+            t->s_epoch += 1;
+            slab_signal(t->s_peer_flags, t->R, t->rank, t->s_epoch, st);
+        };
         switch (stage) {
             case 0:  // binning (replicated), raster forward of the own rows, row FFTs, pack
                 HS_CUDA(cudaMemsetAsync(t->flags.p, 0, sizeof(uint32_t), st));
                 t->rw.project_and_bin(t->params.as<float>(), st);
                 raster_forward(t->rw, t->field.as<float2>(), st, t->h0, t->hr);
                 asm_rows_pass(aw, false, t->field.as<float2>(), aw.T1.as<float2>(), C, t->hr, st);
-                chunk_copy(aw.T1.as<float2>(), send, t->m_pack[0], st);
+                pack(0, aw.T1.as<float2>());
                 break;
             case 1:  // column FFT x H_l + column IFFT on the own tiles, pack loss bands
                 chunk_copy(recv, aw.T1.as<float2>(), t->m_unpack[0], st);
                 asm_cols_pass(aw, false, aw.T1.as<float2>(), aw.T2.as<float2>(), t->rank * t->ts, t->ts, st);
-                chunk_copy(aw.T2.as<float2>(), send, t->m_pack[1], st);
+                pack(1, aw.T2.as<float2>());
                 break;
             case 2: {  // row IFFTs of the loss band, loss + dU, backward row FFTs, pack own rows
                 chunk_copy(recv, t->s_T.as<float2>(), t->m_unpack[1], st);
@@ -1017,13 +1098,13 @@ extern "C" hs_status hs_trainer_slab_stage(hs_trainer* t, int stage) {
                 const int used = loss_launch(a, st);
                 loss_finalize(a, used, t->out3.as<double>(), st);
                 asm_rows_pass(aw, false, t->s_dplanes.as<float2>(), t->s_T.as<float2>(), LC, t->He, st);
-                chunk_copy(t->s_T.as<float2>(), send, t->m_pack[2], st);
+                pack(2, t->s_T.as<float2>());
                 break;
             }
             case 3:  // adjoint column pass on the own tiles, pack
                 chunk_copy(recv, aw.T2.as<float2>(), t->m_unpack[2], st);
                 asm_cols_pass(aw, true, aw.T2.as<float2>(), aw.T1.as<float2>(), t->rank * t->ts, t->ts, st);
-                chunk_copy(aw.T1.as<float2>(), send, t->m_pack[3], st);
+                pack(3, aw.T1.as<float2>());
                 break;
             case 4:  // row IFFTs of the own rows, raster backward over the own rows
                 chunk_copy(recv, aw.T2.as<float2>(), t->m_unpack[3], st);

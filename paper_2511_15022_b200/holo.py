@@ -898,6 +898,40 @@ class Trainer:
         ctx_handle()
         check(_lib.load().hs_trainer_slab_stage(self.h, int(stage)))
 
+    def slab_peer_buffers(self):
+        """Device addresses (recv0, recv1, flags) a peer stores into in the peer-put exchange."""
+        lib = _lib.load()
+        return (int(lib.hs_trainer_slab_recv_ptr(self.h)), int(lib.hs_trainer_slab_recv2_ptr(self.h)),
+                int(lib.hs_trainer_slab_flags_ptr(self.h)))
+
+    def slab_set_peers(self, recv0, recv1, flags):
+        """Peer-put exchange: per-rank device addresses valid in this context (same
+        device, P2P or CUDA IPC mapped); this rank's own entries are its own buffers."""
+        R = self.slab[1]
+        arr = lambda v: (C.c_void_p * R)(*[C.c_void_p(int(x)) for x in v])
+        self._peer_arrays = (arr(recv0), arr(recv1), arr(flags))
+        check(_lib.load().hs_trainer_slab_set_peers(self.h, *self._peer_arrays))
+
+    def slab_status(self) -> int:
+        v = C.c_uint32(0)
+        check(_lib.load().hs_trainer_slab_status(self.h, C.byref(v)))
+        return int(v.value)
+
+
+def ipc_handle(d_ptr: int) -> bytes:
+    """cudaIpcGetMemHandle of a device allocation (64 bytes)."""
+    buf = C.create_string_buffer(64)
+    check(_lib.load().hs_ipc_get_handle(C.c_void_p(int(d_ptr)), buf))
+    return buf.raw
+
+
+def ipc_open(handle: bytes) -> int:
+    """cudaIpcOpenMemHandle (lazy peer access): the peer allocation mapped here."""
+    p = C.c_void_p()
+    buf = C.create_string_buffer(bytes(handle), 64)
+    check(_lib.load().hs_ipc_open_handle(buf, C.byref(p)))
+    return int(p.value)
+
 
 def _wrap(owner, ptr, count) -> torch.Tensor:
     """torch view over trainer-owned device memory (kept alive by owner)."""

@@ -147,19 +147,51 @@ def loss_band(H: int, rank: int, world: int, halo: int = 10) -> Tuple[int, int]:
 
 class SlabShardedStep:
     """One optimisation step of a row-slab sharded trainer (cfg4): five
-    stages with an NCCL all-to-all between them (hs_trainer_slab_stage), then
+    stages with a transpose exchange between them (hs_trainer_slab_stage), then
     the gradient all-reduce and the replicated Adan update.
 
     `trainer` is a holo.Trainer on which set_row_slab(rank, world) was called.
+    exchange="nccl": all_to_all_single on the peer-major send/receive buffers.
+    exchange="put": the pack kernels store straight into the peers' receive
+    buffers (CUDA IPC mappings of every peer's buffers, NVLink stores from the
+    SMs) and signal device flags; the next stage's first kernel waits on them.
+    No collective library call on the transpose data path.
     """
 
-    def __init__(self, trainer, C, H, W, L, group=None):
+    def __init__(self, trainer, C, H, W, L, group=None, exchange="nccl"):
         self.tr = trainer
         self.C, self.H, self.W, self.L = C, H, W, L
         self.group = group
         self.counts = [trainer.slab_counts(e) for e in range(4)]
+        self.put = exchange == "put"
+        self._mapped = []
+        if self.put:
+            self._map_peers()
+
+    def _map_peers(self):
+        from . import holo
+        rank, world = self.tr.slab
+        mine = self.tr.slab_peer_buffers()
+        if world == 1:
+            self.tr.slab_set_peers([mine[0]], [mine[1]], [mine[2]])
+            return
+        handles = [None] * world
+        dist.all_gather_object(handles, [holo.ipc_handle(p) for p in mine], group=self.group)
+        cols = [[], [], []]
+        for r, hs in enumerate(handles):
+            for k in range(3):
+                if r == rank:
+                    cols[k].append(mine[k])
+                else:
+                    p = holo.ipc_open(hs[k])
+                    self._mapped.append(p)
+                    cols[k].append(p)
+        self.tr.slab_set_peers(*cols)
+        dist.barrier(group=self.group)
 
     def _exchange(self, e):
+        if self.put:
+            return  # the pack kernel already stored into the peers and signalled
         send, recv = self.tr.slab_buffers()
         sc, rc = self.counts[e]
         if dist.is_initialized() and dist.get_world_size(self.group) > 1:
@@ -178,6 +210,8 @@ class SlabShardedStep:
             dist.all_reduce(g, op=dist.ReduceOp.SUM, group=self.group)
         self.tr.apply_update()
         parts = torch.tensor(self.tr.loss_partials(), dtype=torch.float64, device=g.device)
+        if self.put and self.tr.slab_status():
+            raise RuntimeError("row slab: a peer-put exchange timed out waiting for a peer")
         if multi:
             dist.all_reduce(parts, op=dist.ReduceOp.SUM, group=self.group)
         return combine_loss(float(parts[0]), float(parts[1]), self.C, self.H, self.W, self.L)
@@ -187,14 +221,24 @@ class LocalSlabGroup:
     """R row-slab trainers on ONE device, stepped in lock-step with the
     all-to-all and the all-reduce done as device copies: the single-GPU
     check that the R-rank decomposition reproduces the unsharded step
-    (tests and bench; a real run uses SlabShardedStep, one rank per GPU)."""
+    (tests and bench; a real run uses SlabShardedStep, one rank per GPU).
+    put=True runs the peer-put exchange instead (the pack kernels store into
+    the other trainers' receive buffers and signal their device flags), the
+    same kernels a multi-GPU run uses over NVLink."""
 
-    def __init__(self, trainers, C, H, W, L):
+    def __init__(self, trainers, C, H, W, L, put=False):
         self.trs = list(trainers)
         self.C, self.H, self.W, self.L = C, H, W, L
         self.counts = [[t.slab_counts(e) for e in range(4)] for t in self.trs]
+        self.put = put
+        if put:
+            bufs = [t.slab_peer_buffers() for t in self.trs]
+            for t in self.trs:
+                t.slab_set_peers([b[0] for b in bufs], [b[1] for b in bufs], [b[2] for b in bufs])
 
     def _exchange(self, e):
+        if self.put:
+            return
         R = len(self.trs)
         for r, tr in enumerate(self.trs):
             recv = tr.slab_buffers()[1]
@@ -222,6 +266,8 @@ class LocalSlabGroup:
         for t in self.trs:
             t.apply_update()
         parts = [t.loss_partials() for t in self.trs]
+        if self.put and any(t.slab_status() for t in self.trs):
+            raise RuntimeError("row slab: a peer-put exchange timed out waiting for a peer")
         return combine_loss(sum(p[0] for p in parts), sum(p[1] for p in parts), self.C, self.H, self.W, self.L)
 
 

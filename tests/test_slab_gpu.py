@@ -32,7 +32,7 @@ def scene(holo, n, c, w, h, L, seed=42):
     return gs, target, masks, dist, spec
 
 
-def run(holo, R, n, c, w, h, L, steps):
+def run(holo, R, n, c, w, h, L, steps, put=False):
     from paper_2511_15022_b200 import parallel as P
     gs, target, masks, dist, spec = scene(holo, n, c, w, h, L)
     full = holo.Trainer(gs, w, h, target, masks, dist, spec, 20)
@@ -41,7 +41,7 @@ def run(holo, R, n, c, w, h, L, steps):
         t = holo.Trainer(gs, w, h, target, masks, dist, spec, 20)
         t.set_row_slab(r, R)
         trs.append(t)
-    grp = P.LocalSlabGroup(trs, c, h, w, L)
+    grp = P.LocalSlabGroup(trs, c, h, w, L, put=put)
     out = []
     for s in range(steps):
         full.forward_backward()
@@ -71,6 +71,30 @@ def test_slab_step_matches_unsharded(holo, R, n, c, w, h, L):
     for p in ps:  # every rank applied the same update
         assert np.array_equal(p, ps[0])
     assert rel_l2(ps[0], pf) < 1e-6
+
+
+@pytest.mark.parametrize("R,n,c,w,h,L", [
+    (1, 400, 3, 64, 48, 1),
+    (2, 400, 3, 64, 48, 2),
+    (4, 800, 2, 96, 64, 3),
+])
+def test_slab_step_peer_put_matches_unsharded(holo, R, n, c, w, h, L):
+    """Peer-put exchange: the pack kernels store into the other ranks' receive
+    buffers and signal their device flags (no copy or collective between the
+    stages); same results as the unsharded step."""
+    out, pf, ps = run(holo, R, n, c, w, h, L, steps=3, put=True)
+    for lf, ls, gerr in out:
+        assert ls == pytest.approx(lf, rel=2e-6), (lf, ls)
+        assert gerr < 1e-5, gerr
+    assert rel_l2(ps[0], pf) < 1e-6
+
+
+def test_slab_step_peer_put_cfg4(holo):
+    out, pf, ps = run(holo, 8, 1_000_000, 3, 3840, 2160, 1, steps=2, put=True)
+    for lf, ls, gerr in out:
+        assert ls == pytest.approx(lf, rel=2e-6), (lf, ls)
+        assert gerr < 1e-5, gerr
+    assert rel_l2(ps[5], pf) < 1e-6
 
 
 @pytest.mark.parametrize("R", [2, 4])
