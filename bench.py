@@ -46,6 +46,9 @@ def parse():
                    help="cfg5: scenes this rank actually runs (a bounded sample of its share; 0 = all)")
     p.add_argument("--train-steps", type=int, default=2000, help="cfg5: optimisation steps per scene")
     p.add_argument("--poh-steps", type=int, default=600, help="cfg5: random-POH conversion steps per scene")
+    p.add_argument("--exchange", choices=("nccl", "put"), default="put",
+                   help="--shard slabs: transposes as NCCL all_to_all_single, or as peer-put stores into "
+                        "the peers' IPC-mapped receive buffers with device-flag synchronisation")
     p.add_argument("--virtual-ranks", type=int, default=0,
                    help="--shard slabs on ONE GPU: R slab trainers stepped in lock-step with the "
                         "all-to-alls done as device copies (parallel.LocalSlabGroup); reports the "
@@ -211,7 +214,8 @@ def config_of(name, cfg, world, shard="replicas"):
     par = {"replicas": f"replicas x{world} (one scene per GPU, no collective)",
            "channels": f"wavelength shards x{world} (one scene; NCCL all-reduce of the 6N geometry gradients)",
            "planes": f"plane shards x{world} (one scene; NCCL all-reduce of the gradient buffer)",
-           "slabs": f"row slabs x{world} (one scene; 4 NCCL all-to-all FFT transposes + gradient all-reduce)",
+           "slabs": f"row slabs x{world} (one scene; 4 FFT transposes as peer-put NVLink stores or NCCL "
+                    "all-to-all + gradient all-reduce)",
            }[shard]
     seed = "init_gaussians(seed 42+rank)" if shard == "replicas" else "init_gaussians(seed 42)"
     return {"workload": f"{name}: {cfg['width']}x{cfg['height']} x{cfg['channels']} wavelengths, "
@@ -263,10 +267,10 @@ def run_sharded(args):
             if args.virtual_ranks > 1 and world == 1:
                 trs = [mk(r, args.virtual_ranks) for r in range(args.virtual_ranks)]
                 tr = trs[0]
-                step = P.LocalSlabGroup(trs, C_, h, w, L)
+                step = P.LocalSlabGroup(trs, C_, h, w, L, put=args.exchange == "put")
             else:
                 tr = mk(rank, world)
-                step = P.SlabShardedStep(tr, C_, h, w, L)
+                step = P.SlabShardedStep(tr, C_, h, w, L, exchange=args.exchange)
         else:
             tr = holo.Trainer(holo.GaussianSet(n, C_, **g32), w, h,
                               holo.RealField(C_, h, w, wl["target"].astype(np.float32).astype(np.float64)),
