@@ -4,7 +4,7 @@ import csv, io, json, subprocess, sys
 
 SLOTS = {  # kernel-name fragment -> bench.py stage slots it serves
     "raster_bwd_kernel": ["raster_bwd"], "raster_fwd_kernel": ["raster_fwd"],
-    "ssim_loss_kernel": ["loss_ssim"], "cols_fwd1": ["cols_fwd"], "cols_bwd1": ["cols_bwd"],
+    "ssim_loss_kernel": ["loss_ssim"], "pcols_fwd": ["cols_fwd"], "pcols_bwd": ["cols_bwd"],
     "srows_fwd": ["rows_fwd", "rows_fwd_bwd"], "srows_inv": ["rows_inv", "rows_inv_bwd"],
 }
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
