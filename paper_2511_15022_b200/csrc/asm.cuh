@@ -118,6 +118,20 @@ void chunk_copy(const float2* src, float2* dst, const ChunkMap& m, cudaStream_t 
 // spins (acquire) until every slot of this rank's flags reaches `epoch`, and
 // gives up after ~2 s with error[0] = 1 (no hang when a peer died).
 void slab_signal(uint32_t* const* peer_flags, int ranks, int me, uint32_t epoch, cudaStream_t st);
+
+// Row FFT whose last stage stores straight into the peers' receive buffers
+// (row-slab peer-put exchange fused into the compute kernel): the output
+// column tile T belongs to rank s = T / ts; only rows [row0, row0 + hout) of
+// each plane are sent, to peer[s] + slot[s] + ((plane ts + T - s ts) hout +
+// y - row0) CC + cc.  Returns false when the grid has no planned row kernel
+// (the caller then runs asm_rows_pass + a pack).
+struct SlabPut {
+    float2* peer[kMaxPeers];
+    int64_t slot[kMaxPeers];
+    int ts, row0, hout;
+    unsigned ts_magic;  // ceil(2^32 / ts)
+};
+bool asm_rows_fwd_put(AsmWork& w, const float2* in, int planes, int h, const SlabPut& sp, cudaStream_t st);
 void slab_wait(const uint32_t* flags, int ranks, uint32_t epoch, uint32_t* error, cudaStream_t st);
 
 // Static (compile-time planned) propagation path; false when (Px, Py) has no plan.

@@ -81,6 +81,33 @@ __global__ void __launch_bounds__(NT) srows_fwd_kernel(RowArgs a, int nrows, con
         }));
 }
 
+// Forward row pass with the peer-put epilogue (SlabPut, asm.cuh).
+template <int N, int RB, int NT, int CCO, class RAD>
+__global__ void __launch_bounds__(NT) srows_fwd_put_kernel(RowArgs a, int nrows, const float2* __restrict__ tw,
+                                                           SlabPut sp) {
+    static_assert(NT % RB == 0, "row of a thread must be fixed");
+    extern __shared__ float2 smem[];
+    const int tid = threadIdx.x;
+    const int rho = blockIdx.x * RB + tid % RB;
+    const int pc = rho / a.H, y = rho - pc * a.H;
+    const int yo = y - sp.row0;
+    const bool ok = rho < nrows, send = ok && yo >= 0 && yo < sp.hout;
+    const float2* src = a.in + static_cast<size_t>(rho) * a.W - a.ox;  // src[i], i in [ox, ox + W)
+    const size_t plane_rows = static_cast<size_t>(pc) * sp.ts;
+    sfft::run<N, RB, NT, -1, sfft::Half, sfft::Full>(
+        smem, tw, tid, RAD{},
+        sfft::in_fn([&](int i, int) { return ok ? src[i] : make_float2(0.f, 0.f); }),
+        sfft::out_fn([&](int i, int, float2 v) {
+            if (!send) return;
+            const unsigned T = static_cast<unsigned>(i / CCO);
+            unsigned r = __umulhi(T, sp.ts_magic);  // T / ts, corrected below
+            if (r * sp.ts > T) --r;
+            else if ((r + 1) * sp.ts <= T) ++r;
+            const size_t tl = T - r * sp.ts;
+            sp.peer[r][sp.slot[r] + ((plane_rows + tl) * sp.hout + yo) * CCO + (i % CCO)] = v;
+        }));
+}
+
 template <int N, int RB, int NT, int CCO, class RAD>
 __global__ void __launch_bounds__(NT) srows_inv_kernel(RowArgs a, int nrows, const float2* __restrict__ tw) {
     static_assert(NT % RB == 0, "row of a thread must be fixed");
@@ -419,6 +446,7 @@ struct RowPlan {
     void (*inv)(RowArgs, int, const float2*);
     int nt, rb;
     std::vector<float2> (*table)(int);
+    void (*fwd_put)(RowArgs, int, const float2*, SlabPut) = nullptr;
 };
 struct ColPlan {
     void (*fwd)(ColArgs, const float2*);
@@ -436,7 +464,7 @@ struct ColPlan {
 template <int N, int RB, int NT, int CCO, class RAD>
 RowPlan row_plan() {
     return RowPlan{srows_fwd_kernel<N, RB, NT, CCO, RAD>, srows_inv_kernel<N, RB, NT, CCO, RAD>, NT, RB,
-                   [](int n) { return sfft::twiddle_table(n, RAD{}); }};
+                   [](int n) { return sfft::twiddle_table(n, RAD{}); }, srows_fwd_put_kernel<N, RB, NT, CCO, RAD>};
 }
 // Column-pair SIMD single-plane kernels (CC = 4), standard multi-plane kernels.
 template <int N, int NT1, int MINB1, int NTL, class RAD>
@@ -579,6 +607,8 @@ void static_prepare(AsmWork& w) {
     const size_t rs = rows_smem(*p), cs = cols_smem(*p, w.L);
     HS_CUDA(cudaFuncSetAttribute(p->row.fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rs)));
     HS_CUDA(cudaFuncSetAttribute(p->row.inv, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rs)));
+    if (p->row.fwd_put)
+        HS_CUDA(cudaFuncSetAttribute(p->row.fwd_put, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rs)));
     for (auto k : {p->col.fwd, p->col.bwd, p->col.fwdL, p->col.bwdL})
         HS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cs)));
     if (p->col.fwdP) {
@@ -654,6 +684,18 @@ bool static_cols_pass(AsmWork& w, bool backward, const float2* in, float2* out, 
     ColArgs c{in, out, w.C, w.H, w.Py, w.Px, w.oy, ntiles_local, w.L, w.plan_y, nullptr, w.tf.as<TfConst>()};
     c.tile0 = tile0;
     launch_cols(p, w, backward, c, st);
+    return true;
+}
+
+bool asm_rows_fwd_put(AsmWork& w, const float2* in, int planes, int h, const SlabPut& sp, cudaStream_t st) {
+    if (!w.use_static) return false;
+    const Plans* p = find(w.Px, w.Py);
+    if (!p || p->cc != w.CC || !p->row.fwd_put) return false;
+    const int rows = planes * h;
+    if (rows == 0) return true;
+    RowArgs r{in, nullptr, w.W, h, w.Px, w.ox, w.ntiles, 1.f, w.plan_x, nullptr};
+    p->row.fwd_put<<<(rows + p->row.rb - 1) / p->row.rb, p->row.nt, rows_smem(*p), st>>>(r, rows, w.stw_x, sp);
+    launch_check("srows_fwd_put");
     return true;
 }
 

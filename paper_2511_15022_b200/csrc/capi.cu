@@ -1073,13 +1073,33 @@ extern "C" hs_status hs_trainer_slab_stage(hs_trainer* t, int stage) {
             t->s_epoch += 1;
             slab_signal(t->s_peer_flags, t->R, t->rank, t->s_epoch, st);
         };
+        // row FFTs whose last stage stores straight into the peers (put mode,
+        // planned grids): the compute kernel IS the exchange; else rows + pack
+        auto rows_put = [&](int k, const float2* in, int planes, int h, int row0) {
+            if (!t->s_put) return false;
+            SlabPut sp{};
+            for (int a = 0; a < t->R; ++a) {
+                sp.peer[a] = t->s_peer_recv[k & 1][a];
+                sp.slot[a] = static_cast<int64_t>(t->rank) * (t->s_counts[k][a] / 2);
+            }
+            sp.ts = t->ts;
+            sp.row0 = row0;
+            sp.hout = t->hr;
+            sp.ts_magic = static_cast<unsigned>((0x100000000ull + t->ts - 1) / t->ts);
+            if (!asm_rows_fwd_put(aw, in, planes, h, sp, st)) return false;
+            t->s_epoch += 1;
+            slab_signal(t->s_peer_flags, t->R, t->rank, t->s_epoch, st);
+            return true;
+        };
         switch (stage) {
             case 0:  // binning (replicated), raster forward of the own rows, row FFTs, pack
                 HS_CUDA(cudaMemsetAsync(t->flags.p, 0, sizeof(uint32_t), st));
                 t->rw.project_and_bin(t->params.as<float>(), st);
                 raster_forward(t->rw, t->field.as<float2>(), st, t->h0, t->hr);
-                asm_rows_pass(aw, false, t->field.as<float2>(), aw.T1.as<float2>(), C, t->hr, st);
-                pack(0, aw.T1.as<float2>());
+                if (!rows_put(0, t->field.as<float2>(), C, t->hr, 0)) {
+                    asm_rows_pass(aw, false, t->field.as<float2>(), aw.T1.as<float2>(), C, t->hr, st);
+                    pack(0, aw.T1.as<float2>());
+                }
                 break;
             case 1:  // column FFT x H_l + column IFFT on the own tiles, pack loss bands
                 chunk_copy(recv, aw.T1.as<float2>(), t->m_unpack[0], st);
@@ -1097,8 +1117,10 @@ extern "C" hs_status hs_trainer_slab_stage(hs_trainer* t, int stage) {
                 a.own1 = t->top + t->hr;
                 const int used = loss_launch(a, st);
                 loss_finalize(a, used, t->out3.as<double>(), st);
-                asm_rows_pass(aw, false, t->s_dplanes.as<float2>(), t->s_T.as<float2>(), LC, t->He, st);
-                pack(2, t->s_T.as<float2>());
+                if (!rows_put(2, t->s_dplanes.as<float2>(), LC, t->He, t->top)) {
+                    asm_rows_pass(aw, false, t->s_dplanes.as<float2>(), t->s_T.as<float2>(), LC, t->He, st);
+                    pack(2, t->s_T.as<float2>());
+                }
                 break;
             }
             case 3:  // adjoint column pass on the own tiles, pack
