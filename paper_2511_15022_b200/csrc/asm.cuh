@@ -132,6 +132,16 @@ struct SlabPut {
     unsigned ts_magic;  // ceil(2^32 / ts)
 };
 bool asm_rows_fwd_put(AsmWork& w, const float2* in, int planes, int h, const SlabPut& sp, cudaStream_t st);
+// Inverse row pass reading its column tiles straight from a peer-major
+// receive buffer [src s][planes][ts][h][CC] (tile T = s ts + tl), i.e. the
+// exchange's unpack fused into the load; false without a planned row kernel.
+struct SlabGet {
+    int ts;
+    unsigned ts_magic;  // ceil(2^32 / ts)
+    int64_t per_src;    // float2 per source segment = planes ts h CC
+};
+bool asm_rows_inv_get(AsmWork& w, const float2* recv, float2* out, int planes, int h, const SlabGet& sg,
+                      cudaStream_t st);
 void slab_wait(const uint32_t* flags, int ranks, uint32_t epoch, uint32_t* error, cudaStream_t st);
 
 // Static (compile-time planned) propagation path; false when (Px, Py) has no plan.

@@ -81,6 +81,35 @@ __global__ void __launch_bounds__(NT) srows_fwd_kernel(RowArgs a, int nrows, con
         }));
 }
 
+// Inverse row pass gathering from the peer-major receive layout (SlabGet, asm.cuh).
+template <int N, int RB, int NT, int CCO, class RAD>
+__global__ void __launch_bounds__(NT) srows_inv_get_kernel(RowArgs a, int nrows, const float2* __restrict__ tw,
+                                                           SlabGet sg) {
+    static_assert(NT % RB == 0, "row of a thread must be fixed");
+    extern __shared__ float2 smem[];
+    const int tid = threadIdx.x;
+    const int rho = blockIdx.x * RB + tid % RB;
+    const bool ok = rho < nrows;
+    const int pc = rho / a.H, y = rho - pc * a.H;
+    const float2* src = a.in + (static_cast<size_t>(pc) * sg.ts * a.H + y) * CCO;
+    const size_t tile_stride = static_cast<size_t>(a.H) * CCO;
+    float2* dst = a.out + static_cast<size_t>(rho) * a.W - a.ox;  // dst[i], i in [ox, ox + W)
+    const float sc = a.scale;
+    sfft::run<N, RB, NT, +1, sfft::Full, sfft::Half>(
+        smem, tw, tid, RAD{},
+        sfft::in_fn([&](int i, int) {
+            if (!ok) return make_float2(0.f, 0.f);
+            const unsigned T = static_cast<unsigned>(i / CCO);
+            unsigned r = __umulhi(T, sg.ts_magic);  // T / ts, corrected below
+            if (r * sg.ts > T) --r;
+            else if ((r + 1) * sg.ts <= T) ++r;
+            return src[r * sg.per_src + (T - r * sg.ts) * tile_stride + (i % CCO)];
+        }),
+        sfft::out_fn([&](int i, int, float2 v) {
+            if (ok) dst[i] = make_float2(v.x * sc, v.y * sc);
+        }));
+}
+
 // Forward row pass with the peer-put epilogue (SlabPut, asm.cuh).
 template <int N, int RB, int NT, int CCO, class RAD>
 __global__ void __launch_bounds__(NT) srows_fwd_put_kernel(RowArgs a, int nrows, const float2* __restrict__ tw,
@@ -447,6 +476,7 @@ struct RowPlan {
     int nt, rb;
     std::vector<float2> (*table)(int);
     void (*fwd_put)(RowArgs, int, const float2*, SlabPut) = nullptr;
+    void (*inv_get)(RowArgs, int, const float2*, SlabGet) = nullptr;
 };
 struct ColPlan {
     void (*fwd)(ColArgs, const float2*);
@@ -464,7 +494,8 @@ struct ColPlan {
 template <int N, int RB, int NT, int CCO, class RAD>
 RowPlan row_plan() {
     return RowPlan{srows_fwd_kernel<N, RB, NT, CCO, RAD>, srows_inv_kernel<N, RB, NT, CCO, RAD>, NT, RB,
-                   [](int n) { return sfft::twiddle_table(n, RAD{}); }, srows_fwd_put_kernel<N, RB, NT, CCO, RAD>};
+                   [](int n) { return sfft::twiddle_table(n, RAD{}); }, srows_fwd_put_kernel<N, RB, NT, CCO, RAD>,
+                   srows_inv_get_kernel<N, RB, NT, CCO, RAD>};
 }
 // Column-pair SIMD single-plane kernels (CC = 4), standard multi-plane kernels.
 template <int N, int NT1, int MINB1, int NTL, class RAD>
@@ -609,6 +640,8 @@ void static_prepare(AsmWork& w) {
     HS_CUDA(cudaFuncSetAttribute(p->row.inv, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rs)));
     if (p->row.fwd_put)
         HS_CUDA(cudaFuncSetAttribute(p->row.fwd_put, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rs)));
+    if (p->row.inv_get)
+        HS_CUDA(cudaFuncSetAttribute(p->row.inv_get, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rs)));
     for (auto k : {p->col.fwd, p->col.bwd, p->col.fwdL, p->col.bwdL})
         HS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cs)));
     if (p->col.fwdP) {
@@ -696,6 +729,20 @@ bool asm_rows_fwd_put(AsmWork& w, const float2* in, int planes, int h, const Sla
     RowArgs r{in, nullptr, w.W, h, w.Px, w.ox, w.ntiles, 1.f, w.plan_x, nullptr};
     p->row.fwd_put<<<(rows + p->row.rb - 1) / p->row.rb, p->row.nt, rows_smem(*p), st>>>(r, rows, w.stw_x, sp);
     launch_check("srows_fwd_put");
+    return true;
+}
+
+bool asm_rows_inv_get(AsmWork& w, const float2* recv, float2* out, int planes, int h, const SlabGet& sg,
+                      cudaStream_t st) {
+    if (!w.use_static) return false;
+    const Plans* p = find(w.Px, w.Py);
+    if (!p || p->cc != w.CC || !p->row.inv_get) return false;
+    const int rows = planes * h;
+    if (rows == 0) return true;
+    RowArgs r{recv, out, w.W, h, w.Px, w.ox, w.ntiles, static_cast<float>(1.0 / (static_cast<double>(w.Px) * w.Py)),
+              w.plan_x, nullptr};
+    p->row.inv_get<<<(rows + p->row.rb - 1) / p->row.rb, p->row.nt, rows_smem(*p), st>>>(r, rows, w.stw_x, sg);
+    launch_check("srows_inv_get");
     return true;
 }
 

@@ -1091,6 +1091,15 @@ extern "C" hs_status hs_trainer_slab_stage(hs_trainer* t, int stage) {
             slab_signal(t->s_peer_flags, t->R, t->rank, t->s_epoch, st);
             return true;
         };
+        // inverse row FFTs gathering straight from the peer-major receive
+        // buffer (the unpack fused into the loads; planned grids)
+        auto rows_get = [&](int k, float2* out, int planes, int h) {
+            SlabGet sg{};
+            sg.ts = t->ts;
+            sg.ts_magic = static_cast<unsigned>((0x100000000ull + t->ts - 1) / t->ts);
+            sg.per_src = t->s_counts[k][t->R] / 2;  // receive count from source 0 (all sources equal)
+            return asm_rows_inv_get(aw, recv, out, planes, h, sg, st);
+        };
         switch (stage) {
             case 0:  // binning (replicated), raster forward of the own rows, row FFTs, pack
                 HS_CUDA(cudaMemsetAsync(t->flags.p, 0, sizeof(uint32_t), st));
@@ -1107,8 +1116,10 @@ extern "C" hs_status hs_trainer_slab_stage(hs_trainer* t, int stage) {
                 pack(1, aw.T2.as<float2>());
                 break;
             case 2: {  // row IFFTs of the loss band, loss + dU, backward row FFTs, pack own rows
-                chunk_copy(recv, t->s_T.as<float2>(), t->m_unpack[1], st);
-                asm_rows_pass(aw, true, t->s_T.as<float2>(), t->s_planes.as<float2>(), LC, t->He, st);
+                if (!rows_get(1, t->s_planes.as<float2>(), LC, t->He)) {
+                    chunk_copy(recv, t->s_T.as<float2>(), t->m_unpack[1], st);
+                    asm_rows_pass(aw, true, t->s_T.as<float2>(), t->s_planes.as<float2>(), LC, t->He, st);
+                }
                 LossArgs a{kLossTraining, t->L, t->L_total, 0, C, t->He, t->w, nullptr, t->s_planes.as<float2>(),
                            t->s_target.as<float>(), t->s_tstats.as<float2>(), t->s_masks.as<uint8_t>(), nullptr,
                            t->s_dplanes.as<float2>(), t->partials.as<double>(), t->C_total};
@@ -1129,8 +1140,10 @@ extern "C" hs_status hs_trainer_slab_stage(hs_trainer* t, int stage) {
                 pack(3, aw.T1.as<float2>());
                 break;
             case 4:  // row IFFTs of the own rows, raster backward over the own rows
-                chunk_copy(recv, aw.T2.as<float2>(), t->m_unpack[3], st);
-                asm_rows_pass(aw, true, aw.T2.as<float2>(), t->back.as<float2>(), C, t->hr, st);
+                if (!rows_get(3, t->back.as<float2>(), C, t->hr)) {
+                    chunk_copy(recv, aw.T2.as<float2>(), t->m_unpack[3], st);
+                    asm_rows_pass(aw, true, aw.T2.as<float2>(), t->back.as<float2>(), C, t->hr, st);
+                }
                 raster_backward(t->rw, t->params.as<float>(), t->back.as<float2>(), t->grads.as<float>(),
                                 t->flags.as<uint32_t>(), st, t->h0, t->hr);
                 break;
