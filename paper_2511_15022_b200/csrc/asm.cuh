@@ -142,6 +142,24 @@ struct SlabGet {
 };
 bool asm_rows_inv_get(AsmWork& w, const float2* recv, float2* out, int planes, int h, const SlabGet& sg,
                       cudaStream_t st);
+// Column pass of a row-slab rank (single plane, planned grids): each tile's
+// H rows are gathered from the R source segments of the peer-major receive
+// buffer by R TMA bulk copies (the unpack fused into the load), and the
+// cropped output rows are either stored to the local T layout (out) or put
+// straight into every peer whose row band [g0[d], g0[d] + he[d]) holds them
+// (peer[d] + slot[d] + ((plane ts + tl) he[d] + y - g0[d]) CC + cc).
+struct SlabCol {
+    const float2* in;
+    int64_t per_src;
+    int R, hr;
+    float inv_hr;
+    int put;
+    float2* peer[kMaxPeers];
+    int64_t slot[kMaxPeers];
+    int g0[kMaxPeers], he[kMaxPeers];
+};
+bool asm_cols_slab(AsmWork& w, bool backward, const SlabCol& sc, float2* out, int tile0, int ntiles_local,
+                   cudaStream_t st);
 void slab_wait(const uint32_t* flags, int ranks, uint32_t epoch, uint32_t* error, cudaStream_t st);
 
 // Static (compile-time planned) propagation path; false when (Px, Py) has no plan.

@@ -384,6 +384,80 @@ __device__ __forceinline__ void pcol_persist(const ColArgs& a, const float2* __r
     }
 }
 
+// ---- row-slab column kernel: segment gather in, peer put (or local) out ----
+__device__ __forceinline__ void bulk_expect(uint64_t* bar, unsigned bytes) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+template <int N, int NT, int MINB, bool CONJ, class RAD>
+__global__ void __launch_bounds__(NT, MINB) pcols_slab_kernel(ColArgs a, const float2* __restrict__ tw, SlabCol sc) {
+    constexpr int CC = 4, NP = 2;
+    extern __shared__ float4 smem4[];
+    float4* work = smem4;
+    const int H = a.H, oy = a.oy, ts = a.ntiles;
+    float4* stage_buf = smem4 + pfft::padded_len4(N * NP);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(stage_buf + H * NP);
+    const int t = blockIdx.x;            // flat tile over (channel, own tile)
+    const int c = t / ts, tl = t - c * ts;
+    const int tid = threadIdx.x, pp = tid % NP;
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        const unsigned seg = static_cast<unsigned>(sc.hr * CC * sizeof(float2));
+        bulk_expect(bar, seg * sc.R);
+        for (int r = 0; r < sc.R; ++r)  // source r's rows [r hr, (r + 1) hr) of this tile
+            bulk_copy(stage_buf + r * sc.hr * NP, sc.in + r * sc.per_src + static_cast<size_t>(t) * sc.hr * CC, seg, bar);
+    }
+    __syncthreads();
+    const TfConst tf = a.tf[c];
+    PairTf ptf;
+    ptf.mx0 = wrapped((a.tile0 + tl) * CC + 2 * pp, a.Px);
+    ptf.mx1 = wrapped((a.tile0 + tl) * CC + 2 * pp + 1, a.Px);
+    {
+        const float f0 = static_cast<float>(ptf.mx0), f1 = static_cast<float>(ptf.mx1);
+        ptf.qx = make_float2(tf.bx * f0 * f0, tf.bx * f1 * f1);
+        ptf.inband = make_float2(abs(ptf.mx0) <= tf.mx_max ? 1.f : 0.f, abs(ptf.mx1) <= tf.mx_max ? 1.f : 0.f);
+    }
+    mbar_wait(bar, 0u);
+    const float4* stg = stage_buf - oy * NP;
+    pfft::run<N, NP, NT, -1, pfft::Half, pfft::Full>(
+        work, tw, tid, RAD{},
+        pfft::in_fn([stg](int i, int p) {
+            const float4 q = stg[i * NP + p];
+            return pfft::C2{make_float2(q.x, q.z), make_float2(q.y, q.w)};
+        }),
+        pfft::out_map([tf, ptf](int i, int, pfft::C2 v) {
+            float2 hc, hs;
+            transfer_pair<CONJ>(tf, ptf, wrapped(i, N), hc, hs);
+            return pfft::C2{f2sub(f2mul(v.re, hc), f2mul(v.im, hs)), f2fma(v.im, hc, f2mul(v.re, hs))};
+        }));
+    float2* lout = a.out + static_cast<size_t>(t) * H * CC;
+    const size_t plane_tiles = static_cast<size_t>(c) * ts + tl;
+    pfft::run<N, NP, NT, +1, pfft::Full, pfft::Half>(
+        work, tw, tid, RAD{}, pfft::InSmem{},
+        pfft::out_fn([&](int i, int p, pfft::C2 v) {
+            const float4 q = make_float4(v.re.x, v.im.x, v.re.y, v.im.y);
+            const int y = i - oy;
+            if (!sc.put) {
+                *reinterpret_cast<float4*>(lout + static_cast<size_t>(y) * CC + 2 * p) = q;
+                return;
+            }
+            const int d0 = __float2int_rz(static_cast<float>(y) * sc.inv_hr);
+#pragma unroll
+            for (int dd = -1; dd <= 1; ++dd) {
+                const int d = d0 + dd;
+                if (d < 0 || d >= sc.R) continue;
+                const int yl = y - sc.g0[d];
+                if (yl < 0 || yl >= sc.he[d]) continue;
+                *reinterpret_cast<float4*>(sc.peer[d] + sc.slot[d] + (plane_tiles * sc.he[d] + yl) * CC + 2 * p) = q;
+            }
+        }));
+}
+
 template <int N, int NT, int MINB, class RAD>
 __global__ void __launch_bounds__(NT, MINB) pcols_fwdP_kernel(ColArgs a, const float2* __restrict__ tw) {
     pcol_persist<N, NT, false, RAD, kPersistTiles>(a, tw);
@@ -487,6 +561,8 @@ struct ColPlan {
     std::vector<float2> (*table)(int);
     int nt1 = 0;        // threads of the single-plane kernels (0: nt)
     bool pair = false;  // single-plane kernels use the column-pair SIMD engine (float4 smem)
+    void (*fwdS)(ColArgs, const float2*, SlabCol) = nullptr;  // row-slab column kernels
+    void (*bwdS)(ColArgs, const float2*, SlabCol) = nullptr;
     void (*fwdP)(ColArgs, const float2*) = nullptr;  // bulk-copy staged single-plane kernels
     void (*bwdP)(ColArgs, const float2*) = nullptr;
 };
@@ -507,6 +583,8 @@ ColPlan pcol_plan() {
     p.pair = true;
     p.fwdP = pcols_fwdP_kernel<N, NT1, MINB1, RAD>;
     p.bwdP = pcols_bwdP_kernel<N, NT1, MINB1, RAD>;
+    p.fwdS = pcols_slab_kernel<N, NT1, MINB1, false, RAD>;
+    p.bwdS = pcols_slab_kernel<N, NT1, MINB1, true, RAD>;
     return p;
 }
 
@@ -650,6 +728,10 @@ void static_prepare(AsmWork& w) {
             HS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, csp));
             HS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         }
+        for (auto k : {p->col.fwdS, p->col.bwdS}) {
+            HS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, csp));
+            HS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        }
     }
 }
 
@@ -743,6 +825,20 @@ bool asm_rows_inv_get(AsmWork& w, const float2* recv, float2* out, int planes, i
               w.plan_x, nullptr};
     p->row.inv_get<<<(rows + p->row.rb - 1) / p->row.rb, p->row.nt, rows_smem(*p), st>>>(r, rows, w.stw_x, sg);
     launch_check("srows_inv_get");
+    return true;
+}
+
+bool asm_cols_slab(AsmWork& w, bool backward, const SlabCol& sc, float2* out, int tile0, int ntiles_local,
+                   cudaStream_t st) {
+    if (!w.use_static || w.L != 1) return false;
+    const Plans* p = find(w.Px, w.Py);
+    if (!p || p->cc != w.CC || !p->col.fwdS) return false;
+    if (w.H % sc.R != 0 || sc.hr * sc.R != w.H) return false;
+    ColArgs c{nullptr, out, w.C, w.H, w.Py, w.Px, w.oy, ntiles_local, w.L, w.plan_y, nullptr, w.tf.as<TfConst>()};
+    c.tile0 = tile0;
+    (backward ? p->col.bwdS : p->col.fwdS)<<<ntiles_local * w.C, p->col.nt1, cols_smem_persist(*p, w.H), st>>>(
+        c, w.stw_y, sc);
+    launch_check(backward ? "scols_bwd_slab" : "scols_fwd_slab");
     return true;
 }
 

@@ -1100,6 +1100,32 @@ extern "C" hs_status hs_trainer_slab_stage(hs_trainer* t, int stage) {
             sg.per_src = t->s_counts[k][t->R] / 2;  // receive count from source 0 (all sources equal)
             return asm_rows_inv_get(aw, recv, out, planes, h, sg, st);
         };
+        // column pass gathering its tiles from the receive buffer of exchange
+        // ki (R bulk copies) and putting its rows into the peers for exchange
+        // ko (put mode) or into the local T layout (then packed)
+        auto cols_slab = [&](bool backward, int ki, int ko, float2* local_out) {
+            SlabCol sc{};
+            sc.in = recv;
+            sc.per_src = t->s_counts[ki][t->R] / 2;
+            sc.R = t->R;
+            sc.hr = t->hr;
+            sc.inv_hr = 1.f / static_cast<float>(t->hr);
+            sc.put = t->s_put ? 1 : 0;
+            for (int a = 0; a < t->R; ++a) {
+                sc.peer[a] = t->s_peer_recv[ko & 1][a];
+                sc.slot[a] = static_cast<int64_t>(t->rank) * (t->s_counts[ko][a] / 2);
+                sc.g0[a] = ko == 1 ? t->g0_of[a] : a * t->hr;
+                sc.he[a] = ko == 1 ? t->He_of[a] : t->hr;
+            }
+            if (!asm_cols_slab(aw, backward, sc, local_out, t->rank * t->ts, t->ts, st)) return false;
+            if (t->s_put) {
+                t->s_epoch += 1;
+                slab_signal(t->s_peer_flags, t->R, t->rank, t->s_epoch, st);
+            } else {
+                chunk_copy(local_out, send, t->m_pack[ko], st);
+            }
+            return true;
+        };
         switch (stage) {
             case 0:  // binning (replicated), raster forward of the own rows, row FFTs, pack
                 HS_CUDA(cudaMemsetAsync(t->flags.p, 0, sizeof(uint32_t), st));
@@ -1111,9 +1137,11 @@ extern "C" hs_status hs_trainer_slab_stage(hs_trainer* t, int stage) {
                 }
                 break;
             case 1:  // column FFT x H_l + column IFFT on the own tiles, pack loss bands
-                chunk_copy(recv, aw.T1.as<float2>(), t->m_unpack[0], st);
-                asm_cols_pass(aw, false, aw.T1.as<float2>(), aw.T2.as<float2>(), t->rank * t->ts, t->ts, st);
-                pack(1, aw.T2.as<float2>());
+                if (!cols_slab(false, 0, 1, aw.T2.as<float2>())) {
+                    chunk_copy(recv, aw.T1.as<float2>(), t->m_unpack[0], st);
+                    asm_cols_pass(aw, false, aw.T1.as<float2>(), aw.T2.as<float2>(), t->rank * t->ts, t->ts, st);
+                    pack(1, aw.T2.as<float2>());
+                }
                 break;
             case 2: {  // row IFFTs of the loss band, loss + dU, backward row FFTs, pack own rows
                 if (!rows_get(1, t->s_planes.as<float2>(), LC, t->He)) {
@@ -1135,9 +1163,11 @@ extern "C" hs_status hs_trainer_slab_stage(hs_trainer* t, int stage) {
                 break;
             }
             case 3:  // adjoint column pass on the own tiles, pack
-                chunk_copy(recv, aw.T2.as<float2>(), t->m_unpack[2], st);
-                asm_cols_pass(aw, true, aw.T2.as<float2>(), aw.T1.as<float2>(), t->rank * t->ts, t->ts, st);
-                pack(3, aw.T1.as<float2>());
+                if (!cols_slab(true, 2, 3, aw.T1.as<float2>())) {
+                    chunk_copy(recv, aw.T2.as<float2>(), t->m_unpack[2], st);
+                    asm_cols_pass(aw, true, aw.T2.as<float2>(), aw.T1.as<float2>(), t->rank * t->ts, t->ts, st);
+                    pack(3, aw.T1.as<float2>());
+                }
                 break;
             case 4:  // row IFFTs of the own rows, raster backward over the own rows
                 if (!rows_get(3, t->back.as<float2>(), C, t->hr)) {

@@ -97,10 +97,12 @@ def test_slab_step_peer_put_cfg4(holo):
     assert rel_l2(ps[5], pf) < 1e-6
 
 
-@pytest.mark.parametrize("R", [2, 4])
-def test_slab_step_cfg2_grid(holo, R):
-    """1080p RGB on the compile-time planned 3840x2160 FFT (CC 4 column tiles)."""
-    out, pf, ps = run(holo, R, 200_000, 3, 1920, 1080, 1, steps=2)
+@pytest.mark.parametrize("R,put", [(2, False), (4, False), (4, True), (8, True)])
+def test_slab_step_cfg2_grid(holo, R, put):
+    """1080p RGB on the compile-time planned 3840x2160 FFT (CC 4 column tiles):
+    the fused slab kernels (row FFT -> peers, column pass gathering its tiles by
+    TMA bulk copies from the receive buffer, rows -> peers)."""
+    out, pf, ps = run(holo, R, 200_000, 3, 1920, 1080, 1, steps=2, put=put)
     for lf, ls, gerr in out:
         assert ls == pytest.approx(lf, rel=2e-6), (lf, ls)
         assert gerr < 1e-5, gerr
