@@ -5,6 +5,7 @@
 #include <limits>
 #include <cstring>
 #include <memory>
+#include <random>
 #include <string>
 #include <vector>
 
@@ -1015,6 +1016,18 @@ extern "C" hs_status hs_trainer_slab_status(hs_trainer* t, uint32_t* error) {
         HS_CUDA(cudaMemcpyAsync(error, t->s_flags.as<uint32_t>() + kMaxPeers, sizeof(uint32_t), cudaMemcpyDeviceToHost,
                                 t->ctx->stream));
         HS_CUDA(cudaStreamSynchronize(t->ctx->stream));
+    });
+}
+
+// holo::Rng(seed).uniform(lo, hi) x n (rng.hpp: std::mt19937_64, 53-bit
+// mapping), on the host: the initial random-POH phase raster of the reference
+// (convert.cpp:88) without a Python-speed generator.
+extern "C" hs_status hs_random_uniform(uint64_t seed, int64_t n, double lo, double hi, double* h_out) {
+    return guard([&] {
+        require(n >= 0 && h_out != nullptr, "random_uniform: bad arguments");
+        std::mt19937_64 eng(seed);
+        for (int64_t i = 0; i < n; ++i)
+            h_out[i] = lo + (hi - lo) * (static_cast<double>(eng() >> 11) * 0x1.0p-53);
     });
 }
 

@@ -518,9 +518,12 @@ class RandomPohResult:
 
 
 def random_phase(seed: int, n: int) -> np.ndarray:
-    """Rng(seed).uniform(-pi, pi) in element order (rng.hpp: mt19937_64, 53-bit)."""
-    from .synthetic import Rng
-    return -math.pi + TWO_PI * Rng(seed).uniform(n)
+    """Rng(seed).uniform(-pi, pi) in element order (rng.hpp: mt19937_64, 53-bit),
+    drawn by std::mt19937_64 in the native library (hs_random_uniform)."""
+    out = np.empty(int(n), dtype=np.float64)
+    check(_lib.load().hs_random_uniform(C.c_uint64(int(seed) & 0xFFFFFFFFFFFFFFFF), C.c_int64(int(n)), -math.pi,
+                                        math.pi, out.ctypes.data_as(C.c_void_p)))
+    return out
 
 
 def convert_random_poh_field(guide_field: ComplexField, planes, target: "TargetStack", spec: PropagationSpec,

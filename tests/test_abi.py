@@ -70,3 +70,14 @@ def test_cxx_dropin_headers_declare_reference_api():
                 "ComplexField propagate_multi_backward(", "double training_loss_grad(",
                 "double cosine_lr(int", "class Adan"):
         assert sig in text, sig
+
+
+def test_random_uniform_matches_reference_rng():
+    """hs_random_uniform (std::mt19937_64, rng.hpp's 53-bit mapping) draws the
+    same sequence as the numpy restatement of holo::Rng used for the inputs."""
+    import math
+    from paper_2511_15022_b200 import holo, synthetic as S
+    for seed in (0, 7, 42, 2**63 + 5):
+        a = holo.random_phase(seed, 4097)
+        b = -math.pi + 2.0 * math.pi * S.Rng(seed).uniform(4097)
+        assert np.array_equal(a, b), seed
