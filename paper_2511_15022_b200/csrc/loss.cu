@@ -615,12 +615,6 @@ __global__ void adan_fused_kernel(float* __restrict__ p, const float* __restrict
     }
 }
 
-__global__ void adan_advance_kernel(int* step, const uint32_t* flags) {
-    if (flags && *flags) return;  // the reference aborts on a non-finite gradient
-    step[0] += 1;
-    step[1] += 1;
-}
-
 __global__ void adan_group_kernel(float* __restrict__ p, const float* __restrict__ g,
                                   float* __restrict__ st, int64_t P, int t, GroupConst k, float b1,
                                   float b2, float b3, float eps) {
