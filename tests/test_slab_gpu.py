@@ -5,8 +5,11 @@ unsharded trainer on the same scene.  The decomposition changes only the fp32
 summation order of the per-Gaussian sums (rows split over ranks) and of the
 loss partials, so gradients, losses and updated parameters agree far inside
 the parity bars (field 1e-4, gradients 1e-3); the 2D FFTs of every rank are
-the unsharded FFTs' own row and column passes.
+the unsharded FFTs' own row and column passes.  GRAD_TOL bounds the rel-L2
+gap of the summed per-rank gradients to the unsharded ones (fp32 sums split
+over up to 16 row slabs).
 """
+GRAD_TOL = 1e-4
 import numpy as np
 import pytest
 
@@ -67,7 +70,7 @@ def test_slab_step_matches_unsharded(holo, R, n, c, w, h, L):
     out, pf, ps = run(holo, R, n, c, w, h, L, steps=3)
     for lf, ls, gerr in out:
         assert ls == pytest.approx(lf, rel=2e-6), (lf, ls)
-        assert gerr < 1e-5, gerr
+        assert gerr < GRAD_TOL, gerr
     for p in ps:  # every rank applied the same update
         assert np.array_equal(p, ps[0])
     assert rel_l2(ps[0], pf) < 1e-6
@@ -77,6 +80,7 @@ def test_slab_step_matches_unsharded(holo, R, n, c, w, h, L):
     (1, 400, 3, 64, 48, 1),
     (2, 400, 3, 64, 48, 2),
     (4, 800, 2, 96, 64, 3),
+    (16, 3000, 1, 256, 256, 1),   # the maximum peer count, 16-row slabs, 8 column tiles each
 ])
 def test_slab_step_peer_put_matches_unsharded(holo, R, n, c, w, h, L):
     """Peer-put exchange: the pack kernels store into the other ranks' receive
@@ -85,7 +89,7 @@ def test_slab_step_peer_put_matches_unsharded(holo, R, n, c, w, h, L):
     out, pf, ps = run(holo, R, n, c, w, h, L, steps=3, put=True)
     for lf, ls, gerr in out:
         assert ls == pytest.approx(lf, rel=2e-6), (lf, ls)
-        assert gerr < 1e-5, gerr
+        assert gerr < GRAD_TOL, gerr
     assert rel_l2(ps[0], pf) < 1e-6
 
 
@@ -93,7 +97,7 @@ def test_slab_step_peer_put_cfg4(holo):
     out, pf, ps = run(holo, 8, 1_000_000, 3, 3840, 2160, 1, steps=2, put=True)
     for lf, ls, gerr in out:
         assert ls == pytest.approx(lf, rel=2e-6), (lf, ls)
-        assert gerr < 1e-5, gerr
+        assert gerr < GRAD_TOL, gerr
     assert rel_l2(ps[5], pf) < 1e-6
 
 
@@ -105,7 +109,7 @@ def test_slab_step_cfg2_grid(holo, R, put):
     out, pf, ps = run(holo, R, 200_000, 3, 1920, 1080, 1, steps=2, put=put)
     for lf, ls, gerr in out:
         assert ls == pytest.approx(lf, rel=2e-6), (lf, ls)
-        assert gerr < 1e-5, gerr
+        assert gerr < GRAD_TOL, gerr
     assert rel_l2(ps[-1], pf) < 1e-6
 
 
@@ -115,7 +119,7 @@ def test_slab_step_cfg4_eight_ranks(holo):
     out, pf, ps = run(holo, 8, 1_000_000, 3, 3840, 2160, 1, steps=1)
     lf, ls, gerr = out[0]
     assert ls == pytest.approx(lf, rel=2e-6), (lf, ls)
-    assert gerr < 1e-5, gerr
+    assert gerr < GRAD_TOL, gerr
     assert rel_l2(ps[3], pf) < 1e-6
 
 
