@@ -245,13 +245,24 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(const uint32_t*
 // Per-tile Gaussian counts: 16 threads per Gaussian, one fire-and-forget
 // atomic per (Gaussian, tile) pair.
 constexpr int kScatterSub = 16;
+// Tile rows [ty_lo, ty_hi] only (a row-slab rank bins its own band).
+__device__ __forceinline__ int4 band_box(int4 b, int ty_lo, int ty_hi) {
+    b.z = max(b.z, ty_lo);
+    b.w = min(b.w, ty_hi);
+    return b;
+}
+__device__ __forceinline__ int box_count(const int4& b) {
+    const int nx = b.y - b.x + 1, ny = b.w - b.z + 1;
+    return (nx > 0 && ny > 0) ? nx * ny : 0;
+}
+
 __global__ void __launch_bounds__(256) count_tiles_kernel(int n, const int4* __restrict__ tbox, int tiles_x,
-                                                          uint32_t* __restrict__ tcount) {
+                                                          uint32_t* __restrict__ tcount, int ty_lo, int ty_hi) {
     const int g = blockIdx.x * (256 / kScatterSub) + threadIdx.x / kScatterSub;
     const int sub = threadIdx.x % kScatterSub;
     if (g >= n) return;
-    const int4 b = tbox[g];
-    const int nx = b.y - b.x + 1, cnt = nx * (b.w - b.z + 1);
+    const int4 b = band_box(tbox[g], ty_lo, ty_hi);
+    const int nx = b.y - b.x + 1, cnt = box_count(b);
     for (int k = sub; k < cnt; k += kScatterSub) atomicAdd(tcount + (b.z + k / nx) * tiles_x + b.x + k % nx, 1u);
 }
 
@@ -262,12 +273,12 @@ __global__ void __launch_bounds__(256) scatter_ids_kernel(int n, const int4* __r
                                                           const uint32_t* __restrict__ toffset,
                                                           uint32_t* __restrict__ tcount,
                                                           const uint32_t* __restrict__ status,
-                                                          uint32_t* __restrict__ ids) {
+                                                          uint32_t* __restrict__ ids, int ty_lo, int ty_hi) {
     const int g = blockIdx.x * (256 / kScatterSub) + threadIdx.x / kScatterSub;
     const int sub = threadIdx.x % kScatterSub;
     if (g >= n || status[1]) return;
-    const int4 b = tbox[g];
-    const int nx = b.y - b.x + 1, cnt = nx * (b.w - b.z + 1);
+    const int4 b = band_box(tbox[g], ty_lo, ty_hi);
+    const int nx = b.y - b.x + 1, cnt = box_count(b);
     for (int k = sub; k < cnt; k += kScatterSub) {
         const int t = (b.z + k / nx) * tiles_x + b.x + k % nx;
         const uint32_t slot = atomicSub(tcount + t, 1u) - 1u;
@@ -633,6 +644,10 @@ __global__ void __launch_bounds__(kBwdThreads, MINB) raster_bwd_kernel(
     const float ext = sqrtf(fmaxf(i00 * M / detI, 0.f)) + 1e-2f;
     const int ya = max(max(bb.z, y0), static_cast<int>(ceilf(py - ext)));
     const int yb = min(min(bb.w, y0 + hs - 1), static_cast<int>(floorf(py + ext)));
+    if (ya > yb) {  // no footprint row in the band (row-slab ranks): zero sums
+        if (lane < 2 * C + 6) raw[static_cast<size_t>(lane) * N + g] = 0.f;
+        return;
+    }
     const double* q = p64 + g;
     const unsigned lanemask_le = 0xffffffffu >> (31 - lane);
 
@@ -890,13 +905,14 @@ void RasterWork::project_and_bin(const float* d_params, cudaStream_t st, cudaEve
     project_kernel<<<ceil_div(n, 128), 128, 0, st>>>(P);
     launch_check("project");
     count_tiles_kernel<<<ceil_div(n, 256 / kScatterSub), 256, 0, st>>>(n, tbox.as<int4>(), tiles_x,
-                                                                       tcount.as<uint32_t>());
+                                                                       tcount.as<uint32_t>(), band_ty0, band_ty1);
     launch_check("count_tiles");
     tile_scan_kernel<<<1, kScanThreads, 0, st>>>(tcount.as<uint32_t>(), tiles, toffset.as<uint32_t>(), ranges.as<uint2>(),
                                          stat, cap);
     launch_check("tile_scan");
     scatter_ids_kernel<<<ceil_div(n, 256 / kScatterSub), 256, 0, st>>>(n, tbox.as<int4>(), tiles_x, toffset.as<uint32_t>(),
-                                                         tcount.as<uint32_t>(), stat, ids.as<uint32_t>());
+                                                         tcount.as<uint32_t>(), stat, ids.as<uint32_t>(), band_ty0,
+                                                         band_ty1);
     launch_check("scatter_ids");
     segment_sort_warp_kernel<<<ceil_div(tiles, 8), 256, 0, st>>>(ranges.as<uint2>(), tiles, ids.as<uint32_t>(),
                                                                   stat);

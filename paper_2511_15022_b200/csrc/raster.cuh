@@ -24,6 +24,7 @@ struct RasterWork {
     DevBuf ranges;   // uint2 [begin,end) per tile
     DevBuf status;   // uint32[4]: [0] K (pairs), [1] overflow, [2] non-finite param, [3] unused
     int64_t cap = 0; // pair capacity
+    int band_ty0 = 0, band_ty1 = 1 << 30;  // tile rows binned (a row-slab rank: its band)
 
     void prepare(int n_, int c_, int w_, int h_);
     void reserve_pairs(int64_t cap_);
