@@ -644,10 +644,6 @@ __global__ void __launch_bounds__(kBwdThreads, MINB) raster_bwd_kernel(
     const float ext = sqrtf(fmaxf(i00 * M / detI, 0.f)) + 1e-2f;
     const int ya = max(max(bb.z, y0), static_cast<int>(ceilf(py - ext)));
     const int yb = min(min(bb.w, y0 + hs - 1), static_cast<int>(floorf(py + ext)));
-    if (ya > yb) {  // no footprint row in the band (row-slab ranks): zero sums
-        if (lane < 2 * C + 6) raw[static_cast<size_t>(lane) * N + g] = 0.f;
-        return;
-    }
     const double* q = p64 + g;
     const unsigned lanemask_le = 0xffffffffu >> (31 - lane);
 
