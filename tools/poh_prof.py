@@ -1,3 +1,5 @@
+"""Wall time of the device-resident random-POH loop (hs_convert_random_poh_field) at the
+cfg5 grid for two step counts: the difference is the per-step cost.  usage: python tools/poh_prof.py [steps]"""
 import sys, os, time
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch, ctypes as C
