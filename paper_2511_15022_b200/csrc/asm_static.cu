@@ -458,6 +458,58 @@ __global__ void __launch_bounds__(NT, MINB) pcols_slab_kernel(ColArgs a, const f
         }));
 }
 
+// Row-slab column kernel on the scalar engine (plans without the pair engine,
+// e.g. the 4K CC 2 plan): the same segment gather in (R TMA bulk copies) and
+// peer put (or local) out as pcols_slab_kernel.
+template <int N, int CC, int NT, int MINB, bool CONJ, class RAD>
+__global__ void __launch_bounds__(NT, MINB) scols_slab_kernel(ColArgs a, const float2* __restrict__ tw, SlabCol sc) {
+    static_assert(NT % CC == 0, "column of a thread must be fixed");
+    extern __shared__ float2 smem[];
+    float2* work = smem;
+    const int H = a.H, oy = a.oy, ts = a.ntiles;
+    float2* stage_buf = smem + fft::padded_len(N * CC);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(stage_buf + H * CC);
+    const int t = blockIdx.x;  // flat tile over (channel, own tile)
+    const int c = t / ts, tl = t - c * ts;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        const unsigned seg = static_cast<unsigned>(sc.hr * CC * sizeof(float2));
+        bulk_expect(bar, seg * sc.R);
+        for (int r = 0; r < sc.R; ++r)
+            bulk_copy(stage_buf + r * sc.hr * CC, sc.in + r * sc.per_src + static_cast<size_t>(t) * sc.hr * CC, seg, bar);
+    }
+    __syncthreads();
+    const TfConst tf = a.tf[c];
+    const int mx = wrapped((a.tile0 + tl) * CC + tid % CC, a.Px);
+    mbar_wait(bar, 0u);
+    const float2* stg = stage_buf - oy * CC;
+    sfft::run<N, CC, NT, -1, sfft::Half, sfft::Full>(
+        work, tw, tid, RAD{}, sfft::in_fn([&](int i, int cc) { return stg[i * CC + cc]; }),
+        sfft::out_smem(work, [&](int i, int, float2 v, float2& slot) {
+            slot = cmul(v, transfer_fast<CONJ>(tf, mx, wrapped(i, N)));
+        }));
+    float2* lout = a.out + static_cast<size_t>(t) * H * CC;
+    const size_t plane_tiles = static_cast<size_t>(c) * ts + tl;
+    sfft::run<N, CC, NT, +1, sfft::Full, sfft::Half>(
+        work, tw, tid, RAD{}, sfft::in_smem(work), sfft::out_fn([&](int i, int cc, float2 v) {
+            const int y = i - oy;
+            if (!sc.put) {
+                lout[static_cast<size_t>(y) * CC + cc] = v;
+                return;
+            }
+            const int d0 = __float2int_rz(static_cast<float>(y) * sc.inv_hr);
+#pragma unroll
+            for (int dd = -1; dd <= 1; ++dd) {
+                const int d = d0 + dd;
+                if (d < 0 || d >= sc.R) continue;
+                const int yl = y - sc.g0[d];
+                if (yl < 0 || yl >= sc.he[d]) continue;
+                sc.peer[d][sc.slot[d] + (plane_tiles * sc.he[d] + yl) * CC + cc] = v;
+            }
+        }));
+}
+
 template <int N, int NT, int MINB, class RAD>
 __global__ void __launch_bounds__(NT, MINB) pcols_fwdP_kernel(ColArgs a, const float2* __restrict__ tw) {
     pcol_persist<N, NT, false, RAD, kPersistTiles>(a, tw);
@@ -592,9 +644,12 @@ ColPlan pcol_plan() {
 // so they run one CTA per SM regardless of MINB: they get the full register file.
 template <int N, int CC, int NT, int MINB, class RAD>
 ColPlan col_plan() {
-    return ColPlan{scols_fwd1_kernel<N, CC, NT, MINB, RAD>, scols_bwd1_kernel<N, CC, NT, MINB, RAD>,
-                   scols_fwdL_kernel<N, CC, NT, 1, RAD>, scols_bwdL_kernel<N, CC, NT, 1, RAD>, NT, CC,
-                   [](int n) { return sfft::twiddle_table(n, RAD{}); }};
+    ColPlan p{scols_fwd1_kernel<N, CC, NT, MINB, RAD>, scols_bwd1_kernel<N, CC, NT, MINB, RAD>,
+              scols_fwdL_kernel<N, CC, NT, 1, RAD>, scols_bwdL_kernel<N, CC, NT, 1, RAD>, NT, CC,
+              [](int n) { return sfft::twiddle_table(n, RAD{}); }};
+    p.fwdS = scols_slab_kernel<N, CC, NT, MINB, false, RAD>;
+    p.bwdS = scols_slab_kernel<N, CC, NT, MINB, true, RAD>;
+    return p;
 }
 
 struct Plans {
@@ -728,8 +783,11 @@ void static_prepare(AsmWork& w) {
             HS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, csp));
             HS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         }
+    }
+    if (p->col.fwdS && cols_smem_persist(*p, w.H) <= 227 * 1024) {
+        const int css = static_cast<int>(cols_smem_persist(*p, w.H));
         for (auto k : {p->col.fwdS, p->col.bwdS}) {
-            HS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, csp));
+            HS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, css));
             HS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         }
     }
@@ -832,12 +890,12 @@ bool asm_cols_slab(AsmWork& w, bool backward, const SlabCol& sc, float2* out, in
                    cudaStream_t st) {
     if (!w.use_static || w.L != 1) return false;
     const Plans* p = find(w.Px, w.Py);
-    if (!p || p->cc != w.CC || !p->col.fwdS) return false;
+    if (!p || p->cc != w.CC || !p->col.fwdS || cols_smem_persist(*p, w.H) > 227 * 1024) return false;
     if (w.H % sc.R != 0 || sc.hr * sc.R != w.H) return false;
     ColArgs c{nullptr, out, w.C, w.H, w.Py, w.Px, w.oy, ntiles_local, w.L, w.plan_y, nullptr, w.tf.as<TfConst>()};
     c.tile0 = tile0;
-    (backward ? p->col.bwdS : p->col.fwdS)<<<ntiles_local * w.C, p->col.nt1, cols_smem_persist(*p, w.H), st>>>(
-        c, w.stw_y, sc);
+    (backward ? p->col.bwdS : p->col.fwdS)<<<ntiles_local * w.C, p->col.nt1 ? p->col.nt1 : p->col.nt,
+                                             cols_smem_persist(*p, w.H), st>>>(c, w.stw_y, sc);
     launch_check(backward ? "scols_bwd_slab" : "scols_fwd_slab");
     return true;
 }
