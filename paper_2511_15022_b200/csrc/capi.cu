@@ -949,6 +949,8 @@ extern "C" hs_status hs_trainer_set_row_slab(hs_trainer* t, int rank, int ranks)
         t->h0 = rank * t->hr;
         t->rw.band_ty0 = t->h0 / kTile;  // the raster forward reads only the band's tiles
         t->rw.band_ty1 = (t->h0 + t->hr - 1) / kTile;
+        t->rw.band_y0 = t->h0;
+        t->rw.band_y1 = t->h0 + t->hr - 1;
         t->g0 = t->g0_of[rank];
         t->He = t->He_of[rank];
         t->top = t->h0 - t->g0;

@@ -174,64 +174,47 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(const uint32_t*
                                                                  uint32_t* __restrict__ toffset,
                                                                  uint2* __restrict__ ranges,
                                                                  uint32_t* __restrict__ status, int64_t cap) {
-    // each thread scans a contiguous run of tiles serially (16-byte loads and
-    // stores when the runs are multiples of 4 tiles); one block scan joins the runs
+    // each thread scans a contiguous run of tiles (16-byte loads and stores
+    // when the run is a whole number of 4-tile groups: the counts are read
+    // twice, from L1/L2, instead of being held in registers); one block scan
+    // joins the runs
     using BSc = cub::BlockScan<unsigned long long, kScanThreads>;
     __shared__ typename BSc::TempStorage tmp;
-    constexpr int kReg = 8;  // tiles per thread held in registers (cfg2: 8160 tiles -> 8 per thread)
     const int per = (tiles + kScanThreads - 1) / kScanThreads;
     const int t0 = threadIdx.x * per, t1 = min(t0 + per, tiles);
     const bool vec = (per % 4) == 0 && t1 - t0 == per;
     unsigned long long run = 0;
-    uint32_t c[kReg];
-    if (vec && per <= kReg) {
-#pragma unroll
-        for (int i = 0; i < kReg; i += 4) {
-            uint4 q = make_uint4(0u, 0u, 0u, 0u);
-            if (i < per) q = *reinterpret_cast<const uint4*>(tcount + t0 + i);
-            c[i] = q.x; c[i + 1] = q.y; c[i + 2] = q.z; c[i + 3] = q.w;
+    if (vec) {
+#pragma unroll 4
+        for (int i = 0; i < per; i += 4) {
+            const uint4 q = *reinterpret_cast<const uint4*>(tcount + t0 + i);
+            run += static_cast<unsigned long long>(q.x) + q.y + q.z + q.w;
         }
     } else {
-#pragma unroll
-        for (int i = 0; i < kReg; ++i) c[i] = (t0 + i < t1) ? tcount[t0 + i] : 0u;
+        for (int t = t0; t < t1; ++t) run += tcount[t];
     }
-#pragma unroll
-    for (int i = 0; i < kReg; ++i) run += c[i];
-    for (int t = t0 + kReg; t < t1; ++t) run += tcount[t];
     unsigned long long ex, agg;
     BSc(tmp).ExclusiveSum(run, ex, agg);
-    if (vec && per <= kReg) {
-#pragma unroll
-        for (int i = 0; i < kReg; i += 4) {
-            if (i < per) {
-                uint32_t o[4];
-                uint2 r[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    o[k] = static_cast<uint32_t>(ex);
-                    r[k] = c[i + k] ? make_uint2(static_cast<uint32_t>(ex), static_cast<uint32_t>(ex + c[i + k]))
-                                    : make_uint2(0u, 0u);
-                    ex += c[i + k];
-                }
-                *reinterpret_cast<uint4*>(toffset + t0 + i) = make_uint4(o[0], o[1], o[2], o[3]);
-                reinterpret_cast<uint4*>(ranges + t0 + i)[0] = make_uint4(r[0].x, r[0].y, r[1].x, r[1].y);
-                reinterpret_cast<uint4*>(ranges + t0 + i)[1] = make_uint4(r[2].x, r[2].y, r[3].x, r[3].y);
-            }
+    auto range = [](unsigned long long e, uint32_t c) {
+        return c ? make_uint2(static_cast<uint32_t>(e), static_cast<uint32_t>(e + c)) : make_uint2(0u, 0u);
+    };
+    if (vec) {
+#pragma unroll 2
+        for (int i = 0; i < per; i += 4) {
+            const uint4 q = *reinterpret_cast<const uint4*>(tcount + t0 + i);
+            const unsigned long long e0 = ex, e1 = e0 + q.x, e2 = e1 + q.y, e3 = e2 + q.z;
+            ex = e3 + q.w;
+            *reinterpret_cast<uint4*>(toffset + t0 + i) = make_uint4(static_cast<uint32_t>(e0), static_cast<uint32_t>(e1),
+                                                                     static_cast<uint32_t>(e2), static_cast<uint32_t>(e3));
+            const uint2 r0 = range(e0, q.x), r1 = range(e1, q.y), r2 = range(e2, q.z), r3 = range(e3, q.w);
+            reinterpret_cast<uint4*>(ranges + t0 + i)[0] = make_uint4(r0.x, r0.y, r1.x, r1.y);
+            reinterpret_cast<uint4*>(ranges + t0 + i)[1] = make_uint4(r2.x, r2.y, r3.x, r3.y);
         }
     } else {
-#pragma unroll
-        for (int i = 0; i < kReg; ++i) {
-            if (t0 + i < t1) {
-                toffset[t0 + i] = static_cast<uint32_t>(ex);
-                ranges[t0 + i] = c[i] ? make_uint2(static_cast<uint32_t>(ex), static_cast<uint32_t>(ex + c[i]))
-                                      : make_uint2(0u, 0u);
-                ex += c[i];
-            }
-        }
-        for (int t = t0 + kReg; t < t1; ++t) {
+        for (int t = t0; t < t1; ++t) {
             const uint32_t v = tcount[t];
             toffset[t] = static_cast<uint32_t>(ex);
-            ranges[t] = v ? make_uint2(static_cast<uint32_t>(ex), static_cast<uint32_t>(ex + v)) : make_uint2(0u, 0u);
+            ranges[t] = range(ex, v);
             ex += v;
         }
     }
@@ -256,11 +239,39 @@ __device__ __forceinline__ int box_count(const int4& b) {
     return (nx > 0 && ny > 0) ? nx * ny : 0;
 }
 
+// Row-slab band: ids of the Gaussians whose pixel box meets rows [y0, y1]
+// (warp-aggregated slots; the order is irrelevant: binning sorts each tile,
+// the backward writes per id).
+__global__ void band_list_kernel(int n, const int4* __restrict__ pbox, int y0, int y1, uint32_t* __restrict__ list,
+                                 uint32_t* __restrict__ list_n) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    bool in = false;
+    if (g < n) {
+        const int4 b = pbox[g];
+        in = b.z <= y1 && b.w >= y0 && b.x <= b.y;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, in);
+    if (!m) return;
+    unsigned base = 0;
+    if (lane == __ffs(m) - 1) base = atomicAdd(list_n, static_cast<unsigned>(__popc(m)));
+    base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+    if (in) list[base + __popc(m & ((1u << lane) - 1u))] = static_cast<uint32_t>(g);
+}
+
+// list (nullable): the Gaussians to bin, *list_n of them (a row-slab rank's band)
+__device__ __forceinline__ int pick(int idx, int n, const uint32_t* list, const uint32_t* list_n) {
+    if (list) return idx < static_cast<int>(*list_n) ? static_cast<int>(list[idx]) : -1;
+    return idx < n ? idx : -1;
+}
+
 __global__ void __launch_bounds__(256) count_tiles_kernel(int n, const int4* __restrict__ tbox, int tiles_x,
-                                                          uint32_t* __restrict__ tcount, int ty_lo, int ty_hi) {
-    const int g = blockIdx.x * (256 / kScatterSub) + threadIdx.x / kScatterSub;
+                                                          uint32_t* __restrict__ tcount, int ty_lo, int ty_hi,
+                                                          const uint32_t* __restrict__ list,
+                                                          const uint32_t* __restrict__ list_n) {
+    const int g = pick(blockIdx.x * (256 / kScatterSub) + threadIdx.x / kScatterSub, n, list, list_n);
     const int sub = threadIdx.x % kScatterSub;
-    if (g >= n) return;
+    if (g < 0) return;
     const int4 b = band_box(tbox[g], ty_lo, ty_hi);
     const int nx = b.y - b.x + 1, cnt = box_count(b);
     for (int k = sub; k < cnt; k += kScatterSub) atomicAdd(tcount + (b.z + k / nx) * tiles_x + b.x + k % nx, 1u);
@@ -273,10 +284,12 @@ __global__ void __launch_bounds__(256) scatter_ids_kernel(int n, const int4* __r
                                                           const uint32_t* __restrict__ toffset,
                                                           uint32_t* __restrict__ tcount,
                                                           const uint32_t* __restrict__ status,
-                                                          uint32_t* __restrict__ ids, int ty_lo, int ty_hi) {
-    const int g = blockIdx.x * (256 / kScatterSub) + threadIdx.x / kScatterSub;
+                                                          uint32_t* __restrict__ ids, int ty_lo, int ty_hi,
+                                                          const uint32_t* __restrict__ list,
+                                                          const uint32_t* __restrict__ list_n) {
+    const int g = pick(blockIdx.x * (256 / kScatterSub) + threadIdx.x / kScatterSub, n, list, list_n);
     const int sub = threadIdx.x % kScatterSub;
-    if (g >= n || status[1]) return;
+    if (g < 0 || status[1]) return;
     const int4 b = band_box(tbox[g], ty_lo, ty_hi);
     const int nx = b.y - b.x + 1, cnt = box_count(b);
     for (int k = sub; k < cnt; k += kScatterSub) {
@@ -599,15 +612,23 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(
 constexpr int kBwdThreads = 256;
 constexpr int kBwdWarps = kBwdThreads / 32;
 
-template <int C, int MINB, int NCH>
+// LIST: a row-slab rank walks only the Gaussians of its band list (the
+// other raw sums were zeroed before the launch).
+template <int C, int MINB, int NCH, bool LIST = false>
 __global__ void __launch_bounds__(kBwdThreads, MINB) raster_bwd_kernel(
     int N, const float4* __restrict__ rec, const float4* __restrict__ shade,
     const double* __restrict__ p64, const int4* __restrict__ pbox, int W, int H,
-    const float2* __restrict__ gfield, float* __restrict__ raw, int y0, int hs) {
+    const float2* __restrict__ gfield, float* __restrict__ raw, int y0, int hs,
+    const uint32_t* __restrict__ list = nullptr, const uint32_t* __restrict__ list_n = nullptr) {
     __shared__ int2 s_rows[kBwdWarps][32];  // compact nonempty rows: (y, x - flat index)
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int g = blockIdx.x * kBwdWarps + wid;
-    if (g >= N) return;
+    int g = blockIdx.x * kBwdWarps + wid;
+    if constexpr (LIST) {
+        if (g >= static_cast<int>(*list_n)) return;
+        g = static_cast<int>(list[g]);
+    } else {
+        if (g >= N) return;
+    }
     const float4 r0 = rec[g];
     const float4 r1 = rec[static_cast<size_t>(N) + g];
     const float4 r2 = rec[2 * static_cast<size_t>(N) + g];
@@ -900,15 +921,28 @@ void RasterWork::project_and_bin(const float* d_params, cudaStream_t st, cudaEve
                  tcount.as<uint32_t>(), stat};
     project_kernel<<<ceil_div(n, 128), 128, 0, st>>>(P);
     launch_check("project");
+    const uint32_t* lst = nullptr;
+    const uint32_t* lst_n = nullptr;
+    if (banded()) {
+        band_list.reserve(sizeof(uint32_t) * n);
+        band_n.reserve(sizeof(uint32_t));
+        HS_CUDA(cudaMemsetAsync(band_n.p, 0, sizeof(uint32_t), st));
+        band_list_kernel<<<ceil_div(n, 256), 256, 0, st>>>(n, pbox.as<int4>(), band_y0, band_y1,
+                                                             band_list.as<uint32_t>(), band_n.as<uint32_t>());
+        launch_check("band_list");
+        lst = band_list.as<uint32_t>();
+        lst_n = band_n.as<uint32_t>();
+    }
     count_tiles_kernel<<<ceil_div(n, 256 / kScatterSub), 256, 0, st>>>(n, tbox.as<int4>(), tiles_x,
-                                                                       tcount.as<uint32_t>(), band_ty0, band_ty1);
+                                                                       tcount.as<uint32_t>(), band_ty0, band_ty1, lst,
+                                                                       lst_n);
     launch_check("count_tiles");
     tile_scan_kernel<<<1, kScanThreads, 0, st>>>(tcount.as<uint32_t>(), tiles, toffset.as<uint32_t>(), ranges.as<uint2>(),
                                          stat, cap);
     launch_check("tile_scan");
     scatter_ids_kernel<<<ceil_div(n, 256 / kScatterSub), 256, 0, st>>>(n, tbox.as<int4>(), tiles_x, toffset.as<uint32_t>(),
                                                          tcount.as<uint32_t>(), stat, ids.as<uint32_t>(), band_ty0,
-                                                         band_ty1);
+                                                         band_ty1, lst, lst_n);
     launch_check("scatter_ids");
     segment_sort_warp_kernel<<<ceil_div(tiles, 8), 256, 0, st>>>(ranges.as<uint2>(), tiles, ids.as<uint32_t>(),
                                                                   stat);
@@ -966,8 +1000,19 @@ static void bwd_launch(const RasterWork& rw, const float* d_params, const float2
     auto go = [&](auto kern) {
         kern<<<ceil_div(rw.n, warps_per_block), kBwdThreads, 0, st>>>(
             rw.n, rw.rec.as<float4>(), rw.shade.as<float4>(), rw.p64.as<double>(), rw.pbox.as<int4>(),
-            rw.width, rw.height, d_gf, rw.raw.as<float>(), y0, hs);
+            rw.width, rw.height, d_gf, rw.raw.as<float>(), y0, hs, nullptr, nullptr);
     };
+    if (rw.banded()) {  // row-slab rank: only the band's Gaussians; the rest sum to zero
+        HS_CUDA(cudaMemsetAsync(rw.raw.p, 0, sizeof(float) * static_cast<size_t>(rw.n) * (2 * C + 6), st));
+        raster_bwd_kernel<C, 4, 1, true><<<ceil_div(rw.n, warps_per_block), kBwdThreads, 0, st>>>(
+            rw.n, rw.rec.as<float4>(), rw.shade.as<float4>(), rw.p64.as<double>(), rw.pbox.as<int4>(), rw.width,
+            rw.height, d_gf, rw.raw.as<float>(), y0, hs, rw.band_list.as<uint32_t>(), rw.band_n.as<uint32_t>());
+        launch_check("raster_bwd");
+        raster_finalize_kernel<C><<<ceil_div(rw.n, 256), 256, 0, st>>>(rw.n, rw.raw.as<float>(), d_params, rw.width,
+                                                                       rw.height, d_grads, d_flags);
+        launch_check("raster_finalize");
+        return;
+    }
     switch (bwd_variant()) {
         case 1: go(raster_bwd_kernel<C, 3, 2>); break;
         default: go(raster_bwd_kernel<C, 4, 1>); break;  // measured best at cfg2

@@ -25,6 +25,11 @@ struct RasterWork {
     DevBuf status;   // uint32[4]: [0] K (pairs), [1] overflow, [2] non-finite param, [3] unused
     int64_t cap = 0; // pair capacity
     int band_ty0 = 0, band_ty1 = 1 << 30;  // tile rows binned (a row-slab rank: its band)
+    // row-slab rank: the Gaussians whose pixel box meets rows [band_y0, band_y1]
+    // (compacted after the projection; binning and the backward walk only them)
+    int band_y0 = -1, band_y1 = -1;
+    DevBuf band_list, band_n;
+    bool banded() const { return band_y0 >= 0; }
 
     void prepare(int n_, int c_, int w_, int h_);
     void reserve_pairs(int64_t cap_);
