@@ -800,12 +800,19 @@ __global__ void __launch_bounds__(kBwdThreads, MINB) raster_bwd_kernel(
 // Chain rule of rasterize_backward (rasterizer.cpp:251-282) in fp64, one
 // thread per Gaussian, from the warp-reduced raw sums [d_amp[C], d_phase[C],
 // d_alpha, gmx, gmy, ga, gb, gc] (SoA, N each).
-template <int C>
+template <int C, bool LIST = false>
 __global__ void __launch_bounds__(256) raster_finalize_kernel(int N, const float* __restrict__ raw,
                                                                const float* __restrict__ params, int W, int H,
-                                                               float* __restrict__ grads, uint32_t* flags) {
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= N) return;
+                                                               float* __restrict__ grads, uint32_t* flags,
+                                                               const uint32_t* __restrict__ list = nullptr,
+                                                               const uint32_t* __restrict__ list_n = nullptr) {
+    int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if constexpr (LIST) {  // row-slab rank: its band's Gaussians (the other gradients were zeroed)
+        if (g >= static_cast<int>(*list_n)) return;
+        g = static_cast<int>(list[g]);
+    } else {
+        if (g >= N) return;
+    }
     const size_t Ns = N;
     auto R = [&](int k) { return static_cast<double>(raw[static_cast<size_t>(k) * Ns + g]); };
     const double d_alpha = R(2 * C), gmx = R(2 * C + 1), gmy = R(2 * C + 2);
@@ -1002,14 +1009,16 @@ static void bwd_launch(const RasterWork& rw, const float* d_params, const float2
             rw.n, rw.rec.as<float4>(), rw.shade.as<float4>(), rw.p64.as<double>(), rw.pbox.as<int4>(),
             rw.width, rw.height, d_gf, rw.raw.as<float>(), y0, hs, nullptr, nullptr);
     };
-    if (rw.banded()) {  // row-slab rank: only the band's Gaussians; the rest sum to zero
-        HS_CUDA(cudaMemsetAsync(rw.raw.p, 0, sizeof(float) * static_cast<size_t>(rw.n) * (2 * C + 6), st));
+    if (rw.banded()) {  // row-slab rank: only the band's Gaussians; the others' gradients are zero
+        const int64_t P = static_cast<int64_t>(rw.n) * (6 + 2 * C);
+        HS_CUDA(cudaMemsetAsync(d_grads, 0, sizeof(float) * P, st));
         raster_bwd_kernel<C, 4, 1, true><<<ceil_div(rw.n, warps_per_block), kBwdThreads, 0, st>>>(
             rw.n, rw.rec.as<float4>(), rw.shade.as<float4>(), rw.p64.as<double>(), rw.pbox.as<int4>(), rw.width,
             rw.height, d_gf, rw.raw.as<float>(), y0, hs, rw.band_list.as<uint32_t>(), rw.band_n.as<uint32_t>());
         launch_check("raster_bwd");
-        raster_finalize_kernel<C><<<ceil_div(rw.n, 256), 256, 0, st>>>(rw.n, rw.raw.as<float>(), d_params, rw.width,
-                                                                       rw.height, d_grads, d_flags);
+        raster_finalize_kernel<C, true><<<ceil_div(rw.n, 256), 256, 0, st>>>(
+            rw.n, rw.raw.as<float>(), d_params, rw.width, rw.height, d_grads, d_flags, rw.band_list.as<uint32_t>(),
+            rw.band_n.as<uint32_t>());
         launch_check("raster_finalize");
         return;
     }
