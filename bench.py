@@ -289,8 +289,8 @@ def run_sharded(args):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         l0 = holo.kernel_launch_count()
-        for _ in range(args.steps):
-            loss = step.step()
+        for i in range(args.steps):
+            loss = step.step(with_loss=i + 1 == args.steps)  # the loss (a host sync) on the last step only
         e1.record(stream)
         e1.synchronize()
         torch.cuda.synchronize()
@@ -315,8 +315,11 @@ def run_sharded(args):
                               "frac": B / (ms * 1e-3) / 1e9 / peak / world, "peak_source": peak_src,
                               "note": "whole-job algorithmic bytes over world x peak"},
             "gpu_launches": int(launches), "clocks": clocks, "loss": loss,
-            "timing": "eager steps (NCCL all-reduce between forward_backward and apply_update), "
-                      "CUDA events on the trainer stream, max over ranks",
+            "timing": ("slab steps: stages 0-4 as one CUDA graph (peer-put, device-flag sync), NCCL "
+                       "all-reduce of the gradients, Adan; " if args.shard == "slabs" and args.exchange == "put"
+                       else "eager steps (NCCL all-reduce between forward_backward and apply_update); ")
+                      + "loss (a host sync) on the last timed step only; CUDA events on the trainer stream, "
+                        "max over ranks",
         }
         if args.shard == "slabs" and args.virtual_ranks > 1 and world == 1:
             R = args.virtual_ranks

@@ -257,6 +257,11 @@ uint32_t* hs_trainer_slab_flags_ptr(hs_trainer* tr);
 hs_status hs_trainer_slab_set_peers(hs_trainer* tr, float* const* recv0, float* const* recv1,
                                     uint32_t* const* flags);
 hs_status hs_trainer_slab_status(hs_trainer* tr, uint32_t* error);
+/* Peer-put mode: stages 0..4 in one call (no host step between them; the
+ * exchange epochs are device counters), replayed as one CUDA graph when
+ * hs_trainer_use_graph is on.  Follow with the gradient all-reduce and
+ * hs_trainer_apply_update. */
+hs_status hs_trainer_slab_forward_backward(hs_trainer* tr);
 /* holo::Rng(seed).uniform(lo, hi) drawn n times into h_out (rng.hpp; host). */
 hs_status hs_random_uniform(uint64_t seed, int64_t n, double lo, double hi, double* h_out);
 /* CUDA IPC of a device allocation: 64-byte handle out; open maps a peer

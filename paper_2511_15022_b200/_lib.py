@@ -126,6 +126,7 @@ _SIGS = {
     "hs_trainer_slab_flags_ptr": [C.c_void_p],
     "hs_trainer_slab_set_peers": [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)],
     "hs_trainer_slab_status": [C.c_void_p, C.POINTER(C.c_uint32)],
+    "hs_trainer_slab_forward_backward": [C.c_void_p],
     "hs_random_uniform": [C.c_uint64, C.c_int64, C.c_double, C.c_double, C.c_void_p],
     "hs_ipc_get_handle": [C.c_void_p, C.c_void_p],
     "hs_ipc_open_handle": [C.c_void_p, C.POINTER(C.c_void_p)],

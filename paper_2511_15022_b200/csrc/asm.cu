@@ -451,8 +451,11 @@ struct PeerFlags {
     uint32_t* f[kMaxPeers];
 };
 
-__global__ void slab_signal_kernel(PeerFlags pf, int ranks, int me, uint32_t epoch) {
+__global__ void slab_signal_kernel(PeerFlags pf, int ranks, int me, uint32_t* epoch_ctr) {
     const int a = threadIdx.x;
+    const uint32_t epoch = *epoch_ctr + 1u;
+    __syncwarp();
+    if (a == 0) *epoch_ctr = epoch;
     if (a >= ranks) return;
     // every store of the preceding pack kernel (stream order) is made visible
     // system-wide before the flag
@@ -460,8 +463,9 @@ __global__ void slab_signal_kernel(PeerFlags pf, int ranks, int me, uint32_t epo
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(pf.f[a] + me), "r"(epoch) : "memory");
 }
 
-__global__ void slab_wait_kernel(const uint32_t* flags, int ranks, uint32_t epoch, uint32_t* error) {
+__global__ void slab_wait_kernel(const uint32_t* flags, int ranks, const uint32_t* epoch_ctr, uint32_t* error) {
     const int a = threadIdx.x;
+    const uint32_t epoch = *epoch_ctr;
     if (a < ranks) {
         const long long t0 = clock64();
         uint32_t v = 0;
@@ -479,14 +483,14 @@ __global__ void slab_wait_kernel(const uint32_t* flags, int ranks, uint32_t epoc
 }
 }  // namespace
 
-void slab_signal(uint32_t* const* peer_flags, int ranks, int me, uint32_t epoch, cudaStream_t st) {
+void slab_signal(uint32_t* const* peer_flags, int ranks, int me, uint32_t* epoch, cudaStream_t st) {
     PeerFlags pf{};
     for (int a = 0; a < ranks; ++a) pf.f[a] = peer_flags[a];
     slab_signal_kernel<<<1, 32, 0, st>>>(pf, ranks, me, epoch);
     launch_check("slab_signal");
 }
 
-void slab_wait(const uint32_t* flags, int ranks, uint32_t epoch, uint32_t* error, cudaStream_t st) {
+void slab_wait(const uint32_t* flags, int ranks, const uint32_t* epoch, uint32_t* error, cudaStream_t st) {
     slab_wait_kernel<<<1, 32, 0, st>>>(flags, ranks, epoch, error);
     launch_check("slab_wait");
 }

@@ -113,11 +113,14 @@ struct ChunkMap {
     float2* dptr[kMaxPeers] = {};
 };
 void chunk_copy(const float2* src, float2* dst, const ChunkMap& m, cudaStream_t st);
-// Exchange flags of the peer-put transposes: signal writes `epoch` into slot
-// `me` of every peer's flag array (system-scope release after a fence); wait
-// spins (acquire) until every slot of this rank's flags reaches `epoch`, and
-// gives up after ~2 s with error[0] = 1 (no hang when a peer died).
-void slab_signal(uint32_t* const* peer_flags, int ranks, int me, uint32_t epoch, cudaStream_t st);
+// Exchange flags of the peer-put transposes.  The exchange epoch lives on the
+// device (*epoch, this rank's counter), so a captured step replays correctly:
+// signal increments it and writes the new value into slot `me` of every
+// peer's flag array (system-scope release after a fence); wait spins
+// (acquire) until every slot of this rank's flags reaches *epoch, and gives
+// up after ~2 s with error[0] = 1 (no hang when a peer died).
+void slab_signal(uint32_t* const* peer_flags, int ranks, int me, uint32_t* epoch, cudaStream_t st);
+void slab_wait(const uint32_t* flags, int ranks, const uint32_t* epoch, uint32_t* error, cudaStream_t st);
 
 // Row FFT whose last stage stores straight into the peers' receive buffers
 // (row-slab peer-put exchange fused into the compute kernel): the output
@@ -160,7 +163,6 @@ struct SlabCol {
 };
 bool asm_cols_slab(AsmWork& w, bool backward, const SlabCol& sc, float2* out, int tile0, int ntiles_local,
                    cudaStream_t st);
-void slab_wait(const uint32_t* flags, int ranks, uint32_t epoch, uint32_t* error, cudaStream_t st);
 
 // Static (compile-time planned) propagation path; false when (Px, Py) has no plan.
 bool static_plan_cc(int Px, int Py, int pad, int L, int* cc);

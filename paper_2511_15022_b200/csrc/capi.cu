@@ -111,8 +111,8 @@ struct hs_trainer {
     bool s_put = false;
     float2* s_peer_recv[2][kMaxPeers] = {};
     uint32_t* s_peer_flags[kMaxPeers] = {};
-    DevBuf s_recv2, s_flags;  // flags: [0, R) per-source epochs, [kMaxPeers] error word
-    uint32_t s_epoch = 0;
+    DevBuf s_recv2, s_flags;  // flags: [0, R) per-source epochs, [kMaxPeers] error word, [kMaxPeers + 1] own epoch
+    cudaGraphExec_t slab_graph = nullptr;  // stages 0..4 of the put exchange, captured
     int s_loss_slots = 0;
     ~hs_trainer() {
         if (graph) cudaGraphExecDestroy(graph);
@@ -122,6 +122,7 @@ struct hs_trainer {
         if (ev_fork) cudaEventDestroy(ev_fork);
         if (ev_ap) cudaEventDestroy(ev_ap);
         if (copy_st) cudaStreamDestroy(copy_st);
+        if (slab_graph) cudaGraphExecDestroy(slab_graph);
         if (h_words) cudaFreeHost(h_words);
         if (h_o3) cudaFreeHost(h_o3);
     }
@@ -951,6 +952,8 @@ extern "C" hs_status hs_trainer_set_row_slab(hs_trainer* t, int rank, int ranks)
         t->rw.band_ty1 = (t->h0 + t->hr - 1) / kTile;
         t->rw.band_y0 = t->h0;
         t->rw.band_y1 = t->h0 + t->hr - 1;
+        t->rw.band_list.reserve(sizeof(uint32_t) * std::max(t->n, 1));  // no allocation inside a captured step
+        t->rw.band_n.reserve(sizeof(uint32_t));
         t->g0 = t->g0_of[rank];
         t->He = t->He_of[rank];
         t->top = t->h0 - t->g0;
@@ -968,10 +971,13 @@ extern "C" hs_status hs_trainer_set_row_slab(hs_trainer* t, int rank, int ranks)
         t->s_send.reserve(sizeof(float2) * LC * tiled);
         t->s_recv.reserve(sizeof(float2) * LC * tiled);
         t->s_recv2.reserve(sizeof(float2) * LC * tiled);
-        t->s_flags.reserve(sizeof(uint32_t) * (kMaxPeers + 1));
-        HS_CUDA(cudaMemsetAsync(t->s_flags.p, 0, sizeof(uint32_t) * (kMaxPeers + 1), st));
-        t->s_epoch = 0;
+        t->s_flags.reserve(sizeof(uint32_t) * (kMaxPeers + 2));
+        HS_CUDA(cudaMemsetAsync(t->s_flags.p, 0, sizeof(uint32_t) * (kMaxPeers + 2), st));
         t->s_put = false;
+        if (t->slab_graph) {
+            HS_CUDA(cudaGraphExecDestroy(t->slab_graph));
+            t->slab_graph = nullptr;
+        }
         // loss-band slices of the target and the masks, and the band's target window stats
         HS_CUDA(cudaMemcpy2DAsync(t->s_target.p, band * sizeof(float), t->target.as<float>() + static_cast<size_t>(t->g0) * W,
                                   static_cast<size_t>(t->h) * W * sizeof(float), band * sizeof(float), C,
@@ -1061,140 +1067,172 @@ extern "C" hs_status hs_ipc_close(void* d_ptr) {
 // hs_trainer_slab_counts).  After stage 4 the gradient buffer holds this
 // rank's partial gradient (sum over its rows): all-reduce it, then
 // hs_trainer_apply_update.  Loss partial sums: hs_trainer_loss_partials.
+static void slab_enqueue(hs_trainer* t, int stage, cudaStream_t st) {
+    AsmWork& aw = t->aw;
+    const int C = t->c, LC = t->L * t->c;
+    float2* send = t->s_send.as<float2>();
+    // exchange k = stage - 1 arrives in the receive buffer of its parity (put
+    // mode; the NCCL path always receives into the first buffer)
+    const float2* recv = (t->s_put && ((stage - 1) & 1)) ? t->s_recv2.as<float2>() : t->s_recv.as<float2>();
+    uint32_t* epoch = t->s_flags.as<uint32_t>() + kMaxPeers + 1;
+    if (t->s_put && stage >= 1 && stage <= 4)
+        slab_wait(t->s_flags.as<uint32_t>(), t->R, epoch, t->s_flags.as<uint32_t>() + kMaxPeers, st);
+    // pack of exchange k: into the send buffer (NCCL), or straight into the
+    // peers' receive buffers at this rank's slot followed by the flag signal
+    auto pack = [&](int k, const float2* src) {
+        if (!t->s_put) {
+            chunk_copy(src, send, t->m_pack[k], st);
+            return;
+        }
+        ChunkMap m = t->m_pack[k];
+        for (int a = 0; a < t->R; ++a) {
+            m.dptr[a] = t->s_peer_recv[k & 1][a];
+            m.dA[a] = static_cast<int64_t>(t->rank) * (t->s_counts[k][a] / 2);
+        }
+        chunk_copy(src, nullptr, m, st);
+        slab_signal(t->s_peer_flags, t->R, t->rank, epoch, st);
+    };
+    // row FFTs whose last stage stores straight into the peers (put mode,
+    // planned grids): the compute kernel IS the exchange; else rows + pack
+    auto rows_put = [&](int k, const float2* in, int planes, int h, int row0) {
+        if (!t->s_put) return false;
+        SlabPut sp{};
+        for (int a = 0; a < t->R; ++a) {
+            sp.peer[a] = t->s_peer_recv[k & 1][a];
+            sp.slot[a] = static_cast<int64_t>(t->rank) * (t->s_counts[k][a] / 2);
+        }
+        sp.ts = t->ts;
+        sp.row0 = row0;
+        sp.hout = t->hr;
+        sp.ts_magic = static_cast<unsigned>((0x100000000ull + t->ts - 1) / t->ts);
+        if (!asm_rows_fwd_put(aw, in, planes, h, sp, st)) return false;
+        slab_signal(t->s_peer_flags, t->R, t->rank, epoch, st);
+        return true;
+    };
+    // inverse row FFTs gathering straight from the peer-major receive
+    // buffer (the unpack fused into the loads; planned grids)
+    auto rows_get = [&](int k, float2* out, int planes, int h) {
+        SlabGet sg{};
+        sg.ts = t->ts;
+        sg.ts_magic = static_cast<unsigned>((0x100000000ull + t->ts - 1) / t->ts);
+        sg.per_src = t->s_counts[k][t->R] / 2;  // receive count from source 0 (all sources equal)
+        return asm_rows_inv_get(aw, recv, out, planes, h, sg, st);
+    };
+    // column pass gathering its tiles from the receive buffer of exchange
+    // ki (R bulk copies) and putting its rows into the peers for exchange
+    // ko (put mode) or into the local T layout (then packed)
+    auto cols_slab = [&](bool backward, int ki, int ko, float2* local_out) {
+        SlabCol sc{};
+        sc.in = recv;
+        sc.per_src = t->s_counts[ki][t->R] / 2;
+        sc.R = t->R;
+        sc.hr = t->hr;
+        sc.inv_hr = 1.f / static_cast<float>(t->hr);
+        sc.put = t->s_put ? 1 : 0;
+        for (int a = 0; a < t->R; ++a) {
+            sc.peer[a] = t->s_peer_recv[ko & 1][a];
+            sc.slot[a] = static_cast<int64_t>(t->rank) * (t->s_counts[ko][a] / 2);
+            sc.g0[a] = ko == 1 ? t->g0_of[a] : a * t->hr;
+            sc.he[a] = ko == 1 ? t->He_of[a] : t->hr;
+        }
+        if (!asm_cols_slab(aw, backward, sc, local_out, t->rank * t->ts, t->ts, st)) return false;
+        if (t->s_put) {
+            slab_signal(t->s_peer_flags, t->R, t->rank, epoch, st);
+        } else {
+            chunk_copy(local_out, send, t->m_pack[ko], st);
+        }
+        return true;
+    };
+    switch (stage) {
+        case 0:  // binning (replicated), raster forward of the own rows, row FFTs, pack
+            HS_CUDA(cudaMemsetAsync(t->flags.p, 0, sizeof(uint32_t), st));
+            t->rw.project_and_bin(t->params.as<float>(), st);
+            raster_forward(t->rw, t->field.as<float2>(), st, t->h0, t->hr);
+            if (!rows_put(0, t->field.as<float2>(), C, t->hr, 0)) {
+                asm_rows_pass(aw, false, t->field.as<float2>(), aw.T1.as<float2>(), C, t->hr, st);
+                pack(0, aw.T1.as<float2>());
+            }
+            break;
+        case 1:  // column FFT x H_l + column IFFT on the own tiles, pack loss bands
+            if (!cols_slab(false, 0, 1, aw.T2.as<float2>())) {
+                chunk_copy(recv, aw.T1.as<float2>(), t->m_unpack[0], st);
+                asm_cols_pass(aw, false, aw.T1.as<float2>(), aw.T2.as<float2>(), t->rank * t->ts, t->ts, st);
+                pack(1, aw.T2.as<float2>());
+            }
+            break;
+        case 2: {  // row IFFTs of the loss band, loss + dU, backward row FFTs, pack own rows
+            if (!rows_get(1, t->s_planes.as<float2>(), LC, t->He)) {
+                chunk_copy(recv, t->s_T.as<float2>(), t->m_unpack[1], st);
+                asm_rows_pass(aw, true, t->s_T.as<float2>(), t->s_planes.as<float2>(), LC, t->He, st);
+            }
+            LossArgs a{kLossTraining, t->L, t->L_total, 0, C, t->He, t->w, nullptr, t->s_planes.as<float2>(),
+                       t->s_target.as<float>(), t->s_tstats.as<float2>(), t->s_masks.as<uint8_t>(), nullptr,
+                       t->s_dplanes.as<float2>(), t->partials.as<double>(), t->C_total};
+            a.H_norm = t->h;
+            a.own0 = t->top;
+            a.own1 = t->top + t->hr;
+            const int used = loss_launch(a, st);
+            loss_finalize(a, used, t->out3.as<double>(), st);
+            if (!rows_put(2, t->s_dplanes.as<float2>(), LC, t->He, t->top)) {
+                asm_rows_pass(aw, false, t->s_dplanes.as<float2>(), t->s_T.as<float2>(), LC, t->He, st);
+                pack(2, t->s_T.as<float2>());
+            }
+            break;
+        }
+        case 3:  // adjoint column pass on the own tiles, pack
+            if (!cols_slab(true, 2, 3, aw.T1.as<float2>())) {
+                chunk_copy(recv, aw.T2.as<float2>(), t->m_unpack[2], st);
+                asm_cols_pass(aw, true, aw.T2.as<float2>(), aw.T1.as<float2>(), t->rank * t->ts, t->ts, st);
+                pack(3, aw.T1.as<float2>());
+            }
+            break;
+        case 4:  // row IFFTs of the own rows, raster backward over the own rows
+            if (!rows_get(3, t->back.as<float2>(), C, t->hr)) {
+                chunk_copy(recv, aw.T2.as<float2>(), t->m_unpack[3], st);
+                asm_rows_pass(aw, true, aw.T2.as<float2>(), t->back.as<float2>(), C, t->hr, st);
+            }
+            raster_backward(t->rw, t->params.as<float>(), t->back.as<float2>(), t->grads.as<float>(),
+                            t->flags.as<uint32_t>(), st, t->h0, t->hr);
+            break;
+        default: throw Error(HS_EINVAL, "row slab: stage outside 0..4");
+    }
+}
+
 extern "C" hs_status hs_trainer_slab_stage(hs_trainer* t, int stage) {
     return guard([&] {
         require(t->R >= 1, "row slab: trainer is not row-slab sharded");
         require(t->host_step <= t->total_steps, "cosine_lr: step outside [0, total_steps]");
+        slab_enqueue(t, stage, t->ctx->stream);
+    });
+}
+
+// All five stages of a peer-put rank (no host step between them), captured
+// into one CUDA graph on the first call when graphs are on.
+extern "C" hs_status hs_trainer_slab_forward_backward(hs_trainer* t) {
+    return guard([&] {
+        require(t->R >= 1, "row slab: trainer is not row-slab sharded");
+        require(t->s_put, "row slab: the one-call step needs the peer-put exchange (hs_trainer_slab_set_peers)");
+        require(t->host_step <= t->total_steps, "cosine_lr: step outside [0, total_steps]");
         cudaStream_t st = t->ctx->stream;
-        AsmWork& aw = t->aw;
-        const int C = t->c, LC = t->L * t->c;
-        float2* send = t->s_send.as<float2>();
-        // exchange k = stage - 1 arrives in the receive buffer of its parity (put
-        // mode; the NCCL path always receives into the first buffer)
-        const float2* recv = (t->s_put && ((stage - 1) & 1)) ? t->s_recv2.as<float2>() : t->s_recv.as<float2>();
-        if (t->s_put && stage >= 1 && stage <= 4)
-            slab_wait(t->s_flags.as<uint32_t>(), t->R, t->s_epoch, t->s_flags.as<uint32_t>() + kMaxPeers, st);
-        // pack of exchange k: into the send buffer (NCCL), or straight into the
-        // peers' receive buffers at this rank's slot followed by the flag signal
-        auto pack = [&](int k, const float2* src) {
-            if (!t->s_put) {
-                chunk_copy(src, send, t->m_pack[k], st);
-                return;
-            }
-            ChunkMap m = t->m_pack[k];
-            for (int a = 0; a < t->R; ++a) {
-                m.dptr[a] = t->s_peer_recv[k & 1][a];
-                m.dA[a] = static_cast<int64_t>(t->rank) * (t->s_counts[k][a] / 2);
-            }
-            chunk_copy(src, nullptr, m, st);
-            t->s_epoch += 1;
-            slab_signal(t->s_peer_flags, t->R, t->rank, t->s_epoch, st);
-        };
-        // row FFTs whose last stage stores straight into the peers (put mode,
-        // planned grids): the compute kernel IS the exchange; else rows + pack
-        auto rows_put = [&](int k, const float2* in, int planes, int h, int row0) {
-            if (!t->s_put) return false;
-            SlabPut sp{};
-            for (int a = 0; a < t->R; ++a) {
-                sp.peer[a] = t->s_peer_recv[k & 1][a];
-                sp.slot[a] = static_cast<int64_t>(t->rank) * (t->s_counts[k][a] / 2);
-            }
-            sp.ts = t->ts;
-            sp.row0 = row0;
-            sp.hout = t->hr;
-            sp.ts_magic = static_cast<unsigned>((0x100000000ull + t->ts - 1) / t->ts);
-            if (!asm_rows_fwd_put(aw, in, planes, h, sp, st)) return false;
-            t->s_epoch += 1;
-            slab_signal(t->s_peer_flags, t->R, t->rank, t->s_epoch, st);
-            return true;
-        };
-        // inverse row FFTs gathering straight from the peer-major receive
-        // buffer (the unpack fused into the loads; planned grids)
-        auto rows_get = [&](int k, float2* out, int planes, int h) {
-            SlabGet sg{};
-            sg.ts = t->ts;
-            sg.ts_magic = static_cast<unsigned>((0x100000000ull + t->ts - 1) / t->ts);
-            sg.per_src = t->s_counts[k][t->R] / 2;  // receive count from source 0 (all sources equal)
-            return asm_rows_inv_get(aw, recv, out, planes, h, sg, st);
-        };
-        // column pass gathering its tiles from the receive buffer of exchange
-        // ki (R bulk copies) and putting its rows into the peers for exchange
-        // ko (put mode) or into the local T layout (then packed)
-        auto cols_slab = [&](bool backward, int ki, int ko, float2* local_out) {
-            SlabCol sc{};
-            sc.in = recv;
-            sc.per_src = t->s_counts[ki][t->R] / 2;
-            sc.R = t->R;
-            sc.hr = t->hr;
-            sc.inv_hr = 1.f / static_cast<float>(t->hr);
-            sc.put = t->s_put ? 1 : 0;
-            for (int a = 0; a < t->R; ++a) {
-                sc.peer[a] = t->s_peer_recv[ko & 1][a];
-                sc.slot[a] = static_cast<int64_t>(t->rank) * (t->s_counts[ko][a] / 2);
-                sc.g0[a] = ko == 1 ? t->g0_of[a] : a * t->hr;
-                sc.he[a] = ko == 1 ? t->He_of[a] : t->hr;
-            }
-            if (!asm_cols_slab(aw, backward, sc, local_out, t->rank * t->ts, t->ts, st)) return false;
-            if (t->s_put) {
-                t->s_epoch += 1;
-                slab_signal(t->s_peer_flags, t->R, t->rank, t->s_epoch, st);
-            } else {
-                chunk_copy(local_out, send, t->m_pack[ko], st);
-            }
-            return true;
-        };
-        switch (stage) {
-            case 0:  // binning (replicated), raster forward of the own rows, row FFTs, pack
-                HS_CUDA(cudaMemsetAsync(t->flags.p, 0, sizeof(uint32_t), st));
-                t->rw.project_and_bin(t->params.as<float>(), st);
-                raster_forward(t->rw, t->field.as<float2>(), st, t->h0, t->hr);
-                if (!rows_put(0, t->field.as<float2>(), C, t->hr, 0)) {
-                    asm_rows_pass(aw, false, t->field.as<float2>(), aw.T1.as<float2>(), C, t->hr, st);
-                    pack(0, aw.T1.as<float2>());
-                }
-                break;
-            case 1:  // column FFT x H_l + column IFFT on the own tiles, pack loss bands
-                if (!cols_slab(false, 0, 1, aw.T2.as<float2>())) {
-                    chunk_copy(recv, aw.T1.as<float2>(), t->m_unpack[0], st);
-                    asm_cols_pass(aw, false, aw.T1.as<float2>(), aw.T2.as<float2>(), t->rank * t->ts, t->ts, st);
-                    pack(1, aw.T2.as<float2>());
-                }
-                break;
-            case 2: {  // row IFFTs of the loss band, loss + dU, backward row FFTs, pack own rows
-                if (!rows_get(1, t->s_planes.as<float2>(), LC, t->He)) {
-                    chunk_copy(recv, t->s_T.as<float2>(), t->m_unpack[1], st);
-                    asm_rows_pass(aw, true, t->s_T.as<float2>(), t->s_planes.as<float2>(), LC, t->He, st);
-                }
-                LossArgs a{kLossTraining, t->L, t->L_total, 0, C, t->He, t->w, nullptr, t->s_planes.as<float2>(),
-                           t->s_target.as<float>(), t->s_tstats.as<float2>(), t->s_masks.as<uint8_t>(), nullptr,
-                           t->s_dplanes.as<float2>(), t->partials.as<double>(), t->C_total};
-                a.H_norm = t->h;
-                a.own0 = t->top;
-                a.own1 = t->top + t->hr;
-                const int used = loss_launch(a, st);
-                loss_finalize(a, used, t->out3.as<double>(), st);
-                if (!rows_put(2, t->s_dplanes.as<float2>(), LC, t->He, t->top)) {
-                    asm_rows_pass(aw, false, t->s_dplanes.as<float2>(), t->s_T.as<float2>(), LC, t->He, st);
-                    pack(2, t->s_T.as<float2>());
-                }
-                break;
-            }
-            case 3:  // adjoint column pass on the own tiles, pack
-                if (!cols_slab(true, 2, 3, aw.T1.as<float2>())) {
-                    chunk_copy(recv, aw.T2.as<float2>(), t->m_unpack[2], st);
-                    asm_cols_pass(aw, true, aw.T2.as<float2>(), aw.T1.as<float2>(), t->rank * t->ts, t->ts, st);
-                    pack(3, aw.T1.as<float2>());
-                }
-                break;
-            case 4:  // row IFFTs of the own rows, raster backward over the own rows
-                if (!rows_get(3, t->back.as<float2>(), C, t->hr)) {
-                    chunk_copy(recv, aw.T2.as<float2>(), t->m_unpack[3], st);
-                    asm_rows_pass(aw, true, aw.T2.as<float2>(), t->back.as<float2>(), C, t->hr, st);
-                }
-                raster_backward(t->rw, t->params.as<float>(), t->back.as<float2>(), t->grads.as<float>(),
-                                t->flags.as<uint32_t>(), st, t->h0, t->hr);
-                break;
-            default: throw Error(HS_EINVAL, "row slab: stage outside 0..4");
+        if (!t->use_graph || st == nullptr) {
+            for (int k = 0; k < 5; ++k) slab_enqueue(t, k, st);
+            return;
         }
+        if (!t->slab_graph) {
+            cudaGraph_t g = nullptr;
+            HS_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            try {
+                for (int k = 0; k < 5; ++k) slab_enqueue(t, k, st);
+            } catch (...) {
+                cudaStreamEndCapture(st, &g);
+                if (g) cudaGraphDestroy(g);
+                throw;
+            }
+            HS_CUDA(cudaStreamEndCapture(st, &g));
+            HS_CUDA(cudaGraphInstantiate(&t->slab_graph, g, 0));
+            HS_CUDA(cudaGraphDestroy(g));
+        }
+        HS_CUDA(cudaGraphLaunch(t->slab_graph, st));
+        note_launch(0);
     });
 }

@@ -915,6 +915,11 @@ class Trainer:
         self._peer_arrays = (arr(recv0), arr(recv1), arr(flags))
         check(_lib.load().hs_trainer_slab_set_peers(self.h, *self._peer_arrays))
 
+    def slab_forward_backward(self):
+        """Peer-put mode: all five stages in one call (one CUDA graph with use_graph)."""
+        ctx_handle()
+        check(_lib.load().hs_trainer_slab_forward_backward(self.h))
+
     def slab_status(self) -> int:
         v = C.c_uint32(0)
         check(_lib.load().hs_trainer_slab_status(self.h, C.byref(v)))

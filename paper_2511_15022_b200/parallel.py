@@ -87,7 +87,8 @@ class ShardedStep:
         self.C, self.H, self.W, self.L = C, H, W, L_total
         self.group = group
 
-    def step(self) -> float:
+    def step(self, with_loss: bool = True):
+        """One step; returns the loss (a host sync) or None when with_loss is False."""
         self.tr.forward_backward()
         g = self.tr.grads_tensor()
         if dist.is_initialized() and dist.get_world_size(self.group) > 1:
@@ -95,6 +96,8 @@ class ShardedStep:
                 torch.cuda.current_stream().synchronize()
             dist.all_reduce(g, op=dist.ReduceOp.SUM, group=self.group)
         self.tr.apply_update()
+        if not with_loss:
+            return None
         parts = torch.tensor(self.tr.loss_partials(), dtype=torch.float64,
                              device=g.device if g.is_cuda else "cpu")
         if dist.is_initialized() and dist.get_world_size(self.group) > 1:
@@ -113,7 +116,8 @@ class ChannelShardedStep:
         self.C, self.H, self.W, self.L = C_total, H, W, L
         self.group = group
 
-    def step(self) -> float:
+    def step(self, with_loss: bool = True):
+        """One step; returns the loss (a host sync) or None when with_loss is False."""
         self.tr.forward_backward()
         g = self.tr.grads_tensor()
         multi = dist.is_initialized() and dist.get_world_size(self.group) > 1
@@ -123,6 +127,8 @@ class ChannelShardedStep:
             for b, e in geometry_ranges(self.n, self.c):
                 dist.all_reduce(g[b:e], op=dist.ReduceOp.SUM, group=self.group)
         self.tr.apply_update()
+        if not with_loss:
+            return None
         parts = torch.tensor(self.tr.loss_partials(), dtype=torch.float64,
                              device=g.device if g.is_cuda else "cpu")
         if multi:
@@ -167,6 +173,7 @@ class SlabShardedStep:
         self._mapped = []
         if self.put:
             self._map_peers()
+            trainer.use_graph(True)
 
     def _map_peers(self):
         from . import holo
@@ -199,16 +206,22 @@ class SlabShardedStep:
         else:
             recv[:sum(rc)].copy_(send[:sum(sc)])
 
-    def step(self) -> float:
-        for e in range(4):
-            self.tr.slab_stage(e)
-            self._exchange(e)
-        self.tr.slab_stage(4)
+    def step(self, with_loss: bool = True):
+        """One step; returns the loss (a host sync) or None when with_loss is False."""
+        if self.put:  # the stages synchronise on device flags: one call, one CUDA graph
+            self.tr.slab_forward_backward()
+        else:
+            for e in range(4):
+                self.tr.slab_stage(e)
+                self._exchange(e)
+            self.tr.slab_stage(4)
         g = self.tr.grads_tensor()
         multi = dist.is_initialized() and dist.get_world_size(self.group) > 1
         if multi:
             dist.all_reduce(g, op=dist.ReduceOp.SUM, group=self.group)
         self.tr.apply_update()
+        if not with_loss:
+            return None
         parts = torch.tensor(self.tr.loss_partials(), dtype=torch.float64, device=g.device)
         if self.put and self.tr.slab_status():
             raise RuntimeError("row slab: a peer-put exchange timed out waiting for a peer")
@@ -250,7 +263,7 @@ class LocalSlabGroup:
                 off += sc[r]
             assert off == sum(self.counts[r][e][1]) and len(sc) == R
 
-    def step(self) -> float:
+    def step(self, with_loss: bool = True):
         for e in range(4):
             for t in self.trs:
                 t.slab_stage(e)
@@ -265,6 +278,8 @@ class LocalSlabGroup:
             g.copy_(total)
         for t in self.trs:
             t.apply_update()
+        if not with_loss:
+            return None
         parts = [t.loss_partials() for t in self.trs]
         if self.put and any(t.slab_status() for t in self.trs):
             raise RuntimeError("row slab: a peer-put exchange timed out waiting for a peer")

@@ -1,8 +1,8 @@
 """Row-slab peer-put exchange across PROCESSES (the multi-GPU code path): two
 ranks in two processes on one B200 map each other's receive buffers and flag
 arrays with CUDA IPC (hs_ipc_*), store their transposes straight into them and
-synchronise on the device flags; gloo carries only the handle exchange and the
-gradient sum.  Checked against an unsharded trainer on the same scene."""
+synchronise on the device flags inside one captured CUDA graph per step; gloo
+carries only the handle exchange and the gradient sum.  Checked against an unsharded trainer on the same scene."""
 import os
 import socket
 
@@ -11,7 +11,7 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-W, H, C, N, L, STEPS = 64, 48, 3, 400, 1, 2
+W, H, C, N, L, STEPS = 64, 48, 3, 400, 1, 3
 
 
 def _free_port():
@@ -38,15 +38,16 @@ def _worker(rank, world, port, q):
     from paper_2511_15022_b200 import holo, parallel as P, synthetic as S
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
+    side = torch.cuda.Stream()  # a capturable stream: the step runs as one CUDA graph
+    torch.cuda.set_stream(side)
     try:
         gs, target, masks, dists, spec = _scene(holo, S)
         tr = holo.Trainer(gs, W, H, target, masks, dists, spec, 10)
         tr.set_row_slab(rank, world)
-        step = P.SlabShardedStep(tr, C, H, W, L, exchange="put")  # IPC mapping of the peers
+        step = P.SlabShardedStep(tr, C, H, W, L, exchange="put")  # IPC mapping of the peers, graphs on
         losses = []
         for _ in range(STEPS):
-            for e in range(5):
-                tr.slab_stage(e)
+            tr.slab_forward_backward()  # stages 0..4 as one captured graph, device-flag sync
             g = tr.grads_tensor()
             gh = g.cpu()
             dist.all_reduce(gh)
