@@ -724,6 +724,16 @@ void intensity_launch(const float2* f, int64_t count, float* out, cudaStream_t s
     launch_check("intensity");
 }
 
+// float4 work items per thread of the fused Adan (HS_ADAN_PER; 2 measured best: 28.7 -> 26.6 us at cfg2)
+static unsigned adan_grid(int64_t items) {
+    static const int per = [] {
+        const char* e = std::getenv("HS_ADAN_PER");
+        return e ? std::max(1, std::atoi(e)) : 2;
+    }();
+    const int64_t b = (items + 256LL * per - 1) / (256LL * per);
+    return static_cast<unsigned>(std::max<int64_t>(1, b));
+}
+
 void adan_fused_launch(float* params, const float* grads, float* state, int64_t P,
                        const AdanGroups& g, int total_steps, double b1, double b2, double b3,
                        double eps, int* d_step, const uint32_t* d_flags, cudaStream_t st) {
@@ -733,8 +743,8 @@ void adan_fused_launch(float* params, const float* grads, float* state, int64_t 
     unsigned* done = reinterpret_cast<unsigned*>(d_step + 2);
     GroupConst* kc = reinterpret_cast<GroupConst*>(d_step + 4);
     if (vec)
-        adan_fused_kernel<true><<<grid_for(P / 4, 256), 256, 0, st>>>(params, grads, state, P, g, total_steps, b1, b2,
-                                                                      b3, eps, d_step, d_flags, done, kc);
+        adan_fused_kernel<true><<<adan_grid(P / 4), 256, 0, st>>>(params, grads, state, P, g, total_steps, b1, b2,
+                                                                  b3, eps, d_step, d_flags, done, kc);
     else
         adan_fused_kernel<false><<<grid_for(P, 256), 256, 0, st>>>(params, grads, state, P, g, total_steps, b1, b2,
                                                                    b3, eps, d_step, d_flags, done, kc);
