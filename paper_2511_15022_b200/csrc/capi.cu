@@ -664,14 +664,24 @@ hs_status hs_trainer_reserve_pairs(hs_trainer* t, int64_t cap) {
             cudaGraphExecDestroy(t->graph);
             t->graph = nullptr;
         }
+        if (t->slab_graph) {
+            cudaGraphExecDestroy(t->slab_graph);
+            t->slab_graph = nullptr;
+        }
+        if (t->host_graph) {
+            cudaGraphExecDestroy(t->host_graph);
+            t->host_graph = nullptr;
+        }
     });
 }
 
 hs_status hs_trainer_use_graph(hs_trainer* t, int enable) {
     t->use_graph = enable != 0;
-    if (!t->use_graph && t->graph) {
-        cudaGraphExecDestroy(t->graph);
-        t->graph = nullptr;
+    if (!t->use_graph) {
+        for (cudaGraphExec_t* g : {&t->graph, &t->host_graph, &t->slab_graph}) {
+            if (*g) cudaGraphExecDestroy(*g);
+            *g = nullptr;
+        }
     }
     return HS_OK;
 }
@@ -1017,6 +1027,10 @@ extern "C" hs_status hs_trainer_slab_set_peers(hs_trainer* t, float* const* recv
             t->s_peer_flags[a] = flags[a];
         }
         t->s_put = true;
+        if (t->slab_graph) {  // the captured step holds the previous peer addresses
+            HS_CUDA(cudaGraphExecDestroy(t->slab_graph));
+            t->slab_graph = nullptr;
+        }
     });
 }
 
