@@ -415,3 +415,29 @@ def test_trainer_step_host_matches_device_step(holo):
     lb = b.step_host(host, host)
     assert lb == la
     assert np.array_equal(host.numpy(), pa)
+
+
+def test_reserve_pairs_recaptures_the_step_graphs(holo):
+    """Growing the tile-pair capacity reallocates the id buffers: the captured
+    step graphs (device step and host-resident step) must be re-captured, so
+    graph-replayed steps keep matching eager steps bit for bit."""
+    import torch
+    c, w, h, n, L = 3, 64, 48, 400, 1
+    g = f32(S.init_gaussians(n, c, w, h, 9))
+    img = S.synthetic_image(42, c, h, w)
+    masks = S.build_masks(S.synthetic_depth(43, h, w), L, True)
+    dist = S.make_depth_planes(L, 3e-3, 2e-3)
+    mk = lambda: holo.Trainer(holo.GaussianSet(n, c, **g), w, h, holo.RealField(c, h, w, img), masks, dist,
+                              holo.PropagationSpec(), 10)
+    eager, graphed = mk(), mk()
+    graphed.use_graph(True)
+    host = torch.from_numpy(graphed.params().copy()).pin_memory()
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        for i in range(4):
+            if i == 2:
+                graphed.reserve_pairs(1 << 22)
+            le = eager.step(sync_loss=True)
+            lg = graphed.step_host(host, host)
+            assert lg == le, (i, lg, le)
+            assert np.array_equal(host.numpy(), eager.params()), i
