@@ -1,0 +1,42 @@
+"""bench.py's byte model: the per-step algorithmic bytes the
+roofline fraction divides by, and the per-kernel split, on CPU."""
+import importlib.util
+import os
+
+import pytest
+
+from paper_2511_15022_b200 import synthetic as S
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _bench():
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(ROOT, "bench.py"))
+    m = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(m)
+    return m
+
+
+def test_step_bytes_match_survey_numbers():
+    b = _bench()
+    # cfg2 1.41 GB (K = 1.91M pairs at init), cfg3 5.59 GB, cfg4 5.79 GB
+    assert b.algorithmic_bytes(S.CONFIGS["cfg2"], 1_910_593) == pytest.approx(1.41e9, rel=5e-3)
+    assert b.algorithmic_bytes(S.CONFIGS["cfg3"], 1_910_593) == pytest.approx(5.59e9, rel=5e-3)
+    assert b.algorithmic_bytes(S.CONFIGS["cfg4"], 7_868_668) == pytest.approx(5.79e9, rel=1e-2)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4"])
+def test_kernel_bytes_cover_the_field_passes(name):
+    """The ASM and loss slots of kernel_bytes add up to the C (13 + 12 L) A field
+    term of the step model (raster fwd/bwd carry one A each), less the target
+    read the model books twice (in F3's loss epilogue and in SSIM) and the
+    fused loss kernel reads once."""
+    b = _bench()
+    cfg = S.CONFIGS[name]
+    A = 8.0 * cfg["height"] * cfg["width"]
+    c, L = cfg["channels"], cfg["planes"]
+    kb = b.kernel_bytes(cfg, 0)
+    field = sum(kb[k] for k in ("rows_fwd", "cols_fwd", "rows_inv", "loss_ssim", "rows_fwd_bwd", "cols_bwd",
+                                "rows_inv_bwd"))
+    field -= L * cfg["height"] * cfg["width"]  # the masks ride with the loss slot
+    assert field + 2 * c * A + 0.5 * c * A == pytest.approx(c * (13 + 12 * L) * A, rel=1e-12)
