@@ -441,3 +441,20 @@ def test_reserve_pairs_recaptures_the_step_graphs(holo):
             lg = graphed.step_host(host, host)
             assert lg == le, (i, lg, le)
             assert np.array_equal(host.numpy(), eager.params()), i
+
+
+def test_trainer_nonfinite_gradient_raises_and_keeps_params(holo):
+    """A NaN in the target poisons every gradient: like Adan::step on the first
+    group (optimizer.cpp:52-54, groups named as pipeline.cpp:244-249) the step
+    raises naming "position", and no group is updated."""
+    c, w, h, n, L = 3, 64, 48, 300, 1
+    g = f32(S.init_gaussians(n, c, w, h, 3))
+    img = S.synthetic_image(42, c, h, w).copy()
+    img[1, 10, 10] = np.nan
+    masks = S.build_masks(S.synthetic_depth(43, h, w), L, True)
+    tr = holo.Trainer(holo.GaussianSet(n, c, **g), w, h, holo.RealField(c, h, w, img), masks,
+                      S.make_depth_planes(L, 3e-3, 2e-3), holo.PropagationSpec(), 10)
+    p0 = tr.params()
+    with pytest.raises(holo.HoloNonFinite, match="group position"):
+        tr.step(sync_loss=True)
+    assert np.array_equal(tr.params(), p0)
