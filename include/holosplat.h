@@ -205,6 +205,10 @@ hs_status hs_trainer_step_host(hs_trainer* tr, const float* h_params_in, float* 
  * (after the caller all-reduced hs_trainer_grads_ptr) the optimizer update. */
 hs_status hs_trainer_forward_backward(hs_trainer* tr);
 hs_status hs_trainer_apply_update(hs_trainer* tr);
+/* After the caller summed the gradient buffer over ranks: re-derive the
+ * per-group non-finite bits from the sum, so every rank skips the same groups
+ * (Adan::step throws on the first non-finite group, optimizer.cpp:52-54). */
+hs_status hs_trainer_check_grads(hs_trainer* tr);
 hs_status hs_trainer_last_loss(hs_trainer* tr, double* loss_out, int64_t* npairs_out);
 /* Loss partial sums of this rank (recon sum, ssim sum) for cross-rank loss. */
 hs_status hs_trainer_loss_partials(hs_trainer* tr, double* out2);

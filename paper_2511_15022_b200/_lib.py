@@ -110,6 +110,7 @@ _SIGS = {
     "hs_trainer_step": [C.c_void_p, C.POINTER(C.c_double)],
     "hs_trainer_forward_backward": [C.c_void_p],
     "hs_trainer_apply_update": [C.c_void_p],
+    "hs_trainer_check_grads": [C.c_void_p],
     "hs_trainer_last_loss": [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)],
     "hs_trainer_loss_partials": [C.c_void_p, C.POINTER(C.c_double)],
     "hs_trainer_reserve_pairs": [C.c_void_p, C.c_int64],

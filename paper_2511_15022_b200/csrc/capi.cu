@@ -698,6 +698,15 @@ hs_status hs_trainer_forward_backward(hs_trainer* t) {
     });
 }
 
+// After a cross-rank gradient all-reduce: re-derive the non-finite group bits
+// from the summed buffer, so every rank takes the same decision (a rank's own
+// partial may be finite while the sum is not).
+hs_status hs_trainer_check_grads(hs_trainer* t) {
+    return guard([&] {
+        group_nonfinite_launch(t->grads.as<float>(), t->P, t->groups, t->flags.as<uint32_t>(), t->ctx->stream);
+    });
+}
+
 hs_status hs_trainer_apply_update(hs_trainer* t) {
     return guard([&] {
         trainer_enqueue_update(t, t->ctx->stream);

@@ -769,6 +769,31 @@ void adan_group_launch(float* params, const float* grads, float* state, int64_t 
     launch_check("adan_group");
 }
 
+namespace {
+// per-group non-finite bits of a flat gradient buffer (bit k: group k)
+__global__ void group_nonfinite_kernel(const float* __restrict__ g, int64_t P, AdanGroups G, uint32_t* flags) {
+    uint32_t bits = 0;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < P;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        if (!isfinite(g[i])) {
+            int gi = 0;
+#pragma unroll
+            for (int k = 1; k < 6; ++k) gi += (i >= G.begin[k]) ? 1 : 0;
+            bits |= 1u << gi;
+        }
+    }
+    bits = __reduce_or_sync(0xffffffffu, bits);
+    if ((threadIdx.x & 31) == 0 && bits) atomicOr(flags, bits);
+}
+}  // namespace
+
+void group_nonfinite_launch(const float* g, int64_t P, const AdanGroups& G, uint32_t* flags, cudaStream_t st) {
+    HS_CUDA(cudaMemsetAsync(flags, 0, sizeof(uint32_t), st));
+    if (P == 0) return;
+    group_nonfinite_kernel<<<grid_for(P, 256), 256, 0, st>>>(g, P, G, flags);
+    launch_check("group_nonfinite");
+}
+
 void nonfinite_launch(const float* g, int64_t n, uint32_t* flag, cudaStream_t st) {
     if (n == 0) return;
     nonfinite_kernel<<<grid_for(n, 256), 256, 0, st>>>(g, n, flag);

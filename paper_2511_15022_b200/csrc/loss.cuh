@@ -90,5 +90,7 @@ void adan_group_launch(float* params, const float* grads, float* state, int64_t 
                        double lr, double b1, double b2, double b3, double eps, cudaStream_t st);
 // Non-finite check of a gradient array -> flag word (bit 0).
 void nonfinite_launch(const float* g, int64_t n, uint32_t* flag, cudaStream_t st);
+// Per-group non-finite bits of the summed gradient buffer -> *flags (reset first).
+void group_nonfinite_launch(const float* g, int64_t P, const AdanGroups& G, uint32_t* flags, cudaStream_t st);
 
 }  // namespace hs

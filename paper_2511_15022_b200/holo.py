@@ -861,6 +861,11 @@ class Trainer:
         ctx_handle()
         check(_lib.load().hs_trainer_apply_update(self.h))
 
+    def check_grads(self):
+        """After a cross-rank sum of grads_tensor(): recompute the non-finite group bits."""
+        ctx_handle()
+        check(_lib.load().hs_trainer_check_grads(self.h))
+
     def last_loss(self):
         v = C.c_double(0.0)
         k = C.c_int64(0)

@@ -95,6 +95,7 @@ class ShardedStep:
             if g.is_cuda:
                 torch.cuda.current_stream().synchronize()
             dist.all_reduce(g, op=dist.ReduceOp.SUM, group=self.group)
+            self.tr.check_grads()
         self.tr.apply_update()
         if not with_loss:
             return None
@@ -219,6 +220,7 @@ class SlabShardedStep:
         multi = dist.is_initialized() and dist.get_world_size(self.group) > 1
         if multi:
             dist.all_reduce(g, op=dist.ReduceOp.SUM, group=self.group)
+            self.tr.check_grads()
         self.tr.apply_update()
         if not with_loss:
             return None
@@ -277,6 +279,7 @@ class LocalSlabGroup:
         for g in grads:
             g.copy_(total)
         for t in self.trs:
+            t.check_grads()
             t.apply_update()
         if not with_loss:
             return None

@@ -94,6 +94,9 @@ class FakeTrainer:
     def grads_tensor(self):
         return self.g
 
+    def check_grads(self):  # the summed-gradient non-finite check (device side in the real trainer)
+        pass
+
     def apply_update(self):
         self.applied = self.g.clone()
 

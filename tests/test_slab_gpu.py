@@ -139,3 +139,27 @@ def test_slab_layout_errors(holo):
     # exchange 1 carries each peer's loss band: rank 0 rows [0, 34), rank 1 rows [14, 48)
     assert t.slab_counts(0) == ([2 * 4 * 16 * 24] * 2, [2 * 4 * 16 * 24] * 2)
     assert t.slab_counts(1) == ([2 * 4 * 16 * 34] * 2, [2 * 4 * 16 * 34] * 2)
+
+
+def test_sharded_nonfinite_is_decided_on_the_summed_gradient(holo):
+    """A NaN that only one slab rank sees: after the gradient sum every rank
+    re-derives the non-finite groups (hs_trainer_check_grads), so all ranks
+    refuse the same update instead of diverging."""
+    from paper_2511_15022_b200 import parallel as P
+    gs, target, masks, dist, spec = scene(holo, 400, 3, 64, 48, 1)
+    vals = target.values.copy()
+    vals[0, 40, 30] = np.nan  # inside rank 1's rows only (rows 24..47 of 48)
+    bad = holo.RealField(3, 48, 64, vals)
+    trs = []
+    for r in range(2):
+        t = holo.Trainer(gs, 64, 48, bad, masks, dist, spec, 10)
+        t.set_row_slab(r, 2)
+        trs.append(t)
+    p0 = [t.params() for t in trs]
+    grp = P.LocalSlabGroup(trs, 3, 48, 64, 1, put=True)
+    with pytest.raises(holo.HoloNonFinite):
+        grp.step()
+        for t in trs:
+            t.last_loss()  # raises on the non-finite flag
+    for t, p in zip(trs, p0):
+        assert np.array_equal(t.params(), p)
