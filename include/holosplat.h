@@ -80,7 +80,7 @@ hs_status hs_rasterize_forward(hs_ctx* ctx, const float* d_params, int n, int c,
 hs_status hs_rasterize_backward(hs_ctx* ctx, const float* d_params, int n, int c, int width,
                                 int height, const float* d_grad_field, float* d_grads);
 
-/* ---- propagation (propagation.hpp:9-49, propagation.cpp:97-243) -------------- */
+/* ---- propagation (propagation.hpp:9-49, propagation.cpp:54-243) -------------- */
 typedef struct {
     const double* wavelengths; /* one per channel, metres */
     int n_wavelengths;
@@ -89,9 +89,9 @@ typedef struct {
     double aperture_radius;    /* padded-frequency-grid pixels; 0 disables */
 } hs_prop_spec;
 
-/* mode 0: propagate(distance)            (propagation.cpp:225-228)
- * mode 1: propagate_with_mask_distance    (:230-233)
- * mode 2: propagate_backward(distance)    (:235-238) */
+/* mode 0: propagate(distance)            (propagation.cpp:174-177)
+ * mode 1: propagate_with_mask_distance    (:179-182)
+ * mode 2: propagate_backward(distance)    (:184-187) */
 hs_status hs_propagate(hs_ctx* ctx, const hs_prop_spec* spec, int mode, double distance,
                        double mask_distance, const float* d_in, int c, int h, int w,
                        float* d_out);
@@ -103,7 +103,7 @@ hs_status hs_propagate_multi_backward(hs_ctx* ctx, const hs_prop_spec* spec,
                                       const double* h_distances, int L, const float* d_grads,
                                       int c, int h, int w, float* d_out);
 
-/* ---- loss (loss.hpp:10-67, loss.cpp:223-398) ----------------------------------- */
+/* ---- loss (loss.hpp:10-67, loss.cpp:154-369) ----------------------------------- */
 /* intensity_of: |u|^2 (field_core.cpp:88-93); count complex elements. */
 hs_status hs_intensity(hs_ctx* ctx, const float* d_field, int64_t count, float* d_out);
 /* kind 0 training_loss_grad, 1 loss_recon_grad, 2 loss_ssim_grad, 3 loss_mse_grad.
@@ -116,24 +116,24 @@ hs_status hs_loss(hs_ctx* ctx, int kind, int L, int c, int h, int w, const float
  * d_recon L x C x H x W intensities, d_target C x H x W; h_psnr, h_ssim L doubles. */
 hs_status hs_compute_metrics(hs_ctx* ctx, int L, int c, int h, int w, const float* d_recon,
                              const float* d_target, double* h_psnr, double* h_ssim);
-/* build_masks (loss.cpp:235-249) on the host, bit-exact. */
+/* build_masks (loss.cpp:166-180) on the host, bit-exact. */
 hs_status hs_build_masks(const double* h_depth, int h, int w, int L, int near_is_high,
                          uint8_t* h_masks);
 
-/* ---- optimizer (optimizer.hpp:10-49, optimizer.cpp:59-123) --------------------- */
+/* ---- optimizer (optimizer.hpp:10-49, optimizer.cpp:8-72) --------------------- */
 typedef struct {
     double beta1, beta2, beta3, eps;
 } hs_adan_config;
 
 /* One Adan step for one group: d_state holds 4*size floats [m | v | n | g_prev].
  * step_t is the group's 1-based step after increment.  The non-finite check
- * happens before any update (optimizer.cpp:103-105): on a non-finite gradient
+ * happens before any update (optimizer.cpp:52-54): on a non-finite gradient
  * nothing is modified and HS_ENONFINITE is returned with group_name in the
  * message. */
 hs_status hs_adan_step(hs_ctx* ctx, const hs_adan_config* cfg, const char* group_name,
                        float* d_params, const float* d_grads, float* d_state, int64_t size,
                        int step_t, double lr);
-/* cosine_lr (optimizer.cpp:59-64). */
+/* cosine_lr (optimizer.cpp:8-13). */
 hs_status hs_cosine_lr(int step, int total_steps, double lr_max, double lr_min, double* out);
 
 /* ---- phase-only hologram conversion (convert.hpp, convert.cpp:20-184) ------------ */
@@ -209,6 +209,12 @@ hs_status hs_trainer_apply_update(hs_trainer* tr);
  * per-group non-finite bits from the sum, so every rank skips the same groups
  * (Adan::step throws on the first non-finite group, optimizer.cpp:52-54). */
 hs_status hs_trainer_check_grads(hs_trainer* tr);
+/* Device word of the step's non-finite gradient groups (bit g = group g, in
+ * the order of pipeline.cpp:244-249).  hs_trainer_apply_update skips every
+ * group from the lowest set bit on, as the reference's Adan::step throw does
+ * (optimizer.cpp:52-54).  Sharded callers make the ranks agree on it (keep
+ * only the lowest bit, min-reduce across ranks) before the update. */
+uint32_t* hs_trainer_flags_ptr(hs_trainer* tr);
 hs_status hs_trainer_last_loss(hs_trainer* tr, double* loss_out, int64_t* npairs_out);
 /* Loss partial sums of this rank (recon sum, ssim sum) for cross-rank loss. */
 hs_status hs_trainer_loss_partials(hs_trainer* tr, double* out2);
@@ -261,6 +267,9 @@ uint32_t* hs_trainer_slab_flags_ptr(hs_trainer* tr);
 hs_status hs_trainer_slab_set_peers(hs_trainer* tr, float* const* recv0, float* const* recv1,
                                     uint32_t* const* flags);
 hs_status hs_trainer_slab_status(hs_trainer* tr, uint32_t* error);
+/* Device address of the peer-put timeout word hs_trainer_slab_status reads
+ * (sticky until hs_trainer_set_row_slab; NULL without row slabs). */
+uint32_t* hs_trainer_slab_error_ptr(hs_trainer* tr);
 /* Peer-put mode: stages 0..4 in one call (no host step between them; the
  * exchange epochs are device counters), replayed as one CUDA graph when
  * hs_trainer_use_graph is on.  Follow with the gradient all-reduce and

@@ -101,7 +101,7 @@ def split(flat, n, c):
     return out
 
 
-def activate_flat(g, n, c, width, height):   # :33-88
+def activate_flat(g, n, c, width, height):   # rasterizer.cpp:33-88
     pp, ps = np.asarray(g["pre_position"]), np.asarray(g["pre_scale"])
     f = {}
     f["px"] = activate_position(pp[0::2], width)
@@ -125,7 +125,7 @@ def activate_flat(g, n, c, width, height):   # :33-88
     return f
 
 
-def build_tile_index(g, n, c, width, height):  # :90-126
+def build_tile_index(g, n, c, width, height):  # rasterizer.cpp:90-126
     if width <= 0 or height <= 0:
         raise ValueError("build_tile_index: empty canvas")
     f = activate_flat(g, n, c, width, height)
@@ -261,12 +261,12 @@ def rasterize_backward(g, n, c, grad_re, grad_im):  # :192-286
 
 
 # ---- propagation.cpp ----------------------------------------------------------------------
-def wrapped_freq_index(k, n):                # :95
+def wrapped_freq_index(k, n):                # :44
     k = np.asarray(k)
     return np.where(k < n - n // 2, k, k - n)
 
 
-def make_band_limit(wavelengths, pitch, mask_distance, channel, pnx, pny):  # :105-121
+def make_band_limit(wavelengths, pitch, mask_distance, channel, pnx, pny):  # make_band_limit :54-70, kz_of :72-75
     if channel < 0 or channel >= len(wavelengths):
         raise ValueError("propagation: channel has no wavelength")
     lam = wavelengths[channel]
@@ -278,7 +278,7 @@ def make_band_limit(wavelengths, pitch, mask_distance, channel, pnx, pny):  # :1
                 fy_max=1.0 / (lam * math.sqrt((2.0 * mask_distance / ly) ** 2 + 1.0)))
 
 
-def transfer(b, ny, nx, phase_distance, aperture):  # apply_transfer :130-160 as a multiplier
+def transfer(b, ny, nx, phase_distance, aperture):  # apply_transfer :79-109 as a multiplier
     my = wrapped_freq_index(np.arange(ny), ny)[:, None]
     mx = wrapped_freq_index(np.arange(nx), nx)[None, :]
     fy, fx = my * b["inv_ly"], mx * b["inv_lx"]
@@ -293,7 +293,7 @@ def transfer(b, ny, nx, phase_distance, aperture):  # apply_transfer :130-160 as
     return H
 
 
-def _pad(u, py, px):                         # pad_center :162-168
+def _pad(u, py, px):                         # pad_center :111-117
     h, w = u.shape
     buf = np.zeros((py, px), dtype=np.complex128)
     oy, ox = (py - h) // 2, (px - w) // 2
@@ -301,20 +301,20 @@ def _pad(u, py, px):                         # pad_center :162-168
     return buf
 
 
-def _crop(buf, h, w):                        # crop_center :170-178
+def _crop(buf, h, w):                        # crop_center :119-127
     py, px = buf.shape
     oy, ox = (py - h) // 2, (px - w) // 2
     return buf[oy:oy + h, ox:ox + w]
 
 
-def _check_spec(c, wavelengths, pad):        # :180-184
+def _check_spec(c, wavelengths, pad):        # check_spec :129-133
     if c != len(wavelengths):
         raise ValueError("propagation: channel count does not match wavelengths")
     if pad < 1:
         raise ValueError("propagation: pad_factor must be >= 1")
 
 
-def propagate_impl(u, wavelengths, pitch, pad, aperture, phase_d, mask_d):  # :186-204
+def propagate_impl(u, wavelengths, pitch, pad, aperture, phase_d, mask_d):  # :135-153
     c, h, w = u.shape
     _check_spec(c, wavelengths, pad)
     px, py = w * pad, h * pad
@@ -326,17 +326,17 @@ def propagate_impl(u, wavelengths, pitch, pad, aperture, phase_d, mask_d):  # :1
     return out
 
 
-def propagate(u, wavelengths, pitch, pad, aperture, d):  # :225-228
+def propagate(u, wavelengths, pitch, pad, aperture, d):  # :174-177
     if not math.isfinite(d):
         raise ValueError("propagate: non-finite distance")
     return propagate_impl(u, wavelengths, pitch, pad, aperture, d, d)
 
 
-def propagate_backward(g, wavelengths, pitch, pad, aperture, d):  # :235-238
+def propagate_backward(g, wavelengths, pitch, pad, aperture, d):  # :184-187
     return propagate_impl(g, wavelengths, pitch, pad, aperture, -d, d)
 
 
-def propagate_multi(u, wavelengths, pitch, pad, aperture, distances):  # :240-263
+def propagate_multi(u, wavelengths, pitch, pad, aperture, distances):  # :189-212
     c, h, w = u.shape
     _check_spec(c, wavelengths, pad)
     px, py = w * pad, h * pad
@@ -349,7 +349,7 @@ def propagate_multi(u, wavelengths, pitch, pad, aperture, distances):  # :240-26
     return out
 
 
-def propagate_multi_backward(grads, wavelengths, pitch, pad, aperture, distances):  # :265-294
+def propagate_multi_backward(grads, wavelengths, pitch, pad, aperture, distances):  # :214-243
     L, c, h, w = grads.shape
     if L == 0 or L != len(distances):
         raise ValueError("propagate_multi_backward: plane count mismatch")
@@ -366,13 +366,13 @@ def propagate_multi_backward(grads, wavelengths, pitch, pad, aperture, distances
 
 
 # ---- loss.cpp -------------------------------------------------------------------------------
-def make_depth_planes(count, d0, dz):        # :223-233
+def make_depth_planes(count, d0, dz):        # :154-164
     if count < 1:
         raise ValueError("make_depth_planes: count must be >= 1")
     return [d0 + (l - (count - 1) * 0.5) * dz for l in range(count)]
 
 
-def build_masks(depth, L, near_is_high=True):  # :235-249
+def build_masks(depth, L, near_is_high=True):  # :166-180
     if L < 1:
         raise ValueError("build_masks: plane count must be >= 1")
     b = np.clip(np.floor(depth * L).astype(np.int64), 0, L - 1)
@@ -380,20 +380,20 @@ def build_masks(depth, L, near_is_high=True):  # :235-249
     return np.stack([(plane == l).astype(np.uint8) for l in range(L)])
 
 
-def ssim_window():                           # :89-100
+def ssim_window():                           # :20-31
     d = np.arange(kSsimWin) - kSsimWin // 2
     g = np.exp(-d * d / (2.0 * kSsimSigma ** 2))
     return g / g.sum()
 
 
-def _corr_valid(img, g):                     # window_mean :103-131 (x then y)
+def _corr_valid(img, g):                     # window_mean :56-62 (corr_x :34-42, then corr_y :45-53)
     h, w = img.shape
     vw, vh = w - g.size + 1, h - g.size + 1
     tmp = sum(g[j] * img[:, j:j + vw] for j in range(g.size))
     return sum(g[i] * tmp[i:i + vh, :] for i in range(g.size))
 
 
-def _spread(valid, h, w, g):                 # spread_t :135-152
+def _spread(valid, h, w, g):                 # spread_t :66-83
     vh, vw = valid.shape
     tmp = np.zeros((h, vw))
     for i in range(g.size):
@@ -404,7 +404,7 @@ def _spread(valid, h, w, g):                 # spread_t :135-152
     return out
 
 
-def ssim_channel(x, y, want_grad):           # :160-214
+def ssim_channel(x, y, want_grad):           # :91-145
     h, w = x.shape
     if h < kSsimWin or w < kSsimWin:
         raise ValueError("ssim: image smaller than the 11x11 window")
@@ -423,7 +423,7 @@ def ssim_channel(x, y, want_grad):           # :160-214
     return float(s.sum()), s.size, grad
 
 
-def _check_pair(recon, target, masks):       # :80-87
+def _check_pair(recon, target, masks):       # check_pair :11-18
     if len(recon) == 0:
         raise ValueError("loss: no reconstruction planes")
     if len(recon) != masks.shape[0]:
@@ -433,7 +433,7 @@ def _check_pair(recon, target, masks):       # :80-87
             raise ValueError("loss: reconstruction shape mismatch")
 
 
-def loss_recon_grad(recon, target, masks, L_norm=None, C_norm=None):  # :317-341
+def loss_recon_grad(recon, target, masks, L_norm=None, C_norm=None):  # :248-272
     _check_pair(recon, target, masks)
     L = len(recon) if L_norm is None else L_norm
     n = target.size if C_norm is None else target.size // target.shape[0] * C_norm  # channel shard: global C
@@ -443,14 +443,14 @@ def loss_recon_grad(recon, target, masks, L_norm=None, C_norm=None):  # :317-341
     return float(np.sum(d * d * k) / (n * L)), w * d * k
 
 
-def loss_mse_grad(recon, target, masks):     # :277-294
+def loss_mse_grad(recon, target, masks):     # loss.cpp:208-225
     _check_pair(recon, target, masks)
     L, n = len(recon), target.size
     d = recon - target[None]
     return float(np.sum(d * d) / (n * L)), (2.0 / (n * L)) * d
 
 
-def loss_ssim_grad(recon, target, masks, L_norm=None, C_norm=None):  # :361-383
+def loss_ssim_grad(recon, target, masks, L_norm=None, C_norm=None):  # loss.cpp:292-314
     _check_pair(recon, target, masks)
     total, count = 0.0, 0
     grads = np.zeros_like(recon)
@@ -467,20 +467,20 @@ def loss_ssim_grad(recon, target, masks, L_norm=None, C_norm=None):  # :361-383
     return 1.0 - total / count, grads * (-1.0 / count), total
 
 
-def training_loss_grad(recon, target, masks):  # :389-398
+def training_loss_grad(recon, target, masks):  # loss.cpp:320-329
     lr, gr = loss_recon_grad(recon, target, masks)
     ls, gs, _ = loss_ssim_grad(recon, target, masks)
     return lr + kSsimWeight * ls, gr + kSsimWeight * gs
 
 
 # ---- optimizer.cpp -----------------------------------------------------------------------------
-def cosine_lr(step, total, lr_max, lr_min):  # :59-64
+def cosine_lr(step, total, lr_max, lr_min):  # :8-13
     if total <= 0 or step < 0 or step > total:
         raise ValueError("cosine_lr: step outside [0, total_steps]")
     return lr_min + 0.5 * (lr_max - lr_min) * (1.0 + math.cos(math.pi * step / total))
 
 
-class Adan:                                  # :66-123
+class Adan:                                  # :15-72 (step :48-72)
     def __init__(self, beta1=0.98, beta2=0.92, beta3=0.99, eps=1e-8):
         self.b = (beta1, beta2, beta3)
         self.eps = eps

@@ -106,6 +106,7 @@ _SIGS = {
     "hs_trainer_get_params": [C.c_void_p, C.c_void_p, C.c_int],
     "hs_trainer_params_ptr": [C.c_void_p],
     "hs_trainer_grads_ptr": [C.c_void_p],
+    "hs_trainer_flags_ptr": [C.c_void_p],
     "hs_trainer_param_count": [C.c_void_p],
     "hs_trainer_step": [C.c_void_p, C.POINTER(C.c_double)],
     "hs_trainer_forward_backward": [C.c_void_p],
@@ -127,6 +128,7 @@ _SIGS = {
     "hs_trainer_slab_flags_ptr": [C.c_void_p],
     "hs_trainer_slab_set_peers": [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)],
     "hs_trainer_slab_status": [C.c_void_p, C.POINTER(C.c_uint32)],
+    "hs_trainer_slab_error_ptr": [C.c_void_p],
     "hs_trainer_slab_forward_backward": [C.c_void_p],
     "hs_random_uniform": [C.c_uint64, C.c_int64, C.c_double, C.c_double, C.c_void_p],
     "hs_ipc_get_handle": [C.c_void_p, C.c_void_p],
@@ -141,6 +143,8 @@ _RESTYPES = {
     "hs_kernel_launch_count": C.c_uint64,
     "hs_trainer_params_ptr": C.c_void_p,
     "hs_trainer_grads_ptr": C.c_void_p,
+    "hs_trainer_flags_ptr": C.c_void_p,
+    "hs_trainer_slab_error_ptr": C.c_void_p,
     "hs_trainer_slab_send_ptr": C.c_void_p,
     "hs_trainer_slab_recv_ptr": C.c_void_p,
     "hs_trainer_slab_recv2_ptr": C.c_void_p,

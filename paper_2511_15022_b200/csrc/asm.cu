@@ -2,9 +2,9 @@
 // column FFT x H(fx,fy,z,lambda) x column IFFT (all planes from one load), and
 // crop-aware row IFFT.
 //
-// Reference: proj/core/src/propagation.cpp -- pad_center/crop_center :162-178,
-// apply_transfer :130-160, make_band_limit/kz_of :105-126, propagate_impl
-// :186-204, propagate_multi :240-263, propagate_multi_backward :265-294.
+// Reference: proj/core/src/propagation.cpp -- pad_center/crop_center :111-127,
+// apply_transfer :79-109, make_band_limit/kz_of :54-75, propagate_impl
+// :135-153, propagate_multi :189-212, propagate_multi_backward :214-243.
 //
 // Data path per channel (Px = pad W, Py = pad H, centred offsets ox, oy):
 //   rows_fwd : H rows, zero-padded to Px, FFT_x          -> T1 (H x Px, column-tiled)
@@ -287,7 +287,7 @@ void AsmWork::set_transfer(const hs_prop_spec& spec, const double* phase_d, cons
             const double lambda = spec.wavelengths[c];
             require(lambda > 0.0 && spec.pixel_pitch > 0.0,
                     "propagation: non-positive wavelength or pitch");
-            // make_band_limit (propagation.cpp:105-121)
+            // make_band_limit (propagation.cpp:54-70)
             const double k = two_pi / lambda;
             const double lx = Px * spec.pixel_pitch, ly = Py * spec.pixel_pitch;
             const double inv_lx = 1.0 / lx, inv_ly = 1.0 / ly;
@@ -296,7 +296,7 @@ void AsmWork::set_transfer(const hs_prop_spec& spec, const double* phase_d, cons
             const double fy_max = 1.0 / (lambda * std::sqrt((2.0 * md / ly) * (2.0 * md / ly) + 1.0));
             auto max_m = [](double inv_l, double fmax, int nn) {
                 int m = 0;
-                // |m * inv_l| < fmax  (strict, :135 and :140)
+                // |m * inv_l| < fmax  (strict, propagation.cpp:84 and :89)
                 while (m <= nn && std::abs(static_cast<double>(m) * inv_l) < fmax) ++m;
                 return m - 1;  // -1: even DC is outside
             };

@@ -7,12 +7,12 @@
 namespace hs {
 
 // Per (channel, plane) transfer-function constants, built on the host in fp64
-// exactly like make_band_limit (propagation.cpp:105-121).
+// exactly like make_band_limit (propagation.cpp:54-70).
 struct TfConst {
     float kd_mod;   // fmod(k * phase_distance, 2 pi)
     float kd;       // k * phase_distance
     float bx, by;   // (2 pi / (nx pitch k))^2, (2 pi / (ny pitch k))^2
-    int mx_max, my_max;  // largest |m| inside the band limit (strict <, :140)
+    int mx_max, my_max;  // largest |m| inside the band limit (strict <, propagation.cpp:89)
     double a4;      // 4 * aperture^2, <= 0 disables the aperture (:149-159)
 };
 
@@ -37,11 +37,11 @@ struct AsmWork {
                       cudaStream_t st);
 };
 
-// forward: in C x H x W -> out L x C x H x W  (propagate_multi, :240-263)
+// forward: in C x H x W -> out L x C x H x W  (propagate_multi, propagation.cpp:189-212)
 // ev (nullable): 3 events recorded after each of the three kernels.
 void asm_forward(AsmWork& w, const float2* d_in, float2* d_out, cudaStream_t st,
                  cudaEvent_t* ev = nullptr);
-// backward: grads L x C x H x W -> out C x H x W (propagate_multi_backward, :265-294)
+// backward: grads L x C x H x W -> out C x H x W (propagate_multi_backward, propagation.cpp:214-243)
 // conj = true applies conj(H) (the adjoint); the transfer constants must be
 // those of the forward planes.
 void asm_backward(AsmWork& w, const float2* d_grads, float2* d_out, cudaStream_t st,

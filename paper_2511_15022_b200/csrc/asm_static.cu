@@ -1,6 +1,6 @@
 // Compile-time planned angular-spectrum kernels for the benchmark grids.
 //
-// Same data path and numerics contract as asm.cu (propagation.cpp:186-294),
+// Same data path and numerics contract as asm.cu (propagation.cpp:135-243),
 // with the FFT engine of fft_static.cuh: in-place stages, constant strides,
 // first stages read straight from global memory (zero pad skipped), last
 // stages write straight to global memory (crop skipped) or apply the transfer
@@ -543,7 +543,7 @@ __global__ void __launch_bounds__(NT, MINB) scols_bwd1_kernel(ColArgs a, const f
 // Multi-plane: one forward FFT per tile shared by all planes (spectrum kept in
 // a second shared buffer; each plane's inverse reads it through H_l); the
 // adjoint accumulates every plane's conj(H_l)-weighted spectrum straight from
-// its FFT's last stage before one inverse FFT (propagation.cpp:240-294).
+// its FFT's last stage before one inverse FFT (propagate_multi_backward propagation.cpp:214-243).
 template <int N, int CC, int NT, int MINB, class RAD>
 __global__ void __launch_bounds__(NT, MINB) scols_fwdL_kernel(ColArgs a, const float2* __restrict__ tw) {
     static_assert(NT % CC == 0, "column of a thread must be fixed");
@@ -666,35 +666,14 @@ const std::vector<Plans>& plans() {
         {512, 320, 4, row_plan<512, 1, 64, 4, Radices<8, 8, 8>>(), col_plan<320, 4, 128, 2, Radices<16, 20>>()},
         {7680, 4320, 2, row_plan<7680, 2, 512, 2, Radices<16, 30, 16>>(),
          col_plan<4320, 2, 360, 2, Radices<12, 30, 12>>()},
-        // tuning variants of the cfg2 grid (HS_FFT_VARIANT=k picks the k-th plan of a grid)
-        {3840, 2160, 4, row_plan<3840, 1, 256, 4, Radices<16, 15, 16>>(),
-         col_plan<2160, 4, 720, 2, Radices<12, 15, 12>>()},
-        {3840, 2160, 4, row_plan<3840, 1, 128, 4, Radices<16, 15, 16>>(),
-         col_plan<2160, 4, 360, 3, Radices<12, 15, 12>>()},
-        {3840, 2160, 4, row_plan<3840, 2, 256, 4, Radices<16, 15, 16>>(),
-         col_plan<2160, 4, 720, 2, Radices<12, 15, 12>>()},
-
     };
     return p;
 }
 
-int variant() {
-    static const int v = [] {
-        const char* e = std::getenv("HS_FFT_VARIANT");
-        return e ? std::atoi(e) : 0;
-    }();
-    return v;
-}
-
 const Plans* find(int Px, int Py) {
-    const Plans* first = nullptr;
-    int k = 0;
-    for (const auto& p : plans()) {
-        if (p.Px != Px || p.Py != Py) continue;
-        if (!first) first = &p;
-        if (k++ == variant()) return &p;
-    }
-    return first;
+    for (const auto& p : plans())
+        if (p.Px == Px && p.Py == Py) return &p;
+    return nullptr;
 }
 
 struct STwCache {
@@ -724,14 +703,6 @@ size_t cols_smem(const Plans& p, int L) {
 }
 int cols_threads(const Plans& p, int L) { return (L == 1 && p.col.nt1) ? p.col.nt1 : p.col.nt; }
 
-// bulk-copy staged column kernels (HS_COL_PERSIST=0 turns them off)
-bool persist_on() {
-    static const bool v = [] {
-        const char* e = std::getenv("HS_COL_PERSIST");
-        return e ? std::atoi(e) != 0 : true;
-    }();
-    return v;
-}
 size_t cols_smem_persist(const Plans& p, int H) {
     return cols_smem(p, 1) + sizeof(float2) * static_cast<size_t>(H) * p.col.cc + 16;
 }
@@ -739,7 +710,7 @@ size_t cols_smem_persist(const Plans& p, int H) {
 // Column pass launch: the staged kernels for a single plane when the plan has
 // them (KT tiles per CTA), else one CTA per (tile, channel).
 void launch_cols(const Plans* p, const AsmWork& w, bool backward, const ColArgs& c, cudaStream_t st) {
-    if (w.L == 1 && p->col.fwdP && persist_on()) {
+    if (w.L == 1 && p->col.fwdP) {
         const int total = c.ntiles * c.C;
         const int grid = (total + kPersistTiles - 1) / kPersistTiles;
         (backward ? p->col.bwdP : p->col.fwdP)<<<grid, p->col.nt1, cols_smem_persist(*p, w.H), st>>>(c, w.stw_y);

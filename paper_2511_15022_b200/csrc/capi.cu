@@ -294,7 +294,7 @@ extern "C" hs_status hs_propagate(hs_ctx* ctx, const hs_prop_spec* spec, int mod
     return guard([&] {
         check_spec(spec, c);
         if (mode == 0 || mode == 2)
-            require(std::isfinite(distance), "propagate: non-finite distance");  // :226
+            require(std::isfinite(distance), "propagate: non-finite distance");  // propagation.cpp:175
         double pd = distance, md = distance;
         if (mode == 1) md = mask_distance;
         if (mode == 2) pd = -distance;  // propagate_backward: phase -d, mask d (:237)
@@ -325,7 +325,7 @@ extern "C" hs_status hs_propagate_multi_backward(hs_ctx* ctx, const hs_prop_spec
                                       const double* h_distances, int L, const float* d_grads, int c,
                                       int h, int w, float* d_out) {
     return guard([&] {
-        require(L >= 1, "propagate_multi_backward: plane count mismatch");  // :268-269
+        require(L >= 1, "propagate_multi_backward: plane count mismatch");  // propagation.cpp:217-218
         check_spec(spec, c);
         AsmWork& aw = work_of(ctx).aw;
         aw.prepare(c, h, w, spec->pad_factor, L);
@@ -439,7 +439,7 @@ extern "C" hs_status hs_intensity(hs_ctx* ctx, const float* d_field, int64_t cou
 extern "C" hs_status hs_loss(hs_ctx* ctx, int kind, int L, int c, int h, int w, const float* d_recon,
                   const float* d_target, const uint8_t* d_masks, float* d_grads, double* loss) {
     return guard([&] {
-        require(L >= 1, "loss: no reconstruction planes");  // loss.cpp:81
+        require(L >= 1, "loss: no reconstruction planes");  // loss.cpp:12
         require(kind >= 0 && kind <= 3, "loss: unknown kind");
         CtxWork& cw = work_of(ctx);
         const int slots = loss_partial_slots(kind, L, c, h, w);
@@ -463,10 +463,10 @@ extern "C" hs_status hs_loss(hs_ctx* ctx, int kind, int L, int c, int h, int w, 
 
 extern "C" hs_status hs_build_masks(const double* h_depth, int h, int w, int L, int near_is_high, uint8_t* h_masks) {
     return guard([&] {
-        require(L >= 1, "build_masks: plane count must be >= 1");  // loss.cpp:236
+        require(L >= 1, "build_masks: plane count must be >= 1");  // loss.cpp:167
         const size_t n = static_cast<size_t>(h) * w;
         std::memset(h_masks, 0, n * L);
-        for (size_t i = 0; i < n; ++i) {  // loss.cpp:241-247
+        for (size_t i = 0; i < n; ++i) {  // loss.cpp:172-178
             int bin = static_cast<int>(std::floor(h_depth[i] * L));
             bin = std::min(std::max(bin, 0), L - 1);
             const int plane = near_is_high ? L - 1 - bin : bin;
@@ -479,7 +479,7 @@ extern "C" hs_status hs_build_masks(const double* h_depth, int h, int w, int L, 
 extern "C" hs_status hs_cosine_lr(int step, int total_steps, double lr_max, double lr_min, double* out) {
     return guard([&] {
         require(!(total_steps <= 0 || step < 0 || step > total_steps),
-                "cosine_lr: step outside [0, total_steps]");  // optimizer.cpp:60-61
+                "cosine_lr: step outside [0, total_steps]");  // optimizer.cpp:9-10
         *out = lr_min + 0.5 * (lr_max - lr_min) *
                             (1.0 + std::cos(3.14159265358979323846 * static_cast<double>(step) / total_steps));
     });
@@ -496,7 +496,7 @@ extern "C" hs_status hs_adan_step(hs_ctx* ctx, const hs_adan_config* cfg, const 
         uint32_t bad = 0;
         HS_CUDA(cudaMemcpyAsync(&bad, cw.flags.p, sizeof(bad), cudaMemcpyDeviceToHost, ctx->stream));
         HS_CUDA(cudaStreamSynchronize(ctx->stream));
-        if (bad)  // optimizer.cpp:103-105
+        if (bad)  // optimizer.cpp:52-54
             throw Error(HS_ENONFINITE, std::string("Adan: non-finite gradient in group ") +
                                            (group_name ? group_name : ""));
         adan_group_launch(d_params, d_grads, d_state, size, step_t, lr, k.beta1, k.beta2, k.beta3, k.eps,
@@ -654,6 +654,7 @@ hs_status hs_trainer_get_params(hs_trainer* t, float* params, int to_device) {
 
 float* hs_trainer_params_ptr(hs_trainer* t) { return t->params.as<float>(); }
 float* hs_trainer_grads_ptr(hs_trainer* t) { return t->grads.as<float>(); }
+uint32_t* hs_trainer_flags_ptr(hs_trainer* t) { return t->flags.as<uint32_t>(); }
 int64_t hs_trainer_param_count(hs_trainer* t) { return t->P; }
 int hs_trainer_step_count(hs_trainer* t) { return t->host_step; }
 
@@ -716,7 +717,7 @@ hs_status hs_trainer_apply_update(hs_trainer* t) {
 
 static void trainer_launch_step(hs_trainer* t) {
     {
-        // cosine_lr(step, steps, ...) throws past the horizon (optimizer.cpp:60-61)
+        // cosine_lr(step, steps, ...) throws past the horizon (optimizer.cpp:9-10)
         require(t->host_step <= t->total_steps, "cosine_lr: step outside [0, total_steps]");
         cudaStream_t st = t->ctx->stream;
         if (t->use_graph) {
@@ -1041,6 +1042,10 @@ extern "C" hs_status hs_trainer_slab_set_peers(hs_trainer* t, float* const* recv
             t->slab_graph = nullptr;
         }
     });
+}
+
+extern "C" uint32_t* hs_trainer_slab_error_ptr(hs_trainer* t) {
+    return t->R >= 1 ? t->s_flags.as<uint32_t>() + kMaxPeers : nullptr;
 }
 
 extern "C" hs_status hs_trainer_slab_status(hs_trainer* t, uint32_t* error) {

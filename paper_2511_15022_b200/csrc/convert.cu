@@ -8,7 +8,7 @@
 // plane's loss terms and dL/dU (plane_recon_loss + the guide's squared-
 // intensity and complex-L1 terms, convert.cpp:116-155), the ASM adjoint sums
 // the planes, and two elementwise kernels apply the chain rule through
-// e^{i phi} and the Adan update (optimizer.cpp:99-123; non-finite gradients
+// e^{i phi} and the Adan update (Adan::step optimizer.cpp:48-72; non-finite gradients
 // stop the updates and raise "Adan: non-finite gradient in group phase").  The
 // per-step loss is reduced on the device into a history buffer read once at the
 // end.  Canonicalisation into [0, 2 pi) happens on the host in fp64.
@@ -139,7 +139,7 @@ __global__ void poh_dphi_kernel(const float* __restrict__ phase, const float2* _
 }
 
 // Adan on the phase group; skipped entirely once a non-finite gradient was seen
-// (the reference throws before touching the parameters, optimizer.cpp:103-105).
+// (the reference throws before touching the parameters, optimizer.cpp:52-54).
 __global__ void poh_adan_kernel(float* __restrict__ phase, const float* __restrict__ dphi, float* __restrict__ st,
                                 int64_t n, int t, GroupConst k, float b1, float b2, float b3, float eps,
                                 const uint32_t* __restrict__ flag) {

@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <map>
 #include <mutex>
 #include <numbers>
 #include <random>
@@ -55,17 +56,57 @@ hs_ctx* ctx() {
     return c;
 }
 
-// RAII device buffer over hs_device_alloc.
+// Device buffers of the value-semantics calls come from a grow-only cache
+// (power-of-two size classes): after the first call of a given size the drop-in
+// performs no cudaMalloc/cudaFree (which would also synchronise the device).
+class DevPool {
+  public:
+    void* take(size_t bytes, size_t* cls) {
+        *cls = size_class(bytes);
+        {
+            std::lock_guard<std::mutex> lock(mu_);
+            auto it = free_.find(*cls);
+            if (it != free_.end() && !it->second.empty()) {
+                void* p = it->second.back();
+                it->second.pop_back();
+                return p;
+            }
+        }
+        void* p = nullptr;
+        check(hs_device_alloc(ctx(), *cls, &p));
+        return p;
+    }
+    void give(void* p, size_t cls) {
+        std::lock_guard<std::mutex> lock(mu_);
+        free_[cls].push_back(p);
+    }
+
+  private:
+    static size_t size_class(size_t b) {
+        size_t c = 256;
+        while (c < b) c <<= 1;
+        return c;
+    }
+    std::mutex mu_;
+    std::map<size_t, std::vector<void*>> free_;
+};
+
+DevPool& pool() {
+    static DevPool* p = new DevPool;  // never destroyed: outlives every Dev, no teardown-order hazards
+    return *p;
+}
+
+// RAII device buffer from the pool.
 struct Dev {
     void* p = nullptr;
-    size_t bytes = 0;
-    explicit Dev(size_t b) : bytes(b) { check(hs_device_alloc(ctx(), std::max<size_t>(b, 4), &p)); }
+    size_t bytes = 0, cls = 0;
+    explicit Dev(size_t b) : bytes(b) { p = pool().take(std::max<size_t>(b, 4), &cls); }
     ~Dev() {
-        if (p) hs_device_free(ctx(), p);
+        if (p) pool().give(p, cls);
     }
     Dev(const Dev&) = delete;
     Dev& operator=(const Dev&) = delete;
-    Dev(Dev&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; }
+    Dev(Dev&& o) noexcept : p(o.p), bytes(o.bytes), cls(o.cls) { o.p = nullptr; }
     template <class T>
     T* as() const { return static_cast<T*>(p); }
     void upload(const void* h, size_t b) { check(hs_copy_h2d(ctx(), p, h, b)); }
@@ -314,7 +355,7 @@ GaussianSetGrads rasterize_backward(const GaussianSet& set, const RealField& gra
 // ---- propagation ----------------------------------------------------------------------------------------
 std::vector<TransferFunctionSample> transfer_function(const PropagationSpec& spec, double distance, int channel,
                                                       int padded_nx, int padded_ny) {
-    // propagation.cpp:105-126 / :208-223 on the host (test-facing sampler)
+    // transfer_function, propagation.cpp:157-172 (make_band_limit :54-70, kz_of :72-75) on the host (test-facing sampler)
     if (padded_nx <= 0 || padded_ny <= 0) throw std::invalid_argument("transfer_function: non-positive dims");
     if (channel < 0 || channel >= static_cast<int>(spec.wavelengths.size()))
         throw std::invalid_argument("propagation: channel has no wavelength");
@@ -474,7 +515,7 @@ double training_loss_grad(const std::vector<RealField>& r, const TargetStack& t,
 }
 
 double plane_recon_loss(const RealField& recon, const TargetStack& target, size_t plane, RealField* grad) {
-    // loss.cpp:400-423: the single-plane recon term (w = 2/n)
+    // plane_recon_loss, loss.cpp:331-354: the single-plane recon term (w = 2/n)
     if (!recon.same_shape(target.intensity)) throw std::invalid_argument("plane_recon_loss: shape mismatch");
     if (plane >= target.masks.size()) throw std::invalid_argument("plane_recon_loss: plane out of range");
     TargetStack one{target.intensity, target.depth, MaskStack{target.masks[plane]}};
@@ -485,7 +526,7 @@ double plane_recon_loss(const RealField& recon, const TargetStack& target, size_
 }
 
 double ssim_value(const RealField& a, const RealField& b) {
-    // loss.cpp:425-438 = 1 - loss_ssim of one plane
+    // ssim_value, loss.cpp:356-369 = 1 - loss_ssim of one plane
     if (!a.same_shape(b)) throw std::invalid_argument("ssim_value: shape mismatch");
     TargetStack t{b, RealField(1, b.height, b.width), MaskStack(1, std::vector<uint8_t>(
                                                                   static_cast<size_t>(b.height) * b.width, 0))};
@@ -540,20 +581,24 @@ void Adan::set_lr(const std::string& name, double lr) { impl_->find(name).lr = l
 double Adan::lr(const std::string& name) const { return impl_->find(name).lr; }
 int Adan::step_count(const std::string& name) const { return impl_->find(name).t; }
 
+// The moments live on the device in fp32; the caller's fp64 parameters never
+// pass through fp32: the kernel runs on a zero "parameter" buffer, so it
+// returns -update, which is then applied to the fp64 values on the host
+// (optimizer.cpp:69: params[i] -= lr * (...) / denom).
 void Adan::step(const std::string& name, std::span<double> params, std::span<const double> grads) {
     Impl::Group& g = impl_->find(name);
     if (params.size() != g.size || grads.size() != g.size)
         throw std::invalid_argument("Adan: size mismatch for group " + name);
-    std::vector<float> p(params.begin(), params.end()), gr(grads.begin(), grads.end());
-    Dev dp(p.size() * 4), dg(gr.size() * 4);
-    dp.upload(p.data(), p.size() * 4);
+    std::vector<float> gr(grads.begin(), grads.end()), d(g.size, 0.f);
+    Dev dd(d.size() * 4), dg(gr.size() * 4);
+    dd.upload(d.data(), d.size() * 4);
     dg.upload(gr.data(), gr.size() * 4);
     hs_adan_config c{cfg_.beta1, cfg_.beta2, cfg_.beta3, cfg_.eps};
-    check(hs_adan_step(ctx(), &c, name.c_str(), dp.as<float>(), dg.as<float>(), static_cast<float*>(g.state),
+    check(hs_adan_step(ctx(), &c, name.c_str(), dd.as<float>(), dg.as<float>(), static_cast<float*>(g.state),
                        static_cast<int64_t>(g.size), g.t + 1, g.lr));
     g.t += 1;
-    dp.download(p.data(), p.size() * 4);
-    std::copy(p.begin(), p.end(), params.begin());
+    dd.download(d.data(), d.size() * 4);
+    for (size_t i = 0; i < g.size; ++i) params[i] += static_cast<double>(d[i]);
 }
 
 // ---- parallel (parallel.cpp:11-44) ---------------------------------------------------------------------------------

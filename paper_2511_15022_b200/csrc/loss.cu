@@ -1,9 +1,9 @@
 // Training loss + gradient (K6 epilogue, K7, K12) and fused Adan (K11).
 //
-// Reference: proj/core/src/loss.cpp -- loss_recon_grad :317-341, ssim_channel
-// :160-214 (window :89-100, corr_x/corr_y/window_mean :103-131, spread_t
-// :135-152), loss_ssim_grad :361-383, training_loss_grad :389-398,
-// loss_mse_grad :277-294; proj/core/src/optimizer.cpp:59-123 (cosine_lr, Adan).
+// Reference: proj/core/src/loss.cpp -- loss_recon_grad :248-272, ssim_channel
+// :91-145 (ssim_window :20-31, corr_x/corr_y/window_mean :34-62, spread_t
+// :66-83), loss_ssim_grad :292-314, training_loss_grad :320-329,
+// loss_mse_grad :208-225; proj/core/src/optimizer.cpp:8-72 (cosine_lr, Adan).
 //
 // SSIM kernel (sliding window): one CTA of 128 threads owns a strip of 118
 // output columns and SR output rows of one (plane, channel) and walks down
@@ -12,10 +12,10 @@
 //   1. correlates its input row horizontally (I, I^2, I t from a shared row),
 //   2. keeps the last 11 such rows in a register ring and correlates them
 //      vertically -> window means of valid row v, SSIM map and the three
-//      derivative maps g1, g2, g3 (ssim_channel :187-205),
+//      derivative maps g1, g2, g3 (ssim_channel loss.cpp:129-135),
 //   3. spreads g back horizontally from a shared row of its 10 left
 //      neighbours, keeps the last 11 spread rows in a second register ring and
-//      spreads vertically -> dSSIM/dI of output row v (spread_t :135-152),
+//      spreads vertically -> dSSIM/dI of output row v (spread_t loss.cpp:66-83),
 //   4. fuses the recon term (I - t)^2 (1 + M + t^2) and, in trainer mode,
 //      dL/dU = 2 U dL/dI (pipeline.cpp:265-274).
 // Every input row is read once per strip (no vertical halo re-reads beyond
@@ -47,7 +47,7 @@ struct Win {
     float g[kWin];
 };
 
-Win ssim_window_f32() {  // loss.cpp:89-100
+Win ssim_window_f32() {  // ssim_window, loss.cpp:20-31
     Win w;
     double g[kWin], sum = 0.0;
     for (int i = 0; i < kWin; ++i) {
@@ -70,7 +70,7 @@ __device__ __forceinline__ float load_I(const LossArgs& a, size_t idx) {
 
 // Target window statistics on the valid grid, per channel: (mu2, sigma2^2) =
 // (E_w[t], E_w[t^2] - E_w[t]^2) -- constant over an optimisation run, so the
-// trainer computes them once (ssim_channel :173-176, :190).
+// trainer computes them once (ssim_channel loss.cpp:105, :107).
 __global__ void ssim_target_stats_kernel(const float* __restrict__ target, int C, int H, int W, Win win,
                                          float2* __restrict__ out) {
     const int vh = H - kWin + 1, vw = W - kWin + 1;
@@ -267,7 +267,7 @@ struct SsimCta {
         const int r = v + kHalo;
         const int buf = s & 1;
         issue(r + kPD, v + kPD);
-        {  // ssim_channel corr_x (loss.cpp:103-111)
+        {  // ssim_channel corr_x (loss.cpp:34-42)
             const float4* row = &S.in[buf][t];
             corr11x3(win, [&](int j) { return row[j]; }, st.r01[U], st.r2[U]);
         }
@@ -307,7 +307,7 @@ struct SsimCta {
 
     // Consumer half (threads 128..255, column t = tid - 128) of row step s:
     // horizontal spread of gm[s & 1] over valid columns c-10..c, vertical spread
-    // over valid rows v-10..v (spread_t, loss.cpp:135-152), output row y = v.
+    // over valid rows v-10..v (spread_t, loss.cpp:66-83), output row y = v.
     template <int U>
     __device__ __forceinline__ void consume(SsimState& st, int s, float& mk_next) const {
         const int v = y0 - 2 * kHalo + s;
@@ -340,9 +340,9 @@ struct SsimCta {
             const Raw uu = S.rawU[slot][t];
             const float tv = S.rawT[slot][t];
             const float iv = intensity(uu);
-            const float gs = G1 + 2.f * iv * G2 + tv * G3;  // loss.cpp:211
+            const float gs = G1 + 2.f * iv * G2 + tv * G3;  // loss.cpp:142
             float g = ws * gs;
-            if (kind == kLossTraining) {  // loss_recon_grad, loss.cpp:317-341
+            if (kind == kLossTraining) {  // loss_recon_grad, loss.cpp:248-272
                 const float d = iv - tv;
                 const float k = 1.f + mk + tv * tv;
                 if (!BAND || static_cast<unsigned>(y - a.own0) < static_cast<unsigned>(a.own1 - a.own0)) st.sum += static_cast<double>(d * d * k);
@@ -535,7 +535,7 @@ __global__ void adan_consts_kernel(AdanGroups G, int total_steps, double b1, dou
     adan_consts(G, total_steps, b1, b2, b3, step[0], step[1] + 1, K);
 }
 
-// Fused Adan over the six groups (optimizer.cpp:99-123) with the group
+// Fused Adan over the six groups (Adan::step optimizer.cpp:48-72) with the group
 // constants of this step precomputed in Kc.  VEC: every group boundary and P
 // are multiples of 4, so a thread updates a float4 of one group with 16-byte
 // loads/stores.  The last CTA to finish advances the device step counter (not
@@ -639,15 +639,8 @@ __global__ void nonfinite_kernel(const float* g, int64_t n, uint32_t* flag) {
         }
 }
 
-constexpr int kSRv0 = 145, kSRv1 = 101;
-int ssim_variant() {
-    static const int v = [] {
-        const char* e = std::getenv("HS_SSIM_VARIANT");
-        return e ? std::atoi(e) : 0;
-    }();
-    return v;
-}
-int ssim_rows() { return ssim_variant() == 1 ? kSRv1 : kSRv0; }
+constexpr int kSsimRows = 145;  // output rows per SSIM CTA (1080 = 7.4 x 145: 8 row strips)
+int ssim_rows() { return kSsimRows; }
 
 unsigned grid_for(int64_t n, int threads) {
     const int64_t b = (n + threads - 1) / threads;
@@ -673,17 +666,14 @@ int loss_launch(const LossArgs& a, cudaStream_t st) {
             HS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
             kern<<<grid, 2 * kSW, smem, st>>>(a, win);
         };
-        const bool v1 = ssim_variant() == 1;
         const bool band = a.own0 > 0 || a.own1 < a.H;
         if (band) {
             require(a.field != nullptr, "ssim: row-band loss needs the complex field");
-            go(ssim_loss_kernel<true, 3, kSRv0, true>, sizeof(SsimSmem<float2>));
+            go(ssim_loss_kernel<true, 3, kSsimRows, true>, sizeof(SsimSmem<float2>));
         } else if (a.field) {
-            if (v1) go(ssim_loss_kernel<true, 4, kSRv1>, sizeof(SsimSmem<float2>));
-            else go(ssim_loss_kernel<true, 3, kSRv0>, sizeof(SsimSmem<float2>));
+            go(ssim_loss_kernel<true, 3, kSsimRows>, sizeof(SsimSmem<float2>));
         } else {
-            if (v1) go(ssim_loss_kernel<false, 4, kSRv1>, sizeof(SsimSmem<float>));
-            else go(ssim_loss_kernel<false, 3, kSRv0>, sizeof(SsimSmem<float>));
+            go(ssim_loss_kernel<false, 3, kSsimRows>, sizeof(SsimSmem<float>));
         }
         launch_check("ssim_loss");
         return static_cast<int>(grid.x * grid.y * grid.z);
@@ -724,12 +714,9 @@ void intensity_launch(const float2* f, int64_t count, float* out, cudaStream_t s
     launch_check("intensity");
 }
 
-// float4 work items per thread of the fused Adan (HS_ADAN_PER; 2 measured best: 28.7 -> 26.6 us at cfg2)
+// float4 work items per thread of the fused Adan (2 measured best: 28.7 -> 26.6 us at cfg2)
 static unsigned adan_grid(int64_t items) {
-    static const int per = [] {
-        const char* e = std::getenv("HS_ADAN_PER");
-        return e ? std::max(1, std::atoi(e)) : 2;
-    }();
+    constexpr int per = 2;
     const int64_t b = (items + 256LL * per - 1) / (256LL * per);
     return static_cast<unsigned>(std::max<int64_t>(1, b));
 }

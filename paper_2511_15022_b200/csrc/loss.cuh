@@ -47,7 +47,7 @@ inline size_t ssim_target_stats_elems(int C, int H, int W) {
     return (H < 11 || W < 11) ? 1 : static_cast<size_t>(C) * (H - 10) * (W - 10);
 }
 
-// One Adan element update (optimizer.cpp:99-123) with per-group constants
+// One Adan element update (Adan::step optimizer.cpp:48-72) with per-group constants
 // lr, 1/bc1, beta2/bc2, 1/bc3.
 struct GroupConst {
     float lr, inv_bc1, b2_bc2, inv_bc3;
@@ -65,7 +65,7 @@ __device__ __forceinline__ void adan_update(float& p, float g, float& m, float& 
     gp = g;
 }
 
-// Fused Adan over the six groups of the parameter buffer (optimizer.cpp:99-123).
+// Fused Adan over the six groups of the parameter buffer (Adan::step optimizer.cpp:48-72).
 struct AdanGroups {
     int64_t begin[6], end[6];
     float base_lr[6];

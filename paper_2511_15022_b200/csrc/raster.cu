@@ -992,14 +992,6 @@ void raster_forward(const RasterWork& rw, float2* d_field, cudaStream_t st, int 
     }
 }
 
-static int bwd_variant() {
-    static const int v = [] {
-        const char* e = std::getenv("HS_BWD_VARIANT");
-        return e ? std::atoi(e) : 0;
-    }();
-    return v;
-}
-
 template <int C>
 static void bwd_launch(const RasterWork& rw, const float* d_params, const float2* d_gf,
                        float* d_grads, uint32_t* d_flags, int y0, int hs, cudaStream_t st) {
@@ -1022,10 +1014,7 @@ static void bwd_launch(const RasterWork& rw, const float* d_params, const float2
         launch_check("raster_finalize");
         return;
     }
-    switch (bwd_variant()) {
-        case 1: go(raster_bwd_kernel<C, 3, 2>); break;
-        default: go(raster_bwd_kernel<C, 4, 1>); break;  // measured best at cfg2
-    }
+    go(raster_bwd_kernel<C, 4, 1>);  // 4 CTAs/SM measured best at cfg2
     launch_check("raster_bwd");
     raster_finalize_kernel<C><<<ceil_div(rw.n, 256), 256, 0, st>>>(rw.n, rw.raw.as<float>(), d_params, rw.width,
                                                                    rw.height, d_grads, d_flags);

@@ -573,7 +573,7 @@ class DepthPlaneSet:
 
 
 def make_depth_planes(count: int, center_distance: float, spacing: float) -> DepthPlaneSet:
-    """loss.cpp:223-233."""
+    """make_depth_planes, loss.cpp:154-164."""
     if count < 1:
         raise HoloInvalidArgument("make_depth_planes: count must be >= 1")
     return DepthPlaneSet(count, center_distance, spacing,
@@ -581,7 +581,7 @@ def make_depth_planes(count: int, center_distance: float, spacing: float) -> Dep
 
 
 def build_masks(depth: RealField, plane_count: int, near_is_high: bool) -> np.ndarray:
-    """loss.cpp:235-249 (via the C ABI, bit-exact); returns L x H x W uint8."""
+    """build_masks, loss.cpp:166-180 (via the C ABI, bit-exact); returns L x H x W uint8."""
     if plane_count < 1:
         raise HoloInvalidArgument("build_masks: plane count must be >= 1")
     if depth.channels != 1:
@@ -695,7 +695,7 @@ class AdanConfig:
 
 
 class Adan:
-    """holo::Adan with device-resident fp32 state (optimizer.cpp:66-123)."""
+    """holo::Adan with device-resident fp32 state (optimizer.cpp:15-72)."""
 
     def __init__(self, cfg: AdanConfig = None):
         self.cfg = cfg or AdanConfig()
@@ -804,6 +804,15 @@ class Trainer:
 
     def grads_tensor(self) -> torch.Tensor:
         return _wrap(self, _lib.load().hs_trainer_grads_ptr(self.h), self.param_count)
+
+    def flags_tensor(self) -> torch.Tensor:
+        """The device word of non-finite gradient groups (int32 view, bit g = group g)."""
+        return _wrap(self, _lib.load().hs_trainer_flags_ptr(self.h), 1, "<i4")
+
+    def slab_error_tensor(self):
+        """The device peer-put timeout word (int32 view), None without row slabs."""
+        p = _lib.load().hs_trainer_slab_error_ptr(self.h)
+        return _wrap(self, p, 1, "<i4") if p else None
 
     def gaussians(self) -> GaussianSet:
         return GaussianSet.from_flat(self.params(), self.n, self.c)
@@ -946,13 +955,13 @@ def ipc_open(handle: bytes) -> int:
     return int(p.value)
 
 
-def _wrap(owner, ptr, count) -> torch.Tensor:
+def _wrap(owner, ptr, count, typestr="<f4") -> torch.Tensor:
     """torch view over trainer-owned device memory (kept alive by owner)."""
     class _Holder:
         pass
 
     dev = torch.cuda.current_device()
-    iface = {"shape": (count,), "typestr": "<f4", "data": (int(ptr), False), "version": 3,
+    iface = {"shape": (count,), "typestr": typestr, "data": (int(ptr), False), "version": 3,
              "strides": None}
     holder = _Holder()
     holder.__cuda_array_interface__ = iface

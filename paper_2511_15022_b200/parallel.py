@@ -69,10 +69,106 @@ def geometry_ranges(n: int, c: int):
 
 def combine_loss(recon_sum: float, ssim_sum: float, C: int, H: int, W: int, L: int,
                  ssim_weight: float = 0.005) -> float:
-    """training_loss from the all-reduced partial sums (loss.cpp:317-398)."""
+    """training_loss from the all-reduced partial sums (loss_recon_grad loss.cpp:248-272, loss_ssim_grad :292-314, training_loss_grad :320-329)."""
     n = C * H * W
     count = L * C * (H - 10) * (W - 10)
     return recon_sum / (n * L) + ssim_weight * (1.0 - ssim_sum / count)
+
+
+GROUP_NAMES = ("position", "scale", "rotation", "amplitude", "phase", "opacity")  # pipeline.cpp:244-249
+_NO_GROUP = 1 << 30
+
+
+def agree_nonfinite(trainer, group=None):
+    """After the cross-rank gradient sum and check_grads(): keep only the lowest
+    non-finite group bit of the trainer's device flag word and min-reduce it over
+    the ranks, so every rank skips the same groups in apply_update -- the groups
+    from the first non-finite one on, as the reference's Adan::step throw stops
+    the step loop there (optimizer.cpp:52-54).  Needed when part of the gradient
+    stays rank-local (channel shards) or a rank's partial alone is non-finite."""
+    ft = getattr(trainer, "flags_tensor", None)
+    if ft is None or not (dist.is_initialized() and dist.get_world_size(group) > 1):
+        return
+    f = ft()
+    low = _lowest_group_bit(f)
+    dist.all_reduce(low, op=dist.ReduceOp.MIN, group=group)
+    f.copy_(torch.where(low == _NO_GROUP, torch.zeros_like(low), low))
+
+
+def _lowest_group_bit(f: torch.Tensor) -> torch.Tensor:
+    low = f & -f
+    return torch.where(low == 0, torch.full_like(low, _NO_GROUP), low)
+
+
+def agree_nonfinite_local(trainers):
+    """agree_nonfinite for trainers that share one process (virtual ranks)."""
+    fs = [t.flags_tensor() for t in trainers]
+    low = torch.stack([_lowest_group_bit(f) for f in fs]).min(dim=0).values
+    word = torch.where(low == _NO_GROUP, torch.zeros_like(low), low)
+    for f in fs:
+        f.copy_(word)
+
+
+class ErrorWatch:
+    """Raises a sharded step's device errors -- the non-finite group word
+    (HoloNonFinite naming the reference's group, as Adan::step's throw) and the
+    peer-put timeout word -- on every step without a per-step host sync: after
+    each update both words are copied into pinned host memory behind an event;
+    step k raises for the last step whose copy has completed, and flush() (also
+    called when the loss is read, which syncs anyway) for the current one."""
+
+    def __init__(self, trainer, depth: int = 4):
+        self.tr = trainer
+        self.ok = hasattr(trainer, "flags_tensor") and torch.cuda.is_available()
+        self.depth = depth
+        self.k = 0
+        if self.ok:
+            self.host = torch.zeros((depth, 2), dtype=torch.int32).pin_memory()
+            self.events = [None] * depth
+            err = trainer.slab_error_tensor() if hasattr(trainer, "slab_error_tensor") else None
+            self.words = [trainer.flags_tensor(), err]
+
+    def post(self):
+        if not self.ok:
+            return
+        slot = self.k % self.depth
+        if self.events[slot] is not None:  # ring full: its copy is `depth` steps old
+            self._check(slot)
+        for j, w in enumerate(self.words):
+            if w is not None:
+                self.host[slot, j:j + 1].copy_(w, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self.events[slot] = ev
+        self.k += 1
+        self.poll()
+
+    def _check(self, slot):
+        self.events[slot].synchronize()
+        self.events[slot] = None
+        flags, err = int(self.host[slot, 0]), int(self.host[slot, 1])
+        if err:
+            raise RuntimeError("row slab: a peer-put exchange timed out waiting for a peer")
+        if flags:
+            from ._lib import HoloNonFinite
+            g = (flags & -flags).bit_length() - 1
+            raise HoloNonFinite(f"Adan: non-finite gradient in group {GROUP_NAMES[g]}")
+
+    def poll(self):
+        if not self.ok:
+            return
+        for i in range(self.k - self.depth, self.k):
+            slot = i % self.depth
+            if i >= 0 and self.events[slot] is not None and self.events[slot].query():
+                self._check(slot)
+
+    def flush(self):
+        if not self.ok:
+            return
+        for i in range(self.k - self.depth, self.k):
+            slot = i % self.depth
+            if i >= 0 and self.events[slot] is not None:
+                self._check(slot)
 
 
 class ShardedStep:
@@ -86,9 +182,12 @@ class ShardedStep:
         self.tr = trainer
         self.C, self.H, self.W, self.L = C, H, W, L_total
         self.group = group
+        self.watch = ErrorWatch(trainer)
 
     def step(self, with_loss: bool = True):
-        """One step; returns the loss (a host sync) or None when with_loss is False."""
+        """One step; returns the loss (a host sync) or None when with_loss is False.
+        Raises HoloNonFinite for a non-finite summed gradient (at the latest one
+        step later when the loss is not read)."""
         self.tr.forward_backward()
         g = self.tr.grads_tensor()
         if dist.is_initialized() and dist.get_world_size(self.group) > 1:
@@ -96,9 +195,12 @@ class ShardedStep:
                 torch.cuda.current_stream().synchronize()
             dist.all_reduce(g, op=dist.ReduceOp.SUM, group=self.group)
             self.tr.check_grads()
+            agree_nonfinite(self.tr, self.group)
         self.tr.apply_update()
+        self.watch.post()
         if not with_loss:
             return None
+        self.watch.flush()
         parts = torch.tensor(self.tr.loss_partials(), dtype=torch.float64,
                              device=g.device if g.is_cuda else "cpu")
         if dist.is_initialized() and dist.get_world_size(self.group) > 1:
@@ -116,6 +218,7 @@ class ChannelShardedStep:
         self.tr, self.n, self.c = trainer, n, c_local
         self.C, self.H, self.W, self.L = C_total, H, W, L
         self.group = group
+        self.watch = ErrorWatch(trainer)
 
     def step(self, with_loss: bool = True):
         """One step; returns the loss (a host sync) or None when with_loss is False."""
@@ -127,9 +230,15 @@ class ChannelShardedStep:
                 torch.cuda.current_stream().synchronize()
             for b, e in geometry_ranges(self.n, self.c):
                 dist.all_reduce(g[b:e], op=dist.ReduceOp.SUM, group=self.group)
+            # the summed geometry may be non-finite where this rank's partial was
+            # not, and the rank-local amplitude/phase groups differ per rank
+            self.tr.check_grads()
+            agree_nonfinite(self.tr, self.group)
         self.tr.apply_update()
+        self.watch.post()
         if not with_loss:
             return None
+        self.watch.flush()
         parts = torch.tensor(self.tr.loss_partials(), dtype=torch.float64,
                              device=g.device if g.is_cuda else "cpu")
         if multi:
@@ -175,6 +284,7 @@ class SlabShardedStep:
         if self.put:
             self._map_peers()
             trainer.use_graph(True)
+        self.watch = ErrorWatch(trainer)
 
     def _map_peers(self):
         from . import holo
@@ -221,12 +331,13 @@ class SlabShardedStep:
         if multi:
             dist.all_reduce(g, op=dist.ReduceOp.SUM, group=self.group)
             self.tr.check_grads()
+            agree_nonfinite(self.tr, self.group)
         self.tr.apply_update()
+        self.watch.post()  # non-finite groups and the peer-put timeout word, every step
         if not with_loss:
             return None
+        self.watch.flush()
         parts = torch.tensor(self.tr.loss_partials(), dtype=torch.float64, device=g.device)
-        if self.put and self.tr.slab_status():
-            raise RuntimeError("row slab: a peer-put exchange timed out waiting for a peer")
         if multi:
             dist.all_reduce(parts, op=dist.ReduceOp.SUM, group=self.group)
         return combine_loss(float(parts[0]), float(parts[1]), self.C, self.H, self.W, self.L)
@@ -246,6 +357,7 @@ class LocalSlabGroup:
         self.C, self.H, self.W, self.L = C, H, W, L
         self.counts = [[t.slab_counts(e) for e in range(4)] for t in self.trs]
         self.put = put
+        self.watches = [ErrorWatch(t) for t in self.trs]
         if put:
             bufs = [t.slab_peer_buffers() for t in self.trs]
             for t in self.trs:
@@ -281,11 +393,13 @@ class LocalSlabGroup:
         for t in self.trs:
             t.check_grads()
             t.apply_update()
+        for w in self.watches:
+            w.post()
         if not with_loss:
             return None
+        for w in self.watches:
+            w.flush()
         parts = [t.loss_partials() for t in self.trs]
-        if self.put and any(t.slab_status() for t in self.trs):
-            raise RuntimeError("row slab: a peer-put exchange timed out waiting for a peer")
         return combine_loss(sum(p[0] for p in parts), sum(p[1] for p in parts), self.C, self.H, self.W, self.L)
 
 

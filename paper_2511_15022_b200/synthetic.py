@@ -198,7 +198,7 @@ def synthetic_depth(seed: int, height: int, width: int) -> np.ndarray:
 
 
 def build_masks(depth: np.ndarray, plane_count: int, near_is_high: bool = True) -> np.ndarray:
-    """loss.cpp:235-249 (host, bit-exact): L x H x W uint8."""
+    """build_masks, loss.cpp:166-180 (host, bit-exact): L x H x W uint8."""
     if plane_count < 1:
         raise ValueError("build_masks: plane count must be >= 1")
     h, w = depth.shape
@@ -212,7 +212,7 @@ def build_masks(depth: np.ndarray, plane_count: int, near_is_high: bool = True) 
 
 
 def make_depth_planes(count: int, d0: float, dz: float):
-    """loss.cpp:223-233."""
+    """make_depth_planes, loss.cpp:154-164."""
     return [d0 + (l - (count - 1) * 0.5) * dz for l in range(count)]
 
 
@@ -241,3 +241,48 @@ def workload(name: str, scene: int = 0):
     g = init_gaussians(cfg["count"], c, w, h, 42 + scene)
     return dict(cfg=cfg, gaussians=g, target=target, depth=depth, masks=masks, distances=dist,
                 wavelengths=WAVELENGTHS[c])
+
+
+# ---- train()'s PNG round trip of its inputs (io.cpp:228-235, 337-395) ----------------------------
+def srgb_to_linear(s):
+    """io.cpp:228-230."""
+    s = np.asarray(s, dtype=np.float64)
+    return np.where(s <= 0.04045, s / 12.92, np.power((s + 0.055) / 1.055, 2.4))
+
+
+def linear_to_srgb(v):
+    """io.cpp:232-235."""
+    v = np.clip(np.asarray(v, dtype=np.float64), 0.0, 1.0)
+    return np.where(v <= 0.0031308, 12.92 * v, 1.055 * np.power(v, 1.0 / 2.4) - 0.055)
+
+
+def _lround(x):
+    return np.floor(np.asarray(x, dtype=np.float64) + 0.5)  # std::lround on non-negative values
+
+
+def png8_srgb_roundtrip(img: np.ndarray) -> np.ndarray:
+    """write_image_srgb (io.cpp:353-368: lround(srgb * 255) into 8 bits) followed by
+    read_image_linear (io.cpp:337-351: srgb_to_linear(v / 255)): the intensity target
+    train() sees for an image written by the reference's tests."""
+    q = _lround(linear_to_srgb(img) * 255.0)
+    return srgb_to_linear(q / 255.0)
+
+
+def png16_depth_roundtrip(depth: np.ndarray) -> np.ndarray:
+    """write_depth_png(..., 16) (io.cpp:378-390) followed by read_depth (io.cpp:370-376)."""
+    q = _lround(np.clip(depth, 0.0, 1.0) * 65535.0)
+    return q / 65535.0
+
+
+def desk_scene(ratio: float):
+    """The reference's end-to-end desk regression (acceptance.cpp:303-334, criteria 6/7):
+    a 256x160 grayscale synthetic image (seed 42) and depth (seed 43) written as an 8-bit
+    sRGB / 16-bit PNG and read back by train(), two planes (3 mm centre, 2 mm spacing),
+    532 nm, N from the parameter ratio, Gaussians from seed 42, 2000 steps."""
+    w, h, c, L = 256, 160, 1, 2
+    target = png8_srgb_roundtrip(synthetic_image(42, c, h, w))
+    depth = png16_depth_roundtrip(synthetic_depth(43, h, w))
+    n = resolve_gaussian_count(c, w, h, parameter_ratio=ratio)
+    return dict(width=w, height=h, channels=c, count=n, target=target, depth=depth,
+                masks=build_masks(depth, L, True), distances=make_depth_planes(L, 3e-3, 2e-3),
+                gaussians=init_gaussians(n, c, w, h, 42), steps=2000, wavelengths=(532e-9,))

@@ -265,7 +265,7 @@ def test_loss(holo, ref, kind, c, h, w, L):
 
 
 def test_adan_matches_reference_trajectory(holo, ref):
-    # test_optimizer.cpp:282-296 vector trajectory (fp32 device state)
+    # test_optimizer.cpp vector trajectory (fp32 device state)
     a = holo.Adan()
     a.add_group("xy", 2, 0.05)
     r = ref.Adan()

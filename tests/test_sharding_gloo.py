@@ -183,3 +183,33 @@ def test_channel_sharded_step_equals_full_step_gloo(tmp_path):
     p = np.load(out + "_parts.npy")
     loss = P.combine_loss(p[0], p[1], C, H, W, L)
     assert loss == pytest.approx(P.combine_loss(full["recon_sum"], full["ssim_sum"], C, H, W, L), rel=1e-12)
+
+
+class _FlagTrainer:
+    def __init__(self, word):
+        self.f = torch.tensor([word], dtype=torch.int32)
+
+    def flags_tensor(self):
+        return self.f
+
+
+def _agree_worker(rank, world, port, words, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    t = _FlagTrainer(words[rank])
+    P.agree_nonfinite(t)
+    q.put((rank, int(t.f.item())))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("words,want", [((0, 0), 0), ((1 << 5, 1 << 3 | 1 << 4), 1 << 3), ((1 << 2, 0), 1 << 2)])
+def test_ranks_agree_on_the_first_nonfinite_group_gloo(words, want):
+    """parallel.agree_nonfinite: every rank ends with the lowest non-finite group
+    of any rank (opacity on rank 0 and amplitude on rank 1 -> both stop at
+    amplitude, where the reference's Adan::step would throw first)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    mp.start_processes(_agree_worker, args=(2, free_port(), words, q), nprocs=2, join=True, start_method="spawn")
+    got = dict(q.get() for _ in range(2))
+    assert got == {0: want, 1: want}

@@ -163,3 +163,49 @@ def test_sharded_nonfinite_is_decided_on_the_summed_gradient(holo):
             t.last_loss()  # raises on the non-finite flag
     for t, p in zip(trs, p0):
         assert np.array_equal(t.params(), p)
+
+
+def test_channel_shards_agree_on_a_rank_local_nonfinite_group(holo):
+    """Wavelength shards keep amplitude/phase rank-local: a NaN in rank 1's
+    amplitude gradient (rank 0's is clean) must still stop BOTH ranks from the
+    amplitude group on (the reference throws at "amplitude" and never reaches
+    phase/opacity), while both apply the same position/scale/rotation update."""
+    from paper_2511_15022_b200 import parallel as P
+    n, c, w, h, L = 300, 3, 64, 48, 1
+    g = {k: np.asarray(v, dtype=np.float32).astype(np.float64) for k, v in S.init_gaussians(n, c, w, h, 5).items()}
+    img = S.synthetic_image(42, c, h, w)
+    masks = S.build_masks(S.synthetic_depth(43, h, w), L, True)
+    dist = S.make_depth_planes(L, 3e-3, 2e-3)
+    wl = S.WAVELENGTHS[c]
+    trs = []
+    for r in range(2):
+        b, e = P.channel_shard(c, r, 2)
+        gs = P.slice_channels(g, n, c, b, e)
+        trs.append(holo.Trainer(holo.GaussianSet(n, e - b, **gs), w, h, holo.RealField(e - b, h, w, img[b:e]),
+                                masks, dist, holo.PropagationSpec(wl[b:e]), 10, channels_total=c))
+    p0 = [t.params() for t in trs]
+    for t in trs:
+        t.forward_backward()
+    grads = [t.grads_tensor() for t in trs]
+    grads[1][5 * n + 7] = float("nan")  # rank 1's amplitude (rank-local group)
+    geo = [P.geometry_ranges(n, 2), P.geometry_ranges(n, 1)]
+    for k in range(2):  # the geometry all-reduce, as device copies
+        total = grads[0][geo[0][k][0]:geo[0][k][1]] + grads[1][geo[1][k][0]:geo[1][k][1]]
+        grads[0][geo[0][k][0]:geo[0][k][1]].copy_(total)
+        grads[1][geo[1][k][0]:geo[1][k][1]].copy_(total)
+    for t in trs:
+        t.check_grads()
+    assert int(trs[0].flags_tensor().item()) == 0 and int(trs[1].flags_tensor().item()) == 1 << 3
+    P.agree_nonfinite_local(trs)
+    watches = [P.ErrorWatch(t) for t in trs]
+    for t, wt in zip(trs, watches):
+        t.apply_update()
+        with pytest.raises(holo.HoloNonFinite, match="group amplitude"):
+            wt.post()  # raises at once when the copy has landed, else at flush()
+            wt.flush()
+    q = [t.params() for t in trs]
+    for r, cl in ((0, 2), (1, 1)):
+        geo0, opa = slice(0, 5 * n), slice(5 * n + 2 * n * cl, 6 * n + 2 * n * cl)
+        assert not np.array_equal(q[r][geo0], p0[r][geo0])          # position/scale/rotation updated
+        assert np.array_equal(q[r][5 * n:], p0[r][5 * n:])          # amplitude, phase, opacity untouched
+    assert np.array_equal(q[0][:5 * n], q[1][:5 * n])                # the same geometry update on both ranks
