@@ -6,11 +6,17 @@ roofline fraction.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 is launched by torchrun (one rank per GPU); every rank optimises its own
-scene (scene seed = rank): replicas, weak scaling, no data-path collective.
-Timing: CUDA events on the trainer's stream around exactly K graph-replayed
-steps, barrier + synchronize on both sides, max over ranks.  The step's
-working set (~0.45 GB) exceeds the 126 MB L2, so no explicit flush is used.
+N = 1: the graph-captured cfg2 step on one B200.
+N > 1: one rank per GPU (launched by torchrun, or by bench.py itself when
+WORLD_SIZE is unset), and by default the SAME cfg2 scene split over the ranks
+as row slabs (strong scaling): the 2D FFTs are distributed with four transposes
+per step, stored by the FFT kernels straight into the peers' receive buffers
+over NVLink, plus an NCCL all-reduce of the gradients (--shard slabs
+--exchange put).  --shard planes (cfg3, 8 planes), channels and replicas are
+the other decompositions.  Fewer visible GPUs than N is an error.
+Timing: CUDA events on the trainer's stream around exactly K steps, barrier +
+synchronize on both sides, max over ranks.  The step's working set (~0.45 GB)
+exceeds the 126 MB L2, so no explicit flush is used.
 """
 from __future__ import annotations
 
@@ -53,14 +59,44 @@ def parse():
                    help="--shard slabs on ONE GPU: R slab trainers stepped in lock-step with the "
                         "all-to-alls done as device copies (parallel.LocalSlabGroup); reports the "
                         "decomposition's compute per rank, no interconnect")
-    p.add_argument("--shard", choices=("replicas", "channels", "planes", "slabs"), default="replicas",
+    p.add_argument("--trained-steps", type=int, default=1000,
+                   help="N=1: also time the step after this many optimisation steps (trained state: "
+                        "moved/rescaled Gaussians, a different pair count); 0 = off")
+    p.add_argument("--shard", choices=("replicas", "channels", "planes", "slabs"), default=None,
                    help="N>1: replicas = one scene per GPU (weak scaling, no collective); "
                         "channels = the wavelengths of one scene split over ranks (<= C ranks), "
                         "planes = the depth planes of one scene (cfg3) split over ranks; both "
                         "all-reduce gradients over NCCL (strong scaling); slabs = the canvas rows "
                         "and spectrum columns of one scene (cfg4) split over ranks: four NCCL "
-                        "all-to-all transposes + the gradient all-reduce per step")
-    return p.parse_args()
+                        "all-to-all transposes + the gradient all-reduce per step.  Default: replicas "
+                        "at N=1 (a single unsharded scene), slabs at N>1")
+    a = p.parse_args()
+    if a.shard is None:
+        a.shard = "slabs" if a.gpus > 1 else "replicas"
+    return a
+
+
+def self_launch(args):
+    """`python bench.py --gpus N` without torchrun: re-launch as N ranks
+    (torch.distributed.run, 127.0.0.1 rendezvous) after checking the GPUs."""
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if args.impl == "ours" and have < args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}\n")
+        raise SystemExit(2)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # the NCCL init lines show the rank count and the transport
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    raise SystemExit(subprocess.call(cmd, env=env))
 
 
 def dist_env():
@@ -176,6 +212,59 @@ def cpu_reference_run(wl, gset32, max_seconds, threads, min_steps=1, max_steps=3
     return float(np.mean(times)), len(times), dict(zip(names, [round(float(x), 2) for x in st]))
 
 
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return "unknown"
+
+
+def fft_speed():
+    """The FFT under the reference arm: oracle/fftw_shim.cpp (FFTW3 is not in the
+    image) against numpy's pocketfft, both fp64 on one core, at the cfg2 padded
+    grid 2160 x 3840: ms per forward + inverse 2D transform pair.  The shim is
+    timed through the reference's single-plane propagate(), i.e. its two FFTs
+    plus pad / transfer / crop."""
+    from oracle import ref
+
+    h, w = 1080, 1920
+    rng = np.random.default_rng(0)
+    re, im = rng.standard_normal((1, h, w)), rng.standard_normal((1, h, w))
+    ref.set_thread_count(1)
+    ref.propagate(re, im, ref.PropagationSpec((532e-9,)), 3e-3)  # plan / warm
+    t0 = time.perf_counter()
+    ref.propagate(re, im, ref.PropagationSpec((532e-9,)), 3e-3)
+    shim = (time.perf_counter() - t0) * 1e3
+    z = (rng.standard_normal((2 * h, 2 * w)) + 1j * rng.standard_normal((2 * h, 2 * w)))
+    np.fft.ifft2(np.fft.fft2(z))
+    t0 = time.perf_counter()
+    np.fft.ifft2(np.fft.fft2(z))
+    pocket = (time.perf_counter() - t0) * 1e3
+    return {"fft": "oracle/fftw_shim.cpp (FFTW3 API, mixed-radix Stockham + Bluestein, fp64); FFTW3 "
+                   "itself is absent from the image",
+            "grid": "2160x3840 complex128", "shim_propagate_ms_1core": round(shim, 1),
+            "numpy_pocketfft_fft2_ifft2_ms_1core": round(pocket, 1)}
+
+
+def cpu_baseline(wl, gset32):
+    """The reference's own fp64 step (oracle/_ref) on this box's host cores:
+    set_thread_count(nproc) (the reported value) and set_thread_count(1), with
+    the CPU model and the FFT used (BASELINE.md CPU-baseline plan)."""
+    nproc = os.cpu_count() or 1
+    sec, k, st = cpu_reference_run(wl, gset32, 30.0, nproc, 1, 3, 0)
+    sec1, k1, st1 = cpu_reference_run(wl, gset32, 20.0, 1, 1, 1, 0)
+    return {"value": 1.0 / sec, "unit": UNIT, "cores": nproc, "kind": "reference",
+            "sample": f"{k} full cfg2 step(s) through the reference's fp64 C++ (oracle/_ref), "
+                      f"set_thread_count({nproc}); only its rasterizer is threaded",
+            "stages_ms": st, "cpu_model": cpu_model(),
+            "single_thread": {"value": 1.0 / sec1, "unit": UNIT, "cores": 1, "steps": k1, "stages_ms": st1},
+            "fft": fft_speed()}
+
+
 def run_reference(args):
     rank, world, local = dist_env()
     if rank != 0:
@@ -204,7 +293,7 @@ def run_reference(args):
                          "sample": f"{k} full step(s) after {w_cap} warm-up of {args.workload} through the "
                                    f"reference's own fp64 C++ (oracle/_ref, FFTW3 API shim), "
                                    f"set_thread_count({threads}); steps capped to stay within minutes",
-                         "stages_ms": stages},
+                         "stages_ms": stages, "cpu_model": cpu_model()},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -243,7 +332,7 @@ def run_sharded(args):
     cfg = wl["cfg"]
     C_, h, w, n, L = cfg["channels"], cfg["height"], cfg["width"], cfg["count"], cfg["planes"]
     g32 = {k: np.asarray(v, np.float32).astype(np.float64) for k, v in wl["gaussians"].items()}
-    total = args.warmup + args.steps + 2
+    total = args.warmup + args.steps + max(1, min(args.e2e_steps, 20)) + 2
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
         if args.shard == "channels":
@@ -299,10 +388,29 @@ def run_sharded(args):
             dist.barrier()
         clocks = sampler.stop()
         ms = e0.elapsed_time(e1) / args.steps
+
+        # e2e through the public API with host-resident parameters: per step the
+        # H2D of this rank's parameters from pinned memory, the sharded step
+        # (exchanges + all-reduce), the loss read (a sync) and the D2H of the
+        # updated parameters.
+        host = torch.empty(tr.param_count, dtype=torch.float32, pin_memory=True)
+        host.copy_(tr.params_tensor())
+        dev = tr.params_tensor()
+        e2e_steps = max(1, min(args.e2e_steps, 20))
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            dev.copy_(host, non_blocking=True)
+            loss = step.step(with_loss=True)
+            host.copy_(dev, non_blocking=True)
+        torch.cuda.synchronize()
+        e2e_s = (time.perf_counter() - t0) / e2e_steps
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([ms, e2e_s], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t[0])
+        ms, e2e_s = float(t[0]), float(t[1])
     if rank == 0:
         peak, peak_src = peaks()
         B = algorithmic_bytes(cfg, tr.last_loss()[1])
@@ -314,6 +422,14 @@ def run_sharded(args):
             "step_roofline": {"bound": "hbm", "achieved": B / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
                               "frac": B / (ms * 1e-3) / 1e9 / peak / world, "peak_source": peak_src,
                               "note": "whole-job algorithmic bytes over world x peak"},
+            "roofline": {"bound": "hbm", "kernel": "whole step (sharded)", "achieved": B / (ms * 1e-3) / 1e9 / world,
+                         "peak": peak, "unit": "GB/s", "frac": B / (ms * 1e-3) / 1e9 / peak / world, "traffic": None,
+                         "peak_source": peak_src,
+                         "note": "per GPU: the step's algorithmic bytes (SURVEY 8d) / world / ms_per_step"},
+            "e2e": {"value": 1.0 / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 4 * tr.param_count,
+                    "d2h_bytes_per_step": 4 * tr.param_count + 16,
+                    "path": "per rank and step: H2D of its parameters (pinned), the sharded step, the loss "
+                            "read and the D2H of the updated parameters; max over ranks"},
             "gpu_launches": int(launches), "clocks": clocks, "loss": loss,
             "timing": ("slab steps: stages 0-4 as one CUDA graph (peer-put, device-flag sync), NCCL "
                        "all-reduce of the gradients, Adan; " if args.shard == "slabs" and args.exchange == "put"
@@ -431,6 +547,12 @@ def run_cfg5(args):
 
 def main():
     args = parse()
+    rank, world, _ = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        self_launch(args)
+    if world != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}\n")
+        raise SystemExit(2)
     if args.impl == "reference":
         run_reference(args)
         return
@@ -456,7 +578,9 @@ def main():
     gs = holo.GaussianSet(n, c, **gset32)
     target = holo.RealField(c, h, w, wl["target"].astype(np.float32).astype(np.float64))
     spec = holo.PropagationSpec(tuple(wl["wavelengths"]))
-    total = args.warmup + args.steps + args.e2e_steps + args.profile_steps + 5
+    trained_extra = max(0, args.trained_steps - args.warmup - args.steps) if args.trained_steps > 0 else 0
+    total = args.warmup + args.steps + trained_extra + (args.steps if args.trained_steps > 0 else 0) \
+        + args.e2e_steps + args.profile_steps + 5
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
         tr = holo.Trainer(gs, w, h, target, wl["masks"], wl["distances"], spec, total_steps=total)
@@ -483,6 +607,26 @@ def main():
         clocks = sampler.stop()
         ms = e0.elapsed_time(e1) / args.steps
         loss, pairs = tr.last_loss()
+
+        trained = None
+        if args.trained_steps > 0:
+            # the same step after `trained_steps` optimisation steps: Gaussians moved,
+            # rescaled and re-weighted, a different pair count and tile balance
+            for _ in range(trained_extra):
+                tr.step(sync_loss=False)
+            tr.last_loss()
+            torch.cuda.synchronize()
+            t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0e.record(stream)
+            for _ in range(args.steps):
+                tr.step(sync_loss=False)
+            t1e.record(stream)
+            t1e.synchronize()
+            tms = t0e.elapsed_time(t1e) / args.steps
+            tloss, tpairs = tr.last_loss()
+            trained = {"after_steps": args.warmup + args.steps + trained_extra, "value": world * 1e3 / tms,
+                       "ms_per_step": tms, "pairs": tpairs, "loss": tloss,
+                       "step_roofline_frac": algorithmic_bytes(cfg, tpairs) / (tms * 1e-3) / 1e9 / peaks()[0]}
 
         # e2e through the public API with a host-resident GaussianSet (like the
         # reference loop): per step H2D params from pinned memory, the step,
@@ -557,13 +701,11 @@ def main():
         "gpu_launches": int(round(per_step_launches * args.steps)),
         "clocks": clocks, "loss": loss, "pairs": pairs,
     }
+    if trained:
+        line["trained"] = trained
     if world == 1 and not args.no_cpu_baseline:
         try:
-            sec, k, st = cpu_reference_run(wl, gset32, 30.0, os.cpu_count() or 1, 1, 3, 0)
-            line["cpu_baseline"] = {
-                "value": 1.0 / sec, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "reference",
-                "sample": f"{k} full cfg2 step(s) through the reference's fp64 C++ (oracle/_ref, FFTW3 API "
-                          f"shim), set_thread_count(nproc)", "stages_ms": st}
+            line["cpu_baseline"] = cpu_baseline(wl, gset32)
         except Exception as e:  # noqa: BLE001
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                                     "sample": f"unavailable: {e}"}

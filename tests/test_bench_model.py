@@ -40,3 +40,17 @@ def test_kernel_bytes_cover_the_field_passes(name):
                                 "rows_inv_bwd"))
     field -= L * cfg["height"] * cfg["width"]  # the masks ride with the loss slot
     assert field + 2 * c * A + 0.5 * c * A == pytest.approx(c * (13 + 12 * L) * A, rel=1e-12)
+
+
+def test_bench_refuses_more_gpus_than_visible():
+    """`bench.py --gpus N` with fewer than N visible GPUs exits non-zero with a
+    clear message instead of silently running one rank."""
+    import subprocess
+    import sys
+    import torch
+    n = max(2, torch.cuda.device_count() + 1)
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(n), "--steps", "1"],
+                       capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode != 0
+    assert f"--gpus {n} needs {n} visible GPUs" in r.stderr
