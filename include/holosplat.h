@@ -275,6 +275,26 @@ uint32_t* hs_trainer_slab_error_ptr(hs_trainer* tr);
  * hs_trainer_use_graph is on.  Follow with the gradient all-reduce and
  * hs_trainer_apply_update. */
 hs_status hs_trainer_slab_forward_backward(hs_trainer* tr);
+/* ---- NCCL communicator in the context + one-call sharded step ----
+ * No reference interface: the reference is single-process.  One rank per GPU.
+ * hs_comm_unique_id (on one rank; ship the 128 bytes to the others out of band),
+ * then hs_ctx_comm_init on every rank; or hs_ctx_comm_adopt a caller-owned
+ * ncclComm_t.  hs_ctx_destroy releases an owned communicator. */
+hs_status hs_comm_unique_id(void* id128);
+hs_status hs_ctx_comm_init(hs_ctx* ctx, const void* id128, int nranks, int rank);
+hs_status hs_ctx_comm_adopt(hs_ctx* ctx, void* nccl_comm);
+hs_status hs_ctx_comm_info(hs_ctx* ctx, int* nranks, int* rank);
+hs_status hs_ctx_comm_destroy(hs_ctx* ctx);
+/* One sharded optimisation step of this rank over the ctx communicator, on the
+ * ctx stream: plane shards (plane_begin/end) and row slabs all-reduce the
+ * gradient buffer, wavelength shards (channels_total > c) its 6N geometry
+ * groups; row slabs exchange by grouped ncclSend/ncclRecv between the stages
+ * (or by the peer-put stores when hs_trainer_slab_set_peers was called).  The
+ * ranks then agree on the first non-finite gradient group (min-reduce of the
+ * lowest flag bit), apply Adan and all-reduce the loss sums.  loss_out
+ * (nullable) syncs and receives the global loss; errors as hs_trainer_step. */
+hs_status hs_trainer_sharded_step(hs_trainer* tr, double* loss_out);
+
 /* holo::Rng(seed).uniform(lo, hi) drawn n times into h_out (rng.hpp; host). */
 hs_status hs_random_uniform(uint64_t seed, int64_t n, double lo, double hi, double* h_out);
 /* CUDA IPC of a device allocation: 64-byte handle out; open maps a peer

@@ -130,6 +130,12 @@ _SIGS = {
     "hs_trainer_slab_status": [C.c_void_p, C.POINTER(C.c_uint32)],
     "hs_trainer_slab_error_ptr": [C.c_void_p],
     "hs_trainer_slab_forward_backward": [C.c_void_p],
+    "hs_comm_unique_id": [C.c_void_p],
+    "hs_ctx_comm_init": [C.c_void_p, C.c_void_p, C.c_int, C.c_int],
+    "hs_ctx_comm_adopt": [C.c_void_p, C.c_void_p],
+    "hs_ctx_comm_info": [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int)],
+    "hs_ctx_comm_destroy": [C.c_void_p],
+    "hs_trainer_sharded_step": [C.c_void_p, C.POINTER(C.c_double)],
     "hs_random_uniform": [C.c_uint64, C.c_int64, C.c_double, C.c_double, C.c_void_p],
     "hs_ipc_get_handle": [C.c_void_p, C.c_void_p],
     "hs_ipc_open_handle": [C.c_void_p, C.POINTER(C.c_void_p)],

@@ -13,31 +13,13 @@
 #include "loss.cuh"
 #include "convert.cuh"
 #include "raster.cuh"
+#include "trainer.cuh"
 
 namespace hs {
 
 namespace {
 thread_local std::string g_last_error;
 std::atomic<uint64_t> g_launches{0};
-
-hs_status fail(hs_status s, const std::string& m) {
-    g_last_error = m;
-    return s;
-}
-
-template <class F>
-hs_status guard(F&& f) {
-    try {
-        f();
-        return HS_OK;
-    } catch (const Error& e) {
-        return fail(e.status, e.what());
-    } catch (const std::bad_alloc&) {
-        return fail(HS_ENOMEM, "host allocation failed");
-    } catch (const std::exception& e) {
-        return fail(HS_ECUDA, e.what());
-    }
-}
 
 const char* kGroupNames[6] = {"position", "scale", "rotation", "amplitude", "phase", "opacity"};
 
@@ -52,6 +34,11 @@ struct CtxWork {
 }  // namespace
 
 void note_launch(int n) { g_launches.fetch_add(static_cast<uint64_t>(n), std::memory_order_relaxed); }
+
+hs_status fail(hs_status s, const std::string& m) {
+    g_last_error = m;
+    return s;
+}
 
 int sm_count(int device) {
     int v = 0;
@@ -69,64 +56,6 @@ static CtxWork& work_of(hs_ctx* ctx) {
     return *static_cast<CtxWork*>(ctx->work);
 }
 
-struct hs_trainer {
-    hs_ctx* ctx = nullptr;
-    int n = 0, c = 0, w = 0, h = 0, L = 0, L_total = 0, plane0 = 0, total_steps = 0, C_total = 0;
-    std::vector<double> distances;
-    std::vector<double> wavelengths;
-    hs_prop_spec spec{};
-    int64_t P = 0;
-    DevBuf params, grads, state, field, planes, dplanes, back, target, tstats, masks, partials, out3,
-        flags, step;
-    RasterWork rw;
-    AsmWork aw;
-    AdanGroups groups{};
-    int host_step = 0;
-    int loss_slots = 0;
-    bool use_graph = false;
-    cudaGraphExec_t graph = nullptr;
-    bool profiling = false;
-    cudaEvent_t ev[12] = {};  // profiling: start + after each of the 11 kernel slots
-    // host-resident step (hs_trainer_step_host): copy stream, fork/join events,
-    // pinned result words, and its own graph keyed by the host buffers
-    cudaStream_t copy_st = nullptr;
-    cudaEvent_t ev_fork = nullptr, ev_ap = nullptr;
-    uint32_t* h_words = nullptr;  // pinned: flags, status[4]
-    double* h_o3 = nullptr;       // pinned: loss, recon sum, ssim sum
-    cudaGraphExec_t host_graph = nullptr;
-    const float* host_in = nullptr;
-    float* host_out = nullptr;
-    // row-slab sharding (hs_trainer_set_row_slab): rank `rank` of R owns canvas
-    // rows [h0, h0 + hr) and column tiles [rank ts, rank ts + ts); its loss band
-    // is rows [g0, g0 + He) (own rows + up to 10 halo rows each side)
-    int R = 0, rank = 0, hr = 0, ts = 0, h0 = 0, g0 = 0, He = 0, top = 0;
-    std::vector<int> He_of, g0_of;
-    DevBuf s_planes, s_dplanes, s_target, s_tstats, s_masks, s_T, s_send, s_recv;
-    ChunkMap m_pack[4], m_unpack[4];
-    int64_t s_counts[4][2 * kMaxPeers] = {};
-    // peer-put exchange (hs_trainer_slab_set_peers): the pack kernels store
-    // straight into the peers' receive buffers (double-buffered by exchange
-    // parity), then signal the peers' flag arrays; the next stage waits on
-    // this rank's flags.  No NCCL call on the data path.
-    bool s_put = false;
-    float2* s_peer_recv[2][kMaxPeers] = {};
-    uint32_t* s_peer_flags[kMaxPeers] = {};
-    DevBuf s_recv2, s_flags;  // flags: [0, R) per-source epochs, [kMaxPeers] error word, [kMaxPeers + 1] own epoch
-    cudaGraphExec_t slab_graph = nullptr;  // stages 0..4 of the put exchange, captured
-    int s_loss_slots = 0;
-    ~hs_trainer() {
-        if (graph) cudaGraphExecDestroy(graph);
-        if (host_graph) cudaGraphExecDestroy(host_graph);
-        for (auto& e : ev)
-            if (e) cudaEventDestroy(e);
-        if (ev_fork) cudaEventDestroy(ev_fork);
-        if (ev_ap) cudaEventDestroy(ev_ap);
-        if (copy_st) cudaStreamDestroy(copy_st);
-        if (slab_graph) cudaGraphExecDestroy(slab_graph);
-        if (h_words) cudaFreeHost(h_words);
-        if (h_o3) cudaFreeHost(h_o3);
-    }
-};
 
 extern "C" {
 
@@ -152,6 +81,7 @@ hs_status hs_ctx_create(int device, hs_ctx** out) {
 
 void hs_ctx_destroy(hs_ctx* ctx) {
     if (!ctx) return;
+    hs_ctx_comm_destroy(ctx);
     delete static_cast<CtxWork*>(ctx->work);
     ctx->work = nullptr;
     delete ctx;
@@ -508,7 +438,7 @@ extern "C" hs_status hs_adan_step(hs_ctx* ctx, const hs_adan_config* cfg, const 
 // Profiling slots (kernel boundaries): 0 start, 1 binning, 2 raster_fwd,
 // 3 rows_fwd, 4 cols_fwd, 5 rows_inv, 6 loss, 7 rows_fwd(bwd), 8 cols_bwd,
 // 9 rows_inv(bwd), 10 raster_bwd, 11 adan.
-static void trainer_enqueue_fwd_bwd(hs_trainer* t, cudaStream_t st, cudaEvent_t shading_ready = nullptr) {
+void hs::trainer_enqueue_fwd_bwd(hs_trainer* t, cudaStream_t st, cudaEvent_t shading_ready) {
     const bool prof = t->profiling && !t->use_graph;
     auto mark = [&](int i) {
         if (prof) HS_CUDA(cudaEventRecord(t->ev[i], st));
@@ -532,7 +462,7 @@ static void trainer_enqueue_fwd_bwd(hs_trainer* t, cudaStream_t st, cudaEvent_t 
     mark(10);
 }
 
-static void trainer_enqueue_update(hs_trainer* t, cudaStream_t st) {
+void hs::trainer_enqueue_update(hs_trainer* t, cudaStream_t st) {
     adan_fused_launch(t->params.as<float>(), t->grads.as<float>(), t->state.as<float>(), t->P, t->groups,
                       t->total_steps, 0.98, 0.92, 0.99, 1e-8, t->step.as<int>(), t->flags.as<uint32_t>(), st);
     if (t->profiling && !t->use_graph) HS_CUDA(cudaEventRecord(t->ev[11], st));
@@ -540,7 +470,7 @@ static void trainer_enqueue_update(hs_trainer* t, cudaStream_t st) {
 
 static void trainer_raise(hs_trainer* t, uint32_t flags, const uint32_t* stat);
 
-static void trainer_check_after(hs_trainer* t) {
+void hs::trainer_check_after(hs_trainer* t) {
     uint32_t flags = 0, stat[4];
     cudaStream_t st = t->ctx->stream;
     HS_CUDA(cudaMemcpyAsync(&flags, t->flags.p, sizeof(flags), cudaMemcpyDeviceToHost, st));
@@ -1095,7 +1025,7 @@ extern "C" hs_status hs_ipc_close(void* d_ptr) {
 // hs_trainer_slab_counts).  After stage 4 the gradient buffer holds this
 // rank's partial gradient (sum over its rows): all-reduce it, then
 // hs_trainer_apply_update.  Loss partial sums: hs_trainer_loss_partials.
-static void slab_enqueue(hs_trainer* t, int stage, cudaStream_t st) {
+void hs::slab_enqueue(hs_trainer* t, int stage, cudaStream_t st) {
     AsmWork& aw = t->aw;
     const int C = t->c, LC = t->L * t->c;
     float2* send = t->s_send.as<float2>();

@@ -78,6 +78,11 @@ struct hs_ctx {
     int num_sms = 148;
     // reusable work buffers of the standalone C-ABI entry points (capi.cu)
     void* work = nullptr;
+    // NCCL communicator of the sharded steps (comm.cu): one rank per GPU
+    void* comm = nullptr;  // ncclComm_t
+    int comm_size = 1, comm_rank = 0;
+    bool comm_owned = false;
+    void* comm_scratch = nullptr;  // device: agreement word + loss sums
 };
 
 // Device helpers ------------------------------------------------------------------

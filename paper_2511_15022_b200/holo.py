@@ -934,10 +934,39 @@ class Trainer:
         ctx_handle()
         check(_lib.load().hs_trainer_slab_forward_backward(self.h))
 
+    def sharded_step(self, with_loss: bool = True):
+        """One sharded step over the context's NCCL communicator
+        (hs_trainer_sharded_step): exchanges, gradient all-reduce, agreement on
+        the first non-finite group, Adan, loss sums -- all inside the library."""
+        self._ctx = ctx_handle()
+        if with_loss:
+            v = C.c_double(0.0)
+            check(_lib.load().hs_trainer_sharded_step(self.h, C.byref(v)))
+            return v.value
+        check(_lib.load().hs_trainer_sharded_step(self.h, None))
+        return None
+
     def slab_status(self) -> int:
         v = C.c_uint32(0)
         check(_lib.load().hs_trainer_slab_status(self.h, C.byref(v)))
         return int(v.value)
+
+
+def comm_unique_id() -> bytes:
+    """ncclGetUniqueId (hs_comm_unique_id): 128 bytes to ship to every rank."""
+    buf = (C.c_char * 128)()
+    check(_lib.load().hs_comm_unique_id(buf))
+    return bytes(buf)
+
+
+def ctx_comm_init(uid: bytes, nranks: int, rank: int, device=None):
+    """Creates the NCCL communicator inside this device's context (hs_ctx_comm_init)."""
+    buf = (C.c_char * 128).from_buffer_copy(uid)
+    check(_lib.load().hs_ctx_comm_init(ctx_handle(device), buf, int(nranks), int(rank)))
+
+
+def ctx_comm_destroy(device=None):
+    check(_lib.load().hs_ctx_comm_destroy(ctx_handle(device)))
 
 
 def ipc_handle(d_ptr: int) -> bytes:

@@ -343,6 +343,33 @@ class SlabShardedStep:
         return combine_loss(float(parts[0]), float(parts[1]), self.C, self.H, self.W, self.L)
 
 
+class NativeShardedStep:
+    """The sharded step run entirely inside the native library
+    (hs_trainer_sharded_step) over an NCCL communicator held by the device
+    context: the same decompositions as ShardedStep / ChannelShardedStep /
+    SlabShardedStep (chosen by how `trainer` was built), with no torch
+    collective on the step path.  torch.distributed only ships the 128-byte
+    NCCL id once at construction; a C/C++ host does the same with
+    hs_comm_unique_id / hs_ctx_comm_init."""
+
+    def __init__(self, trainer, group=None):
+        from . import holo
+        self.tr = trainer
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        box = [holo.comm_unique_id() if rank == 0 else None]
+        if world > 1:
+            dist.broadcast_object_list(box, src=0, group=group)
+        holo.ctx_comm_init(box[0], world, rank)
+
+    def step(self, with_loss: bool = True):
+        return self.tr.sharded_step(with_loss)
+
+    def close(self):
+        from . import holo
+        holo.ctx_comm_destroy()
+
+
 class LocalSlabGroup:
     """R row-slab trainers on ONE device, stepped in lock-step with the
     all-to-all and the all-reduce done as device copies: the single-GPU

@@ -209,3 +209,49 @@ def test_channel_shards_agree_on_a_rank_local_nonfinite_group(holo):
         assert not np.array_equal(q[r][geo0], p0[r][geo0])          # position/scale/rotation updated
         assert np.array_equal(q[r][5 * n:], p0[r][5 * n:])          # amplitude, phase, opacity untouched
     assert np.array_equal(q[0][:5 * n], q[1][:5 * n])                # the same geometry update on both ranks
+
+
+def _native_scene(holo, n=400, c=3, w=64, h=48, L=2, seed=42, bad=False):
+    gs, target, masks, dist, spec = scene(holo, n, c, w, h, L, seed)
+    if bad:
+        vals = target.values.copy()
+        vals[1, 10, 10] = np.nan
+        target = holo.RealField(c, h, w, vals)
+    return gs, target, masks, dist, spec
+
+
+@pytest.mark.parametrize("mode", ["unsharded", "slab"])
+def test_native_nccl_sharded_step_one_rank(holo, mode):
+    """hs_trainer_sharded_step over a 1-rank NCCL communicator held by the
+    context: the all-reduces, the non-finite agreement, the loss recombination
+    and (row slabs) the grouped ncclSend/ncclRecv transposes all run, and the
+    step equals the plain trainer step."""
+    from paper_2511_15022_b200 import parallel as P
+    gs, target, masks, dist, spec = _native_scene(holo)
+    ref = holo.Trainer(gs, 64, 48, target, masks, dist, spec, 10)
+    t = holo.Trainer(gs, 64, 48, target, masks, dist, spec, 10)
+    if mode == "slab":
+        t.set_row_slab(0, 1)
+    step = P.NativeShardedStep(t)
+    try:
+        for _ in range(3):
+            lr = ref.step(sync_loss=True)
+            ln = step.step(with_loss=True)
+            assert ln == pytest.approx(lr, rel=2e-6), (ln, lr)
+        assert rel_l2(t.params(), ref.params()) < 1e-6
+    finally:
+        step.close()
+
+
+def test_native_nccl_sharded_step_raises_nonfinite(holo):
+    from paper_2511_15022_b200 import parallel as P
+    gs, target, masks, dist, spec = _native_scene(holo, bad=True)
+    t = holo.Trainer(gs, 64, 48, target, masks, dist, spec, 10)
+    p0 = t.params()
+    step = P.NativeShardedStep(t)
+    try:
+        with pytest.raises(holo.HoloNonFinite, match="group position"):
+            step.step(with_loss=True)
+        assert np.array_equal(t.params(), p0)
+    finally:
+        step.close()
