@@ -59,6 +59,9 @@ def parse():
                    help="--shard slabs on ONE GPU: R slab trainers stepped in lock-step with the "
                         "all-to-alls done as device copies (parallel.LocalSlabGroup); reports the "
                         "decomposition's compute per rank, no interconnect")
+    p.add_argument("--native", action="store_true",
+                   help="sharded modes: run the whole sharded step inside the library over its own NCCL "
+                        "communicator (hs_trainer_sharded_step) instead of torch.distributed collectives")
     p.add_argument("--trained-steps", type=int, default=1000,
                    help="N=1: also time the step after this many optimisation steps (trained state: "
                         "moved/rescaled Gaussians, a different pair count); 0 = off")
@@ -366,6 +369,8 @@ def run_sharded(args):
                               wl["masks"], wl["distances"], holo.PropagationSpec(tuple(wl["wavelengths"])),
                               total_steps=total, plane_range=P.plane_shard(L, rank, world))
             step = P.ShardedStep(tr, C_, h, w, L)
+        if args.native and not (args.shard == "slabs" and args.virtual_ranks > 1 and world == 1):
+            step = P.NativeShardedStep(tr)  # (slab peer buffers were mapped by SlabShardedStep above)
         for _ in range(args.warmup):
             loss = step.step()
         stream.synchronize()

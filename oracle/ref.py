@@ -421,3 +421,34 @@ def compute_metrics(recon, target):
     psnr, ssim = np.zeros(L), np.zeros(L)
     _check(lib().ref_compute_metrics(L, c, h, w, _p(recon), _p(target), _p(psnr), _p(ssim)))
     return psnr, ssim
+
+
+# ---- artifact formats (io.cpp:237-335: the reference's own CGHF / CGGS code) --------------------
+def write_field(path, re, im, as_f64=True):
+    c, h, w = re.shape
+    re = np.ascontiguousarray(re, dtype=np.float64)
+    im = np.ascontiguousarray(im, dtype=np.float64)
+    _check(lib().ref_write_field(str(path).encode(), c, h, w, _p(re), _p(im), int(as_f64)))
+
+
+def read_field(path):
+    chw = (C.c_int * 3)()
+    _check(lib().ref_read_field(str(path).encode(), chw, None, None))
+    c, h, w = chw
+    re, im = np.zeros((c, h, w)), np.zeros((c, h, w))
+    _check(lib().ref_read_field(str(path).encode(), chw, _p(re), _p(im)))
+    return re, im
+
+
+def write_gaussians(path, s: GaussianSet):
+    _check(lib().ref_write_gaussians(str(path).encode(), s.count, s.channels, *s.ptrs()))
+
+
+def read_gaussians(path) -> GaussianSet:
+    nc = (C.c_int * 2)()
+    _check(lib().ref_read_gaussians(str(path).encode(), nc, *([None] * 6)))
+    g = GaussianSet.empty(nc[0], nc[1])
+    _check(lib().ref_read_gaussians(str(path).encode(), nc, *g.ptrs()))
+    for name, a in zip(GROUPS, g._keep):
+        setattr(g, name, a)
+    return g

@@ -22,6 +22,7 @@
 #include "holo/complex_field.hpp"
 #include "holo/field_core.hpp"
 #include "holo/gaussian_set.hpp"
+#include "holo/io.hpp"
 #include "holo/convert.hpp"
 #include "holo/loss.hpp"
 #include "holo/optimizer.hpp"
@@ -123,6 +124,37 @@ const char* ref_last_error() { return g_err.c_str(); }
 
 void ref_set_thread_count(int t) { set_thread_count(t); }
 int ref_thread_count() { return thread_count(); }
+
+// ---- artifact formats (io.cpp:237-335, the reference's own writers/readers) ----
+int ref_write_field(const char* path, int c, int h, int w, const double* re, const double* im, int as_f64) {
+    return guard([&] {
+        ComplexField f(c, h, w);
+        std::memcpy(f.real.data(), re, f.size() * sizeof(double));
+        std::memcpy(f.imag.data(), im, f.size() * sizeof(double));
+        write_field(path, f, as_f64 != 0);
+    });
+}
+// shape query (re == nullptr) or read into re/im of the caller's size
+int ref_read_field(const char* path, int* chw, double* re, double* im) {
+    return guard([&] {
+        const ComplexField f = read_field(path);
+        chw[0] = f.channels;
+        chw[1] = f.height;
+        chw[2] = f.width;
+        if (re) store_field(f, re, im);
+    });
+}
+int ref_write_gaussians(const char* path, SET_ARGS) {
+    return guard([&] { write_gaussians(path, make_set(n, c, pos, scale, rot, amp, phase, opac)); });
+}
+int ref_read_gaussians(const char* path, int* nc, SET_OUT) {
+    return guard([&] {
+        const GaussianSet s = read_gaussians(path);
+        nc[0] = s.count;
+        nc[1] = s.channels;
+        if (o_pos) unpack_set(s, o_pos, o_scale, o_rot, o_amp, o_phase, o_opac);
+    });
+}
 
 // ---- fixtures (tests/test_util.hpp, pipeline.cpp:165-200) -----------------
 int ref_random_set(uint64_t seed, int count, int channels, int width, int height, SET_OUT) {

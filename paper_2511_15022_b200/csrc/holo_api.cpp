@@ -771,7 +771,7 @@ struct ByteReader {
     const unsigned char* p;
     size_t left;
     void need(size_t n) const {
-        if (left < n) throw std::runtime_error(path + ": truncated file");
+        if (left < n) throw std::runtime_error("truncated file");  // io.cpp:44-47 (no path)
     }
     template <class T>
     T get() {

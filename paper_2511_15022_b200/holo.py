@@ -382,7 +382,7 @@ def read_field(path: str) -> ComplexField:
     if len(data) < 4 or data[:4] != b"CGHF":
         raise HoloError(f"{path}: not a CGHF file")
     if len(data) < 19:
-        raise HoloError(f"{path}: truncated file")
+        raise HoloError("truncated file")  # io.cpp:44-47 (no path)
     ver, c, h, w, dtype = struct.unpack_from("<HIIIB", data, 4)
     if ver != 1:
         raise HoloError(f"{path}: unsupported CGHF version")
@@ -391,7 +391,7 @@ def read_field(path: str) -> ComplexField:
     n = c * h * w
     item = 8 if dtype else 4
     if len(data) < 19 + 2 * n * item:
-        raise HoloError(f"{path}: truncated file")
+        raise HoloError("truncated file")  # io.cpp:44-47 (no path)
     if len(data) != 19 + 2 * n * item:
         raise HoloError(f"{path}: trailing bytes")
     v = np.frombuffer(data, dtype="<f8" if dtype else "<f4", offset=19, count=2 * n).astype(np.float64)
@@ -411,13 +411,13 @@ def read_gaussians(path: str) -> GaussianSet:
     if len(data) < 4 or data[:4] != b"CGGS":
         raise HoloError(f"{path}: not a CGGS file")
     if len(data) < 14:
-        raise HoloError(f"{path}: truncated file")
+        raise HoloError("truncated file")  # io.cpp:44-47 (no path)
     ver, n, c = struct.unpack_from("<HII", data, 4)
     if ver != 1:
         raise HoloError(f"{path}: unsupported CGGS version")
     count = (6 + 2 * c) * n
     if len(data) < 14 + 4 * count:
-        raise HoloError(f"{path}: truncated file")
+        raise HoloError("truncated file")  # io.cpp:44-47 (no path)
     if len(data) != 14 + 4 * count:
         raise HoloError(f"{path}: trailing bytes")
     flat = np.frombuffer(data, dtype="<f4", offset=14, count=count).astype(np.float64)
