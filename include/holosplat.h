@@ -69,6 +69,11 @@ hs_status hs_copy_d2h(hs_ctx* ctx, void* h_dst, const void* d_src, size_t bytes)
  * [begin,end) of tile t, {0,0} when empty.  Two-call protocol: with cap <
  * needed nothing but *npairs and tiles_xy is written.  Bit-exact with
  * holo::build_tile_index on the same (fp32-valued) parameters. */
+/* Binning of the standalone raster entry points (default 1 = tight): keep only
+ * the (tile, Gaussian) pairs whose tile the Gaussian's ellipse can reach; the
+ * rasterized field is bit-identical to binning with the reference's box lists
+ * (0).  hs_build_tile_index always exports the reference's exact lists. */
+hs_status hs_ctx_set_tight_binning(hs_ctx* ctx, int tight);
 hs_status hs_build_tile_index(hs_ctx* ctx, const float* d_params, int n, int c, int width,
                               int height, uint32_t* d_tiles, uint32_t* d_ids,
                               uint64_t* d_ranges, int64_t cap, int64_t* npairs, int* tiles_xy);

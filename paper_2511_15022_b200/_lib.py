@@ -11,7 +11,9 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libholosplat.so")
+# HOLOSPLAT_LIB: load another build of the same library (A/B timing of two
+# builds in one process tree, tools/ab_build.sh); the default is the in-tree build.
+LIB_PATH = os.environ.get("HOLOSPLAT_LIB") or os.path.join(_HERE, "libholosplat.so")
 CXX_LIB_PATH = os.path.join(_HERE, "libholo_b200.so")
 
 HS_OK, HS_EINVAL, HS_ENONFINITE, HS_ECUDA, HS_ENOMEM, HS_EOVERFLOW = range(6)
@@ -136,6 +138,7 @@ _SIGS = {
     "hs_ctx_comm_info": [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int)],
     "hs_ctx_comm_destroy": [C.c_void_p],
     "hs_trainer_sharded_step": [C.c_void_p, C.POINTER(C.c_double)],
+    "hs_ctx_set_tight_binning": [C.c_void_p, C.c_int],
     "hs_random_uniform": [C.c_uint64, C.c_int64, C.c_double, C.c_double, C.c_void_p],
     "hs_ipc_get_handle": [C.c_void_p, C.c_void_p],
     "hs_ipc_open_handle": [C.c_void_p, C.POINTER(C.c_void_p)],
@@ -175,6 +178,8 @@ def load(path: str = LIB_PATH):
             "(there is no CPU fallback)")
     lib = C.CDLL(path)
     for name, args in _SIGS.items():
+        if os.environ.get("HOLOSPLAT_LIB") and not hasattr(lib, name):
+            continue  # an older A/B build (tools/ab_build.sh) without a newer entry point
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = _RESTYPES.get(name, C.c_int)

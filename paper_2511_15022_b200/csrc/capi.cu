@@ -140,6 +140,11 @@ extern "C" hs_status hs_build_tile_index(hs_ctx* ctx, const float* d_params, int
         tiles_xy[0] = rw.tiles_x;
         tiles_xy[1] = rw.tiles_y;
         cudaStream_t st = ctx->stream;
+        rw.tight = false;  // the reference's exact (tile, id) list (rasterizer.cpp:90-119)
+        struct Restore {
+            RasterWork& r;
+            ~Restore() { r.tight = true; }
+        } restore{rw};  // (back to the default: tight)
         for (int attempt = 0; attempt < 2; ++attempt) {
             rw.project_and_bin(d_params, st);
             uint32_t stat[4] = {0, 0, 0, 0};
@@ -165,6 +170,10 @@ extern "C" hs_status hs_build_tile_index(hs_ctx* ctx, const float* d_params, int
         }
         throw Error(HS_EOVERFLOW, "build_tile_index: pair capacity");
     });
+}
+
+extern "C" hs_status hs_ctx_set_tight_binning(hs_ctx* ctx, int tight) {
+    return guard([&] { work_of(ctx).rw.tight = tight != 0; });
 }
 
 static void raster_prepare_and_bin(hs_ctx* ctx, RasterWork& rw, const float* d_params, int n, int c,

@@ -224,6 +224,37 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(const uint32_t*
     }
 }
 
+// Conservative test: can any pixel of the cell [cx0, cx0 + cw] x [cy0, cy0 + ch]
+// (inclusive integer pixel coordinates) pass the Gaussian's exact skip tests?
+// The ellipse mahal <= cut + tol, widened by 1e-2 px, against the rectangle:
+// for the rectangle's row band the ellipse's x-extent at the band row closest
+// to the centre (widest chord) around the centre line shifted to both band edges.
+__device__ __forceinline__ bool cell_hit(float4 r0, float4 r1, float4 r2, float cx0, float cy0,
+                                         float cw, float ch) {
+    const float M = r1.w + r2.y;
+    const float px = r0.x + r0.z, py = r0.y + r0.w;
+    const float dya = cy0 - py, dyb = dya + ch;
+    const float dyc = fminf(fmaxf(0.f, dya), dyb);
+    const float D = r1.x * M - r2.z * dyc * dyc;
+    if (D < 0.f) return false;
+    const float hw = sqrtf(D) * r2.w + 1e-2f;
+    const float ratio = r1.y * r2.w;
+    const float ca = -ratio * dya, cb = -ratio * dyb;
+    const float xlo = px + fminf(ca, cb) - hw, xhi = px + fmaxf(ca, cb) + hw;
+    return xhi >= cx0 && xlo <= cx0 + cw;
+}
+
+// Tight binning (trainer and forward paths): a (tile, Gaussian) pair of the
+// reference's box list (rasterizer.cpp:95-108) is kept only if the ellipse can
+// reach the tile.  Dropped pairs contribute exactly zero to every pixel of the
+// tile (their pixels all fail mahal <= cutoff), and the kept ids stay ascending,
+// so the forward field is bit-identical; build_tile_index (the exported,
+// reference-exact list) bins with tight = 0.
+__device__ __forceinline__ bool tile_touch(float4 r0, float4 r1, float4 r2, int tx, int ty) {
+    return cell_hit(r0, r1, r2, static_cast<float>(tx * kTile), static_cast<float>(ty * kTile),
+                    static_cast<float>(kTile - 1), static_cast<float>(kTile - 1));
+}
+
 // Scatter (duplicate-with-keys, :94-108): tcount is consumed as a countdown.
 // Per-tile Gaussian counts: 16 threads per Gaussian, one fire-and-forget
 // atomic per (Gaussian, tile) pair.
@@ -268,13 +299,24 @@ __device__ __forceinline__ int pick(int idx, int n, const uint32_t* list, const 
 __global__ void __launch_bounds__(256) count_tiles_kernel(int n, const int4* __restrict__ tbox, int tiles_x,
                                                           uint32_t* __restrict__ tcount, int ty_lo, int ty_hi,
                                                           const uint32_t* __restrict__ list,
-                                                          const uint32_t* __restrict__ list_n) {
+                                                          const uint32_t* __restrict__ list_n,
+                                                          const float4* __restrict__ rec, int tight) {
     const int g = pick(blockIdx.x * (256 / kScatterSub) + threadIdx.x / kScatterSub, n, list, list_n);
     const int sub = threadIdx.x % kScatterSub;
     if (g < 0) return;
     const int4 b = band_box(tbox[g], ty_lo, ty_hi);
     const int nx = b.y - b.x + 1, cnt = box_count(b);
-    for (int k = sub; k < cnt; k += kScatterSub) atomicAdd(tcount + (b.z + k / nx) * tiles_x + b.x + k % nx, 1u);
+    float4 r0{}, r1{}, r2{};
+    if (tight && cnt > 1) {
+        r0 = rec[g];
+        r1 = rec[static_cast<size_t>(n) + g];
+        r2 = rec[2 * static_cast<size_t>(n) + g];
+    }
+    for (int k = sub; k < cnt; k += kScatterSub) {
+        const int tx = b.x + k % nx, ty = b.z + k / nx;
+        if (tight && cnt > 1 && !tile_touch(r0, r1, r2, tx, ty)) continue;
+        atomicAdd(tcount + ty * tiles_x + tx, 1u);
+    }
 }
 
 // 16 threads per Gaussian, thread k handling tiles k, k + 16, ... of its tile
@@ -286,14 +328,23 @@ __global__ void __launch_bounds__(256) scatter_ids_kernel(int n, const int4* __r
                                                           const uint32_t* __restrict__ status,
                                                           uint32_t* __restrict__ ids, int ty_lo, int ty_hi,
                                                           const uint32_t* __restrict__ list,
-                                                          const uint32_t* __restrict__ list_n) {
+                                                          const uint32_t* __restrict__ list_n,
+                                                          const float4* __restrict__ rec, int tight) {
     const int g = pick(blockIdx.x * (256 / kScatterSub) + threadIdx.x / kScatterSub, n, list, list_n);
     const int sub = threadIdx.x % kScatterSub;
     if (g < 0 || status[1]) return;
     const int4 b = band_box(tbox[g], ty_lo, ty_hi);
     const int nx = b.y - b.x + 1, cnt = box_count(b);
+    float4 r0{}, r1{}, r2{};
+    if (tight && cnt > 1) {
+        r0 = rec[g];
+        r1 = rec[static_cast<size_t>(n) + g];
+        r2 = rec[2 * static_cast<size_t>(n) + g];
+    }
     for (int k = sub; k < cnt; k += kScatterSub) {
-        const int t = (b.z + k / nx) * tiles_x + b.x + k % nx;
+        const int tx = b.x + k % nx, ty = b.z + k / nx;
+        if (tight && cnt > 1 && !tile_touch(r0, r1, r2, tx, ty)) continue;
+        const int t = ty * tiles_x + tx;
         const uint32_t slot = atomicSub(tcount + t, 1u) - 1u;
         ids[toffset[t] + slot] = static_cast<uint32_t>(g);
     }
@@ -476,20 +527,6 @@ __device__ __noinline__ float4 exact_contrib4(const double* __restrict__ q, size
 constexpr int kFwdThreads = 128;  // 4 warps per 16x16 tile, each an 8x8 cell
 constexpr int kFwdBatch = 128;
 
-__device__ __forceinline__ bool cell_hit(float4 r0, float4 r1, float4 r2, float cx0, float cy0,
-                                         float cw, float ch) {
-    const float M = r1.w + r2.y;
-    const float px = r0.x + r0.z, py = r0.y + r0.w;
-    const float dya = cy0 - py, dyb = dya + ch;
-    const float dyc = fminf(fmaxf(0.f, dya), dyb);
-    const float D = r1.x * M - r2.z * dyc * dyc;
-    if (D < 0.f) return false;
-    const float hw = sqrtf(D) * r2.w + 1e-2f;
-    const float ratio = r1.y * r2.w;
-    const float ca = -ratio * dya, cb = -ratio * dyb;
-    const float xlo = px + fminf(ca, cb) - hw, xhi = px + fmaxf(ca, cb) + hw;
-    return xhi >= cx0 && xlo <= cx0 + cw;
-}
 
 // staged Gaussian of the forward kernel (shared memory)
 template <int C>
@@ -942,14 +979,14 @@ void RasterWork::project_and_bin(const float* d_params, cudaStream_t st, cudaEve
     }
     count_tiles_kernel<<<ceil_div(n, 256 / kScatterSub), 256, 0, st>>>(n, tbox.as<int4>(), tiles_x,
                                                                        tcount.as<uint32_t>(), band_ty0, band_ty1, lst,
-                                                                       lst_n);
+                                                                       lst_n, rec.as<float4>(), tight ? 1 : 0);
     launch_check("count_tiles");
     tile_scan_kernel<<<1, kScanThreads, 0, st>>>(tcount.as<uint32_t>(), tiles, toffset.as<uint32_t>(), ranges.as<uint2>(),
                                          stat, cap);
     launch_check("tile_scan");
     scatter_ids_kernel<<<ceil_div(n, 256 / kScatterSub), 256, 0, st>>>(n, tbox.as<int4>(), tiles_x, toffset.as<uint32_t>(),
                                                          tcount.as<uint32_t>(), stat, ids.as<uint32_t>(), band_ty0,
-                                                         band_ty1, lst, lst_n);
+                                                         band_ty1, lst, lst_n, rec.as<float4>(), tight ? 1 : 0);
     launch_check("scatter_ids");
     segment_sort_warp_kernel<<<ceil_div(tiles, 8), 256, 0, st>>>(ranges.as<uint2>(), tiles, ids.as<uint32_t>(),
                                                                   stat);

@@ -30,6 +30,10 @@ struct RasterWork {
     int band_y0 = -1, band_y1 = -1;
     DevBuf band_list, band_n;
     bool banded() const { return band_y0 >= 0; }
+    // Tight binning (default): keep only the (tile, Gaussian) pairs whose tile the
+    // ellipse can reach; the forward field is bit-identical.  false: the
+    // reference's exact box list (build_tile_index export).
+    bool tight = true;
 
     void prepare(int n_, int c_, int w_, int h_);
     void reserve_pairs(int64_t cap_);

@@ -354,3 +354,34 @@ def test_desk_regression_matches_reference_run(holo, ref, ratio):
     assert abs(m.mean_psnr - DESK_PSNR[ratio]) <= 0.1, (ratio, m.mean_psnr)
     if ratio == 2.0:
         assert abs(m.mean_ssim - DESK_SSIM_R2) <= 0.005, m.mean_ssim
+
+
+def _field_with_binning(holo, g, n, c, w, h, tight):
+    import ctypes as C
+    from paper_2511_15022_b200 import _lib
+    holo.check(_lib.load().hs_ctx_set_tight_binning(holo.ctx_handle(), int(tight)))
+    try:
+        return holo.rasterize_forward(holo.GaussianSet(n, c, **g), w, h)
+    finally:
+        holo.check(_lib.load().hs_ctx_set_tight_binning(holo.ctx_handle(), 1))
+
+
+@pytest.mark.parametrize("state", ["init", "trained"])
+def test_tight_binning_field_is_bit_identical(holo, ref, state):
+    """The trainer bins tightly (only tiles the ellipse can reach): the forward
+    field is bit-identical to binning with the reference's box lists, with
+    fewer (tile, Gaussian) pairs."""
+    if state == "init":
+        sc = Scene(holo, ref, "cfg2")
+        g = sc.g
+    else:
+        sc, g = trained(holo, ref, "cfg2", 200)
+    a = _field_with_binning(holo, g, sc.n, sc.c, sc.w, sc.h, True)
+    b = _field_with_binning(holo, g, sc.n, sc.c, sc.w, sc.h, False)
+    assert np.array_equal(a.real, b.real) and np.array_equal(a.imag, b.imag)
+    tr = sc.trainer(groups=g)
+    tr.forward_backward()
+    k_tight = tr.last_loss()[1]
+    k_ref = holo.build_tile_index(holo.GaussianSet(sc.n, sc.c, **g), sc.w, sc.h).pairs.shape[0]
+    print(f"PARITY tight binning ({state}): field bit-identical, pairs {k_tight} vs reference {k_ref}")
+    assert k_tight < k_ref
