@@ -52,7 +52,105 @@ struct ProjParams {
     int4* tbox;
     uint32_t* tcount;  // Gaussians per tile (atomics)
     uint32_t* status;
+    int fuse_shade;    // also write the per-channel shading record
+    uint4* trows;      // tight binning: touched tile columns per box row (nullptr: off)
 };
+
+// Per-channel shading (rasterizer.cpp:78-85).  fp32: the record is only
+// consumed in fp32, and sincosf has accurate range reduction (~1 ulp).
+__device__ __forceinline__ void shade_one(const float* __restrict__ params, int g, int n, int c,
+                                          float4* __restrict__ shade, uint32_t* __restrict__ status) {
+    const size_t N = n;
+    const float* amp = params + 5 * N;       // after pre_position 2N | pre_scale 2N | rotation N
+    const float* pha = amp + N * c;
+    for (int ch = 0; ch < c; ++ch) {
+        const size_t i = static_cast<size_t>(g) * c + ch;
+        const float a = fminf(fmaxf(amp[i], 0.f), 1.f);
+        const float ph = pha[i];
+        if (!isfinite(ph) || !isfinite(amp[i])) atomicOr(status + 2, 1u);
+        float sp, cp;
+        sincosf(ph, &sp, &cp);
+        shade[static_cast<size_t>(ch) * N + g] = make_float4(a * cp, a * sp, cp, sp);
+    }
+}
+
+// Its own kernel when the amplitude/phase groups can still be in flight
+// (host-resident parameter upload) while the geometry is binned.
+__global__ void shade_kernel(const float* __restrict__ params, int n, int c, float4* __restrict__ shade,
+                             uint32_t* __restrict__ status) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < n) shade_one(params, g, n, c, shade, status);
+}
+
+// Conservative x-extent [xlo, xhi] (pixels) of the Gaussian's skip-test region
+// (the ellipse mahal <= cut + tol, widened by 1e-2 px) over the row band
+// [cy0, cy0 + ch]: the widest chord (band row closest to the centre) around the
+// centre line shifted to both band edges.  False when no band row meets it.
+__device__ __forceinline__ bool row_band_extent(float4 r0, float4 r1, float4 r2, float cy0, float ch, float& xlo,
+                                                float& xhi) {
+    const float M = r1.w + r2.y;
+    const float px = r0.x + r0.z, py = r0.y + r0.w;
+    const float dya = cy0 - py, dyb = dya + ch;
+    const float dyc = fminf(fmaxf(0.f, dya), dyb);
+    const float D = r1.x * M - r2.z * dyc * dyc;
+    if (D < 0.f) return false;
+    const float hw = sqrtf(D) * r2.w + 1e-2f;
+    const float ratio = r1.y * r2.w;
+    const float ca = -ratio * dya, cb = -ratio * dyb;
+    xlo = px + fminf(ca, cb) - hw;
+    xhi = px + fmaxf(ca, cb) + hw;
+    return true;
+}
+
+// Can any pixel of the cell [cx0, cx0 + cw] x [cy0, cy0 + ch] pass the exact tests?
+__device__ __forceinline__ bool cell_hit(float4 r0, float4 r1, float4 r2, float cx0, float cy0,
+                                         float cw, float ch) {
+    float xlo, xhi;
+    if (!row_band_extent(r0, r1, r2, cy0, ch, xlo, xhi)) return false;
+    return xhi >= cx0 && xlo <= cx0 + cw;
+}
+
+// Tight binning (trainer and forward paths): a (tile, Gaussian) pair of the
+// reference's box list (rasterizer.cpp:95-108) is kept only if the ellipse can
+// reach the tile.  Dropped pairs contribute exactly zero to every pixel of the
+// tile (their pixels all fail mahal <= cutoff), and the kept ids stay ascending,
+// so the forward field is bit-identical; build_tile_index (the exported,
+// reference-exact list) bins with tight off.  The projection stores, for the
+// first kTightRows tile rows of the box, the touched tile-column range relative
+// to the box (one byte each for lo and hi, lo > hi = none); rows beyond that,
+// or boxes wider than 255 tiles, keep the whole box row.
+constexpr int kTightRows = 8;
+
+__device__ __forceinline__ uint4 tight_rows(float4 r0, float4 r1, float4 r2, int tx0, int tx1, int ty0, int ty1) {
+    uint32_t lo[2] = {0u, 0u}, hi[2] = {0xffffffffu, 0xffffffffu};  // default: whole row
+    if (tx1 - tx0 > 254) return make_uint4(lo[0], lo[1], hi[0], hi[1]);
+    for (int r = 0; r < kTightRows && ty0 + r <= ty1; ++r) {
+        float xlo, xhi;
+        int a = 255, b = 0;  // empty
+        if (row_band_extent(r0, r1, r2, static_cast<float>((ty0 + r) * kTile), static_cast<float>(kTile - 1), xlo,
+                            xhi)) {
+            // tiles tx with xlo <= tx*16 + 15 and tx*16 <= xhi: cell_hit over the tile, exactly
+            // (xlo - 15 and the scalings by 1/16 are exact in fp32 on the canvas range)
+            a = max(static_cast<int>(ceilf((xlo - static_cast<float>(kTile - 1)) * (1.f / kTile))), tx0) - tx0;
+            b = min(static_cast<int>(floorf(xhi * (1.f / kTile))), tx1) - tx0;
+            if (a > b) a = 255, b = 0;
+        }
+        const int w = r >> 2, sh = 8 * (r & 3);
+        lo[w] = (lo[w] & ~(0xffu << sh)) | (static_cast<uint32_t>(a) << sh);
+        hi[w] = (hi[w] & ~(0xffu << sh)) | (static_cast<uint32_t>(b) << sh);
+    }
+    return make_uint4(lo[0], lo[1], hi[0], hi[1]);
+}
+
+// Is tile (tx, ty) of the box (origin tx0, ty0) in the tight set?
+__device__ __forceinline__ bool tight_has(uint4 t, int tx, int ty, int tx0, int ty0) {
+    const int r = ty - ty0;
+    if (r >= kTightRows) return true;
+    const int sh = 8 * (r & 3);
+    const uint32_t lo = ((r < 4 ? t.x : t.y) >> sh) & 0xffu, hi = ((r < 4 ? t.z : t.w) >> sh) & 0xffu;
+    const uint32_t o = static_cast<uint32_t>(tx - tx0);
+    return o >= lo && o <= hi;
+}
 
 __global__ void project_kernel(ProjParams P) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
@@ -129,35 +227,20 @@ __global__ void project_kernel(ProjParams P) {
     P.rec[g] = make_float4(px_hi, py_hi, px_lo, py_lo);
     P.rec[N + g] = make_float4(static_cast<float>(i00), static_cast<float>(i01),
                                static_cast<float>(i11), static_cast<float>(mahal_cutoff));
-    P.rec[2 * N + g] = make_float4(static_cast<float>(log2(alpha)), static_cast<float>(tol),
-                                   static_cast<float>(det_inv), static_cast<float>(1.0 / i00));
+    const float4 q0 = make_float4(px_hi, py_hi, px_lo, py_lo);
+    const float4 q1 = make_float4(static_cast<float>(i00), static_cast<float>(i01), static_cast<float>(i11),
+                                  static_cast<float>(mahal_cutoff));
+    const float4 q2 = make_float4(static_cast<float>(log2(alpha)), static_cast<float>(tol),
+                                  static_cast<float>(det_inv), static_cast<float>(1.0 / i00));
+    P.rec[2 * N + g] = q2;
+    if (P.trows) P.trows[g] = tight_rows(q0, q1, q2, tx0, tx1, ty0, ty1);
     double* q = P.p64 + g;
     q[0] = px; q[N] = py; q[2 * N] = i00; q[3 * N] = i01; q[4 * N] = i11; q[5 * N] = mahal_cutoff;
     q[6 * N] = alpha; q[7 * N] = r;
-    // per-channel shading (rasterizer.cpp:78-85): shade_kernel
     if (!finite(th)) atomicOr(P.status + 2, 1u);
-}
-
-// Per-channel shading (rasterizer.cpp:78-85), its own kernel so that the
-// amplitude/phase groups can still be in flight (host-resident parameter
-// upload) while the geometry is binned.  fp32: the record is only consumed in
-// fp32, and sincosf has accurate range reduction (~1 ulp).
-__global__ void shade_kernel(const float* __restrict__ params, int n, int c, float4* __restrict__ shade,
-                             uint32_t* __restrict__ status) {
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= n) return;
-    const size_t N = n;
-    const float* amp = params + 5 * N;       // after pre_position 2N | pre_scale 2N | rotation N
-    const float* pha = amp + N * c;
-    for (int ch = 0; ch < c; ++ch) {
-        const size_t i = static_cast<size_t>(g) * c + ch;
-        const float a = fminf(fmaxf(amp[i], 0.f), 1.f);
-        const float ph = pha[i];
-        if (!isfinite(ph) || !isfinite(amp[i])) atomicOr(status + 2, 1u);
-        float sp, cp;
-        sincosf(ph, &sp, &cp);
-        shade[static_cast<size_t>(ch) * N + g] = make_float4(a * cp, a * sp, cp, sp);
-    }
+    // per-channel shading (rasterizer.cpp:78-85), fused unless the amplitude /
+    // phase groups may still be uploading (then shade_kernel runs after them)
+    if (P.fuse_shade) shade_one(P.params, g, P.n, P.c, P.shade, P.status);
 }
 
 // ---------------------------------------------------------------------------
@@ -224,37 +307,6 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(const uint32_t*
     }
 }
 
-// Conservative test: can any pixel of the cell [cx0, cx0 + cw] x [cy0, cy0 + ch]
-// (inclusive integer pixel coordinates) pass the Gaussian's exact skip tests?
-// The ellipse mahal <= cut + tol, widened by 1e-2 px, against the rectangle:
-// for the rectangle's row band the ellipse's x-extent at the band row closest
-// to the centre (widest chord) around the centre line shifted to both band edges.
-__device__ __forceinline__ bool cell_hit(float4 r0, float4 r1, float4 r2, float cx0, float cy0,
-                                         float cw, float ch) {
-    const float M = r1.w + r2.y;
-    const float px = r0.x + r0.z, py = r0.y + r0.w;
-    const float dya = cy0 - py, dyb = dya + ch;
-    const float dyc = fminf(fmaxf(0.f, dya), dyb);
-    const float D = r1.x * M - r2.z * dyc * dyc;
-    if (D < 0.f) return false;
-    const float hw = sqrtf(D) * r2.w + 1e-2f;
-    const float ratio = r1.y * r2.w;
-    const float ca = -ratio * dya, cb = -ratio * dyb;
-    const float xlo = px + fminf(ca, cb) - hw, xhi = px + fmaxf(ca, cb) + hw;
-    return xhi >= cx0 && xlo <= cx0 + cw;
-}
-
-// Tight binning (trainer and forward paths): a (tile, Gaussian) pair of the
-// reference's box list (rasterizer.cpp:95-108) is kept only if the ellipse can
-// reach the tile.  Dropped pairs contribute exactly zero to every pixel of the
-// tile (their pixels all fail mahal <= cutoff), and the kept ids stay ascending,
-// so the forward field is bit-identical; build_tile_index (the exported,
-// reference-exact list) bins with tight = 0.
-__device__ __forceinline__ bool tile_touch(float4 r0, float4 r1, float4 r2, int tx, int ty) {
-    return cell_hit(r0, r1, r2, static_cast<float>(tx * kTile), static_cast<float>(ty * kTile),
-                    static_cast<float>(kTile - 1), static_cast<float>(kTile - 1));
-}
-
 // Scatter (duplicate-with-keys, :94-108): tcount is consumed as a countdown.
 // Per-tile Gaussian counts: 16 threads per Gaussian, one fire-and-forget
 // atomic per (Gaussian, tile) pair.
@@ -300,21 +352,17 @@ __global__ void __launch_bounds__(256) count_tiles_kernel(int n, const int4* __r
                                                           uint32_t* __restrict__ tcount, int ty_lo, int ty_hi,
                                                           const uint32_t* __restrict__ list,
                                                           const uint32_t* __restrict__ list_n,
-                                                          const float4* __restrict__ rec, int tight) {
+                                                          const uint4* __restrict__ trows) {
     const int g = pick(blockIdx.x * (256 / kScatterSub) + threadIdx.x / kScatterSub, n, list, list_n);
     const int sub = threadIdx.x % kScatterSub;
     if (g < 0) return;
-    const int4 b = band_box(tbox[g], ty_lo, ty_hi);
+    const int4 b0 = tbox[g];
+    const int4 b = band_box(b0, ty_lo, ty_hi);
     const int nx = b.y - b.x + 1, cnt = box_count(b);
-    float4 r0{}, r1{}, r2{};
-    if (tight && cnt > 1) {
-        r0 = rec[g];
-        r1 = rec[static_cast<size_t>(n) + g];
-        r2 = rec[2 * static_cast<size_t>(n) + g];
-    }
+    const uint4 tr = trows ? trows[g] : make_uint4(0u, 0u, ~0u, ~0u);
     for (int k = sub; k < cnt; k += kScatterSub) {
         const int tx = b.x + k % nx, ty = b.z + k / nx;
-        if (tight && cnt > 1 && !tile_touch(r0, r1, r2, tx, ty)) continue;
+        if (!tight_has(tr, tx, ty, b0.x, b0.z)) continue;
         atomicAdd(tcount + ty * tiles_x + tx, 1u);
     }
 }
@@ -329,21 +377,17 @@ __global__ void __launch_bounds__(256) scatter_ids_kernel(int n, const int4* __r
                                                           uint32_t* __restrict__ ids, int ty_lo, int ty_hi,
                                                           const uint32_t* __restrict__ list,
                                                           const uint32_t* __restrict__ list_n,
-                                                          const float4* __restrict__ rec, int tight) {
+                                                          const uint4* __restrict__ trows) {
     const int g = pick(blockIdx.x * (256 / kScatterSub) + threadIdx.x / kScatterSub, n, list, list_n);
     const int sub = threadIdx.x % kScatterSub;
     if (g < 0 || status[1]) return;
-    const int4 b = band_box(tbox[g], ty_lo, ty_hi);
+    const int4 b0 = tbox[g];
+    const int4 b = band_box(b0, ty_lo, ty_hi);
     const int nx = b.y - b.x + 1, cnt = box_count(b);
-    float4 r0{}, r1{}, r2{};
-    if (tight && cnt > 1) {
-        r0 = rec[g];
-        r1 = rec[static_cast<size_t>(n) + g];
-        r2 = rec[2 * static_cast<size_t>(n) + g];
-    }
+    const uint4 tr = trows ? trows[g] : make_uint4(0u, 0u, ~0u, ~0u);
     for (int k = sub; k < cnt; k += kScatterSub) {
         const int tx = b.x + k % nx, ty = b.z + k / nx;
-        if (tight && cnt > 1 && !tile_touch(r0, r1, r2, tx, ty)) continue;
+        if (!tight_has(tr, tx, ty, b0.x, b0.z)) continue;
         const int t = ty * tiles_x + tx;
         const uint32_t slot = atomicSub(tcount + t, 1u) - 1u;
         ids[toffset[t] + slot] = static_cast<uint32_t>(g);
@@ -430,7 +474,11 @@ __global__ void __launch_bounds__(256) segment_sort_warp_kernel(const uint2* __r
     const uint2 r = ranges[t];
     const int n = static_cast<int>(r.y - r.x);
     if (n <= 1 || n > kWarpSeg) return;
-    if (n <= 256) warp_bitonic<8>(ids + r.x, n, lane);
+    // network size by segment length (tight binning: ~100 ids per tile at cfg2)
+    if (n <= 32) warp_bitonic<1>(ids + r.x, n, lane);
+    else if (n <= 64) warp_bitonic<2>(ids + r.x, n, lane);
+    else if (n <= 128) warp_bitonic<4>(ids + r.x, n, lane);
+    else if (n <= 256) warp_bitonic<8>(ids + r.x, n, lane);
     else warp_bitonic<16>(ids + r.x, n, lane);
 }
 
@@ -936,6 +984,7 @@ void RasterWork::prepare(int n_, int c_, int w_, int h_) {
     p64.reserve(N * 8 * sizeof(double));
     pbox.reserve(N * sizeof(int4));
     tbox.reserve(N * sizeof(int4));
+    trows.reserve(N * sizeof(uint4));
     raw.reserve(N * (2 * c + 6) * sizeof(float));
     tcount.reserve(static_cast<size_t>(tiles_x) * tiles_y * sizeof(uint32_t));
     toffset.reserve(static_cast<size_t>(tiles_x) * tiles_y * sizeof(uint32_t));
@@ -962,7 +1011,7 @@ void RasterWork::project_and_bin(const float* d_params, cudaStream_t st, cudaEve
     HS_CUDA(cudaMemsetAsync(tcount.p, 0, static_cast<size_t>(tiles) * sizeof(uint32_t), st));
     ProjParams P{d_params, n,  c,  width, height, tiles_x, tiles_y, rec.as<float4>(),
                  shade.as<float4>(), p64.as<double>(), pbox.as<int4>(), tbox.as<int4>(),
-                 tcount.as<uint32_t>(), stat};
+                 tcount.as<uint32_t>(), stat, shading_ready ? 0 : 1, tight ? trows.as<uint4>() : nullptr};
     project_kernel<<<ceil_div(n, 128), 128, 0, st>>>(P);
     launch_check("project");
     const uint32_t* lst = nullptr;
@@ -979,14 +1028,14 @@ void RasterWork::project_and_bin(const float* d_params, cudaStream_t st, cudaEve
     }
     count_tiles_kernel<<<ceil_div(n, 256 / kScatterSub), 256, 0, st>>>(n, tbox.as<int4>(), tiles_x,
                                                                        tcount.as<uint32_t>(), band_ty0, band_ty1, lst,
-                                                                       lst_n, rec.as<float4>(), tight ? 1 : 0);
+                                                                       lst_n, tight ? trows.as<uint4>() : nullptr);
     launch_check("count_tiles");
     tile_scan_kernel<<<1, kScanThreads, 0, st>>>(tcount.as<uint32_t>(), tiles, toffset.as<uint32_t>(), ranges.as<uint2>(),
                                          stat, cap);
     launch_check("tile_scan");
     scatter_ids_kernel<<<ceil_div(n, 256 / kScatterSub), 256, 0, st>>>(n, tbox.as<int4>(), tiles_x, toffset.as<uint32_t>(),
                                                          tcount.as<uint32_t>(), stat, ids.as<uint32_t>(), band_ty0,
-                                                         band_ty1, lst, lst_n, rec.as<float4>(), tight ? 1 : 0);
+                                                         band_ty1, lst, lst_n, tight ? trows.as<uint4>() : nullptr);
     launch_check("scatter_ids");
     segment_sort_warp_kernel<<<ceil_div(tiles, 8), 256, 0, st>>>(ranges.as<uint2>(), tiles, ids.as<uint32_t>(),
                                                                   stat);
@@ -994,9 +1043,11 @@ void RasterWork::project_and_bin(const float* d_params, cudaStream_t st, cudaEve
     segment_sort_kernel<<<ceil_div(tiles, 256), 256, 0, st>>>(ranges.as<uint2>(), tiles, ids.as<uint32_t>(),
                                                                scratch.as<uint32_t>(), stat);
     launch_check("segment_sort");
-    if (shading_ready) HS_CUDA(cudaStreamWaitEvent(st, shading_ready, 0));  // amplitude/phase uploaded
-    shade_kernel<<<ceil_div(n, 256), 256, 0, st>>>(d_params, n, c, shade.as<float4>(), stat);
-    launch_check("shade");
+    if (shading_ready) {  // amplitude/phase uploaded: shade now (else project_kernel did)
+        HS_CUDA(cudaStreamWaitEvent(st, shading_ready, 0));
+        shade_kernel<<<ceil_div(n, 256), 256, 0, st>>>(d_params, n, c, shade.as<float4>(), stat);
+        launch_check("shade");
+    }
 }
 
 void export_tile_index(const RasterWork& rw, int64_t k, uint32_t* d_tiles, uint32_t* d_ids,

@@ -16,6 +16,7 @@ struct RasterWork {
     DevBuf p64;      // 8 x N doubles, SoA (exact fp64 record for boundary rechecks)
     DevBuf pbox;     // int4 pixel bbox (x0,x1,y0,y1) clamped to the canvas
     DevBuf tbox;     // int4 tile bbox
+    DevBuf trows;    // uint4 per Gaussian: touched tile columns of the first box rows (tight binning)
     DevBuf tcount;   // uint32 Gaussians per tile
     DevBuf toffset;  // uint32 exclusive scan of tcount
     DevBuf raw;      // backward partial sums, (7+2C) x N floats (SoA)
