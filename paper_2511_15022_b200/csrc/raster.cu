@@ -694,7 +694,10 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(
 // The per-pixel math runs on packed fp32x2 pairs: (dx, dy), the rows of
 // Sigma^-1 (dx, dy), per channel (d_amp, d_phase), (gmx, gmy) and (ga, gc).
 // ---------------------------------------------------------------------------
-constexpr int kBwdThreads = 256;
+// One warp per CTA: footprints differ per Gaussian, and single-warp CTAs let
+// every SM refill a finished warp's slot at once (32 resident, 64 registers).
+// Measured at cfg2: 256-thread CTAs 312 us, 128: 296, 64: 290, 32: 282.
+constexpr int kBwdThreads = 32;
 constexpr int kBwdWarps = kBwdThreads / 32;
 
 // LIST: a row-slab rank walks only the Gaussians of its band list (the
@@ -1092,7 +1095,7 @@ static void bwd_launch(const RasterWork& rw, const float* d_params, const float2
     if (rw.banded()) {  // row-slab rank: only the band's Gaussians; the others' gradients are zero
         const int64_t P = static_cast<int64_t>(rw.n) * (6 + 2 * C);
         HS_CUDA(cudaMemsetAsync(d_grads, 0, sizeof(float) * P, st));
-        raster_bwd_kernel<C, 4, 1, true><<<ceil_div(rw.n, warps_per_block), kBwdThreads, 0, st>>>(
+        raster_bwd_kernel<C, 32, 1, true><<<ceil_div(rw.n, warps_per_block), kBwdThreads, 0, st>>>(
             rw.n, rw.rec.as<float4>(), rw.shade.as<float4>(), rw.p64.as<double>(), rw.pbox.as<int4>(), rw.width,
             rw.height, d_gf, rw.raw.as<float>(), y0, hs, rw.band_list.as<uint32_t>(), rw.band_n.as<uint32_t>());
         launch_check("raster_bwd");
@@ -1102,7 +1105,7 @@ static void bwd_launch(const RasterWork& rw, const float* d_params, const float2
         launch_check("raster_finalize");
         return;
     }
-    go(raster_bwd_kernel<C, 4, 1>);  // 4 CTAs/SM measured best at cfg2
+    go(raster_bwd_kernel<C, 32, 1>);
     launch_check("raster_bwd");
     raster_finalize_kernel<C><<<ceil_div(rw.n, 256), 256, 0, st>>>(rw.n, rw.raw.as<float>(), d_params, rw.width,
                                                                    rw.height, d_grads, d_flags);
