@@ -702,13 +702,13 @@ constexpr int kBwdWarps = kBwdThreads / 32;
 
 // LIST: a row-slab rank walks only the Gaussians of its band list (the
 // other raw sums were zeroed before the launch).
-template <int C, int MINB, int NCH, bool LIST = false>
+template <int C, int MINB, bool LIST = false>
 __global__ void __launch_bounds__(kBwdThreads, MINB) raster_bwd_kernel(
     int N, const float4* __restrict__ rec, const float4* __restrict__ shade,
     const double* __restrict__ p64, const int4* __restrict__ pbox, int W, int H,
     const float2* __restrict__ gfield, float* __restrict__ raw, int y0, int hs,
     const uint32_t* __restrict__ list = nullptr, const uint32_t* __restrict__ list_n = nullptr) {
-    __shared__ int2 s_rows[kBwdWarps][32];  // compact nonempty rows: (y, x - flat index)
+    __shared__ int4 s_rows[kBwdWarps][32];  // compact nonempty rows (see the walk)
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     int g = blockIdx.x * kBwdWarps + wid;
     if constexpr (LIST) {
@@ -720,12 +720,10 @@ __global__ void __launch_bounds__(kBwdThreads, MINB) raster_bwd_kernel(
     const float4 r0 = rec[g];
     const float4 r1 = rec[static_cast<size_t>(N) + g];
     const float4 r2 = rec[2 * static_cast<size_t>(N) + g];
-    float2 A[C], B[C], S[C];  // (sh.z, -sh.y), (sh.w, sh.x), (sh.x, sh.y)
+    float2 S[C];  // (amp cos, amp sin) per channel
 #pragma unroll
     for (int c = 0; c < C; ++c) {
         const float4 sh = shade[static_cast<size_t>(c) * N + g];
-        A[c] = make_float2(sh.z, -sh.y);
-        B[c] = make_float2(sh.w, sh.x);
         S[c] = make_float2(sh.x, sh.y);
     }
     const int4 bb = pbox[g];
@@ -737,16 +735,17 @@ __global__ void __launch_bounds__(kBwdThreads, MINB) raster_bwd_kernel(
     const float M = cut + tol;
     const float ratio = i01 * inv_i00;
     // channel planes of the gradient field: rows [y0, y0 + hs) of the canvas
-    // (the whole canvas unless row-slab sharded), indexed by canvas offset
-    // y W + x (32-bit) from one base; channel c is c * cs further on
+    // (the whole canvas unless row-slab sharded), indexed by the band offset
+    // (y - y0) W + x (32-bit) from the kernel parameter; channel c is c * cs further on
     (void)H;
-    const float2* gbase = gfield - static_cast<ptrdiff_t>(y0) * W;
     const unsigned cs = static_cast<unsigned>(hs) * static_cast<unsigned>(W);
-    const unsigned o_idle = static_cast<unsigned>(y0) * static_cast<unsigned>(W);  // a valid pixel for idle lanes
 
-    float2 dap[C];  // (d_amp, d_phase) per channel
+    // Sg[c] = sum of alpha_eff * g_c over the footprint.  (d_amp, d_phase) are
+    // linear in it with per-Gaussian coefficients, so they are formed once after
+    // the walk: d_amp = cos Sg.re + sin Sg.im, d_phase = amp (cos Sg.im - sin Sg.re).
+    float2 Sg[C];
 #pragma unroll
-    for (int c = 0; c < C; ++c) dap[c] = make_float2(0.f, 0.f);
+    for (int c = 0; c < C; ++c) Sg[c] = make_float2(0.f, 0.f);
     float2 gm = make_float2(0.f, 0.f), gac = make_float2(0.f, 0.f);
     float d_alpha = 0.f, gb = 0.f;
 
@@ -781,76 +780,63 @@ __global__ void __launch_bounds__(kBwdThreads, MINB) raster_bwd_kernel(
         const int excl = incl - wdt;
         const unsigned nonempty = __ballot_sync(0xffffffffu, wdt > 0);
         __syncwarp();
-        if (wdt > 0) s_rows[wid][__popc(nonempty & (lanemask_le >> 1))] = make_int2(row, xl - excl);
+        // row table: flat pixel f of this row sits at band offset f + .x and
+        // column f + .y; .z = the row's exact dy = (y - py_hi) - py_lo, .w = y
+        if (wdt > 0)
+            s_rows[wid][__popc(nonempty & (lanemask_le >> 1))] =
+                make_int4((row - y0) * W + xl - excl, xl - excl,
+                          __float_as_int((static_cast<float>(row) - p_hi.y) - p_lo.y), row);
         __syncwarp();
-        // NCH 32-pixel chunks per iteration: their gathers are in flight together.
-        for (int fb = 0; fb < total; fb += 32 * NCH) {
-            int ox[NCH], oy[NCH];
-            bool act[NCH];
+        for (int cb = 0; cb < total; cb += 32) {
+            const unsigned d = static_cast<unsigned>(excl - cb - 1);  // start strictly inside the chunk
+            const unsigned bit = (wdt > 0 && d < 31u) ? 2u << d : 0u;
+            const unsigned starts = __reduce_or_sync(0xffffffffu, bit);
+            const int k0 = static_cast<int>(__reduce_add_sync(0xffffffffu, (wdt > 0 && excl <= cb) ? 1u : 0u)) - 1;
+            const int f = cb + lane;
+            if (f >= total) continue;
+            const int4 info = s_rows[wid][k0 + __popc(starts & lanemask_le)];
+            const int x = f + info.y;
+            const float dxf = (static_cast<float>(x) - p_hi.x) - p_lo.x;
+            const float2 dxy = make_float2(dxf, __int_as_float(info.z));
+            const float2 e = f2fma(f2splat(dxy.x), row0, f2mul(f2splat(dxy.y), row1));  // Sigma^-1 (dx, dy)
+            const float m = fmaf(dxy.x, e.x, dxy.y * e.y);
+            if (m > M) continue;
+            const float2* p = gfield + static_cast<unsigned>(f + info.x);
+            float2 gv[C];
 #pragma unroll
-            for (int u = 0; u < NCH; ++u) {
-                const int cb = fb + 32 * u;
-                const unsigned d = static_cast<unsigned>(excl - cb - 1);  // start strictly inside the chunk
-                const unsigned bit = (wdt > 0 && d < 31u) ? 2u << d : 0u;
-                const unsigned starts = __reduce_or_sync(0xffffffffu, bit);
-                const int k0 = static_cast<int>(__reduce_add_sync(0xffffffffu, (wdt > 0 && excl <= cb) ? 1u : 0u)) - 1;
-                const int f = cb + lane;
-                act[u] = f < total;
-                const int kk = min(k0 + __popc(starts & lanemask_le), 31);
-                const int2 info = s_rows[wid][kk];
-                oy[u] = info.x;
-                ox[u] = f + info.y;
+            for (int c = 0; c < C; ++c) {
+                gv[c] = __ldg(p);
+                p += cs;
             }
-            // inactive lanes load the band's first pixel (always valid) and skip the math
-            float2 gv[NCH][C];
-#pragma unroll
-            for (int u = 0; u < NCH; ++u) {
-                const unsigned o = act[u] ? static_cast<unsigned>(oy[u] * W + ox[u]) : o_idle;
-                const float2* p = gbase + o;
-#pragma unroll
-                for (int c = 0; c < C; ++c) {
-                    gv[u][c] = __ldg(p);
-                    p += cs;
-                }
+            float G = ex2f(m * kNegHalfLog2e), aeff;
+            bool sat;
+            float aG = alpha * G;
+            if (m <= cut - tol && fabsf(aG - 0.99f) > 1e-5f) {
+                sat = aG > 0.99f;
+                aeff = sat ? 0.99f : aG;
+            } else {
+                const float4 e4 = exact_contrib4(q, N, x, info.w);
+                if (e4.w == 0.f) continue;
+                G = e4.x;
+                aG = alpha * G;
+                aeff = e4.y;
+                sat = e4.z != 0.f;
             }
+            // s_amp = sum_c Re(conj(amp e^{i phi}) g_c), as packed pairs
+            float2 sa = f2mul(S[0], gv[0]);
+            Sg[0] = f2fma(f2splat(aeff), gv[0], Sg[0]);
 #pragma unroll
-            for (int u = 0; u < NCH; ++u) {
-                if (!act[u]) continue;
-                const int x = ox[u], y = oy[u];
-                const float2 dxy = f2sub(f2sub(make_float2(static_cast<float>(x), static_cast<float>(y)), p_hi), p_lo);
-                const float2 e = f2fma(f2splat(dxy.x), row0, f2mul(f2splat(dxy.y), row1));  // Sigma^-1 (dx, dy)
-                const float m = fmaf(dxy.x, e.x, dxy.y * e.y);
-                if (m > M) continue;
-                float G = ex2f(m * kNegHalfLog2e), aeff;
-                bool sat;
-                float aG = alpha * G;
-                if (m <= cut - tol && fabsf(aG - 0.99f) > 1e-5f) {
-                    sat = aG > 0.99f;
-                    aeff = sat ? 0.99f : aG;
-                } else {
-                    const float4 e4 = exact_contrib4(q, N, x, y);
-                    if (e4.w == 0.f) continue;
-                    G = e4.x;
-                    aG = alpha * G;
-                    aeff = e4.y;
-                    sat = e4.z != 0.f;
-                }
-                float s_amp = 0.f;
-#pragma unroll
-                for (int c = 0; c < C; ++c) {
-                    const float2 g2 = gv[u][c];
-                    // (common, cross) = (cos g.re + sin g.im, amp cos g.im - amp sin g.re)
-                    const float2 P = f2fma(f2splat(g2.y), B[c], f2mul(f2splat(g2.x), A[c]));
-                    dap[c] = f2fma(f2splat(aeff), P, dap[c]);
-                    s_amp = fmaf(S[c].x, g2.x, fmaf(S[c].y, g2.y, s_amp));
-                }
-                if (!sat) {
-                    d_alpha = fmaf(s_amp, G, d_alpha);
-                    const float qv = s_amp * aG;  // = -2 w of the reference (w = s_amp alpha G / -2)
-                    gm = f2fma(f2splat(qv), e, gm);
-                    gac = f2fma(f2splat(-0.5f * qv), f2mul(dxy, dxy), gac);
-                    gb = fmaf(-qv * dxy.x, dxy.y, gb);
-                }
+            for (int c = 1; c < C; ++c) {
+                Sg[c] = f2fma(f2splat(aeff), gv[c], Sg[c]);
+                sa = f2fma(S[c], gv[c], sa);
+            }
+            const float s_amp = sa.x + sa.y;
+            if (!sat) {
+                d_alpha = fmaf(s_amp, G, d_alpha);
+                const float qv = s_amp * aG;  // = -2 w of the reference (w = s_amp alpha G / -2)
+                gm = f2fma(f2splat(qv), e, gm);
+                gac = f2fma(f2splat(-0.5f * qv), f2mul(dxy, dxy), gac);
+                gb = fmaf(-qv * dxy.x, dxy.y, gb);
             }
         }
     }
@@ -859,8 +845,9 @@ __global__ void __launch_bounds__(kBwdThreads, MINB) raster_bwd_kernel(
     float v[16];
 #pragma unroll
     for (int c = 0; c < C; ++c) {
-        v[c] = dap[c].x;
-        v[C + c] = dap[c].y;
+        const float4 sh = shade[static_cast<size_t>(c) * N + g];  // (amp cos, amp sin, cos, sin)
+        v[c] = fmaf(sh.z, Sg[c].x, sh.w * Sg[c].y);
+        v[C + c] = fmaf(sh.x, Sg[c].y, -sh.y * Sg[c].x);
     }
     v[2 * C + 0] = d_alpha;
     v[2 * C + 1] = gm.x;
@@ -1095,7 +1082,7 @@ static void bwd_launch(const RasterWork& rw, const float* d_params, const float2
     if (rw.banded()) {  // row-slab rank: only the band's Gaussians; the others' gradients are zero
         const int64_t P = static_cast<int64_t>(rw.n) * (6 + 2 * C);
         HS_CUDA(cudaMemsetAsync(d_grads, 0, sizeof(float) * P, st));
-        raster_bwd_kernel<C, 32, 1, true><<<ceil_div(rw.n, warps_per_block), kBwdThreads, 0, st>>>(
+        raster_bwd_kernel<C, 32, true><<<ceil_div(rw.n, warps_per_block), kBwdThreads, 0, st>>>(
             rw.n, rw.rec.as<float4>(), rw.shade.as<float4>(), rw.p64.as<double>(), rw.pbox.as<int4>(), rw.width,
             rw.height, d_gf, rw.raw.as<float>(), y0, hs, rw.band_list.as<uint32_t>(), rw.band_n.as<uint32_t>());
         launch_check("raster_bwd");
@@ -1105,7 +1092,7 @@ static void bwd_launch(const RasterWork& rw, const float* d_params, const float2
         launch_check("raster_finalize");
         return;
     }
-    go(raster_bwd_kernel<C, 32, 1>);
+    go(raster_bwd_kernel<C, 32>);
     launch_check("raster_bwd");
     raster_finalize_kernel<C><<<ceil_div(rw.n, 256), 256, 0, st>>>(rw.n, rw.raw.as<float>(), d_params, rw.width,
                                                                    rw.height, d_grads, d_flags);
