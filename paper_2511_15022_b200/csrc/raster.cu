@@ -699,24 +699,19 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(
 // Measured at cfg2: 256-thread CTAs 312 us, 128: 296, 64: 290, 32: 282.
 constexpr int kBwdThreads = 32;
 constexpr int kBwdWarps = kBwdThreads / 32;
+constexpr int kBwdGrab = 4;  // Gaussians per work-counter atomic
 
 // LIST: a row-slab rank walks only the Gaussians of its band list (the
 // other raw sums were zeroed before the launch).
-template <int C, int MINB, bool LIST = false>
-__global__ void __launch_bounds__(kBwdThreads, MINB) raster_bwd_kernel(
-    int N, const float4* __restrict__ rec, const float4* __restrict__ shade,
-    const double* __restrict__ p64, const int4* __restrict__ pbox, int W, int H,
-    const float2* __restrict__ gfield, float* __restrict__ raw, int y0, int hs,
-    const uint32_t* __restrict__ list = nullptr, const uint32_t* __restrict__ list_n = nullptr) {
+// One Gaussian of the backward walk (one warp).
+template <int C, bool LIST>
+__device__ __forceinline__ void raster_bwd_one(int g, int N, const float4* __restrict__ rec,
+                                               const float4* __restrict__ shade, const double* __restrict__ p64,
+                                               const int4* __restrict__ pbox, int W, int H,
+                                               const float2* __restrict__ gfield, float* __restrict__ raw, int y0,
+                                               int hs) {
     __shared__ int4 s_rows[kBwdWarps][32];  // compact nonempty rows (see the walk)
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    int g = blockIdx.x * kBwdWarps + wid;
-    if constexpr (LIST) {
-        if (g >= static_cast<int>(*list_n)) return;
-        g = static_cast<int>(list[g]);
-    } else {
-        if (g >= N) return;
-    }
     const float4 r0 = rec[g];
     const float4 r1 = rec[static_cast<size_t>(N) + g];
     const float4 r2 = rec[2 * static_cast<size_t>(N) + g];
@@ -872,6 +867,34 @@ __global__ void __launch_bounds__(kBwdThreads, MINB) raster_bwd_kernel(
     if ((lane & 1) == 0 && k < 2 * C + 6) raw[static_cast<size_t>(k) * N + g] = v[0];
 }
 
+template <int C, int MINB, bool LIST = false>
+__global__ void __launch_bounds__(kBwdThreads, MINB) raster_bwd_kernel(
+    int N, const float4* __restrict__ rec, const float4* __restrict__ shade,
+    const double* __restrict__ p64, const int4* __restrict__ pbox, int W, int H,
+    const float2* __restrict__ gfield, float* __restrict__ raw, int y0, int hs,
+    const uint32_t* __restrict__ list, const uint32_t* __restrict__ list_n, uint32_t* __restrict__ work) {
+    // Band list (row-slab rank): persistent warps, each grabbing kBwdGrab list
+    // entries per atomic on the work counter, so a short list launches no
+    // empty CTAs (the list length is only known on the device).
+    const int lane = threadIdx.x & 31;
+    const int limit = LIST ? static_cast<int>(*list_n) : N;
+    if constexpr (!LIST) {  // the whole set: one Gaussian per one-warp CTA (measured faster than persistent)
+        if (static_cast<int>(blockIdx.x) < limit)
+            raster_bwd_one<C, LIST>(blockIdx.x, N, rec, shade, p64, pbox, W, H, gfield, raw, y0, hs);
+        return;
+    }
+    for (;;) {
+        int base = 0;
+        if (lane == 0) base = static_cast<int>(atomicAdd(work, static_cast<uint32_t>(kBwdGrab)));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (base >= limit) return;
+        const int end = min(base + kBwdGrab, limit);
+        for (int i = base; i < end; ++i)
+            raster_bwd_one<C, LIST>(LIST ? static_cast<int>(list[i]) : i, N, rec, shade, p64, pbox, W, H, gfield,
+                                    raw, y0, hs);
+    }
+}
+
 // Chain rule of rasterize_backward (rasterizer.cpp:251-282) in fp64, one
 // thread per Gaussian, from the warp-reduced raw sums [d_amp[C], d_phase[C],
 // d_alpha, gmx, gmy, ga, gb, gc] (SoA, N each).
@@ -980,6 +1003,12 @@ void RasterWork::prepare(int n_, int c_, int w_, int h_) {
     toffset.reserve(static_cast<size_t>(tiles_x) * tiles_y * sizeof(uint32_t));
     ranges.reserve(static_cast<size_t>(tiles_x) * tiles_y * sizeof(uint2));
     status.reserve(4 * sizeof(uint32_t));
+    work.reserve(sizeof(uint32_t));
+    if (sms == 0) {
+        int dev = 0;
+        HS_CUDA(cudaGetDevice(&dev));
+        sms = sm_count(dev);
+    }
     if (cap == 0) reserve_pairs(std::max<int64_t>(int64_t(1) << 20, 16 * static_cast<int64_t>(N)));
 }
 
@@ -1073,18 +1102,16 @@ void raster_forward(const RasterWork& rw, float2* d_field, cudaStream_t st, int 
 template <int C>
 static void bwd_launch(const RasterWork& rw, const float* d_params, const float2* d_gf,
                        float* d_grads, uint32_t* d_flags, int y0, int hs, cudaStream_t st) {
-    const int warps_per_block = kBwdThreads / 32;
-    auto go = [&](auto kern) {
-        kern<<<ceil_div(rw.n, warps_per_block), kBwdThreads, 0, st>>>(
-            rw.n, rw.rec.as<float4>(), rw.shade.as<float4>(), rw.p64.as<double>(), rw.pbox.as<int4>(),
-            rw.width, rw.height, d_gf, rw.raw.as<float>(), y0, hs, nullptr, nullptr);
-    };
-    if (rw.banded()) {  // row-slab rank: only the band's Gaussians; the others' gradients are zero
+    // persistent: 32 one-warp CTAs per SM (the register-limited residency)
+    const int grid = std::max(1, std::min(static_cast<int>(ceil_div(rw.n, kBwdGrab)), 32 * rw.sms));
+    uint32_t* work = rw.work.as<uint32_t>();
+    if (rw.banded()) {
+        HS_CUDA(cudaMemsetAsync(work, 0, sizeof(uint32_t), st));  // row-slab rank: only the band's Gaussians; the others' gradients are zero
         const int64_t P = static_cast<int64_t>(rw.n) * (6 + 2 * C);
         HS_CUDA(cudaMemsetAsync(d_grads, 0, sizeof(float) * P, st));
-        raster_bwd_kernel<C, 32, true><<<ceil_div(rw.n, warps_per_block), kBwdThreads, 0, st>>>(
+        raster_bwd_kernel<C, 32, true><<<grid, kBwdThreads, 0, st>>>(
             rw.n, rw.rec.as<float4>(), rw.shade.as<float4>(), rw.p64.as<double>(), rw.pbox.as<int4>(), rw.width,
-            rw.height, d_gf, rw.raw.as<float>(), y0, hs, rw.band_list.as<uint32_t>(), rw.band_n.as<uint32_t>());
+            rw.height, d_gf, rw.raw.as<float>(), y0, hs, rw.band_list.as<uint32_t>(), rw.band_n.as<uint32_t>(), work);
         launch_check("raster_bwd");
         raster_finalize_kernel<C, true><<<ceil_div(rw.n, 256), 256, 0, st>>>(
             rw.n, rw.raw.as<float>(), d_params, rw.width, rw.height, d_grads, d_flags, rw.band_list.as<uint32_t>(),
@@ -1092,7 +1119,9 @@ static void bwd_launch(const RasterWork& rw, const float* d_params, const float2
         launch_check("raster_finalize");
         return;
     }
-    go(raster_bwd_kernel<C, 32>);
+    raster_bwd_kernel<C, 32><<<rw.n, kBwdThreads, 0, st>>>(
+        rw.n, rw.rec.as<float4>(), rw.shade.as<float4>(), rw.p64.as<double>(), rw.pbox.as<int4>(), rw.width,
+        rw.height, d_gf, rw.raw.as<float>(), y0, hs, nullptr, nullptr, work);
     launch_check("raster_bwd");
     raster_finalize_kernel<C><<<ceil_div(rw.n, 256), 256, 0, st>>>(rw.n, rw.raw.as<float>(), d_params, rw.width,
                                                                    rw.height, d_grads, d_flags);

@@ -24,6 +24,8 @@ struct RasterWork {
     DevBuf scratch;  // 2 x cap uint32: global bitonic fallback for huge tiles
     DevBuf ranges;   // uint2 [begin,end) per tile
     DevBuf status;   // uint32[4]: [0] K (pairs), [1] overflow, [2] non-finite param, [3] unused
+    DevBuf work;     // uint32 work counter of the persistent backward
+    int sms = 0;     // SM count of the device (persistent grids)
     int64_t cap = 0; // pair capacity
     int band_ty0 = 0, band_ty1 = 1 << 30;  // tile rows binned (a row-slab rank: its band)
     // row-slab rank: the Gaussians whose pixel box meets rows [band_y0, band_y1]
