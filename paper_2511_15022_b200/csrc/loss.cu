@@ -24,6 +24,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <type_traits>
+#include <utility>
 
 #include <cub/block/block_reduce.cuh>
 
@@ -639,8 +640,47 @@ __global__ void nonfinite_kernel(const float* g, int64_t n, uint32_t* flag) {
         }
 }
 
-constexpr int kSsimRows = 145;  // output rows per SSIM CTA (1080 = 7.4 x 145: 8 row strips)
-int ssim_rows() { return kSsimRows; }
+// Output rows per SSIM CTA (SR + 20 steps must be whole 11-step ring
+// cycles).  All CTAs walk the same number of steps and are resident 3 per SM,
+// so the kernel takes about waves x (SR + 20) step-times: the row count is
+// chosen per launch to minimise that (1080p x 3: 145 -> 8 row strips, one
+// wave; 1080p x 24 planes: 156; a 155-row slab band x 24: 156, one CTA row
+// instead of two; a small band x 3: 35).
+constexpr int kSsimRowChoices[] = {35, 79, 145, 156, 167};
+constexpr int kSsimMinBlocks = 3;
+
+int ssim_rows(int planes, int H, int W) {
+    static const int sms = [] {
+        int dev = 0;
+        HS_CUDA(cudaGetDevice(&dev));
+        return sm_count(dev);
+    }();
+    const int64_t slots = static_cast<int64_t>(kSsimMinBlocks) * sms;
+    int best = kSsimRowChoices[0];
+    int64_t best_cost = -1;
+    for (int sr : kSsimRowChoices) {
+        const int64_t ctas = static_cast<int64_t>(ceil_div(W, kSO)) * ceil_div(H, sr) * planes;
+        const int64_t cost = (ctas + slots - 1) / slots * (sr + 2 * kHalo);
+        if (best_cost < 0 || cost < best_cost) {
+            best = sr;
+            best_cost = cost;
+        }
+    }
+    return best;
+}
+
+template <bool FROM_FIELD, bool BAND, int... SR>
+auto ssim_kernel_for(int sr, std::integer_sequence<int, SR...>) {
+    using K = void (*)(LossArgs, Win);
+    K k = nullptr;
+    ((sr == SR ? (k = ssim_loss_kernel<FROM_FIELD, kSsimMinBlocks, SR, BAND>, 0) : 0), ...);
+    require(k != nullptr, "ssim: no kernel for the row count");
+    return k;
+}
+template <bool FROM_FIELD, bool BAND>
+auto ssim_kernel(int sr) {
+    return ssim_kernel_for<FROM_FIELD, BAND>(sr, std::integer_sequence<int, 35, 79, 145, 156, 167>{});
+}
 
 unsigned grid_for(int64_t n, int threads) {
     const int64_t b = (n + threads - 1) / threads;
@@ -651,7 +691,7 @@ unsigned grid_for(int64_t n, int threads) {
 
 int loss_partial_slots(int kind, int L, int C, int H, int W) {
     if (kind == kLossTraining || kind == kLossSsim)
-        return ceil_div(W, kSO) * ceil_div(H, ssim_rows()) * L * C;
+        return ceil_div(W, kSO) * ceil_div(H, ssim_rows(L * C, H, W)) * L * C;
     const int64_t total = static_cast<int64_t>(L) * C * H * W;
     return static_cast<int>(grid_for(total, kLossThreads));
 }
@@ -659,21 +699,22 @@ int loss_partial_slots(int kind, int L, int C, int H, int W) {
 int loss_launch(const LossArgs& a, cudaStream_t st) {
     if (a.kind == kLossTraining || a.kind == kLossSsim) {
         require(a.H >= kWin && a.W >= kWin, "ssim: image smaller than the 11x11 window");
-        const dim3 grid(ceil_div(a.W, kSO), ceil_div(a.H, ssim_rows()), a.L * a.C);
+        const int sr = ssim_rows(a.L * a.C, a.H, a.W);
+        const dim3 grid(ceil_div(a.W, kSO), ceil_div(a.H, sr), a.L * a.C);
         static const Win win = ssim_window_f32();
         require(a.tstats != nullptr, "ssim: target statistics missing");
-        auto go = [&](auto kern, size_t smem) {
+        auto go = [&](void (*kern)(LossArgs, Win), size_t smem) {
             HS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
             kern<<<grid, 2 * kSW, smem, st>>>(a, win);
         };
         const bool band = a.own0 > 0 || a.own1 < a.H;
         if (band) {
             require(a.field != nullptr, "ssim: row-band loss needs the complex field");
-            go(ssim_loss_kernel<true, 3, kSsimRows, true>, sizeof(SsimSmem<float2>));
+            go(ssim_kernel<true, true>(sr), sizeof(SsimSmem<float2>));
         } else if (a.field) {
-            go(ssim_loss_kernel<true, 3, kSsimRows>, sizeof(SsimSmem<float2>));
+            go(ssim_kernel<true, false>(sr), sizeof(SsimSmem<float2>));
         } else {
-            go(ssim_loss_kernel<false, 3, kSsimRows>, sizeof(SsimSmem<float>));
+            go(ssim_kernel<false, false>(sr), sizeof(SsimSmem<float>));
         }
         launch_check("ssim_loss");
         return static_cast<int>(grid.x * grid.y * grid.z);
