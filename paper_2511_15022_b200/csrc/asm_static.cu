@@ -394,10 +394,45 @@ __device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned b
                  ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
 
+// Peer table of a row-slab column kernel, staged in shared memory at entry:
+// the output rows of a thread go to different peers, and indexing the
+// SlabCol kernel parameter by a per-thread peer number would serialise on the
+// constant cache.
+struct PeerEnt {
+    float2* base;  // peer receive buffer + this rank's slot
+    int g0, he;    // canvas rows [g0, g0 + he) the peer receives
+};
+__device__ __forceinline__ void load_peers(const SlabCol& sc, PeerEnt* tab) {
+    if (static_cast<int>(threadIdx.x) < sc.R)
+        tab[threadIdx.x] = PeerEnt{sc.peer[threadIdx.x] + sc.slot[threadIdx.x], sc.g0[threadIdx.x], sc.he[threadIdx.x]};
+}
+// Store of one element (float2, or a float4 column pair) of cropped output row
+// y: into every peer whose row range holds y (the slab of y, plus a
+// neighbour's loss band for halo rows), or into the local column-side layout.
+template <class T>
+__device__ __forceinline__ void slab_store(const SlabCol& sc, const PeerEnt* tab, float2* lout, size_t plane_tiles,
+                                           int y, int CC, int off, T v) {
+    if (!sc.put) {
+        *reinterpret_cast<T*>(lout + static_cast<size_t>(y) * CC + off) = v;
+        return;
+    }
+    const int d0 = __float2int_rz(static_cast<float>(y) * sc.inv_hr);
+#pragma unroll
+    for (int dd = -1; dd <= 1; ++dd) {
+        const int d = d0 + dd;
+        if (d < 0 || d >= sc.R) continue;
+        const PeerEnt e = tab[d];
+        const int yl = y - e.g0;
+        if (yl < 0 || yl >= e.he) continue;
+        *reinterpret_cast<T*>(e.base + (plane_tiles * e.he + yl) * CC + off) = v;
+    }
+}
+
 template <int N, int NT, int MINB, bool CONJ, class RAD>
 __global__ void __launch_bounds__(NT, MINB) pcols_slab_kernel(ColArgs a, const float2* __restrict__ tw, SlabCol sc) {
     constexpr int CC = 4, NP = 2;
     extern __shared__ float4 smem4[];
+    __shared__ PeerEnt peers[kMaxPeers];
     float4* work = smem4;
     const int H = a.H, oy = a.oy, ts = a.ntiles;
     float4* stage_buf = smem4 + pfft::padded_len4(N * NP);
@@ -412,6 +447,7 @@ __global__ void __launch_bounds__(NT, MINB) pcols_slab_kernel(ColArgs a, const f
         for (int r = 0; r < sc.R; ++r)  // source r's rows [r hr, (r + 1) hr) of this tile
             bulk_copy(stage_buf + r * sc.hr * NP, sc.in + r * sc.per_src + static_cast<size_t>(t) * sc.hr * CC, seg, bar);
     }
+    load_peers(sc, peers);
     __syncthreads();
     const TfConst tf = a.tf[c];
     PairTf ptf;
@@ -440,21 +476,7 @@ __global__ void __launch_bounds__(NT, MINB) pcols_slab_kernel(ColArgs a, const f
     pfft::run<N, NP, NT, +1, pfft::Full, pfft::Half>(
         work, tw, tid, RAD{}, pfft::InSmem{},
         pfft::out_fn([&](int i, int p, pfft::C2 v) {
-            const float4 q = make_float4(v.re.x, v.im.x, v.re.y, v.im.y);
-            const int y = i - oy;
-            if (!sc.put) {
-                *reinterpret_cast<float4*>(lout + static_cast<size_t>(y) * CC + 2 * p) = q;
-                return;
-            }
-            const int d0 = __float2int_rz(static_cast<float>(y) * sc.inv_hr);
-#pragma unroll
-            for (int dd = -1; dd <= 1; ++dd) {
-                const int d = d0 + dd;
-                if (d < 0 || d >= sc.R) continue;
-                const int yl = y - sc.g0[d];
-                if (yl < 0 || yl >= sc.he[d]) continue;
-                *reinterpret_cast<float4*>(sc.peer[d] + sc.slot[d] + (plane_tiles * sc.he[d] + yl) * CC + 2 * p) = q;
-            }
+            slab_store(sc, peers, lout, plane_tiles, i - oy, CC, 2 * p, make_float4(v.re.x, v.im.x, v.re.y, v.im.y));
         }));
 }
 
@@ -465,6 +487,7 @@ template <int N, int CC, int NT, int MINB, bool CONJ, class RAD>
 __global__ void __launch_bounds__(NT, MINB) scols_slab_kernel(ColArgs a, const float2* __restrict__ tw, SlabCol sc) {
     static_assert(NT % CC == 0, "column of a thread must be fixed");
     extern __shared__ float2 smem[];
+    __shared__ PeerEnt peers[kMaxPeers];
     float2* work = smem;
     const int H = a.H, oy = a.oy, ts = a.ntiles;
     float2* stage_buf = smem + fft::padded_len(N * CC);
@@ -479,6 +502,7 @@ __global__ void __launch_bounds__(NT, MINB) scols_slab_kernel(ColArgs a, const f
         for (int r = 0; r < sc.R; ++r)
             bulk_copy(stage_buf + r * sc.hr * CC, sc.in + r * sc.per_src + static_cast<size_t>(t) * sc.hr * CC, seg, bar);
     }
+    load_peers(sc, peers);
     __syncthreads();
     const TfConst tf = a.tf[c];
     const int mx = wrapped((a.tile0 + tl) * CC + tid % CC, a.Px);
@@ -492,22 +516,108 @@ __global__ void __launch_bounds__(NT, MINB) scols_slab_kernel(ColArgs a, const f
     float2* lout = a.out + static_cast<size_t>(t) * H * CC;
     const size_t plane_tiles = static_cast<size_t>(c) * ts + tl;
     sfft::run<N, CC, NT, +1, sfft::Full, sfft::Half>(
-        work, tw, tid, RAD{}, sfft::in_smem(work), sfft::out_fn([&](int i, int cc, float2 v) {
-            const int y = i - oy;
-            if (!sc.put) {
-                lout[static_cast<size_t>(y) * CC + cc] = v;
-                return;
-            }
-            const int d0 = __float2int_rz(static_cast<float>(y) * sc.inv_hr);
-#pragma unroll
-            for (int dd = -1; dd <= 1; ++dd) {
-                const int d = d0 + dd;
-                if (d < 0 || d >= sc.R) continue;
-                const int yl = y - sc.g0[d];
-                if (yl < 0 || yl >= sc.he[d]) continue;
-                sc.peer[d][sc.slot[d] + (plane_tiles * sc.he[d] + yl) * CC + cc] = v;
-            }
-        }));
+        work, tw, tid, RAD{}, sfft::in_smem(work),
+        sfft::out_fn([&](int i, int cc, float2 v) { slab_store(sc, peers, lout, plane_tiles, i - oy, CC, cc, v); }));
+}
+
+// Multi-plane row-slab column kernels (scalar engine, one CTA per (channel,
+// own tile)): the exchange is fused at both ends as in scols_slab_kernel.
+// Forward: gather the tile's H rows from the R source segments (R TMA bulk
+// copies on one mbarrier), one forward FFT into the spectrum buffer, then per
+// plane l the inverse FFT of H_l x spectrum stores its cropped rows straight
+// into the loss bands of the peers (plane l C + c of the exchange layout).
+template <int N, int CC, int NT, bool CONJ, class RAD>
+__global__ void __launch_bounds__(NT, 1) scols_fwdL_slab_kernel(ColArgs a, const float2* __restrict__ tw, SlabCol sc) {
+    static_assert(NT % CC == 0, "column of a thread must be fixed");
+    extern __shared__ float2 smem[];
+    __shared__ PeerEnt peers[kMaxPeers];
+    float2* A = smem;
+    float2* Sp = smem + fft::padded_len(N * CC);
+    float2* stage_buf = Sp + fft::padded_len(N * CC);
+    const int H = a.H, oy = a.oy, ts = a.ntiles;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(stage_buf + H * CC);
+    const int t = blockIdx.x;  // flat tile over (channel, own tile)
+    const int c = t / ts, tl = t - c * ts;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        const unsigned seg = static_cast<unsigned>(sc.hr * CC * sizeof(float2));
+        bulk_expect(bar, seg * sc.R);
+        for (int r = 0; r < sc.R; ++r)
+            bulk_copy(stage_buf + r * sc.hr * CC, sc.in + r * sc.per_src + static_cast<size_t>(t) * sc.hr * CC, seg, bar);
+    }
+    load_peers(sc, peers);
+    __syncthreads();
+    const int mx = wrapped((a.tile0 + tl) * CC + tid % CC, a.Px);
+    mbar_wait(bar, 0u);
+    const float2* stg = stage_buf - oy * CC;
+    sfft::run<N, CC, NT, -1, sfft::Half, sfft::Full>(
+        Sp, tw, tid, RAD{}, sfft::in_fn([&](int i, int cc) { return stg[i * CC + cc]; }), sfft::out_smem(Sp));
+#pragma unroll 1
+    for (int l = 0; l < a.L; ++l) {
+        const TfConst tf = a.tf[l * a.C + c];
+        const size_t plane_tiles = (static_cast<size_t>(l) * a.C + c) * ts + tl;
+        float2* lout = a.out + plane_tiles * H * CC;
+        sfft::run<N, CC, NT, +1, sfft::Full, sfft::Half>(
+            A, sfft::launder(tw), sfft::launder(tid), RAD{},
+            sfft::in_smem(Sp, [&](int i, int, float2 v) { return cmul(v, transfer_fast<CONJ>(tf, mx, wrapped(i, N))); }),
+            sfft::out_fn([&](int i, int cc, float2 v) { slab_store(sc, peers, lout, plane_tiles, i - oy, CC, cc, v); }));
+    }
+}
+
+// Adjoint: per plane l, the tile's rows of plane l C + c arrive from the R
+// source segments (double-buffered: plane l + 1 is copied while plane l is
+// transformed); each plane's forward FFT accumulates conj(H_l) x spectrum from
+// its last stage; one inverse FFT stores the own-slab rows into the peers.
+template <int N, int CC, int NT, class RAD>
+__global__ void __launch_bounds__(NT, 1) scols_bwdL_slab_kernel(ColArgs a, const float2* __restrict__ tw, SlabCol sc) {
+    static_assert(NT % CC == 0, "column of a thread must be fixed");
+    extern __shared__ float2 smem[];
+    __shared__ PeerEnt peers[kMaxPeers];
+    float2* A = smem;
+    float2* Z = smem + fft::padded_len(N * CC);
+    const int H = a.H, oy = a.oy, ts = a.ntiles;
+    float2* stage0 = Z + fft::padded_len(N * CC);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(stage0 + 2 * H * CC);  // bar[0], bar[1]
+    const int t = blockIdx.x;  // flat tile over (channel, own tile)
+    const int c = t / ts, tl = t - c * ts;
+    const int tid = threadIdx.x;
+    const unsigned seg = static_cast<unsigned>(sc.hr * CC * sizeof(float2));
+    auto fetch = [&](int l) {  // thread 0: plane l's segments -> stage buffer l & 1
+        float2* dst = stage0 + (l & 1) * H * CC;
+        const size_t p = (static_cast<size_t>(l) * a.C + c) * ts + tl;
+        bulk_expect(bar + (l & 1), seg * sc.R);
+        for (int r = 0; r < sc.R; ++r)
+            bulk_copy(dst + r * sc.hr * CC, sc.in + r * sc.per_src + p * sc.hr * CC, seg, bar + (l & 1));
+    };
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        mbar_init(bar + 1, 1);
+        fetch(0);
+    }
+    load_peers(sc, peers);
+    __syncthreads();
+    const int mx = wrapped((a.tile0 + tl) * CC + tid % CC, a.Px);
+#pragma unroll 1
+    for (int l = 0; l < a.L; ++l) {
+        // the other buffer was last read by plane l - 1, whose FFT ended with a barrier
+        if (tid == 0 && l + 1 < a.L) fetch(l + 1);
+        mbar_wait(bar + (l & 1), static_cast<unsigned>((l >> 1) & 1));
+        const TfConst tf = a.tf[l * a.C + c];
+        const float2* stg = sfft::launder(stage0 + (l & 1) * H * CC) - oy * CC;
+        const bool first = l == 0;
+        sfft::run<N, CC, NT, -1, sfft::Half, sfft::Full>(
+            A, sfft::launder(tw), sfft::launder(tid), RAD{}, sfft::in_fn([&](int i, int cc) { return stg[i * CC + cc]; }),
+            sfft::out_smem(Z, [&](int i, int, float2 v, float2& slot) {
+                const float2 w = cmul(v, transfer_fast<true>(tf, mx, wrapped(i, N)));
+                slot = first ? w : cadd(slot, w);
+            }));
+    }
+    const size_t plane_tiles = static_cast<size_t>(c) * ts + tl;
+    float2* lout = a.out + plane_tiles * H * CC;
+    sfft::run<N, CC, NT, +1, sfft::Full, sfft::Half>(
+        Z, tw, tid, RAD{}, sfft::in_smem(Z),
+        sfft::out_fn([&](int i, int cc, float2 v) { slab_store(sc, peers, lout, plane_tiles, i - oy, CC, cc, v); }));
 }
 
 template <int N, int NT, int MINB, class RAD>
@@ -615,6 +725,8 @@ struct ColPlan {
     bool pair = false;  // single-plane kernels use the column-pair SIMD engine (float4 smem)
     void (*fwdS)(ColArgs, const float2*, SlabCol) = nullptr;  // row-slab column kernels
     void (*bwdS)(ColArgs, const float2*, SlabCol) = nullptr;
+    void (*fwdSL)(ColArgs, const float2*, SlabCol) = nullptr;  // multi-plane row-slab column kernels
+    void (*bwdSL)(ColArgs, const float2*, SlabCol) = nullptr;
     void (*fwdP)(ColArgs, const float2*) = nullptr;  // bulk-copy staged single-plane kernels
     void (*bwdP)(ColArgs, const float2*) = nullptr;
 };
@@ -637,6 +749,8 @@ ColPlan pcol_plan() {
     p.bwdP = pcols_bwdP_kernel<N, NT1, MINB1, RAD>;
     p.fwdS = pcols_slab_kernel<N, NT1, MINB1, false, RAD>;
     p.bwdS = pcols_slab_kernel<N, NT1, MINB1, true, RAD>;
+    p.fwdSL = scols_fwdL_slab_kernel<N, 4, NTL, false, RAD>;
+    p.bwdSL = scols_bwdL_slab_kernel<N, 4, NTL, RAD>;
     return p;
 }
 
@@ -649,6 +763,8 @@ ColPlan col_plan() {
               [](int n) { return sfft::twiddle_table(n, RAD{}); }};
     p.fwdS = scols_slab_kernel<N, CC, NT, MINB, false, RAD>;
     p.bwdS = scols_slab_kernel<N, CC, NT, MINB, true, RAD>;
+    p.fwdSL = scols_fwdL_slab_kernel<N, CC, NT, false, RAD>;
+    p.bwdSL = scols_bwdL_slab_kernel<N, CC, NT, RAD>;
     return p;
 }
 
@@ -702,6 +818,13 @@ size_t cols_smem(const Plans& p, int L) {
     return sizeof(float2) * fft::padded_len(p.Py * p.col.cc) * (L > 1 ? 2 : 1);
 }
 int cols_threads(const Plans& p, int L) { return (L == 1 && p.col.nt1) ? p.col.nt1 : p.col.nt; }
+
+// multi-plane slab kernels: work + spectrum buffers, one (forward) or two
+// (adjoint) staging buffers of H rows, mbarriers
+size_t cols_smem_slabL(const Plans& p, int H, bool backward) {
+    return sizeof(float2) * (2 * static_cast<size_t>(fft::padded_len(p.Py * p.col.cc)) +
+                             (backward ? 2 : 1) * static_cast<size_t>(H) * p.col.cc) + 16;
+}
 
 size_t cols_smem_persist(const Plans& p, int H) {
     return cols_smem(p, 1) + sizeof(float2) * static_cast<size_t>(H) * p.col.cc + 16;
@@ -859,7 +982,24 @@ bool asm_rows_inv_get(AsmWork& w, const float2* recv, float2* out, int planes, i
 
 bool asm_cols_slab(AsmWork& w, bool backward, const SlabCol& sc, float2* out, int tile0, int ntiles_local,
                    cudaStream_t st) {
-    if (!w.use_static || w.L != 1) return false;
+    if (!w.use_static) return false;
+    if (w.L > 1) {
+        const Plans* p = find(w.Px, w.Py);
+        if (!p || p->cc != w.CC || !p->col.fwdSL) return false;
+        const size_t sm = cols_smem_slabL(*p, w.H, backward);
+        if (sm > 227 * 1024 || w.H % sc.R != 0 || sc.hr * sc.R != w.H) return false;
+        auto k = backward ? p->col.bwdSL : p->col.fwdSL;
+        static std::mutex mu;
+        {
+            std::lock_guard<std::mutex> lock(mu);
+            HS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+        }
+        ColArgs c{nullptr, out, w.C, w.H, w.Py, w.Px, w.oy, ntiles_local, w.L, w.plan_y, nullptr, w.tf.as<TfConst>()};
+        c.tile0 = tile0;
+        k<<<ntiles_local * w.C, p->col.nt, sm, st>>>(c, w.stw_y, sc);
+        launch_check(backward ? "scols_bwdL_slab" : "scols_fwdL_slab");
+        return true;
+    }
     const Plans* p = find(w.Px, w.Py);
     if (!p || p->cc != w.CC || !p->col.fwdS || cols_smem_persist(*p, w.H) > 227 * 1024) return false;
     if (w.H % sc.R != 0 || sc.hr * sc.R != w.H) return false;

@@ -113,6 +113,28 @@ def test_slab_step_cfg2_grid(holo, R, put):
     assert rel_l2(ps[-1], pf) < 1e-6
 
 
+@pytest.mark.parametrize("R,put", [(2, False), (4, True)])
+def test_slab_step_multiplane_planned_grid(holo, R, put):
+    """Two planes on the compile-time planned 512x320 grid: the multi-plane
+    slab column kernels (segment gather in, one spectrum for every plane,
+    loss-band / slab rows straight to the peers or to the local layout)."""
+    out, pf, ps = run(holo, R, 2000, 3, 256, 160, 2, steps=3, put=put)
+    for lf, ls, gerr in out:
+        assert ls == pytest.approx(lf, rel=2e-6), (lf, ls)
+        assert gerr < GRAD_TOL, gerr
+    assert rel_l2(ps[-1], pf) < 1e-6
+
+
+def test_slab_step_cfg3_eight_ranks(holo):
+    """cfg3 (1080p RGB, 8 depth planes) in 8 row slabs with the peer-put
+    exchange fused into the multi-plane column kernels."""
+    out, pf, ps = run(holo, 8, 200_000, 3, 1920, 1080, 8, steps=1, put=True)
+    lf, ls, gerr = out[0]
+    assert ls == pytest.approx(lf, rel=2e-6), (lf, ls)
+    assert gerr < GRAD_TOL, gerr
+    assert rel_l2(ps[7], pf) < 1e-6
+
+
 def test_slab_step_cfg4_eight_ranks(holo):
     """cfg4 (4K RGB, 1M Gaussians) split into 8 row slabs of 270 rows and 8
     column slabs of 480 two-column tiles of the 7680x4320 spectrum."""
