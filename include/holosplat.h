@@ -206,6 +206,16 @@ hs_status hs_trainer_step(hs_trainer* tr, double* loss_out);
  * queued on the trainer stream with a single synchronisation.  Use pinned host
  * memory for full copy bandwidth. */
 hs_status hs_trainer_step_host(hs_trainer* tr, const float* h_params_in, float* h_params_out, double* loss_out);
+/* `steps` steps with host-resident parameters: h_params (pinned, the flat
+ * [pos | scale | rot | amp | phase | opa] fp32 layout) is uploaded before and
+ * overwritten with the updated parameters after EVERY step, as `steps` calls
+ * of hs_trainer_step_host(tr, h, h, ...) would do; the copies are pipelined
+ * across steps (step k's amplitude/phase download overlaps step k+1's geometry
+ * upload and projection).  losses_out (nullable) receives each step's loss.
+ * A non-finite gradient / rasterizer error at step j raises as
+ * hs_trainer_step_host would at step j; later steps of the call leave the
+ * parameters untouched (the reference's loop stops at the throw). */
+hs_status hs_trainer_run_host(hs_trainer* tr, float* h_params, int steps, double* losses_out);
 /* Split form for multi-GPU: forward+backward into the gradient buffer, then
  * (after the caller all-reduced hs_trainer_grads_ptr) the optimizer update. */
 hs_status hs_trainer_forward_backward(hs_trainer* tr);

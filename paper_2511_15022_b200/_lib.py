@@ -69,6 +69,7 @@ class hs_poh_config(C.Structure):
 
 _SIGS = {
     "hs_trainer_step_host": [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_double)],
+    "hs_trainer_run_host": [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_double)],
     "hs_compute_metrics": [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
                            C.POINTER(C.c_double), C.POINTER(C.c_double)],
     "hs_dpac_encode": [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p],

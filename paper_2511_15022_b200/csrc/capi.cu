@@ -778,6 +778,140 @@ hs_status hs_trainer_step_host(hs_trainer* t, const float* h_params_in, float* h
     });
 }
 
+// ---- pipelined multi-step run with host-resident parameters ----
+// Per-step gate between the raster backward and Adan: logs the step's
+// non-finite group bits and rasterizer status (overflow, non-finite input) and
+// its loss; after a failed step every later step of the run applies no update
+// (flags = group 0: Adan skips all groups and keeps its step counter), so the
+// parameters stay as the reference leaves them when Adan::step throws.
+}  // extern "C"
+namespace hs {
+namespace {
+__global__ void run_gate_kernel(uint32_t* flags, const uint32_t* stat, const double* o3, uint32_t* words,
+                                uint32_t* flog, double* llog) {
+    const uint32_t f = *flags;
+    const uint32_t s = (stat[1] ? 0x100u : 0u) | (stat[2] ? 0x200u : 0u);
+    const uint32_t k = words[1]++;
+    flog[k] = f | s;
+    llog[k] = o3[0];
+    if (words[0]) *flags = 1u;
+    else if (f | s) words[0] = 1u;
+}
+constexpr int kRunBatch = 1024;  // steps per device log (one host check per batch)
+}  // namespace
+}  // namespace hs
+extern "C" {
+
+// One step of the run.  Steady state (tail = true) overlaps the previous
+// step's amplitude/phase download (copy stream 2) with this step's geometry
+// upload and projection; the graph ends with the download of the geometry
+// groups, so the next step's upload reads the values this step wrote.
+static void enqueue_run_step(hs_trainer* t, cudaStream_t st, float* h, bool tail) {
+    const size_t N = t->n, geo0 = 5 * N, ap = 2 * N * t->c;  // [pos 2N | scale 2N | rot N | amp | phase | opa N]
+    float* d = t->params.as<float>();
+    if (tail) {  // D2H of step k-1's amplitude/phase groups, alongside this step's start
+        HS_CUDA(cudaEventRecord(t->ev_fork, st));
+        HS_CUDA(cudaStreamWaitEvent(t->copy_st2, t->ev_fork, 0));
+        HS_CUDA(cudaMemcpyAsync(h + geo0, d + geo0, sizeof(float) * ap, cudaMemcpyDeviceToHost, t->copy_st2));
+        HS_CUDA(cudaEventRecord(t->ev_apdown, t->copy_st2));
+    }
+    HS_CUDA(cudaMemcpyAsync(d, h, sizeof(float) * geo0, cudaMemcpyHostToDevice, st));
+    HS_CUDA(cudaMemcpyAsync(d + geo0 + ap, h + geo0 + ap, sizeof(float) * N, cudaMemcpyHostToDevice, st));
+    HS_CUDA(cudaEventRecord(t->ev_fork, st));
+    HS_CUDA(cudaStreamWaitEvent(t->copy_st, t->ev_fork, 0));
+    if (tail) HS_CUDA(cudaStreamWaitEvent(t->copy_st, t->ev_apdown, 0));
+    HS_CUDA(cudaMemcpyAsync(d + geo0, h + geo0, sizeof(float) * ap, cudaMemcpyHostToDevice, t->copy_st));
+    HS_CUDA(cudaEventRecord(t->ev_ap, t->copy_st));
+    trainer_enqueue_fwd_bwd(t, st, t->ev_ap);
+    run_gate_kernel<<<1, 1, 0, st>>>(t->flags.as<uint32_t>(), t->rw.status.as<uint32_t>(), t->out3.as<double>(),
+                                     t->run_words.as<uint32_t>(), t->run_flog.as<uint32_t>(),
+                                     t->run_llog.as<double>());
+    launch_check("run_gate");
+    trainer_enqueue_update(t, st);
+    HS_CUDA(cudaMemcpyAsync(h, d, sizeof(float) * geo0, cudaMemcpyDeviceToHost, st));
+    HS_CUDA(cudaMemcpyAsync(h + geo0 + ap, d + geo0 + ap, sizeof(float) * N, cudaMemcpyDeviceToHost, st));
+}
+
+hs_status hs_trainer_run_host(hs_trainer* t, float* h_params, int steps, double* losses_out) {
+    return guard([&] {
+        require(steps >= 0 && h_params != nullptr, "run_host: bad arguments");
+        require(t->R == 0, "run_host: not for row-slab shards (use the slab stages)");
+        if (steps == 0) return;
+        // cosine_lr(step, steps, ...) throws past the horizon (optimizer.cpp:9-10)
+        require(t->host_step + steps - 1 <= t->total_steps, "cosine_lr: step outside [0, total_steps]");
+        cudaStream_t st = t->ctx->stream;
+        if (!t->copy_st) {
+            HS_CUDA(cudaStreamCreateWithFlags(&t->copy_st, cudaStreamNonBlocking));
+            HS_CUDA(cudaEventCreateWithFlags(&t->ev_fork, cudaEventDisableTiming));
+            HS_CUDA(cudaEventCreateWithFlags(&t->ev_ap, cudaEventDisableTiming));
+            HS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&t->h_words), 5 * sizeof(uint32_t), cudaHostAllocDefault));
+            HS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&t->h_o3), 3 * sizeof(double), cudaHostAllocDefault));
+        }
+        if (!t->copy_st2) {
+            HS_CUDA(cudaStreamCreateWithFlags(&t->copy_st2, cudaStreamNonBlocking));
+            HS_CUDA(cudaEventCreateWithFlags(&t->ev_apdown, cudaEventDisableTiming));
+            t->run_words.reserve(2 * sizeof(uint32_t));
+            t->run_flog.reserve(kRunBatch * sizeof(uint32_t));
+            t->run_llog.reserve(kRunBatch * sizeof(double));
+        }
+        if (t->run_host != h_params) {
+            for (cudaGraphExec_t* g : {&t->run_graph0, &t->run_graph})
+                if (*g) {
+                    HS_CUDA(cudaGraphExecDestroy(*g));
+                    *g = nullptr;
+                }
+            t->run_host = h_params;
+        }
+        auto capture = [&](bool tail) {
+            cudaGraph_t g = nullptr;
+            cudaGraphExec_t ge = nullptr;
+            HS_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            try {
+                enqueue_run_step(t, st, h_params, tail);
+            } catch (...) {
+                cudaStreamEndCapture(st, &g);
+                if (g) cudaGraphDestroy(g);
+                throw;
+            }
+            HS_CUDA(cudaStreamEndCapture(st, &g));
+            HS_CUDA(cudaGraphInstantiate(&ge, g, 0));
+            HS_CUDA(cudaGraphDestroy(g));
+            return ge;
+        };
+        std::vector<uint32_t> flog(kRunBatch);
+        std::vector<double> llog(kRunBatch);
+        const size_t N = t->n, geo0 = 5 * N, ap = 2 * N * t->c;
+        for (int b0 = 0; b0 < steps; b0 += kRunBatch) {
+            const int nb = std::min(kRunBatch, steps - b0);
+            HS_CUDA(cudaMemsetAsync(t->run_words.p, 0, 2 * sizeof(uint32_t), st));
+            for (int i = 0; i < nb; ++i) {
+                if (t->use_graph && st != nullptr) {  // (no capture on the legacy stream)
+                    cudaGraphExec_t& ge = i == 0 ? t->run_graph0 : t->run_graph;
+                    if (!ge) ge = capture(i != 0);
+                    HS_CUDA(cudaGraphLaunch(ge, st));
+                    note_launch(0);
+                } else {
+                    enqueue_run_step(t, st, h_params, i != 0);
+                }
+            }
+            // the last step's amplitude/phase download, the logs, one synchronisation
+            float* d = t->params.as<float>();
+            HS_CUDA(cudaMemcpyAsync(h_params + geo0, d + geo0, sizeof(float) * ap, cudaMemcpyDeviceToHost, st));
+            HS_CUDA(cudaMemcpyAsync(flog.data(), t->run_flog.p, nb * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+            HS_CUDA(cudaMemcpyAsync(llog.data(), t->run_llog.p, nb * sizeof(double), cudaMemcpyDeviceToHost, st));
+            HS_CUDA(cudaStreamSynchronize(st));
+            for (int i = 0; i < nb; ++i) {
+                t->host_step += 1;
+                if (losses_out) losses_out[b0 + i] = llog[i];
+                if (flog[i]) {
+                    const uint32_t stat[4] = {0u, (flog[i] & 0x100u) ? 1u : 0u, (flog[i] & 0x200u) ? 1u : 0u, 0u};
+                    trainer_raise(t, flog[i] & 0xffu, stat);
+                }
+            }
+        }
+    });
+}
+
 hs_status hs_trainer_last_loss(hs_trainer* t, double* loss_out, int64_t* npairs_out) {
     return guard([&] {
         trainer_check_after(t);

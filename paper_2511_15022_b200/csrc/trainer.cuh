@@ -65,6 +65,15 @@ struct hs_trainer {
     cudaGraphExec_t host_graph = nullptr;
     const float* host_in = nullptr;
     float* host_out = nullptr;
+    // pipelined multi-step host run (hs_trainer_run_host): a second copy
+    // stream for the deferred amplitude/phase download, the first-step and
+    // steady-state graphs keyed by the host buffer, and the per-run device
+    // words {halt, step index} + per-step flag / loss logs
+    cudaStream_t copy_st2 = nullptr;
+    cudaEvent_t ev_apdown = nullptr;
+    cudaGraphExec_t run_graph0 = nullptr, run_graph = nullptr;
+    float* run_host = nullptr;
+    DevBuf run_words, run_flog, run_llog;
     // row-slab sharding (hs_trainer_set_row_slab): rank `rank` of R owns canvas
     // rows [h0, h0 + hr) and column tiles [rank ts, rank ts + ts); its loss band
     // is rows [g0, g0 + He) (own rows + up to 10 halo rows each side)
@@ -86,6 +95,10 @@ struct hs_trainer {
     ~hs_trainer() {
         if (graph) cudaGraphExecDestroy(graph);
         if (host_graph) cudaGraphExecDestroy(host_graph);
+        if (run_graph0) cudaGraphExecDestroy(run_graph0);
+        if (run_graph) cudaGraphExecDestroy(run_graph);
+        if (ev_apdown) cudaEventDestroy(ev_apdown);
+        if (copy_st2) cudaStreamDestroy(copy_st2);
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
         if (ev_fork) cudaEventDestroy(ev_fork);

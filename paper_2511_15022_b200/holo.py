@@ -853,6 +853,27 @@ class Trainer:
         check(_lib.load().hs_trainer_step_host(self.h, addr(params_in), addr(params_out), C.byref(v)))
         return v.value
 
+    def run_host(self, params, steps: int):
+        """`steps` steps with host-resident parameters (hs_trainer_run_host):
+        `params` (pinned fp32 torch tensor or numpy array of param_count floats)
+        is uploaded before and overwritten with the updated parameters after
+        every step, the copies pipelined across steps.  Returns the per-step
+        losses (numpy float64)."""
+        self._ctx = ctx_handle()
+        if isinstance(params, torch.Tensor):
+            if params.is_cuda or params.dtype != torch.float32 or not params.is_contiguous() \
+                    or params.numel() != self.param_count:
+                raise HoloInvalidArgument("run_host: need a contiguous fp32 host tensor of param_count floats")
+            ptr = C.c_void_p(params.data_ptr())
+        else:
+            if params.dtype != np.float32 or not params.flags.c_contiguous or params.size != self.param_count:
+                raise HoloInvalidArgument("run_host: need a contiguous fp32 array of param_count floats")
+            ptr = params.ctypes.data_as(C.c_void_p)
+        losses = np.zeros(max(int(steps), 0), np.float64)
+        check(_lib.load().hs_trainer_run_host(self.h, ptr, int(steps),
+                                              losses.ctypes.data_as(C.POINTER(C.c_double))))
+        return losses
+
     def step(self, sync_loss=True):
         self._ctx = ctx_handle()
         if sync_loss:

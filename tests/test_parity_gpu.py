@@ -417,6 +417,53 @@ def test_trainer_step_host_matches_device_step(holo):
     assert np.array_equal(host.numpy(), pa)
 
 
+@pytest.mark.parametrize("graphs", [False, True])
+def test_trainer_run_host_matches_device_steps(holo, graphs):
+    """hs_trainer_run_host (host-resident parameters uploaded and downloaded
+    every step, copies pipelined across steps) == the same number of device
+    steps, bit for bit, losses included."""
+    import torch
+    c, w, h, n, L = 3, 64, 48, 400, 1
+    g = f32(S.init_gaussians(n, c, w, h, 6))
+    img = S.synthetic_image(42, c, h, w)
+    masks = S.build_masks(S.synthetic_depth(43, h, w), L, True)
+    dist = S.make_depth_planes(L, 3e-3, 2e-3)
+    mk = lambda: holo.Trainer(holo.GaussianSet(n, c, **g), w, h, holo.RealField(c, h, w, img), masks, dist,
+                              holo.PropagationSpec(), 20)
+    a, b = mk(), mk()
+    b.use_graph(graphs)
+    host = torch.from_numpy(b.params().copy()).pin_memory()
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        la = [a.step(sync_loss=True) for _ in range(7)]
+        lb = list(b.run_host(host, 3)) + list(b.run_host(host, 4))
+    assert lb == la
+    assert np.array_equal(host.numpy(), a.params())
+
+
+def test_trainer_run_host_nonfinite_stops_updates(holo):
+    """A non-finite gradient in the first step of a run raises naming the
+    group (as step_host would), and no later step of the run moves the
+    parameters: the host copy equals the initial parameters."""
+    import torch
+    c, w, h, n, L = 3, 64, 48, 300, 1
+    g = f32(S.init_gaussians(n, c, w, h, 3))
+    img = S.synthetic_image(42, c, h, w).copy()
+    img[1, 10, 10] = np.nan
+    masks = S.build_masks(S.synthetic_depth(43, h, w), L, True)
+    tr = holo.Trainer(holo.GaussianSet(n, c, **g), w, h, holo.RealField(c, h, w, img), masks,
+                      S.make_depth_planes(L, 3e-3, 2e-3), holo.PropagationSpec(), 10)
+    tr.use_graph(True)
+    p0 = tr.params()
+    host = torch.from_numpy(p0.copy()).pin_memory()
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        with pytest.raises(holo.HoloNonFinite, match="group position"):
+            tr.run_host(host, 5)
+    assert np.array_equal(host.numpy(), p0)
+    assert np.array_equal(tr.params(), p0)
+
+
 def test_reserve_pairs_recaptures_the_step_graphs(holo):
     """Growing the tile-pair capacity reallocates the id buffers: the captured
     step graphs (device step and host-resident step) must be re-captured, so
