@@ -895,15 +895,201 @@ __global__ void __launch_bounds__(kBwdThreads, MINB) raster_bwd_kernel(
     }
 }
 
+// ---------------------------------------------------------------------------
+// K3t: backward, per tile (the north_star form).  One CTA per 16x16 tile, four
+// warps, each an 8x8 cell of the tile, as the forward.  A warp stages its
+// cell's 64 gradient pixels (C channels) in shared memory and walks the tile's
+// sorted Gaussian list 32 candidates at a time: each lane tests one candidate
+// against the cell (the forward's row-band bound), the hits are compacted into
+// a per-warp queue, and every 32 queued hits run as one batch with LANE =
+// GAUSSIAN: the warp loops over the cell's 64 pixels (position and gradient are
+// warp-uniform -- shared-memory broadcasts, no gathers), every lane evaluating
+// its own Gaussian at that pixel with the same fast/exact decision as K3, and
+// accumulates its Gaussian's 7 + 2C partial sums in registers.  The sums over
+// the cell go to the Gaussian's row of an AoS [N][16] buffer with four 16-byte
+// vector atomics (red.global.add.v4.f32): one reduction in registers over the
+// cell's pixels before one atomic per (cell, Gaussian, 4 values).  Not
+// deterministic in the last bits (atomic order); K3 is the deterministic path.
+// ---------------------------------------------------------------------------
+constexpr int kTbQ = 64;  // per-warp hit queue (two batches)
+
+__device__ __forceinline__ void red_add_v4(float* dst, float a, float b, float c, float d) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(a), "f"(b), "f"(c), "f"(d)
+                 : "memory");
+}
+
+template <int C>
+__global__ void __launch_bounds__(kFwdThreads, 6) raster_bwd_tile_kernel(
+    const uint32_t* __restrict__ ids, const uint2* __restrict__ ranges, const float4* __restrict__ rec,
+    const float4* __restrict__ shade, const double* __restrict__ p64, int N, int tiles_x, int W, int H,
+    const float2* __restrict__ gfield, float* __restrict__ raw16, int y0, int hs, int ty0) {
+    static_assert(2 * C + 6 <= 16, "AoS row of 16 floats");
+    __shared__ float2 s_g[kFwdThreads / 32][C][64];  // cell gradient, pixel p = (p >> 3, p & 7)
+    __shared__ uint32_t s_q[kFwdThreads / 32][kTbQ];
+    const int tile = blockIdx.x + ty0 * tiles_x;
+    const int tx = tile % tiles_x, ty = tile / tiles_x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int cx0 = tx * kTile + (warp & 1) * 8;
+    const int cy0 = ty * kTile + (warp >> 1) * 8;
+    // the cell's rows inside the band [y0, y0 + hs) and the canvas; columns inside the canvas
+    const int ry0 = max(cy0, y0), ry1 = min(min(cy0 + 8, y0 + hs), H);  // [ry0, ry1)
+    const int cx1 = min(cx0 + 8, W);
+    if (ry0 >= ry1 || cx0 >= cx1) return;  // warp-uniform (whole cell outside)
+    (void)N;
+    const unsigned cs = static_cast<unsigned>(hs) * static_cast<unsigned>(W);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {  // lane stages pixels lane and lane + 32
+        const int pix = lane + 32 * k;
+        const int x = cx0 + (pix & 7), y = cy0 + (pix >> 3);
+        const bool ok = x < cx1 && y >= ry0 && y < ry1;
+        const float2* src = gfield + (ok ? static_cast<unsigned>(y - y0) * static_cast<unsigned>(W) + x : 0u);
+#pragma unroll
+        for (int c = 0; c < C; ++c) s_g[warp][c][pix] = ok ? __ldg(src + static_cast<size_t>(c) * cs) : make_float2(0.f, 0.f);
+    }
+    __syncwarp();
+    const uint2 rg = ranges[tile];
+    int qn = 0;  // queued hits (warp-uniform)
+    const unsigned lanemask_lt = (1u << lane) - 1u;
+    auto batch = [&](int nb) {  // process s_q[0, nb)
+        const bool act = lane < nb;
+        const uint32_t g = act ? s_q[warp][lane] : s_q[warp][0];
+        const float4 r0 = rec[g];
+        const float4 r1 = rec[static_cast<size_t>(N) + g];
+        const float4 r2 = rec[2 * static_cast<size_t>(N) + g];
+        float2 S[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            const float4 sh = shade[static_cast<size_t>(c) * N + g];
+            S[c] = make_float2(sh.x, sh.y);
+        }
+        const float i00 = r1.x, i01 = r1.y, i11 = r1.z;
+        const float cut = r1.w, tol = r2.y, l2a = r2.x, alpha = exp2f(r2.x);
+        const float M = act ? cut + tol : -1.f;  // idle lanes never pass m <= M
+        const float Mfast = cut - tol;
+        const double* q = p64 + g;
+        // per-lane sums over the cell: Sg_c = sum a_eff g_c; over the unsaturated
+        // pixels with qv = s_amp alpha G: QA = sum qv, T1 = sum qv (dx, dy),
+        // T2 = sum qv (dx^2, dy^2), T3 = sum qv dx dy  (gm = Sigma^-1 T1,
+        // (ga, gc) = -T2 / 2, gb = -T3, d_alpha = QA / alpha)
+        float2 Sg[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) Sg[c] = make_float2(0.f, 0.f);
+        float2 T1 = make_float2(0.f, 0.f), T2 = make_float2(0.f, 0.f);
+        float QA = 0.f, T3 = 0.f;
+        // accumulate one pixel with weight w = a_eff (0 outside) and qv
+        auto accum = [&](const float2* gp, float dx, float dy, float w, float qv0) {
+            float2 gv[C];
+#pragma unroll
+            for (int c = 0; c < C; ++c) gv[c] = gp[c * 64];
+            float2 sa = f2mul(S[0], gv[0]);
+            Sg[0] = f2fma(f2splat(w), gv[0], Sg[0]);
+#pragma unroll
+            for (int c = 1; c < C; ++c) {
+                Sg[c] = f2fma(f2splat(w), gv[c], Sg[c]);
+                sa = f2fma(S[c], gv[c], sa);
+            }
+            const float qv = (sa.x + sa.y) * qv0;
+            QA += qv;
+            const float2 dxy = make_float2(dx, dy);
+            const float2 t = f2mul(f2splat(qv), dxy);
+            T1 = f2add(T1, t);
+            T2 = f2fma(t, dxy, T2);
+            T3 = fmaf(t.x, dy, T3);
+        };
+        // fast fp32 pass over the cell; pixels inside a Gaussian's error band
+        // (or at the saturation threshold) are only flagged in a 64-bit mask
+        uint32_t band_lo = 0u, band_hi = 0u;
+        for (int y = ry0; y < ry1; ++y) {
+            const float dy = (static_cast<float>(y) - r0.y) - r0.w;
+            const float bq = 2.f * i01 * dy, cq = i11 * dy * dy;  // m = (i00 dx + bq) dx + cq
+            const float2* gp = &s_g[warp][0][(y - cy0) << 3];
+            uint32_t rowband = 0u;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const float dx = (static_cast<float>(cx0 + k) - r0.x) - r0.z;
+                const float m = fmaf(fmaf(i00, dx, bq), dx, cq);
+                const float aG = ex2f(fmaf(m, kNegHalfLog2e, l2a));  // alpha e^{-m/2}
+                const bool in = m <= M;
+                const bool fast = m <= Mfast && fabsf(aG - 0.99f) > 1e-5f;
+                rowband |= (in && !fast) ? (1u << k) : 0u;
+                const bool use = in && fast;
+                accum(gp + k, dx, dy, use ? fminf(aG, 0.99f) : 0.f, (use && aG <= 0.99f) ? aG : 0.f);
+            }
+            const int sh = (y - cy0) << 3;
+            if (sh < 32) band_lo |= rowband << sh;
+            else band_hi |= rowband << (sh - 32);
+        }
+        // rare: the exact fp64 decision for the flagged pixels (rasterizer.cpp:220-228)
+        if (__any_sync(0xffffffffu, (band_lo | band_hi) != 0u)) {
+            const int xmax = cx1 - cx0;
+            for (uint64_t bm = (static_cast<uint64_t>(band_hi) << 32) | band_lo; bm; bm &= bm - 1) {
+                const int pix = __ffsll(static_cast<long long>(bm)) - 1;
+                const int k = pix & 7, y = cy0 + (pix >> 3), x = cx0 + k;
+                if (k >= xmax) continue;  // outside the canvas
+                const float4 e4 = exact_contrib4(q, N, x, y);
+                if (e4.w == 0.f) continue;
+                const float dx = (static_cast<float>(x) - r0.x) - r0.z;
+                const float dy = (static_cast<float>(y) - r0.y) - r0.w;
+                accum(&s_g[warp][0][pix], dx, dy, e4.y, e4.z != 0.f ? 0.f : alpha * e4.x);
+            }
+        }
+        if (act) {
+            float v[16];
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                v[c] = Sg[c].x;
+                v[C + c] = Sg[c].y;
+            }
+            v[2 * C + 0] = alpha > 0.f ? QA / alpha : 0.f;
+            v[2 * C + 1] = fmaf(i00, T1.x, i01 * T1.y);
+            v[2 * C + 2] = fmaf(i01, T1.x, i11 * T1.y);
+            v[2 * C + 3] = -0.5f * T2.x;
+            v[2 * C + 4] = -T3;
+            v[2 * C + 5] = -0.5f * T2.y;
+#pragma unroll
+            for (int i = 2 * C + 6; i < 16; ++i) v[i] = 0.f;
+            float* dst = raw16 + static_cast<size_t>(g) * 16;
+#pragma unroll
+            for (int k = 0; k < (2 * C + 6 + 3) / 4; ++k) red_add_v4(dst + 4 * k, v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+        }
+    };
+    const float fcx = static_cast<float>(cx0), fcy = static_cast<float>(cy0);
+    for (uint32_t base = rg.x; base < rg.y; base += 32) {
+        const uint32_t i = base + lane;
+        bool hit = false;
+        uint32_t g = 0;
+        if (i < rg.y) {
+            g = ids[i];
+            hit = cell_hit(rec[g], rec[static_cast<size_t>(N) + g], rec[2 * static_cast<size_t>(N) + g], fcx, fcy, 7.f,
+                           7.f);
+        }
+        const unsigned mask = __ballot_sync(0xffffffffu, hit);
+        if (hit) s_q[warp][qn + __popc(mask & lanemask_lt)] = g;
+        qn += __popc(mask);
+        __syncwarp();
+        if (qn >= 32) {
+            batch(32);
+            __syncwarp();
+            qn -= 32;
+            if (lane < qn) s_q[warp][lane] = s_q[warp][32 + lane];
+            __syncwarp();
+        }
+    }
+    if (qn > 0) batch(qn);
+}
+
 // Chain rule of rasterize_backward (rasterizer.cpp:251-282) in fp64, one
 // thread per Gaussian, from the warp-reduced raw sums [d_amp[C], d_phase[C],
 // d_alpha, gmx, gmy, ga, gb, gc] (SoA, N each).
-template <int C, bool LIST = false>
+// AOS: the per-tile backward's [N][16] rows (sum alpha_eff g_c re/im instead of
+// (d_amp, d_phase), converted here with the Gaussian's shading record).
+template <int C, bool LIST = false, bool AOS = false>
 __global__ void __launch_bounds__(256) raster_finalize_kernel(int N, const float* __restrict__ raw,
                                                                const float* __restrict__ params, int W, int H,
                                                                float* __restrict__ grads, uint32_t* flags,
                                                                const uint32_t* __restrict__ list = nullptr,
-                                                               const uint32_t* __restrict__ list_n = nullptr) {
+                                                               const uint32_t* __restrict__ list_n = nullptr,
+                                                               const float4* __restrict__ shade = nullptr) {
     int g = blockIdx.x * blockDim.x + threadIdx.x;
     if constexpr (LIST) {  // row-slab rank: its band's Gaussians (the other gradients were zeroed)
         if (g >= static_cast<int>(*list_n)) return;
@@ -912,7 +1098,21 @@ __global__ void __launch_bounds__(256) raster_finalize_kernel(int N, const float
         if (g >= N) return;
     }
     const size_t Ns = N;
-    auto R = [&](int k) { return static_cast<double>(raw[static_cast<size_t>(k) * Ns + g]); };
+    auto R = [&](int k) {
+        return static_cast<double>(AOS ? raw[static_cast<size_t>(g) * 16 + k] : raw[static_cast<size_t>(k) * Ns + g]);
+    };
+    // (d_amp, d_phase) of channel c: stored (K3), or from sum alpha_eff g_c (K3t):
+    // d_amp = cos Sg.re + sin Sg.im, d_phase = amp (cos Sg.im - sin Sg.re)
+    auto DA = [&](int c) {
+        if constexpr (!AOS) return R(c);
+        const float4 sh = shade[static_cast<size_t>(c) * Ns + g];
+        return static_cast<double>(sh.z) * R(c) + static_cast<double>(sh.w) * R(C + c);
+    };
+    auto DP = [&](int c) {
+        if constexpr (!AOS) return R(C + c);
+        const float4 sh = shade[static_cast<size_t>(c) * Ns + g];
+        return static_cast<double>(sh.x) * R(C + c) - static_cast<double>(sh.y) * R(c);
+    };
     const double d_alpha = R(2 * C), gmx = R(2 * C + 1), gmy = R(2 * C + 2);
     const double ga = R(2 * C + 3), gb = R(2 * C + 4), gc = R(2 * C + 5);
     const float* pp = params;
@@ -938,8 +1138,8 @@ __global__ void __launch_bounds__(256) raster_finalize_kernel(int N, const float
     for (int c = 0; c < C; ++c) {
         const size_t i = static_cast<size_t>(g) * C + c;
         const float rawp = amp[i];
-        put(gamp + i, (rawp >= 0.f && rawp <= 1.f) ? R(c) : 0.0, 3);
-        put(gpha + i, R(C + c), 4);
+        put(gamp + i, (rawp >= 0.f && rawp <= 1.f) ? DA(c) : 0.0, 3);
+        put(gpha + i, DP(c), 4);
     }
     const double po = opa[g];
     const double sig = 1.0 / (1.0 + exp(-po));
@@ -1004,6 +1204,7 @@ void RasterWork::prepare(int n_, int c_, int w_, int h_) {
     ranges.reserve(static_cast<size_t>(tiles_x) * tiles_y * sizeof(uint2));
     status.reserve(4 * sizeof(uint32_t));
     work.reserve(sizeof(uint32_t));
+    raw16.reserve(N * 16 * sizeof(float));
     if (sms == 0) {
         int dev = 0;
         HS_CUDA(cudaGetDevice(&dev));
@@ -1116,6 +1317,19 @@ static void bwd_launch(const RasterWork& rw, const float* d_params, const float2
         raster_finalize_kernel<C, true><<<ceil_div(rw.n, 256), 256, 0, st>>>(
             rw.n, rw.raw.as<float>(), d_params, rw.width, rw.height, d_grads, d_flags, rw.band_list.as<uint32_t>(),
             rw.band_n.as<uint32_t>());
+        launch_check("raster_finalize");
+        return;
+    }
+    if (rw.tile_bwd) {  // per-tile backward with vector atomics into the AoS rows
+        const int ty0 = y0 / kTile, ty1 = (y0 + hs - 1) / kTile;
+        float* r16 = rw.raw16.as<float>();
+        HS_CUDA(cudaMemsetAsync(r16, 0, sizeof(float) * 16 * static_cast<size_t>(rw.n), st));
+        raster_bwd_tile_kernel<C><<<rw.tiles_x * (ty1 - ty0 + 1), kFwdThreads, 0, st>>>(
+            rw.ids.as<uint32_t>(), rw.ranges.as<uint2>(), rw.rec.as<float4>(), rw.shade.as<float4>(),
+            rw.p64.as<double>(), rw.n, rw.tiles_x, rw.width, rw.height, d_gf, r16, y0, hs, ty0);
+        launch_check("raster_bwd_tile");
+        raster_finalize_kernel<C, false, true><<<ceil_div(rw.n, 256), 256, 0, st>>>(
+            rw.n, r16, d_params, rw.width, rw.height, d_grads, d_flags, nullptr, nullptr, rw.shade.as<float4>());
         launch_check("raster_finalize");
         return;
     }

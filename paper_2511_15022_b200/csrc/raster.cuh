@@ -8,6 +8,10 @@ namespace hs {
 
 // Device-resident projection + tile index for one (set, canvas).  Buffers are
 // reused across calls and only grow.
+#ifndef HS_TILE_BWD_DEFAULT
+#define HS_TILE_BWD_DEFAULT true
+#endif
+
 struct RasterWork {
     int n = 0, c = 0, width = 0, height = 0;
     int tiles_x = 0, tiles_y = 0, tile_bits = 0;
@@ -25,6 +29,10 @@ struct RasterWork {
     DevBuf ranges;   // uint2 [begin,end) per tile
     DevBuf status;   // uint32[4]: [0] K (pairs), [1] overflow, [2] non-finite param, [3] unused
     DevBuf work;     // uint32 work counter of the persistent backward
+    DevBuf raw16;    // per-tile backward: [N][16] float partial sums (AoS, vector atomics)
+    // Backward form: per-tile with atomics (fast, last bits depend on the
+    // atomic order) or the deterministic per-Gaussian gather (K3).
+    bool tile_bwd = HS_TILE_BWD_DEFAULT;
     int sms = 0;     // SM count of the device (persistent grids)
     int64_t cap = 0; // pair capacity
     int band_ty0 = 0, band_ty1 = 1 << 30;  // tile rows binned (a row-slab rank: its band)
