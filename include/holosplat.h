@@ -52,6 +52,9 @@ hs_status hs_ctx_create(int device, hs_ctx** out);
 void hs_ctx_destroy(hs_ctx* ctx);
 /* cudaStream_t passed as void*; NULL = legacy default stream. */
 hs_status hs_ctx_set_stream(hs_ctx* ctx, void* stream);
+/* Backward form of the stand-alone hs_rasterize_backward: 1 (default)
+ * deterministic per-Gaussian gather, 0 the per-tile backward with atomics. */
+hs_status hs_ctx_set_deterministic(hs_ctx* ctx, int enable);
 hs_status hs_ctx_synchronize(hs_ctx* ctx);
 const char* hs_last_error(void);
 /* Number of kernels this library has launched in this process (for the bench's
@@ -236,6 +239,11 @@ hs_status hs_trainer_loss_partials(hs_trainer* tr, double* out2);
 hs_status hs_trainer_reserve_pairs(hs_trainer* tr, int64_t cap);
 /* Capture one step into a CUDA graph and replay it (0/1). */
 hs_status hs_trainer_use_graph(hs_trainer* tr, int enable);
+/* Raster backward form.  Default (0): the per-tile backward with vector
+ * atomics into per-Gaussian rows (fastest; the last bits of the gradients
+ * depend on the atomic order).  1: the per-Gaussian gather, bit-reproducible
+ * run to run.  Row-slab shards always use the gather over their band list. */
+hs_status hs_trainer_set_deterministic(hs_trainer* tr, int enable);
 /* Device event timing of the last (eager) step, ms per kernel slot:
  * [binning, raster_fwd, rows_fwd, cols_fwd, rows_inv, loss, rows_fwd(bwd),
  *  cols_bwd, rows_inv(bwd), raster_bwd, adan, total].  Needs profiling on and

@@ -119,6 +119,8 @@ _SIGS = {
     "hs_trainer_loss_partials": [C.c_void_p, C.POINTER(C.c_double)],
     "hs_trainer_reserve_pairs": [C.c_void_p, C.c_int64],
     "hs_trainer_use_graph": [C.c_void_p, C.c_int],
+    "hs_trainer_set_deterministic": [C.c_void_p, C.c_int],
+    "hs_ctx_set_deterministic": [C.c_void_p, C.c_int],
     "hs_trainer_set_profiling": [C.c_void_p, C.c_int],
     "hs_trainer_stage_ms": [C.c_void_p, C.POINTER(C.c_double)],
     "hs_trainer_step_count": [C.c_void_p],

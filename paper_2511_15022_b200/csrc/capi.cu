@@ -24,6 +24,7 @@ std::atomic<uint64_t> g_launches{0};
 const char* kGroupNames[6] = {"position", "scale", "rotation", "amplitude", "phase", "opacity"};
 
 struct CtxWork {
+    CtxWork() { rw.tile_bwd = false; }  // the stand-alone rasterize_backward: deterministic by default
     RasterWork rw;
     AsmWork aw;
     DevBuf flags, partials, out3, tstats;
@@ -624,6 +625,22 @@ hs_status hs_trainer_use_graph(hs_trainer* t, int enable) {
         }
     }
     return HS_OK;
+}
+
+hs_status hs_trainer_set_deterministic(hs_trainer* t, int enable) {
+    const bool tile = enable == 0;
+    if (t->rw.tile_bwd != tile) {
+        t->rw.tile_bwd = tile;
+        for (cudaGraphExec_t* g : {&t->graph, &t->host_graph, &t->slab_graph, &t->run_graph0, &t->run_graph}) {
+            if (*g) cudaGraphExecDestroy(*g);
+            *g = nullptr;
+        }
+    }
+    return HS_OK;
+}
+
+hs_status hs_ctx_set_deterministic(hs_ctx* ctx, int enable) {
+    return guard([&] { work_of(ctx).rw.tile_bwd = enable == 0; });
 }
 
 hs_status hs_trainer_set_profiling(hs_trainer* t, int enable) {

@@ -820,6 +820,11 @@ class Trainer:
     def use_graph(self, on=True):
         check(_lib.load().hs_trainer_use_graph(self.h, int(on)))
 
+    def set_deterministic(self, on=True):
+        """Raster backward as the bit-reproducible per-Gaussian gather (on) or the
+        faster per-tile backward with atomics (off, the default)."""
+        check(_lib.load().hs_trainer_set_deterministic(self.h, int(on)))
+
     def set_profiling(self, on=True):
         check(_lib.load().hs_trainer_set_profiling(self.h, int(on)))
 

@@ -326,11 +326,43 @@ def test_trainer_graph_replay_matches_eager(holo):
     dist = S.make_depth_planes(L, 3e-3, 2e-3)
     a = holo.Trainer(hs, w, h, target, masks, dist, holo.PropagationSpec(), 50)
     b = holo.Trainer(hs, w, h, target, masks, dist, holo.PropagationSpec(), 50)
+    for t in (a, b):
+        t.set_deterministic(True)  # bit-for-bit needs the gather backward (no atomics)
     b.use_graph(True)
     la = [a.step() for _ in range(5)]
     lb = [b.step() for _ in range(5)]
     assert np.allclose(la, lb, rtol=0, atol=0)
     assert np.array_equal(a.params(), b.params())
+
+
+def test_tile_backward_matches_deterministic_gather(holo, ref):
+    """The default per-tile backward (vector atomics into per-Gaussian rows)
+    and the deterministic per-Gaussian gather give the same gradients to fp32
+    summation-order noise, and both match the reference."""
+    c, w, h, n, L = 3, 256, 160, 4000, 2
+    g = f32(S.init_gaussians(n, c, w, h, 11))
+    img = S.synthetic_image(42, c, h, w)
+    depth = S.synthetic_depth(43, h, w)
+    masks = S.build_masks(depth, L, True)
+    dist = S.make_depth_planes(L, 3e-3, 2e-3)
+    mk = lambda: holo.Trainer(holo.GaussianSet(n, c, **g), w, h, holo.RealField(c, h, w, img), masks, dist,
+                              holo.PropagationSpec(), 20)
+    a, b = mk(), mk()
+    b.set_deterministic(True)
+    ga, gb = [], []
+    for t, out in ((a, ga), (b, gb)):
+        t.forward_backward()
+        out.append(t.grads_tensor().cpu().numpy().astype(np.float64))
+    assert rel_l2(ga[0], gb[0]) < 1e-5, rel_l2(ga[0], gb[0])
+    rs = ref.GaussianSet(n, c, *[np.ascontiguousarray(g[k]) for k in ref.GROUPS])
+    rt = ref.Trainer(rs, w, h, img.astype(np.float32).astype(np.float64), depth, L, 3e-3, 2e-3,
+                     ref.PropagationSpec(), 20)
+    _, rgrads = rt.step(want_grads=True)
+    want = np.concatenate([getattr(rgrads, k) for k in ref.GROUPS])
+    o = 0
+    for k, size in zip(ref.GROUPS, (2 * n, 2 * n, n, n * c, n * c, n)):
+        assert rel_l2(ga[0][o:o + size], want[o:o + size]) <= 1e-3, k
+        o += size
 
 
 def test_plane_sharded_trainers_sum_to_full_step(holo):
@@ -345,12 +377,14 @@ def test_plane_sharded_trainers_sum_to_full_step(holo):
     dist = S.make_depth_planes(L, 3e-3, 4e-3 / 7)
     spec = holo.PropagationSpec()
     full = holo.Trainer(hs, w, h, target, masks, dist, spec, 10)
+    full.set_deterministic(True)
     full.forward_backward()
     gfull = full.grads_tensor().cpu().numpy().astype(np.float64)
     pf = full.loss_partials()
     gs, parts = 0.0, np.zeros(2)
     for r in range(2):
         t = holo.Trainer(hs, w, h, target, masks, dist, spec, 10, plane_range=P.plane_shard(L, r, 2))
+        t.set_deterministic(True)
         t.forward_backward()
         gs = gs + t.grads_tensor().cpu().numpy().astype(np.float64)
         parts += np.array(t.loss_partials())
@@ -372,6 +406,7 @@ def test_channel_sharded_trainers_match_full_step(holo):
     wl = S.WAVELENGTHS[c]
     full = holo.Trainer(holo.GaussianSet(n, c, **g), w, h, holo.RealField(c, h, w, img), masks, dist,
                         holo.PropagationSpec(wl), 10)
+    full.set_deterministic(True)
     full.forward_backward()
     gf = full.grads_tensor().cpu().numpy().astype(np.float64)
     pf = np.array(full.loss_partials())
@@ -382,6 +417,7 @@ def test_channel_sharded_trainers_match_full_step(holo):
         gs = P.slice_channels(g, n, c, b, e)
         t = holo.Trainer(holo.GaussianSet(n, cl, **gs), w, h, holo.RealField(cl, h, w, img[b:e]), masks, dist,
                          holo.PropagationSpec(wl[b:e]), 10, channels_total=c)
+        t.set_deterministic(True)
         t.forward_backward()
         gr = t.grads_tensor().cpu().numpy().astype(np.float64)
         geo = np.concatenate([gr[lo:hi] for lo, hi in P.geometry_ranges(n, cl)])
@@ -408,6 +444,8 @@ def test_trainer_step_host_matches_device_step(holo):
     mk = lambda: holo.Trainer(holo.GaussianSet(n, c, **g), w, h, holo.RealField(c, h, w, img), masks, dist,
                               holo.PropagationSpec(), 10)
     a, b = mk(), mk()
+    for t in (a, b):
+        t.set_deterministic(True)
     p0 = a.params()
     host = torch.from_numpy(p0.copy()).pin_memory()
     la = a.step(sync_loss=True)
@@ -431,6 +469,8 @@ def test_trainer_run_host_matches_device_steps(holo, graphs):
     mk = lambda: holo.Trainer(holo.GaussianSet(n, c, **g), w, h, holo.RealField(c, h, w, img), masks, dist,
                               holo.PropagationSpec(), 20)
     a, b = mk(), mk()
+    for t in (a, b):
+        t.set_deterministic(True)
     b.use_graph(graphs)
     host = torch.from_numpy(b.params().copy()).pin_memory()
     side = torch.cuda.Stream()
@@ -477,6 +517,8 @@ def test_reserve_pairs_recaptures_the_step_graphs(holo):
     mk = lambda: holo.Trainer(holo.GaussianSet(n, c, **g), w, h, holo.RealField(c, h, w, img), masks, dist,
                               holo.PropagationSpec(), 10)
     eager, graphed = mk(), mk()
+    for t in (eager, graphed):
+        t.set_deterministic(True)
     graphed.use_graph(True)
     host = torch.from_numpy(graphed.params().copy()).pin_memory()
     side = torch.cuda.Stream()

@@ -39,6 +39,7 @@ def run(holo, R, n, c, w, h, L, steps, put=False):
     from paper_2511_15022_b200 import parallel as P
     gs, target, masks, dist, spec = scene(holo, n, c, w, h, L)
     full = holo.Trainer(gs, w, h, target, masks, dist, spec, 20)
+    full.set_deterministic(True)  # the slab ranks' backward is the gather: compare like with like
     trs = []
     for r in range(R):
         t = holo.Trainer(gs, w, h, target, masks, dist, spec, 20)
