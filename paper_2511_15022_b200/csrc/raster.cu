@@ -1009,11 +1009,12 @@ __global__ void __launch_bounds__(kFwdThreads, 6) raster_bwd_tile_kernel(
                 const float dx = (static_cast<float>(cx0 + k) - r0.x) - r0.z;
                 const float m = fmaf(fmaf(i00, dx, bq), dx, cq);
                 const float aG = ex2f(fmaf(m, kNegHalfLog2e, l2a));  // alpha e^{-m/2}
-                const bool in = m <= M;
-                const bool fast = m <= Mfast && fabsf(aG - 0.99f) > 1e-5f;
-                rowband |= (in && !fast) ? (1u << k) : 0u;
-                const bool use = in && fast;
-                accum(gp + k, dx, dy, use ? fminf(aG, 0.99f) : 0.f, (use && aG <= 0.99f) ? aG : 0.f);
+                // fast: clearly inside the cutoff and clearly unsaturated; the
+                // rest of the ellipse (cutoff band, saturation) goes to the exact pass
+                const bool fast = m <= Mfast && aG < 0.99f - 1e-5f;
+                rowband |= (m <= M && !fast) ? (1u << k) : 0u;
+                const float w = fast ? aG : 0.f;
+                accum(gp + k, dx, dy, w, w);
             }
             const int sh = (y - cy0) << 3;
             if (sh < 32) band_lo |= rowband << sh;
