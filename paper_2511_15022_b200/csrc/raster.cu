@@ -919,7 +919,7 @@ __device__ __forceinline__ void red_add_v4(float* dst, float a, float b, float c
 }
 
 template <int C>
-__global__ void __launch_bounds__(kFwdThreads, 6) raster_bwd_tile_kernel(
+__global__ void __launch_bounds__(kFwdThreads, 5) raster_bwd_tile_kernel(
     const uint32_t* __restrict__ ids, const uint2* __restrict__ ranges, const float4* __restrict__ rec,
     const float4* __restrict__ shade, const double* __restrict__ p64, int N, int tiles_x, int W, int H,
     const float2* __restrict__ gfield, float* __restrict__ raw16, int y0, int hs, int ty0) {
@@ -997,25 +997,57 @@ __global__ void __launch_bounds__(kFwdThreads, 6) raster_bwd_tile_kernel(
             T3 = fmaf(t.x, dy, T3);
         };
         // fast fp32 pass over the cell; pixels inside a Gaussian's error band
-        // (or at the saturation threshold) are only flagged in a 64-bit mask
+        // (or at the saturation threshold) are only flagged in a 64-bit mask.
+        // The column offsets are exact per lane and column (computed once);
+        // forms and exponents run on pixel pairs; along a row dy is constant, so
+        // the row sums R0 = sum qv, (R1, R2) = sum qv (dx, dx^2) are folded
+        // into QA, T1, T2, T3 once per row.
+        float dxk[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) dxk[k] = (static_cast<float>(cx0 + k) - r0.x) - r0.z;
+        const float2 i00_2 = f2splat(i00), kx2 = f2splat(kNegHalfLog2e), l2a2 = f2splat(l2a);
         uint32_t band_lo = 0u, band_hi = 0u;
         for (int y = ry0; y < ry1; ++y) {
             const float dy = (static_cast<float>(y) - r0.y) - r0.w;
-            const float bq = 2.f * i01 * dy, cq = i11 * dy * dy;  // m = (i00 dx + bq) dx + cq
+            const float2 bq2 = f2splat(2.f * i01 * dy), cq2 = f2splat(i11 * dy * dy);  // m = (i00 dx + bq) dx + cq
             const float2* gp = &s_g[warp][0][(y - cy0) << 3];
             uint32_t rowband = 0u;
+            float R0 = 0.f;
+            float2 R12 = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const float dx = (static_cast<float>(cx0 + k) - r0.x) - r0.z;
-                const float m = fmaf(fmaf(i00, dx, bq), dx, cq);
-                const float aG = ex2f(fmaf(m, kNegHalfLog2e, l2a));  // alpha e^{-m/2}
-                // fast: clearly inside the cutoff and clearly unsaturated; the
-                // rest of the ellipse (cutoff band, saturation) goes to the exact pass
-                const bool fast = m <= Mfast && aG < 0.99f - 1e-5f;
-                rowband |= (m <= M && !fast) ? (1u << k) : 0u;
-                const float w = fast ? aG : 0.f;
-                accum(gp + k, dx, dy, w, w);
+            for (int k = 0; k < 8; k += 2) {
+                const float2 dxp = make_float2(dxk[k], dxk[k + 1]);
+                const float2 m2 = f2fma(f2fma(i00_2, dxp, bq2), dxp, cq2);
+                const float2 arg = f2fma(m2, kx2, l2a2);
+                const float aGs[2] = {ex2f(arg.x), ex2f(arg.y)};  // alpha e^{-m/2}
+                const float ms[2] = {m2.x, m2.y};
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const float m = ms[h], aG = aGs[h], dx = dxk[k + h];
+                    // fast: clearly inside the cutoff and clearly unsaturated; the
+                    // rest of the ellipse (cutoff band, saturation) goes to the exact pass
+                    const bool fast = m <= Mfast && aG < 0.99f - 1e-5f;
+                    rowband |= (m <= M && !fast) ? (1u << (k + h)) : 0u;
+                    const float w = fast ? aG : 0.f;
+                    float2 gv[C];
+#pragma unroll
+                    for (int c = 0; c < C; ++c) gv[c] = gp[c * 64 + k + h];
+                    float2 sa = f2mul(S[0], gv[0]);
+                    Sg[0] = f2fma(f2splat(w), gv[0], Sg[0]);
+#pragma unroll
+                    for (int c = 1; c < C; ++c) {
+                        Sg[c] = f2fma(f2splat(w), gv[c], Sg[c]);
+                        sa = f2fma(S[c], gv[c], sa);
+                    }
+                    const float qv = (sa.x + sa.y) * w;
+                    R0 += qv;
+                    R12 = f2fma(f2splat(qv), make_float2(dx, dx * dx), R12);
+                }
             }
+            QA += R0;
+            T1 = f2add(T1, make_float2(R12.x, dy * R0));
+            T2 = f2add(T2, make_float2(R12.y, dy * dy * R0));
+            T3 = fmaf(dy, R12.x, T3);
             const int sh = (y - cy0) << 3;
             if (sh < 32) band_lo |= rowband << sh;
             else band_hi |= rowband << (sh - 32);
