@@ -912,6 +912,9 @@ __global__ void __launch_bounds__(kBwdThreads, MINB) raster_bwd_kernel(
 // deterministic in the last bits (atomic order); K3 is the deterministic path.
 // ---------------------------------------------------------------------------
 constexpr int kTbQ = 64;  // per-warp hit queue (two batches)
+#ifndef HS_TILE_BWD_1W
+#define HS_TILE_BWD_1W 1
+#endif
 
 __device__ __forceinline__ void red_add_v4(float* dst, float a, float b, float c, float d) {
     asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(a), "f"(b), "f"(c), "f"(d)
@@ -1114,6 +1117,209 @@ __global__ void __launch_bounds__(kFwdThreads, 5) raster_bwd_tile_kernel(
 // Chain rule of rasterize_backward (rasterizer.cpp:251-282) in fp64, one
 // thread per Gaussian, from the warp-reduced raw sums [d_amp[C], d_phase[C],
 // d_alpha, gmx, gmy, ga, gb, gc] (SoA, N each).
+// K3t, one-warp form: one warp per 16x16 tile.  Hits are queued as (Gaussian,
+// cell) entries of all four 8x8 cells of the tile, so a batch of 32 lanes mixes
+// cells and only the tile's last batch runs partly empty (per-cell queues
+// leave one partial batch per cell).  Each lane walks the 64 pixels of its own
+// cell; the tile's gradient is staged per cell with a 2-bank shift between
+// cells, so the four cells' pixel p sit in different banks (one wavefront).
+constexpr int kTb1Stride = 65;  // float2 per staged cell (64 + 1 pad)
+constexpr int kTb1Q = 160;      // queue: < 32 left over + 4 x 32 new entries
+
+template <int C>
+__global__ void __launch_bounds__(32, 16) raster_bwd_tile1w_kernel(
+    const uint32_t* __restrict__ ids, const uint2* __restrict__ ranges, const float4* __restrict__ rec,
+    const float4* __restrict__ shade, const double* __restrict__ p64, int N, int tiles_x, int W, int H,
+    const float2* __restrict__ gfield, float* __restrict__ raw16, int y0, int hs, int ty0) {
+    static_assert(2 * C + 6 <= 16, "AoS row of 16 floats");
+    __shared__ float2 s_t[C][4 * kTb1Stride];
+    __shared__ uint32_t s_q[kTb1Q];
+    const int tile = blockIdx.x + ty0 * tiles_x;
+    const int tx = tile % tiles_x, ty = tile / tiles_x;
+    const int lane = threadIdx.x;
+    const int ylo = max(y0, 0), yhi = min(y0 + hs, H);  // valid rows [ylo, yhi)
+    const unsigned cs = static_cast<unsigned>(hs) * static_cast<unsigned>(W);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {  // stage the tile's 256 pixels: cell = pix >> 6
+        const int pix = lane + 32 * j, cell = pix >> 6, p = pix & 63;
+        const int x = tx * kTile + (cell & 1) * 8 + (p & 7), y = ty * kTile + (cell >> 1) * 8 + (p >> 3);
+        const bool ok = x < W && y >= ylo && y < yhi;
+        const float2* src = gfield + (ok ? static_cast<unsigned>(y - y0) * static_cast<unsigned>(W) + x : 0u);
+#pragma unroll
+        for (int c = 0; c < C; ++c)
+            s_t[c][cell * kTb1Stride + p] = ok ? __ldg(src + static_cast<size_t>(c) * cs) : make_float2(0.f, 0.f);
+    }
+    // cells with at least one valid pixel (warp-uniform)
+    unsigned cell_ok = 0u;
+#pragma unroll
+    for (int cell = 0; cell < 4; ++cell) {
+        const int cx = tx * kTile + (cell & 1) * 8, cy = ty * kTile + (cell >> 1) * 8;
+        if (cx < W && max(cy, ylo) < min(cy + 8, yhi)) cell_ok |= 1u << cell;
+    }
+    __syncwarp();
+    const uint2 rg = ranges[tile];
+    int qn = 0;
+    const unsigned lanemask_lt = (1u << lane) - 1u;
+    auto batch = [&](int nb) {  // process s_q[0, nb)
+        const bool act = lane < nb;
+        const uint32_t e = act ? s_q[lane] : s_q[0];
+        const uint32_t g = e >> 2;
+        const int cell = static_cast<int>(e & 3u);
+        const int cx0 = tx * kTile + (cell & 1) * 8, cy0 = ty * kTile + (cell >> 1) * 8;
+        const float4 r0 = rec[g];
+        const float4 r1 = rec[static_cast<size_t>(N) + g];
+        const float4 r2 = rec[2 * static_cast<size_t>(N) + g];
+        float2 S[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            const float4 sh = shade[static_cast<size_t>(c) * N + g];
+            S[c] = make_float2(sh.x, sh.y);
+        }
+        const float i00 = r1.x, i01 = r1.y, i11 = r1.z;
+        const float cut = r1.w, tol = r2.y, l2a = r2.x, alpha = exp2f(r2.x);
+        const float M = act ? cut + tol : -1.f;  // idle lanes never pass m <= M
+        const float Mfast = cut - tol;
+        const double* q = p64 + g;
+        float2 Sg[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) Sg[c] = make_float2(0.f, 0.f);
+        float2 T1 = make_float2(0.f, 0.f), T2 = make_float2(0.f, 0.f);
+        float QA = 0.f, T3 = 0.f;
+        const float2* gcell = &s_t[0][cell * kTb1Stride];
+        float dxk[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) dxk[k] = (static_cast<float>(cx0 + k) - r0.x) - r0.z;
+        const float2 i00_2 = f2splat(i00), kx2 = f2splat(kNegHalfLog2e), l2a2 = f2splat(l2a);
+        uint32_t band_lo = 0u, band_hi = 0u;
+#pragma unroll 1
+        for (int r = 0; r < 8; ++r) {
+            const int y = cy0 + r;
+            const bool rowok = y >= ylo && y < yhi;
+            const float Mr = rowok ? M : -1.f, Mfr = rowok ? Mfast : -1.f;
+            const float dy = (static_cast<float>(y) - r0.y) - r0.w;
+            const float2 bq2 = f2splat(2.f * i01 * dy), cq2 = f2splat(i11 * dy * dy);  // m = (i00 dx + bq) dx + cq
+            const float2* gp = gcell + (r << 3);
+            uint32_t rowband = 0u;
+            float R0 = 0.f;
+            float2 R12 = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int k = 0; k < 8; k += 2) {
+                const float2 dxp = make_float2(dxk[k], dxk[k + 1]);
+                const float2 m2 = f2fma(f2fma(i00_2, dxp, bq2), dxp, cq2);
+                const float2 arg = f2fma(m2, kx2, l2a2);
+                const float aGs[2] = {ex2f(arg.x), ex2f(arg.y)};  // alpha e^{-m/2}
+                const float ms[2] = {m2.x, m2.y};
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const float m = ms[h], aG = aGs[h], dx = dxk[k + h];
+                    const bool fast = m <= Mfr && aG < 0.99f - 1e-5f;
+                    rowband |= (m <= Mr && !fast) ? (1u << (k + h)) : 0u;
+                    const float w = fast ? aG : 0.f;
+                    float2 gv[C];
+#pragma unroll
+                    for (int c = 0; c < C; ++c) gv[c] = gp[c * 4 * kTb1Stride + k + h];
+                    float2 sa = f2mul(S[0], gv[0]);
+                    Sg[0] = f2fma(f2splat(w), gv[0], Sg[0]);
+#pragma unroll
+                    for (int c = 1; c < C; ++c) {
+                        Sg[c] = f2fma(f2splat(w), gv[c], Sg[c]);
+                        sa = f2fma(S[c], gv[c], sa);
+                    }
+                    const float qv = (sa.x + sa.y) * w;
+                    R0 += qv;
+                    R12 = f2fma(f2splat(qv), make_float2(dx, dx * dx), R12);
+                }
+            }
+            QA += R0;
+            T1 = f2add(T1, make_float2(R12.x, dy * R0));
+            T2 = f2add(T2, make_float2(R12.y, dy * dy * R0));
+            T3 = fmaf(dy, R12.x, T3);
+            if (r < 4) band_lo |= rowband << (r << 3);
+            else band_hi |= rowband << ((r - 4) << 3);
+        }
+        // rare: the exact fp64 decision for the flagged pixels (rasterizer.cpp:220-228)
+        if (__any_sync(0xffffffffu, (band_lo | band_hi) != 0u)) {
+            const int xmax = W - cx0;
+            for (uint64_t bm = (static_cast<uint64_t>(band_hi) << 32) | band_lo; bm; bm &= bm - 1) {
+                const int pix = __ffsll(static_cast<long long>(bm)) - 1;
+                const int k = pix & 7, y = cy0 + (pix >> 3), x = cx0 + k;
+                if (k >= xmax) continue;  // outside the canvas
+                const float4 e4 = exact_contrib4(q, N, x, y);
+                if (e4.w == 0.f) continue;
+                const float dx = (static_cast<float>(x) - r0.x) - r0.z;
+                const float dy = (static_cast<float>(y) - r0.y) - r0.w;
+                const float w = e4.y, qv0 = e4.z != 0.f ? 0.f : alpha * e4.x;
+                float2 gv[C];
+#pragma unroll
+                for (int c = 0; c < C; ++c) gv[c] = gcell[c * 4 * kTb1Stride + pix];
+                float2 sa = f2mul(S[0], gv[0]);
+                Sg[0] = f2fma(f2splat(w), gv[0], Sg[0]);
+#pragma unroll
+                for (int c = 1; c < C; ++c) {
+                    Sg[c] = f2fma(f2splat(w), gv[c], Sg[c]);
+                    sa = f2fma(S[c], gv[c], sa);
+                }
+                const float qv = (sa.x + sa.y) * qv0;
+                QA += qv;
+                const float2 dxy = make_float2(dx, dy);
+                const float2 t = f2mul(f2splat(qv), dxy);
+                T1 = f2add(T1, t);
+                T2 = f2fma(t, dxy, T2);
+                T3 = fmaf(t.x, dy, T3);
+            }
+        }
+        if (act) {
+            float v[16];
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                v[c] = Sg[c].x;
+                v[C + c] = Sg[c].y;
+            }
+            v[2 * C + 0] = alpha > 0.f ? QA / alpha : 0.f;
+            v[2 * C + 1] = fmaf(i00, T1.x, i01 * T1.y);
+            v[2 * C + 2] = fmaf(i01, T1.x, i11 * T1.y);
+            v[2 * C + 3] = -0.5f * T2.x;
+            v[2 * C + 4] = -T3;
+            v[2 * C + 5] = -0.5f * T2.y;
+#pragma unroll
+            for (int i = 2 * C + 6; i < 16; ++i) v[i] = 0.f;
+            float* dst = raw16 + static_cast<size_t>(g) * 16;
+#pragma unroll
+            for (int k = 0; k < (2 * C + 6 + 3) / 4; ++k) red_add_v4(dst + 4 * k, v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+        }
+    };
+    for (uint32_t base = rg.x; base < rg.y; base += 32) {
+        const uint32_t i = base + lane;
+        uint32_t g = 0;
+        float4 r0, r1, r2;
+        const bool valid = i < rg.y;
+        if (valid) {
+            g = ids[i];
+            r0 = rec[g];
+            r1 = rec[static_cast<size_t>(N) + g];
+            r2 = rec[2 * static_cast<size_t>(N) + g];
+        }
+#pragma unroll
+        for (int cell = 0; cell < 4; ++cell) {
+            const bool hit = valid && ((cell_ok >> cell) & 1u) &&
+                             cell_hit(r0, r1, r2, static_cast<float>(tx * kTile + (cell & 1) * 8),
+                                      static_cast<float>(ty * kTile + (cell >> 1) * 8), 7.f, 7.f);
+            const unsigned mask = __ballot_sync(0xffffffffu, hit);
+            if (hit) s_q[qn + __popc(mask & lanemask_lt)] = (g << 2) | static_cast<uint32_t>(cell);
+            qn += __popc(mask);
+        }
+        __syncwarp();
+        while (qn >= 32) {
+            batch(32);
+            __syncwarp();
+            qn -= 32;
+            for (int j = lane; j < qn; j += 32) s_q[j] = s_q[32 + j];
+            __syncwarp();
+        }
+    }
+    if (qn > 0) batch(qn);
+}
+
 // AOS: the per-tile backward's [N][16] rows (sum alpha_eff g_c re/im instead of
 // (d_amp, d_phase), converted here with the Gaussian's shading record).
 template <int C, bool LIST = false, bool AOS = false>
@@ -1357,7 +1563,11 @@ static void bwd_launch(const RasterWork& rw, const float* d_params, const float2
         const int ty0 = y0 / kTile, ty1 = (y0 + hs - 1) / kTile;
         float* r16 = rw.raw16.as<float>();
         HS_CUDA(cudaMemsetAsync(r16, 0, sizeof(float) * 16 * static_cast<size_t>(rw.n), st));
+#if HS_TILE_BWD_1W
+        raster_bwd_tile1w_kernel<C><<<rw.tiles_x * (ty1 - ty0 + 1), 32, 0, st>>>(
+#else
         raster_bwd_tile_kernel<C><<<rw.tiles_x * (ty1 - ty0 + 1), kFwdThreads, 0, st>>>(
+#endif
             rw.ids.as<uint32_t>(), rw.ranges.as<uint2>(), rw.rec.as<float4>(), rw.shade.as<float4>(),
             rw.p64.as<double>(), rw.n, rw.tiles_x, rw.width, rw.height, d_gf, r16, y0, hs, ty0);
         launch_check("raster_bwd_tile");
