@@ -896,233 +896,29 @@ __global__ void __launch_bounds__(kBwdThreads, MINB) raster_bwd_kernel(
 }
 
 // ---------------------------------------------------------------------------
-// K3t: backward, per tile (the north_star form).  One CTA per 16x16 tile, four
-// warps, each an 8x8 cell of the tile, as the forward.  A warp stages its
-// cell's 64 gradient pixels (C channels) in shared memory and walks the tile's
-// sorted Gaussian list 32 candidates at a time: each lane tests one candidate
-// against the cell (the forward's row-band bound), the hits are compacted into
-// a per-warp queue, and every 32 queued hits run as one batch with LANE =
-// GAUSSIAN: the warp loops over the cell's 64 pixels (position and gradient are
-// warp-uniform -- shared-memory broadcasts, no gathers), every lane evaluating
-// its own Gaussian at that pixel with the same fast/exact decision as K3, and
-// accumulates its Gaussian's 7 + 2C partial sums in registers.  The sums over
-// the cell go to the Gaussian's row of an AoS [N][16] buffer with four 16-byte
-// vector atomics (red.global.add.v4.f32): one reduction in registers over the
-// cell's pixels before one atomic per (cell, Gaussian, 4 values).  Not
-// deterministic in the last bits (atomic order); K3 is the deterministic path.
+// K3t: backward, per tile (the north_star form; the default trainer path).
+// One warp per 16x16 tile, cells of 8x8 pixels as the forward.  The warp
+// stages the tile's gradient (C channels) in shared memory and walks the
+// tile's sorted Gaussian list 32 candidates at a time: each lane tests one
+// candidate against the four cells (the forward's row-band bound) and the hits
+// are compacted into one queue of (Gaussian, cell) entries.  Every 32 queued
+// entries run as one batch with LANE = (GAUSSIAN, CELL): the lane walks the 64
+// pixels of its cell (gradient values from shared memory, the cells staged
+// with a 2-bank shift so the lanes' reads take one wavefront; no global
+// gathers), evaluates its Gaussian there with the same fast/exact decision as
+// K3 and accumulates the 7 + 2C partial sums in registers.  Only the tile's
+// last batch runs partly empty.  The sums over the cell go to the Gaussian's
+// row of an AoS [N][16] buffer with 16-byte vector atomics
+// (red.global.add.v4.f32): the reduction over the cell's pixels happens in
+// registers before one atomic per (cell, Gaussian, 4 values).  The last bits
+// depend on the atomic order; K3 is the deterministic path.
 // ---------------------------------------------------------------------------
-constexpr int kTbQ = 64;  // per-warp hit queue (two batches)
-#ifndef HS_TILE_BWD_1W
-#define HS_TILE_BWD_1W 1
-#endif
 
 __device__ __forceinline__ void red_add_v4(float* dst, float a, float b, float c, float d) {
     asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(a), "f"(b), "f"(c), "f"(d)
                  : "memory");
 }
 
-template <int C>
-__global__ void __launch_bounds__(kFwdThreads, 5) raster_bwd_tile_kernel(
-    const uint32_t* __restrict__ ids, const uint2* __restrict__ ranges, const float4* __restrict__ rec,
-    const float4* __restrict__ shade, const double* __restrict__ p64, int N, int tiles_x, int W, int H,
-    const float2* __restrict__ gfield, float* __restrict__ raw16, int y0, int hs, int ty0) {
-    static_assert(2 * C + 6 <= 16, "AoS row of 16 floats");
-    __shared__ float2 s_g[kFwdThreads / 32][C][64];  // cell gradient, pixel p = (p >> 3, p & 7)
-    __shared__ uint32_t s_q[kFwdThreads / 32][kTbQ];
-    const int tile = blockIdx.x + ty0 * tiles_x;
-    const int tx = tile % tiles_x, ty = tile / tiles_x;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int cx0 = tx * kTile + (warp & 1) * 8;
-    const int cy0 = ty * kTile + (warp >> 1) * 8;
-    // the cell's rows inside the band [y0, y0 + hs) and the canvas; columns inside the canvas
-    const int ry0 = max(cy0, y0), ry1 = min(min(cy0 + 8, y0 + hs), H);  // [ry0, ry1)
-    const int cx1 = min(cx0 + 8, W);
-    if (ry0 >= ry1 || cx0 >= cx1) return;  // warp-uniform (whole cell outside)
-    (void)N;
-    const unsigned cs = static_cast<unsigned>(hs) * static_cast<unsigned>(W);
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {  // lane stages pixels lane and lane + 32
-        const int pix = lane + 32 * k;
-        const int x = cx0 + (pix & 7), y = cy0 + (pix >> 3);
-        const bool ok = x < cx1 && y >= ry0 && y < ry1;
-        const float2* src = gfield + (ok ? static_cast<unsigned>(y - y0) * static_cast<unsigned>(W) + x : 0u);
-#pragma unroll
-        for (int c = 0; c < C; ++c) s_g[warp][c][pix] = ok ? __ldg(src + static_cast<size_t>(c) * cs) : make_float2(0.f, 0.f);
-    }
-    __syncwarp();
-    const uint2 rg = ranges[tile];
-    int qn = 0;  // queued hits (warp-uniform)
-    const unsigned lanemask_lt = (1u << lane) - 1u;
-    auto batch = [&](int nb) {  // process s_q[0, nb)
-        const bool act = lane < nb;
-        const uint32_t g = act ? s_q[warp][lane] : s_q[warp][0];
-        const float4 r0 = rec[g];
-        const float4 r1 = rec[static_cast<size_t>(N) + g];
-        const float4 r2 = rec[2 * static_cast<size_t>(N) + g];
-        float2 S[C];
-#pragma unroll
-        for (int c = 0; c < C; ++c) {
-            const float4 sh = shade[static_cast<size_t>(c) * N + g];
-            S[c] = make_float2(sh.x, sh.y);
-        }
-        const float i00 = r1.x, i01 = r1.y, i11 = r1.z;
-        const float cut = r1.w, tol = r2.y, l2a = r2.x, alpha = exp2f(r2.x);
-        const float M = act ? cut + tol : -1.f;  // idle lanes never pass m <= M
-        const float Mfast = cut - tol;
-        const double* q = p64 + g;
-        // per-lane sums over the cell: Sg_c = sum a_eff g_c; over the unsaturated
-        // pixels with qv = s_amp alpha G: QA = sum qv, T1 = sum qv (dx, dy),
-        // T2 = sum qv (dx^2, dy^2), T3 = sum qv dx dy  (gm = Sigma^-1 T1,
-        // (ga, gc) = -T2 / 2, gb = -T3, d_alpha = QA / alpha)
-        float2 Sg[C];
-#pragma unroll
-        for (int c = 0; c < C; ++c) Sg[c] = make_float2(0.f, 0.f);
-        float2 T1 = make_float2(0.f, 0.f), T2 = make_float2(0.f, 0.f);
-        float QA = 0.f, T3 = 0.f;
-        // accumulate one pixel with weight w = a_eff (0 outside) and qv
-        auto accum = [&](const float2* gp, float dx, float dy, float w, float qv0) {
-            float2 gv[C];
-#pragma unroll
-            for (int c = 0; c < C; ++c) gv[c] = gp[c * 64];
-            float2 sa = f2mul(S[0], gv[0]);
-            Sg[0] = f2fma(f2splat(w), gv[0], Sg[0]);
-#pragma unroll
-            for (int c = 1; c < C; ++c) {
-                Sg[c] = f2fma(f2splat(w), gv[c], Sg[c]);
-                sa = f2fma(S[c], gv[c], sa);
-            }
-            const float qv = (sa.x + sa.y) * qv0;
-            QA += qv;
-            const float2 dxy = make_float2(dx, dy);
-            const float2 t = f2mul(f2splat(qv), dxy);
-            T1 = f2add(T1, t);
-            T2 = f2fma(t, dxy, T2);
-            T3 = fmaf(t.x, dy, T3);
-        };
-        // fast fp32 pass over the cell; pixels inside a Gaussian's error band
-        // (or at the saturation threshold) are only flagged in a 64-bit mask.
-        // The column offsets are exact per lane and column (computed once);
-        // forms and exponents run on pixel pairs; along a row dy is constant, so
-        // the row sums R0 = sum qv, (R1, R2) = sum qv (dx, dx^2) are folded
-        // into QA, T1, T2, T3 once per row.
-        float dxk[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) dxk[k] = (static_cast<float>(cx0 + k) - r0.x) - r0.z;
-        const float2 i00_2 = f2splat(i00), kx2 = f2splat(kNegHalfLog2e), l2a2 = f2splat(l2a);
-        uint32_t band_lo = 0u, band_hi = 0u;
-        for (int y = ry0; y < ry1; ++y) {
-            const float dy = (static_cast<float>(y) - r0.y) - r0.w;
-            const float2 bq2 = f2splat(2.f * i01 * dy), cq2 = f2splat(i11 * dy * dy);  // m = (i00 dx + bq) dx + cq
-            const float2* gp = &s_g[warp][0][(y - cy0) << 3];
-            uint32_t rowband = 0u;
-            float R0 = 0.f;
-            float2 R12 = make_float2(0.f, 0.f);
-#pragma unroll
-            for (int k = 0; k < 8; k += 2) {
-                const float2 dxp = make_float2(dxk[k], dxk[k + 1]);
-                const float2 m2 = f2fma(f2fma(i00_2, dxp, bq2), dxp, cq2);
-                const float2 arg = f2fma(m2, kx2, l2a2);
-                const float aGs[2] = {ex2f(arg.x), ex2f(arg.y)};  // alpha e^{-m/2}
-                const float ms[2] = {m2.x, m2.y};
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const float m = ms[h], aG = aGs[h], dx = dxk[k + h];
-                    // fast: clearly inside the cutoff and clearly unsaturated; the
-                    // rest of the ellipse (cutoff band, saturation) goes to the exact pass
-                    const bool fast = m <= Mfast && aG < 0.99f - 1e-5f;
-                    rowband |= (m <= M && !fast) ? (1u << (k + h)) : 0u;
-                    const float w = fast ? aG : 0.f;
-                    float2 gv[C];
-#pragma unroll
-                    for (int c = 0; c < C; ++c) gv[c] = gp[c * 64 + k + h];
-                    float2 sa = f2mul(S[0], gv[0]);
-                    Sg[0] = f2fma(f2splat(w), gv[0], Sg[0]);
-#pragma unroll
-                    for (int c = 1; c < C; ++c) {
-                        Sg[c] = f2fma(f2splat(w), gv[c], Sg[c]);
-                        sa = f2fma(S[c], gv[c], sa);
-                    }
-                    const float qv = (sa.x + sa.y) * w;
-                    R0 += qv;
-                    R12 = f2fma(f2splat(qv), make_float2(dx, dx * dx), R12);
-                }
-            }
-            QA += R0;
-            T1 = f2add(T1, make_float2(R12.x, dy * R0));
-            T2 = f2add(T2, make_float2(R12.y, dy * dy * R0));
-            T3 = fmaf(dy, R12.x, T3);
-            const int sh = (y - cy0) << 3;
-            if (sh < 32) band_lo |= rowband << sh;
-            else band_hi |= rowband << (sh - 32);
-        }
-        // rare: the exact fp64 decision for the flagged pixels (rasterizer.cpp:220-228)
-        if (__any_sync(0xffffffffu, (band_lo | band_hi) != 0u)) {
-            const int xmax = cx1 - cx0;
-            for (uint64_t bm = (static_cast<uint64_t>(band_hi) << 32) | band_lo; bm; bm &= bm - 1) {
-                const int pix = __ffsll(static_cast<long long>(bm)) - 1;
-                const int k = pix & 7, y = cy0 + (pix >> 3), x = cx0 + k;
-                if (k >= xmax) continue;  // outside the canvas
-                const float4 e4 = exact_contrib4(q, N, x, y);
-                if (e4.w == 0.f) continue;
-                const float dx = (static_cast<float>(x) - r0.x) - r0.z;
-                const float dy = (static_cast<float>(y) - r0.y) - r0.w;
-                accum(&s_g[warp][0][pix], dx, dy, e4.y, e4.z != 0.f ? 0.f : alpha * e4.x);
-            }
-        }
-        if (act) {
-            float v[16];
-#pragma unroll
-            for (int c = 0; c < C; ++c) {
-                v[c] = Sg[c].x;
-                v[C + c] = Sg[c].y;
-            }
-            v[2 * C + 0] = alpha > 0.f ? QA / alpha : 0.f;
-            v[2 * C + 1] = fmaf(i00, T1.x, i01 * T1.y);
-            v[2 * C + 2] = fmaf(i01, T1.x, i11 * T1.y);
-            v[2 * C + 3] = -0.5f * T2.x;
-            v[2 * C + 4] = -T3;
-            v[2 * C + 5] = -0.5f * T2.y;
-#pragma unroll
-            for (int i = 2 * C + 6; i < 16; ++i) v[i] = 0.f;
-            float* dst = raw16 + static_cast<size_t>(g) * 16;
-#pragma unroll
-            for (int k = 0; k < (2 * C + 6 + 3) / 4; ++k) red_add_v4(dst + 4 * k, v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
-        }
-    };
-    const float fcx = static_cast<float>(cx0), fcy = static_cast<float>(cy0);
-    for (uint32_t base = rg.x; base < rg.y; base += 32) {
-        const uint32_t i = base + lane;
-        bool hit = false;
-        uint32_t g = 0;
-        if (i < rg.y) {
-            g = ids[i];
-            hit = cell_hit(rec[g], rec[static_cast<size_t>(N) + g], rec[2 * static_cast<size_t>(N) + g], fcx, fcy, 7.f,
-                           7.f);
-        }
-        const unsigned mask = __ballot_sync(0xffffffffu, hit);
-        if (hit) s_q[warp][qn + __popc(mask & lanemask_lt)] = g;
-        qn += __popc(mask);
-        __syncwarp();
-        if (qn >= 32) {
-            batch(32);
-            __syncwarp();
-            qn -= 32;
-            if (lane < qn) s_q[warp][lane] = s_q[warp][32 + lane];
-            __syncwarp();
-        }
-    }
-    if (qn > 0) batch(qn);
-}
-
-// Chain rule of rasterize_backward (rasterizer.cpp:251-282) in fp64, one
-// thread per Gaussian, from the warp-reduced raw sums [d_amp[C], d_phase[C],
-// d_alpha, gmx, gmy, ga, gb, gc] (SoA, N each).
-// K3t, one-warp form: one warp per 16x16 tile.  Hits are queued as (Gaussian,
-// cell) entries of all four 8x8 cells of the tile, so a batch of 32 lanes mixes
-// cells and only the tile's last batch runs partly empty (per-cell queues
-// leave one partial batch per cell).  Each lane walks the 64 pixels of its own
-// cell; the tile's gradient is staged per cell with a 2-bank shift between
-// cells, so the four cells' pixel p sit in different banks (one wavefront).
 constexpr int kTb1Stride = 65;  // float2 per staged cell (64 + 1 pad)
 constexpr int kTb1Q = 160;      // queue: < 32 left over + 4 x 32 new entries
 
@@ -1563,11 +1359,7 @@ static void bwd_launch(const RasterWork& rw, const float* d_params, const float2
         const int ty0 = y0 / kTile, ty1 = (y0 + hs - 1) / kTile;
         float* r16 = rw.raw16.as<float>();
         HS_CUDA(cudaMemsetAsync(r16, 0, sizeof(float) * 16 * static_cast<size_t>(rw.n), st));
-#if HS_TILE_BWD_1W
         raster_bwd_tile1w_kernel<C><<<rw.tiles_x * (ty1 - ty0 + 1), 32, 0, st>>>(
-#else
-        raster_bwd_tile_kernel<C><<<rw.tiles_x * (ty1 - ty0 + 1), kFwdThreads, 0, st>>>(
-#endif
             rw.ids.as<uint32_t>(), rw.ranges.as<uint2>(), rw.rec.as<float4>(), rw.shade.as<float4>(),
             rw.p64.as<double>(), rw.n, rw.tiles_x, rw.width, rw.height, d_gf, r16, y0, hs, ty0);
         launch_check("raster_bwd_tile");
