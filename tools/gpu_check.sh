@@ -2,7 +2,7 @@
 # One gpurun call: GPU parity tests, smoke, bench line (+ reference arm), launch list,
 # ncu --set full on the top kernels.   usage: tools/gpu_check.sh TAG [ncu-kernel-regex] [skip] [count]
 TAG=${1:-check}
-KRE=${2:-'raster_bwd_kernel|ssim_loss_kernel|pcols_fwd|pcols_bwd|raster_fwd_kernel|srows_inv|srows_fwd|adan_fused|scatter_ids'}
+KRE=${2:-'raster_bwd_tile1w|raster_bwd_kernel|ssim_loss_kernel|pcols_fwd|pcols_bwd|raster_fwd_kernel|srows_inv|srows_fwd|adan_fused|scatter_ids'}
 SKIP=${3:-22}; CNT=${4:-11}
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/${TAG}_smi.txt 2>&1
