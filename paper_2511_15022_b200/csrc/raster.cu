@@ -631,42 +631,67 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(
                 hit = cell_hit(s_g[j].r0, s_g[j].r1, s_g[j].r2, static_cast<float>(cx0), static_cast<float>(cy0),
                                7.f, 7.f);
             uint32_t mask = __ballot_sync(0xffffffffu, hit);
-            while (mask) {  // warp-uniform: hits in ascending id order
-                const int jj = sub + __ffs(mask) - 1;
-                mask &= mask - 1;
+            // fast fp32 alphas of hit jj for both pixels (rows y, y + 4); band = inside
+            // the error band [cut - tol, cut + tol] (decided exactly afterwards)
+            auto fast = [&](int jj, float& aA, float& aB, bool& bA, bool& bB) {
                 const FwdRec<C>& G = s_g[jj];
                 const float4 r0 = G.r0, r1 = G.r1, r2 = G.r2;
                 const float dx = (fx - r0.x) - r0.z;
                 const float dyA = (fy - r0.y) - r0.w;
                 const float dyB = dyA + 4.f;
-                // Sigma^-1 (dx, dy) for both pixels (rows y, y + 4), then the quadratic forms
+                // Sigma^-1 (dx, dy) for both pixels, then the quadratic forms
                 const float2 i0 = make_float2(r1.x, r1.y), i1 = make_float2(r1.y, r1.z);
                 const float2 eA = f2fma(f2splat(dyA), i1, f2mul(f2splat(dx), i0));
                 const float2 eB = f2fma(f2splat(4.f), i1, eA);
                 const float mA = fmaf(dx, eA.x, dyA * eA.y);
                 const float mB = fmaf(dx, eB.x, dyB * eB.y);
-                // fast fp32 decision outside the error band [cut - tol, cut + tol];
                 // alpha e^{-m/2} = 2^(log2 alpha - m / (2 ln 2))
                 const float lo = r1.w - r2.y, hi = r1.w + r2.y;
-                float aA = mA <= lo ? fminf(0.99f, ex2f(fmaf(mA, kNegHalfLog2e, r2.x))) : 0.f;
-                float aB = mB <= lo ? fminf(0.99f, ex2f(fmaf(mB, kNegHalfLog2e, r2.x))) : 0.f;
-                const bool bandA = mA > lo && mA <= hi, bandB = mB > lo && mB <= hi;
-                if (__any_sync(0xffffffffu, bandA || bandB)) {  // rare: exact fp64 decision
-                    const double* q = p64 + G.id;
-                    if (bandA) {
-                        const float4 e4 = exact_contrib4(q, N, x, y);
-                        aA = e4.w != 0.f ? e4.y : 0.f;
-                    }
-                    if (bandB) {
-                        const float4 e4 = exact_contrib4(q, N, x, y + 4);
-                        aB = e4.w != 0.f ? e4.y : 0.f;
-                    }
+                aA = mA <= lo ? fminf(0.99f, ex2f(fmaf(mA, kNegHalfLog2e, r2.x))) : 0.f;
+                aB = mB <= lo ? fminf(0.99f, ex2f(fmaf(mB, kNegHalfLog2e, r2.x))) : 0.f;
+                bA = mA > lo && mA <= hi;
+                bB = mB > lo && mB <= hi;
+            };
+            auto exact = [&](int jj, float& aA, float& aB, bool bA, bool bB) {  // rare: fp64 decision
+                const double* q = p64 + s_g[jj].id;
+                if (bA) {
+                    const float4 e4 = exact_contrib4(q, N, x, y);
+                    aA = e4.w != 0.f ? e4.y : 0.f;
                 }
+                if (bB) {
+                    const float4 e4 = exact_contrib4(q, N, x, y + 4);
+                    aB = e4.w != 0.f ? e4.y : 0.f;
+                }
+            };
+            auto accum = [&](int jj, float aA, float aB) {
 #pragma unroll
                 for (int c = 0; c < C; ++c) {
-                    const float2 sh = G.sh[c];
+                    const float2 sh = s_g[jj].sh[c];
                     accA[c] = f2fma(f2splat(aA), sh, accA[c]);
                     accB[c] = f2fma(f2splat(aB), sh, accB[c]);
+                }
+            };
+            while (mask) {  // warp-uniform: hits in ascending id order, two per iteration
+                const int j1 = sub + __ffs(mask) - 1;
+                mask &= mask - 1;
+                float a1A, a1B;
+                bool b1A, b1B;
+                fast(j1, a1A, a1B, b1A, b1B);
+                if (mask) {
+                    const int j2 = sub + __ffs(mask) - 1;
+                    mask &= mask - 1;
+                    float a2A, a2B;
+                    bool b2A, b2B;
+                    fast(j2, a2A, a2B, b2A, b2B);
+                    if (__any_sync(0xffffffffu, b1A || b1B || b2A || b2B)) {
+                        exact(j1, a1A, a1B, b1A, b1B);
+                        exact(j2, a2A, a2B, b2A, b2B);
+                    }
+                    accum(j1, a1A, a1B);
+                    accum(j2, a2A, a2B);
+                } else {
+                    if (__any_sync(0xffffffffu, b1A || b1B)) exact(j1, a1A, a1B, b1A, b1B);
+                    accum(j1, a1A, a1B);
                 }
             }
         }
