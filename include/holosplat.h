@@ -242,7 +242,7 @@ hs_status hs_trainer_use_graph(hs_trainer* tr, int enable);
 /* Raster backward form.  Default (0): the per-tile backward with vector
  * atomics into per-Gaussian rows (fastest; the last bits of the gradients
  * depend on the atomic order).  1: the per-Gaussian gather, bit-reproducible
- * run to run.  Row-slab shards always use the gather over their band list. */
+ * run to run (row-slab shards: over their band list). */
 hs_status hs_trainer_set_deterministic(hs_trainer* tr, int enable);
 /* Device event timing of the last (eager) step, ms per kernel slot:
  * [binning, raster_fwd, rows_fwd, cols_fwd, rows_inv, loss, rows_fwd(bwd),

@@ -1370,6 +1370,20 @@ static void bwd_launch(const RasterWork& rw, const float* d_params, const float2
         HS_CUDA(cudaMemsetAsync(work, 0, sizeof(uint32_t), st));  // row-slab rank: only the band's Gaussians; the others' gradients are zero
         const int64_t P = static_cast<int64_t>(rw.n) * (6 + 2 * C);
         HS_CUDA(cudaMemsetAsync(d_grads, 0, sizeof(float) * P, st));
+        if (rw.tile_bwd) {  // the band's tiles (binned for the band only) with the per-tile backward
+            const int ty0 = y0 / kTile, ty1 = (y0 + hs - 1) / kTile;
+            float* r16 = rw.raw16.as<float>();
+            HS_CUDA(cudaMemsetAsync(r16, 0, sizeof(float) * 16 * static_cast<size_t>(rw.n), st));
+            raster_bwd_tile1w_kernel<C><<<rw.tiles_x * (ty1 - ty0 + 1), 32, 0, st>>>(
+                rw.ids.as<uint32_t>(), rw.ranges.as<uint2>(), rw.rec.as<float4>(), rw.shade.as<float4>(),
+                rw.p64.as<double>(), rw.n, rw.tiles_x, rw.width, rw.height, d_gf, r16, y0, hs, ty0);
+            launch_check("raster_bwd_tile");
+            raster_finalize_kernel<C, true, true><<<ceil_div(rw.n, 256), 256, 0, st>>>(
+                rw.n, r16, d_params, rw.width, rw.height, d_grads, d_flags, rw.band_list.as<uint32_t>(),
+                rw.band_n.as<uint32_t>(), rw.shade.as<float4>());
+            launch_check("raster_finalize");
+            return;
+        }
         raster_bwd_kernel<C, 32, true><<<grid, kBwdThreads, 0, st>>>(
             rw.n, rw.rec.as<float4>(), rw.shade.as<float4>(), rw.p64.as<double>(), rw.pbox.as<int4>(), rw.width,
             rw.height, d_gf, rw.raw.as<float>(), y0, hs, rw.band_list.as<uint32_t>(), rw.band_n.as<uint32_t>(), work);

@@ -43,6 +43,7 @@ def run(holo, R, n, c, w, h, L, steps, put=False):
     trs = []
     for r in range(R):
         t = holo.Trainer(gs, w, h, target, masks, dist, spec, 20)
+        t.set_deterministic(True)
         t.set_row_slab(r, R)
         trs.append(t)
     grp = P.LocalSlabGroup(trs, c, h, w, L, put=put)
@@ -134,6 +135,31 @@ def test_slab_step_cfg3_eight_ranks(holo):
     assert ls == pytest.approx(lf, rel=2e-6), (lf, ls)
     assert gerr < GRAD_TOL, gerr
     assert rel_l2(ps[7], pf) < 1e-6
+
+
+def test_slab_step_tile_backward_matches_unsharded(holo):
+    """The default per-tile backward on the row-slab bands (band tile rows
+    only) against the unsharded per-tile backward: the decomposition changes
+    only the atomic and partial-sum order."""
+    from paper_2511_15022_b200 import parallel as P
+    R, n, c, w, h, L = 4, 3000, 3, 256, 160, 2
+    gs, target, masks, dist, spec = scene(holo, n, c, w, h, L)
+    full = holo.Trainer(gs, w, h, target, masks, dist, spec, 20)
+    trs = []
+    for r in range(R):
+        t = holo.Trainer(gs, w, h, target, masks, dist, spec, 20)
+        t.set_row_slab(r, R)
+        trs.append(t)
+    grp = P.LocalSlabGroup(trs, c, h, w, L, put=True)
+    for _ in range(2):
+        full.forward_backward()
+        gfull = full.grads_tensor().cpu().numpy().astype(np.float64)
+        full.apply_update()
+        lf = full.last_loss()[0]
+        ls = grp.step()
+        gslab = trs[0].grads_tensor().cpu().numpy().astype(np.float64)
+        assert ls == pytest.approx(lf, rel=2e-6), (lf, ls)
+        assert rel_l2(gslab, gfull) < GRAD_TOL
 
 
 def test_slab_step_cfg4_eight_ranks(holo):

@@ -43,6 +43,7 @@ def _worker(rank, world, port, q):
     try:
         gs, target, masks, dists, spec = _scene(holo, S)
         tr = holo.Trainer(gs, W, H, target, masks, dists, spec, 10)
+        tr.set_deterministic(True)  # compared with the deterministic full trainer
         tr.set_row_slab(rank, world)
         step = P.SlabShardedStep(tr, C, H, W, L, exchange="put")  # IPC mapping of the peers, graphs on
         losses = []
