@@ -1158,8 +1158,22 @@ __global__ void __launch_bounds__(256) raster_finalize_kernel(int N, const float
         if (g >= N) return;
     }
     const size_t Ns = N;
+    // AoS: the Gaussian's 16-float row as four 16-byte loads
+    float row[AOS ? 16 : 1];
+    if constexpr (AOS) {
+        const float4* r4 = reinterpret_cast<const float4*>(raw + static_cast<size_t>(g) * 16);
+#pragma unroll
+        for (int i = 0; i < (2 * C + 6 + 3) / 4; ++i) {
+            const float4 v = r4[i];
+            row[4 * i] = v.x;
+            row[4 * i + 1] = v.y;
+            row[4 * i + 2] = v.z;
+            row[4 * i + 3] = v.w;
+        }
+    }
     auto R = [&](int k) {
-        return static_cast<double>(AOS ? raw[static_cast<size_t>(g) * 16 + k] : raw[static_cast<size_t>(k) * Ns + g]);
+        if constexpr (AOS) return static_cast<double>(row[k]);
+        else return static_cast<double>(raw[static_cast<size_t>(k) * Ns + g]);
     };
     // (d_amp, d_phase) of channel c: stored (K3), or from sum alpha_eff g_c (K3t):
     // d_amp = cos Sg.re + sin Sg.im, d_phase = amp (cos Sg.im - sin Sg.re)
