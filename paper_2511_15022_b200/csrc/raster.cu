@@ -944,7 +944,7 @@ __device__ __forceinline__ void red_add_v4(float* dst, float a, float b, float c
                  : "memory");
 }
 
-constexpr int kTb1Stride = 65;  // float2 per staged cell (64 + 1 pad)
+constexpr int kTb1Stride = 66;  // float2 per staged cell (64 + 2 pad: 16-byte pixel pairs, 4-bank shift per cell)
 constexpr int kTb1Q = 160;      // queue: < 32 left over + 4 x 32 new entries
 
 template <int C>
@@ -953,7 +953,7 @@ __global__ void __launch_bounds__(32, 16) raster_bwd_tile1w_kernel(
     const float4* __restrict__ shade, const double* __restrict__ p64, int N, int tiles_x, int W, int H,
     const float2* __restrict__ gfield, float* __restrict__ raw16, int y0, int hs, int ty0) {
     static_assert(2 * C + 6 <= 16, "AoS row of 16 floats");
-    __shared__ float2 s_t[C][4 * kTb1Stride];
+    __shared__ __align__(16) float2 s_t[C][4 * kTb1Stride];
     __shared__ uint32_t s_q[kTb1Q];
     const int tile = blockIdx.x + ty0 * tiles_x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
@@ -1030,6 +1030,9 @@ __global__ void __launch_bounds__(32, 16) raster_bwd_tile1w_kernel(
                 const float2 arg = f2fma(m2, kx2, l2a2);
                 const float aGs[2] = {ex2f(arg.x), ex2f(arg.y)};  // alpha e^{-m/2}
                 const float ms[2] = {m2.x, m2.y};
+                float4 g4[C];  // both pixels' gradient per channel: one 16-byte load
+#pragma unroll
+                for (int c = 0; c < C; ++c) g4[c] = *reinterpret_cast<const float4*>(gp + c * 4 * kTb1Stride + k);
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const float m = ms[h], aG = aGs[h], dx = dxk[k + h];
@@ -1038,7 +1041,7 @@ __global__ void __launch_bounds__(32, 16) raster_bwd_tile1w_kernel(
                     const float w = fast ? aG : 0.f;
                     float2 gv[C];
 #pragma unroll
-                    for (int c = 0; c < C; ++c) gv[c] = gp[c * 4 * kTb1Stride + k + h];
+                    for (int c = 0; c < C; ++c) gv[c] = h ? make_float2(g4[c].z, g4[c].w) : make_float2(g4[c].x, g4[c].y);
                     float2 sa = f2mul(S[0], gv[0]);
                     Sg[0] = f2fma(f2splat(w), gv[0], Sg[0]);
 #pragma unroll
