@@ -3,7 +3,7 @@
 import csv, io, json, subprocess, sys
 
 SLOTS = {  # kernel-name fragment -> bench.py stage slots it serves
-    "raster_bwd_kernel": ["raster_bwd"], "raster_fwd_kernel": ["raster_fwd"],
+    "raster_bwd_tile1w": ["raster_bwd"], "raster_fwd_kernel": ["raster_fwd"],
     "ssim_loss_kernel": ["loss_ssim"], "pcols_fwd": ["cols_fwd"], "pcols_bwd": ["cols_bwd"],
     "srows_fwd": ["rows_fwd", "rows_fwd_bwd"], "srows_inv": ["rows_inv", "rows_inv_bwd"],
 }
