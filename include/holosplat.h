@@ -317,6 +317,14 @@ hs_status hs_ctx_comm_destroy(hs_ctx* ctx);
  * lowest flag bit), apply Adan and all-reduce the loss sums.  loss_out
  * (nullable) syncs and receives the global loss; errors as hs_trainer_step. */
 hs_status hs_trainer_sharded_step(hs_trainer* tr, double* loss_out);
+/* Sharded optimizer update (ZeRO-1 style, after a reduce-scatter of the
+ * gradient): the non-finite group bits of grads[begin, end) only (agree on
+ * them across ranks, then), and Adan over params[begin, end) with the
+ * matching moments -- then all-gather the parameters.  Both ranges must
+ * start on a multiple of 4 floats for the vectorised update; the device
+ * step counter and the cosine schedule advance as in hs_trainer_apply_update. */
+hs_status hs_trainer_check_grads_range(hs_trainer* tr, int64_t begin, int64_t end);
+hs_status hs_trainer_apply_update_range(hs_trainer* tr, int64_t begin, int64_t end);
 
 /* holo::Rng(seed).uniform(lo, hi) drawn n times into h_out (rng.hpp; host). */
 hs_status hs_random_uniform(uint64_t seed, int64_t n, double lo, double hi, double* h_out);

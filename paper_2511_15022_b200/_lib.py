@@ -120,6 +120,8 @@ _SIGS = {
     "hs_trainer_reserve_pairs": [C.c_void_p, C.c_int64],
     "hs_trainer_use_graph": [C.c_void_p, C.c_int],
     "hs_trainer_set_deterministic": [C.c_void_p, C.c_int],
+    "hs_trainer_check_grads_range": [C.c_void_p, C.c_int64, C.c_int64],
+    "hs_trainer_apply_update_range": [C.c_void_p, C.c_int64, C.c_int64],
     "hs_ctx_set_deterministic": [C.c_void_p, C.c_int],
     "hs_trainer_set_profiling": [C.c_void_p, C.c_int],
     "hs_trainer_stage_ms": [C.c_void_p, C.POINTER(C.c_double)],

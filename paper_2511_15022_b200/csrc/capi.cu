@@ -671,6 +671,23 @@ hs_status hs_trainer_apply_update(hs_trainer* t) {
     });
 }
 
+hs_status hs_trainer_check_grads_range(hs_trainer* t, int64_t begin, int64_t end) {
+    return guard([&] {
+        group_nonfinite_launch(t->grads.as<float>(), t->P, t->groups, t->flags.as<uint32_t>(), t->ctx->stream, begin,
+                               end);
+    });
+}
+
+hs_status hs_trainer_apply_update_range(hs_trainer* t, int64_t begin, int64_t end) {
+    return guard([&] {
+        require(t->host_step <= t->total_steps, "cosine_lr: step outside [0, total_steps]");
+        adan_fused_launch(t->params.as<float>(), t->grads.as<float>(), t->state.as<float>(), t->P, t->groups,
+                          t->total_steps, 0.98, 0.92, 0.99, 1e-8, t->step.as<int>(), t->flags.as<uint32_t>(),
+                          t->ctx->stream, begin, end);
+        t->host_step += 1;
+    });
+}
+
 static void trainer_launch_step(hs_trainer* t) {
     {
         // cosine_lr(step, steps, ...) throws past the horizon (optimizer.cpp:9-10)

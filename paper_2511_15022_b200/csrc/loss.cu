@@ -544,7 +544,7 @@ __global__ void adan_consts_kernel(AdanGroups G, int total_steps, double b1, dou
 // step's constants.
 template <bool VEC>
 __global__ void adan_fused_kernel(float* __restrict__ p, const float* __restrict__ g,
-                                  float* __restrict__ st, int64_t P, AdanGroups G, int total_steps,
+                                  float* __restrict__ st, int64_t P, int64_t PS, AdanGroups G, int total_steps,
                                   double b1, double b2, double b3, double eps,
                                   int* __restrict__ step, const uint32_t* __restrict__ flags,
                                   unsigned* __restrict__ done, GroupConst* __restrict__ Kc) {
@@ -559,10 +559,12 @@ __global__ void adan_fused_kernel(float* __restrict__ p, const float* __restrict
     __syncthreads();
     const float fb1 = static_cast<float>(b1), fb2 = static_cast<float>(b2), fb3 = static_cast<float>(b3);
     const float feps = static_cast<float>(eps);
+    // state moments of the P elements updated here, at stride PS (the whole
+    // buffer's element count; PS > P when one rank updates its shard only)
     float* m = st;
-    float* v = st + P;
-    float* n = st + 2 * P;
-    float* gp = st + 3 * P;
+    float* v = st + PS;
+    float* n = st + 2 * PS;
+    float* gp = st + 3 * PS;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     if constexpr (VEC) {
         const int64_t P4 = P / 4;
@@ -763,19 +765,29 @@ static unsigned adan_grid(int64_t items) {
 }
 
 void adan_fused_launch(float* params, const float* grads, float* state, int64_t P,
-                       const AdanGroups& g, int total_steps, double b1, double b2, double b3,
-                       double eps, int* d_step, const uint32_t* d_flags, cudaStream_t st) {
-    bool vec = P % 4 == 0;
+                       const AdanGroups& g0, int total_steps, double b1, double b2, double b3,
+                       double eps, int* d_step, const uint32_t* d_flags, cudaStream_t st, int64_t begin,
+                       int64_t end) {
+    // [begin, end): a rank's shard of the flat buffer (end < 0: all of it)
+    if (end < 0) end = P;
+    require(begin >= 0 && begin <= end && end <= P, "adan: update range outside the parameter buffer");
+    const int64_t PS = P;
+    const AdanGroups g = shift_groups(g0, begin, end);
+    params += begin;
+    grads += begin;
+    state += begin;
+    P = end - begin;
+    bool vec = P % 4 == 0 && begin % 4 == 0 && PS % 4 == 0;
     for (int k = 0; k < 6; ++k) vec = vec && g.begin[k] % 4 == 0;
     // d_step holds {loop step, adan t, CTA done counter, pad, GroupConst[6]}
     unsigned* done = reinterpret_cast<unsigned*>(d_step + 2);
     GroupConst* kc = reinterpret_cast<GroupConst*>(d_step + 4);
     if (vec)
-        adan_fused_kernel<true><<<adan_grid(P / 4), 256, 0, st>>>(params, grads, state, P, g, total_steps, b1, b2,
-                                                                  b3, eps, d_step, d_flags, done, kc);
+        adan_fused_kernel<true><<<adan_grid(P / 4), 256, 0, st>>>(params, grads, state, P, PS, g, total_steps, b1,
+                                                                  b2, b3, eps, d_step, d_flags, done, kc);
     else
-        adan_fused_kernel<false><<<grid_for(P, 256), 256, 0, st>>>(params, grads, state, P, g, total_steps, b1, b2,
-                                                                   b3, eps, d_step, d_flags, done, kc);
+        adan_fused_kernel<false><<<grid_for(P, 256), 256, 0, st>>>(params, grads, state, P, PS, g, total_steps, b1,
+                                                                   b2, b3, eps, d_step, d_flags, done, kc);
     launch_check("adan_fused");
 }
 
@@ -815,7 +827,22 @@ __global__ void group_nonfinite_kernel(const float* __restrict__ g, int64_t P, A
 }
 }  // namespace
 
-void group_nonfinite_launch(const float* g, int64_t P, const AdanGroups& G, uint32_t* flags, cudaStream_t st) {
+AdanGroups shift_groups(const AdanGroups& G, int64_t begin, int64_t end) {
+    AdanGroups s = G;
+    for (int k = 0; k < 6; ++k) {
+        s.begin[k] = std::min(std::max(G.begin[k], begin), end) - begin;
+        s.end[k] = std::min(std::max(G.end[k], begin), end) - begin;
+    }
+    return s;
+}
+
+void group_nonfinite_launch(const float* g, int64_t P, const AdanGroups& G0, uint32_t* flags, cudaStream_t st,
+                            int64_t begin, int64_t end) {
+    if (end < 0) end = P;
+    require(begin >= 0 && begin <= end && end <= P, "non-finite check: range outside the gradient buffer");
+    const AdanGroups G = shift_groups(G0, begin, end);
+    g += begin;
+    P = end - begin;
     HS_CUDA(cudaMemsetAsync(flags, 0, sizeof(uint32_t), st));
     if (P == 0) return;
     group_nonfinite_kernel<<<grid_for(P, 256), 256, 0, st>>>(g, P, G, flags);

@@ -84,13 +84,17 @@ void adan_init_consts(const AdanGroups& g, int total_steps, double b1, double b2
 // 1e-2, 1e-3) (pipeline.cpp:254).
 void adan_fused_launch(float* params, const float* grads, float* state, int64_t P,
                        const AdanGroups& g, int total_steps, double b1, double b2, double b3,
-                       double eps, int* d_step, const uint32_t* d_flags, cudaStream_t st);
+                       double eps, int* d_step, const uint32_t* d_flags, cudaStream_t st, int64_t begin = 0,
+                       int64_t end = -1);
+// The groups of [begin, end) of the flat buffer, re-based to begin.
+AdanGroups shift_groups(const AdanGroups& G, int64_t begin, int64_t end);
 // Single group, explicit lr/t (C-ABI hs_adan_step).
 void adan_group_launch(float* params, const float* grads, float* state, int64_t size, int t,
                        double lr, double b1, double b2, double b3, double eps, cudaStream_t st);
 // Non-finite check of a gradient array -> flag word (bit 0).
 void nonfinite_launch(const float* g, int64_t n, uint32_t* flag, cudaStream_t st);
 // Per-group non-finite bits of the summed gradient buffer -> *flags (reset first).
-void group_nonfinite_launch(const float* g, int64_t P, const AdanGroups& G, uint32_t* flags, cudaStream_t st);
+void group_nonfinite_launch(const float* g, int64_t P, const AdanGroups& G, uint32_t* flags, cudaStream_t st,
+                            int64_t begin = 0, int64_t end = -1);
 
 }  // namespace hs

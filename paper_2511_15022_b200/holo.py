@@ -901,6 +901,17 @@ class Trainer:
         ctx_handle()
         check(_lib.load().hs_trainer_check_grads(self.h))
 
+    def check_grads_range(self, begin: int, end: int):
+        """Non-finite group bits of grads[begin, end) only (a rank's shard after a
+        reduce-scatter; agree on them across ranks afterwards)."""
+        ctx_handle()
+        check(_lib.load().hs_trainer_check_grads_range(self.h, int(begin), int(end)))
+
+    def apply_update_range(self, begin: int, end: int):
+        """Adan over params[begin, end) only (sharded update; all-gather after)."""
+        ctx_handle()
+        check(_lib.load().hs_trainer_apply_update_range(self.h, int(begin), int(end)))
+
     def last_loss(self):
         v = C.c_double(0.0)
         k = C.c_int64(0)

@@ -246,6 +246,47 @@ class ChannelShardedStep:
         return combine_loss(float(parts[0]), float(parts[1]), self.C, self.H, self.W, self.L)
 
 
+def update_shard(P: int, rank: int, world: int) -> Tuple[int, int]:
+    """Elements [begin, end) of the flat P-float parameter buffer whose Adan
+    update `rank` owns in a sharded update: equal parts rounded to multiples of
+    4 floats (the vectorised update), the last rank takes the rest."""
+    per = ((P + world - 1) // world + 3) // 4 * 4
+    b = min(rank * per, P)
+    return b, min(b + per, P) if rank < world - 1 else P
+
+
+def sharded_update(tr, group=None):
+    """Reduce-scatter the gradient buffer, update this rank's shard of the
+    parameters (ZeRO-1 style: the Adan moments of the other shards stay
+    untouched and are never read), agree on the first non-finite group over
+    the ranks, all-gather the parameters.  Same result as all-reduce +
+    check_grads + replicated apply_update, with 1/world of the update work."""
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    g = tr.grads_tensor()
+    P = g.numel()
+    parts = [update_shard(P, r, world) for r in range(world)]
+    b, e = parts[rank]
+    # equal shards: reduce-scatter + all-gather (NCCL, or gloo on host tensors);
+    # otherwise all-reduce + per-shard broadcasts (the update stays sharded)
+    even = all(pe - pb == e - b for pb, pe in parts) and P % world == 0 and \
+        (dist.get_backend(group) == "nccl" or not g.is_cuda)
+    if even:
+        out = torch.empty(e - b, dtype=g.dtype, device=g.device)
+        dist.reduce_scatter_tensor(out, g, group=group)
+        g[b:e].copy_(out)
+    else:  # uneven shards: all-reduce (the update below is still sharded)
+        dist.all_reduce(g, op=dist.ReduceOp.SUM, group=group)
+    tr.check_grads_range(b, e)
+    agree_nonfinite(tr, group)
+    tr.apply_update_range(b, e)
+    p = tr.params_tensor()
+    if even:
+        dist.all_gather_into_tensor(p, p[b:e].clone(), group=group)
+    else:
+        for r, (pb, pe) in enumerate(parts):
+            dist.broadcast(p[pb:pe], src=dist.get_global_rank(group, r) if group is not None else r, group=group)
+
+
 def row_slab(H: int, rank: int, world: int) -> Tuple[int, int]:
     """Rows [begin, end) of the canvas owned by `rank` (equal slabs)."""
     if world < 1 or not 0 <= rank < world or H % world:
@@ -274,10 +315,11 @@ class SlabShardedStep:
     No collective library call on the transpose data path.
     """
 
-    def __init__(self, trainer, C, H, W, L, group=None, exchange="nccl"):
+    def __init__(self, trainer, C, H, W, L, group=None, exchange="nccl", shard_update=True):
         self.tr = trainer
         self.C, self.H, self.W, self.L = C, H, W, L
         self.group = group
+        self.shard_update = shard_update  # reduce-scatter / sharded Adan / all-gather
         self.counts = [trainer.slab_counts(e) for e in range(4)]
         self.put = exchange == "put"
         self._mapped = []
@@ -328,11 +370,14 @@ class SlabShardedStep:
             self.tr.slab_stage(4)
         g = self.tr.grads_tensor()
         multi = dist.is_initialized() and dist.get_world_size(self.group) > 1
-        if multi:
-            dist.all_reduce(g, op=dist.ReduceOp.SUM, group=self.group)
-            self.tr.check_grads()
-            agree_nonfinite(self.tr, self.group)
-        self.tr.apply_update()
+        if multi and self.shard_update:
+            sharded_update(self.tr, self.group)
+        else:
+            if multi:
+                dist.all_reduce(g, op=dist.ReduceOp.SUM, group=self.group)
+                self.tr.check_grads()
+                agree_nonfinite(self.tr, self.group)
+            self.tr.apply_update()
         self.watch.post()  # non-finite groups and the peer-put timeout word, every step
         if not with_loss:
             return None
@@ -379,9 +424,10 @@ class LocalSlabGroup:
     the other trainers' receive buffers and signal their device flags), the
     same kernels a multi-GPU run uses over NVLink."""
 
-    def __init__(self, trainers, C, H, W, L, put=False):
+    def __init__(self, trainers, C, H, W, L, put=False, shard_update=True):
         self.trs = list(trainers)
         self.C, self.H, self.W, self.L = C, H, W, L
+        self.shard_update = shard_update
         self.counts = [[t.slab_counts(e) for e in range(4)] for t in self.trs]
         self.put = put
         self.watches = [ErrorWatch(t) for t in self.trs]
@@ -415,11 +461,27 @@ class LocalSlabGroup:
         total = grads[0].clone()
         for g in grads[1:]:
             total += g
-        for g in grads:
-            g.copy_(total)
-        for t in self.trs:
-            t.check_grads()
-            t.apply_update()
+        if self.shard_update:  # the sharded Adan / all-gather of sharded_update
+            R, P = len(self.trs), total.numel()
+            parts = [update_shard(P, r, R) for r in range(R)]
+            for t, g, (b, e) in zip(self.trs, grads, parts):
+                g.copy_(total)  # (every rank keeps the whole sum here, for inspection)
+                t.check_grads_range(b, e)
+            agree_nonfinite_local(self.trs)
+            for t, (b, e) in zip(self.trs, parts):
+                t.apply_update_range(b, e)
+            # all-gather: assemble the shards once, hand the result to every rank
+            full = total  # (the summed gradient is no longer needed)
+            for t, (b, e) in zip(self.trs, parts):
+                full[b:e].copy_(t.params_tensor()[b:e])
+            for t in self.trs:
+                t.params_tensor().copy_(full)
+        else:
+            for g in grads:
+                g.copy_(total)
+            for t in self.trs:
+                t.check_grads()
+                t.apply_update()
         for w in self.watches:
             w.post()
         if not with_loss:

@@ -52,6 +52,7 @@ class NumpySlabTrainer:
         self.send = torch.zeros(size, dtype=torch.float64)
         self.recv = torch.zeros(size, dtype=torch.float64)
         self.grads = torch.zeros(2 * H * W, dtype=torch.float64)
+        self.params = torch.zeros(2 * H * W, dtype=torch.float64)
         self.partial = 0.0
         self.x = field()[self.h0:self.h1]
 
@@ -115,6 +116,16 @@ class NumpySlabTrainer:
     def apply_update(self):
         pass
 
+    # sharded update (parallel.sharded_update): a toy update p -= g on the shard
+    def check_grads_range(self, b, e):
+        pass
+
+    def apply_update_range(self, b, e):
+        self.params[b:e] -= self.grads[b:e]
+
+    def params_tensor(self):
+        return self.params
+
     def loss_partials(self):
         return self.partial, 0.0
 
@@ -135,7 +146,7 @@ def _worker(rank, R, port, q):
         tr = NumpySlabTrainer(rank, R)
         step = P.SlabShardedStep(tr, 1, H, W, 1)
         loss = step.step()
-        q.put((rank, loss, tr.grads.numpy().copy(), tr.u_band, tr.g0))
+        q.put((rank, loss, tr.grads.numpy().copy(), tr.u_band, tr.g0, tr.params.numpy().copy()))
     finally:
         dist.destroy_process_group()
 
@@ -157,12 +168,16 @@ def test_slab_protocol_gloo(R):
     u = np.fft.ifft2(np.fft.fft2(x) * Hf)
     back = np.fft.ifft2(np.fft.fft2(2.0 * u) * np.conj(Hf))
     ssim_free_loss = np.sum(np.abs(u) ** 2)
-    for rank, loss, g, band, g0 in res:
+    full = np.stack([back.real, back.imag], -1).ravel()
+    for rank, loss, g, band, g0, prm in res:
         # P.combine_loss normalises recon_sum by C H W L; undo it
         n = H * W
         assert (loss - 0.005) * n == pytest.approx(ssim_free_loss, rel=1e-12)
-        gc = g.reshape(H, W, 2)
-        np.testing.assert_allclose(gc[..., 0] + 1j * gc[..., 1], back, atol=1e-11)
+        # sharded update: this rank's shard of the gradient is the global sum
+        # (reduce-scatter); every rank holds all updated parameters (all-gather)
+        b, e = P.update_shard(full.size, rank, R)
+        np.testing.assert_allclose(g[b:e], full[b:e], atol=1e-11)
+        np.testing.assert_allclose(prm, -full, atol=1e-11)
         np.testing.assert_allclose(band, u[g0:g0 + band.shape[0]], atol=1e-12)
 
 
@@ -173,3 +188,11 @@ def test_row_slab_and_loss_band():
     assert P.loss_band(2160, 7, 8) == (1880, 2160)
     with pytest.raises(ValueError):
         P.row_slab(1080, 0, 7)
+
+
+def test_update_shards_cover_the_buffer():
+    for P_, R in ((2_400_000, 8), (12, 3), (1000, 7), (5, 4)):
+        parts = [P.update_shard(P_, r, R) for r in range(R)]
+        assert parts[0][0] == 0 and parts[-1][1] == P_
+        for (b0, e0), (b1, e1) in zip(parts, parts[1:]):
+            assert e0 == b1 and (b0 % 4 == 0 or b0 == P_)
