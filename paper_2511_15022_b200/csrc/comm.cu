@@ -42,6 +42,8 @@ struct Nccl {
     ncclResult_t (*CommCount)(const ncclComm_t, int*);
     ncclResult_t (*CommUserRank)(const ncclComm_t, int*);
     ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
+    ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
     ncclResult_t (*GroupStart)();
     ncclResult_t (*GroupEnd)();
     ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
@@ -71,6 +73,8 @@ const Nccl& nccl() {
         api.CommCount = reinterpret_cast<decltype(api.CommCount)>(sym("ncclCommCount"));
         api.CommUserRank = reinterpret_cast<decltype(api.CommUserRank)>(sym("ncclCommUserRank"));
         api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
+        api.ReduceScatter = reinterpret_cast<decltype(api.ReduceScatter)>(sym("ncclReduceScatter"));
+        api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
         api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
         api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
         api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
@@ -222,10 +226,19 @@ hs_status hs_trainer_sharded_step(hs_trainer* t, double* loss_out) {
             trainer_enqueue_fwd_bwd(t, st);
         }
         // gradient sum: everything (planes, slabs) or the geometry groups (channels)
-        // (also at world 1, where the collectives are copies: one code path)
+        // (also at world 1, where the collectives are copies: one code path).
+        // Planes and slabs shard the update ZeRO-1 style when the buffer splits
+        // into equal multiples of 4 floats: reduce-scatter (in place), the
+        // non-finite check and Adan on the own shard, all-gather (in place).
         float* g = t->grads.as<float>();
+        const int64_t shard = t->P / world;
+        const bool sharded = !(channels && !planes && !slabs) && world > 1 && t->P % world == 0 && shard % 4 == 0;
+        const int64_t sb = sharded ? shard * ctx->comm_rank : 0, se = sharded ? sb + shard : t->P;
         {
-            if (channels && !planes && !slabs) {
+            if (sharded) {
+                nccl_check(nccl().ReduceScatter(g, g + sb, static_cast<size_t>(shard), ncclFloat, ncclSum, comm, st),
+                           "ncclReduceScatter");
+            } else if (channels && !planes && !slabs) {
                 const size_t N = t->n;
                 nccl_check(nccl().AllReduce(g, g, 5 * N, ncclFloat, ncclSum, comm, st), "ncclAllReduce");
                 float* opa = g + 5 * N + 2 * N * t->c;
@@ -236,7 +249,7 @@ hs_status hs_trainer_sharded_step(hs_trainer* t, double* loss_out) {
             }
             // the non-finite groups of the SUMMED gradient, then every rank keeps
             // the lowest group any rank saw (channel shards hold rank-local groups)
-            group_nonfinite_launch(g, t->P, t->groups, t->flags.as<uint32_t>(), st);
+            group_nonfinite_launch(g, t->P, t->groups, t->flags.as<uint32_t>(), st, sb, se);
             lowest_group_kernel<<<1, 1, 0, st>>>(t->flags.as<uint32_t>(), word);
             nccl_check(nccl().AllReduce(word, word, 1, ncclUint32, ncclMin, comm, st), "ncclAllReduce");
             apply_group_kernel<<<1, 1, 0, st>>>(word, t->flags.as<uint32_t>());
@@ -250,7 +263,15 @@ hs_status hs_trainer_sharded_step(hs_trainer* t, double* loss_out) {
             loss_combine_kernel<<<1, 1, 0, st>>>(o3, n_el, t->L_total, count);
             launch_check("sharded_step loss");
         }
-        trainer_enqueue_update(t, st);
+        if (sharded) {
+            float* prm = t->params.as<float>();
+            adan_fused_launch(prm, g, t->state.as<float>(), t->P, t->groups, t->total_steps, 0.98, 0.92, 0.99, 1e-8,
+                              t->step.as<int>(), t->flags.as<uint32_t>(), st, sb, se);
+            nccl_check(nccl().AllGather(prm + sb, prm, static_cast<size_t>(shard), ncclFloat, comm, st),
+                       "ncclAllGather");
+        } else {
+            trainer_enqueue_update(t, st);
+        }
         t->host_step += 1;
         if (loss_out) {
             if (slabs && t->s_put) {
