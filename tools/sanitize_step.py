@@ -1,5 +1,5 @@
 """One trainer step (and one 1080p propagation) for compute-sanitizer runs on
-the compile-time planned kernels.  usage: python tools/sanitize_step.py {cfg1|prop1080}"""
+the compile-time planned kernels.  usage: python tools/sanitize_step.py {cfg1|runhost|prop1080}"""
 import os
 import sys
 
@@ -18,6 +18,15 @@ if what == "cfg1":
     tr = holo.Trainer(holo.GaussianSet(n, c, **g), w, h, holo.RealField(c, h, w, wl["target"].astype(np.float32)),
                       wl["masks"], wl["distances"], holo.PropagationSpec(tuple(wl["wavelengths"])), 5)
     print("loss", tr.step())
+elif what == "runhost":  # the per-tile backward (default) + the pipelined host loop at cfg1
+    wl = S.workload("cfg1")
+    cfg = wl["cfg"]
+    c, h, w, n = cfg["channels"], cfg["height"], cfg["width"], cfg["count"]
+    g = {k: np.asarray(v, np.float32).astype(np.float64) for k, v in wl["gaussians"].items()}
+    tr = holo.Trainer(holo.GaussianSet(n, c, **g), w, h, holo.RealField(c, h, w, wl["target"].astype(np.float32)),
+                      wl["masks"], wl["distances"], holo.PropagationSpec(tuple(wl["wavelengths"])), 10)
+    host = torch.from_numpy(tr.params().copy()).pin_memory()
+    print("losses", tr.run_host(host, 3))
 else:
     f = torch.randn((3, 1080, 1920, 2), device="cuda")
     out = holo.propagate_multi_device(f, holo.PropagationSpec(), [3e-3])
