@@ -256,6 +256,13 @@ def rasterize_forward(s: GaussianSet, width: int, height: int) -> ComplexField:
     return ComplexField.from_device(rasterize_forward_device(s.to_device(), s.count, s.channels, width, height))
 
 
+def set_backward_deterministic(on: bool = True):
+    """Backward form of the stand-alone rasterize_backward on this context:
+    the bit-reproducible per-Gaussian gather (default) or the per-tile backward
+    with vector atomics (hs_ctx_set_deterministic)."""
+    check(_lib.load().hs_ctx_set_deterministic(ctx_handle(), int(on)))
+
+
 def rasterize_backward_device(params: torch.Tensor, n, c, grad_field: torch.Tensor) -> torch.Tensor:
     cc, h, w, _ = grad_field.shape
     if cc != c:

@@ -100,21 +100,38 @@ def test_high_opacity_tails(holo, ref):
     assert abs(a.real[0, 32, 39]) > 0.0
 
 
+@pytest.mark.parametrize("tile", [False, True])
 @pytest.mark.parametrize("seed,n,c,w,h", CASES)
-def test_rasterize_backward(holo, ref, seed, n, c, w, h):
+def test_rasterize_backward(holo, ref, seed, n, c, w, h, tile):
+    """Both backward forms (the deterministic gather and the per-tile backward
+    with atomics) on canvases that are not whole tiles (partial edge cells)."""
     g = f32(S.random_set(seed, n, c))
     hs, rs = sets(holo, ref, g, n, c)
     wre = S.random_real(seed + 40, c, h, w, -1.0, 1.0).astype(np.float32).astype(np.float64)
     wim = S.random_real(seed + 41, c, h, w, -1.0, 1.0).astype(np.float32).astype(np.float64)
-    a = holo.rasterize_backward(hs, holo.RealField(c, h, w, wre), holo.RealField(c, h, w, wim))
+    holo.set_backward_deterministic(not tile)
+    try:
+        a = holo.rasterize_backward(hs, holo.RealField(c, h, w, wre), holo.RealField(c, h, w, wim))
+    finally:
+        holo.set_backward_deterministic(True)
     b = ref.rasterize_backward(rs, wre, wim)
     for k in ref.GROUPS:
         err = rel_l2(getattr(a, k), getattr(b, k))
         assert err <= GRAD_TOL, (k, err)
 
 
-def test_saturation_gates(holo):
-    # test_rasterizer.cpp:225-244
+@pytest.mark.parametrize("tile", [False, True])
+def test_saturation_gates(holo, tile):
+    # test_rasterizer.cpp:225-244 (both backward forms: saturated pixels take the
+    # per-tile backward's exact pass)
+    holo.set_backward_deterministic(not tile)
+    try:
+        _saturation_gates(holo)
+    finally:
+        holo.set_backward_deterministic(True)
+
+
+def _saturation_gates(holo):
     g = dict(pre_position=np.zeros(2), pre_scale=np.log([10.0, 10.0]), rotation=np.zeros(1),
              amplitude=np.ones(1), phase=np.array([0.3]), pre_opacity=np.array([8.0]))
     hs = holo.GaussianSet(1, 1, **f32(g))
