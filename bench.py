@@ -585,7 +585,7 @@ def main():
     spec = holo.PropagationSpec(tuple(wl["wavelengths"]))
     trained_extra = max(0, args.trained_steps - args.warmup - args.steps) if args.trained_steps > 0 else 0
     total = args.warmup + args.steps + trained_extra + (args.steps if args.trained_steps > 0 else 0) \
-        + 2 * args.e2e_steps + args.profile_steps + 10
+        + 2 * args.e2e_steps + args.profile_steps + args.steps + 10
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
         tr = holo.Trainer(gs, w, h, target, wl["masks"], wl["distances"], spec, total_steps=total)
@@ -612,6 +612,18 @@ def main():
         clocks = sampler.stop()
         ms = e0.elapsed_time(e1) / args.steps
         loss, pairs = tr.last_loss()
+        # per-step distribution (median and p10/p90): the same
+        # graph step, K more times, an event pair around each launch
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        for a0, a1 in evs:
+            a0.record(stream)
+            tr.step(sync_loss=False)
+            a1.record(stream)
+        torch.cuda.synchronize()
+        per = np.array([a0.elapsed_time(a1) for a0, a1 in evs])
+        dist_ms = {"median": float(np.median(per)), "p10": float(np.percentile(per, 10)),
+                   "p90": float(np.percentile(per, 90)), "n": len(per)}
 
         trained = None
         if args.trained_steps > 0:
@@ -707,6 +719,7 @@ def main():
         "step_roofline": {"bound": "hbm", "achieved": step_gbs, "peak": peak, "unit": "GB/s",
                           "frac": step_gbs / peak, "algorithmic_bytes_per_step": B,
                           "formula": "C(13+12L)8HW + LHW + 592N + 24K (SURVEY §8d)"},
+        "step_ms_dist": dist_ms,
         "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
         "e2e": {"value": world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 4 * P,
                 "d2h_bytes_per_step": 4 * P + 12,

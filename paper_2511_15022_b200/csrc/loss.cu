@@ -542,8 +542,9 @@ __global__ void adan_consts_kernel(AdanGroups G, int total_steps, double b1, dou
 // loads/stores.  The last CTA to finish advances the device step counter (not
 // after a non-finite gradient: the reference aborts) and precomputes the next
 // step's constants.
+constexpr int kAdanMinBlocks = 4;
 template <bool VEC>
-__global__ void adan_fused_kernel(float* __restrict__ p, const float* __restrict__ g,
+__global__ void __launch_bounds__(256, kAdanMinBlocks) adan_fused_kernel(float* __restrict__ p, const float* __restrict__ g,
                                   float* __restrict__ st, int64_t P, int64_t PS, AdanGroups G, int total_steps,
                                   double b1, double b2, double b3, double eps,
                                   int* __restrict__ step, const uint32_t* __restrict__ flags,
@@ -757,11 +758,16 @@ void intensity_launch(const float2* f, int64_t count, float* out, cudaStream_t s
     launch_check("intensity");
 }
 
-// float4 work items per thread of the fused Adan (2 measured best: 28.7 -> 26.6 us at cfg2)
+// float4 work items per thread of the fused Adan: a resident grid
+// (kAdanMinBlocks CTAs per SM, grid-stride), no partial last wave
 static unsigned adan_grid(int64_t items) {
-    constexpr int per = 2;
-    const int64_t b = (items + 256LL * per - 1) / (256LL * per);
-    return static_cast<unsigned>(std::max<int64_t>(1, b));
+    static const int sms = [] {
+        int dev = 0;
+        HS_CUDA(cudaGetDevice(&dev));
+        return sm_count(dev);
+    }();
+    const int64_t b = (items + 255) / 256;
+    return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(b, static_cast<int64_t>(sms) * kAdanMinBlocks)));
 }
 
 void adan_fused_launch(float* params, const float* grads, float* state, int64_t P,

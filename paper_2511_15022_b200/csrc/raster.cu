@@ -465,23 +465,6 @@ __device__ __forceinline__ void warp_bitonic(uint32_t* __restrict__ seg, int n, 
     }
 }
 
-__global__ void __launch_bounds__(256) segment_sort_warp_kernel(const uint2* __restrict__ ranges, int tiles,
-                                                                uint32_t* __restrict__ ids,
-                                                                const uint32_t* __restrict__ status) {
-    const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (t >= tiles || status[1]) return;
-    const uint2 r = ranges[t];
-    const int n = static_cast<int>(r.y - r.x);
-    if (n <= 1 || n > kWarpSeg) return;
-    // network size by segment length (tight binning: ~100 ids per tile at cfg2)
-    if (n <= 32) warp_bitonic<1>(ids + r.x, n, lane);
-    else if (n <= 64) warp_bitonic<2>(ids + r.x, n, lane);
-    else if (n <= 128) warp_bitonic<4>(ids + r.x, n, lane);
-    else if (n <= 256) warp_bitonic<8>(ids + r.x, n, lane);
-    else warp_bitonic<16>(ids + r.x, n, lane);
-}
-
 __device__ void sort_big_tile(const uint2 r, uint32_t* __restrict__ ids, uint32_t* __restrict__ scratch) {
     __shared__ uint32_t s[kSegSmem];
     const int n = static_cast<int>(r.y - r.x);
@@ -503,20 +486,31 @@ __device__ void sort_big_tile(const uint2 r, uint32_t* __restrict__ ids, uint32_
     for (int i = threadIdx.x; i < n; i += blockDim.x) ids[r.x + i] = g[i];
 }
 
-// Tiles with more than kWarpSeg ids (rare): each CTA checks 256 tiles at once
-// and sorts the big ones it found, one after another.
+// Warp per tile; tiles with more than kWarpSeg ids (rare) are collected and
+// then sorted one after another by the whole CTA (8 tiles per CTA).
 __global__ void __launch_bounds__(256) segment_sort_kernel(const uint2* __restrict__ ranges, int tiles,
                                                            uint32_t* __restrict__ ids, uint32_t* __restrict__ scratch,
                                                            const uint32_t* __restrict__ status) {
-    __shared__ int s_big[256];
+    __shared__ int s_big[8];
     __shared__ int s_nbig;
-    if (status[1]) return;
+    if (status[1]) return;  // grid-uniform
     if (threadIdx.x == 0) s_nbig = 0;
     __syncthreads();
-    const int t = blockIdx.x * 256 + threadIdx.x;
+    const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
     if (t < tiles) {
         const uint2 r = ranges[t];
-        if (static_cast<int>(r.y - r.x) > kWarpSeg) s_big[atomicAdd(&s_nbig, 1)] = t;
+        const int n = static_cast<int>(r.y - r.x);
+        // network size by segment length (tight binning: ~100 ids per tile at cfg2)
+        if (n > kWarpSeg) {
+            if (lane == 0) s_big[atomicAdd(&s_nbig, 1)] = t;
+        } else if (n > 1) {
+            if (n <= 32) warp_bitonic<1>(ids + r.x, n, lane);
+            else if (n <= 64) warp_bitonic<2>(ids + r.x, n, lane);
+            else if (n <= 128) warp_bitonic<4>(ids + r.x, n, lane);
+            else if (n <= 256) warp_bitonic<8>(ids + r.x, n, lane);
+            else warp_bitonic<16>(ids + r.x, n, lane);
+        }
     }
     __syncthreads();
     const int nb = s_nbig;
@@ -1334,11 +1328,8 @@ void RasterWork::project_and_bin(const float* d_params, cudaStream_t st, cudaEve
                                                          tcount.as<uint32_t>(), stat, ids.as<uint32_t>(), band_ty0,
                                                          band_ty1, lst, lst_n, tight ? trows.as<uint4>() : nullptr);
     launch_check("scatter_ids");
-    segment_sort_warp_kernel<<<ceil_div(tiles, 8), 256, 0, st>>>(ranges.as<uint2>(), tiles, ids.as<uint32_t>(),
-                                                                  stat);
-    launch_check("segment_sort_warp");
-    segment_sort_kernel<<<ceil_div(tiles, 256), 256, 0, st>>>(ranges.as<uint2>(), tiles, ids.as<uint32_t>(),
-                                                               scratch.as<uint32_t>(), stat);
+    segment_sort_kernel<<<ceil_div(tiles, 8), 256, 0, st>>>(ranges.as<uint2>(), tiles, ids.as<uint32_t>(),
+                                                             scratch.as<uint32_t>(), stat);
     launch_check("segment_sort");
     if (shading_ready) {  // amplitude/phase uploaded: shade now (else project_kernel did)
         HS_CUDA(cudaStreamWaitEvent(st, shading_ready, 0));
