@@ -22,6 +22,7 @@
 //    the 7 + 2C partial sums and lane 0 applies the fp64 chain rule.  No
 //    atomics: the gradients are deterministic.
 #include <cstdlib>
+#include <type_traits>
 
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
@@ -962,7 +963,12 @@ __global__ void __launch_bounds__(32, 16) raster_bwd_tile1w_kernel(
         const float2* src = gfield + (ok ? static_cast<unsigned>(y - y0) * static_cast<unsigned>(W) + x : 0u);
 #pragma unroll
         for (int c = 0; c < C; ++c)
-            s_t[c][cell * kTb1Stride + p] = ok ? __ldg(src + static_cast<size_t>(c) * cs) : make_float2(0.f, 0.f);
+        {
+            float* sc = reinterpret_cast<float*>(&s_t[c][cell * kTb1Stride]) + (p >> 1) * 4 + (p & 1);
+            const float2 v = ok ? __ldg(src + static_cast<size_t>(c) * cs) : make_float2(0.f, 0.f);
+            sc[0] = v.x;
+            sc[2] = v.y;
+        }
     }
     // cells with at least one valid pixel (warp-uniform)
     unsigned cell_ok = 0u;
@@ -995,103 +1001,142 @@ __global__ void __launch_bounds__(32, 16) raster_bwd_tile1w_kernel(
         const float M = act ? cut + tol : -1.f;  // idle lanes never pass m <= M
         const float Mfast = cut - tol;
         const double* q = p64 + g;
-        float2 Sg[C];
+        // per channel: (sum over even pixels, sum over odd pixels) of alpha_eff g re / im
+        float2 SgRe[C], SgIm[C];
 #pragma unroll
-        for (int c = 0; c < C; ++c) Sg[c] = make_float2(0.f, 0.f);
+        for (int c = 0; c < C; ++c) SgRe[c] = SgIm[c] = make_float2(0.f, 0.f);
         float2 T1 = make_float2(0.f, 0.f), T2 = make_float2(0.f, 0.f);
         float QA = 0.f, T3 = 0.f;
-        const float2* gcell = &s_t[0][cell * kTb1Stride];
+        const float* gcell = reinterpret_cast<const float*>(&s_t[0][cell * kTb1Stride]);  // pair-transposed
         float dxk[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) dxk[k] = (static_cast<float>(cx0 + k) - r0.x) - r0.z;
         const float2 i00_2 = f2splat(i00), kx2 = f2splat(kNegHalfLog2e), l2a2 = f2splat(l2a);
-        uint32_t band_lo = 0u, band_hi = 0u;
+        // the row terms of m = (i00 dx + bq) dx + cq: shared by the fast walk and
+        // the exact pass so that both see the same fp32 m for a pixel
+        auto row_terms = [&](float dy, float& bq, float& cq) {
+            bq = 2.f * i01 * dy;
+            cq = i11 * dy * dy;
+        };
+        // pixel fast/band decision (same in both passes): fast = inside the
+        // cutoff by more than the tolerance and not saturating (SAT: the lane
+        // can saturate at all); band = could contribute but not fast
+        auto decide = [&](auto satc, float m, float aG, float Mfr, float Mr, bool& fast, bool& band) {
+            fast = m <= Mfr;
+            if constexpr (decltype(satc)::value) fast = fast && aG < 0.99f - 1e-5f;
+            band = m <= Mr && !fast;
+        };
+        // rows holding a band pixel (bit r): redone exactly afterwards
+        uint32_t rowmask = 0u;
+        auto walk = [&](auto satc) {
 #pragma unroll 1
-        for (int r = 0; r < 8; ++r) {
-            const int y = cy0 + r;
-            const bool rowok = y >= ylo && y < yhi;
-            const float Mr = rowok ? M : -1.f, Mfr = rowok ? Mfast : -1.f;
-            const float dy = (static_cast<float>(y) - r0.y) - r0.w;
-            const float2 bq2 = f2splat(2.f * i01 * dy), cq2 = f2splat(i11 * dy * dy);  // m = (i00 dx + bq) dx + cq
-            const float2* gp = gcell + (r << 3);
-            uint32_t rowband = 0u;
-            float R0 = 0.f;
-            float2 R12 = make_float2(0.f, 0.f);
+            for (int r = 0; r < 8; ++r) {
+                const int y = cy0 + r;
+                const bool rowok = y >= ylo && y < yhi;
+                const float Mr = rowok ? M : -1.f, Mfr = rowok ? Mfast : -1.f;
+                const float dy = (static_cast<float>(y) - r0.y) - r0.w;
+                float bq, cq;
+                row_terms(dy, bq, cq);
+                const float2 bq2 = f2splat(bq), cq2 = f2splat(cq);
+                const float* gp = gcell + (r << 4);
+                bool rb = false;
+                float2 R0p = make_float2(0.f, 0.f), R1p = R0p, R2p = R0p;
 #pragma unroll
-            for (int k = 0; k < 8; k += 2) {
-                const float2 dxp = make_float2(dxk[k], dxk[k + 1]);
-                const float2 m2 = f2fma(f2fma(i00_2, dxp, bq2), dxp, cq2);
-                const float2 arg = f2fma(m2, kx2, l2a2);
-                const float aGs[2] = {ex2f(arg.x), ex2f(arg.y)};  // alpha e^{-m/2}
-                const float ms[2] = {m2.x, m2.y};
-                float4 g4[C];  // both pixels' gradient per channel: one 16-byte load
+                for (int k = 0; k < 8; k += 2) {
+                    const float2 dxp = make_float2(dxk[k], dxk[k + 1]);
+                    const float2 m2 = f2fma(f2fma(i00_2, dxp, bq2), dxp, cq2);
+                    const float2 arg = f2fma(m2, kx2, l2a2);
+                    const float aG0 = ex2f(arg.x), aG1 = ex2f(arg.y);  // alpha e^{-m/2}
+                    // the pixel pair's gradient per channel: (re0, re1, im0, im1), one 16-byte load
+                    float4 g4[C];
 #pragma unroll
-                for (int c = 0; c < C; ++c) g4[c] = *reinterpret_cast<const float4*>(gp + c * 4 * kTb1Stride + k);
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const float m = ms[h], aG = aGs[h], dx = dxk[k + h];
-                    const bool fast = m <= Mfr && aG < 0.99f - 1e-5f;
-                    rowband |= (m <= Mr && !fast) ? (1u << (k + h)) : 0u;
-                    const float w = fast ? aG : 0.f;
-                    float2 gv[C];
-#pragma unroll
-                    for (int c = 0; c < C; ++c) gv[c] = h ? make_float2(g4[c].z, g4[c].w) : make_float2(g4[c].x, g4[c].y);
-                    float2 sa = f2mul(S[0], gv[0]);
-                    Sg[0] = f2fma(f2splat(w), gv[0], Sg[0]);
+                    for (int c = 0; c < C; ++c) g4[c] = *reinterpret_cast<const float4*>(gp + c * 8 * kTb1Stride + 2 * k);
+                    bool f0, b0, f1, b1;
+                    decide(satc, m2.x, aG0, Mfr, Mr, f0, b0);
+                    decide(satc, m2.y, aG1, Mfr, Mr, f1, b1);
+                    rb = rb || b0 || b1;
+                    const float2 w = make_float2(f0 ? aG0 : 0.f, f1 ? aG1 : 0.f);
+                    float2 sx = f2mul(f2splat(S[0].x), make_float2(g4[0].x, g4[0].y));
+                    float2 sy = f2mul(f2splat(S[0].y), make_float2(g4[0].z, g4[0].w));
+                    SgRe[0] = f2fma(w, make_float2(g4[0].x, g4[0].y), SgRe[0]);
+                    SgIm[0] = f2fma(w, make_float2(g4[0].z, g4[0].w), SgIm[0]);
 #pragma unroll
                     for (int c = 1; c < C; ++c) {
-                        Sg[c] = f2fma(f2splat(w), gv[c], Sg[c]);
+                        const float2 gre = make_float2(g4[c].x, g4[c].y), gim = make_float2(g4[c].z, g4[c].w);
+                        SgRe[c] = f2fma(w, gre, SgRe[c]);
+                        SgIm[c] = f2fma(w, gim, SgIm[c]);
+                        sx = f2fma(f2splat(S[c].x), gre, sx);
+                        sy = f2fma(f2splat(S[c].y), gim, sy);
+                    }
+                    const float2 qv = f2mul(f2add(sx, sy), w);
+                    R0p = f2add(R0p, qv);
+                    R1p = f2fma(qv, dxp, R1p);
+                    R2p = f2fma(qv, f2mul(dxp, dxp), R2p);
+                }
+                const float R0 = R0p.x + R0p.y;
+                const float2 R12 = make_float2(R1p.x + R1p.y, R2p.x + R2p.y);
+                QA += R0;
+                T1 = f2add(T1, make_float2(R12.x, dy * R0));
+                T2 = f2add(T2, make_float2(R12.y, dy * dy * R0));
+                T3 = fmaf(dy, R12.x, T3);
+                if (rb) rowmask |= 1u << r;
+            }
+        };
+        // a Gaussian whose peak alpha is clearly below the cap cannot saturate
+        // (alpha e^{-m/2} <= alpha, with margin for the fp32 m near 0)
+        const bool sat_free = __all_sync(0xffffffffu, !act || alpha * 1.001f < 0.99f - 1e-5f);
+        if (sat_free) walk(std::false_type{});
+        else walk(std::true_type{});
+        // rare: the exact fp64 decision for the band pixels of the flagged rows
+        // (rasterizer.cpp:220-228)
+        if (__any_sync(0xffffffffu, rowmask != 0u)) {
+            const int xmax = W - cx0;
+            for (uint32_t rm = rowmask; rm; rm &= rm - 1) {
+                const int r = __ffs(rm) - 1, y = cy0 + r;
+                const float dy = (static_cast<float>(y) - r0.y) - r0.w;
+                float bq, cq;
+                row_terms(dy, bq, cq);
+                for (int k = 0; k < 8; ++k) {
+                    if (k >= xmax) break;  // outside the canvas
+                    const float dx = dxk[k];
+                    const float m = fmaf(fmaf(i00, dx, bq), dx, cq);
+                    const float aG = ex2f(fmaf(m, kNegHalfLog2e, l2a));
+                    bool fast, band;
+                    decide(std::true_type{}, m, aG, Mfast, M, fast, band);  // rows of the mask are valid rows
+                    if (!band) continue;
+                    const int pix = (r << 3) + k, x = cx0 + k;
+                    const float4 e4 = exact_contrib4(q, N, x, y);
+                    if (e4.w == 0.f) continue;
+                    const float w = e4.y, qv0 = e4.z != 0.f ? 0.f : alpha * e4.x;
+                    float2 gv[C];
+                    const float* gq = gcell + (pix >> 1) * 4 + (pix & 1);
+#pragma unroll
+                    for (int c = 0; c < C; ++c) gv[c] = make_float2(gq[c * 8 * kTb1Stride], gq[c * 8 * kTb1Stride + 2]);
+                    float2 sa = f2mul(S[0], gv[0]);
+                    SgRe[0].x = fmaf(w, gv[0].x, SgRe[0].x);
+                    SgIm[0].x = fmaf(w, gv[0].y, SgIm[0].x);
+#pragma unroll
+                    for (int c = 1; c < C; ++c) {
+                        SgRe[c].x = fmaf(w, gv[c].x, SgRe[c].x);
+                        SgIm[c].x = fmaf(w, gv[c].y, SgIm[c].x);
                         sa = f2fma(S[c], gv[c], sa);
                     }
-                    const float qv = (sa.x + sa.y) * w;
-                    R0 += qv;
-                    R12 = f2fma(f2splat(qv), make_float2(dx, dx * dx), R12);
+                    const float qv = (sa.x + sa.y) * qv0;
+                    QA += qv;
+                    const float2 dxy = make_float2(dx, dy);
+                    const float2 t = f2mul(f2splat(qv), dxy);
+                    T1 = f2add(T1, t);
+                    T2 = f2fma(t, dxy, T2);
+                    T3 = fmaf(t.x, dy, T3);
                 }
-            }
-            QA += R0;
-            T1 = f2add(T1, make_float2(R12.x, dy * R0));
-            T2 = f2add(T2, make_float2(R12.y, dy * dy * R0));
-            T3 = fmaf(dy, R12.x, T3);
-            if (r < 4) band_lo |= rowband << (r << 3);
-            else band_hi |= rowband << ((r - 4) << 3);
-        }
-        // rare: the exact fp64 decision for the flagged pixels (rasterizer.cpp:220-228)
-        if (__any_sync(0xffffffffu, (band_lo | band_hi) != 0u)) {
-            const int xmax = W - cx0;
-            for (uint64_t bm = (static_cast<uint64_t>(band_hi) << 32) | band_lo; bm; bm &= bm - 1) {
-                const int pix = __ffsll(static_cast<long long>(bm)) - 1;
-                const int k = pix & 7, y = cy0 + (pix >> 3), x = cx0 + k;
-                if (k >= xmax) continue;  // outside the canvas
-                const float4 e4 = exact_contrib4(q, N, x, y);
-                if (e4.w == 0.f) continue;
-                const float dx = (static_cast<float>(x) - r0.x) - r0.z;
-                const float dy = (static_cast<float>(y) - r0.y) - r0.w;
-                const float w = e4.y, qv0 = e4.z != 0.f ? 0.f : alpha * e4.x;
-                float2 gv[C];
-#pragma unroll
-                for (int c = 0; c < C; ++c) gv[c] = gcell[c * 4 * kTb1Stride + pix];
-                float2 sa = f2mul(S[0], gv[0]);
-                Sg[0] = f2fma(f2splat(w), gv[0], Sg[0]);
-#pragma unroll
-                for (int c = 1; c < C; ++c) {
-                    Sg[c] = f2fma(f2splat(w), gv[c], Sg[c]);
-                    sa = f2fma(S[c], gv[c], sa);
-                }
-                const float qv = (sa.x + sa.y) * qv0;
-                QA += qv;
-                const float2 dxy = make_float2(dx, dy);
-                const float2 t = f2mul(f2splat(qv), dxy);
-                T1 = f2add(T1, t);
-                T2 = f2fma(t, dxy, T2);
-                T3 = fmaf(t.x, dy, T3);
             }
         }
         if (act) {
             float v[16];
 #pragma unroll
             for (int c = 0; c < C; ++c) {
-                v[c] = Sg[c].x;
-                v[C + c] = Sg[c].y;
+                v[c] = SgRe[c].x + SgRe[c].y;
+                v[C + c] = SgIm[c].x + SgIm[c].y;
             }
             v[2 * C + 0] = alpha > 0.f ? QA / alpha : 0.f;
             v[2 * C + 1] = fmaf(i00, T1.x, i01 * T1.y);
