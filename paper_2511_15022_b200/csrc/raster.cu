@@ -561,11 +561,14 @@ __device__ __noinline__ float4 exact_contrib4(const double* __restrict__ q, size
 }
 
 // ---------------------------------------------------------------------------
-// K2: forward.  One CTA per 16x16 tile, 8 warps, each warp a 4-row x 8-col
-// cell.  The tile's sorted Gaussian list is staged in shared memory 256 at a
-// time; lane j of a warp tests Gaussian j of a 32-batch against the warp's
-// cell (exact row-band ellipse bound, conservative), the ballot is walked in
-// ascending order and every lane evaluates its pixel.
+// K2: forward.  One CTA per 16x16 tile, 4 warps, each warp an 8x8 cell (a
+// lane owns two pixels of a column).  The tile's sorted Gaussian list is
+// staged in shared memory 128 at a time; the staging thread of a Gaussian
+// tests it against the tile's four cells (exact row-band ellipse bound,
+// conservative) and stores the cell bits with Sigma^-1 repacked as aligned
+// pairs and the cutoff band precomputed; each warp ballots its cell's bit over
+// a 32-batch, walks the hits in ascending order and every lane evaluates its
+// pixels.
 // ---------------------------------------------------------------------------
 constexpr int kFwdThreads = 128;  // 4 warps per 16x16 tile, each an 8x8 cell
 constexpr int kFwdBatch = 128;
@@ -574,8 +577,10 @@ constexpr int kFwdBatch = 128;
 // staged Gaussian of the forward kernel (shared memory)
 template <int C>
 struct alignas(16) FwdRec {
-    float4 r0, r1, r2;  // projection record (raster.cu K0)
-    float2 sh[C];       // (amp cos, amp sin) per channel
+    float4 r0;     // projection record r0 (centre, split)
+    float4 iq;     // (i00, i01, i01, i11): both rows of Sigma^-1 as aligned pairs
+    float4 q;      // (cut - tol, cut + tol, log2 alpha, bits: cells of the tile it can reach)
+    float2 sh[C];  // (amp cos, amp sin) per channel
     uint32_t id;
 };
 
@@ -609,9 +614,17 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(
             const uint32_t g = ids[base + threadIdx.x];
             FwdRec<C>& d = s_g[threadIdx.x];
             d.id = g;
-            d.r0 = rec[g];
-            d.r1 = rec[static_cast<size_t>(N) + g];
-            d.r2 = rec[2 * static_cast<size_t>(N) + g];
+            const float4 r0 = rec[g], r1 = rec[static_cast<size_t>(N) + g], r2 = rec[2 * static_cast<size_t>(N) + g];
+            // the cells (warps) of this tile the Gaussian can reach
+            uint32_t cm = 0u;
+#pragma unroll
+            for (int cl = 0; cl < 4; ++cl)
+                if (cell_hit(r0, r1, r2, static_cast<float>(tx * kTile + (cl & 1) * 8),
+                             static_cast<float>(ty * kTile + (cl >> 1) * 8), 7.f, 7.f))
+                    cm |= 1u << cl;
+            d.r0 = r0;
+            d.iq = make_float4(r1.x, r1.y, r1.y, r1.z);
+            d.q = make_float4(r1.w - r2.y, r1.w + r2.y, r2.x, __uint_as_float(cm));
 #pragma unroll
             for (int c = 0; c < C; ++c) {
                 const float4 sh = shade[static_cast<size_t>(c) * N + g];
@@ -622,28 +635,26 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(
         for (int sub = 0; sub < cnt; sub += 32) {
             const int j = sub + lane;
             bool hit = false;
-            if (j < cnt)
-                hit = cell_hit(s_g[j].r0, s_g[j].r1, s_g[j].r2, static_cast<float>(cx0), static_cast<float>(cy0),
-                               7.f, 7.f);
+            if (j < cnt) hit = (__float_as_uint(s_g[j].q.w) >> warp) & 1u;
             uint32_t mask = __ballot_sync(0xffffffffu, hit);
             // fast fp32 alphas of hit jj for both pixels (rows y, y + 4); band = inside
             // the error band [cut - tol, cut + tol] (decided exactly afterwards)
             auto fast = [&](int jj, float& aA, float& aB, bool& bA, bool& bB) {
                 const FwdRec<C>& G = s_g[jj];
-                const float4 r0 = G.r0, r1 = G.r1, r2 = G.r2;
+                const float4 r0 = G.r0, iq = G.iq, q = G.q;
                 const float dx = (fx - r0.x) - r0.z;
                 const float dyA = (fy - r0.y) - r0.w;
                 const float dyB = dyA + 4.f;
                 // Sigma^-1 (dx, dy) for both pixels, then the quadratic forms
-                const float2 i0 = make_float2(r1.x, r1.y), i1 = make_float2(r1.y, r1.z);
+                const float2 i0 = make_float2(iq.x, iq.y), i1 = make_float2(iq.z, iq.w);
                 const float2 eA = f2fma(f2splat(dyA), i1, f2mul(f2splat(dx), i0));
                 const float2 eB = f2fma(f2splat(4.f), i1, eA);
                 const float mA = fmaf(dx, eA.x, dyA * eA.y);
                 const float mB = fmaf(dx, eB.x, dyB * eB.y);
                 // alpha e^{-m/2} = 2^(log2 alpha - m / (2 ln 2))
-                const float lo = r1.w - r2.y, hi = r1.w + r2.y;
-                aA = mA <= lo ? fminf(0.99f, ex2f(fmaf(mA, kNegHalfLog2e, r2.x))) : 0.f;
-                aB = mB <= lo ? fminf(0.99f, ex2f(fmaf(mB, kNegHalfLog2e, r2.x))) : 0.f;
+                const float lo = q.x, hi = q.y;
+                aA = mA <= lo ? fminf(0.99f, ex2f(fmaf(mA, kNegHalfLog2e, q.z))) : 0.f;
+                aB = mB <= lo ? fminf(0.99f, ex2f(fmaf(mB, kNegHalfLog2e, q.z))) : 0.f;
                 bA = mA > lo && mA <= hi;
                 bB = mB > lo && mB <= hi;
             };
