@@ -193,16 +193,33 @@ struct PairTf {
     float2 qx;       // (bx mx0^2, bx mx1^2)
     float2 inband;   // 1 / 0 per column of the |mx| band limit
     int mx0, mx1;
+    bool simple;     // no aperture, every |my| in band, q < 1/32 down the whole column
 };
-template <bool CONJ>
+
+// The pair's column constants; simple when every row takes the series branch
+// (q grows with |my|, whose wrapped maximum is N/2).
+template <int N>
+__device__ __forceinline__ PairTf pair_tf(const TfConst& t, int mx0, int mx1) {
+    PairTf p;
+    p.mx0 = mx0;
+    p.mx1 = mx1;
+    const float f0 = static_cast<float>(mx0), f1 = static_cast<float>(mx1);
+    p.qx = make_float2(t.bx * f0 * f0, t.bx * f1 * f1);
+    p.inband = make_float2(abs(mx0) <= t.mx_max ? 1.f : 0.f, abs(mx1) <= t.mx_max ? 1.f : 0.f);
+    const float fy = static_cast<float>(N / 2);
+    const float2 qm = f2add(p.qx, f2splat(t.by * fy * fy));
+    p.simple = !(t.a4 > 0.0) && t.my_max >= N / 2 && qm.x < 0.03125f && qm.y < 0.03125f;
+    return p;
+}
+template <bool CONJ, bool SIMPLE = false>
 __device__ __forceinline__ void transfer_pair(const TfConst& t, const PairTf& p, int my, float2& hc, float2& hs) {
-    if (abs(my) > t.my_max) {
+    if (!SIMPLE && abs(my) > t.my_max) {
         hc = hs = make_float2(0.f, 0.f);
         return;
     }
     const float fmy = static_cast<float>(my);
     const float2 q = f2add(p.qx, f2splat(t.by * fmy * fmy));
-    if (t.a4 > 0.0 || q.x >= 0.03125f || q.y >= 0.03125f) {
+    if (!SIMPLE && (t.a4 > 0.0 || q.x >= 0.03125f || q.y >= 0.03125f)) {
         const float2 h0 = transfer_fast<CONJ>(t, p.mx0, my), h1 = transfer_fast<CONJ>(t, p.mx1, my);
         hc = make_float2(h0.x, h1.x);
         hs = make_float2(h0.y, h1.y);
@@ -242,14 +259,8 @@ __device__ __forceinline__ void pcol_single(const ColArgs& a, const float2* __re
     float2* dst = a.out + (static_cast<size_t>(plane) * a.ntiles + tile) * tile_elems - shift;
     const TfConst t = a.tf[c];
     const int pp = tid % NP;
-    PairTf ptf;
-    ptf.mx0 = wrapped((a.tile0 + tile) * CC + 2 * pp, a.Px);
-    ptf.mx1 = wrapped((a.tile0 + tile) * CC + 2 * pp + 1, a.Px);
-    {
-        const float f0 = static_cast<float>(ptf.mx0), f1 = static_cast<float>(ptf.mx1);
-        ptf.qx = make_float2(t.bx * f0 * f0, t.bx * f1 * f1);
-        ptf.inband = make_float2(abs(ptf.mx0) <= t.mx_max ? 1.f : 0.f, abs(ptf.mx1) <= t.mx_max ? 1.f : 0.f);
-    }
+    const PairTf ptf = pair_tf<N>(t, wrapped((a.tile0 + tile) * CC + 2 * pp, a.Px),
+                                  wrapped((a.tile0 + tile) * CC + 2 * pp + 1, a.Px));
     pfft::run<N, NP, NT, -1, pfft::Half, pfft::Full>(
         smem4, tw, tid, RAD{},
         pfft::in_fn([&](int i, int p) {
@@ -258,7 +269,8 @@ __device__ __forceinline__ void pcol_single(const ColArgs& a, const float2* __re
         }),
         pfft::out_map([&](int i, int, pfft::C2 v) {
             float2 hc, hs;
-            transfer_pair<CONJ>(t, ptf, wrapped(i, N), hc, hs);
+            if (ptf.simple) transfer_pair<CONJ, true>(t, ptf, wrapped(i, N), hc, hs);
+            else transfer_pair<CONJ>(t, ptf, wrapped(i, N), hc, hs);
             // (re + i im)(hc + i hs) per column
             return pfft::C2{f2sub(f2mul(v.re, hc), f2mul(v.im, hs)), f2fma(v.im, hc, f2mul(v.re, hs))};
         }));
@@ -312,14 +324,8 @@ __device__ __forceinline__ void pcol_tile(float4* work, float4* stage_buf, uint6
     constexpr int CC = 4, NP = 2;
     const int tid = threadIdx.x, pp = tid % NP;
     const int tile = t % ntiles;
-    PairTf ptf;
-    ptf.mx0 = wrapped((tile0 + tile) * CC + 2 * pp, Px);
-    ptf.mx1 = wrapped((tile0 + tile) * CC + 2 * pp + 1, Px);
-    {
-        const float f0 = static_cast<float>(ptf.mx0), f1 = static_cast<float>(ptf.mx1);
-        ptf.qx = make_float2(tf.bx * f0 * f0, tf.bx * f1 * f1);
-        ptf.inband = make_float2(abs(ptf.mx0) <= tf.mx_max ? 1.f : 0.f, abs(ptf.mx1) <= tf.mx_max ? 1.f : 0.f);
-    }
+    const PairTf ptf = pair_tf<N>(tf, wrapped((tile0 + tile) * CC + 2 * pp, Px),
+                                  wrapped((tile0 + tile) * CC + 2 * pp + 1, Px));
     mbar_wait(bar, parity);
     const float4* stg = stage_buf - oy * NP;  // row i of the padded column
     pfft::run<N, NP, NT, -1, pfft::Half, pfft::Full>(
@@ -330,7 +336,8 @@ __device__ __forceinline__ void pcol_tile(float4* work, float4* stage_buf, uint6
         }),
         pfft::out_map([tf, ptf](int i, int, pfft::C2 v) {
             float2 hc, hs;
-            transfer_pair<CONJ>(tf, ptf, wrapped(i, N), hc, hs);
+            if (ptf.simple) transfer_pair<CONJ, true>(tf, ptf, wrapped(i, N), hc, hs);
+            else transfer_pair<CONJ>(tf, ptf, wrapped(i, N), hc, hs);
             return pfft::C2{f2sub(f2mul(v.re, hc), f2mul(v.im, hs)), f2fma(v.im, hc, f2mul(v.re, hs))};
         }));
     // the staging buffer is free (the forward FFT ended with a barrier): prefetch tile tn
@@ -450,14 +457,8 @@ __global__ void __launch_bounds__(NT, MINB) pcols_slab_kernel(ColArgs a, const f
     load_peers(sc, peers);
     __syncthreads();
     const TfConst tf = a.tf[c];
-    PairTf ptf;
-    ptf.mx0 = wrapped((a.tile0 + tl) * CC + 2 * pp, a.Px);
-    ptf.mx1 = wrapped((a.tile0 + tl) * CC + 2 * pp + 1, a.Px);
-    {
-        const float f0 = static_cast<float>(ptf.mx0), f1 = static_cast<float>(ptf.mx1);
-        ptf.qx = make_float2(tf.bx * f0 * f0, tf.bx * f1 * f1);
-        ptf.inband = make_float2(abs(ptf.mx0) <= tf.mx_max ? 1.f : 0.f, abs(ptf.mx1) <= tf.mx_max ? 1.f : 0.f);
-    }
+    const PairTf ptf = pair_tf<N>(tf, wrapped((a.tile0 + tl) * CC + 2 * pp, a.Px),
+                                  wrapped((a.tile0 + tl) * CC + 2 * pp + 1, a.Px));
     mbar_wait(bar, 0u);
     const float4* stg = stage_buf - oy * NP;
     pfft::run<N, NP, NT, -1, pfft::Half, pfft::Full>(
@@ -468,7 +469,8 @@ __global__ void __launch_bounds__(NT, MINB) pcols_slab_kernel(ColArgs a, const f
         }),
         pfft::out_map([tf, ptf](int i, int, pfft::C2 v) {
             float2 hc, hs;
-            transfer_pair<CONJ>(tf, ptf, wrapped(i, N), hc, hs);
+            if (ptf.simple) transfer_pair<CONJ, true>(tf, ptf, wrapped(i, N), hc, hs);
+            else transfer_pair<CONJ>(tf, ptf, wrapped(i, N), hc, hs);
             return pfft::C2{f2sub(f2mul(v.re, hc), f2mul(v.im, hs)), f2fma(v.im, hc, f2mul(v.re, hs))};
         }));
     float2* lout = a.out + static_cast<size_t>(t) * H * CC;
