@@ -144,6 +144,51 @@ def _saturation_gates(holo):
     assert gr.amplitude[0] != 0.0
 
 
+def _knife_edge_set(c):
+    """A Gaussian whose cutoff ellipse passes exactly through pixel centres:
+    centre (32, 32) (pre-position 0 on a 64x64 canvas), Sigma = 2.5 I (scale
+    sqrt(2.4) plus the 0.1 covariance epsilon) and alpha = e^5 / 255, so
+    mahal = d^2 / 2.5 = 10 = 2 ln(255 alpha) for the pixels at distance 5
+    ((3, 4), (5, 0), ...): the fp32 fast paths see them inside the error band
+    and the fp64 decision of rasterizer.cpp:164-169 / :220-228 settles them.
+    A second, high-opacity Gaussian (alpha ~ 0.9997, saturating near its centre)
+    shares the tile, so a warp holds both the saturating and the band case.
+    (The reference keeps the distance-5 pixels: alpha_eff = 1/255 there, so a
+    fast path that dropped or mis-weighted them would miss the 1e-6 bar.)"""
+    a = np.exp(5.0) / 255.0
+    g = dict(pre_position=np.array([0.0, 0.0, np.arctanh(38 / 32 - 1), np.arctanh(29 / 32 - 1)]),
+             pre_scale=np.log(np.array([np.sqrt(2.4) - 0.1] * 2 + [2.0, 1.5])),
+             rotation=np.array([0.0, 0.4]),
+             amplitude=np.linspace(0.3, 0.9, 2 * c), phase=np.linspace(-1.0, 2.0, 2 * c),
+             pre_opacity=np.array([np.log(a / (1 - a)), 8.0]))
+    return g
+
+
+@pytest.mark.parametrize("c", [1, 3])
+@pytest.mark.parametrize("tile", [False, True])
+def test_band_pixels_decided_exactly(holo, ref, c, tile):
+    g = f32(_knife_edge_set(c))
+    # the fp32 mahalanobis distance of the distance-5 pixels lies inside the
+    # band around the cutoff, i.e. the exact passes are exercised
+    s2 = (np.float32(np.exp(np.float32(g["pre_scale"][0]))) + np.float32(0.1)) ** 2 + np.float32(0.1)
+    m = np.float32(25.0) / np.float32(s2)
+    assert abs(float(m) - 10.0) < 1e-5
+    hs, rs = sets(holo, ref, g, 2, c)
+    a = holo.rasterize_forward(hs, 64, 64)
+    re, im = ref.rasterize_forward(rs, 64, 64)
+    assert np.max(np.abs(a.real - re)) <= 1e-6 and np.max(np.abs(a.imag - im)) <= 1e-6
+    wre = S.random_real(7, c, 64, 64, -1.0, 1.0).astype(np.float32).astype(np.float64)
+    wim = S.random_real(8, c, 64, 64, -1.0, 1.0).astype(np.float32).astype(np.float64)
+    holo.set_backward_deterministic(not tile)
+    try:
+        gr = holo.rasterize_backward(hs, holo.RealField(c, 64, 64, wre), holo.RealField(c, 64, 64, wim))
+    finally:
+        holo.set_backward_deterministic(True)
+    want = ref.rasterize_backward(rs, wre, wim)
+    for k in ref.GROUPS:
+        assert rel_l2(getattr(gr, k), getattr(want, k)) <= 1e-5, k
+
+
 def spec_for(holo, ref, channels, pad=2, aperture=0.0):
     wl = S.WAVELENGTHS[channels]
     return (holo.PropagationSpec(wl, 3.74e-6, pad, aperture), ref.PropagationSpec(wl, 3.74e-6, pad, aperture))
