@@ -934,10 +934,14 @@ __global__ void __launch_bounds__(kBwdThreads, MINB) raster_bwd_kernel(
 // candidate against the four cells (the forward's row-band bound) and the hits
 // are compacted into one queue of (Gaussian, cell) entries.  Every 32 queued
 // entries run as one batch with LANE = (GAUSSIAN, CELL): the lane walks the 64
-// pixels of its cell (gradient values from shared memory, the cells staged
-// with a 2-bank shift so the lanes' reads take one wavefront; no global
-// gathers), evaluates its Gaussian there with the same fast/exact decision as
-// K3 and accumulates the 7 + 2C partial sums in registers.  Only the tile's
+// pixels of its cell row by row (gradient values from shared memory, staged
+// pair-transposed -- (re0, re1, im0, im1) per pixel pair and channel, cells at
+// a 4-bank shift -- so a pixel pair is one 16-byte load per channel and its
+// weights, Sigma S.g and moments run as packed fp32x2; no global gathers),
+// evaluates its Gaussian there with the fast fp32 decision (rows holding a
+// pixel inside the error band, or a saturating one, are flagged and their
+// band pixels redone with the fp64 decision afterwards, as K3) and
+// accumulates the 7 + 2C partial sums in registers.  Only the tile's
 // last batch runs partly empty.  The sums over the cell go to the Gaussian's
 // row of an AoS [N][16] buffer with 16-byte vector atomics
 // (red.global.add.v4.f32): the reduction over the cell's pixels happens in
