@@ -585,7 +585,7 @@ def main():
     spec = holo.PropagationSpec(tuple(wl["wavelengths"]))
     trained_extra = max(0, args.trained_steps - args.warmup - args.steps) if args.trained_steps > 0 else 0
     total = args.warmup + args.steps + trained_extra + (args.steps if args.trained_steps > 0 else 0) \
-        + 2 * args.e2e_steps + args.profile_steps + args.steps + 10
+        + 2 * args.e2e_steps + args.profile_steps + args.steps + 11
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
         tr = holo.Trainer(gs, w, h, target, wl["masks"], wl["distances"], spec, total_steps=total)
@@ -669,16 +669,20 @@ def main():
         torch.cuda.synchronize()
         e2e_s = (time.perf_counter() - t0) / args.e2e_steps
 
-        # per-kernel profile: eager steps with events at every kernel boundary
+        # kernels per step: one eager step (every kernel a counted launch)
         tr.use_graph(False)
+        l0 = holo.kernel_launch_count()
+        tr.step(sync_loss=False)
+        per_step_launches = holo.kernel_launch_count() - l0
+        # per-stage profile: graph-replayed steps whose graph also holds an event
+        # record at every stage boundary (the same kernels, no host enqueue gaps)
+        tr.use_graph(True)
         tr.set_profiling(True)
         stages = {}
-        l0 = holo.kernel_launch_count()
         for i in range(args.profile_steps):
             tr.step(sync_loss=False)
             for k, v in tr.stage_ms().items():
                 stages.setdefault(k, []).append(v)
-        per_step_launches = (holo.kernel_launch_count() - l0) / max(args.profile_steps, 1)
         stage_ms = {k: float(np.median(v)) for k, v in stages.items()}
 
     if world > 1:

@@ -244,10 +244,13 @@ hs_status hs_trainer_use_graph(hs_trainer* tr, int enable);
  * depend on the atomic order).  1: the per-Gaussian gather, bit-reproducible
  * run to run (row-slab shards: over their band list). */
 hs_status hs_trainer_set_deterministic(hs_trainer* tr, int enable);
-/* Device event timing of the last (eager) step, ms per kernel slot:
+/* Device event timing of the last step, ms per kernel slot:
  * [binning, raster_fwd, rows_fwd, cols_fwd, rows_inv, loss, rows_fwd(bwd),
- *  cols_bwd, rows_inv(bwd), raster_bwd, adan, total].  Needs profiling on and
- * graphs off. */
+ *  cols_bwd, rows_inv(bwd), raster_bwd, adan, total].  Needs profiling on.
+ * With graphs on, profiled steps replay a separate step graph that holds the
+ * stage event records (no host enqueue gaps in the stage times); with graphs
+ * off the events are recorded eagerly (also by forward_backward +
+ * apply_update). */
 hs_status hs_trainer_set_profiling(hs_trainer* tr, int enable);
 hs_status hs_trainer_stage_ms(hs_trainer* tr, double* out12);
 int hs_trainer_step_count(hs_trainer* tr);

@@ -330,17 +330,17 @@ static void launch_forward(AsmWork& w, const float2* d_in, float2* d_out, cudaSt
     RowArgs r{d_in, w.T1.as<float2>(), w.W, w.H, w.Px, w.ox, w.ntiles, 1.f, w.plan_x, w.twx_ptr};
     rows_fwd_kernel<CC><<<w.C * w.H, 256, w.smem_rows, st>>>(r);
     launch_check("rows_fwd");
-    if (ev) HS_CUDA(cudaEventRecord(ev[0], st));
+    if (ev) HS_CUDA(cudaEventRecordWithFlags(ev[0], st, cudaEventRecordExternal));
     ColArgs c{w.T1.as<float2>(), w.T2.as<float2>(), w.C, w.H, w.Py, w.Px, w.oy, w.ntiles, w.L,
               w.plan_y, w.twy_ptr, w.tf.as<TfConst>()};
     cols_fwd_kernel<CC><<<dim3(w.ntiles, w.C), 256, w.smem_cols, st>>>(c);
     launch_check("cols_fwd");
-    if (ev) HS_CUDA(cudaEventRecord(ev[1], st));
+    if (ev) HS_CUDA(cudaEventRecordWithFlags(ev[1], st, cudaEventRecordExternal));
     RowArgs ri{w.T2.as<float2>(), d_out, w.W, w.H, w.Px, w.ox, w.ntiles,
                static_cast<float>(1.0 / (static_cast<double>(w.Px) * w.Py)), w.plan_x, w.twx_ptr};
     rows_inv_kernel<CC><<<w.L * w.C * w.H, 256, w.smem_rows, st>>>(ri);
     launch_check("rows_inv");
-    if (ev) HS_CUDA(cudaEventRecord(ev[2], st));
+    if (ev) HS_CUDA(cudaEventRecordWithFlags(ev[2], st, cudaEventRecordExternal));
 }
 
 template <int CC>
@@ -350,17 +350,17 @@ static void launch_backward(AsmWork& w, const float2* d_grads, float2* d_out, cu
               w.twx_ptr};
     rows_fwd_kernel<CC><<<w.L * w.C * w.H, 256, w.smem_rows, st>>>(r);
     launch_check("rows_fwd");
-    if (ev) HS_CUDA(cudaEventRecord(ev[0], st));
+    if (ev) HS_CUDA(cudaEventRecordWithFlags(ev[0], st, cudaEventRecordExternal));
     ColArgs c{w.T2.as<float2>(), w.T1.as<float2>(), w.C, w.H, w.Py, w.Px, w.oy, w.ntiles, w.L,
               w.plan_y, w.twy_ptr, w.tf.as<TfConst>()};
     cols_bwd_kernel<CC><<<dim3(w.ntiles, w.C), 256, w.smem_cols, st>>>(c);
     launch_check("cols_bwd");
-    if (ev) HS_CUDA(cudaEventRecord(ev[1], st));
+    if (ev) HS_CUDA(cudaEventRecordWithFlags(ev[1], st, cudaEventRecordExternal));
     RowArgs ri{w.T1.as<float2>(), d_out, w.W, w.H, w.Px, w.ox, w.ntiles,
                static_cast<float>(1.0 / (static_cast<double>(w.Px) * w.Py)), w.plan_x, w.twx_ptr};
     rows_inv_kernel<CC><<<w.C * w.H, 256, w.smem_rows, st>>>(ri);
     launch_check("rows_inv");
-    if (ev) HS_CUDA(cudaEventRecord(ev[2], st));
+    if (ev) HS_CUDA(cudaEventRecordWithFlags(ev[2], st, cudaEventRecordExternal));
 }
 
 void asm_forward(AsmWork& w, const float2* d_in, float2* d_out, cudaStream_t st, cudaEvent_t* ev) {

@@ -898,17 +898,17 @@ bool static_forward(AsmWork& w, const float2* d_in, float2* d_out, cudaStream_t 
     RowArgs r{d_in, w.T1.as<float2>(), w.W, w.H, w.Px, w.ox, w.ntiles, 1.f, w.plan_x, nullptr};
     p->row.fwd<<<(rows1 + p->row.rb - 1) / p->row.rb, p->row.nt, rs, st>>>(r, rows1, w.stw_x);
     launch_check("srows_fwd");
-    if (ev) HS_CUDA(cudaEventRecord(ev[0], st));
+    if (ev) HS_CUDA(cudaEventRecordWithFlags(ev[0], st, cudaEventRecordExternal));
     ColArgs c{w.T1.as<float2>(), w.T2.as<float2>(), w.C, w.H, w.Py, w.Px, w.oy, w.ntiles, w.L, w.plan_y, nullptr,
               w.tf.as<TfConst>()};
     launch_cols(p, w, false, c, st);
-    if (ev) HS_CUDA(cudaEventRecord(ev[1], st));
+    if (ev) HS_CUDA(cudaEventRecordWithFlags(ev[1], st, cudaEventRecordExternal));
     const int rows2 = w.L * w.C * w.H;
     RowArgs ri{w.T2.as<float2>(), d_out, w.W, w.H, w.Px, w.ox, w.ntiles,
                static_cast<float>(1.0 / (static_cast<double>(w.Px) * w.Py)), w.plan_x, nullptr};
     p->row.inv<<<(rows2 + p->row.rb - 1) / p->row.rb, p->row.nt, rs, st>>>(ri, rows2, w.stw_x);
     launch_check("srows_inv");
-    if (ev) HS_CUDA(cudaEventRecord(ev[2], st));
+    if (ev) HS_CUDA(cudaEventRecordWithFlags(ev[2], st, cudaEventRecordExternal));
     return true;
 }
 
@@ -920,17 +920,17 @@ bool static_backward(AsmWork& w, const float2* d_grads, float2* d_out, cudaStrea
     RowArgs r{d_grads, w.T2.as<float2>(), w.W, w.H, w.Px, w.ox, w.ntiles, 1.f, w.plan_x, nullptr};
     p->row.fwd<<<(rows1 + p->row.rb - 1) / p->row.rb, p->row.nt, rs, st>>>(r, rows1, w.stw_x);
     launch_check("srows_fwd");
-    if (ev) HS_CUDA(cudaEventRecord(ev[0], st));
+    if (ev) HS_CUDA(cudaEventRecordWithFlags(ev[0], st, cudaEventRecordExternal));
     ColArgs c{w.T2.as<float2>(), w.T1.as<float2>(), w.C, w.H, w.Py, w.Px, w.oy, w.ntiles, w.L, w.plan_y, nullptr,
               w.tf.as<TfConst>()};
     launch_cols(p, w, true, c, st);
-    if (ev) HS_CUDA(cudaEventRecord(ev[1], st));
+    if (ev) HS_CUDA(cudaEventRecordWithFlags(ev[1], st, cudaEventRecordExternal));
     const int rows2 = w.C * w.H;
     RowArgs ri{w.T1.as<float2>(), d_out, w.W, w.H, w.Px, w.ox, w.ntiles,
                static_cast<float>(1.0 / (static_cast<double>(w.Px) * w.Py)), w.plan_x, nullptr};
     p->row.inv<<<(rows2 + p->row.rb - 1) / p->row.rb, p->row.nt, rs, st>>>(ri, rows2, w.stw_x);
     launch_check("srows_inv");
-    if (ev) HS_CUDA(cudaEventRecord(ev[2], st));
+    if (ev) HS_CUDA(cudaEventRecordWithFlags(ev[2], st, cudaEventRecordExternal));
     return true;
 }
 

@@ -449,9 +449,9 @@ extern "C" hs_status hs_adan_step(hs_ctx* ctx, const hs_adan_config* cfg, const 
 // 3 rows_fwd, 4 cols_fwd, 5 rows_inv, 6 loss, 7 rows_fwd(bwd), 8 cols_bwd,
 // 9 rows_inv(bwd), 10 raster_bwd, 11 adan.
 void hs::trainer_enqueue_fwd_bwd(hs_trainer* t, cudaStream_t st, cudaEvent_t shading_ready) {
-    const bool prof = t->profiling && !t->use_graph;
+    const bool prof = t->mark_events;
     auto mark = [&](int i) {
-        if (prof) HS_CUDA(cudaEventRecord(t->ev[i], st));
+        if (prof) HS_CUDA(cudaEventRecordWithFlags(t->ev[i], st, cudaEventRecordExternal));  // external: kept as a graph node
     };
     mark(0);
     HS_CUDA(cudaMemsetAsync(t->flags.p, 0, sizeof(uint32_t), st));
@@ -475,7 +475,7 @@ void hs::trainer_enqueue_fwd_bwd(hs_trainer* t, cudaStream_t st, cudaEvent_t sha
 void hs::trainer_enqueue_update(hs_trainer* t, cudaStream_t st) {
     adan_fused_launch(t->params.as<float>(), t->grads.as<float>(), t->state.as<float>(), t->P, t->groups,
                       t->total_steps, 0.98, 0.92, 0.99, 1e-8, t->step.as<int>(), t->flags.as<uint32_t>(), st);
-    if (t->profiling && !t->use_graph) HS_CUDA(cudaEventRecord(t->ev[11], st));
+    if (t->mark_events) HS_CUDA(cudaEventRecordWithFlags(t->ev[11], st, cudaEventRecordExternal));
 }
 
 static void trainer_raise(hs_trainer* t, uint32_t flags, const uint32_t* stat);
@@ -598,32 +598,26 @@ uint32_t* hs_trainer_flags_ptr(hs_trainer* t) { return t->flags.as<uint32_t>(); 
 int64_t hs_trainer_param_count(hs_trainer* t) { return t->P; }
 int hs_trainer_step_count(hs_trainer* t) { return t->host_step; }
 
+// Every captured graph of the trainer (they bake in buffer addresses and the
+// backward form): dropped when either changes, re-captured on next use.
+static void drop_graphs(hs_trainer* t) {
+    for (cudaGraphExec_t* g : {&t->graph, &t->prof_graph, &t->host_graph, &t->slab_graph, &t->run_graph0,
+                               &t->run_graph}) {
+        if (*g) cudaGraphExecDestroy(*g);
+        *g = nullptr;
+    }
+}
+
 hs_status hs_trainer_reserve_pairs(hs_trainer* t, int64_t cap) {
     return guard([&] {
         t->rw.reserve_pairs(cap);
-        if (t->graph) {
-            cudaGraphExecDestroy(t->graph);
-            t->graph = nullptr;
-        }
-        if (t->slab_graph) {
-            cudaGraphExecDestroy(t->slab_graph);
-            t->slab_graph = nullptr;
-        }
-        if (t->host_graph) {
-            cudaGraphExecDestroy(t->host_graph);
-            t->host_graph = nullptr;
-        }
+        drop_graphs(t);
     });
 }
 
 hs_status hs_trainer_use_graph(hs_trainer* t, int enable) {
     t->use_graph = enable != 0;
-    if (!t->use_graph) {
-        for (cudaGraphExec_t* g : {&t->graph, &t->host_graph, &t->slab_graph}) {
-            if (*g) cudaGraphExecDestroy(*g);
-            *g = nullptr;
-        }
-    }
+    if (!t->use_graph) drop_graphs(t);
     return HS_OK;
 }
 
@@ -631,10 +625,7 @@ hs_status hs_trainer_set_deterministic(hs_trainer* t, int enable) {
     const bool tile = enable == 0;
     if (t->rw.tile_bwd != tile) {
         t->rw.tile_bwd = tile;
-        for (cudaGraphExec_t* g : {&t->graph, &t->host_graph, &t->slab_graph, &t->run_graph0, &t->run_graph}) {
-            if (*g) cudaGraphExecDestroy(*g);
-            *g = nullptr;
-        }
+        drop_graphs(t);
     }
     return HS_OK;
 }
@@ -651,7 +642,14 @@ hs_status hs_trainer_set_profiling(hs_trainer* t, int enable) {
 hs_status hs_trainer_forward_backward(hs_trainer* t) {
     return guard([&] {
         require(t->host_step <= t->total_steps, "cosine_lr: step outside [0, total_steps]");
-        trainer_enqueue_fwd_bwd(t, t->ctx->stream);
+        t->mark_events = t->profiling;  // eager split step: stage events as the plain step
+        try {
+            trainer_enqueue_fwd_bwd(t, t->ctx->stream);
+        } catch (...) {
+            t->mark_events = false;
+            throw;
+        }
+        t->mark_events = false;
     });
 }
 
@@ -666,7 +664,9 @@ hs_status hs_trainer_check_grads(hs_trainer* t) {
 
 hs_status hs_trainer_apply_update(hs_trainer* t) {
     return guard([&] {
+        t->mark_events = t->profiling;
         trainer_enqueue_update(t, t->ctx->stream);
+        t->mark_events = false;
         t->host_step += 1;
     });
 }
@@ -693,8 +693,17 @@ static void trainer_launch_step(hs_trainer* t) {
         // cosine_lr(step, steps, ...) throws past the horizon (optimizer.cpp:9-10)
         require(t->host_step <= t->total_steps, "cosine_lr: step outside [0, total_steps]");
         cudaStream_t st = t->ctx->stream;
+        // profiling: the stage events are recorded by this step only (eagerly,
+        // or as event-record nodes of a separate step graph, so that the
+        // stage times carry no host enqueue gaps)
+        struct Marks {
+            hs_trainer* t;
+            ~Marks() { t->mark_events = false; }
+        } marks{t};
+        t->mark_events = t->profiling;
         if (t->use_graph) {
-            if (!t->graph) {
+            cudaGraphExec_t& ge = t->profiling ? t->prof_graph : t->graph;
+            if (!ge) {
                 cudaStream_t cap_st = st;
                 bool own = false;
                 if (cap_st == nullptr) {  // legacy stream cannot be captured
@@ -713,11 +722,11 @@ static void trainer_launch_step(hs_trainer* t) {
                     throw;
                 }
                 HS_CUDA(cudaStreamEndCapture(cap_st, &g));
-                HS_CUDA(cudaGraphInstantiate(&t->graph, g, 0));
+                HS_CUDA(cudaGraphInstantiate(&ge, g, 0));
                 HS_CUDA(cudaGraphDestroy(g));
                 if (own) HS_CUDA(cudaStreamDestroy(cap_st));
             }
-            HS_CUDA(cudaGraphLaunch(t->graph, st));
+            HS_CUDA(cudaGraphLaunch(ge, st));
             note_launch(0);
         } else {
             trainer_enqueue_fwd_bwd(t, st);
@@ -970,7 +979,7 @@ hs_status hs_trainer_loss_partials(hs_trainer* t, double* out2) {
 
 hs_status hs_trainer_stage_ms(hs_trainer* t, double* out12) {
     return guard([&] {
-        require(t->profiling && !t->use_graph, "trainer: stage timing needs profiling on and graphs off");
+        require(t->profiling, "trainer: stage timing needs profiling on");
         HS_CUDA(cudaEventSynchronize(t->ev[11]));
         for (int i = 0; i < 11; ++i) {
             float ms = 0.f;

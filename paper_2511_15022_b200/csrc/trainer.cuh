@@ -54,6 +54,8 @@ struct hs_trainer {
     int loss_slots = 0;
     bool use_graph = false;
     cudaGraphExec_t graph = nullptr;
+    cudaGraphExec_t prof_graph = nullptr;  // the step graph with the stage-timing event records
+    bool mark_events = false;              // record the stage events while enqueuing (profiled step)
     bool profiling = false;
     cudaEvent_t ev[12] = {};  // profiling: start + after each of the 11 kernel slots
     // host-resident step (hs_trainer_step_host): copy stream, fork/join events,
@@ -94,6 +96,7 @@ struct hs_trainer {
     int s_loss_slots = 0;
     ~hs_trainer() {
         if (graph) cudaGraphExecDestroy(graph);
+        if (prof_graph) cudaGraphExecDestroy(prof_graph);
         if (host_graph) cudaGraphExecDestroy(host_graph);
         if (run_graph0) cudaGraphExecDestroy(run_graph0);
         if (run_graph) cudaGraphExecDestroy(run_graph);

@@ -397,6 +397,33 @@ def test_trainer_graph_replay_matches_eager(holo):
     assert np.array_equal(a.params(), b.params())
 
 
+def test_profiled_graph_step_matches_and_times_stages(holo):
+    """Profiling with graphs on replays a second step graph that also records
+    the stage events: the same results as the plain graph, and stage times
+    that are positive and add up to the step."""
+    c, w, h, n, L = 3, 96, 64, 1500, 2
+    g = f32(S.init_gaussians(n, c, w, h, 42))
+    target = holo.RealField(c, h, w, S.synthetic_image(42, c, h, w))
+    masks = S.build_masks(S.synthetic_depth(43, h, w), L, True)
+    dist = S.make_depth_planes(L, 3e-3, 2e-3)
+    a, b = (holo.Trainer(holo.GaussianSet(n, c, **g), w, h, target, masks, dist, holo.PropagationSpec(), 50)
+            for _ in range(2))
+    for t in (a, b):
+        t.set_deterministic(True)
+        t.use_graph(True)
+    b.set_profiling(True)
+    for _ in range(3):
+        la, lb = a.step(), b.step()
+        assert la == lb
+        st = b.stage_ms()
+        parts = [v for k, v in st.items() if k != "total"]
+        assert all(v > 0.0 for v in parts), st
+        assert abs(sum(parts) - st["total"]) <= 1e-3 * st["total"] + 1e-3, st
+    assert np.array_equal(a.params(), b.params())
+    b.set_profiling(False)  # back to the plain step graph
+    assert a.step() == b.step()
+
+
 def test_tile_backward_matches_deterministic_gather(holo, ref):
     """The default per-tile backward (vector atomics into per-Gaussian rows)
     and the deterministic per-Gaussian gather give the same gradients to fp32
