@@ -621,6 +621,32 @@ def test_reserve_pairs_recaptures_the_step_graphs(holo):
             assert np.array_equal(host.numpy(), eager.params()), i
 
 
+def test_reserve_pairs_recaptures_the_run_graphs(holo):
+    """The same for the pipelined host loop (hs_trainer_run_host): its captured
+    first-step and steady-state graphs are dropped with the pair buffers."""
+    import torch
+    c, w, h, n, L = 3, 64, 48, 400, 1
+    g = f32(S.init_gaussians(n, c, w, h, 9))
+    img = S.synthetic_image(42, c, h, w)
+    masks = S.build_masks(S.synthetic_depth(43, h, w), L, True)
+    dist = S.make_depth_planes(L, 3e-3, 2e-3)
+    mk = lambda: holo.Trainer(holo.GaussianSet(n, c, **g), w, h, holo.RealField(c, h, w, img), masks, dist,
+                              holo.PropagationSpec(), 20)
+    eager, graphed = mk(), mk()
+    for t in (eager, graphed):
+        t.set_deterministic(True)
+    graphed.use_graph(True)
+    host = torch.from_numpy(graphed.params().copy()).pin_memory()
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        want = [eager.step(sync_loss=True) for _ in range(6)]
+        got = list(graphed.run_host(host, 3))
+        graphed.reserve_pairs(1 << 22)
+        got += list(graphed.run_host(host, 3))
+    assert got == want
+    assert np.array_equal(host.numpy(), eager.params())
+
+
 def test_trainer_nonfinite_gradient_raises_and_keeps_params(holo):
     """A NaN in the target poisons every gradient: like Adan::step on the first
     group (optimizer.cpp:52-54, groups named as pipeline.cpp:244-249) the step
