@@ -718,7 +718,7 @@ def main():
                      "frac": dom_gbs / peak, "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": kb[dom], "ms_per_launch": kern[dom],
                      "note": "the rasterizer, SSIM and FFT kernels are instruction-issue bound (ncu issue-active "
-                             "44-71%, profiles/r02_ncu_summary_v6.md), not HBM bound: the HBM fraction "
+                             "44-71%, profiles/r02_ncu_summary_v7.md), not HBM bound: the HBM fraction "
                              "measures bytes, not the binding resource (DESIGN.md section 3)"},
         "step_roofline": {"bound": "hbm", "achieved": step_gbs, "peak": peak, "unit": "GB/s",
                           "frac": step_gbs / peak, "algorithmic_bytes_per_step": B,
