@@ -644,17 +644,18 @@ __global__ void __launch_bounds__(kFwdThreads) raster_fwd_kernel(
                 const float4 r0 = G.r0, iq = G.iq, q = G.q;
                 const float dx = (fx - r0.x) - r0.z;
                 const float dyA = (fy - r0.y) - r0.w;
-                const float dyB = dyA + 4.f;
-                // Sigma^-1 (dx, dy) for both pixels, then the quadratic forms
-                const float2 i0 = make_float2(iq.x, iq.y), i1 = make_float2(iq.z, iq.w);
-                const float2 eA = f2fma(f2splat(dyA), i1, f2mul(f2splat(dx), i0));
-                const float2 eB = f2fma(f2splat(4.f), i1, eA);
-                const float mA = fmaf(dx, eA.x, dyA * eA.y);
-                const float mB = fmaf(dx, eB.x, dyB * eB.y);
+                // both pixels (rows y, y + 4) as one fp32x2 pair: Sigma^-1 (dx, dy)
+                // by component, then the quadratic forms and the exponents
+                const float2 dy2 = make_float2(dyA, dyA + 4.f);
+                const float2 ex = f2fma(dy2, f2splat(iq.y), f2splat(dx * iq.x));  // i00 dx + i01 dy
+                const float2 ey = f2fma(dy2, f2splat(iq.w), f2splat(dx * iq.z));  // i01 dx + i11 dy
+                const float2 m = f2fma(f2splat(dx), ex, f2mul(dy2, ey));
+                const float2 arg = f2fma(m, f2splat(kNegHalfLog2e), f2splat(q.z));
+                const float mA = m.x, mB = m.y;
                 // alpha e^{-m/2} = 2^(log2 alpha - m / (2 ln 2))
                 const float lo = q.x, hi = q.y;
-                aA = mA <= lo ? fminf(0.99f, ex2f(fmaf(mA, kNegHalfLog2e, q.z))) : 0.f;
-                aB = mB <= lo ? fminf(0.99f, ex2f(fmaf(mB, kNegHalfLog2e, q.z))) : 0.f;
+                aA = mA <= lo ? fminf(0.99f, ex2f(arg.x)) : 0.f;
+                aB = mB <= lo ? fminf(0.99f, ex2f(arg.y)) : 0.f;
                 bA = mA > lo && mA <= hi;
                 bB = mB > lo && mB <= hi;
             };
