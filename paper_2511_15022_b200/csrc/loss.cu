@@ -194,7 +194,7 @@ struct SsimCta {
     const LossArgs& a;
     const Win& win;
     SsimSmem<Raw>& S;
-    int t, x0, y0, c, H, W, vh, vw, kind;
+    int t, x0, y0, y1, c, H, W, vh, vw, kind;  // output rows [y0, y1) of this CTA (at most SR)
     size_t plane_off;
     const float* tgt;
     const float2* tst;
@@ -295,7 +295,7 @@ struct SsimCta {
             const float rb1 = __fdividef(1.f, b1), rb2 = __fdividef(1.f, b2);
             const float inv = rb1 * rb2;
             const float sv = a1 * a2 * inv;
-            if (t >= kHalo && v >= y0 && v < y0 + SR &&
+            if (t >= kHalo && v >= y0 && v < y1 &&
                 (!BAND || static_cast<unsigned>(v - a.own0) < static_cast<unsigned>(a.own1 - a.own0)))
                 st.sum += static_cast<double>(sv);
             gv.x = 2.f * (a2 * inv * m2 - sv * rb1 * m1 + sv * rb2 * m1 - a1 * inv * m2);
@@ -314,11 +314,11 @@ struct SsimCta {
         const int v = y0 - 2 * kHalo + s;
         const int buf = s & 1;
         const int y = v, x = c;
-        const bool out_ok = t >= kHalo && y >= y0 && y < y0 + SR && y < H && x < W;
+        const bool out_ok = t >= kHalo && y >= y0 && y < y1 && y < H && x < W;
         const float mk = mk_next;
         if (kind == kLossTraining) {  // mask of the next step's output row, one step ahead
             const int yn = y + 1;
-            mk_next = (t >= kHalo && yn >= y0 && yn < y0 + SR && yn < H && x < W)
+            mk_next = (t >= kHalo && yn >= y0 && yn < y1 && yn < H && x < W)
                           ? (mask[static_cast<unsigned>(yn) * static_cast<unsigned>(W) + static_cast<unsigned>(x)] ? 1.f : 0.f)
                           : 0.f;
         }
@@ -373,7 +373,11 @@ __global__ void __launch_bounds__(2 * kSW, MINB) ssim_loss_kernel(LossArgs a, Wi
     SsimCta<FROM_FIELD, SR, BAND> K{a, win, S};
     K.t = producer ? threadIdx.x : threadIdx.x - kSW;
     K.x0 = blockIdx.x * kSO;
-    K.y0 = blockIdx.y * SR;
+    // the launch's row strips split H evenly (1080 rows in 8 strips: 135 rows,
+    // 155 steps instead of SR + 20 = 165)
+    const int sr = (a.H + static_cast<int>(gridDim.y) - 1) / static_cast<int>(gridDim.y);
+    K.y0 = blockIdx.y * sr;
+    K.y1 = K.y0 + sr;
     K.c = K.x0 - kHalo + K.t;
     K.H = a.H;
     K.W = a.W;
@@ -397,7 +401,7 @@ __global__ void __launch_bounds__(2 * kSW, MINB) ssim_loss_kernel(LossArgs a, Wi
         st.r2[i] = 0.f;
     }
     st.sum = 0.0;
-    // steps s = 0 .. kSteps-1 cover valid rows v = y0-20 .. y0+SR-1 (output rows y0..y0+SR-1);
+    // steps s = 0 .. steps-1 cover valid rows v = y0-20 .. y0+sr-1 (output rows y0..y0+sr-1);
     // rows past the image are guarded inside the steps
     constexpr int kSteps = SR + 2 * kHalo;
     static_assert(kSteps % kWin == 0, "whole ring cycles");
@@ -413,7 +417,8 @@ __global__ void __launch_bounds__(2 * kSW, MINB) ssim_loss_kernel(LossArgs a, Wi
 #define HS_SSIM_STEP(U)                                      \
     if (producer) K.template produce<U>(st, sb + U);         \
     __syncthreads();                                         \
-    if (!producer) K.template consume<U>(st, sb + U, mk_next);
+    if (!producer) K.template consume<U>(st, sb + U, mk_next); \
+    if (K.y0 + sb + (U + 1 - 2 * kHalo) >= K.y1) break;  /* sr + 20 <= kSteps steps: the last ring cycle may stop part way */
 #pragma unroll 1
     for (int sb = 0; sb < kSteps; sb += kWin) {
         HS_SSIM_STEP(0) HS_SSIM_STEP(1) HS_SSIM_STEP(2) HS_SSIM_STEP(3) HS_SSIM_STEP(4) HS_SSIM_STEP(5)
@@ -662,8 +667,9 @@ int ssim_rows(int planes, int H, int W) {
     int best = kSsimRowChoices[0];
     int64_t best_cost = -1;
     for (int sr : kSsimRowChoices) {
-        const int64_t ctas = static_cast<int64_t>(ceil_div(W, kSO)) * ceil_div(H, sr) * planes;
-        const int64_t cost = (ctas + slots - 1) / slots * (sr + 2 * kHalo);
+        const int strips = ceil_div(H, sr);
+        const int64_t ctas = static_cast<int64_t>(ceil_div(W, kSO)) * strips * planes;
+        const int64_t cost = (ctas + slots - 1) / slots * (ceil_div(H, strips) + 2 * kHalo);
         if (best_cost < 0 || cost < best_cost) {
             best = sr;
             best_cost = cost;
