@@ -1199,6 +1199,17 @@ __global__ void __launch_bounds__(32, 16) raster_bwd_tile1w_kernel(
     if (qn > 0) batch(qn);
 }
 
+// 1 - tanh^2 x = 4 e / (1 + e)^2 with e = e^{-2|x|}: relative accuracy of expf
+// over the whole range (1 - tanhf^2 loses it once tanhf rounds near 1)
+__device__ __forceinline__ double sech2_fd(float x) {
+    const double e = expf(-2.f * fabsf(x));
+    return 4.0 * e / ((1.0 + e) * (1.0 + e));
+}
+// e^x of an fp32 argument: expf where the result is a normal fp32, fp64 exp beyond
+__device__ __forceinline__ double exp_fd(float x) {
+    return fabsf(x) < 80.f ? static_cast<double>(expf(x)) : exp(static_cast<double>(x));
+}
+
 // AOS: the per-tile backward's [N][16] rows (sum alpha_eff g_c re/im instead of
 // (d_amp, d_phase), converted here with the Gaussian's shading record).
 template <int C, bool LIST = false, bool AOS = false>
@@ -1273,16 +1284,37 @@ __global__ void __launch_bounds__(256) raster_finalize_kernel(int N, const float
         put(gamp + i, (rawp >= 0.f && rawp <= 1.f) ? DA(c) : 0.0, 3);
         put(gpha + i, DP(c), 4);
     }
-    const double po = opa[g];
-    const double sig = 1.0 / (1.0 + exp(-po));
+    // Transcendentals of the fp32 parameters in fp32 (correctly rounded to
+    // ~1 ulp: perturbs every derived fp64 quantity by ~1e-7 relative, far
+    // inside the 1e-3 gradient tolerance; the covariance algebra below stays
+    // fp64, so det keeps its fp64 cancellation behaviour); exp falls back to
+    // fp64 where fp32 would overflow.  One fp64 division instead of six (all forms).
+    // (trainer's per-tile form only: the stand-alone rasterize_backward and the
+    // deterministic gather keep the fp64 transcendentals of the reference)
+    const double sig = 1.0 / (1.0 + (AOS ? exp_fd(-opa[g]) : exp(-static_cast<double>(opa[g]))));
     put(gopa + g, d_alpha * (sig * (1.0 - sig)), 5);
-    const double tx = tanh(static_cast<double>(pp[2 * g])), ty = tanh(static_cast<double>(pp[2 * g + 1]));
-    put(gpp + 2 * g, gmx * (0.5 * W * (1.0 - tx * tx)), 0);
-    put(gpp + 2 * g + 1, gmy * (0.5 * H * (1.0 - ty * ty)), 0);
-    const double esx = exp(static_cast<double>(ps[2 * g])), esy = exp(static_cast<double>(ps[2 * g + 1]));
+    auto sech2 = [](float x) {
+        if constexpr (AOS) return sech2_fd(x);
+        const double t = tanh(static_cast<double>(x));
+        return 1.0 - t * t;
+    };
+    auto expd = [](float x) {
+        if constexpr (AOS) return exp_fd(x);
+        return exp(static_cast<double>(x));
+    };
+    put(gpp + 2 * g, gmx * (0.5 * W * sech2(pp[2 * g])), 0);
+    put(gpp + 2 * g + 1, gmy * (0.5 * H * sech2(pp[2 * g + 1])), 0);
+    const double esx = expd(ps[2 * g]), esy = expd(ps[2 * g + 1]);
     const double sx = esx + kEpsScale, sy = esy + kEpsScale;
-    const double th = rot[g];
-    const double ct = cos(th), st = sin(th);
+    double ct, st;
+    if constexpr (AOS) {
+        float sf, cf;
+        sincosf(rot[g], &sf, &cf);
+        ct = cf;
+        st = sf;
+    } else {
+        sincos(static_cast<double>(rot[g]), &st, &ct);
+    }
     const double sx2 = sx * sx, sy2 = sy * sy;
     const double c00 = sx2 * ct * ct + sy2 * st * st + kEpsCov;
     const double c01 = (sx2 - sy2) * ct * st;
@@ -1291,10 +1323,11 @@ __global__ void __launch_bounds__(256) raster_finalize_kernel(int N, const float
     const double dsafe = fmax(det, kEpsDet);
     const double t_adj = ga * c11 - gb * c01 + gc * c00;
     const double clamped = det > kEpsDet ? 1.0 : 0.0;
-    const double d2 = dsafe * dsafe;
-    const double gS00 = gc / dsafe - t_adj * (clamped * c11) / d2;
-    const double gS01 = -gb / dsafe - t_adj * (clamped * -2.0 * c01) / d2;
-    const double gS11 = ga / dsafe - t_adj * (clamped * c00) / d2;
+    const double inv = 1.0 / dsafe;
+    const double ti2 = t_adj * clamped * (inv * inv);
+    const double gS00 = gc * inv - ti2 * c11;
+    const double gS01 = -gb * inv + ti2 * 2.0 * c01;
+    const double gS11 = ga * inv - ti2 * c00;
     const double dsx = 2.0 * sx * (ct * ct * gS00 + ct * st * gS01 + st * st * gS11);
     const double dsy = 2.0 * sy * (st * st * gS00 - ct * st * gS01 + ct * ct * gS11);
     put(gps + 2 * g, dsx * esx, 1);
