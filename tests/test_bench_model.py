@@ -56,14 +56,15 @@ def test_bench_refuses_more_gpus_than_visible():
     assert f"--gpus {n} needs {n} visible GPUs" in r.stderr
 
 
-def test_fft_adjusted_estimate_scales_only_the_propagation_stages():
+def test_fft_adjusted_estimate_charges_the_steps_fft2s_at_pocketfft_speed():
     import bench
     st = {"raster_fwd": 270.0, "propagate_multi": 2300.0, "training_loss_grad": 790.0,
           "propagate_multi_backward": 2300.0, "rasterize_backward": 250.0, "adan": 17.0, "total": 5927.0}
-    est = bench.fft_adjusted(st, {"shim_propagate_ms_1core": 800.0, "numpy_pocketfft_fft2_ifft2_ms_1core": 400.0})
-    assert est["fft_ratio"] == 0.5
-    assert abs(est["ms_per_step"] - (5927.0 - 0.5 * 4600.0)) < 0.1
+    fft = {"shim_fft2_ifft2_ms_1core": 800.0, "numpy_pocketfft_fft2_ifft2_ms_1core": 600.0}
+    est = bench.fft_adjusted(st, fft, 3, 1)  # cfg2: 3 channels x (1 forward + 1 inverse) x 2 directions
+    assert est["fft2_per_step"] == 12
+    assert abs(est["ms_per_step"] - (5927.0 - 12 * 100.0)) < 0.1
     assert abs(est["value"] - 1e3 / est["ms_per_step"]) < 1e-3
     assert "estimate" in est["note"]
-    assert bench.fft_adjusted({"total": 1.0}, {"shim_propagate_ms_1core": 1.0,
-                                               "numpy_pocketfft_fft2_ifft2_ms_1core": 1.0}) is None
+    assert bench.fft_adjusted(st, fft, 3, 8)["fft2_per_step"] == 54
+    assert bench.fft_adjusted({"total": 1.0}, {}, 3, 1) is None
