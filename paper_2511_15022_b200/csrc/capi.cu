@@ -455,24 +455,43 @@ void hs::trainer_enqueue_fwd_bwd(hs_trainer* t, cudaStream_t st, cudaEvent_t sha
     };
     mark(0);
     HS_CUDA(cudaMemsetAsync(t->flags.p, 0, sizeof(uint32_t), st));
-    t->rw.project_and_bin(t->params.as<float>(), st, shading_ready);
+    {
+        NvtxRange r("binning");
+        t->rw.project_and_bin(t->params.as<float>(), st, shading_ready);
+    }
     mark(1);
-    raster_forward(t->rw, t->field.as<float2>(), st);
+    {
+        NvtxRange r("raster_fwd");
+        raster_forward(t->rw, t->field.as<float2>(), st);
+    }
     mark(2);
-    asm_forward(t->aw, t->field.as<float2>(), t->planes.as<float2>(), st, prof ? t->ev + 3 : nullptr);
-    LossArgs a{kLossTraining, t->L, t->L_total, t->plane0, t->c, t->h, t->w, nullptr, t->planes.as<float2>(),
-               t->target.as<float>(), t->tstats.as<float2>(), t->masks.as<uint8_t>(), nullptr,
-               t->dplanes.as<float2>(), t->partials.as<double>(), t->C_total};
-    const int used = loss_launch(a, st);
-    loss_finalize(a, used, t->out3.as<double>(), st);
+    {
+        NvtxRange r("asm_forward");
+        asm_forward(t->aw, t->field.as<float2>(), t->planes.as<float2>(), st, prof ? t->ev + 3 : nullptr);
+    }
+    {
+        NvtxRange r("loss");
+        LossArgs a{kLossTraining, t->L, t->L_total, t->plane0, t->c, t->h, t->w, nullptr, t->planes.as<float2>(),
+                   t->target.as<float>(), t->tstats.as<float2>(), t->masks.as<uint8_t>(), nullptr,
+                   t->dplanes.as<float2>(), t->partials.as<double>(), t->C_total};
+        const int used = loss_launch(a, st);
+        loss_finalize(a, used, t->out3.as<double>(), st);
+    }
     mark(6);
-    asm_backward(t->aw, t->dplanes.as<float2>(), t->back.as<float2>(), st, prof ? t->ev + 7 : nullptr);
-    raster_backward(t->rw, t->params.as<float>(), t->back.as<float2>(), t->grads.as<float>(),
-                    t->flags.as<uint32_t>(), st);
+    {
+        NvtxRange r("asm_backward");
+        asm_backward(t->aw, t->dplanes.as<float2>(), t->back.as<float2>(), st, prof ? t->ev + 7 : nullptr);
+    }
+    {
+        NvtxRange r("raster_bwd");
+        raster_backward(t->rw, t->params.as<float>(), t->back.as<float2>(), t->grads.as<float>(),
+                        t->flags.as<uint32_t>(), st);
+    }
     mark(10);
 }
 
 void hs::trainer_enqueue_update(hs_trainer* t, cudaStream_t st) {
+    NvtxRange r("adan");
     adan_fused_launch(t->params.as<float>(), t->grads.as<float>(), t->state.as<float>(), t->P, t->groups,
                       t->total_steps, 0.98, 0.92, 0.99, 1e-8, t->step.as<int>(), t->flags.as<uint32_t>(), st);
     if (t->mark_events) HS_CUDA(cudaEventRecordWithFlags(t->ev[11], st, cudaEventRecordExternal));
@@ -641,6 +660,7 @@ hs_status hs_trainer_set_profiling(hs_trainer* t, int enable) {
 
 hs_status hs_trainer_forward_backward(hs_trainer* t) {
     return guard([&] {
+        NvtxRange nvtx("hs_trainer_forward_backward");
         require(t->host_step <= t->total_steps, "cosine_lr: step outside [0, total_steps]");
         t->mark_events = t->profiling;  // eager split step: stage events as the plain step
         try {
@@ -664,6 +684,7 @@ hs_status hs_trainer_check_grads(hs_trainer* t) {
 
 hs_status hs_trainer_apply_update(hs_trainer* t) {
     return guard([&] {
+        NvtxRange nvtx("hs_trainer_apply_update");
         t->mark_events = t->profiling;
         trainer_enqueue_update(t, t->ctx->stream);
         t->mark_events = false;
@@ -738,6 +759,7 @@ static void trainer_launch_step(hs_trainer* t) {
 
 hs_status hs_trainer_step(hs_trainer* t, double* loss_out) {
     return guard([&] {
+        NvtxRange nvtx("hs_trainer_step");
         trainer_launch_step(t);
         if (loss_out) {
             trainer_check_after(t);
@@ -778,6 +800,7 @@ static void enqueue_host_step(hs_trainer* t, cudaStream_t st, const float* in, f
 
 hs_status hs_trainer_step_host(hs_trainer* t, const float* h_params_in, float* h_params_out, double* loss_out) {
     return guard([&] {
+        NvtxRange nvtx("hs_trainer_step_host");
         require(t->host_step <= t->total_steps, "cosine_lr: step outside [0, total_steps]");
         cudaStream_t st = t->ctx->stream;
         if (!t->copy_st) {
@@ -877,6 +900,7 @@ static void enqueue_run_step(hs_trainer* t, cudaStream_t st, float* h, bool tail
 
 hs_status hs_trainer_run_host(hs_trainer* t, float* h_params, int steps, double* losses_out) {
     return guard([&] {
+        NvtxRange nvtx("hs_trainer_run_host");
         require(steps >= 0 && h_params != nullptr, "run_host: bad arguments");
         require(t->R == 0, "run_host: not for row-slab shards (use the slab stages)");
         if (steps == 0) return;

@@ -9,9 +9,22 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: no-ops unless a tool (nsys / ncu --nvtx) is attached
+
 #include "holosplat.h"
 
 namespace hs {
+
+// Host-side NVTX range (SURVEY §5 tracing row): names the C-ABI trainer calls
+// and, on eager enqueues, the step's stages, so `ncu --nvtx --nvtx-include`
+// can select a stage's kernels.  Inside a graph capture it marks the capture.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 
 constexpr int kTile = 16;  // rasterizer.hpp:12 kTileSize
 constexpr double kEpsScale = 0.1, kEpsCov = 0.1, kEpsDet = 1e-10;  // field_core.hpp:10-12
