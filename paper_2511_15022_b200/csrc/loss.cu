@@ -175,9 +175,10 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
 
-constexpr int kRaw = 16;  // ring of raw input rows (U or I, and t): covers rows r-12 .. r+3
-constexpr int kPD = 3;    // prefetch distance (rows) of the cp.async pipeline
+constexpr int kRaw = 16;  // ring of raw input rows (U or I, and t): covers rows r-12 .. r+kPD
+constexpr int kPD = 2;    // prefetch distance (rows) of the cp.async pipeline (3: +1.2 us; 5 needs kTsRing > 5)
 constexpr int kTsRing = 4;
+static_assert(kTsRing > kPD && kRaw >= 2 * kHalo / 2 + 3 + kPD, "cp.async rings must outlive the prefetch distance");
 
 template <class Raw>
 struct SsimSmem {
