@@ -178,7 +178,7 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 constexpr int kRaw = 16;  // ring of raw input rows (U or I, and t): covers rows r-12 .. r+kPD
 constexpr int kPD = 2;    // prefetch distance (rows) of the cp.async pipeline (3: +1.2 us; 5 needs kTsRing > 5)
 constexpr int kTsRing = 4;
-static_assert(kTsRing > kPD && kRaw >= 2 * kHalo / 2 + 3 + kPD, "cp.async rings must outlive the prefetch distance");
+static_assert(kTsRing > kPD && kRaw >= 13 + kPD, "cp.async rings must outlive the prefetch distance");
 
 template <class Raw>
 struct SsimSmem {
